@@ -1,0 +1,381 @@
+"""Algorithmic oracle: RQI-PCGTLS-MP on the CPU in fp64 with emulated u_f
+rounding (oracle c2; TEST INFRASTRUCTURE ONLY, see oracle/__init__.py).
+
+Follows, in the paper's order and notation:
+  Alg. 4 RQI-PCGTLS-MP    PAPER.md l.221-258 (§3)
+  Alg. 3 l-step PCGTLS    PAPER.md l.186-204 (§2), operator of l.322-328 (§3.1)
+  psi_k termination       PAPER.md l.260-265 (Eq. psik)
+  scaled Cholesky         PAPER.md l.290-307 (§3.1)
+Where the paper is silent or ambiguous the DESIGN.md reading is cited as R<n>.
+
+The u_f rounding is applied exactly where the GPU path rounds (R10): the scaled
+matrix A D^{-1} before the Gram, the Gram's fp32 accumulation per chunk of K_t
+rows (fp16/bf16 only), and the Cholesky factor R -> R~ = fl_uf(R).  Everything
+else is fp64 (u = u_r = fp64, BASELINE north_star).
+
+A may be a dense numpy array or a scipy.sparse CSR matrix (BASELINE cfg3).
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import List, Optional
+
+import numpy as np
+import scipy.linalg
+import scipy.linalg.lapack
+import scipy.sparse
+
+from .rounding import round_to
+
+# status codes (include/tlsrqi.h mirrors the numbers; the oracle does not read it)
+OK, CHOL_BREAKDOWN, PCG_BREAKDOWN, MAX_OUTER, NONFINITE, RANGE, NOT_MINIMAL, STAGNATED = range(8)
+# termination reasons
+T_NONE, T_CONVERGED_TOL, T_PSI_INCREASE_CONVERGED, T_STAGNATED, T_MAX_OUTER, T_BREAKDOWN, T_NONFINITE = range(7)
+
+
+# ----------------------------------------------------------------------------- helpers
+def _is_sparse(A) -> bool:
+    return scipy.sparse.issparse(A)
+
+
+def matvec(A, x):
+    return np.asarray(A @ x).reshape(-1)
+
+
+def rmatvec(A, t):
+    return np.asarray(A.T @ t).reshape(-1)
+
+
+# ----------------------------------------------------------------------------- scaling
+def column_scaling(A):
+    """Exact two-sided scaling stand-in (reading R2):
+    d_j = 2^floor(log2 max_i |a_ij|), so that |a_ij / d_j| < 2 and the scaling
+    itself is exact (the paper assumes it "without incurring additional
+    rounding error", l.307).  Also returns ||A||_F^2 for the tol stop (R6).
+    A zero column makes A rank deficient (PAPER.md l.30 rank(A) = n): ValueError."""
+    if _is_sparse(A):
+        amax = np.asarray(abs(A).max(axis=0).todense()).reshape(-1)
+        normA2 = float(A.multiply(A).sum())
+    else:
+        amax = np.max(np.abs(A), axis=0)
+        normA2 = float(np.sum(A * A))
+    if np.any(amax == 0) or not np.all(np.isfinite(amax)):
+        raise ValueError("A has a zero or non-finite column")
+    _, E = np.frexp(amax)
+    d = np.ldexp(1.0, E - 1)
+    return d, normA2
+
+
+# ----------------------------------------------------------------------------- Gram
+def gram_uf(A, d: np.ndarray, u_f: str, K_t: int = 2048) -> np.ndarray:
+    """G = sum over chunks c of K_t consecutive rows (in order) of
+    fp64( fl32-accumulated  A^_c^T A^_c ),  A^ = fl_uf(A D^{-1})   (R10, R11).
+
+    u_f in {fp16, bf16}: the products of u_f values are exact in fp32 and each
+    chunk is summed in fp32 (a float32 matmul), as the tensor cores accumulate
+    in fp32; chunks are added in fp64.  u_f = fp32: A^ in fp32, G formed in
+    fp64.  u_f = fp64: G = (A D^{-1})^T (A D^{-1}) in fp64 (control)."""
+    m, n = A.shape
+    G = np.zeros((n, n))
+    for c0 in range(0, m, K_t):
+        blk = A[c0:c0 + K_t]
+        blk = blk.toarray() if _is_sparse(blk) else np.asarray(blk)
+        Ah = round_to(blk / d[None, :], u_f)
+        if not np.all(np.isfinite(Ah)):
+            raise OverflowError("A D^-1 overflows u_f")
+        if u_f in ("fp16", "bf16"):
+            A32 = Ah.astype(np.float32)
+            S = (A32.T @ A32).astype(np.float64)
+        else:
+            S = Ah.T @ Ah
+        G += S
+    return G
+
+
+def gram_exact_bound(A, d: np.ndarray, u_f: str, K_t: int = 2048) -> np.ndarray:
+    """Elementwise bound on |G_fp32chunks - A^^T A^| (standard dot-product error
+    bound, gamma_k = k u/(1 - k u) with u = 2^-24 per fp32 chunk of length <= K_t,
+    plus the fp64 chunk sums)."""
+    m, n = A.shape
+    B = np.zeros((n, n))
+    u32 = 2.0 ** -24
+    k = min(K_t, m)
+    gam = k * u32 / (1 - k * u32)
+    for c0 in range(0, m, K_t):
+        blk = A[c0:c0 + K_t]
+        blk = blk.toarray() if _is_sparse(blk) else np.asarray(blk)
+        Ah = np.abs(round_to(blk / d[None, :], u_f))
+        B += Ah.T @ Ah
+    nchunks = (m + K_t - 1) // K_t
+    return (gam + (nchunks + 1) * 2.0 ** -53) * B
+
+
+# ----------------------------------------------------------------------------- Cholesky
+@dataclasses.dataclass
+class Precond:
+    """P = R~ D with P^T P ~ A^T A."""
+    Rt: np.ndarray      # R~ = fl_uf(R), n x n upper triangular, values held in fp64
+    d: np.ndarray       # column scaling, powers of two
+    u_f: str
+    normA2: float       # ||A||_F^2
+    status: int = OK
+    chol_pivot: int = 0  # 1-based index of the first failed pivot (CHOL_BREAKDOWN)
+    G: Optional[np.ndarray] = None
+    R: Optional[np.ndarray] = None
+
+
+def factor_precond(A, u_f: str, K_t: int = 2048, keep: bool = False) -> Precond:
+    """tls_factor_precond: scaling, u_f Gram, fp64 Cholesky G = R^T R (LAPACK
+    dpotrf, upper), R~ = fl_uf(R)  (PAPER.md l.231 with the Cholesky route of
+    l.290-307; readings R10, R11)."""
+    n = A.shape[1]
+    d, normA2 = column_scaling(A)
+    try:
+        G = gram_uf(A, d, u_f, K_t)
+    except OverflowError:
+        return Precond(np.zeros((n, n)), d, u_f, normA2, RANGE)
+    R, info = scipy.linalg.lapack.dpotrf(G, lower=0, clean=1)
+    if info > 0 or not np.all(np.isfinite(np.diag(R))):
+        piv = int(info) if info > 0 else int(np.argmin(np.isfinite(np.diag(R)))) + 1
+        return Precond(np.zeros((n, n)), d, u_f, normA2, CHOL_BREAKDOWN, piv,
+                       G if keep else None)
+    Rt = round_to(np.triu(R), u_f)
+    if not np.all(np.isfinite(Rt)) or np.any(np.diag(Rt) == 0):
+        return Precond(Rt, d, u_f, normA2, RANGE)
+    return Precond(Rt, d, u_f, normA2, OK, 0, G if keep else None, R if keep else None)
+
+
+def apply_Pinv(pc: Precond, y: np.ndarray) -> np.ndarray:
+    """P^{-1} y = D^{-1} (R~^{-1} y): back substitution (Alg. 3 l.193;
+    Table 1 "Forward/Backward Subs", l.427)."""
+    return scipy.linalg.solve_triangular(pc.Rt, y, lower=False) / pc.d
+
+
+def apply_PinvT(pc: Precond, y: np.ndarray) -> np.ndarray:
+    """P^{-T} y = R~^{-T} (D^{-1} y): forward substitution (Alg. 3 l.191, l.197)."""
+    return scipy.linalg.solve_triangular(pc.Rt, y / pc.d, trans="T", lower=False)
+
+
+# ----------------------------------------------------------------------------- PCGTLS
+@dataclasses.dataclass
+class PcgResult:
+    omega: np.ndarray
+    count: int              # number of alpha-updates executed (R3)
+    breakdown: bool = False
+    breakdown_j: int = -1
+    delta_min: float = math.inf
+
+
+def pcgtls(A, pc: Precond, sigma2: float, f: np.ndarray, l: int, tol_inner: float,
+           variant: str = "A", breakdown_rule: str = "spec") -> PcgResult:
+    """l-step PCGTLS for (A^T A - sigma^2 I) omega = f (Alg. 3, l.186-204).
+
+    variant "A" (default, reading R1): the preconditioned operator
+        C^ = P^{-T}(A^T A - sigma^2 I) P^{-1}
+    applied with A in the loop: t = A q, delta = t^T t - sigma^2 q^T q,
+    w = P^{-T}(A^T t - sigma^2 q).
+    variant "paper": Alg. 3 as printed, C~ = I - sigma^2 P^{-T} P^{-1} (l.206):
+    delta = p^T p - sigma^2 q^T q (l.194), w = p - sigma^2 P^{-T} q (l.197-198).
+    Loop guard (R3): delta non-finite or zero stops before the update (l.192);
+    delta < 0 is a breakdown under the "spec" rule; at most l updates (R3);
+    early exit after an update when eta_{j+1} <= tol_inner^2 eta_0."""
+    n = f.shape[0]
+    omega = np.zeros(n)                        # l.191
+    s = apply_PinvT(pc, f)
+    p = s.copy()
+    eta = float(s @ s)
+    eta0 = eta
+    res = PcgResult(omega, 0)
+    if eta0 == 0.0:
+        return res
+    for j in range(l):                         # l.192
+        q = apply_Pinv(pc, p)                  # l.193
+        if variant == "A":
+            t = matvec(A, q)
+            delta = float(t @ t) - sigma2 * float(q @ q)
+        else:
+            delta = float(p @ p) - sigma2 * float(q @ q)   # l.194
+        res.delta_min = min(res.delta_min, delta)
+        if not math.isfinite(delta) or delta == 0.0:
+            break
+        if delta < 0.0 and breakdown_rule == "spec":
+            res.breakdown, res.breakdown_j = True, j
+            break
+        alpha = eta / delta                    # l.195
+        omega = omega + alpha * q              # l.196
+        if variant == "A":
+            w = apply_PinvT(pc, rmatvec(A, t) - sigma2 * q)
+        else:
+            w = p - sigma2 * apply_PinvT(pc, q)            # l.197
+        s = s - alpha * w                      # l.198
+        eta_new = float(s @ s)                 # l.199
+        res.count += 1
+        if eta_new <= tol_inner * tol_inner * eta0:
+            break
+        beta = eta_new / eta                   # l.200
+        p = s + beta * p                       # l.201
+        eta = eta_new
+    res.omega = omega
+    return res
+
+
+# ----------------------------------------------------------------------------- RQI
+@dataclasses.dataclass
+class RqiOptions:
+    """Mirrors tls_rqi_opts_t (include/tlsrqi.h); defaults are DESIGN.md's."""
+    budget_rule: int = 0       # 0: k+1 PCG steps at RQI step k; 1: until tol (cap 400)
+    stop_rule: int = 0         # 0: strict psi increase (l.265); 1: weak (>=, l.532)
+    max_outer: int = 50
+    polish: int = 1            # RQI steps taken after the tol crossing (R6)
+    tol_inner: float = -1.0    # <= 0 -> tol
+    boot: int = 0              # 0: x_LS by preconditioned CGLS (R5); 1: semi-normal
+    boot_tol: float = 1e-8
+    boot_max: int = 200
+    op_variant: int = 0        # 0: A-in-loop (R1); 1: paper Alg. 3
+    breakdown_rule: int = 0    # 0: delta <= 0 stops (spec); 1: delta == 0 only (paper)
+    gram_chunk: int = 2048
+
+
+@dataclasses.dataclass
+class RqiResult:
+    x: np.ndarray
+    sigma: float
+    status: int
+    termination: int
+    rqi_iters: int
+    boot_iters: int
+    pcg_iters: List[tuple]
+    sigma2_trace: List[float]
+    psi_trace: List[float]
+    breakdown_k: int = -1
+    breakdown_rhs: int = -1
+    breakdown_j: int = -1
+    passes: int = 0            # passes over A (unbatched) for perf accounting
+
+
+def newton_residual(A, b: np.ndarray, x: np.ndarray):
+    """One outer residual evaluation (Alg. 4 l.238-245 and Eq. psik l.262):
+    r = b - A x, sigma^2 = r^T r/(1 + x^T x), f = -A^T r - sigma^2 x (x read as x_k,
+    reading R15), g = -b^T r + sigma^2, psi = ((f^T f + g^2)/(x^T x + 1))^{1/2}."""
+    r = b - matvec(A, x)                   # l.238
+    v = rmatvec(A, r)
+    xx = float(x @ x)
+    sig2 = float(r @ r) / (1.0 + xx)       # l.240
+    f = -v - sig2 * x                      # l.242
+    g = -float(b @ r) + sig2               # l.244
+    psi = math.sqrt((float(f @ f) + g * g) / (xx + 1.0))   # l.262
+    return sig2, f, g, psi
+
+
+def rqi_pcgtls_mp(A, b: np.ndarray, pc: Precond, tol: float = 1e-14,
+                  opts: Optional[RqiOptions] = None) -> RqiResult:
+    """RQI-PCGTLS-MP, Alg. 4 (l.221-258), u = u_r = fp64 and the
+    preconditioner R~ stored in u_f.  Stop tests (R6), in this order at step k
+    after the residual pass:
+      (ii) k* = first k with psi_k <= tol ||[A,b]||_F^2; at k = k* + polish
+           return CONVERGED_TOL with (x_k, sigma_k), or (x_{k-1}, sigma_{k-1}) if
+           psi rose in that last step (at the fp64 floor that comparison is
+           roundoff, so it picks the iterate, never the count or the reason);
+      (i)  otherwise, k >= 2 and psi_k > psi_{k-1} (>= under the weak rule,
+           l.532): return (x_{k-1}, sigma_{k-1}); PSI_INCREASE_CONVERGED if the
+           tol crossing already happened, else STAGNATED (status 7, R7);
+      (iii) k > max_outer: MAX_OUTER (status 3)."""
+    o = opts or RqiOptions()
+    variant = "A" if o.op_variant == 0 else "paper"
+    rule = "spec" if o.breakdown_rule == 0 else "paper"
+    tol_in = tol if o.tol_inner <= 0 else o.tol_inner
+    n = A.shape[1]
+    if pc.status != OK:
+        return RqiResult(np.zeros(n), math.nan, pc.status, T_BREAKDOWN, 0, 0, [], [], [])
+    passes = 0
+    normAb2 = pc.normA2 + float(b @ b)
+    h = rmatvec(A, b)                          # A^T b (setup pass)
+    passes += 1
+    # l.226  x_0 = x_LS  (R5: preconditioned CGLS = PCGTLS at sigma^2 = 0)
+    if o.boot == 0:
+        br = pcgtls(A, pc, 0.0, h, o.boot_max, o.boot_tol, "A", rule)
+        x0, B0 = br.omega, br.count
+        passes += 2 * br.count + (1 if br.count < o.boot_max else 0)
+    else:
+        x0, B0 = apply_Pinv(pc, apply_PinvT(pc, h)), 0
+    r0 = b - matvec(A, x0)                     # l.227
+    passes += 1
+    sig0 = float(r0 @ r0) / (1.0 + float(x0 @ x0))   # l.229
+    u0 = apply_Pinv(pc, apply_PinvT(pc, x0))   # l.233 (reading R9)
+    x = x0 + sig0 * u0                         # l.235
+
+    res = RqiResult(x, math.nan, OK, T_NONE, 0, B0, [], [], [])
+    prev = None           # (x, sigma2) of step k-1
+    psi_prev = None
+    crossed_at = None
+    k = 1
+    while True:
+        sig2, f, g, psi = newton_residual(A, b, x)
+        passes += 1
+        res.sigma2_trace.append(sig2)
+        res.psi_trace.append(psi)
+        res.rqi_iters = k
+        if not (math.isfinite(sig2) and math.isfinite(psi)):
+            res.x, res.sigma, res.status, res.termination = x, math.nan, NONFINITE, T_NONFINITE
+            break
+        increased = k >= 2 and (psi > psi_prev or (o.stop_rule == 1 and psi >= psi_prev))
+        # (ii) tol crossing + polish (R6): the count is fixed by the crossing; at
+        # the last polish step the better of x_k, x_{k-1} (by psi) is returned.
+        if crossed_at is None and psi <= tol * normAb2:
+            crossed_at = k
+        if crossed_at is not None and k == crossed_at + o.polish:
+            if increased:
+                res.x, res.sigma = prev[0], math.sqrt(prev[1])
+            else:
+                res.x, res.sigma = x, math.sqrt(sig2)
+            res.status, res.termination = OK, T_CONVERGED_TOL
+            break
+        # (i) psi increase (l.265)
+        if increased:
+            res.x, res.sigma = prev[0], math.sqrt(prev[1])
+            if crossed_at is not None:
+                res.status, res.termination = OK, T_PSI_INCREASE_CONVERGED
+            else:
+                res.status, res.termination = STAGNATED, T_STAGNATED
+            break
+        # (iii) cap
+        if k > o.max_outer:
+            res.x, res.sigma, res.status, res.termination = x, math.sqrt(sig2), MAX_OUTER, T_MAX_OUTER
+            break
+        budget = k + 1 if o.budget_rule == 0 else 400
+        ra = pcgtls(A, pc, sig2, -f, budget, tol_in, variant, rule)     # l.246
+        rb = pcgtls(A, pc, sig2, x, budget, tol_in, variant, rule)      # l.252
+        if variant == "A":
+            passes += ra.count + rb.count + (ra.breakdown or ra.count < budget) + (rb.breakdown or rb.count < budget)
+        res.pcg_iters.append((ra.count, rb.count))
+        if ra.breakdown or rb.breakdown:
+            res.x, res.sigma = x, math.sqrt(sig2)
+            res.status, res.termination = PCG_BREAKDOWN, T_BREAKDOWN
+            res.breakdown_k = k
+            res.breakdown_rhs = 0 if ra.breakdown else 1
+            res.breakdown_j = ra.breakdown_j if ra.breakdown else rb.breakdown_j
+            break
+        z = x + ra.omega                       # l.248
+        beta = (float(z @ f) - g) / (float(z @ x) + 1.0)   # l.250
+        x_new = z + beta * rb.omega            # l.254
+        prev, psi_prev = (x, sig2), psi
+        x = x_new
+        k += 1
+    res.passes = passes
+    return res
+
+
+def certify_sigma(A, b: np.ndarray, x: np.ndarray) -> float:
+    """sigma = sqrt(||b - A x||^2 / (1 + ||x||^2)) with exactly rounded sums
+    (math.fsum), the compensated final certificate."""
+    Ax = matvec(A, x)
+    r = b - Ax
+    return math.sqrt(math.fsum(r * r) / (1.0 + math.fsum(x * x)))
+
+
+def solve(A, b, u_f: str, tol: float = 1e-14, opts: Optional[RqiOptions] = None):
+    """Factor + RQI in one call (the whole hot path)."""
+    o = opts or RqiOptions()
+    pc = factor_precond(A, u_f, o.gram_chunk)
+    return pc, rqi_pcgtls_mp(A, b, pc, tol, o)

@@ -1,0 +1,289 @@
+"""Pins for oracle/rqi.py (Alg. 3 PCGTLS, Alg. 4 RQI-PCGTLS-MP, scaled Cholesky).
+
+Each test checks the oracle against something other than itself: a different
+LAPACK route, a closed form, exact integer arithmetic, an independent model of
+Alg. 2 in the singular-vector basis, or the paper's printed op counts."""
+import math
+
+import numpy as np
+import pytest
+import scipy.sparse
+
+import tlsgen
+from oracle import exact, perfmodel, rqi
+from oracle.rounding import round_to
+
+
+def _small(m=300, n=24, kappa=1e2, eps=1e-4, seed=11, twin=False):
+    return tlsgen.dense_problem(m, n, kappa, eps, seed, twin=twin)
+
+
+# ----------------------------------------------------------------------------- scaling / Gram
+def test_column_scaling_powers_of_two():
+    P = _small()
+    d, normA2 = rqi.column_scaling(P.A)
+    m2, e = np.frexp(d)
+    assert np.all(m2 == 0.5)                                # exact powers of two
+    amax = np.max(np.abs(P.A / d), axis=0)
+    assert np.all((amax >= 1) & (amax < 2))
+    assert normA2 == pytest.approx(np.linalg.norm(P.A) ** 2, rel=1e-14)
+
+
+def test_gram_integer_inputs_exact():
+    """Small integers are exact in fp16 and all partial sums stay exact in fp32,
+    so the emulated Gram equals the exact integer Gram (scaled by d d^T)."""
+    rng = np.random.default_rng(0)
+    A = rng.integers(-7, 8, size=(5000, 12)).astype(np.float64)
+    A[0] = 7.0
+    d, _ = rqi.column_scaling(A)
+    for fmt in ("fp16", "bf16", "fp32", "fp64"):
+        G = rqi.gram_uf(A, d, fmt, K_t=2048)
+        exactG = (A.T.astype(np.int64) @ A.astype(np.int64)).astype(np.float64) / np.outer(d, d)
+        assert np.array_equal(G, exactG)
+
+
+def test_gram_error_bound_and_chunking():
+    P = tlsgen.config("cfg2w", m=8192, n=64)
+    d, _ = rqi.column_scaling(P.A)
+    for fmt in ("fp16", "bf16"):
+        Ah = round_to(P.A / d, fmt)
+        G64 = Ah.T @ Ah
+        G = rqi.gram_uf(P.A, d, fmt, K_t=2048)
+        B = rqi.gram_exact_bound(P.A, d, fmt, K_t=2048)
+        assert np.all(np.abs(G - G64) <= B)
+        assert np.max(np.abs(G - G64)) > 0                  # fp32 accumulation is visible
+        # one row per chunk: fp32 products exact -> fp64 sum of exact products
+        G1 = rqi.gram_uf(P.A[:512], d, fmt, K_t=1)
+        np.testing.assert_allclose(G1, Ah[:512].T @ Ah[:512], rtol=1e-13, atol=1e-12)
+
+
+# ----------------------------------------------------------------------------- Cholesky
+def test_cholesky_reconstruction_and_qr_route():
+    P = _small(m=2000, n=40, kappa=1e2)
+    pc = rqi.factor_precond(P.A, "fp64", keep=True)
+    assert pc.status == rqi.OK
+    np.testing.assert_allclose(pc.R.T @ pc.R, pc.G, rtol=1e-13, atol=1e-10 * np.abs(pc.G).max())
+    assert np.all(np.diag(pc.R) > 0)
+    # R-factor of Householder QR of A D^-1 equals the Cholesky factor up to row signs
+    Rq = np.linalg.qr(P.A / pc.d, mode="r")
+    np.testing.assert_allclose(np.abs(Rq), np.abs(pc.R), rtol=1e-9, atol=1e-9 * np.abs(pc.R).max())
+    # R~ is R rounded to u_f
+    pc16 = rqi.factor_precond(P.A, "fp16", keep=True)
+    assert np.array_equal(pc16.Rt, round_to(np.triu(pc16.R), "fp16"))
+
+
+def test_cholesky_breakdown_index():
+    """kappa^2 > 1/u: an exactly repeated column makes the Gram singular."""
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((500, 8))
+    A[:, 5] = A[:, 2]
+    pc = rqi.factor_precond(A, "fp64")
+    assert pc.status == rqi.CHOL_BREAKDOWN and pc.chol_pivot == 6
+
+
+def test_precond_solves_vs_dense_solve():
+    P = _small()
+    pc = rqi.factor_precond(P.A, "bf16")
+    Pm = pc.Rt * pc.d[None, :]                              # P = R~ D
+    y = np.random.default_rng(0).standard_normal(P.n)
+    np.testing.assert_allclose(rqi.apply_Pinv(pc, y), np.linalg.solve(Pm, y), rtol=1e-10)
+    np.testing.assert_allclose(rqi.apply_PinvT(pc, y), np.linalg.solve(Pm.T, y), rtol=1e-10)
+
+
+# ----------------------------------------------------------------------------- PCGTLS
+def test_pcgtls_identities():
+    """f = 0 -> 0 iterations; sigma = 0 with an exact factor ->
+    one iteration gives (A^T A)^{-1} f; l = n -> the direct solve."""
+    P = _small(m=400, n=16)
+    f = np.random.default_rng(1).standard_normal(P.n)
+    pc64 = rqi.factor_precond(P.A, "fp64")
+    r0 = rqi.pcgtls(P.A, pc64, 0.3, np.zeros(P.n), 5, 1e-14)
+    assert r0.count == 0 and not np.any(r0.omega)
+    r1 = rqi.pcgtls(P.A, pc64, 0.0, f, 5, 1e-10)
+    assert r1.count == 1
+    np.testing.assert_allclose(r1.omega, np.linalg.solve(P.A.T @ P.A, f), rtol=1e-10)
+    sA = np.linalg.svd(P.A, compute_uv=False)
+    sig2 = 0.5 * sA[-1] ** 2
+    pc16 = rqi.factor_precond(P.A, "fp16")
+    M = P.A.T @ P.A - sig2 * np.eye(P.n)
+    for variant in ("A", "paper"):
+        rn = rqi.pcgtls(P.A, pc16 if variant == "A" else pc64, sig2, f, P.n, 1e-15, variant)
+        np.testing.assert_allclose(rn.omega, np.linalg.solve(M, f), rtol=1e-9)
+
+
+def test_pcgtls_variants_agree_for_exact_factor():
+    """Reading R1: with R~ = R (u_f = fp64) both operator forms are the same
+    operator, so their iterates agree to ~kappa(A)^2 u."""
+    P = _small(m=500, n=20, kappa=1e2)
+    pc = rqi.factor_precond(P.A, "fp64")
+    f = np.random.default_rng(2).standard_normal(P.n)
+    sig2 = 0.3 * np.linalg.svd(P.A, compute_uv=False)[-1] ** 2
+    for l in (1, 2, 3):
+        a = rqi.pcgtls(P.A, pc, sig2, f, l, 0.0, "A")
+        b = rqi.pcgtls(P.A, pc, sig2, f, l, 0.0, "paper")
+        assert a.count == b.count == l
+        np.testing.assert_allclose(a.omega, b.omega, rtol=1e-8)
+
+
+def test_pcgtls_indefinite_breakdown():
+    """sigma^2 above sigma'_n^2: A^T A - sigma^2 I is indefinite; a direction of
+    negative curvature gives delta < 0 -> breakdown (spec rule, R3)."""
+    P = _small(m=400, n=16)
+    pc = rqi.factor_precond(P.A, "fp64")
+    sA = np.linalg.svd(P.A, full_matrices=False)
+    v_min = sA[2][-1]
+    sig2 = 2.0 * sA[1][-1] ** 2
+    r = rqi.pcgtls(P.A, pc, sig2, v_min, 5, 1e-14)
+    assert r.breakdown and r.breakdown_j == 0 and r.delta_min < 0
+
+
+def test_cgls_bootstrap_is_least_squares():
+    P = _small(m=800, n=30, kappa=1e3)
+    pc = rqi.factor_precond(P.A, "fp16")
+    r = rqi.pcgtls(P.A, pc, 0.0, P.A.T @ P.b, 200, 1e-13)
+    xls = np.linalg.lstsq(P.A, P.b, rcond=None)[0]
+    np.testing.assert_allclose(r.omega, xls, rtol=1e-9)
+
+
+# ----------------------------------------------------------------------------- RQI
+def _diag_model_trace(s, c, rho, steps):
+    """Alg. 2 with EXACT inner solves written in the right-singular basis
+    y = V^T x of A = U diag(s) V^T (independent of the oracle's code):
+    r = U(c - s y) + b_perp, A^T r = V(s (c - s y)), b^T r = c^T(c - s y) + rho^2,
+    (A^T A - sig2 I) -> diag(s^2 - sig2)."""
+    y = c / s                                          # x_LS
+    e = c - s * y
+    sig0 = (e @ e + rho * rho) / (1 + y @ y)
+    y = y + sig0 * y / s ** 2                          # x_1 = x_0 + sig0 (A^TA)^-1 x_0
+    out = []
+    for _ in range(steps):
+        e = c - s * y
+        yy = y @ y
+        sig2 = (e @ e + rho * rho) / (1 + yy)
+        f = -(s * e) - sig2 * y
+        g = -(c @ e + rho * rho) + sig2
+        psi = math.sqrt((f @ f + g * g) / (yy + 1))
+        out.append((sig2, psi))
+        om = -f / (s * s - sig2)
+        z = y + om
+        beta = (z @ f - g) / (z @ y + 1)
+        u = y / (s * s - sig2)
+        y = z + beta * u
+    return out
+
+
+def test_rqi_matches_diagonal_exact_model():
+    """with u_f = fp64 and inner solves run to tol (budget rule
+    1), the oracle's sigma_k^2 and psi_k follow the exact-solve model step by step."""
+    P = tlsgen.dense_problem(600, 12, 1e2, 1e-2, 21, twin=True)
+    c = P.U.T @ P.b
+    rho = np.linalg.norm(P.b - P.U @ c)
+    pc = rqi.factor_precond(P.A, "fp64")
+    opts = rqi.RqiOptions(budget_rule=1, tol_inner=1e-15, boot_tol=1e-15, polish=1)
+    res = rqi.rqi_pcgtls_mp(P.A, P.b, pc, tol=1e-15, opts=opts)
+    model = _diag_model_trace(P.s, c, rho, len(res.sigma2_trace))
+    normAb2 = np.linalg.norm(P.A) ** 2 + P.b @ P.b
+    checked = 0
+    for k, ((s2m, psim), s2o, psio) in enumerate(zip(model, res.sigma2_trace, res.psi_trace)):
+        assert s2o == pytest.approx(s2m, rel=1e-10)
+        if psim > 1e-13 * normAb2:
+            assert psio == pytest.approx(psim, rel=1e-3)
+            checked += 1
+    assert checked >= 2
+    ex = exact.tls_svd(P.A, P.b)
+    assert math.sqrt(res.sigma2_trace[-1]) == pytest.approx(ex.sigma, rel=1e-12)
+
+
+def test_tau_identity():
+    """with J z = A^T b, tau = b^T(b - A z) - rho = z^T f - g."""
+    P = _small(m=300, n=10, kappa=1e1)
+    x = np.random.default_rng(5).standard_normal(P.n)
+    sig2, f, g, _ = rqi.newton_residual(P.A, P.b, x)
+    J = P.A.T @ P.A - sig2 * np.eye(P.n)
+    z = x + np.linalg.solve(J, -f)
+    np.testing.assert_allclose(J @ z, P.A.T @ P.b, rtol=1e-9)
+    tau1 = P.b @ (P.b - P.A @ z) - sig2
+    tau2 = z @ f - g
+    assert tau1 == pytest.approx(tau2, rel=1e-8)
+
+
+def test_newton_residual_zero_at_solution():
+    """at x_TLS, f = 0 and g = 0 (PAPER.md Eq. newton, l.109-119)."""
+    P = _small()
+    ex = exact.tls_svd(P.A, P.b)
+    sig2, f, g, psi = rqi.newton_residual(P.A, P.b, ex.x)
+    assert sig2 == pytest.approx(ex.sigma ** 2, rel=1e-12)
+    assert psi < 1e-14 * (np.linalg.norm(P.A) ** 2)
+
+
+@pytest.mark.parametrize("u_f", ["fp16", "bf16", "fp32", "fp64"])
+def test_rqi_end_to_end_cfg1(u_f):
+    P = tlsgen.config("cfg1")
+    ex = exact.tls_svd(P.A, P.b)
+    pc, res = rqi.solve(P.A, P.b, u_f)
+    assert res.status == rqi.OK and res.termination == rqi.T_CONVERGED_TOL
+    assert np.linalg.norm(res.x - ex.x) / np.linalg.norm(ex.x) < 1e-12
+    assert abs(res.sigma - ex.sigma) / ex.sigma < 1e-12
+    assert rqi.certify_sigma(P.A, P.b, res.x) == pytest.approx(ex.sigma, rel=1e-12)
+    assert all(a == k + 1 and b == k + 1 for k, (a, b) in enumerate(res.pcg_iters, start=1))
+
+
+def test_mixed_precision_needs_at_least_as_many_steps():
+    """MP performs at least as many RQI steps as the
+    uniform-precision run and reaches a similar limiting accuracy."""
+    P = tlsgen.config("cfg2w", m=2048, n=256)
+    ex = exact.tls_svd(P.A, P.b)
+    K = {}
+    for u_f in ("fp64", "fp16", "bf16"):
+        _, res = rqi.solve(P.A, P.b, u_f)
+        assert res.status == rqi.OK
+        K[u_f] = res.rqi_iters
+        assert np.linalg.norm(res.x - ex.x) / np.linalg.norm(ex.x) < 1e-10
+    assert K["fp16"] >= K["fp64"] and K["bf16"] >= K["fp64"]
+
+
+def test_literal_cfg2_breaks_down_at_first_step():
+    """Reading R8: on literal cfg2, RQ(x_LS) lies far above sigma'_n^2, so the first
+    PCG step meets negative curvature even with an exact factor."""
+    P = tlsgen.config("cfg2")
+    for u_f in ("fp64", "bf16"):
+        _, res = rqi.solve(P.A, P.b, u_f)
+        assert res.status == rqi.PCG_BREAKDOWN and res.breakdown_k == 1 and res.breakdown_j == 0
+
+
+def test_sparse_matches_dense():
+    Pc = tlsgen.csr_problem(m=3000, n=60, per_row=6, seed=7)
+    As = scipy.sparse.csr_matrix((Pc.vals, Pc.colidx, Pc.rowptr), shape=(Pc.m, Pc.n))
+    Ad = Pc.to_dense()
+    assert np.all(np.diff(Pc.rowptr) == 7)
+    for i in range(0, Pc.m, 397):                        # A20: distinct + fixed column
+        cols = Pc.colidx[Pc.rowptr[i]:Pc.rowptr[i + 1]]
+        assert len(set(cols)) == 7 and (i % Pc.n) in cols and np.all(np.diff(cols) > 0)
+    pcs, rs = rqi.solve(As, Pc.b, "fp16")
+    pcd, rd = rqi.solve(Ad, Pc.b, "fp16")
+    assert np.array_equal(pcs.Rt, pcd.Rt)
+    assert rs.rqi_iters == rd.rqi_iters
+    np.testing.assert_allclose(rs.x, rd.x, rtol=1e-12)
+    ex = exact.tls_svd(Ad, Pc.b)
+    np.testing.assert_allclose(rs.x, ex.x, rtol=1e-11)
+
+
+# ----------------------------------------------------------------------------- cost model
+def test_cost_model_equals_sum_of_alg4_line_counts():
+    """PAPER.md l.410-412 closed form == the per-line op counts printed in Alg. 4
+    (l.227-255), PCGTLS performing exactly k+1 iterations at step k (l.405)."""
+    for (m, n, r) in [(100, 60, 8), (30, 15, 5), (4096, 512, 7), (200, 20, 1)]:
+        pre = (2*m*n + m) + (2*m + 2*n - 2) + (2*n*n) + (2*n)          # l.227-236 minus QR
+        qr = 2*m*n*n - 2*n**3 / 3                                      # l.231-232
+        per_k = lambda k: ((2*m*n + m) + (2*m + 2*n - 2) + (2*m*n + 2*n) + (2*m - 1)
+                           + n + (4*n - 2) + (2*n))                    # l.238-255, u lines
+        pcg_k = lambda k: 2 * ((k + 1) * (2*n*n + 14*n - 3) + (n*n + 2*n - 1))   # l.246-253
+        tot_u = pre + sum(per_k(k) for k in range(1, r + 1))
+        tot_p = sum(pcg_k(k) for k in range(1, r + 1))
+        assert perfmodel.cost(m, n, r, 1, 0, 0) == tot_u
+        assert perfmodel.cost(m, n, r, 0, 1, 0) == tot_p
+        assert float(perfmodel.cost(m, n, r, 0, 0, 1)) == pytest.approx(qr, rel=1e-15)
+    # "speedup never below 1" (l.449) and "up to 4x" (l.26)
+    for (m, n, r) in [(10**6, 10**3, 5), (10**4, 10**4, 2000), (100, 60, 8)]:
+        s = perfmodel.speedup(m, n, r)
+        assert 1.0 <= s <= 4.0

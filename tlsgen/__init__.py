@@ -1,0 +1,220 @@
+"""Seeded synthetic TLS problem generators (shared by the oracle tests, the GPU
+parity tests and bench.py).
+
+This module holds NO arithmetic of the RQI-PCGTLS-MP method: it only draws
+random numbers and builds the input matrices A, b of BASELINE.json's configs
+(DESIGN.md "Input recipe").  The oracle (oracle/) and the CUDA path
+(paper_2305_19028_b200/) both consume the bytes produced here and nothing else
+from each other.
+
+Construction (BASELINE.json configs[0..4]):
+  A = U diag(s) V^T,  U (m x n) orthonormalised Gaussian (Householder QR of a
+  Gaussian, columns sign-fixed so diag(R) > 0), V (n x n) the same ("Haar"),
+  s = logspace(0, -log10(kappa), n), x_true ~ N(0, I), g ~ N(0, I),
+  b = A x_true + eps * g            (literal configs)
+  b = A x_true + eps * g / sqrt(m)  ("w" twins, reading R3)
+A is returned row-major (C-contiguous) fp64, which is the layout the C ABI
+takes (include/tlsrqi.h, TLS_DENSE_ROWMAJOR).
+
+Draw order (fixed): G_U (m*n), G_V (n*n), x_true (n), g (m).
+CPU generation uses numpy Generator(PCG64(seed)); the large configs (cfg4,
+cfg5 at full size) are generated on a CUDA device with torch's seeded Philox
+generator + torch.linalg.qr, because a host QR of a 2^20 x 1024 matrix takes
+minutes.  Either way the oracle and the GPU read the same bytes.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import Optional
+
+import numpy as np
+
+__all__ = [
+    "DenseProblem", "CsrProblem", "dense_problem", "csr_problem", "config",
+    "CONFIGS", "shard_rows",
+]
+
+
+@dataclasses.dataclass
+class DenseProblem:
+    name: str
+    A: object            # (m, n) float64 row-major; numpy array or torch tensor
+    b: object            # (m,) float64
+    x_true: object       # (n,)
+    s: np.ndarray        # (n,) singular values of A by construction
+    V: Optional[object]  # (n, n) right singular vectors of A (small cases)
+    U: Optional[object]  # (m, n) left singular vectors (small cases only)
+    kappa: float
+    eps: float
+    twin: bool
+    seed: int
+    u_f: str = "fp16"
+
+    @property
+    def m(self) -> int:
+        return int(self.A.shape[0])
+
+    @property
+    def n(self) -> int:
+        return int(self.A.shape[1])
+
+
+@dataclasses.dataclass
+class CsrProblem:
+    name: str
+    m: int
+    n: int
+    rowptr: np.ndarray   # (m+1,) int64
+    colidx: np.ndarray   # (nnz,) int32, sorted within each row
+    vals: np.ndarray     # (nnz,) float64
+    b: np.ndarray        # (m,)
+    x_true: np.ndarray   # (n,)
+    eps: float
+    seed: int
+    u_f: str = "fp16"
+
+    def to_dense(self) -> np.ndarray:
+        A = np.zeros((self.m, self.n))
+        rows = np.repeat(np.arange(self.m), np.diff(self.rowptr))
+        A[rows, self.colidx] = self.vals
+        return A
+
+
+def _orthonormal_np(G: np.ndarray) -> np.ndarray:
+    Q, R = np.linalg.qr(G, mode="reduced")
+    sgn = np.sign(np.diag(R))
+    sgn[sgn == 0] = 1.0
+    return Q * sgn[None, :]
+
+
+def dense_problem(m: int, n: int, kappa: float, eps: float, seed: int,
+                  twin: bool = False, device: str = "cpu", name: str = "",
+                  u_f: str = "fp16", keep_factors: Optional[bool] = None) -> DenseProblem:
+    """Build A = U diag(s) V^T and b = A x_true + noise (module docstring).
+
+    device="cpu": numpy arrays; device="cuda[:i]": torch tensors on that device.
+    keep_factors: return U and V (default: only when m*n <= 2^22).
+    """
+    if keep_factors is None:
+        keep_factors = m * n <= (1 << 22)
+    s = np.logspace(0.0, -math.log10(kappa), n)
+    scale = eps / math.sqrt(m) if twin else eps
+    if device == "cpu":
+        rng = np.random.Generator(np.random.PCG64(seed))
+        GU = rng.standard_normal((m, n))
+        GV = rng.standard_normal((n, n))
+        x_true = rng.standard_normal(n)
+        g = rng.standard_normal(m)
+        U = _orthonormal_np(GU)
+        del GU
+        V = _orthonormal_np(GV)
+        A = np.ascontiguousarray((U * s[None, :]) @ V.T)
+        b = A @ x_true + scale * g
+        return DenseProblem(name, A, b, x_true, s, V if keep_factors else None,
+                            U if keep_factors else None, kappa, eps, twin, seed, u_f)
+    import torch
+    dev = torch.device(device)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    GU = torch.randn((m, n), generator=gen, dtype=torch.float64, device=dev)
+    GV = torch.randn((n, n), generator=gen, dtype=torch.float64, device=dev)
+    x_true = torch.randn((n,), generator=gen, dtype=torch.float64, device=dev)
+    g = torch.randn((m,), generator=gen, dtype=torch.float64, device=dev)
+    U, R = torch.linalg.qr(GU, mode="reduced")
+    del GU
+    sg = torch.sign(torch.diagonal(R))
+    sg[sg == 0] = 1.0
+    U.mul_(sg[None, :])
+    del R
+    V, RV = torch.linalg.qr(GV, mode="reduced")
+    sv = torch.sign(torch.diagonal(RV))
+    sv[sv == 0] = 1.0
+    V = V * sv[None, :]
+    st = torch.as_tensor(s, dtype=torch.float64, device=dev)
+    A = U @ (st[:, None] * V.T)
+    if not keep_factors:
+        del U
+        U = None
+    A = A.contiguous()
+    b = A @ x_true + scale * g
+    return DenseProblem(name, A, b, x_true, s, V if keep_factors else None,
+                        U, kappa, eps, twin, seed, u_f)
+
+
+def csr_problem(m: int = 200000, n: int = 2000, per_row: int = 10, eps: float = 1e-3,
+                seed: int = 3, name: str = "cfg3", u_f: str = "fp16") -> CsrProblem:
+    """BASELINE.json configs[2]: each row i holds `per_row` DISTINCT columns drawn
+    uniformly from {0..n-1} minus {i mod n}, plus column i mod n (DESIGN.md
+    reading R9); values N(0,1); columns sorted; b = A x_true + eps*g.
+    Draw order: per row the column sample, then all values, then x_true, g."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    cols = np.empty((m, per_row + 1), dtype=np.int64)
+    diag = np.arange(m) % n
+    # Distinct draws by whole-row rejection: draw per_row values in [0, n-1);
+    # redraw every row that holds a duplicate; then shift values >= i mod n by
+    # one so the fixed column is never drawn.
+    cand = rng.integers(0, n - 1, size=(m, per_row))
+    while True:
+        srt = np.sort(cand, axis=1)
+        dup = (srt[:, 1:] == srt[:, :-1]).any(axis=1)
+        if not dup.any():
+            break
+        cand[dup] = rng.integers(0, n - 1, size=(int(dup.sum()), per_row))
+    cand = cand + (cand >= diag[:, None])
+    cols[:, :per_row] = cand
+    cols[:, per_row] = diag
+    cols.sort(axis=1)
+    vals = rng.standard_normal(m * (per_row + 1))
+    x_true = rng.standard_normal(n)
+    g = rng.standard_normal(m)
+    rowptr = np.arange(0, m * (per_row + 1) + 1, per_row + 1, dtype=np.int64)
+    colidx = cols.reshape(-1).astype(np.int32)
+    # b = A x_true + eps g, A applied row by row from the CSR arrays
+    prod = (vals * x_true[colidx]).reshape(m, per_row + 1).sum(axis=1)
+    b = prod + eps * g
+    return CsrProblem(name, m, n, rowptr, colidx, vals, b, x_true, eps, seed, u_f)
+
+
+# name -> (m, n, kappa, eps, seed, twin, u_f); cfg3 (CSR) handled separately.
+CONFIGS = {
+    "cfg1": (200, 20, 1e2, 1e-4, 1, False, "fp16"),
+    "cfg2": (4096, 512, 1e3, 1e-3, 2, False, "bf16"),
+    "cfg2w": (4096, 512, 1e3, 1e-3, 2, True, "bf16"),
+    "cfg4": (1 << 20, 1024, 1e4, 1e-3, 4, False, "fp16"),
+    "cfg4w": (1 << 20, 1024, 1e4, 1e-3, 4, True, "fp16"),
+}
+
+
+def config(name: str, device: str = "cpu", **kw):
+    """Build one of BASELINE.json's configs by name.
+
+    cfg5 cells are named "cfg5:k1e4:e1e-6" (kappa, eps); u_f is chosen by the caller.
+    Scaled-down stand-ins keep the recipe: pass m=..., n=... to override sizes.
+    """
+    if name == "cfg3":
+        return csr_problem(**kw)
+    if name.startswith("cfg5"):
+        fields = name.split(":")
+        kappa = float(fields[1][1:]) if len(fields) > 1 else 1e4
+        eps = float(fields[2][1:]) if len(fields) > 2 else 1e-6
+        m = kw.pop("m", 65536)
+        n = kw.pop("n", 2048)
+        return dense_problem(m, n, kappa, eps, 5, twin=False, device=device, name=name,
+                             u_f=kw.pop("u_f", "fp16"), **kw)
+    m, n, kappa, eps, seed, twin, u_f = CONFIGS[name]
+    m = kw.pop("m", m)
+    n = kw.pop("n", n)
+    return dense_problem(m, n, kappa, eps, seed, twin=twin, device=device, name=name,
+                         u_f=kw.pop("u_f", u_f), **kw)
+
+
+def shard_rows(m: int, nranks: int, rank: int) -> tuple[int, int]:
+    """Contiguous row block [lo, hi) of rank `rank` out of `nranks`:
+    the first m % nranks ranks get one extra row."""
+    if not (0 <= rank < nranks):
+        raise ValueError("rank out of range")
+    base, extra = divmod(m, nranks)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
