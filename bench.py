@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""bench.py — TLS time-to-solution of the B200 RQI-PCGTLS-MP hot path.
+
+One step = one whole hot path on one (A, b): tls_factor_precond (§8 rows a1-a3)
++ tls_rqi_pcgtls (a4-a9), inputs resident in HBM.  Default workload: cfg4w,
+the well-posed twin of BASELINE.json configs[3] (dense 2^20 x 1024 fp64,
+kappa 1e4, u_f fp16; reading R8), row-sharded over N GPUs.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one process per GPU, RANK/LOCAL_RANK/WORLD_SIZE
+from the env); times are CUDA events on the solve stream, max over ranks.
+Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle
+(oracle/, the only reference this paper has) on a bounded sample of the same
+workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "TLS time-to-solution (s) & PCG iters/s, % HBM roofline, 1/2/4/8 B200"
+WORKLOADS = {
+    # name: (tlsgen config, m, n, u_f, description)
+    "cfg4w": ("cfg4w", 1 << 20, 1024, "fp16",
+              "cfg4w: dense 1048576x1024 fp64 A=U diag(s) V^T, kappa 1e4, b noise 1e-3*N(0,1)/sqrt(m), u_f fp16"),
+    "cfg4": ("cfg4", 1 << 20, 1024, "fp16",
+             "cfg4 (literal): dense 1048576x1024 fp64, kappa 1e4, b noise 1e-3*N(0,1), u_f fp16"),
+    "cfg2w": ("cfg2w", 4096, 512, "bf16", "cfg2w: dense 4096x512 fp64, kappa 1e3, u_f bf16"),
+    "cfg5": ("cfg5:k1e4:e1e-6", 65536, 2048, "fp16", "cfg5 cell kappa 1e4 eps 1e-6: dense 65536x2048 fp64, u_f fp16"),
+}
+
+
+def _env_int(k, d):
+    v = os.environ.get(k)
+    return int(v) if v not in (None, "") else d
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            j = json.load(fh)
+        return float(j.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, gpu_index: int):
+        self.p = None
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        for ln in out.strip().splitlines():
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for name, val in zip(self.NAMES, f[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        loaded = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def make_problem(wl, device):
+    import tlsgen
+    cfg, m, n, u_f, _ = WORKLOADS[wl]
+    return tlsgen.config(cfg, device=device, keep_factors=False), u_f
+
+
+# ----------------------------------------------------------------------------- oracle timing
+def oracle_sample(A_np, b_np, u_f, counts, row_scale=16, iters=2):
+    """Time the CPU oracle on a bounded sample of the workload and scale it to one
+    whole solve: (1) the oracle preconditioner build on the first m/row_scale rows
+    (its cost is linear in m), x row_scale; (2) `iters` oracle PCGTLS iterations
+    (A-in-loop, one RHS) and one residual evaluation on the FULL A; composed with
+    the iteration counts of the solve (same algorithm, same counts):
+      T = row_scale*t_factor + t_resid*(K + 2) + t_iter*(B0 + sum_k (c_a + c_b))."""
+    from oracle import rqi as orq
+    import numpy as np
+    m, n = A_np.shape
+    blk = max(n + 1, m // row_scale)
+    t0 = time.perf_counter()
+    pc = orq.factor_precond(A_np[:blk], u_f)
+    t_factor = (time.perf_counter() - t0) * (m / blk)
+    f = np.ones(n)
+    t0 = time.perf_counter()
+    orq.pcgtls(A_np, pc, 0.0, f, iters, 0.0, "A")
+    t_iter = (time.perf_counter() - t0) / iters
+    x = np.zeros(n)
+    t0 = time.perf_counter()
+    orq.newton_residual(A_np, b_np, x)
+    t_resid = time.perf_counter() - t0
+    K, B0, pcg = counts
+    total = t_factor + t_resid * (K + 2) + t_iter * (B0 + sum(a + b for a, b in pcg))
+    sample = (f"oracle factor on {blk} of {m} rows (x{m / blk:.0f}) + {iters} oracle PCGTLS iterations "
+              f"and 1 residual pass on the full A, composed with the solve's counts K={K}, B0={B0}, "
+              f"PCG={sum(a + b for a, b in pcg)}")
+    return total, sample, {"t_factor_s": t_factor, "t_iter_s": t_iter, "t_resid_s": t_resid}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands, on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import numpy as np
+    import torch
+    from oracle import rqi as orq
+    wl = args.workload
+    dev = "cuda:0" if torch.cuda.is_available() else "cpu"
+    P, u_f = make_problem(wl, dev)
+    A_np = P.A.cpu().numpy() if hasattr(P.A, "cpu") else P.A
+    b_np = P.b.cpu().numpy() if hasattr(P.b, "cpu") else P.b
+    del P
+    # the oracle's own counts on this workload need a full oracle solve (too long);
+    # use the counts recorded by the last GPU run when present, else the oracle on
+    # a 1/16 row block as a stand-in for K and B0
+    counts = None
+    cpath = os.path.join(ROOT, "profiles", f"counts_{wl}.json")
+    if os.path.exists(cpath):
+        with open(cpath) as fh:
+            c = json.load(fh)
+        counts = (c["K"], c["B0"], [tuple(p) for p in c["pcg"]])
+    if counts is None:
+        blk = A_np.shape[0] // 16
+        _, res = orq.solve(A_np[:blk], b_np[:blk], u_f)
+        counts = (res.rqi_iters, res.boot_iters, res.pcg_iters)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t, sample, parts = oracle_sample(A_np, b_np, u_f, counts, row_scale=64, iters=1)
+        if it >= args.warmup:
+            times.append(t)
+    v = statistics.mean(times)
+    cores = os.cpu_count()
+    line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": WORKLOADS[wl][4], "m": int(A_np.shape[0]), "n": int(A_np.shape[1]),
+                       "u_f": u_f, "l2": "inputs larger than L2", "parallelism": "host cores"},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "parts": parts}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg4w", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
+    if args.gpus > 1 and world == 1:
+        sys.exit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+
+    import torch
+    import torch.distributed as tdist
+    if world > 1:
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        if world > 1:
+            tdist.destroy_process_group()
+        return
+
+    torch.cuda.set_device(local)
+    from paper_2305_19028_b200 import build as _build, dist as pdist, tlsrqi
+    _build.build()
+    tlsrqi.lib()
+    wl = args.workload
+    _, m, n, u_f, desc = WORKLOADS[wl]
+
+    P, u_f = make_problem(wl, f"cuda:{local}")
+    m = P.m
+    lo, hi = pdist.shard_rows(m, world, rank)
+    A_loc = P.A[lo:hi].clone()
+    b_loc = P.b[lo:hi].clone()
+    keep_host = (rank == 0 and world == 1 and not args.no_cpu_baseline)
+    A_full_host = P.A.cpu() if keep_host else None
+    b_full_host = P.b.cpu() if keep_host else None
+    del P
+    torch.cuda.empty_cache()
+    comm = pdist.init_comm(local) if world > 1 else None
+    M = tlsrqi.matrix(A_loc, m_global=m, row_offset=lo)
+    ws = tlsrqi.workspace(M)
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        rc, R, fi = tlsrqi.tls_factor_precond(M, u_f, comm=comm, stream=stream, ws=ws)
+        if R is None:
+            raise RuntimeError(f"factor failed: {tlsrqi.STATUS.get(rc)}")
+        rc, _, sig, info = tlsrqi.tls_rqi_pcgtls(M, b_loc, R, comm=comm, stream=stream, ws=ws, x_out=x)
+        return fi, info, sig
+
+    for _ in range(args.warmup):
+        fi, info, sig = step()
+    tlsrqi.tls_profile_enable(True)
+    sampler = ClockSampler(local)
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    launches = 0
+    passes = 0
+    infos = []
+    for _ in range(args.steps):
+        fi, info, sig = step()
+        launches += fi["launches"] + info["launches"]
+        passes += fi["passes"] + info["passes"]
+        infos.append(info)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
+    clocks = sampler.stop()
+    prof = tlsrqi.tls_profile_read()
+    tlsrqi.tls_profile_enable(False)
+    ms_total = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    tts = ms_step / 1e3
+
+    info = infos[-1]
+    pcg_per_solve = info["boot_iters"] + sum(a + b for a, b in info["pcg_iters"])
+    peak, peak_kind = load_peaks()
+    p2 = prof["pass_op2"]
+    bytes_per_pass = 8.0 * (hi - lo) * M.ld
+    roof = None
+    if p2["count"] > 0:
+        avg_ms = p2["ms"] / p2["count"]
+        ach = bytes_per_pass / (avg_ms * 1e-3) / 1e9
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", f"traffic_{wl}.json")
+        if os.path.exists(tpath):
+            with open(tpath) as fh:
+                traffic = json.load(fh).get("pass_op2_dram_bytes_per_launch")
+        roof = {"kernel": "k_pass<2,operator> (t = A q, v = A^T t, 2 RHS, one read of A)",
+                "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": traffic, "algorithmic_bytes_per_launch": bytes_per_pass,
+                "avg_launch_ms": avg_ms, "launches": p2["count"], "peak_kind": peak_kind}
+    kshare = {k: v["ms"] / ms_total for k, v in prof.items() if v["count"]}
+
+    # ---- e2e: the same solve through tls_solve_host from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        A_h = A_loc.cpu().pin_memory()
+        b_h = b_loc.cpu().pin_memory()
+        x_h = torch.empty(n, dtype=torch.float64).pin_memory()
+        dev_buf = torch.empty(tlsrqi.tls_solve_host_bytes(hi - lo, n, M.ld), dtype=torch.uint8, device="cuda")
+        del A_loc
+        torch.cuda.empty_cache()
+        tlsrqi.tls_solve_host(A_h, b_h, u_f, dev_buf=dev_buf, stream=stream, x_host=x_h, comm=comm,
+                              m_global=m, row_offset=lo)
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            tlsrqi.tls_solve_host(A_h, b_h, u_f, dev_buf=dev_buf, stream=stream, x_host=x_h, comm=comm,
+                                  m_global=m, row_offset=lo)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": e_ms / args.steps / 1e3, "unit": "s",
+               "h2d_bytes_per_step": int(A_h.numel() * 8 + b_h.numel() * 8),
+               "d2h_bytes_per_step": int(n * 8)}
+
+    if rank == 0:
+        os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+        with open(os.path.join(ROOT, "profiles", f"counts_{wl}.json"), "w") as fh:
+            json.dump({"K": info["rqi_iters"], "B0": info["boot_iters"], "pcg": info["pcg_iters"]}, fh)
+
+    cpu = None
+    if keep_host:
+        import numpy as np
+        counts = (info["rqi_iters"], info["boot_iters"], info["pcg_iters"])
+        t_cpu, sample, parts = oracle_sample(A_full_host.numpy(), b_full_host.numpy(), u_f, counts)
+        cpu = {"value": t_cpu, "unit": "s", "cores": os.cpu_count(), "kind": "oracle", "sample": sample,
+               "parts": parts}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": tts, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "m": m, "n": n, "u_f": u_f, "ld": int(M.ld),
+                       "l2": "inputs larger than L2 (A = %.1f GB)" % (8.0 * m * n / 1e9),
+                       "parallelism": f"row-shard x{world} (NCCL all-reduce)"},
+            "status": info["status_name"], "termination": info["termination_name"],
+            "rqi_iters": info["rqi_iters"], "boot_iters": info["boot_iters"], "pcg_iters": info["pcg_iters"],
+            "sigma": sig, "pcg_iters_per_s": pcg_per_solve / tts,
+            "passes_per_step": passes / args.steps,
+            "a_passes_per_s": passes / args.steps / tts,
+            "roofline": roof, "kernel_share": kshare,
+            "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if comm:
+        tlsrqi.tls_comm_destroy(comm)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,168 @@
+// k_gram.cu — the u_f Gram matrix G = A^^T A^, A^ = fl_uf(A D^{-1})  (
+// PAPER.md l.231, l.290-307; readings R10, R11).
+//
+// This file holds the CUDA-core SYRK path: 64x64 upper tiles, split-K over
+// chunks of K_t rows.  For u_f in {fp16, bf16} each chunk is accumulated in
+// fp32 (products of u_f values are exact in fp32, as on the tensor cores) and
+// drained into fp64 registers at the chunk end; for u_f in {fp32, fp64} the
+// accumulation is fp64.  Partial tiles are summed over splits in fixed order.
+#include "tls_common.cuh"
+#include "tls_kernels.h"
+
+namespace tls {
+
+constexpr int kGT = 64;    // tile edge
+constexpr int kGKB = 32;   // rows per smem step
+
+static void gram_shape(const DenseView& A, int K_t, int& TT, int& ntiles, int& nchunks, int& nsplit) {
+  TT = (A.n + kGT - 1) / kGT;
+  ntiles = TT * (TT + 1) / 2;
+  nchunks = (int)((A.m + K_t - 1) / K_t);
+  if (nchunks < 1) nchunks = 1;
+  const int target = 4 * num_sms();
+  nsplit = (target + ntiles - 1) / ntiles;
+  if (nsplit > nchunks) nsplit = nchunks;
+  if (nsplit < 1) nsplit = 1;
+}
+
+size_t gram_ws_doubles(const DenseView& A, int K_t) {
+  int TT, nt, nc, ns;
+  gram_shape(A, K_t, TT, nt, nc, ns);
+  return (size_t)ns * nt * kGT * kGT;
+}
+
+template <typename ACC, int PREC>
+__global__ void __launch_bounds__(256)
+k_gram_cc(const double* __restrict__ A, int64_t m, int n, int64_t ld, const double* __restrict__ dinv,
+          int K_t, int nchunks, int nsplit, int TT, double* __restrict__ part, int* __restrict__ range) {
+  __shared__ ACC As[kGKB][kGT + 4];
+  __shared__ ACC Bs[kGKB][kGT + 4];
+  // tile index -> (I, J), I <= J, row-major over the upper triangle of tiles
+  int t = blockIdx.x, I = 0;
+  while (t >= TT - I) { t -= TT - I; ++I; }
+  const int J = I + t;
+  const bool diag = (I == J);
+  const int s = blockIdx.y;
+  const int c0 = (int)((int64_t)nchunks * s / nsplit), c1 = (int)((int64_t)nchunks * (s + 1) / nsplit);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int I0 = I * kGT, J0 = J * kGT;
+
+  double dacc[4][4];
+  ACC facc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dacc[i][j] = 0.0;
+  int bad = 0;
+
+  for (int c = c0; c < c1; ++c) {
+    const int64_t rb = (int64_t)c * K_t;
+    const int64_t re = min(rb + (int64_t)K_t, m);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) facc[i][j] = (ACC)0;
+    for (int64_t r = rb; r < re; r += kGKB) {
+      // stage kGKB rows x 64 columns for I (and J) as rounded u_f values
+      for (int e = threadIdx.x; e < kGKB * kGT; e += 256) {
+        const int rr = e / kGT, cc = e % kGT;
+        const int64_t row = r + rr;
+        ACC va = (ACC)0, vb = (ACC)0;
+        if (row < re) {
+          const int ca = I0 + cc;
+          if (ca < n) {
+            const double v = round_uf(A[row * ld + ca] * dinv[ca], PREC);
+            bad |= !isfinite(v);
+            va = (ACC)v;
+          }
+          if (!diag) {
+            const int cb = J0 + cc;
+            if (cb < n) {
+              const double v = round_uf(A[row * ld + cb] * dinv[cb], PREC);
+              bad |= !isfinite(v);
+              vb = (ACC)v;
+            }
+          }
+        }
+        As[rr][cc] = va;
+        if (!diag) Bs[rr][cc] = vb;
+      }
+      __syncthreads();
+      const ACC(*Bp)[kGT + 4] = diag ? As : Bs;
+#pragma unroll 8
+      for (int k = 0; k < kGKB; ++k) {
+        ACC a[4], bb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = As[k][ty * 4 + i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bb[j] = Bp[k][tx * 4 + j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) facc[i][j] = fma(a[i], bb[j], facc[i][j]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dacc[i][j] += (double)facc[i][j];
+  }
+  if (bad) atomicExch(range, 1);
+  double* out = part + ((size_t)s * gridDim.x + blockIdx.x) * (kGT * kGT);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) out[(ty * 4 + i) * kGT + tx * 4 + j] = dacc[i][j];
+}
+
+// Sum the split partials in fixed order; write the tile and its mirror image.
+__global__ void k_gram_reduce(const double* __restrict__ part, int ntiles, int nsplit, int TT, int n,
+                              double* __restrict__ G) {
+  int t = blockIdx.x, I = 0;
+  while (t >= TT - I) { t -= TT - I; ++I; }
+  const int J = I + t;
+  for (int e = threadIdx.x; e < kGT * kGT; e += blockDim.x) {
+    const int i = e / kGT, j = e % kGT;
+    const int gi = I * kGT + i, gj = J * kGT + j;
+    double acc = 0.0;
+    for (int s = 0; s < nsplit; ++s) acc += part[((size_t)s * ntiles + blockIdx.x) * (kGT * kGT) + e];
+    if (gi < n && gj < n) {
+      G[(size_t)gi * n + gj] = acc;
+      G[(size_t)gj * n + gi] = acc;
+    }
+  }
+}
+
+int launch_gram(const DenseView& A, int u_f, const double* dinv, int K_t, double* G, double* ws,
+                size_t ws_doubles, int* range_flag, cudaStream_t st, int* launches) {
+  if (K_t < 1) K_t = 2048;
+  int TT, ntiles, nchunks, nsplit;
+  gram_shape(A, K_t, TT, ntiles, nchunks, nsplit);
+  if ((size_t)nsplit * ntiles * kGT * kGT > ws_doubles) {
+    set_error("gram: workspace too small");
+    return TLS_ERR_WORKSPACE;
+  }
+  dim3 grid(ntiles, nsplit);
+  switch (u_f) {
+    case TLS_FP16:
+      k_gram_cc<float, TLS_FP16><<<grid, 256, 0, st>>>(A.A, A.m, A.n, A.ld, dinv, K_t, nchunks, nsplit, TT, ws, range_flag);
+      break;
+    case TLS_BF16:
+      k_gram_cc<float, TLS_BF16><<<grid, 256, 0, st>>>(A.A, A.m, A.n, A.ld, dinv, K_t, nchunks, nsplit, TT, ws, range_flag);
+      break;
+    case TLS_FP32:
+      k_gram_cc<double, TLS_FP32><<<grid, 256, 0, st>>>(A.A, A.m, A.n, A.ld, dinv, K_t, nchunks, nsplit, TT, ws, range_flag);
+      break;
+    default:
+      k_gram_cc<double, TLS_FP64><<<grid, 256, 0, st>>>(A.A, A.m, A.n, A.ld, dinv, K_t, nchunks, nsplit, TT, ws, range_flag);
+      break;
+  }
+  TLS_LAUNCH_CHECK();
+  k_gram_reduce<<<ntiles, 256, 0, st>>>(ws, ntiles, nsplit, TT, A.n, G);
+  TLS_LAUNCH_CHECK();
+  if (launches) *launches += 2;
+  return 0;
+}
+
+}  // namespace tls

@@ -1,0 +1,367 @@
+// k_pass.cu — the HBM-bound streaming passes over A.
+//
+// One persistent CTA per SM streams a contiguous block of rows of A through a
+// 6-stage shared-memory ring filled by the TMA bulk-copy engine
+// (cp.async.bulk, one elected producer lane, mbarrier completion); 8 consumer
+// warps own fixed column chunks (16 B each) of every row, so q and the
+// accumulator v = A^T t live in registers for the whole pass and A is read from
+// HBM exactly once.  Per group of rows the row dot products t_i = a_i . q are
+// reduced across the CTA (warp transpose-reduce + one shared-memory exchange),
+// then v += t_i a_i.  Modes:
+//   operator (a7):  t = A q_r (r < nrhs), v_r = A^T t_r, s_r = t_r^T t_r
+//   residual (a5):  t = b - A x, v = A^T t, s0 = t^T t, s1 = b^T t
+//   colstats (a1):  per column max |a_ij| and sum a_ij^2
+// Each CTA writes a partial; k_reduce_partials sums them in fixed CTA order
+// (deterministic).
+#include "tls_common.cuh"
+#include "tls_kernels.h"
+
+namespace tls {
+
+constexpr int kPassConsumers = 256;
+constexpr int kPassWarps = kPassConsumers / 32;
+constexpr int kPassThreads = kPassConsumers + 32;
+constexpr int kPassStages = 6;
+constexpr int kPassStageBytes = 32 * 1024;
+constexpr size_t kPassSmem = (size_t)kPassStages * kPassStageBytes + 2 * kPassStages * 8 +
+                             (kPassWarps * 16 + 16 + 32) * 8;
+
+static int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+static int rows_per_stage(const DenseView& A) {
+  int64_t r = kPassStageBytes / (A.ld * 8);
+  return (int)(r < 1 ? 1 : r);
+}
+
+int pass_grid(const DenseView& A) {
+  const int rps = rows_per_stage(A);
+  int64_t stages = (A.m + rps - 1) / rps;
+  int64_t g = num_sms();
+  if (stages < g) g = stages;
+  return (int)(g < 1 ? 1 : g);
+}
+
+size_t pass_partials_doubles(const DenseView& A) {
+  return (size_t)pass_grid(A) * (size_t)(2 * A.n + 2);
+}
+
+template <int NRHS, int MODE, int CPT>
+__global__ void __launch_bounds__(kPassThreads, 1)
+k_pass(const double* __restrict__ A, int64_t m, int n, int64_t ld, int rps,
+       const double* __restrict__ q, const double* __restrict__ b,
+       double* __restrict__ partials, int W, const int* __restrict__ active) {
+  if (active != nullptr && *active == 0) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* ring = reinterpret_cast<double*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kPassStages * kPassStageBytes);
+  uint64_t* empty = full + kPassStages;
+  double* red = reinterpret_cast<double*>(empty + kPassStages);  // [warps][16]
+  double* tfin = red + kPassWarps * 16;                           // [16]
+  double* sred = tfin + 16;                                       // [32]
+  constexpr int kStageDoubles = kPassStageBytes / 8;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t G = gridDim.x;
+  const int64_t r0 = m * (int64_t)blockIdx.x / G;
+  const int64_t r1 = m * (int64_t)(blockIdx.x + 1) / G;
+  const int nst = (int)((r1 - r0 + rps - 1) / rps);
+
+  if (tid == 0) {
+    for (int s = 0; s < kPassStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kPassWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kPassWarps) {  // ---------------- producer: TMA bulk copies of row blocks
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      for (int it = 0; it < nst; ++it) {
+        const int s = it % kPassStages;
+        const uint32_t ph = (uint32_t)(it / kPassStages) & 1u;
+        if (it >= kPassStages) mbar_wait(&empty[s], ph ^ 1u);
+        const int64_t rs = r0 + (int64_t)it * rps;
+        const int rows = (int)min((int64_t)rps, r1 - rs);
+        const uint32_t bytes = (uint32_t)(rows * ld * 8);
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_g2s(ring + (size_t)s * kStageDoubles, A + rs * ld, bytes, &full[s], pol);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers
+  constexpr int RB = (CPT >= 8) ? 1 : 8 / CPT;  // rows per reduction group
+  constexpr int V = RB * NRHS;
+  const int nchunks = (n + 1) >> 1;
+
+  double2 qr[NRHS][CPT];
+  double2 acc[NRHS][CPT];
+  bool okc[CPT], ok1[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int ch = tid + c * kPassConsumers;
+    const int col = 2 * ch;
+    okc[c] = ch < nchunks;
+    ok1[c] = col + 1 < n;
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) {
+      acc[r][c] = make_double2(0.0, 0.0);
+      if (MODE != PASS_COLSTATS) {
+        const double qx = okc[c] ? q[(size_t)r * n + col] : 0.0;
+        const double qy = ok1[c] ? q[(size_t)r * n + col + 1] : 0.0;
+        qr[r][c] = make_double2(qx, qy);
+      }
+    }
+  }
+  double sacc = 0.0, sacc2 = 0.0;
+
+  for (int it = 0; it < nst; ++it) {
+    const int s = it % kPassStages;
+    const uint32_t ph = (uint32_t)(it / kPassStages) & 1u;
+    mbar_wait(&full[s], ph);
+    const double* st = ring + (size_t)s * kStageDoubles;
+    const int64_t rs = r0 + (int64_t)it * rps;
+    const int rows = (int)min((int64_t)rps, r1 - rs);
+
+    if (MODE == PASS_COLSTATS) {
+      for (int rr = 0; rr < rows; ++rr) {
+        const double2* rowp = reinterpret_cast<const double2*>(st + (size_t)rr * ld);
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          if (!okc[c]) continue;
+          double2 a = rowp[tid + c * kPassConsumers];
+          if (!ok1[c]) a.y = 0.0;
+          acc[0][c].x = fmax(acc[0][c].x, fabs(a.x));
+          acc[0][c].y = fmax(acc[0][c].y, fabs(a.y));
+          acc[1][c].x = fma(a.x, a.x, acc[1][c].x);
+          acc[1][c].y = fma(a.y, a.y, acc[1][c].y);
+        }
+      }
+    } else {
+      for (int rb = 0; rb < rows; rb += RB) {
+        double2 a[RB][CPT];
+        double part[V];
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+          const bool rv = rb + rr < rows;
+          const double2* rowp = reinterpret_cast<const double2*>(st + (size_t)(rb + rr) * ld);
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) {
+            double2 v = make_double2(0.0, 0.0);
+            if (rv && okc[c]) {
+              v = rowp[tid + c * kPassConsumers];
+              if (!ok1[c]) v.y = 0.0;
+            }
+            a[rr][c] = v;
+          }
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) {
+            double d = 0.0;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+              d = fma(a[rr][c].x, qr[r][c].x, d);
+              d = fma(a[rr][c].y, qr[r][c].y, d);
+            }
+            part[rr * NRHS + r] = d;
+          }
+        }
+        warp_transpose_reduce<V>(part, lane);
+        if ((lane & (32 / V - 1)) == 0) red[warp * 16 + transpose_reduce_index<V>(lane)] = part[0];
+        named_bar_sync(1, kPassConsumers);
+        if (tid < V) {
+          double t = 0.0;
+#pragma unroll
+          for (int w = 0; w < kPassWarps; ++w) t += red[w * 16 + tid];
+          const int row = rb + tid / NRHS;
+          if (row >= rows) {
+            t = 0.0;
+          } else if (MODE == PASS_RESIDUAL) {
+            const double bi = b[rs + row];
+            t = bi - t;
+            sacc2 = fma(bi, t, sacc2);
+          }
+          sacc = fma(t, t, sacc);
+          tfin[tid] = t;
+        }
+        named_bar_sync(1, kPassConsumers);
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) {
+            const double t = tfin[rr * NRHS + r];
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+              acc[r][c].x = fma(t, a[rr][c].x, acc[r][c].x);
+              acc[r][c].y = fma(t, a[rr][c].y, acc[r][c].y);
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ---------------- write this CTA's partial
+  double* out = partials + (size_t)blockIdx.x * W;
+#pragma unroll
+  for (int r = 0; r < NRHS; ++r) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      if (!okc[c]) continue;
+      const int col = 2 * (tid + c * kPassConsumers);
+      out[(size_t)r * n + col] = acc[r][c].x;
+      if (ok1[c]) out[(size_t)r * n + col + 1] = acc[r][c].y;
+    }
+  }
+  if (MODE != PASS_COLSTATS) {
+    if (tid < 16) {
+      sred[tid] = tid < V ? sacc : 0.0;
+      sred[16 + tid] = tid < V ? sacc2 : 0.0;
+    }
+    named_bar_sync(1, kPassConsumers);
+    if (tid == 0) {
+      double s0 = 0.0, s1 = 0.0;
+      for (int i = 0; i < V; ++i) {
+        if (NRHS == 2) {
+          if (i % 2 == 0) s0 += sred[i]; else s1 += sred[i];
+        } else {
+          s0 += sred[i];
+          s1 += sred[16 + i];
+        }
+      }
+      out[(size_t)NRHS * n] = s0;
+      out[(size_t)NRHS * n + 1] = s1;
+    }
+  }
+}
+
+template <int NRHS, int MODE, int CPT>
+static int launch_pass_t(const DenseView& A, const double* q, const double* b, double* partials,
+                         int W, const int* active, cudaStream_t st, int G) {
+  auto kern = k_pass<NRHS, MODE, CPT>;
+  static bool attr = false;
+  if (!attr) {
+    TLS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem));
+    attr = true;
+  }
+  kern<<<G, kPassThreads, kPassSmem, st>>>(A.A, A.m, A.n, A.ld, rows_per_stage(A), q, b, partials, W,
+                                           active);
+  TLS_LAUNCH_CHECK();
+  return 0;
+}
+
+template <int NRHS, int MODE>
+static int launch_pass_cpt(const DenseView& A, const double* q, const double* b, double* partials,
+                           int W, const int* active, cudaStream_t st, int G) {
+  const int chunks = (A.n + 1) / 2;
+  if (chunks <= kPassConsumers) return launch_pass_t<NRHS, MODE, 1>(A, q, b, partials, W, active, st, G);
+  if (chunks <= 2 * kPassConsumers) return launch_pass_t<NRHS, MODE, 2>(A, q, b, partials, W, active, st, G);
+  if (chunks <= 4 * kPassConsumers) return launch_pass_t<NRHS, MODE, 4>(A, q, b, partials, W, active, st, G);
+  return launch_pass_t<NRHS, MODE, 8>(A, q, b, partials, W, active, st, G);
+}
+
+int launch_pass(const DenseView& A, int mode, int nrhs, const double* q, const double* b,
+                double* partials, const int* active, cudaStream_t st, int* grid_out) {
+  if (A.n > kMaxDenseN || (A.ld & 1) || A.ld < A.n) {
+    set_error("dense pass: need n <= %d and even ld >= n", kMaxDenseN);
+    return TLS_ERR_UNSUPPORTED;
+  }
+  const int G = pass_grid(A);
+  if (grid_out) *grid_out = G;
+  if (A.m == 0) return 0;
+  if (mode == PASS_COLSTATS)
+    return launch_pass_cpt<2, PASS_COLSTATS>(A, q, b, partials, 2 * A.n, active, st, G);
+  if (mode == PASS_RESIDUAL)
+    return launch_pass_cpt<1, PASS_RESIDUAL>(A, q, b, partials, A.n + 2, active, st, G);
+  if (nrhs == 1) return launch_pass_cpt<1, PASS_OPERATOR>(A, q, b, partials, A.n + 2, active, st, G);
+  return launch_pass_cpt<2, PASS_OPERATOR>(A, q, b, partials, 2 * A.n + 2, active, st, G);
+}
+
+// --------------------------------------------------------------------------- partial reduction
+__global__ void k_reduce_partials(const double* __restrict__ partials, int G, int W, int nmax,
+                                  double* __restrict__ out, const int* __restrict__ active) {
+  if (active != nullptr && *active == 0) return;
+  __shared__ double sm[8][33];
+  const int tx = threadIdx.x, grp = threadIdx.y;
+  const int w = blockIdx.x * 32 + tx;
+  const int g0 = G * grp / 8, g1 = G * (grp + 1) / 8;
+  const bool ismax = w < nmax;
+  double acc = 0.0;
+  if (w < W) {
+    for (int g = g0; g < g1; ++g) {
+      const double v = partials[(size_t)g * W + w];
+      acc = ismax ? fmax(acc, v) : acc + v;
+    }
+  }
+  sm[grp][tx] = acc;
+  __syncthreads();
+  if (grp == 0 && w < W) {
+    double r = sm[0][tx];
+    for (int k = 1; k < 8; ++k) r = ismax ? fmax(r, sm[k][tx]) : r + sm[k][tx];
+    out[w] = r;
+  }
+}
+
+int launch_reduce(const double* partials, int G, int W, int nmax, double* out, const int* active,
+                  cudaStream_t st) {
+  dim3 blk(32, 8);
+  k_reduce_partials<<<(W + 31) / 32, blk, 0, st>>>(partials, G, W, nmax, out, active);
+  TLS_LAUNCH_CHECK();
+  return 0;
+}
+
+// --------------------------------------------------------------------------- scaling D (R2)
+__global__ void k_scaling(const double* __restrict__ colmax, const double* __restrict__ sumsq, int n,
+                          double* __restrict__ d, double* __restrict__ dinv, double* __restrict__ normA2,
+                          int* __restrict__ flag) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const double cm = colmax[j];
+    if (!(cm > 0.0) || !isfinite(cm)) atomicExch(flag, 1);
+    int e = 0;
+    frexp(cm, &e);
+    d[j] = scalbn(1.0, e - 1);
+    dinv[j] = scalbn(1.0, 1 - e);
+    s += sumsq[j];
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *normA2 = s;
+}
+
+int launch_scaling(const double* colmax, const double* sumsq, int n, double* d, double* dinv,
+                   double* normA2, int* flag, cudaStream_t st) {
+  k_scaling<<<1, 1024, 0, st>>>(colmax, sumsq, n, d, dinv, normA2, flag);
+  TLS_LAUNCH_CHECK();
+  return 0;
+}
+
+__global__ void k_round(const double* __restrict__ x, double* __restrict__ y, int64_t n, int prec) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = round_uf(x[i], prec);
+}
+
+int launch_round(const double* x, double* y, int64_t n, int prec, cudaStream_t st) {
+  if (n == 0) return 0;
+  int64_t g = (n + 255) / 256;
+  if (g > 4096) g = 4096;
+  k_round<<<(int)g, 256, 0, st>>>(x, y, n, prec);
+  TLS_LAUNCH_CHECK();
+  return 0;
+}
+
+}  // namespace tls

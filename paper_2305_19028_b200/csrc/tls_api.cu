@@ -1,0 +1,879 @@
+// tls_api.cu — the C ABI of libtlsrqi.so (include/tlsrqi.h) and the host
+// runtime around the kernels: workspace carving, the NCCL shim, the
+// preconditioner build and the RQI-PCGTLS-MP host loop
+// (a4-a9).  The host loop is the only host<->device crossing of a solve: one
+// small D2H read after each residual evaluation and after each PCG batch;
+// inside PCGTLS all control (breakdown, early exit) is device-resident.
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <vector>
+
+#include "tls_common.cuh"
+#include "tls_kernels.h"
+
+// ------------------------------------------------------------------------------ errors
+namespace tls {
+static thread_local char g_err[1024] = "";
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+}  // namespace tls
+
+using namespace tls;
+
+#define TLS_TRY(expr)        \
+  do {                       \
+    int _rc = (expr);        \
+    if (_rc != 0) return _rc; \
+  } while (0)
+
+// ------------------------------------------------------------------------------ NCCL shim
+// Minimal declarations matching nccl.h (NCCL 2.x ABI); libnccl.so.2 is dlopen'ed so
+// the library loads (and single-GPU runs) without NCCL.
+namespace {
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+enum { ncclSuccess = 0 };
+enum { ncclSum = 0, ncclMax = 2 };
+enum { ncclFloat64 = 8, ncclInt32 = 2 };
+struct NcclApi {
+  int (*GetUniqueId)(ncclUniqueId*);
+  int (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  int (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t);
+  int (*CommDestroy)(ncclComm_t);
+  const char* (*GetErrorString)(int);
+  bool ok = false;
+};
+NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = (int (*)(ncclUniqueId*))dlsym(h, "ncclGetUniqueId");
+      api.CommInitRank = (int (*)(ncclComm_t*, int, ncclUniqueId, int))dlsym(h, "ncclCommInitRank");
+      api.AllReduce = (int (*)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclAllReduce");
+      api.CommDestroy = (int (*)(ncclComm_t))dlsym(h, "ncclCommDestroy");
+      api.GetErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+      api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy;
+    }
+  }
+  return api.ok ? &api : nullptr;
+}
+}  // namespace
+
+struct tls_comm_s {
+  ncclComm_t comm;
+  int nranks, rank, device;
+};
+
+struct tls_precond_s {
+  PrecondDev dev;
+  void* base;
+  int device;
+  double normA2_host;
+};
+
+static int allreduce(tls_comm_t comm, double* buf, size_t count, int op, cudaStream_t st) {
+  if (comm == nullptr || comm->nranks <= 1 || count == 0) return 0;
+  NcclApi* api = nccl_api();
+  const int r = api->AllReduce(buf, buf, count, ncclFloat64, op, comm->comm, st);
+  if (r != ncclSuccess) {
+    set_error("ncclAllReduce: %s", api->GetErrorString ? api->GetErrorString(r) : "error");
+    return TLS_ERR_NCCL;
+  }
+  return 0;
+}
+
+
+// ------------------------------------------------------------------------------ profiling
+namespace {
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  struct Pend { cudaEvent_t a, b; int cat; };
+  std::vector<Pend> pend;
+  double ms[TLS_PROF_NCAT] = {};
+  long long cnt[TLS_PROF_NCAT] = {};
+};
+Prof& prof() {
+  static Prof p;
+  return p;
+}
+cudaEvent_t ev_get() {
+  Prof& p = prof();
+  if (!p.pool.empty()) {
+    cudaEvent_t e = p.pool.back();
+    p.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+void prof_drain() {
+  Prof& p = prof();
+  for (auto& q : p.pend) {
+    float ms = 0.f;
+    cudaEventSynchronize(q.b);
+    if (cudaEventElapsedTime(&ms, q.a, q.b) == cudaSuccess) {
+      p.ms[q.cat] += ms;
+      p.cnt[q.cat] += 1;
+    }
+    p.pool.push_back(q.a);
+    p.pool.push_back(q.b);
+  }
+  p.pend.clear();
+}
+struct ProfScope {
+  int cat;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(int c, cudaStream_t s) : cat(c), st(s) {
+    if (prof().on) {
+      a = ev_get();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = ev_get();
+      cudaEventRecord(b, st);
+      prof().pend.push_back({a, b, cat});
+      if (prof().pend.size() > 4096) prof_drain();
+    }
+  }
+};
+}  // namespace
+
+// ------------------------------------------------------------------------------ workspace
+namespace {
+struct Carver {
+  char* p;
+  size_t left;
+  bool ok = true;
+  template <typename T>
+  T* take(size_t count) {
+    const size_t bytes = (count * sizeof(T) + 255) & ~(size_t)255;
+    if (bytes > left) {
+      ok = false;
+      return nullptr;
+    }
+    T* r = reinterpret_cast<T*>(p);
+    p += bytes;
+    left -= bytes;
+    return r;
+  }
+};
+
+struct Work {
+  double* partials;
+  double* passout;
+  double* colstats;
+  PcgVecs vec;
+  double* x;
+  double* x_prev;
+  double* x0;
+  double* zero;
+  PcgState* S;
+  int* flags;    // [0] scaling, [1] range, [2] pivot
+  double* G;
+  double* gram_ws;
+  size_t gram_ws_doubles;
+  double* d_tmp;
+};
+
+bool carve(const tls_matrix_t* A, void* ws, size_t bytes, Work& w, bool factor) {
+  const int n = (int)A->n;
+  DenseView dv{A->vals, A->m_local, n, A->ld};
+  Carver c{static_cast<char*>(ws), ws ? bytes : 0};
+  w.partials = c.take<double>(pass_partials_doubles(dv));
+  w.passout = c.take<double>(2 * (size_t)n + 2);
+  w.colstats = c.take<double>(2 * (size_t)n);
+  w.vec.omega = c.take<double>(2 * (size_t)n);
+  w.vec.s = c.take<double>(2 * (size_t)n);
+  w.vec.p = c.take<double>(2 * (size_t)n);
+  w.vec.q = c.take<double>(2 * (size_t)n);
+  w.vec.rhs = c.take<double>(2 * (size_t)n);
+  w.x = c.take<double>(n);
+  w.x_prev = c.take<double>(n);
+  w.x0 = c.take<double>(n);
+  w.zero = c.take<double>(n);
+  w.S = c.take<PcgState>(1);
+  w.flags = c.take<int>(8);
+  w.d_tmp = c.take<double>(2 * (size_t)n + 2);
+  if (factor) {
+    w.G = c.take<double>((size_t)n * n);
+    // K_t only changes the number of chunks; K_t = 1 gives the largest split count
+    w.gram_ws_doubles = gram_ws_doubles(dv, 1);
+    w.gram_ws = c.take<double>(w.gram_ws_doubles);
+  } else {
+    w.G = nullptr;
+    w.gram_ws = nullptr;
+    w.gram_ws_doubles = 0;
+  }
+  return c.ok;
+}
+
+size_t ws_need(const tls_matrix_t* A, bool factor) {
+  const int n = (int)A->n;
+  DenseView dv{A->vals, A->m_local, n, A->ld};
+  size_t tot = 0;
+  auto add = [&](size_t bytes) { tot += (bytes + 255) & ~(size_t)255; };
+  add(pass_partials_doubles(dv) * 8);
+  add((2 * (size_t)n + 2) * 8);
+  add(2 * (size_t)n * 8);
+  for (int i = 0; i < 5; ++i) add(2 * (size_t)n * 8);
+  for (int i = 0; i < 4; ++i) add((size_t)n * 8);
+  add(sizeof(PcgState));
+  add(8 * sizeof(int));
+  add((2 * (size_t)n + 2) * 8);
+  if (factor) {
+    add((size_t)n * n * 8);
+    add(gram_ws_doubles(dv, 1) * 8);
+  }
+  return tot;
+}
+
+int check_matrix(const tls_matrix_t* A) {
+  if (!A) { set_error("A is NULL"); return TLS_ERR_ARG; }
+  if (A->layout != TLS_DENSE_ROWMAJOR) { set_error("CSR layout not supported by this build"); return TLS_ERR_UNSUPPORTED; }
+  if (A->n < 1 || A->m_local < 0 || A->m_global < A->n + 1 || A->ld < A->n || (A->ld & 1)) {
+    set_error("bad shape: need n >= 1, m_global >= n+1, ld >= n, ld even");
+    return TLS_ERR_ARG;
+  }
+  if (A->n > kMaxDenseN) { set_error("n > %d unsupported", kMaxDenseN); return TLS_ERR_UNSUPPORTED; }
+  if (A->m_local > 0 && (A->vals == nullptr || (reinterpret_cast<uintptr_t>(A->vals) & 15))) {
+    set_error("A->vals must be a 16-byte aligned device pointer");
+    return TLS_ERR_ARG;
+  }
+  return 0;
+}
+
+__global__ void k_recip(const double* __restrict__ d, double* __restrict__ dinv, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dinv[i] = 1.0 / d[i];
+}
+
+__global__ void k_copy(const double* __restrict__ a, double* __restrict__ b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
+}
+
+struct Ctx {
+  cudaStream_t st;
+  tls_comm_t comm;
+  int launches = 0;
+  int64_t passes = 0;
+};
+
+// one pass over A (+ fixed-order reduction + all-reduce over ranks) into w.passout
+int run_pass(Ctx& cx, const DenseView& dv, int mode, int nrhs, const double* q, const double* b, Work& w,
+             const int* active) {
+  int G = 1;
+  {
+    const int cat = mode == PASS_COLSTATS ? TLS_PROF_COLSTATS
+                    : mode == PASS_RESIDUAL ? TLS_PROF_PASS_RESID
+                    : (nrhs == 2 ? TLS_PROF_PASS_OP2 : TLS_PROF_PASS_OP1);
+    ProfScope ps(cat, cx.st);
+    TLS_TRY(launch_pass(dv, mode, nrhs, q, b, w.partials, active, cx.st, &G));
+  }
+  const int W = (mode == PASS_COLSTATS) ? 2 * dv.n : nrhs * dv.n + 2;
+  double* out = (mode == PASS_COLSTATS) ? w.colstats : w.passout;
+  if (dv.m > 0) {
+    ProfScope ps(TLS_PROF_REDUCE, cx.st);
+    TLS_TRY(launch_reduce(w.partials, G, W, mode == PASS_COLSTATS ? dv.n : 0, out, active, cx.st));
+    cx.launches += 2;
+  } else {
+    TLS_CUDA_TRY(cudaMemsetAsync(out, 0, (size_t)W * 8, cx.st));
+  }
+  cx.passes += 1;
+  if (mode == PASS_COLSTATS) {
+    TLS_TRY(allreduce(cx.comm, out, dv.n, ncclMax, cx.st));
+    TLS_TRY(allreduce(cx.comm, out + dv.n, dv.n, ncclSum, cx.st));
+  } else {
+    TLS_TRY(allreduce(cx.comm, out, W, ncclSum, cx.st));
+  }
+  return 0;
+}
+
+void fill_info_defaults(tls_info_t* info) {
+  if (!info) return;
+  info->status = 0;
+  info->termination = TLS_TERM_NONE;
+  info->rqi_iters = 0;
+  info->boot_iters = 0;
+  info->breakdown_k = info->breakdown_rhs = info->breakdown_j = -1;
+  info->chol_pivot = 0;
+  info->sigma2 = NAN;
+  info->passes = 0;
+  info->launches = 0;
+  info->pcg_steps = 0;
+}
+
+int alloc_precond(int n, int u_f, tls_precond_t* out) {
+  tls_precond_s* h = new tls_precond_s();
+  const int npad = (n + 31) / 32 * 32;
+  const size_t es = (u_f == TLS_FP64) ? 8 : (u_f == TLS_FP32 ? 4 : 2);
+  const size_t bytes = precond_bytes(n, u_f);
+  cudaError_t e = cudaMalloc(&h->base, bytes);
+  if (e != cudaSuccess) {
+    delete h;
+    set_error("cudaMalloc(precond %zu B): %s", bytes, cudaGetErrorString(e));
+    return TLS_ERR_CUDA;
+  }
+  cudaGetDevice(&h->device);
+  char* p = static_cast<char*>(h->base);
+  PrecondDev& d = h->dev;
+  d.n = n;
+  d.npad = npad;
+  d.u_f = u_f;
+  d.Rrow = p; p += (size_t)npad * npad * es;
+  d.RTrow = p; p += (size_t)npad * npad * es;
+  d.DinvB = reinterpret_cast<double*>(p); p += (size_t)npad * 32 * 8;
+  d.DinvF = reinterpret_cast<double*>(p); p += (size_t)npad * 32 * 8;
+  d.d = reinterpret_cast<double*>(p); p += (size_t)npad * 8;
+  d.dinv = reinterpret_cast<double*>(p); p += (size_t)npad * 8;
+  d.normA2 = reinterpret_cast<double*>(p);
+  *out = h;
+  return 0;
+}
+
+__global__ void k_fill_scaling(double* __restrict__ d, double* __restrict__ dinv, const double* __restrict__ src_d,
+                               const double* __restrict__ src_dinv, int n, int npad) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npad; i += gridDim.x * blockDim.x) {
+    d[i] = i < n ? src_d[i] : 1.0;
+    dinv[i] = i < n ? src_dinv[i] : 1.0;
+  }
+}
+}  // namespace
+
+// ------------------------------------------------------------------------------ C ABI
+extern "C" {
+
+int tls_abi_version(void) { return TLSRQI_ABI_VERSION; }
+
+int tls_profile_enable(int on) {
+  prof_drain();
+  Prof& p = prof();
+  p.on = on != 0;
+  for (int i = 0; i < TLS_PROF_NCAT; ++i) { p.ms[i] = 0.0; p.cnt[i] = 0; }
+  return 0;
+}
+
+int tls_profile_read(double* ms, int64_t* count, int ncat) {
+  prof_drain();
+  Prof& p = prof();
+  for (int i = 0; i < ncat && i < TLS_PROF_NCAT; ++i) {
+    if (ms) ms[i] = p.ms[i];
+    if (count) count[i] = p.cnt[i];
+  }
+  return 0;
+}
+
+void tls_rqi_opts_default(tls_rqi_opts_t* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->budget_rule = 0;
+  o->stop_rule = 0;
+  o->max_outer = 50;
+  o->polish = 1;
+  o->tol_inner = -1.0;
+  o->boot = 0;
+  o->boot_max = 200;
+  o->boot_tol = 1e-8;
+  o->op_variant = 0;
+  o->breakdown_rule = 0;
+  o->gram_chunk = 2048;
+}
+
+const char* tls_status_string(int s) {
+  switch (s) {
+    case TLS_OK: return "OK";
+    case TLS_CHOL_BREAKDOWN: return "CHOL_BREAKDOWN";
+    case TLS_PCG_BREAKDOWN: return "PCG_BREAKDOWN";
+    case TLS_MAX_OUTER: return "MAX_OUTER";
+    case TLS_NONFINITE: return "NONFINITE";
+    case TLS_RANGE: return "RANGE";
+    case TLS_NOT_MINIMAL: return "NOT_MINIMAL";
+    case TLS_STAGNATED: return "STAGNATED";
+    case TLS_ERR_ARG: return "ERR_ARG";
+    case TLS_ERR_CUDA: return "ERR_CUDA";
+    case TLS_ERR_NCCL: return "ERR_NCCL";
+    case TLS_ERR_WORKSPACE: return "ERR_WORKSPACE";
+    case TLS_ERR_UNSUPPORTED: return "ERR_UNSUPPORTED";
+    default: return "UNKNOWN";
+  }
+}
+
+const char* tls_last_error(void) { return g_err; }
+
+int tls_comm_get_unique_id(void* id_out) {
+  NcclApi* api = nccl_api();
+  if (!api) { set_error("libnccl.so.2 not loadable"); return TLS_ERR_NCCL; }
+  ncclUniqueId id;
+  const int r = api->GetUniqueId(&id);
+  if (r != ncclSuccess) { set_error("ncclGetUniqueId failed: %d", r); return TLS_ERR_NCCL; }
+  std::memcpy(id_out, &id, sizeof(id));
+  return 0;
+}
+
+int tls_comm_init(int nranks, int rank, const void* id_host, int device, tls_comm_t* out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks) { set_error("bad comm args"); return TLS_ERR_ARG; }
+  TLS_CUDA_TRY(cudaSetDevice(device));
+  tls_comm_s* c = new tls_comm_s{nullptr, nranks, rank, device};
+  if (nranks > 1) {
+    NcclApi* api = nccl_api();
+    if (!api) { delete c; set_error("libnccl.so.2 not loadable"); return TLS_ERR_NCCL; }
+    ncclUniqueId id;
+    std::memcpy(&id, id_host, sizeof(id));
+    const int r = api->CommInitRank(&c->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      set_error("ncclCommInitRank: %s", api->GetErrorString ? api->GetErrorString(r) : "error");
+      return TLS_ERR_NCCL;
+    }
+  }
+  *out = c;
+  return 0;
+}
+
+int tls_comm_destroy(tls_comm_t c) {
+  if (!c) return 0;
+  if (c->comm) {
+    NcclApi* api = nccl_api();
+    if (api) api->CommDestroy(c->comm);
+  }
+  delete c;
+  return 0;
+}
+
+size_t tls_workspace_size(const tls_matrix_t* A, int32_t /*max_outer*/) {
+  if (check_matrix(A) != 0) return 0;
+  return ws_need(A, true);
+}
+
+int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t* opts, tls_comm_t comm,
+                       void* stream, void* ws, size_t ws_bytes, tls_precond_t* R_out, tls_info_t* info) {
+  fill_info_defaults(info);
+  if (R_out) *R_out = nullptr;
+  TLS_TRY(check_matrix(A));
+  if (!R_out || u_f < TLS_FP16 || u_f > TLS_FP64) { set_error("bad u_f or R_out"); return TLS_ERR_ARG; }
+  tls_rqi_opts_t o;
+  if (opts) o = *opts; else tls_rqi_opts_default(&o);
+  const int K_t = o.gram_chunk > 0 ? o.gram_chunk : 2048;
+  Work w;
+  if (!carve(A, ws, ws_bytes, w, true)) { set_error("workspace too small (need %zu)", ws_need(A, true)); return TLS_ERR_WORKSPACE; }
+  Ctx cx{static_cast<cudaStream_t>(stream), comm};
+  const int n = (int)A->n;
+  DenseView dv{A->vals, A->m_local, n, A->ld};
+  TLS_CUDA_TRY(cudaMemsetAsync(w.flags, 0, 8 * sizeof(int), cx.st));
+  // a1: column max / sums of squares, all-reduced; D = powers of two (R2)
+  TLS_TRY(run_pass(cx, dv, PASS_COLSTATS, 2, nullptr, nullptr, w, nullptr));
+  double* d = w.d_tmp;
+  double* dinv = w.d_tmp + n;
+  double* normA2 = w.d_tmp + 2 * n;
+  TLS_TRY(launch_scaling(w.colstats, w.colstats + n, n, d, dinv, normA2, &w.flags[0], cx.st));
+  cx.launches += 1;
+  // a2: u_f Gram, all-reduced
+  if (dv.m > 0) {
+    ProfScope ps(TLS_PROF_GRAM, cx.st);
+    TLS_TRY(launch_gram(dv, u_f, dinv, K_t, w.G, w.gram_ws, w.gram_ws_doubles, &w.flags[1], cx.st, &cx.launches));
+  } else {
+    TLS_CUDA_TRY(cudaMemsetAsync(w.G, 0, (size_t)n * n * 8, cx.st));
+  }
+  cx.passes += 1;
+  TLS_TRY(allreduce(comm, w.G, (size_t)n * n, ncclSum, cx.st));
+  // a3: Cholesky (replicated on every rank: identical bits)
+  {
+    ProfScope ps(TLS_PROF_CHOL, cx.st);
+    TLS_TRY(launch_cholesky(w.G, n, &w.flags[2], cx.st, &cx.launches));
+  }
+  int hflags[8];
+  double hnorm = 0.0;
+  TLS_CUDA_TRY(cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, cx.st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(&hnorm, normA2, sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+  TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+  if (info) { info->passes = cx.passes; info->launches = cx.launches; }
+  if (hflags[0]) { set_error("A has a zero or non-finite column (rank deficient)"); return TLS_ERR_ARG; }
+  if (hflags[1]) { if (info) info->status = TLS_RANGE; return TLS_RANGE; }
+  if (hflags[2]) {
+    if (info) { info->status = TLS_CHOL_BREAKDOWN; info->chol_pivot = hflags[2]; }
+    return TLS_CHOL_BREAKDOWN;
+  }
+  tls_precond_t h = nullptr;
+  TLS_TRY(alloc_precond(n, u_f, &h));
+  h->normA2_host = hnorm;
+  k_fill_scaling<<<(h->dev.npad + 255) / 256, 256, 0, cx.st>>>(h->dev.d, h->dev.dinv, d, dinv, n, h->dev.npad);
+  TLS_CUDA_TRY(cudaMemcpyAsync(h->dev.normA2, normA2, sizeof(double), cudaMemcpyDeviceToDevice, cx.st));
+  int rc = launch_pack_R(w.G, n, h->dev, &w.flags[1], cx.st, &cx.launches);
+  cx.launches += 1;  // k_fill_scaling
+  if (rc) { tls_precond_destroy(h); return rc; }
+  TLS_CUDA_TRY(cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, cx.st));
+  TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+  if (info) { info->passes = cx.passes; info->launches = cx.launches; }
+  if (hflags[1]) {
+    tls_precond_destroy(h);
+    if (info) info->status = TLS_RANGE;
+    return TLS_RANGE;
+  }
+  *R_out = h;
+  return 0;
+}
+
+int tls_precond_import(int64_t n, int32_t u_f, const double* Rt_host, const double* d_host, double normA2,
+                       void* stream, tls_precond_t* out) {
+  if (!out || n < 1 || n > kMaxDenseN || !Rt_host || !d_host || u_f < TLS_FP16 || u_f > TLS_FP64) {
+    set_error("bad import args");
+    return TLS_ERR_ARG;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  tls_precond_t h = nullptr;
+  TLS_TRY(alloc_precond((int)n, u_f, &h));
+  h->normA2_host = normA2;
+  double* tmp = nullptr;
+  int* flag = nullptr;
+  TLS_CUDA_TRY(cudaMalloc(&tmp, (size_t)n * n * 8 + 4 * (size_t)n * 8 + 256));
+  flag = reinterpret_cast<int*>(tmp + (size_t)n * n + 4 * n);
+  std::vector<double> dinv(n);
+  for (int64_t i = 0; i < n; ++i) dinv[i] = 1.0 / d_host[i];
+  TLS_CUDA_TRY(cudaMemcpyAsync(tmp, Rt_host, (size_t)n * n * 8, cudaMemcpyHostToDevice, st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(tmp + (size_t)n * n, d_host, n * 8, cudaMemcpyHostToDevice, st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(tmp + (size_t)n * n + n, dinv.data(), n * 8, cudaMemcpyHostToDevice, st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(h->dev.normA2, &normA2, 8, cudaMemcpyHostToDevice, st));
+  TLS_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  k_fill_scaling<<<(h->dev.npad + 255) / 256, 256, 0, st>>>(h->dev.d, h->dev.dinv, tmp + (size_t)n * n,
+                                                           tmp + (size_t)n * n + n, (int)n, h->dev.npad);
+  int rc = launch_pack_R(tmp, (int)n, h->dev, flag, st, nullptr);
+  int hflag = 0;
+  TLS_CUDA_TRY(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TLS_CUDA_TRY(cudaStreamSynchronize(st));
+  cudaFree(tmp);
+  if (rc || hflag) {
+    tls_precond_destroy(h);
+    if (!rc) { set_error("imported R~ not representable in u_f or singular"); rc = TLS_RANGE; }
+    return rc;
+  }
+  *out = h;
+  return 0;
+}
+
+static double host_dec(const void* base, size_t idx, int u_f) {
+  if (u_f == TLS_FP64) return static_cast<const double*>(base)[idx];
+  if (u_f == TLS_FP32) return static_cast<const float*>(base)[idx];
+  const uint16_t h = static_cast<const uint16_t*>(base)[idx];
+  if (u_f == TLS_BF16) {
+    uint32_t u = (uint32_t)h << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+  }
+  const int s = h >> 15, e = (h >> 10) & 0x1f, m = h & 0x3ff;
+  double v;
+  if (e == 0) v = std::ldexp((double)m, -24);
+  else if (e == 31) v = m ? NAN : INFINITY;
+  else v = std::ldexp((double)(m | 0x400), e - 25);
+  return s ? -v : v;
+}
+
+int tls_precond_export(tls_precond_t R, double* Rt_host, double* d_host, double* normA2_host) {
+  if (!R) { set_error("NULL handle"); return TLS_ERR_ARG; }
+  const int n = R->dev.n, npad = R->dev.npad, u_f = R->dev.u_f;
+  const size_t es = (u_f == TLS_FP64) ? 8 : (u_f == TLS_FP32 ? 4 : 2);
+  if (Rt_host) {
+    std::vector<char> raw((size_t)npad * npad * es);
+    TLS_CUDA_TRY(cudaMemcpy(raw.data(), R->dev.Rrow, raw.size(), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) Rt_host[(size_t)i * n + j] = host_dec(raw.data(), (size_t)i * npad + j, u_f);
+  }
+  if (d_host) TLS_CUDA_TRY(cudaMemcpy(d_host, R->dev.d, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  if (normA2_host) *normA2_host = R->normA2_host;
+  return 0;
+}
+
+void tls_precond_destroy(tls_precond_t R) {
+  if (!R) return;
+  if (R->base) cudaFree(R->base);
+  delete R;
+}
+
+// ------------------------------------------------------------------------------ RQI-PCGTLS-MP
+int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R, int32_t u, int32_t u_r, double tol,
+                   const tls_rqi_opts_t* opts, tls_comm_t comm, void* stream, void* ws, size_t ws_bytes, double* x_out,
+                   double* sigma_out, tls_info_t* info) {
+  fill_info_defaults(info);
+  TLS_TRY(check_matrix(A));
+  if (u != TLS_FP64 || u_r != TLS_FP64) { set_error("u and u_r must be TLS_FP64 in this build"); return TLS_ERR_UNSUPPORTED; }
+  if (!R || R->dev.n != A->n || !x_out || (A->m_local > 0 && !b)) { set_error("bad rqi args"); return TLS_ERR_ARG; }
+  tls_rqi_opts_t o;
+  if (opts) o = *opts; else tls_rqi_opts_default(&o);
+  if (o.op_variant != 0) { set_error("op_variant 1 (paper A-free PCGTLS) not in this build"); return TLS_ERR_UNSUPPORTED; }
+  if (o.max_outer < 1) o.max_outer = 1;
+  Work w;
+  if (!carve(A, ws, ws_bytes, w, false)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
+  Ctx cx{static_cast<cudaStream_t>(stream), comm};
+  const int n = (int)A->n;
+  const PrecondDev& pc = R->dev;
+  DenseView dv{A->vals, A->m_local, n, A->ld};
+  const double tol_in = o.tol_inner > 0 ? o.tol_inner : tol;
+  PcgState hS;
+
+  auto set_state_scalars = [&](double sigma2, double tol2) -> int {
+    // host -> device: sigma^2 for PCG and the early-exit threshold (small pageable copies)
+    static thread_local double buf[2];
+    buf[0] = sigma2;
+    buf[1] = tol2;
+    TLS_CUDA_TRY(cudaMemcpyAsync(&w.S->sigma2, &buf[0], 8, cudaMemcpyHostToDevice, cx.st));
+    TLS_CUDA_TRY(cudaMemcpyAsync(&w.S->tol2, &buf[1], 8, cudaMemcpyHostToDevice, cx.st));
+    TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+    return 0;
+  };
+  auto read_state = [&]() -> int {
+    TLS_CUDA_TRY(cudaMemcpyAsync(&hS, w.S, sizeof(PcgState), cudaMemcpyDeviceToHost, cx.st));
+    TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+    return 0;
+  };
+  // PCG iterations j = 0..budget-1 with device-side predication; with a large
+  // budget the host polls any_active every 8 iterations.
+  auto pcg_loop = [&](int nrhs, int budget) -> int {
+    for (int j = 0; j < budget; ++j) {
+      TLS_TRY(run_pass(cx, dv, PASS_OPERATOR, nrhs, w.vec.q, nullptr, w, &w.S->any_active));
+      {
+        ProfScope ps(TLS_PROF_PCG_STEP, cx.st);
+        TLS_TRY(launch_pcg_step(pc, w.vec, w.passout, w.S, o.breakdown_rule, j + 1 < budget ? 1 : 0, cx.st));
+      }
+      cx.launches += 1;
+      if (budget > 16 && (j % 8) == 7) {
+        int act = 0;
+        TLS_CUDA_TRY(cudaMemcpyAsync(&act, &w.S->any_active, sizeof(int), cudaMemcpyDeviceToHost, cx.st));
+        TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+        if (!act) break;
+      }
+    }
+    return 0;
+  };
+
+  TLS_CUDA_TRY(cudaMemsetAsync(w.zero, 0, (size_t)n * 8, cx.st));
+  TLS_CUDA_TRY(cudaMemsetAsync(w.vec.rhs, 0, 2 * (size_t)n * 8, cx.st));
+  // setup (a1): h = A^T b, b^T b from the residual pass at x = 0
+  TLS_TRY(run_pass(cx, dv, PASS_RESIDUAL, 1, w.zero, b, w, nullptr));
+  double bb = 0.0;
+  TLS_CUDA_TRY(cudaMemcpyAsync(&bb, w.passout + n, 8, cudaMemcpyDeviceToHost, cx.st));
+  k_copy<<<(n + 255) / 256, 256, 0, cx.st>>>(w.passout, w.vec.rhs, n);
+  cx.launches += 1;
+  // a4: bootstrap x_0 = x_LS (R5)
+  int boot_iters = 0;
+  if (o.boot == 0) {
+    TLS_TRY(set_state_scalars(0.0, o.boot_tol * o.boot_tol));
+    {
+      ProfScope ps(TLS_PROF_PCG_INIT, cx.st);
+      TLS_TRY(launch_pcg_init(pc, 1, w.vec, w.S, cx.st));
+    }
+    cx.launches += 1;
+    TLS_TRY(pcg_loop(1, o.boot_max));
+    TLS_TRY(read_state());
+    boot_iters = hS.count[0];
+    k_copy<<<(n + 255) / 256, 256, 0, cx.st>>>(w.vec.omega, w.x0, n);
+  } else {
+    k_copy<<<(n + 255) / 256, 256, 0, cx.st>>>(w.vec.rhs, w.x0, n);
+    TLS_TRY(launch_precond_apply(pc, 1, 1, w.x0, n, cx.st));
+    TLS_TRY(launch_precond_apply(pc, 0, 1, w.x0, n, cx.st));
+    cx.launches += 2;
+  }
+  cx.launches += 1;
+  TLS_TRY(run_pass(cx, dv, PASS_RESIDUAL, 1, w.x0, b, w, nullptr));     // r_0 (l.227)
+  TLS_TRY(launch_boot_x1(pc, w.passout, w.x0, w.x, cx.st));              // l.229-235
+  cx.launches += 1;
+  TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+  const double normAb2 = R->normA2_host + bb;
+
+  std::vector<double> s2tr, psitr;
+  std::vector<int> pcgc;
+  int status = TLS_OK, term = TLS_TERM_NONE, k = 1, crossed = 0, use_prev = 0;
+  double psi_prev = 0.0, sig2_prev = NAN, sig2_ret = NAN;
+  int bk = -1, brhs = -1, bj = -1;
+  for (;; ++k) {
+    // a5: residual pass, sigma_k^2, f_k, g_k, psi_k (l.238-245, l.262)
+    TLS_TRY(run_pass(cx, dv, PASS_RESIDUAL, 1, w.x, b, w, nullptr));
+    TLS_TRY(launch_rqi_eval(pc, w.passout, w.x, w.vec, w.S, cx.st));
+    cx.launches += 1;
+    TLS_TRY(read_state());
+    const double sig2 = hS.sigma2, psi = hS.psi;
+    s2tr.push_back(sig2);
+    psitr.push_back(psi);
+    if (!std::isfinite(sig2) || !std::isfinite(psi)) { status = TLS_NONFINITE; term = TLS_TERM_NONFINITE; sig2_ret = sig2; break; }
+    const bool increased = k >= 2 && (psi > psi_prev || (o.stop_rule == 1 && psi >= psi_prev));
+    if (!crossed && psi <= tol * normAb2) crossed = k;
+    if (crossed && k == crossed + o.polish) {                     // (ii) R6
+      if (increased) { use_prev = 1; sig2_ret = sig2_prev; } else { sig2_ret = sig2; }
+      term = TLS_TERM_CONVERGED_TOL;
+      break;
+    }
+    if (increased) {                                              // (i) l.265, R7
+      use_prev = 1;
+      sig2_ret = sig2_prev;
+      if (crossed) term = TLS_TERM_PSI_INCREASE_CONVERGED;
+      else { status = TLS_STAGNATED; term = TLS_TERM_STAGNATED; }
+      break;
+    }
+    if (k > o.max_outer) { status = TLS_MAX_OUTER; term = TLS_TERM_MAX_OUTER; sig2_ret = sig2; break; }
+    // a6-a8: the two PCGTLS solves, batched (l.246, l.252)
+    const int budget = o.budget_rule == 0 ? k + 1 : 400;
+    TLS_TRY(set_state_scalars(sig2, tol_in * tol_in));
+    {
+      ProfScope ps(TLS_PROF_PCG_INIT, cx.st);
+      TLS_TRY(launch_pcg_init(pc, 2, w.vec, w.S, cx.st));
+    }
+    cx.launches += 1;
+    TLS_TRY(pcg_loop(2, budget));
+    TLS_TRY(read_state());
+    pcgc.push_back(hS.count[0]);
+    pcgc.push_back(hS.count[1]);
+    if (hS.brk[0] || hS.brk[1]) {                                  // R3, R18
+      status = TLS_PCG_BREAKDOWN;
+      term = TLS_TERM_BREAKDOWN;
+      bk = k;
+      brhs = hS.brk[0] ? 0 : 1;
+      bj = hS.brk_j[brhs];
+      sig2_ret = sig2;
+      break;
+    }
+    // a9: z, beta_k, x_{k+1} (l.248-255)
+    TLS_TRY(launch_rqi_update(pc, w.vec, w.S, w.x, w.x_prev, cx.st));
+    cx.launches += 1;
+    psi_prev = psi;
+    sig2_prev = sig2;
+  }
+  k_copy<<<(n + 255) / 256, 256, 0, cx.st>>>(use_prev ? w.x_prev : w.x, x_out, n);
+  cx.launches += 1;
+  TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+  TLS_LAUNCH_CHECK();
+  if (sigma_out) *sigma_out = std::sqrt(sig2_ret);
+  if (info) {
+    info->status = status;
+    info->termination = term;
+    info->rqi_iters = k;
+    info->boot_iters = boot_iters;
+    info->breakdown_k = bk;
+    info->breakdown_rhs = brhs;
+    info->breakdown_j = bj;
+    info->sigma2 = sig2_ret;
+    info->passes = cx.passes;
+    info->launches = cx.launches;
+    info->pcg_steps = (int32_t)(pcgc.size() / 2);
+    if (info->pcg_iters)
+      for (size_t i = 0; i < pcgc.size() && i < 2 * (size_t)o.max_outer; ++i) info->pcg_iters[i] = pcgc[i];
+    if (info->sigma2_trace)
+      for (size_t i = 0; i < s2tr.size() && i < (size_t)o.max_outer + 1; ++i) info->sigma2_trace[i] = s2tr[i];
+    if (info->psi_trace)
+      for (size_t i = 0; i < psitr.size() && i < (size_t)o.max_outer + 1; ++i) info->psi_trace[i] = psitr[i];
+  }
+  return status;
+}
+
+// ------------------------------------------------------------------------------ host-buffer e2e
+size_t tls_solve_host_bytes(int64_t m, int64_t n, int64_t ld, int32_t max_outer) {
+  tls_matrix_t A{TLS_DENSE_ROWMAJOR, 0, m, n, m + n + 1, 0, ld, reinterpret_cast<const double*>(256), nullptr, nullptr, 0};
+  const size_t a = ((size_t)m * ld * 8 + 255) & ~(size_t)255;
+  const size_t bv = ((size_t)m * 8 + 255) & ~(size_t)255;
+  const size_t xv = ((size_t)n * 8 + 255) & ~(size_t)255;
+  return a + bv + xv + tls_workspace_size(&A, max_outer);
+}
+
+int tls_solve_host(const double* A_host, const double* b_host, int64_t m, int64_t n, int64_t ld, int64_t m_global,
+                   int64_t row_offset, int32_t u_f, double tol, const tls_rqi_opts_t* opts, tls_comm_t comm, void* stream,
+                   void* dev_buf, size_t dev_bytes, double* x_host, double* sigma_out, tls_info_t* info) {
+  const size_t need = tls_solve_host_bytes(m, n, ld, opts ? opts->max_outer : 50);
+  if (!dev_buf || dev_bytes < need) { set_error("device buffer too small (need %zu)", need); return TLS_ERR_WORKSPACE; }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* p = static_cast<char*>(dev_buf);
+  double* Ad = reinterpret_cast<double*>(p); p += ((size_t)m * ld * 8 + 255) & ~(size_t)255;
+  double* bd = reinterpret_cast<double*>(p); p += ((size_t)m * 8 + 255) & ~(size_t)255;
+  double* xd = reinterpret_cast<double*>(p); p += ((size_t)n * 8 + 255) & ~(size_t)255;
+  const size_t wsb = dev_bytes - (size_t)(p - static_cast<char*>(dev_buf));
+  TLS_CUDA_TRY(cudaMemcpyAsync(Ad, A_host, (size_t)m * ld * 8, cudaMemcpyHostToDevice, st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(bd, b_host, (size_t)m * 8, cudaMemcpyHostToDevice, st));
+  tls_matrix_t A{TLS_DENSE_ROWMAJOR, 0, m, n, m_global, row_offset, ld, Ad, nullptr, nullptr, 0};
+  tls_precond_t R = nullptr;
+  tls_info_t finfo;
+  int rc = tls_factor_precond(&A, u_f, opts, comm, stream, p, wsb, &R, &finfo);
+  if (rc != 0) {
+    if (info) { int32_t* pi = info->pcg_iters; double* s2 = info->sigma2_trace; double* ps = info->psi_trace;
+      *info = finfo; info->pcg_iters = pi; info->sigma2_trace = s2; info->psi_trace = ps; }
+    return rc;
+  }
+  rc = tls_rqi_pcgtls(&A, bd, R, TLS_FP64, TLS_FP64, tol, opts, comm, stream, p, wsb, xd, sigma_out, info);
+  if (info) { info->passes += finfo.passes; info->launches += finfo.launches; }
+  tls_precond_destroy(R);
+  if (rc < 0) return rc;
+  TLS_CUDA_TRY(cudaMemcpyAsync(x_host, xd, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+  TLS_CUDA_TRY(cudaStreamSynchronize(st));
+  return rc;
+}
+
+// ------------------------------------------------------------------------------ single steps
+int tls_colstats(const tls_matrix_t* A, double* colmax, double* sumsq, void* stream, void* ws, size_t ws_bytes) {
+  TLS_TRY(check_matrix(A));
+  Work w;
+  if (!carve(A, ws, ws_bytes, w, false)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
+  Ctx cx{static_cast<cudaStream_t>(stream), nullptr};
+  const int n = (int)A->n;
+  DenseView dv{A->vals, A->m_local, n, A->ld};
+  TLS_CUDA_TRY(cudaMemsetAsync(w.flags, 0, 8 * sizeof(int), cx.st));
+  TLS_TRY(run_pass(cx, dv, PASS_COLSTATS, 2, nullptr, nullptr, w, nullptr));
+  TLS_TRY(launch_scaling(w.colstats, w.colstats + n, n, w.d_tmp, w.d_tmp + n, w.d_tmp + 2 * n, &w.flags[0], cx.st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(colmax, w.colstats, (size_t)n * 8, cudaMemcpyDeviceToDevice, cx.st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(sumsq, w.d_tmp + 2 * n, 8, cudaMemcpyDeviceToDevice, cx.st));
+  return 0;
+}
+
+int tls_gram(const tls_matrix_t* A, int32_t u_f, const double* d_dev, int32_t K_t, double* G_dev, void* stream, void* ws,
+             size_t ws_bytes) {
+  TLS_TRY(check_matrix(A));
+  Work w;
+  if (!carve(A, ws, ws_bytes, w, true)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int n = (int)A->n;
+  DenseView dv{A->vals, A->m_local, n, A->ld};
+  TLS_CUDA_TRY(cudaMemsetAsync(w.flags, 0, 8 * sizeof(int), st));
+  k_recip<<<(n + 255) / 256, 256, 0, st>>>(d_dev, w.d_tmp, n);
+  TLS_LAUNCH_CHECK();
+  TLS_TRY(launch_gram(dv, u_f, w.d_tmp, K_t > 0 ? K_t : 2048, G_dev, w.gram_ws, w.gram_ws_doubles, &w.flags[1], st, nullptr));
+  int hf[8];
+  TLS_CUDA_TRY(cudaMemcpyAsync(hf, w.flags, sizeof(hf), cudaMemcpyDeviceToHost, st));
+  TLS_CUDA_TRY(cudaStreamSynchronize(st));
+  return hf[1] ? TLS_RANGE : 0;
+}
+
+int tls_pass(const tls_matrix_t* A, int32_t mode, int32_t nrhs, const double* q, const double* b, double* v, double* s,
+             void* stream, void* ws, size_t ws_bytes) {
+  TLS_TRY(check_matrix(A));
+  if ((mode != 0 && mode != 1) || nrhs < 1 || nrhs > 2 || (mode == 1 && nrhs != 1)) { set_error("bad pass args"); return TLS_ERR_ARG; }
+  Work w;
+  if (!carve(A, ws, ws_bytes, w, false)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
+  Ctx cx{static_cast<cudaStream_t>(stream), nullptr};
+  const int n = (int)A->n;
+  DenseView dv{A->vals, A->m_local, n, A->ld};
+  TLS_TRY(run_pass(cx, dv, mode == 0 ? PASS_OPERATOR : PASS_RESIDUAL, nrhs, q, b, w, nullptr));
+  TLS_CUDA_TRY(cudaMemcpyAsync(v, w.passout, (size_t)nrhs * n * 8, cudaMemcpyDeviceToDevice, cx.st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(s, w.passout + (size_t)nrhs * n, 16, cudaMemcpyDeviceToDevice, cx.st));
+  return 0;
+}
+
+int tls_precond_apply(const tls_precond_t R, int32_t trans, int32_t nrhs, double* Y, void* stream) {
+  if (!R || nrhs < 1 || nrhs > 2 || !Y) { set_error("bad apply args"); return TLS_ERR_ARG; }
+  return launch_precond_apply(R->dev, trans ? 1 : 0, nrhs, Y, R->dev.n, static_cast<cudaStream_t>(stream));
+}
+
+int tls_round(const double* x, double* y, int64_t n, int32_t prec, void* stream) {
+  if (n < 0 || prec < TLS_FP16 || prec > TLS_FP64) { set_error("bad round args"); return TLS_ERR_ARG; }
+  return launch_round(x, y, n, prec, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+// tls_kernels.h — host-side launchers of the libtlsrqi kernels (internal).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tls {
+
+constexpr int kMaxDenseN = 4096;   // register-resident column ownership in k_pass (CPT <= 8)
+
+int num_sms();
+
+// ---- streaming passes over A (k_pass.cu) ---------------------------------------------
+enum PassMode { PASS_OPERATOR = 0, PASS_RESIDUAL = 1, PASS_COLSTATS = 2 };
+struct DenseView {
+  const double* A;
+  int64_t m;
+  int n;
+  int64_t ld;
+};
+// CTAs used by one pass and the partial-buffer doubles it needs.
+int pass_grid(const DenseView& A);
+size_t pass_partials_doubles(const DenseView& A);
+// Writes gridDim x W partials; W = nrhs*n + 2 (operator/residual) or 2n (colstats).
+int launch_pass(const DenseView& A, int mode, int nrhs, const double* q, const double* b,
+                double* partials, const int* active, cudaStream_t st, int* grid_out);
+// out[w] = sum_g partials[g][w] (max for w < nmax), fixed order.
+int launch_reduce(const double* partials, int G, int W, int nmax, double* out, const int* active,
+                  cudaStream_t st);
+// d_j = 2^floor(log2 colmax_j), dinv_j = 1/d_j, normA2 = sum_j sumsq_j; *flag = 1 on a zero or
+// non-finite column.
+int launch_scaling(const double* colmax, const double* sumsq, int n, double* d, double* dinv,
+                   double* normA2, int* flag, cudaStream_t st);
+int launch_round(const double* x, double* y, int64_t n, int prec, cudaStream_t st);
+
+// ---- Gram (k_gram.cu) ------------------------------------------------------------------
+size_t gram_ws_doubles(const DenseView& A, int K_t);
+int launch_gram(const DenseView& A, int u_f, const double* dinv, int K_t, double* G, double* ws,
+                size_t ws_doubles, int* range_flag, cudaStream_t st, int* launches);
+
+// ---- Cholesky and R~ packing (k_chol.cu) -----------------------------------------------
+// In-place upper Cholesky of G (n x n, row-major, only the upper triangle is used).
+// *pivot = 1-based index of the first failed pivot (0 if none).
+int launch_cholesky(double* G, int n, int* pivot, cudaStream_t st, int* launches);
+// R~ = fl_uf(R) into the handle layouts; *range = 1 on overflow or a zero diagonal.
+struct PrecondDev {
+  int n, npad, u_f;
+  void* Rrow;       // npad x npad u_f, row-major R~ (lower part 0, padded diagonal 1)
+  void* RTrow;      // npad x npad u_f, row-major R~^T
+  double* DinvB;    // (npad/32) blocks of 32x32: DinvB[kb][l][i] = (R~_kk^{-1})[i][l]
+  double* DinvF;    // (npad/32) blocks of 32x32: DinvF[kb][l][i] = (R~_kk^{-1})[l][i]
+  double* d;        // npad (1 on padding)
+  double* dinv;     // npad
+  double* normA2;   // 1 (device)
+};
+int launch_pack_R(const double* R, int ldR, PrecondDev& pc, int* range, cudaStream_t st,
+                  int* launches);
+size_t precond_bytes(int n, int u_f);
+
+// ---- triangular solves, PCG and RQI vector kernels (k_trsv.cu) -------------------------
+struct PcgState {
+  double eta[2], eta0[2], qq[2], delta_min[2];
+  double sigma2, g, psi, xx, tol2;
+  int active[2], count[2], brk[2], brk_j[2];
+  int any_active;
+  int nrhs;
+  int iter;       // iteration index j of the next step
+  int pad_;
+};
+struct PcgVecs {  // device, each [2][npad]
+  double *omega, *s, *p, *q, *rhs;
+};
+int launch_precond_apply(const PrecondDev& pc, int trans, int nrhs, double* Y, int ldY,
+                         cudaStream_t st);
+int launch_pcg_init(const PrecondDev& pc, int nrhs, PcgVecs v, PcgState* S, cudaStream_t st);
+int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgState* S,
+                    int breakdown_rule, int compute_next_q, cudaStream_t st);
+// step record: sigma2, f (stored as rhs0 = -f), g, psi; copies x into rhs1.
+int launch_rqi_eval(const PrecondDev& pc, const double* passout, const double* x, PcgVecs v,
+                    PcgState* S, cudaStream_t st);
+int launch_rqi_update(const PrecondDev& pc, PcgVecs v, const PcgState* S, double* x,
+                      double* x_prev, cudaStream_t st);
+// x1 = x0 + sigma0^2 P^{-1} P^{-T} x0, sigma0^2 = rho0/(1 + x0^T x0) (Alg. 4 l.229-235).
+int launch_boot_x1(const PrecondDev& pc, const double* passout_r0, const double* x0, double* x1,
+                   cudaStream_t st);
+
+}  // namespace tls

@@ -1,0 +1,65 @@
+"""CPU checks of the C ABI library: it loads, exports every symbol that
+include/tlsrqi.h declares, and its host-only entry points behave (no GPU needed)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2305_19028_b200 import build, tlsrqi
+    build.build()
+    return tlsrqi.lib()
+
+
+def _header_symbols():
+    with open(os.path.join(ROOT, "include", "tlsrqi.h")) as fh:
+        txt = fh.read()
+    return sorted(set(re.findall(r"TLS_API\s+[\w\s\*]*?\b(tls_\w+)\s*\(", txt)))
+
+
+def test_exports_every_header_symbol(L):
+    syms = _header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(L, s), s
+    from paper_2305_19028_b200 import tlsrqi
+    assert sorted(tlsrqi.EXPORTED) == syms
+
+
+def test_host_entry_points(L):
+    from paper_2305_19028_b200 import tlsrqi
+    assert L.tls_abi_version() == 1
+    for code, name in tlsrqi.STATUS.items():
+        assert tlsrqi.tls_status_string(code) == name
+    o = tlsrqi.tls_rqi_opts_default()
+    from oracle.rqi import RqiOptions   # defaults agree with the oracle's
+    ro = RqiOptions()
+    for f in ("budget_rule", "stop_rule", "max_outer", "polish", "boot", "boot_max", "op_variant",
+              "breakdown_rule", "gram_chunk"):
+        assert getattr(o, f) == getattr(ro, f), f
+    assert o.boot_tol == ro.boot_tol and o.tol_inner == ro.tol_inner
+
+
+def test_struct_layouts_match_header(L):
+    from paper_2305_19028_b200 import tlsrqi
+    assert C.sizeof(tlsrqi.tls_matrix_t) == 4 + 4 + 5 * 8 + 3 * 8 + 8
+    assert tlsrqi.tls_info_t.sigma2.offset % 8 == 0
+
+
+def test_argument_validation_without_gpu(L):
+    from paper_2305_19028_b200 import tlsrqi
+    M = tlsrqi.tls_matrix_t()
+    M.layout, M.n, M.m_local, M.m_global, M.ld = 0, 4, 3, 3, 4   # m_global < n + 1
+    assert L.tls_workspace_size(C.byref(M), 50) == 0
+    M.layout = 1
+    M.m_global = 10
+    assert L.tls_workspace_size(C.byref(M), 50) == 0             # CSR not in this build
+    M.layout, M.ld = 0, 5                                        # odd ld
+    assert L.tls_workspace_size(C.byref(M), 50) == 0
+    M.ld, M.vals = 4, 256
+    assert L.tls_workspace_size(C.byref(M), 50) > 0

@@ -12,7 +12,7 @@ Construction (BASELINE.json configs[0..4]):
   Gaussian, columns sign-fixed so diag(R) > 0), V (n x n) the same ("Haar"),
   s = logspace(0, -log10(kappa), n), x_true ~ N(0, I), g ~ N(0, I),
   b = A x_true + eps * g            (literal configs)
-  b = A x_true + eps * g / sqrt(m)  ("w" twins, reading R3)
+  b = A x_true + eps * g / sqrt(m)  ("w" twins, reading R8)
 A is returned row-major (C-contiguous) fp64, which is the layout the C ABI
 takes (include/tlsrqi.h, TLS_DENSE_ROWMAJOR).
 
@@ -32,7 +32,7 @@ import numpy as np
 
 __all__ = [
     "DenseProblem", "CsrProblem", "dense_problem", "csr_problem", "config",
-    "CONFIGS", "shard_rows",
+    "CONFIGS",
 ]
 
 
@@ -50,6 +50,8 @@ class DenseProblem:
     twin: bool
     seed: int
     u_f: str = "fp16"
+    c: Optional[np.ndarray] = None   # U^T b (reduced "arrow" model, oracle/exact.py)
+    rho: Optional[float] = None      # ||b - U U^T b||
 
     @property
     def m(self) -> int:
@@ -111,8 +113,10 @@ def dense_problem(m: int, n: int, kappa: float, eps: float, seed: int,
         V = _orthonormal_np(GV)
         A = np.ascontiguousarray((U * s[None, :]) @ V.T)
         b = A @ x_true + scale * g
+        c = U.T @ b
+        rho = float(np.linalg.norm(b - U @ c))
         return DenseProblem(name, A, b, x_true, s, V if keep_factors else None,
-                            U if keep_factors else None, kappa, eps, twin, seed, u_f)
+                            U if keep_factors else None, kappa, eps, twin, seed, u_f, c, rho)
     import torch
     dev = torch.device(device)
     gen = torch.Generator(device=dev)
@@ -133,20 +137,23 @@ def dense_problem(m: int, n: int, kappa: float, eps: float, seed: int,
     V = V * sv[None, :]
     st = torch.as_tensor(s, dtype=torch.float64, device=dev)
     A = U @ (st[:, None] * V.T)
+    A = A.contiguous()
+    b = A @ x_true + scale * g
+    c = U.T @ b
+    rho = float(torch.linalg.norm(b - U @ c))
+    c = c.cpu().numpy()
     if not keep_factors:
         del U
         U = None
-    A = A.contiguous()
-    b = A @ x_true + scale * g
-    return DenseProblem(name, A, b, x_true, s, V if keep_factors else None,
-                        U, kappa, eps, twin, seed, u_f)
+    return DenseProblem(name, A, b, x_true, s, V.cpu().numpy(), U, kappa, eps, twin, seed, u_f,
+                        c, rho)
 
 
 def csr_problem(m: int = 200000, n: int = 2000, per_row: int = 10, eps: float = 1e-3,
                 seed: int = 3, name: str = "cfg3", u_f: str = "fp16") -> CsrProblem:
     """BASELINE.json configs[2]: each row i holds `per_row` DISTINCT columns drawn
     uniformly from {0..n-1} minus {i mod n}, plus column i mod n (DESIGN.md
-    reading R9); values N(0,1); columns sorted; b = A x_true + eps*g.
+    reading R16); values N(0,1); columns sorted; b = A x_true + eps*g.
     Draw order: per row the column sample, then all values, then x_true, g."""
     rng = np.random.Generator(np.random.PCG64(seed))
     cols = np.empty((m, per_row + 1), dtype=np.int64)
@@ -207,14 +214,3 @@ def config(name: str, device: str = "cpu", **kw):
     n = kw.pop("n", n)
     return dense_problem(m, n, kappa, eps, seed, twin=twin, device=device, name=name,
                          u_f=kw.pop("u_f", u_f), **kw)
-
-
-def shard_rows(m: int, nranks: int, rank: int) -> tuple[int, int]:
-    """Contiguous row block [lo, hi) of rank `rank` out of `nranks`:
-    the first m % nranks ranks get one extra row."""
-    if not (0 <= rank < nranks):
-        raise ValueError("rank out of range")
-    base, extra = divmod(m, nranks)
-    lo = rank * base + min(rank, extra)
-    hi = lo + base + (1 if rank < extra else 0)
-    return lo, hi
