@@ -28,7 +28,9 @@ static void gram_shape(const DenseView& A, int K_t, int& TT, int& ntiles, int& n
 size_t gram_ws_doubles(const DenseView& A, int K_t) {
   int TT, nt, nc, ns;
   gram_shape(A, K_t, TT, nt, nc, ns);
-  return (size_t)ns * nt * kGT * kGT;
+  const size_t cc = (size_t)ns * nt * kGT * kGT;
+  const size_t tc = (gram_tc_ws_bytes(A.m, A.n, 64) + 7) / 8;
+  return cc > tc ? cc : tc;
 }
 
 template <typename ACC, int PREC>
@@ -137,6 +139,8 @@ __global__ void k_gram_reduce(const double* __restrict__ part, int ntiles, int n
 int launch_gram(const DenseView& A, int u_f, const double* dinv, int K_t, double* G, double* ws,
                 size_t ws_doubles, int* range_flag, cudaStream_t st, int* launches) {
   if (K_t < 1) K_t = 2048;
+  if (gram_tc_supported(u_f, K_t))
+    return launch_gram_tc(A, u_f, dinv, K_t, G, ws, ws_doubles * 8, range_flag, st, launches);
   int TT, ntiles, nchunks, nsplit;
   gram_shape(A, K_t, TT, ntiles, nchunks, nsplit);
   if ((size_t)nsplit * ntiles * kGT * kGT > ws_doubles) {

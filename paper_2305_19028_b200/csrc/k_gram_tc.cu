@@ -1,0 +1,376 @@
+// k_gram_tc.cu — the u_f Gram on the 5th-generation tensor cores (SURVEY §8(a)
+// row a2; readings R10, R11), u_f in {fp16, bf16}.
+//
+//  1. k_round_scaled: A^ = fl_uf(A D^{-1}) (direct fp64 -> u_f RNE, reading R4)
+//     written once as a row-major 16-bit matrix (HBM-bound pass).
+//  2. k_gram_tc: G_IJ = A^_I^T A^_J for 128x128 tiles of the upper triangle,
+//     split over K_t-row chunks.  Warp-specialised persistent-tile CTA:
+//       warp 0      TMA producer: 2-D tensor loads (128B swizzle) of the two
+//                   64-row x 128-column operand panels into a 4-stage ring
+//       warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//                   (kind::f16, M=128 N=128 K=16, fp32 accumulators in TMEM,
+//                   both operands MN-major straight from the row-major A^)
+//       warps 2-9   epilogue: after every K_t rows, tcgen05.ld the fp32 chunk
+//                   sum and add it to fp64 registers (reading R11: fp32
+//                   accumulation per chunk, fp64 across chunks); two TMEM
+//                   accumulators ping-pong so the MMA never waits for a drain.
+//  3. the split partials are summed in fixed order (k_gram_reduce_t).
+#include <cuda.h>
+
+#include "tls_common.cuh"
+#include "tls_kernels.h"
+
+namespace tls {
+
+constexpr int kTcTile = 128;      // output tile edge (UMMA M = N = 128)
+constexpr int kTcBK = 64;         // rows of A^ per pipeline stage
+constexpr int kTcStages = 4;
+constexpr int kTcPanel = kTcTile * kTcBK * 2;   // 16 KB: one operand panel (2 TMA boxes of 8 KB)
+constexpr int kTcThreads = 320;
+
+// ------------------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+#define TLS_TMEM_LD32(taddr, r)                                                                                  \
+  asm volatile(                                                                                                  \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                             \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),         \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),   \
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), \
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])  \
+      : "r"(taddr)                                                                                               \
+      : "memory")
+
+// UMMA shared-memory descriptor, 128-byte swizzle, MN-major canonical layout
+// ((8 elem,8,m),(8 rows,k)) : ((1,8,LBO),(64 elem,SBO)) — what a TMA box of
+// 64 columns (128 B) x 64 rows with CU_TENSOR_MAP_SWIZZLE_128B produces.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// kind::f16 instruction descriptor: D fp32, A/B = fp16 (0) or bf16 (1), both MN-major, M = N = 128.
+__host__ __device__ constexpr uint32_t idesc_f16(int fmt) {
+  return (1u << 4) | ((uint32_t)fmt << 7) | ((uint32_t)fmt << 10) | (1u << 15) | (1u << 16) |
+         ((uint32_t)(kTcTile >> 3) << 17) | ((uint32_t)(kTcTile >> 4) << 24);
+}
+
+// ------------------------------------------------------------------------------ 1. A^ = fl_uf(A D^-1)
+template <int PREC>
+__global__ void k_round_scaled(const double* __restrict__ A, int64_t m, int n, int64_t ld, const double* __restrict__ dinv,
+                               uint16_t* __restrict__ Ah, int npad, int* __restrict__ range) {
+  const int groups = npad / 8;  // 8 columns -> one 16-byte store
+  const int64_t tot = m * groups;
+  int bad = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / groups;
+    const int c0 = (int)(e % groups) * 8;
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint16_t h[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int c = c0 + 2 * k + t;
+        double v = 0.0;
+        if (c < n) {
+          v = round_uf(A[row * ld + c] * dinv[c], PREC);
+          bad |= !isfinite(v);
+        }
+        h[t] = PREC == TLS_FP16 ? enc_f16(v) : enc_b16(v);
+      }
+      w[k] = (uint32_t)h[0] | ((uint32_t)h[1] << 16);
+    }
+    *reinterpret_cast<uint4*>(Ah + row * npad + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  if (bad) atomicExch(range, 1);
+}
+
+// ------------------------------------------------------------------------------ 2. tcgen05 SYRK
+template <int FMT>
+__global__ void __launch_bounds__(kTcThreads, 1)
+k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchunks, int nsplit, int kpc,
+          double* __restrict__ part) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte alignment for the 128B-swizzled operand panels
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* panA = smem;                                  // [stages][16 KB]
+  unsigned char* panB = smem + kTcStages * kTcPanel;           // [stages][16 KB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * kTcStages * kTcPanel);
+  uint64_t* empty = full + kTcStages;
+  uint64_t* tfull = empty + kTcStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int t = blockIdx.x, I = 0;
+  while (t >= TT - I) { t -= TT - I; ++I; }
+  const int J = I + t;
+  const bool diag = (I == J);
+  const int s = blockIdx.y;
+  const int c0 = (int)((int64_t)nchunks * s / nsplit), c1 = (int)((int64_t)nchunks * (s + 1) / nsplit);
+  const int kb_total = (int)((m + kTcBK - 1) / kTcBK);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTcStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);  // one arrive per epilogue warp
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(256)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      const uint32_t bytes = diag ? kTcPanel : 2 * kTcPanel;
+      int it = 0;
+      for (int c = c0; c < c1; ++c) {
+        const int kb1 = min((c + 1) * kpc, kb_total);
+        for (int kb = c * kpc; kb < kb1; ++kb, ++it) {
+          const int st = it % kTcStages;
+          const uint32_t ph = (uint32_t)(it / kTcStages) & 1u;
+          if (it >= kTcStages) mbar_wait(&empty[st], ph ^ 1u);
+          mbar_arrive_expect_tx(&full[st], bytes);
+          const int row = kb * kTcBK;
+          unsigned char* a = panA + st * kTcPanel;
+          tma_load_2d(a, &tmap, I * kTcTile, row, &full[st]);
+          tma_load_2d(a + kTcPanel / 2, &tmap, I * kTcTile + 64, row, &full[st]);
+          if (!diag) {
+            unsigned char* b = panB + st * kTcPanel;
+            tma_load_2d(b, &tmap, J * kTcTile, row, &full[st]);
+            tma_load_2d(b + kTcPanel / 2, &tmap, J * kTcTile + 64, row, &full[st]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread)
+    if (lane == 0) {
+      const uint32_t idesc = idesc_f16(FMT);
+      int it = 0;
+      for (int c = c0; c < c1; ++c) {
+        const int j = c - c0;
+        const int buf = j & 1;
+        if (j >= 2) mbar_wait(&tempty[buf], (uint32_t)((j >> 1) - 1) & 1u);
+        tc_fence_after();
+        const uint32_t dtm = tmem_base + (uint32_t)(buf * kTcTile);
+        const int kb1 = min((c + 1) * kpc, kb_total);
+        for (int kb = c * kpc; kb < kb1; ++kb, ++it) {
+          const int st = it % kTcStages;
+          const uint32_t ph = (uint32_t)(it / kTcStages) & 1u;
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(panA + st * kTcPanel);
+          const uint32_t b0 = smem_u32((diag ? panA : panB) + st * kTcPanel);
+#pragma unroll
+          for (int kk = 0; kk < kTcBK / 16; ++kk) {
+            // K = 16 rows = two 8-row groups of 1024 B (SBO); MN halves 8 KB apart (LBO)
+            const uint64_t ad = sw128_desc(a0 + kk * 2048, kTcPanel / 2, 1024);
+            const uint64_t bd = sw128_desc(b0 + kk * 2048, kTcPanel / 2, 1024);
+            tc_mma_f16(dtm, ad, bd, idesc, (kb > c * kpc || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty[st]);
+        }
+        tc_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    // ---------------- epilogue: fp32 chunk sums -> fp64 registers
+    const int q = warp & 3;                 // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;       // column half: 0 -> cols 0..63, 1 -> 64..127
+    double acc[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) acc[i] = 0.0;
+    for (int c = c0; c < c1; ++c) {
+      const int j = c - c0;
+      const int buf = j & 1;
+      mbar_wait(&tfull[buf], (uint32_t)(j >> 1) & 1u);
+      tc_fence_after();
+#pragma unroll
+      for (int piece = 0; piece < 2; ++piece) {
+        uint32_t r[32];
+        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kTcTile + half * 64 + piece * 32);
+        TLS_TMEM_LD32(ta, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int k = 0; k < 32; ++k) acc[piece * 32 + k] += (double)__uint_as_float(r[k]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+    }
+    const int row = q * 32 + lane;
+    double* out = part + ((size_t)s * gridDim.x + blockIdx.x) * (kTcTile * kTcTile) + (size_t)row * kTcTile + half * 64;
+#pragma unroll
+    for (int k = 0; k < 64; k += 2) *reinterpret_cast<double2*>(out + k) = make_double2(acc[k], acc[k + 1]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------------------ 3. split reduction
+__global__ void k_gram_reduce_t(const double* __restrict__ part, int ntiles, int nsplit, int TT, int tile, int n,
+                                double* __restrict__ G) {
+  int t = blockIdx.x, I = 0;
+  while (t >= TT - I) { t -= TT - I; ++I; }
+  const int J = I + t;
+  const int te = tile * tile;
+  for (int e = threadIdx.x; e < te; e += blockDim.x) {
+    const int i = e / tile, j = e % tile;
+    const int gi = I * tile + i, gj = J * tile + j;
+    double acc = 0.0;
+    for (int s = 0; s < nsplit; ++s) acc += part[((size_t)s * ntiles + blockIdx.x) * te + e];
+    if (gi < n && gj < n) {
+      G[(size_t)gi * n + gj] = acc;
+      G[(size_t)gj * n + gi] = acc;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+static void tc_shape(int64_t m, int n, int K_t, int& TT, int& ntiles, int& nchunks, int& nsplit) {
+  TT = (n + kTcTile - 1) / kTcTile;
+  ntiles = TT * (TT + 1) / 2;
+  nchunks = (int)((m + K_t - 1) / K_t);
+  if (nchunks < 1) nchunks = 1;
+  const int target = 2 * num_sms();
+  nsplit = (target + ntiles - 1) / ntiles;
+  if (nsplit > nchunks) nsplit = nchunks;
+  if (nsplit < 1) nsplit = 1;
+}
+
+bool gram_tc_supported(int u_f, int K_t) {
+  if (u_f != TLS_FP16 && u_f != TLS_BF16) return false;
+  if (K_t % kTcBK != 0) return false;
+  const char* e = getenv("TLS_GRAM");
+  if (e && e[0] == 'c') return false;  // TLS_GRAM=cc forces the CUDA-core path
+  return encode_fn() != nullptr;
+}
+
+size_t gram_tc_ws_bytes(int64_t m, int n, int K_t) {
+  int TT, ntiles, nchunks, nsplit;
+  tc_shape(m, n, K_t < kTcBK ? kTcBK : K_t, TT, ntiles, nchunks, nsplit);
+  const int npad = (n + 7) / 8 * 8;
+  const size_t ah = ((size_t)m * npad * 2 + 1023) & ~(size_t)1023;
+  return ah + (size_t)nsplit * ntiles * kTcTile * kTcTile * 8;
+}
+
+int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, double* G, void* ws, size_t ws_bytes,
+                   int* range_flag, cudaStream_t st, int* launches) {
+  int TT, ntiles, nchunks, nsplit;
+  tc_shape(A.m, A.n, K_t, TT, ntiles, nchunks, nsplit);
+  const int npad = (A.n + 7) / 8 * 8;
+  const size_t ah_bytes = ((size_t)A.m * npad * 2 + 1023) & ~(size_t)1023;
+  if (gram_tc_ws_bytes(A.m, A.n, K_t) > ws_bytes) {
+    set_error("gram_tc: workspace too small");
+    return TLS_ERR_WORKSPACE;
+  }
+  uint16_t* Ah = static_cast<uint16_t*>(ws);
+  double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + ah_bytes);
+  // 1. A^ = fl_uf(A D^-1)
+  {
+    const int64_t tot = A.m * (npad / 8);
+    int64_t g = (tot + 255) / 256;
+    const int64_t gmax = (int64_t)num_sms() * 16;
+    if (g > gmax) g = gmax;
+    if (u_f == TLS_FP16)
+      k_round_scaled<TLS_FP16><<<(int)g, 256, 0, st>>>(A.A, A.m, A.n, A.ld, dinv, Ah, npad, range_flag);
+    else
+      k_round_scaled<TLS_BF16><<<(int)g, 256, 0, st>>>(A.A, A.m, A.n, A.ld, dinv, Ah, npad, range_flag);
+    TLS_LAUNCH_CHECK();
+  }
+  // 2. tensor map over A^ (row-major m x npad, 16-bit), 64x64 boxes, 128B swizzle
+  CUtensorMap tmap;
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)npad, (cuuint64_t)A.m};
+    const cuuint64_t strides[1] = {(cuuint64_t)npad * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)kTcBK};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&tmap, u_f == TLS_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                   2, Ah, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+      return TLS_ERR_CUDA;
+    }
+  }
+  const size_t smem = 2 * kTcStages * kTcPanel + 1024 + 256;
+  dim3 grid(ntiles, nsplit);
+  if (u_f == TLS_FP16) {
+    TLS_CUDA_TRY(cudaFuncSetAttribute(k_gram_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_gram_tc<0><<<grid, kTcThreads, smem, st>>>(tmap, A.m, TT, nchunks, nsplit, K_t / kTcBK, part);
+  } else {
+    TLS_CUDA_TRY(cudaFuncSetAttribute(k_gram_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_gram_tc<1><<<grid, kTcThreads, smem, st>>>(tmap, A.m, TT, nchunks, nsplit, K_t / kTcBK, part);
+  }
+  TLS_LAUNCH_CHECK();
+  k_gram_reduce_t<<<ntiles, 256, 0, st>>>(part, ntiles, nsplit, TT, kTcTile, A.n, G);
+  TLS_LAUNCH_CHECK();
+  if (launches) *launches += 3;
+  return 0;
+}
+
+}  // namespace tls

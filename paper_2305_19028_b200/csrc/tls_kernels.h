@@ -33,8 +33,12 @@ int launch_scaling(const double* colmax, const double* sumsq, int n, double* d, 
                    double* normA2, int* flag, cudaStream_t st);
 int launch_round(const double* x, double* y, int64_t n, int prec, cudaStream_t st);
 
-// ---- Gram (k_gram.cu) ------------------------------------------------------------------
-size_t gram_ws_doubles(const DenseView& A, int K_t);
+// ---- Gram (k_gram.cu: CUDA-core fp64/fp32 path; k_gram_tc.cu: tcgen05 path) -------------
+size_t gram_ws_doubles(const DenseView& A, int K_t);   // workspace of either path (doubles)
+bool gram_tc_supported(int u_f, int K_t);
+size_t gram_tc_ws_bytes(int64_t m, int n, int K_t);
+int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, double* G, void* ws, size_t ws_bytes,
+                   int* range_flag, cudaStream_t st, int* launches);
 int launch_gram(const DenseView& A, int u_f, const double* dinv, int K_t, double* G, double* ws,
                 size_t ws_doubles, int* range_flag, cudaStream_t st, int* launches);
 

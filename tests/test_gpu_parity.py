@@ -103,9 +103,15 @@ def test_pass_odd_n_padded(T):
 
 
 # ----------------------------------------------------------------------------- a2 / a3
+@pytest.mark.parametrize("path", ["tc", "cc"])
 @pytest.mark.parametrize("fmt", ["fp16", "bf16", "fp32", "fp64"])
-@pytest.mark.parametrize("m,n", [(5000, 64), (9000, 200), (2100, 513)])
-def test_gram_within_accumulation_bound(T, fmt, m, n):
+@pytest.mark.parametrize("m,n", [(5000, 64), (9000, 200), (2100, 513), (70001, 256), (300, 40)])
+def test_gram_within_accumulation_bound(T, fmt, m, n, path, monkeypatch):
+    """tc: tcgen05 kernel (fp16/bf16); cc: CUDA-core kernel (TLS_GRAM=cc)."""
+    if path == "cc":
+        monkeypatch.setenv("TLS_GRAM", "cc")
+    elif fmt in ("fp32", "fp64"):
+        pytest.skip("fp32/fp64 Gram has only the fp64 CUDA-core path")
     P = _problem(m, n)
     d, _ = rqi.column_scaling(P.A)
     rc, G = T.tls_gram(T.matrix(T.dense_operand(dev(P.A))), fmt, dev(d), 2048)
