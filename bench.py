@@ -249,8 +249,15 @@ def main():
     launches = 0
     passes = 0
     infos = []
+    dbg = os.environ.get("BENCH_DEBUG") == "1"
     for _ in range(args.steps):
+        if dbg:
+            ev_a = torch.cuda.Event(enable_timing=True); ev_a.record(stream); th = time.perf_counter()
         fi, info, sig = step()
+        if dbg:
+            ev_b = torch.cuda.Event(enable_timing=True); ev_b.record(stream); ev_b.synchronize()
+            print(f"[bench] step device {ev_a.elapsed_time(ev_b):.2f} ms host {1e3 * (time.perf_counter() - th):.2f} ms",
+                  file=sys.stderr, flush=True)
         launches += fi["launches"] + info["launches"]
         passes += fi["passes"] + info["passes"]
         infos.append(info)

@@ -104,7 +104,7 @@ typedef struct {
   double boot_tol;        /* [1e-8] */
   int32_t op_variant;     /* 0: A-in-loop operator (R1) [0]; other values unsupported */
   int32_t breakdown_rule; /* 0: delta < 0 is a breakdown (R3) [0]; 1: only delta == 0 stops */
-  int32_t gram_chunk;     /* K_t rows per fp32 accumulation chunk (R11) [2048] */
+  int32_t gram_chunk;     /* K_t rows per fp32 accumulation chunk (R11) [64]; multiple of 64 for the tensor-core path */
   int32_t reserved[5];
 } tls_rqi_opts_t;
 

@@ -68,7 +68,7 @@ def column_scaling(A):
 
 
 # ----------------------------------------------------------------------------- Gram
-def gram_uf(A, d: np.ndarray, u_f: str, K_t: int = 2048) -> np.ndarray:
+def gram_uf(A, d: np.ndarray, u_f: str, K_t: int = 64) -> np.ndarray:
     """G = sum over chunks c of K_t consecutive rows (in order) of
     fp64( fl32-accumulated  A^_c^T A^_c ),  A^ = fl_uf(A D^{-1})   (R10, R11).
 
@@ -93,7 +93,7 @@ def gram_uf(A, d: np.ndarray, u_f: str, K_t: int = 2048) -> np.ndarray:
     return G
 
 
-def gram_exact_bound(A, d: np.ndarray, u_f: str, K_t: int = 2048) -> np.ndarray:
+def gram_exact_bound(A, d: np.ndarray, u_f: str, K_t: int = 64) -> np.ndarray:
     """Elementwise bound on |G_fp32chunks - A^^T A^| (standard dot-product error
     bound, gamma_k = k u/(1 - k u) with u = 2^-24 per fp32 chunk of length <= K_t,
     plus the fp64 chunk sums)."""
@@ -125,7 +125,7 @@ class Precond:
     R: Optional[np.ndarray] = None
 
 
-def factor_precond(A, u_f: str, K_t: int = 2048, keep: bool = False) -> Precond:
+def factor_precond(A, u_f: str, K_t: int = 64, keep: bool = False) -> Precond:
     """tls_factor_precond: scaling, u_f Gram, fp64 Cholesky G = R^T R (LAPACK
     dpotrf, upper), R~ = fl_uf(R)  (PAPER.md l.231 with the Cholesky route of
     l.290-307; readings R10, R11)."""
@@ -234,7 +234,7 @@ class RqiOptions:
     boot_max: int = 200
     op_variant: int = 0        # 0: A-in-loop (R1); 1: paper Alg. 3
     breakdown_rule: int = 0    # 0: delta <= 0 stops (spec); 1: delta == 0 only (paper)
-    gram_chunk: int = 2048
+    gram_chunk: int = 64
 
 
 @dataclasses.dataclass

@@ -138,7 +138,7 @@ __global__ void k_gram_reduce(const double* __restrict__ part, int ntiles, int n
 
 int launch_gram(const DenseView& A, int u_f, const double* dinv, int K_t, double* G, double* ws,
                 size_t ws_doubles, int* range_flag, cudaStream_t st, int* launches) {
-  if (K_t < 1) K_t = 2048;
+  if (K_t < 1) K_t = 64;
   if (gram_tc_supported(u_f, K_t))
     return launch_gram_tc(A, u_f, dinv, K_t, G, ws, ws_doubles * 8, range_flag, st, launches);
   int TT, ntiles, nchunks, nsplit;

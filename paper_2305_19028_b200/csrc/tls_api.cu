@@ -6,6 +6,7 @@
 // inside PCGTLS all control (breakdown, early exit) is device-resident.
 #include <dlfcn.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstring>
@@ -78,6 +79,7 @@ struct tls_comm_s {
 struct tls_precond_s {
   PrecondDev dev;
   void* base;
+  size_t bytes;
   int device;
   double normA2_host;
 };
@@ -150,6 +152,42 @@ struct ProfScope {
       prof().pend.push_back({a, b, cat});
       if (prof().pend.size() > 4096) prof_drain();
     }
+  }
+};
+}  // namespace
+
+
+// ------------------------------------------------------------------------------ phase trace
+// TLS_TRACE=1: events + host clock at phase marks, printed to stderr at the end of
+// each top-level call (device time vs host time between consecutive marks).
+namespace {
+struct Tracer {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  std::vector<double> host;
+  explicit Tracer(cudaStream_t s) : st(s) {
+    const char* e = getenv("TLS_TRACE");
+    on = e && e[0] == '1';
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.push_back({name, e});
+    host.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count());
+  }
+  ~Tracer() {
+    if (!on || ev.empty()) return;
+    cudaEventSynchronize(ev.back().second);
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+      fprintf(stderr, "[tls_trace] %-18s -> %-18s device %9.3f ms  host %9.3f ms\n", ev[i - 1].first, ev[i].first, ms,
+              host[i] - host[i - 1]);
+    }
+    for (auto& p : ev) cudaEventDestroy(p.second);
   }
 };
 }  // namespace
@@ -317,18 +355,39 @@ void fill_info_defaults(tls_info_t* info) {
   info->pcg_steps = 0;
 }
 
+// Device buffers of destroyed handles are kept for reuse (keyed by device and size):
+// repeated factorizations (one per solve in a benchmark or a service) then do no
+// cudaMalloc/cudaFree, which were measured to stall the stream for up to ~25 ms.
+struct PoolEntry { int device; size_t bytes; void* ptr; };
+static std::vector<PoolEntry>& precond_pool() {
+  static std::vector<PoolEntry> p;
+  return p;
+}
+
 int alloc_precond(int n, int u_f, tls_precond_t* out) {
   tls_precond_s* h = new tls_precond_s();
   const int npad = (n + 31) / 32 * 32;
   const size_t es = (u_f == TLS_FP64) ? 8 : (u_f == TLS_FP32 ? 4 : 2);
   const size_t bytes = precond_bytes(n, u_f);
-  cudaError_t e = cudaMalloc(&h->base, bytes);
-  if (e != cudaSuccess) {
-    delete h;
-    set_error("cudaMalloc(precond %zu B): %s", bytes, cudaGetErrorString(e));
-    return TLS_ERR_CUDA;
-  }
   cudaGetDevice(&h->device);
+  h->base = nullptr;
+  auto& pool = precond_pool();
+  for (size_t i = 0; i < pool.size(); ++i) {
+    if (pool[i].device == h->device && pool[i].bytes == bytes) {
+      h->base = pool[i].ptr;
+      pool.erase(pool.begin() + (long)i);
+      break;
+    }
+  }
+  if (!h->base) {
+    cudaError_t e = cudaMalloc(&h->base, bytes);
+    if (e != cudaSuccess) {
+      delete h;
+      set_error("cudaMalloc(precond %zu B): %s", bytes, cudaGetErrorString(e));
+      return TLS_ERR_CUDA;
+    }
+  }
+  h->bytes = bytes;
   char* p = static_cast<char*>(h->base);
   PrecondDev& d = h->dev;
   d.n = n;
@@ -390,7 +449,7 @@ void tls_rqi_opts_default(tls_rqi_opts_t* o) {
   o->boot_tol = 1e-8;
   o->op_variant = 0;
   o->breakdown_rule = 0;
-  o->gram_chunk = 2048;
+  o->gram_chunk = 64;
 }
 
 const char* tls_status_string(int s) {
@@ -467,12 +526,14 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
   if (!R_out || u_f < TLS_FP16 || u_f > TLS_FP64) { set_error("bad u_f or R_out"); return TLS_ERR_ARG; }
   tls_rqi_opts_t o;
   if (opts) o = *opts; else tls_rqi_opts_default(&o);
-  const int K_t = o.gram_chunk > 0 ? o.gram_chunk : 2048;
+  const int K_t = o.gram_chunk > 0 ? o.gram_chunk : 64;
   Work w;
   if (!carve(A, ws, ws_bytes, w, true)) { set_error("workspace too small (need %zu)", ws_need(A, true)); return TLS_ERR_WORKSPACE; }
   Ctx cx{static_cast<cudaStream_t>(stream), comm};
   const int n = (int)A->n;
   DenseView dv{A->vals, A->m_local, n, A->ld};
+  Tracer tr(cx.st);
+  tr.mark("factor:start");
   TLS_CUDA_TRY(cudaMemsetAsync(w.flags, 0, 8 * sizeof(int), cx.st));
   // a1: column max / sums of squares, all-reduced; D = powers of two (R2)
   TLS_TRY(run_pass(cx, dv, PASS_COLSTATS, 2, nullptr, nullptr, w, nullptr));
@@ -481,6 +542,7 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
   double* normA2 = w.d_tmp + 2 * n;
   TLS_TRY(launch_scaling(w.colstats, w.colstats + n, n, d, dinv, normA2, &w.flags[0], cx.st));
   cx.launches += 1;
+  tr.mark("colstats");
   // a2: u_f Gram, all-reduced
   if (dv.m > 0) {
     ProfScope ps(TLS_PROF_GRAM, cx.st);
@@ -490,11 +552,13 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
   }
   cx.passes += 1;
   TLS_TRY(allreduce(comm, w.G, (size_t)n * n, ncclSum, cx.st));
+  tr.mark("gram");
   // a3: Cholesky (replicated on every rank: identical bits)
   {
     ProfScope ps(TLS_PROF_CHOL, cx.st);
     TLS_TRY(launch_cholesky(w.G, n, &w.flags[2], cx.st, &cx.launches));
   }
+  tr.mark("cholesky");
   int hflags[8];
   double hnorm = 0.0;
   TLS_CUDA_TRY(cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, cx.st));
@@ -507,16 +571,20 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
     if (info) { info->status = TLS_CHOL_BREAKDOWN; info->chol_pivot = hflags[2]; }
     return TLS_CHOL_BREAKDOWN;
   }
+  tr.mark("sync1");
   tls_precond_t h = nullptr;
   TLS_TRY(alloc_precond(n, u_f, &h));
+  tr.mark("alloc");
   h->normA2_host = hnorm;
   k_fill_scaling<<<(h->dev.npad + 255) / 256, 256, 0, cx.st>>>(h->dev.d, h->dev.dinv, d, dinv, n, h->dev.npad);
   TLS_CUDA_TRY(cudaMemcpyAsync(h->dev.normA2, normA2, sizeof(double), cudaMemcpyDeviceToDevice, cx.st));
   int rc = launch_pack_R(w.G, n, h->dev, &w.flags[1], cx.st, &cx.launches);
   cx.launches += 1;  // k_fill_scaling
   if (rc) { tls_precond_destroy(h); return rc; }
+  tr.mark("pack");
   TLS_CUDA_TRY(cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, cx.st));
   TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+  tr.mark("sync2");
   if (info) { info->passes = cx.passes; info->launches = cx.launches; }
   if (hflags[1]) {
     tls_precond_destroy(h);
@@ -599,7 +667,15 @@ int tls_precond_export(tls_precond_t R, double* Rt_host, double* d_host, double*
 
 void tls_precond_destroy(tls_precond_t R) {
   if (!R) return;
-  if (R->base) cudaFree(R->base);
+  if (R->base) {
+    auto& pool = precond_pool();
+    if (pool.size() < 8) {
+      cudaDeviceSynchronize();  // like cudaFree: no queued work may still read the buffer
+      pool.push_back({R->device, R->bytes, R->base});
+    } else {
+      cudaFree(R->base);
+    }
+  }
   delete R;
 }
 
@@ -659,6 +735,8 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
     return 0;
   };
 
+  Tracer tr(cx.st);
+  tr.mark("rqi:start");
   TLS_CUDA_TRY(cudaMemsetAsync(w.zero, 0, (size_t)n * 8, cx.st));
   TLS_CUDA_TRY(cudaMemsetAsync(w.vec.rhs, 0, 2 * (size_t)n * 8, cx.st));
   // setup (a1): h = A^T b, b^T b from the residual pass at x = 0
@@ -667,6 +745,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   TLS_CUDA_TRY(cudaMemcpyAsync(&bb, w.passout + n, 8, cudaMemcpyDeviceToHost, cx.st));
   k_copy<<<(n + 255) / 256, 256, 0, cx.st>>>(w.passout, w.vec.rhs, n);
   cx.launches += 1;
+  tr.mark("setup");
   // a4: bootstrap x_0 = x_LS (R5)
   int boot_iters = 0;
   if (o.boot == 0) {
@@ -687,6 +766,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
     cx.launches += 2;
   }
   cx.launches += 1;
+  tr.mark("boot_cgls");
   TLS_TRY(run_pass(cx, dv, PASS_RESIDUAL, 1, w.x0, b, w, nullptr));     // r_0 (l.227)
   TLS_TRY(launch_boot_x1(pc, w.passout, w.x0, w.x, cx.st));              // l.229-235
   cx.launches += 1;
@@ -703,7 +783,9 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
     TLS_TRY(run_pass(cx, dv, PASS_RESIDUAL, 1, w.x, b, w, nullptr));
     TLS_TRY(launch_rqi_eval(pc, w.passout, w.x, w.vec, w.S, cx.st));
     cx.launches += 1;
+    tr.mark("resid+eval");
     TLS_TRY(read_state());
+    tr.mark("read_state");
     const double sig2 = hS.sigma2, psi = hS.psi;
     s2tr.push_back(sig2);
     psitr.push_back(psi);
@@ -731,7 +813,9 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
       TLS_TRY(launch_pcg_init(pc, 2, w.vec, w.S, cx.st));
     }
     cx.launches += 1;
+    tr.mark("pcg_init");
     TLS_TRY(pcg_loop(2, budget));
+    tr.mark("pcg_loop");
     TLS_TRY(read_state());
     pcgc.push_back(hS.count[0]);
     pcgc.push_back(hS.count[1]);
@@ -844,7 +928,7 @@ int tls_gram(const tls_matrix_t* A, int32_t u_f, const double* d_dev, int32_t K_
   TLS_CUDA_TRY(cudaMemsetAsync(w.flags, 0, 8 * sizeof(int), st));
   k_recip<<<(n + 255) / 256, 256, 0, st>>>(d_dev, w.d_tmp, n);
   TLS_LAUNCH_CHECK();
-  TLS_TRY(launch_gram(dv, u_f, w.d_tmp, K_t > 0 ? K_t : 2048, G_dev, w.gram_ws, w.gram_ws_doubles, &w.flags[1], st, nullptr));
+  TLS_TRY(launch_gram(dv, u_f, w.d_tmp, K_t > 0 ? K_t : 64, G_dev, w.gram_ws, w.gram_ws_doubles, &w.flags[1], st, nullptr));
   int hf[8];
   TLS_CUDA_TRY(cudaMemcpyAsync(hf, w.flags, sizeof(hf), cudaMemcpyDeviceToHost, st));
   TLS_CUDA_TRY(cudaStreamSynchronize(st));

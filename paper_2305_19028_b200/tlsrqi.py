@@ -315,7 +315,7 @@ def tls_colstats(M: tls_matrix_t, stream=None, ws=None):
     return colmax, sumsq
 
 
-def tls_gram(M: tls_matrix_t, u_f, d: torch.Tensor, K_t: int = 2048, stream=None, ws=None):
+def tls_gram(M: tls_matrix_t, u_f, d: torch.Tensor, K_t: int = 64, stream=None, ws=None):
     if ws is None:
         ws = workspace(M)
     n = int(M.n)

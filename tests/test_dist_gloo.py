@@ -1,0 +1,110 @@
+"""Multi-GPU host logic on the CPU: world size 2 over torch.distributed (gloo).
+
+The library's N > 1 path is: contiguous row shards
+(paper_2305_19028_b200.dist.shard_rows), per-rank partial sums of every pass
+over A, an fp64 all-reduce (sum; max for the column maxima), and replicated
+n-vector work.  Here each rank computes its partials with the oracle's
+primitives on its row block, all-reduces them with gloo, and the results must
+equal the unsharded computation; the NCCL unique id is broadcast the way
+dist.init_comm does it."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as tdist
+import torch.multiprocessing as mp
+
+import tlsgen
+from oracle import rqi
+from paper_2305_19028_b200.dist import broadcast_unique_id, shard_rows
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_shard_rows_partition():
+    for m in (1, 7, 200, 4096, 1 << 20, 65537):
+        for P in (1, 2, 3, 4, 8):
+            blocks = [shard_rows(m, P, r) for r in range(P)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == m
+            for (lo, hi), (lo2, _) in zip(blocks, blocks[1:]):
+                assert hi == lo2
+            sizes = [hi - lo for lo, hi in blocks]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _allreduce(x: np.ndarray, op=tdist.ReduceOp.SUM) -> np.ndarray:
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
+    tdist.all_reduce(t, op=op)
+    return t.numpy()
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        P = tlsgen.config("cfg1")
+        A, b = P.A, P.b
+        m, n = A.shape
+        lo, hi = shard_rows(m, world, rank)
+        Al, bl = A[lo:hi], b[lo:hi]
+        res = {}
+        # a1: column max (max-reduce) and sums of squares (sum-reduce) -> identical D
+        cm = _allreduce(np.max(np.abs(Al), axis=0), tdist.ReduceOp.MAX)
+        ss = _allreduce(np.sum(Al * Al, axis=0))
+        d_full, nrm_full = rqi.column_scaling(A)
+        _, E = np.frexp(cm)
+        res["d_equal"] = bool(np.array_equal(np.ldexp(1.0, E - 1), d_full))
+        res["normA2_rel"] = abs(ss.sum() - nrm_full) / nrm_full
+        # a2: partial u_f Grams summed over ranks (chunks are local to each rank)
+        G = _allreduce(rqi.gram_uf(Al, d_full, "fp16", 64))
+        B = rqi.gram_exact_bound(A, d_full, "fp16", 64)
+        Ah = rqi.round_to(A / d_full, "fp16")
+        res["gram_in_bound"] = bool(np.all(np.abs(G - Ah.T @ Ah) <= 2 * B))
+        # a7: operator pass, 2 RHS: v_r = sum_p A_p^T (A_p q_r), tau_r = sum_p ||A_p q_r||^2
+        Q = np.random.default_rng(0).standard_normal((2, n))
+        for r in range(2):
+            t = Al @ Q[r]
+            v = _allreduce(np.concatenate([Al.T @ t, [t @ t]]))
+            tf = A @ Q[r]
+            res[f"op_rel_{r}"] = np.linalg.norm(v[:n] - A.T @ tf) / np.linalg.norm(A.T @ tf)
+            res[f"tau_rel_{r}"] = abs(v[n] - tf @ tf) / (tf @ tf)
+        # a5: residual pass: v = A^T(b - Ax), rho = r^T r, gamma = b^T r
+        x = np.random.default_rng(1).standard_normal(n)
+        rl = bl - Al @ x
+        v = _allreduce(np.concatenate([Al.T @ rl, [rl @ rl, bl @ rl]]))
+        rf = b - A @ x
+        res["resid_rel"] = np.linalg.norm(v[:n] - A.T @ rf) / np.linalg.norm(A.T @ rf)
+        res["rho_rel"] = abs(v[n] - rf @ rf) / (rf @ rf)
+        # replicated n-vector work: every rank derives identical bits from identical inputs
+        sig2 = v[n] / (1 + x @ x)
+        f = -v[:n] - sig2 * x
+        allf = [torch.zeros(n, dtype=torch.float64) for _ in range(world)]
+        tdist.all_gather(allf, torch.from_numpy(f))
+        res["replicas_identical"] = all(torch.equal(allf[0], a) for a in allf)
+        # NCCL unique id broadcast over the process group (dist.init_comm)
+        uid = bytes(range(128)) if rank == 0 else None
+        res["uid_ok"] = broadcast_unique_id(uid) == bytes(range(128))
+        out[rank] = res
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_row_sharded_passes_world2():
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+    for rank in range(world):
+        r = out[rank]
+        assert r["d_equal"] and r["gram_in_bound"] and r["replicas_identical"] and r["uid_ok"]
+        assert r["normA2_rel"] < 1e-14
+        for k in ("op_rel_0", "op_rel_1", "tau_rel_0", "tau_rel_1", "resid_rel", "rho_rel"):
+            assert r[k] < 1e-13, (k, r[k])

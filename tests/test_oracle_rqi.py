@@ -73,12 +73,18 @@ def test_cholesky_reconstruction_and_qr_route():
 
 
 def test_cholesky_breakdown_index():
-    """kappa^2 > 1/u: an exactly repeated column makes the Gram singular."""
-    rng = np.random.default_rng(3)
-    A = rng.standard_normal((500, 8))
-    A[:, 5] = A[:, 2]
-    pc = rqi.factor_precond(A, "fp64")
-    assert pc.status == rqi.CHOL_BREAKDOWN and pc.chol_pivot == 6
+    """Exact arithmetic: 39 orthogonal 0/1 columns with four ones each (G_jj = 4,
+    R_jj = 2 exactly) and column 40 = column 18, so the 40th pivot is exactly 0
+    for every u_f and chunk size."""
+    n = 40
+    A = np.zeros((4 * (n - 1), n))
+    for i in range(A.shape[0]):
+        A[i, i % (n - 1)] = 1.0
+    A[:, n - 1] = A[:, 17]
+    for fmt in ("fp16", "bf16", "fp32", "fp64"):
+        for K_t in (1, 64, 2048):
+            pc = rqi.factor_precond(A, fmt, K_t)
+            assert pc.status == rqi.CHOL_BREAKDOWN and pc.chol_pivot == n
 
 
 def test_precond_solves_vs_dense_solve():
