@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
 k_pass(const double* __restrict__ A, int64_t m, int n, int64_t ld, int rps,
        const double* __restrict__ q, const double* __restrict__ b,
        double* __restrict__ partials, int W, const int* __restrict__ active) {
-  if (active != nullptr && *active == 0) return;
+  if (active != nullptr && (active[0] | active[1]) == 0) return;
   extern __shared__ __align__(128) unsigned char smem[];
   double* ring = reinterpret_cast<double*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kPassStages * kPassStageBytes);
@@ -293,7 +293,7 @@ int launch_pass(const DenseView& A, int mode, int nrhs, const double* q, const d
 // --------------------------------------------------------------------------- partial reduction
 __global__ void k_reduce_partials(const double* __restrict__ partials, int G, int W, int nmax,
                                   double* __restrict__ out, const int* __restrict__ active) {
-  if (active != nullptr && *active == 0) return;
+  if (active != nullptr && (active[0] | active[1]) == 0) return;
   __shared__ double sm[8][33];
   const int tx = threadIdx.x, grp = threadIdx.y;
   const int w = blockIdx.x * 32 + tx;

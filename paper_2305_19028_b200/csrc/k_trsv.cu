@@ -3,14 +3,15 @@
 //
 //   back   q = P^{-1} p  = D^{-1} (R~^{-1} p)      (Alg. 3 l.193)
 //   fwd    w = P^{-T} y  = R~^{-T} (D^{-1} y)      (Alg. 3 l.191, l.197)
-// Both are blocked column sweeps over 32-row blocks inside ONE CTA (the
-// n-vectors live in shared memory): a warp solves the 32x32 diagonal block
-// with the fp64 inverse of R~_kk (staged ahead by cp.async into shared
-// memory), then all warps apply the block to the remaining rows, streaming
-// 32-element row segments of R~ (back) or R~^T (fwd) from L2 in u_f and
-// upcasting on load.  Loads of the segments are issued before the diagonal
-// solve so their latency overlaps it.  Both right-hand sides of the batched
-// PCG (RHS a: -f, RHS b: x_k) are solved together.
+// Both are blocked solves over 32-row blocks inside ONE CTA per right-hand
+// side (the n-vector lives in shared memory), warp-specialised by block row
+// (trsv_ws below): each warp owns every kTW-th block row, accumulates its tile
+// updates as soon as the mbarrier of the needed solution block fires, and
+// solves its diagonal block with the fp64 inverse of R~_kk (staged by cp.async)
+// — so only one tile update and one 32 x 32 solve per block row are on the
+// critical path.  Tiles of R~ (back) or R~^T (fwd) are streamed from L2 in u_f
+// and upcast on load.  The two right-hand sides of a batched PCG step (RHS a:
+// -f, RHS b: x_k) run on two CTAs (two SMs) concurrently.
 //
 // The PCG recurrences of Alg. 3 (delta, alpha, omega, s, eta, beta, p;
 // PAPER.md l.191-201 with the A-in-loop operator of l.324, reading R1) are
@@ -67,357 +68,346 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Warp 0 stages the 32x32 fp64 inverse block `src` (8 KB) into `dst` (smem).
-__device__ __forceinline__ void stage_dinv(double* dst, const double* src) {
+// ---------------------------------------------------------------- warp-specialised blocked TRSV
+// One CTA (kTW warps) solves one right-hand side.  The npad x npad triangle is
+// cut into NB = npad/32 block rows, numbered u = 0..NB-1 in SOLVE order
+// (back substitution: real block NB-1-u; forward: real block u).  Warp w owns the
+// blocks u = w (mod kTW).  For each owned block, in ascending u, the warp
+// accumulates acc = sum_{u' < u} M_{u,u'} x_{u'} over the 32 x 32 tiles of its
+// block row, waiting on the mbarrier of x_{u'} before each tile, then solves
+// x_u = D_u (y_u - acc) with the fp64 inverse D_u of the diagonal block (staged in
+// the warp's shared-memory slot by cp.async while the warp accumulates) and
+// publishes x_u (smem + mbarrier arrive).  Tile rows of R~ (u_f, 32 values per
+// lane) are loaded from L2 through a register FIFO of depth TileDP ahead of use,
+// so the loads overlap the wait for x.  The critical path per block row is one
+// tile update plus one 32 x 32 solve; the other tile updates of all warps run
+// concurrently with it.
+constexpr int kTW = 16;  // warps of a TRSV CTA
+
+template <typename T> struct TileDP { static constexpr int v = SegTraits<T>::NV <= 4 ? 4 : (SegTraits<T>::NV <= 8 ? 2 : 1); };
+
+struct TrsvSm {
+  uint32_t phase; // parity of the barrier phase the next solve completes (one phase per solve)
+  double* y;      // [npad] right-hand side in, solution out (in place)
+  double* D;      // [kTW][1024] per-warp slot for the inverse of the diagonal block
+  double* ys;     // [kTW][32] per-warp scratch of the block solve
+  uint64_t* bar;  // [NB] x_u published
+  double* red;    // [32] block_sum scratch
+};
+// dynamic smem of a TRSV CTA
+static size_t trsv_smem(int npad) {
+  return (size_t)npad * 8 + (size_t)kTW * 1024 * 8 + (size_t)kTW * 32 * 8 + (size_t)(npad / 32) * 8 + 32 * 8;
+}
+__device__ __forceinline__ TrsvSm trsv_carve(int npad) {
+  extern __shared__ __align__(16) double tsm[];
+  TrsvSm s;
+  s.phase = 0;
+  s.y = tsm;
+  s.D = s.y + npad;
+  s.ys = s.D + kTW * 1024;
+  s.red = s.ys + kTW * 32;
+  s.bar = reinterpret_cast<uint64_t*>(s.red + 32);
+  return s;
+}
+
+// Initialise the block barriers once per kernel (they are never re-initialised:
+// each solve completes exactly one phase of every barrier).  All threads call it.
+__device__ __forceinline__ void trsv_init(const TrsvSm& sm, int npad) {
+  for (int i = threadIdx.x; i < (npad >> 5); i += blockDim.x) mbar_init(&sm.bar[i], 1);
+  __syncthreads();
+}
+
+__device__ __forceinline__ void stage_dinv_warp(double* dst, const double* src) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int k = 0; k < 16; ++k) cp_async16(dst + (k * 32 + lane) * 2, src + (k * 32 + lane) * 2);
   cp_async_commit();
 }
 
-// Row-block update y[r][i] -= sum_l M[i][c0+l] x_r[l] (x_r = y[r][c0..c0+31]) for the
-// rows i = i0 + tid + k*kTT (k < MAXR) with lo <= i < hi.  For 16-bit u_f the
-// 32-value row segments are loaded before the diagonal solve (PF, latency
-// overlap); wide types load them in the loop.
-template <typename T, int NRHS, int MAXR>
-struct RowUpd {
-  static constexpr int NV = SegTraits<T>::NV;
-  static constexpr bool PF = MAXR * NV <= 16;
-  uint4 raw[PF ? MAXR : 1][NV];
-  __device__ __forceinline__ void prefetch(const T* __restrict__ M, int npad, int c0, int i0, int lo, int hi) {
-    if constexpr (PF) {
+// Element e of a 16-byte chunk of u_f values.
+template <typename T> __device__ __forceinline__ double chunk_get(const uint4& u, int e);
+template <> __device__ __forceinline__ double chunk_get<F16s>(const uint4& u, int e) {
+  // one F2F.F64.F16 (half-register select), no fp32 step
+  const uint32_t w = (e >> 1) == 0 ? u.x : (e >> 1) == 1 ? u.y : (e >> 1) == 2 ? u.z : u.w;
+  const uint16_t h = (e & 1) ? (uint16_t)(w >> 16) : (uint16_t)(w & 0xffff);
+  double d;
+  asm("cvt.f64.f16 %0, %1;" : "=d"(d) : "h"(h));
+  return d;
+}
+template <> __device__ __forceinline__ double chunk_get<B16s>(const uint4& u, int e) {
+  const uint32_t w = (e >> 1) == 0 ? u.x : (e >> 1) == 1 ? u.y : (e >> 1) == 2 ? u.z : u.w;
+  return (double)__uint_as_float((e & 1) ? (w & 0xffff0000u) : (w << 16));
+}
+template <> __device__ __forceinline__ double chunk_get<float>(const uint4& u, int e) {
+  return (double)__uint_as_float(e == 0 ? u.x : e == 1 ? u.y : e == 2 ? u.z : u.w);
+}
+template <> __device__ __forceinline__ double chunk_get<double>(const uint4& u, int e) {
+  return e ? __hiloint2double((int)u.w, (int)u.z) : __hiloint2double((int)u.y, (int)u.x);
+}
+
+// BACK: solve R~ x = y with M = Rrow (upper), Dinv = DinvB.
+// !BACK: solve R~^T x = y with M = RTrow (lower), Dinv = DinvF.
+// Tile loads are coalesced: load k of a tile brings RPI = 32/CPR whole 32-value row
+// segments (lane group g = lane/CPR reads row k*RPI + g, 16-byte chunk lane%CPR), so
+// each lane accumulates, per k, a partial dot product over its chunk's columns; the
+// partials of a row are combined across its CPR lanes only when the block is solved.
+// All threads of the CTA must call it (after trsv_init); ends with __syncthreads().
+template <typename T, bool BACK>
+__device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv, int npad, TrsvSm& sm) {
+  constexpr int NV = SegTraits<T>::NV, DP = TileDP<T>::v;
+  constexpr int CPR = NV, RPI = 32 / CPR, EPC = 16 / (int)sizeof(T);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane / CPR, cpos = lane % CPR;
+  const int NB = npad >> 5;
+  const uint32_t ph = sm.phase;
+  __syncthreads();  // y is filled
+  if (warp < NB) {
+    double* Dw = sm.D + warp * 1024;
+    double* ysw = sm.ys + warp * 32;
+    auto real = [&](int u) { return BACK ? NB - 1 - u : u; };
+    auto issue = [&](int ui, int ci, uint4 (&raw)[NV]) {
+      const T* base = M + (size_t)(32 * real(ui) + grp) * npad + 32 * real(ci) + cpos * EPC;
 #pragma unroll
-      for (int k = 0; k < MAXR; ++k) {
-        const int i = i0 + (int)threadIdx.x + k * kTT;
-        if (i >= lo && i < hi) seg_load<T>(M + (size_t)i * npad + c0, raw[k]);
+      for (int k = 0; k < NV; ++k) raw[k] = __ldg(reinterpret_cast<const uint4*>(base + (size_t)k * RPI * npad));
+    };
+    int total = 0;
+    for (int u = warp; u < NB; u += kTW) total += u;
+    stage_dinv_warp(Dw, Dinv + (size_t)real(warp) * 1024);
+    int ui = warp, ci = 0;
+    if (ui == 0) ui += kTW;
+    uint4 raw[DP][NV];
+#pragma unroll
+    for (int s = 0; s < DP; ++s) {
+      if (s < total) {
+        issue(ui, ci, raw[s]);
+        if (++ci == ui) { ui += kTW; ci = 0; }
       }
     }
-  }
-  __device__ __forceinline__ void apply(const T* __restrict__ M, int npad, int c0, int i0, int lo, int hi, double* y) {
-    double s[MAXR][NRHS];
+    int uc = warp, cc = 0;
+    double acc[NV];
 #pragma unroll
-    for (int k = 0; k < MAXR; ++k)
+    for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+    auto solve = [&]() {
+      // row sums: combine the CPR chunk partials of each row, then move row i's sum to lane i
+      double mine = 0.0;
 #pragma unroll
-      for (int r = 0; r < NRHS; ++r) s[k][r] = 0.0;
-    if constexpr (PF) {
+      for (int k = 0; k < NV; ++k) {
+        double v = acc[k];
 #pragma unroll
-      for (int l = 0; l < 32; ++l) {
-        double xv[NRHS];
+        for (int o = CPR / 2; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const double t = __shfl_sync(0xffffffffu, v, (lane % RPI) * CPR);
+        if (k == lane / RPI) mine = t;
+        acc[k] = 0.0;
+      }
+      const int o = 32 * real(uc);
+      ysw[lane] = sm.y[o + lane] - mine;
+      cp_async_wait<0>();
+      __syncwarp();
+      double x0 = 0.0, x1 = 0.0;
 #pragma unroll
-        for (int r = 0; r < NRHS; ++r) xv[r] = y[r * npad + c0 + l];
+      for (int l = 0; l < 32; l += 2) {
+        x0 = fma(Dw[l * 32 + lane], ysw[l], x0);
+        x1 = fma(Dw[(l + 1) * 32 + lane], ysw[l + 1], x1);
+      }
+      sm.y[o + lane] = x0 + x1;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.bar[uc]);
+      uc += kTW;
+      cc = 0;
+      if (uc < NB) stage_dinv_warp(Dw, Dinv + (size_t)real(uc) * 1024);
+    };
+    if (uc == 0) solve();
+    for (int kb = 0; kb < total; kb += DP) {
 #pragma unroll
-        for (int k = 0; k < MAXR; ++k) {
-          const int i = i0 + (int)threadIdx.x + k * kTT;
-          if (i >= lo && i < hi) {
-            const double a = seg_get<T>(raw[k], l);
+      for (int s = 0; s < DP; ++s) {
+        if (kb + s < total) {
+          mbar_wait_spin(&sm.bar[cc], ph);
+          double xv[EPC];
+          const double2* xp = reinterpret_cast<const double2*>(sm.y + 32 * real(cc) + cpos * EPC);
 #pragma unroll
-            for (int r = 0; r < NRHS; ++r) s[k][r] = fma(a, xv[r], s[k][r]);
+          for (int e = 0; e < EPC; e += 2) {
+            const double2 t = xp[e >> 1];
+            xv[e] = t.x;
+            xv[e + 1] = t.y;
           }
+#pragma unroll
+          for (int k = 0; k < NV; ++k)
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) acc[k] = fma(chunk_get<T>(raw[s][k], e), xv[e], acc[k]);
+          if (kb + s + DP < total) {
+            issue(ui, ci, raw[s]);
+            if (++ci == ui) { ui += kTW; ci = 0; }
+          }
+          if (++cc == uc) solve();
         }
       }
-    } else {
-#pragma unroll 1
-      for (int k = 0; k < MAXR; ++k) {
-        const int i = i0 + (int)threadIdx.x + k * kTT;
-        if (i >= lo && i < hi) {
-          seg_load<T>(M + (size_t)i * npad + c0, raw[0]);
-#pragma unroll
-          for (int l = 0; l < 32; ++l) {
-            const double a = seg_get<T>(raw[0], l);
-#pragma unroll
-            for (int r = 0; r < NRHS; ++r) s[k][r] = fma(a, y[r * npad + c0 + l], s[k][r]);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < MAXR; ++k) {
-      const int i = i0 + (int)threadIdx.x + k * kTT;
-      if (i >= lo && i < hi) {
-#pragma unroll
-        for (int r = 0; r < NRHS; ++r) y[r * npad + i] -= s[k][r];
-      }
     }
   }
-};
-
-// Warp 0: x_blk = D x_blk with the staged 32x32 block, D[l][lane] layout.
-template <int NRHS>
-__device__ __forceinline__ void diag_block(const double* D, int npad, int c0, double* y) {
-  const int lane = threadIdx.x & 31;
-  double acc[NRHS];
-#pragma unroll
-  for (int r = 0; r < NRHS; ++r) acc[r] = 0.0;
-#pragma unroll 8
-  for (int l = 0; l < 32; ++l) {
-    const double dv = D[l * 32 + lane];
-#pragma unroll
-    for (int r = 0; r < NRHS; ++r) acc[r] = fma(dv, y[r * npad + c0 + l], acc[r]);
-  }
-  __syncwarp();
-#pragma unroll
-  for (int r = 0; r < NRHS; ++r) y[r * npad + c0 + lane] = acc[r];
-}
-
-// y: smem [NRHS][npad].  Solves R~ x = y (upper, back substitution) in place.
-// Rrow: R~ row-major; DinvB[kb][l][i] = (R~_kk^{-1})[i][l].  dbuf: smem 2 x 1024 doubles.
-template <typename T, int NRHS, int MAXR>
-__device__ void trsv_back(const T* __restrict__ Rrow, const double* __restrict__ DinvB, int npad, double* y,
-                          double* dbuf) {
-  const int warp = threadIdx.x >> 5;
-  const int NB = npad >> 5;
-  if (warp == 0) stage_dinv(dbuf + ((NB - 1) & 1) * 1024, DinvB + (size_t)(NB - 1) * 1024);
-  for (int jb = NB - 1; jb >= 0; --jb) {
-    const int c0 = jb * 32;
-    RowUpd<T, NRHS, MAXR> upd;
-    upd.prefetch(Rrow, npad, c0, 0, 0, c0);       // rows i < c0
-    if (warp == 0) {
-      if (jb > 0) {
-        stage_dinv(dbuf + ((jb - 1) & 1) * 1024, DinvB + (size_t)(jb - 1) * 1024);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      __syncwarp();
-      diag_block<NRHS>(dbuf + (jb & 1) * 1024, npad, c0, y);
-    }
-    __syncthreads();
-    if (c0 > 0) upd.apply(Rrow, npad, c0, 0, 0, c0, y);
-    __syncthreads();
-  }
-}
-
-// Solves R~^T x = y (lower, forward substitution) in place.
-// RTrow: R~^T row-major; DinvF[kb][l][i] = (R~_kk^{-1})[l][i].
-template <typename T, int NRHS, int MAXR>
-__device__ void trsv_fwd(const T* __restrict__ RTrow, const double* __restrict__ DinvF, int npad, double* y,
-                         double* dbuf) {
-  const int warp = threadIdx.x >> 5;
-  const int NB = npad >> 5;
-  if (warp == 0) stage_dinv(dbuf, DinvF);
-  for (int jb = 0; jb < NB; ++jb) {
-    const int c0 = jb * 32, c1 = c0 + 32;
-    RowUpd<T, NRHS, MAXR> upd;
-    upd.prefetch(RTrow, npad, c0, c1, c1, npad);  // rows i >= c1
-    if (warp == 0) {
-      if (jb + 1 < NB) {
-        stage_dinv(dbuf + ((jb + 1) & 1) * 1024, DinvF + (size_t)(jb + 1) * 1024);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      __syncwarp();
-      diag_block<NRHS>(dbuf + (jb & 1) * 1024, npad, c0, y);
-    }
-    __syncthreads();
-    if (c1 < npad) upd.apply(RTrow, npad, c0, c1, c1, npad, y);
-    __syncthreads();
-  }
-}
-
-// dynamic smem of the single-CTA kernels: y [2][npad] + dbuf [2][1024] + red [32]
-static size_t vec_smem(int npad) { return (size_t)(2 * npad + 2048 + 32) * 8; }
-
-struct VecSmem {
-  double* y;
-  double* dbuf;
-  double* red;
-};
-__device__ __forceinline__ VecSmem carve(int npad) {
-  extern __shared__ __align__(16) double vsm[];
-  return VecSmem{vsm, vsm + 2 * npad, vsm + 2 * npad + 2048};
+  sm.phase ^= 1u;
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------- plain apply (API / tests)
-template <typename T, int NRHS, int MAXR>
-__global__ void __launch_bounds__(kTT) k_precond_apply(PrecondDev pc, int trans, double* __restrict__ Y, int ldY) {
-  VecSmem sm = carve(pc.npad);
-  const int n = pc.n, npad = pc.npad;
-  for (int r = 0; r < NRHS; ++r)
-    for (int i = threadIdx.x; i < npad; i += kTT) {
-      double v = i < n ? Y[(size_t)r * ldY + i] : 0.0;
-      if (trans) v *= pc.dinv[i];
-      sm.y[r * npad + i] = v;
-    }
-  __syncthreads();
-  if (trans) trsv_fwd<T, NRHS, MAXR>((const T*)pc.RTrow, pc.DinvF, npad, sm.y, sm.dbuf);
-  else trsv_back<T, NRHS, MAXR>((const T*)pc.Rrow, pc.DinvB, npad, sm.y, sm.dbuf);
-  for (int r = 0; r < NRHS; ++r)
-    for (int i = threadIdx.x; i < n; i += kTT) {
-      double v = sm.y[r * npad + i];
-      if (!trans) v *= pc.dinv[i];
-      Y[(size_t)r * ldY + i] = v;
-    }
+// One CTA per right-hand side r (blockIdx.x).
+template <typename T>
+__global__ void __launch_bounds__(kTW * 32) k_precond_apply(PrecondDev pc, int trans, double* __restrict__ Y, int ldY) {
+  TrsvSm sm = trsv_carve(pc.npad);
+  trsv_init(sm, pc.npad);
+  const int n = pc.n, npad = pc.npad, r = blockIdx.x;
+  for (int i = threadIdx.x; i < npad; i += blockDim.x) {
+    double v = i < n ? Y[(size_t)r * ldY + i] : 0.0;
+    if (trans) v *= pc.dinv[i];
+    sm.y[i] = v;
+  }
+  if (trans) trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, npad, sm);
+  else trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, npad, sm);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double v = sm.y[i];
+    if (!trans) v *= pc.dinv[i];
+    Y[(size_t)r * ldY + i] = v;
+  }
 }
 
 // ---------------------------------------------------------------- PCGTLS (Alg. 3)
-// Vectors in global memory have stride n (q feeds the pass over A directly).
-template <typename T, int MAXR>
-__global__ void __launch_bounds__(kTT) k_pcg_init(PrecondDev pc, int nrhs, PcgVecs v, PcgState* __restrict__ S) {
-  VecSmem sm = carve(pc.npad);
-  const int n = pc.n, npad = pc.npad, tid = threadIdx.x;
-  // l.191: s_0 = p_0 = P^{-T} f, eta_0 = ||s_0||^2, omega_0 = 0
-  for (int r = 0; r < 2; ++r)
-    for (int i = tid; i < npad; i += kTT)
-      sm.y[r * npad + i] = (r < nrhs && i < n) ? v.rhs[(size_t)r * n + i] * pc.dinv[i] : 0.0;
-  __syncthreads();
-  trsv_fwd<T, 2, MAXR>((const T*)pc.RTrow, pc.DinvF, npad, sm.y, sm.dbuf);
-  double eta[2];
-  for (int r = 0; r < 2; ++r) {
-    double e = 0.0;
-    for (int i = tid; i < n; i += kTT) {
-      const double s = sm.y[r * npad + i];
-      v.s[(size_t)r * n + i] = s;
-      v.p[(size_t)r * n + i] = s;
-      v.omega[(size_t)r * n + i] = 0.0;
-      e = fma(s, s, e);
-    }
-    eta[r] = block_sum(e, sm.red);
-  }
-  // first q = P^{-1} p (l.193)
-  trsv_back<T, 2, MAXR>((const T*)pc.Rrow, pc.DinvB, npad, sm.y, sm.dbuf);
-  double qq[2];
-  for (int r = 0; r < 2; ++r) {
-    double e = 0.0;
-    for (int i = tid; i < n; i += kTT) {
-      const double q = sm.y[r * npad + i] * pc.dinv[i];
-      v.q[(size_t)r * n + i] = q;
-      e = fma(q, q, e);
-    }
-    qq[r] = block_sum(e, sm.red);
-  }
-  if (tid == 0) {
-    int any = 0;
-    for (int r = 0; r < 2; ++r) {
-      const bool on = r < nrhs && eta[r] > 0.0;
-      S->eta[r] = eta[r];
-      S->eta0[r] = eta[r];
-      S->qq[r] = qq[r];
+// One CTA per right-hand side r = blockIdx.x (the two solves of an RQI step are
+// independent until the RQI update).  Vectors in global memory have stride n
+// (q feeds the pass over A directly).
+template <typename T>
+__global__ void __launch_bounds__(kTW * 32) k_pcg_init(PrecondDev pc, int nrhs, PcgVecs v, PcgState* __restrict__ S) {
+  TrsvSm sm = trsv_carve(pc.npad);
+  trsv_init(sm, pc.npad);
+  const int n = pc.n, npad = pc.npad, tid = threadIdx.x, r = blockIdx.x;
+  if (r >= nrhs) {                 // the unused RHS slot of a 1-RHS solve
+    if (tid == 0) {
+      S->active[r] = 0; S->count[r] = 0; S->brk[r] = 0; S->brk_j[r] = -1; S->iter[r] = 0;
+      S->eta[r] = S->eta0[r] = S->qq[r] = 0.0;
       S->delta_min[r] = __longlong_as_double(0x7ff0000000000000ll);
-      S->active[r] = on;
-      S->count[r] = 0;
-      S->brk[r] = 0;
-      S->brk_j[r] = -1;
-      any |= on;
     }
-    S->any_active = any;
-    S->nrhs = nrhs;
-    S->iter = 0;
+    return;
+  }
+  const size_t off = (size_t)r * n;
+  // l.191: s_0 = p_0 = P^{-T} f, eta_0 = ||s_0||^2, omega_0 = 0
+  for (int i = tid; i < npad; i += blockDim.x) sm.y[i] = i < n ? v.rhs[off + i] * pc.dinv[i] : 0.0;
+  trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, npad, sm);
+  double e = 0.0;
+  for (int i = tid; i < n; i += blockDim.x) {
+    const double s = sm.y[i];
+    v.s[off + i] = s;
+    v.p[off + i] = s;
+    v.omega[off + i] = 0.0;
+    e = fma(s, s, e);
+  }
+  const double eta = block_sum(e, sm.red);
+  // first q = P^{-1} p (l.193)
+  trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, npad, sm);
+  e = 0.0;
+  for (int i = tid; i < n; i += blockDim.x) {
+    const double q = sm.y[i] * pc.dinv[i];
+    v.q[off + i] = q;
+    e = fma(q, q, e);
+  }
+  const double qq = block_sum(e, sm.red);
+  if (tid == 0) {
+    S->eta[r] = eta;
+    S->eta0[r] = eta;
+    S->qq[r] = qq;
+    S->delta_min[r] = __longlong_as_double(0x7ff0000000000000ll);
+    S->active[r] = eta > 0.0;
+    S->count[r] = 0;
+    S->brk[r] = 0;
+    S->brk_j[r] = -1;
+    S->iter[r] = 0;
   }
 }
 
-// One PCGTLS iteration after the pass t = A q_r, v_r = A^T t_r, tau_r = t_r^T t_r
-// (passout = [v_0 .. v_{nrhs-1} (stride n), tau_0, tau_1]).
-template <typename T, int MAXR>
-__global__ void __launch_bounds__(kTT) k_pcg_step(PrecondDev pc, PcgVecs v, const double* __restrict__ passout,
-                                                   PcgState* __restrict__ S, int rule, int next_q) {
-  __shared__ double s_alpha[2], s_beta[2];
-  __shared__ int s_upd[2], s_cont[2];
-  if (S->any_active == 0) return;
-  VecSmem sm = carve(pc.npad);
+// One PCGTLS iteration of RHS r = blockIdx.x after the pass t = A q_r,
+// v_r = A^T t_r, tau_r = t_r^T t_r (passout = [v_0 .. v_{nrhs-1} (stride n), tau_0, tau_1]).
+template <typename T>
+__global__ void __launch_bounds__(kTW * 32) k_pcg_step(PrecondDev pc, PcgVecs v, const double* __restrict__ passout,
+                                                       PcgState* __restrict__ S, int nrhs, int rule, int next_q) {
+  __shared__ double s_alpha, s_beta;
+  __shared__ int s_upd, s_cont;
+  const int r = blockIdx.x;
+  if (r >= nrhs || S->active[r] == 0) return;
+  TrsvSm sm = trsv_carve(pc.npad);
+  trsv_init(sm, pc.npad);
   const int n = pc.n, npad = pc.npad, tid = threadIdx.x;
-  const int nrhs = S->nrhs;
+  const size_t off = (size_t)r * n;
   const double sig2 = S->sigma2;
   if (tid == 0) {
-    for (int r = 0; r < 2; ++r) {
-      s_upd[r] = 0;
-      s_alpha[r] = 0.0;
-      if (r >= nrhs || !S->active[r]) continue;
-      const double tau = passout[(size_t)nrhs * n + r];
-      const double delta = tau - sig2 * S->qq[r];          // l.194 with the operator of l.324
-      S->delta_min[r] = fmin(S->delta_min[r], delta);
-      if (!isfinite(delta) || delta == 0.0) {               // loop guard l.192 (R3)
-        S->active[r] = 0;
-      } else if (delta < 0.0 && rule == 0) {                // breakdown (R3)
-        S->active[r] = 0;
-        S->brk[r] = 1;
-        S->brk_j[r] = S->iter;
-      } else {
-        s_alpha[r] = S->eta[r] / delta;                     // l.195
-        s_upd[r] = 1;
-      }
+    s_upd = 0;
+    s_alpha = 0.0;
+    const double tau = passout[(size_t)nrhs * n + r];
+    const double delta = tau - sig2 * S->qq[r];            // l.194 with the operator of l.324
+    S->delta_min[r] = fmin(S->delta_min[r], delta);
+    if (!isfinite(delta) || delta == 0.0) {                 // loop guard l.192 (R3)
+      S->active[r] = 0;
+    } else if (delta < 0.0 && rule == 0) {                  // breakdown (R3)
+      S->active[r] = 0;
+      S->brk[r] = 1;
+      S->brk_j[r] = S->iter[r];
+    } else {
+      s_alpha = S->eta[r] / delta;                          // l.195
+      s_upd = 1;
     }
   }
   __syncthreads();
+  if (!s_upd) return;
+  const double al = s_alpha;
   // omega += alpha q (l.196); y = D^{-1}(A^T t - sigma^2 q) for w = P^{-T}(...) (R1)
-  for (int r = 0; r < 2; ++r) {
-    const bool u = s_upd[r];
-    const double al = s_alpha[r];
-    for (int i = tid; i < npad; i += kTT) {
-      double yv = 0.0;
-      if (u && i < n) {
-        const double q = v.q[(size_t)r * n + i];
-        v.omega[(size_t)r * n + i] = fma(al, q, v.omega[(size_t)r * n + i]);
-        yv = (passout[(size_t)r * n + i] - sig2 * q) * pc.dinv[i];
-      }
-      sm.y[r * npad + i] = yv;
+  for (int i = tid; i < npad; i += blockDim.x) {
+    double yv = 0.0;
+    if (i < n) {
+      const double q = v.q[off + i];
+      v.omega[off + i] = fma(al, q, v.omega[off + i]);
+      yv = (passout[off + i] - sig2 * q) * pc.dinv[i];
     }
+    sm.y[i] = yv;
   }
-  __syncthreads();
-  trsv_fwd<T, 2, MAXR>((const T*)pc.RTrow, pc.DinvF, npad, sm.y, sm.dbuf);
+  trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, npad, sm);
   // s -= alpha w (l.198), eta' = ||s||^2 (l.199)
-  double etan[2];
-  for (int r = 0; r < 2; ++r) {
-    double e = 0.0;
-    if (s_upd[r]) {
-      const double al = s_alpha[r];
-      for (int i = tid; i < n; i += kTT) {
-        const double s = fma(-al, sm.y[r * npad + i], v.s[(size_t)r * n + i]);
-        v.s[(size_t)r * n + i] = s;
-        e = fma(s, s, e);
-      }
-    }
-    etan[r] = block_sum(e, sm.red);
+  double e = 0.0;
+  for (int i = tid; i < n; i += blockDim.x) {
+    const double s = fma(-al, sm.y[i], v.s[off + i]);
+    v.s[off + i] = s;
+    e = fma(s, s, e);
   }
+  const double etan = block_sum(e, sm.red);
   if (tid == 0) {
-    for (int r = 0; r < 2; ++r) {
-      s_cont[r] = 0;
-      if (!s_upd[r]) continue;
-      S->count[r] += 1;
-      if (etan[r] <= S->tol2 * S->eta0[r]) {                // early exit (R3)
-        S->active[r] = 0;
-      } else {
-        s_beta[r] = etan[r] / S->eta[r];                    // l.200
-        S->eta[r] = etan[r];
-        s_cont[r] = 1;
-      }
+    s_cont = 0;
+    S->count[r] += 1;
+    S->iter[r] += 1;
+    if (etan <= S->tol2 * S->eta0[r]) {                     // early exit (R3)
+      S->active[r] = 0;
+    } else {
+      s_beta = etan / S->eta[r];                            // l.200
+      S->eta[r] = etan;
+      s_cont = 1;
     }
-    S->iter += 1;
-    S->any_active = (S->active[0] != 0) | (S->active[1] != 0);
   }
   __syncthreads();
+  if (!s_cont) return;
   // p = s + beta p (l.201)
-  for (int r = 0; r < 2; ++r) {
-    const bool c = s_cont[r];
-    const double be = s_beta[r];
-    for (int i = tid; i < npad; i += kTT) {
-      double pv = 0.0;
-      if (c && i < n) {
-        pv = fma(be, v.p[(size_t)r * n + i], v.s[(size_t)r * n + i]);
-        v.p[(size_t)r * n + i] = pv;
-      }
-      sm.y[r * npad + i] = pv;
+  const double be = s_beta;
+  for (int i = tid; i < npad; i += blockDim.x) {
+    double pv = 0.0;
+    if (i < n) {
+      pv = fma(be, v.p[off + i], v.s[off + i]);
+      v.p[off + i] = pv;
     }
+    sm.y[i] = pv;
   }
-  if (!next_q || !(s_cont[0] || s_cont[1])) return;
-  __syncthreads();
+  if (!next_q) return;
   // next q = P^{-1} p (l.193 of the next iteration)
-  trsv_back<T, 2, MAXR>((const T*)pc.Rrow, pc.DinvB, npad, sm.y, sm.dbuf);
-  double qq[2];
-  for (int r = 0; r < 2; ++r) {
-    double e = 0.0;
-    if (s_cont[r]) {
-      for (int i = tid; i < n; i += kTT) {
-        const double q = sm.y[r * npad + i] * pc.dinv[i];
-        v.q[(size_t)r * n + i] = q;
-        e = fma(q, q, e);
-      }
-    }
-    qq[r] = block_sum(e, sm.red);
+  trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, npad, sm);
+  e = 0.0;
+  for (int i = tid; i < n; i += blockDim.x) {
+    const double q = sm.y[i] * pc.dinv[i];
+    v.q[off + i] = q;
+    e = fma(q, q, e);
   }
-  if (tid == 0)
-    for (int r = 0; r < 2; ++r)
-      if (s_cont[r]) S->qq[r] = qq[r];
+  const double qq = block_sum(e, sm.red);
+  if (tid == 0) S->qq[r] = qq;
 }
 
 // ---------------------------------------------------------------- RQI (Alg. 4)
@@ -471,22 +461,23 @@ __global__ void __launch_bounds__(kTT) k_rqi_update(int n, PcgVecs v, const PcgS
 }
 
 // l.227-235: sigma_0^2 = r_0^T r_0/(1 + x_0^T x_0); u_0 = P^{-1} P^{-T} x_0 (R9); x_1 = x_0 + sigma_0^2 u_0.
-template <typename T, int MAXR>
-__global__ void __launch_bounds__(kTT) k_boot_x1(PrecondDev pc, const double* __restrict__ passout,
-                                                  const double* __restrict__ x0, double* __restrict__ x1) {
-  VecSmem sm = carve(pc.npad);
+template <typename T>
+__global__ void __launch_bounds__(kTW * 32) k_boot_x1(PrecondDev pc, const double* __restrict__ passout,
+                                                      const double* __restrict__ x0, double* __restrict__ x1) {
+  TrsvSm sm = trsv_carve(pc.npad);
+  trsv_init(sm, pc.npad);
   const int n = pc.n, npad = pc.npad, tid = threadIdx.x;
   double e = 0.0;
-  for (int i = tid; i < npad; i += kTT) {
+  for (int i = tid; i < npad; i += blockDim.x) {
     const double xv = i < n ? x0[i] : 0.0;
     e = fma(xv, xv, e);
     sm.y[i] = i < n ? xv * pc.dinv[i] : 0.0;
   }
   const double xx = block_sum(e, sm.red);
   const double sig0 = passout[n] / (1.0 + xx);
-  trsv_fwd<T, 1, MAXR>((const T*)pc.RTrow, pc.DinvF, npad, sm.y, sm.dbuf);
-  trsv_back<T, 1, MAXR>((const T*)pc.Rrow, pc.DinvB, npad, sm.y, sm.dbuf);
-  for (int i = tid; i < n; i += kTT) x1[i] = fma(sig0, sm.y[i] * pc.dinv[i], x0[i]);
+  trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, npad, sm);
+  trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, npad, sm);
+  for (int i = tid; i < n; i += blockDim.x) x1[i] = fma(sig0, sm.y[i] * pc.dinv[i], x0[i]);
 }
 
 // ---------------------------------------------------------------- launchers
@@ -495,15 +486,6 @@ static int set_smem(F kern, size_t bytes) {
   TLS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   return 0;
 }
-
-#define TLS_DISPATCH_MAXR(npad, ...)                                   \
-  do {                                                                 \
-    const int _rows = ((npad) + kTT - 1) / kTT;                        \
-    if (_rows <= 1) { constexpr int MAXR = 1; __VA_ARGS__; }           \
-    else if (_rows <= 2) { constexpr int MAXR = 2; __VA_ARGS__; }      \
-    else if (_rows <= 4) { constexpr int MAXR = 4; __VA_ARGS__; }      \
-    else { constexpr int MAXR = 8; __VA_ARGS__; }                      \
-  } while (0)
 
 #define TLS_DISPATCH_UF(uf, ...)                          \
   switch (uf) {                                           \
@@ -514,40 +496,35 @@ static int set_smem(F kern, size_t bytes) {
   }
 
 int launch_precond_apply(const PrecondDev& pc, int trans, int nrhs, double* Y, int ldY, cudaStream_t st) {
-  const size_t sm = vec_smem(pc.npad);
+  const size_t sm = trsv_smem(pc.npad);
   int rc = 0;
-  TLS_DISPATCH_UF(pc.u_f, TLS_DISPATCH_MAXR(pc.npad, {
-    if (nrhs == 1) {
-      if ((rc = set_smem(k_precond_apply<T, 1, MAXR>, sm))) return rc;
-      k_precond_apply<T, 1, MAXR><<<1, kTT, sm, st>>>(pc, trans, Y, ldY);
-    } else {
-      if ((rc = set_smem(k_precond_apply<T, 2, MAXR>, sm))) return rc;
-      k_precond_apply<T, 2, MAXR><<<1, kTT, sm, st>>>(pc, trans, Y, ldY);
-    }
-  }));
+  TLS_DISPATCH_UF(pc.u_f, {
+    if ((rc = set_smem(k_precond_apply<T>, sm))) return rc;
+    k_precond_apply<T><<<nrhs, kTW * 32, sm, st>>>(pc, trans, Y, ldY);
+  });
   TLS_LAUNCH_CHECK();
   return 0;
 }
 
 int launch_pcg_init(const PrecondDev& pc, int nrhs, PcgVecs v, PcgState* S, cudaStream_t st) {
-  const size_t sm = vec_smem(pc.npad);
+  const size_t sm = trsv_smem(pc.npad);
   int rc = 0;
-  TLS_DISPATCH_UF(pc.u_f, TLS_DISPATCH_MAXR(pc.npad, {
-    if ((rc = set_smem(k_pcg_init<T, MAXR>, sm))) return rc;
-    k_pcg_init<T, MAXR><<<1, kTT, sm, st>>>(pc, nrhs, v, S);
-  }));
+  TLS_DISPATCH_UF(pc.u_f, {
+    if ((rc = set_smem(k_pcg_init<T>, sm))) return rc;
+    k_pcg_init<T><<<2, kTW * 32, sm, st>>>(pc, nrhs, v, S);
+  });
   TLS_LAUNCH_CHECK();
   return 0;
 }
 
-int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgState* S, int rule, int next_q,
-                    cudaStream_t st) {
-  const size_t sm = vec_smem(pc.npad);
+int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgState* S, int nrhs, int rule,
+                    int next_q, cudaStream_t st) {
+  const size_t sm = trsv_smem(pc.npad);
   int rc = 0;
-  TLS_DISPATCH_UF(pc.u_f, TLS_DISPATCH_MAXR(pc.npad, {
-    if ((rc = set_smem(k_pcg_step<T, MAXR>, sm))) return rc;
-    k_pcg_step<T, MAXR><<<1, kTT, sm, st>>>(pc, v, passout, S, rule, next_q);
-  }));
+  TLS_DISPATCH_UF(pc.u_f, {
+    if ((rc = set_smem(k_pcg_step<T>, sm))) return rc;
+    k_pcg_step<T><<<nrhs, kTW * 32, sm, st>>>(pc, v, passout, S, nrhs, rule, next_q);
+  });
   TLS_LAUNCH_CHECK();
   return 0;
 }
@@ -567,12 +544,12 @@ int launch_rqi_update(const PrecondDev& pc, PcgVecs v, const PcgState* S, double
 }
 
 int launch_boot_x1(const PrecondDev& pc, const double* passout_r0, const double* x0, double* x1, cudaStream_t st) {
-  const size_t sm = vec_smem(pc.npad);
+  const size_t sm = trsv_smem(pc.npad);
   int rc = 0;
-  TLS_DISPATCH_UF(pc.u_f, TLS_DISPATCH_MAXR(pc.npad, {
-    if ((rc = set_smem(k_boot_x1<T, MAXR>, sm))) return rc;
-    k_boot_x1<T, MAXR><<<1, kTT, sm, st>>>(pc, passout_r0, x0, x1);
-  }));
+  TLS_DISPATCH_UF(pc.u_f, {
+    if ((rc = set_smem(k_boot_x1<T>, sm))) return rc;
+    k_boot_x1<T><<<1, kTW * 32, sm, st>>>(pc, passout_r0, x0, x1);
+  });
   TLS_LAUNCH_CHECK();
   return 0;
 }

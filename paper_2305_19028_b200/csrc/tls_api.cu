@@ -716,20 +716,20 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
     return 0;
   };
   // PCG iterations j = 0..budget-1 with device-side predication; with a large
-  // budget the host polls any_active every 8 iterations.
+  // budget the host polls the activity flags every 8 iterations.
   auto pcg_loop = [&](int nrhs, int budget) -> int {
     for (int j = 0; j < budget; ++j) {
-      TLS_TRY(run_pass(cx, dv, PASS_OPERATOR, nrhs, w.vec.q, nullptr, w, &w.S->any_active));
+      TLS_TRY(run_pass(cx, dv, PASS_OPERATOR, nrhs, w.vec.q, nullptr, w, w.S->active));
       {
         ProfScope ps(TLS_PROF_PCG_STEP, cx.st);
-        TLS_TRY(launch_pcg_step(pc, w.vec, w.passout, w.S, o.breakdown_rule, j + 1 < budget ? 1 : 0, cx.st));
+        TLS_TRY(launch_pcg_step(pc, w.vec, w.passout, w.S, nrhs, o.breakdown_rule, j + 1 < budget ? 1 : 0, cx.st));
       }
       cx.launches += 1;
       if (budget > 16 && (j % 8) == 7) {
-        int act = 0;
-        TLS_CUDA_TRY(cudaMemcpyAsync(&act, &w.S->any_active, sizeof(int), cudaMemcpyDeviceToHost, cx.st));
+        int act[2] = {0, 0};
+        TLS_CUDA_TRY(cudaMemcpyAsync(act, w.S->active, sizeof(act), cudaMemcpyDeviceToHost, cx.st));
         TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
-        if (!act) break;
+        if (!(act[0] | act[1])) break;
       }
     }
     return 0;

@@ -22,6 +22,7 @@ struct DenseView {
 int pass_grid(const DenseView& A);
 size_t pass_partials_doubles(const DenseView& A);
 // Writes gridDim x W partials; W = nrhs*n + 2 (operator/residual) or 2n (colstats).
+// `active` (may be NULL): int[2] of PCG activity flags; the kernel is a no-op when both are 0.
 int launch_pass(const DenseView& A, int mode, int nrhs, const double* q, const double* b,
                 double* partials, const int* active, cudaStream_t st, int* grid_out);
 // out[w] = sum_g partials[g][w] (max for w < nmax), fixed order.
@@ -66,10 +67,7 @@ struct PcgState {
   double eta[2], eta0[2], qq[2], delta_min[2];
   double sigma2, g, psi, xx, tol2;
   int active[2], count[2], brk[2], brk_j[2];
-  int any_active;
-  int nrhs;
-  int iter;       // iteration index j of the next step
-  int pad_;
+  int iter[2];    // iteration index j of the next step, per RHS
 };
 struct PcgVecs {  // device, each [2][npad]
   double *omega, *s, *p, *q, *rhs;
@@ -77,7 +75,8 @@ struct PcgVecs {  // device, each [2][npad]
 int launch_precond_apply(const PrecondDev& pc, int trans, int nrhs, double* Y, int ldY,
                          cudaStream_t st);
 int launch_pcg_init(const PrecondDev& pc, int nrhs, PcgVecs v, PcgState* S, cudaStream_t st);
-int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgState* S,
+// One CTA per RHS; an RHS whose active flag is 0 is left untouched.
+int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgState* S, int nrhs,
                     int breakdown_rule, int compute_next_q, cudaStream_t st);
 // step record: sigma2, f (stored as rhs0 = -f), g, psi; copies x into rhs1.
 int launch_rqi_eval(const PrecondDev& pc, const double* passout, const double* x, PcgVecs v,
