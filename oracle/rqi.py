@@ -68,14 +68,47 @@ def column_scaling(A):
 
 
 # ----------------------------------------------------------------------------- Gram
+def _gram_sparse(A, d: np.ndarray, u_f: str) -> np.ndarray:
+    """CSR A (reading R19): no tensor-core chunks on this path, so G = A^^T A^ with
+    A^ = fl_uf(A D^{-1}) is the exact sum of the exact u_f products, rounded ONCE
+    to fp64.  fp16: every A^ entry is an integer multiple of 2^-24 with |A^| < 2
+    (column scaling R2), so I = A^ 2^24 is an integer below 2^25; I = H 2^13 + L
+    (0 <= L < 2^13) keeps the three integer products H^T H, H^T L + L^T H, L^T L
+    exact in int64, and their exact combination is rounded by Python's
+    correctly rounded int -> float.  bf16/fp32/fp64: the products (exact for
+    bf16/fp32) summed in fp64 by scipy."""
+    A = scipy.sparse.csr_matrix(A)
+    Ah = A.copy()
+    Ah.data = round_to(A.data / d[A.indices], u_f)
+    if not np.all(np.isfinite(Ah.data)):
+        raise OverflowError("A D^-1 overflows u_f")
+    if u_f != "fp16":
+        return np.asarray((Ah.T @ Ah).todense())
+    scaled = Ah.data * 2.0 ** 24
+    I = scaled.astype(np.int64)
+    assert np.array_equal(I.astype(np.float64), scaled)         # exact integers
+    Hm, Lm = Ah.copy(), Ah.copy()
+    Hm.data, Lm.data = I >> 13, I & 8191
+    Hm = Hm.astype(np.int64)
+    Lm = Lm.astype(np.int64)
+    SA = np.asarray((Hm.T @ Hm).todense(), dtype=np.int64)
+    SB = np.asarray((Hm.T @ Lm + Lm.T @ Hm).todense(), dtype=np.int64)
+    SC = np.asarray((Lm.T @ Lm).todense(), dtype=np.int64)
+    T = SA.astype(object) * (1 << 26) + SB.astype(object) * (1 << 13) + SC.astype(object)
+    G = np.array([float(t) for t in T.ravel()], dtype=np.float64).reshape(T.shape)
+    return G * 2.0 ** -48
+
+
 def gram_uf(A, d: np.ndarray, u_f: str, K_t: int = 64) -> np.ndarray:
-    """G = sum over chunks c of K_t consecutive rows (in order) of
+    """Dense A:  G = sum over chunks c of K_t consecutive rows (in order) of
     fp64( fl32-accumulated  A^_c^T A^_c ),  A^ = fl_uf(A D^{-1})   (R10, R11).
 
     u_f in {fp16, bf16}: the products of u_f values are exact in fp32 and each
     chunk is summed in fp32 (a float32 matmul), as the tensor cores accumulate
     in fp32; chunks are added in fp64.  u_f = fp32: A^ in fp32, G formed in
     fp64.  u_f = fp64: G = (A D^{-1})^T (A D^{-1}) in fp64 (control)."""
+    if _is_sparse(A):
+        return _gram_sparse(A, d, u_f)
     m, n = A.shape
     G = np.zeros((n, n))
     for c0 in range(0, m, K_t):

@@ -42,7 +42,7 @@ typedef struct ncclComm* ncclComm_t;
 typedef struct { char internal[128]; } ncclUniqueId;
 enum { ncclSuccess = 0 };
 enum { ncclSum = 0, ncclMax = 2 };
-enum { ncclFloat64 = 8, ncclInt32 = 2 };
+enum { ncclFloat64 = 8, ncclInt32 = 2, ncclInt64 = 4 };
 struct NcclApi {
   int (*GetUniqueId)(ncclUniqueId*);
   int (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
@@ -95,6 +95,17 @@ static int allreduce(tls_comm_t comm, double* buf, size_t count, int op, cudaStr
   return 0;
 }
 
+// int64 sum (exact, order-free): the fixed-point limbs of the CSR fp16 Gram
+static int allreduce_i64(tls_comm_t comm, void* buf, size_t count, cudaStream_t st) {
+  if (comm == nullptr || comm->nranks <= 1 || count == 0) return 0;
+  NcclApi* api = nccl_api();
+  const int r = api->AllReduce(buf, buf, count, ncclInt64, ncclSum, comm->comm, st);
+  if (r != ncclSuccess) {
+    set_error("ncclAllReduce(int64): %s", api->GetErrorString ? api->GetErrorString(r) : "error");
+    return TLS_ERR_NCCL;
+  }
+  return 0;
+}
 
 // ------------------------------------------------------------------------------ profiling
 namespace {
@@ -194,23 +205,31 @@ struct Tracer {
 
 // ------------------------------------------------------------------------------ workspace
 namespace {
+// Bump allocator over the caller's workspace; with base == nullptr it only
+// measures (tls_workspace_size), so carving and sizing cannot disagree.
 struct Carver {
-  char* p;
-  size_t left;
+  char* base;
+  size_t cap;
+  size_t off = 0;
   bool ok = true;
   template <typename T>
   T* take(size_t count) {
     const size_t bytes = (count * sizeof(T) + 255) & ~(size_t)255;
-    if (bytes > left) {
-      ok = false;
-      return nullptr;
+    T* r = nullptr;
+    if (base) {
+      if (off + bytes > cap) ok = false;
+      else r = reinterpret_cast<T*>(base + off);
     }
-    T* r = reinterpret_cast<T*>(p);
-    p += bytes;
-    left -= bytes;
+    off += bytes;
     return r;
   }
 };
+
+bool is_csr(const tls_matrix_t* A) { return A->layout == TLS_CSR; }
+DenseView dense_view(const tls_matrix_t* A) { return DenseView{A->vals, A->m_local, (int)A->n, A->ld}; }
+CsrView csr_view(const tls_matrix_t* A) {
+  return CsrView{A->rowptr, A->colidx, A->vals, A->m_local, (int)A->n, A->nnz_local};
+}
 
 struct Work {
   double* partials;
@@ -227,13 +246,19 @@ struct Work {
   double* gram_ws;
   size_t gram_ws_doubles;
   double* d_tmp;
+  // CSR only
+  CscView csc;
+  void* csc_scratch;
+  double* tbuf;
 };
 
-bool carve(const tls_matrix_t* A, void* ws, size_t bytes, Work& w, bool factor) {
+// Carves `ws` (or measures when ws == nullptr); returns the bytes needed.
+size_t carve(const tls_matrix_t* A, void* ws, size_t bytes, Work& w, bool factor, bool* ok = nullptr) {
   const int n = (int)A->n;
-  DenseView dv{A->vals, A->m_local, n, A->ld};
+  const bool csr = is_csr(A);
   Carver c{static_cast<char*>(ws), ws ? bytes : 0};
-  w.partials = c.take<double>(pass_partials_doubles(dv));
+  const size_t npart = csr ? csr_pass_partials_doubles() : pass_partials_doubles(dense_view(A));
+  w.partials = c.take<double>(npart);
   w.passout = c.take<double>(2 * (size_t)n + 2);
   w.colstats = c.take<double>(2 * (size_t)n);
   w.vec.omega = c.take<double>(2 * (size_t)n);
@@ -248,47 +273,56 @@ bool carve(const tls_matrix_t* A, void* ws, size_t bytes, Work& w, bool factor) 
   w.S = c.take<PcgState>(1);
   w.flags = c.take<int>(8);
   w.d_tmp = c.take<double>(2 * (size_t)n + 2);
+  w.csc = CscView{nullptr, nullptr, nullptr};
+  w.csc_scratch = nullptr;
+  w.tbuf = nullptr;
+  if (csr) {
+    w.tbuf = c.take<double>(2 * (size_t)A->m_local);
+    w.csc.colptr = c.take<int64_t>((size_t)n + 1);
+    w.csc.rowidx = c.take<int32_t>((size_t)A->nnz_local);
+    w.csc.vals = c.take<double>((size_t)A->nnz_local);
+    w.csc_scratch = c.take<char>(csc_scratch_bytes(A->m_local, n));
+  }
+  w.G = nullptr;
+  w.gram_ws = nullptr;
+  w.gram_ws_doubles = 0;
   if (factor) {
     w.G = c.take<double>((size_t)n * n);
     // K_t only changes the number of chunks; K_t = 1 gives the largest split count
-    w.gram_ws_doubles = gram_ws_doubles(dv, 1);
+    w.gram_ws_doubles = csr ? csr_gram_ws_bytes(n) / 8 : gram_ws_doubles(dense_view(A), 1);
     w.gram_ws = c.take<double>(w.gram_ws_doubles);
-  } else {
-    w.G = nullptr;
-    w.gram_ws = nullptr;
-    w.gram_ws_doubles = 0;
   }
-  return c.ok;
+  if (ok) *ok = c.ok;
+  return c.off;
 }
 
 size_t ws_need(const tls_matrix_t* A, bool factor) {
-  const int n = (int)A->n;
-  DenseView dv{A->vals, A->m_local, n, A->ld};
-  size_t tot = 0;
-  auto add = [&](size_t bytes) { tot += (bytes + 255) & ~(size_t)255; };
-  add(pass_partials_doubles(dv) * 8);
-  add((2 * (size_t)n + 2) * 8);
-  add(2 * (size_t)n * 8);
-  for (int i = 0; i < 5; ++i) add(2 * (size_t)n * 8);
-  for (int i = 0; i < 4; ++i) add((size_t)n * 8);
-  add(sizeof(PcgState));
-  add(8 * sizeof(int));
-  add((2 * (size_t)n + 2) * 8);
-  if (factor) {
-    add((size_t)n * n * 8);
-    add(gram_ws_doubles(dv, 1) * 8);
-  }
-  return tot;
+  Work w;
+  return carve(A, nullptr, 0, w, factor);
+}
+
+bool carve_ok(const tls_matrix_t* A, void* ws, size_t bytes, Work& w, bool factor) {
+  bool ok = false;
+  carve(A, ws, bytes, w, factor, &ok);
+  return ok && ws != nullptr;
 }
 
 int check_matrix(const tls_matrix_t* A) {
   if (!A) { set_error("A is NULL"); return TLS_ERR_ARG; }
-  if (A->layout != TLS_DENSE_ROWMAJOR) { set_error("CSR layout not supported by this build"); return TLS_ERR_UNSUPPORTED; }
-  if (A->n < 1 || A->m_local < 0 || A->m_global < A->n + 1 || A->ld < A->n || (A->ld & 1)) {
-    set_error("bad shape: need n >= 1, m_global >= n+1, ld >= n, ld even");
+  if (A->layout != TLS_DENSE_ROWMAJOR && A->layout != TLS_CSR) { set_error("unknown layout"); return TLS_ERR_ARG; }
+  if (A->n < 1 || A->m_local < 0 || A->m_global < A->n + 1) {
+    set_error("bad shape: need n >= 1, m_global >= n+1");
     return TLS_ERR_ARG;
   }
   if (A->n > kMaxDenseN) { set_error("n > %d unsupported", kMaxDenseN); return TLS_ERR_UNSUPPORTED; }
+  if (is_csr(A)) {
+    if (A->nnz_local < 0 || A->rowptr == nullptr || (A->nnz_local > 0 && (A->colidx == nullptr || A->vals == nullptr))) {
+      set_error("CSR: rowptr (m_local+1), colidx and vals (nnz_local) device pointers required");
+      return TLS_ERR_ARG;
+    }
+    return 0;
+  }
+  if (A->ld < A->n || (A->ld & 1)) { set_error("dense: need ld >= n, ld even"); return TLS_ERR_ARG; }
   if (A->m_local > 0 && (A->vals == nullptr || (reinterpret_cast<uintptr_t>(A->vals) & 15))) {
     set_error("A->vals must be a 16-byte aligned device pointer");
     return TLS_ERR_ARG;
@@ -312,32 +346,70 @@ struct Ctx {
 };
 
 // one pass over A (+ fixed-order reduction + all-reduce over ranks) into w.passout
-int run_pass(Ctx& cx, const DenseView& dv, int mode, int nrhs, const double* q, const double* b, Work& w,
+// (w.colstats for PASS_COLSTATS).  CSR operator/residual passes need w.csc built.
+int run_pass(Ctx& cx, const tls_matrix_t* A, int mode, int nrhs, const double* q, const double* b, Work& w,
              const int* active) {
-  int G = 1;
-  {
-    const int cat = mode == PASS_COLSTATS ? TLS_PROF_COLSTATS
-                    : mode == PASS_RESIDUAL ? TLS_PROF_PASS_RESID
-                    : (nrhs == 2 ? TLS_PROF_PASS_OP2 : TLS_PROF_PASS_OP1);
-    ProfScope ps(cat, cx.st);
-    TLS_TRY(launch_pass(dv, mode, nrhs, q, b, w.partials, active, cx.st, &G));
-  }
-  const int W = (mode == PASS_COLSTATS) ? 2 * dv.n : nrhs * dv.n + 2;
+  const int n = (int)A->n;
+  const int W = (mode == PASS_COLSTATS) ? 2 * n : nrhs * n + 2;
   double* out = (mode == PASS_COLSTATS) ? w.colstats : w.passout;
-  if (dv.m > 0) {
-    ProfScope ps(TLS_PROF_REDUCE, cx.st);
-    TLS_TRY(launch_reduce(w.partials, G, W, mode == PASS_COLSTATS ? dv.n : 0, out, active, cx.st));
+  const int cat = mode == PASS_COLSTATS ? TLS_PROF_COLSTATS
+                  : mode == PASS_RESIDUAL ? TLS_PROF_PASS_RESID
+                  : (nrhs == 2 ? TLS_PROF_PASS_OP2 : TLS_PROF_PASS_OP1);
+  if (is_csr(A)) {
+    const CsrView cv = csr_view(A);
+    ProfScope ps(cat, cx.st);
+    if (mode == PASS_COLSTATS) TLS_TRY(launch_csr_colstats(cv, out, w.partials, cx.st));
+    else TLS_TRY(launch_csr_pass(cv, w.csc, mode, nrhs, q, b, w.tbuf, w.partials, out, active, cx.st));
     cx.launches += 2;
   } else {
-    TLS_CUDA_TRY(cudaMemsetAsync(out, 0, (size_t)W * 8, cx.st));
+    const DenseView dv = dense_view(A);
+    int G = 1;
+    {
+      ProfScope ps(cat, cx.st);
+      TLS_TRY(launch_pass(dv, mode, nrhs, q, b, w.partials, active, cx.st, &G));
+    }
+    if (dv.m > 0) {
+      ProfScope ps(TLS_PROF_REDUCE, cx.st);
+      TLS_TRY(launch_reduce(w.partials, G, W, mode == PASS_COLSTATS ? dv.n : 0, out, active, cx.st));
+      cx.launches += 2;
+    } else {
+      TLS_CUDA_TRY(cudaMemsetAsync(out, 0, (size_t)W * 8, cx.st));
+    }
   }
   cx.passes += 1;
   if (mode == PASS_COLSTATS) {
-    TLS_TRY(allreduce(cx.comm, out, dv.n, ncclMax, cx.st));
-    TLS_TRY(allreduce(cx.comm, out + dv.n, dv.n, ncclSum, cx.st));
+    TLS_TRY(allreduce(cx.comm, out, n, ncclMax, cx.st));
+    TLS_TRY(allreduce(cx.comm, out + n, n, ncclSum, cx.st));
   } else {
     TLS_TRY(allreduce(cx.comm, out, W, ncclSum, cx.st));
   }
+  return 0;
+}
+
+// u_f Gram of the local block into w.G, summed over ranks (a2).
+int run_gram(Ctx& cx, const tls_matrix_t* A, int u_f, const double* dinv, int K_t, Work& w) {
+  const int n = (int)A->n;
+  ProfScope ps(TLS_PROF_GRAM, cx.st);
+  if (is_csr(A)) {
+    const bool ranks = cx.comm != nullptr && cx.comm->nranks > 1;
+    if (u_f == TLS_FP16 && ranks) {
+      // exact fixed-point limbs are summed over ranks as int64 (exact, order-free), then rounded once
+      TLS_TRY(launch_csr_gram(csr_view(A), u_f, dinv, w.G, w.gram_ws, w.gram_ws_doubles * 8, &w.flags[1], cx.st,
+                              &cx.launches, true));
+      TLS_TRY(allreduce_i64(cx.comm, w.gram_ws, 2 * (size_t)n * n, cx.st));
+      TLS_TRY(launch_csr_gram_fin(w.gram_ws, n, w.G, cx.st));
+      cx.launches += 1;
+      return 0;
+    }
+    TLS_TRY(launch_csr_gram(csr_view(A), u_f, dinv, w.G, w.gram_ws, w.gram_ws_doubles * 8, &w.flags[1], cx.st,
+                            &cx.launches, false));
+  } else if (A->m_local > 0) {
+    TLS_TRY(launch_gram(dense_view(A), u_f, dinv, K_t, w.G, w.gram_ws, w.gram_ws_doubles, &w.flags[1], cx.st,
+                        &cx.launches));
+  } else {
+    TLS_CUDA_TRY(cudaMemsetAsync(w.G, 0, (size_t)n * n * 8, cx.st));
+  }
+  TLS_TRY(allreduce(cx.comm, w.G, (size_t)n * n, ncclSum, cx.st));
   return 0;
 }
 
@@ -528,15 +600,14 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
   if (opts) o = *opts; else tls_rqi_opts_default(&o);
   const int K_t = o.gram_chunk > 0 ? o.gram_chunk : 64;
   Work w;
-  if (!carve(A, ws, ws_bytes, w, true)) { set_error("workspace too small (need %zu)", ws_need(A, true)); return TLS_ERR_WORKSPACE; }
+  if (!carve_ok(A, ws, ws_bytes, w, true)) { set_error("workspace too small (need %zu)", ws_need(A, true)); return TLS_ERR_WORKSPACE; }
   Ctx cx{static_cast<cudaStream_t>(stream), comm};
   const int n = (int)A->n;
-  DenseView dv{A->vals, A->m_local, n, A->ld};
   Tracer tr(cx.st);
   tr.mark("factor:start");
   TLS_CUDA_TRY(cudaMemsetAsync(w.flags, 0, 8 * sizeof(int), cx.st));
   // a1: column max / sums of squares, all-reduced; D = powers of two (R2)
-  TLS_TRY(run_pass(cx, dv, PASS_COLSTATS, 2, nullptr, nullptr, w, nullptr));
+  TLS_TRY(run_pass(cx, A, PASS_COLSTATS, 2, nullptr, nullptr, w, nullptr));
   double* d = w.d_tmp;
   double* dinv = w.d_tmp + n;
   double* normA2 = w.d_tmp + 2 * n;
@@ -544,14 +615,8 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
   cx.launches += 1;
   tr.mark("colstats");
   // a2: u_f Gram, all-reduced
-  if (dv.m > 0) {
-    ProfScope ps(TLS_PROF_GRAM, cx.st);
-    TLS_TRY(launch_gram(dv, u_f, dinv, K_t, w.G, w.gram_ws, w.gram_ws_doubles, &w.flags[1], cx.st, &cx.launches));
-  } else {
-    TLS_CUDA_TRY(cudaMemsetAsync(w.G, 0, (size_t)n * n * 8, cx.st));
-  }
+  TLS_TRY(run_gram(cx, A, u_f, dinv, K_t, w));
   cx.passes += 1;
-  TLS_TRY(allreduce(comm, w.G, (size_t)n * n, ncclSum, cx.st));
   tr.mark("gram");
   // a3: Cholesky (replicated on every rank: identical bits)
   {
@@ -692,11 +757,11 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   if (o.op_variant != 0) { set_error("op_variant 1 (paper A-free PCGTLS) not in this build"); return TLS_ERR_UNSUPPORTED; }
   if (o.max_outer < 1) o.max_outer = 1;
   Work w;
-  if (!carve(A, ws, ws_bytes, w, false)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
+  if (!carve_ok(A, ws, ws_bytes, w, false)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
   Ctx cx{static_cast<cudaStream_t>(stream), comm};
   const int n = (int)A->n;
   const PrecondDev& pc = R->dev;
-  DenseView dv{A->vals, A->m_local, n, A->ld};
+  if (is_csr(A)) TLS_TRY(launch_csc_build(csr_view(A), w.csc, w.csc_scratch, cx.st, &cx.launches));
   const double tol_in = o.tol_inner > 0 ? o.tol_inner : tol;
   PcgState hS;
 
@@ -719,7 +784,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   // budget the host polls the activity flags every 8 iterations.
   auto pcg_loop = [&](int nrhs, int budget) -> int {
     for (int j = 0; j < budget; ++j) {
-      TLS_TRY(run_pass(cx, dv, PASS_OPERATOR, nrhs, w.vec.q, nullptr, w, w.S->active));
+      TLS_TRY(run_pass(cx, A, PASS_OPERATOR, nrhs, w.vec.q, nullptr, w, w.S->active));
       {
         ProfScope ps(TLS_PROF_PCG_STEP, cx.st);
         TLS_TRY(launch_pcg_step(pc, w.vec, w.passout, w.S, nrhs, o.breakdown_rule, j + 1 < budget ? 1 : 0, cx.st));
@@ -740,7 +805,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   TLS_CUDA_TRY(cudaMemsetAsync(w.zero, 0, (size_t)n * 8, cx.st));
   TLS_CUDA_TRY(cudaMemsetAsync(w.vec.rhs, 0, 2 * (size_t)n * 8, cx.st));
   // setup (a1): h = A^T b, b^T b from the residual pass at x = 0
-  TLS_TRY(run_pass(cx, dv, PASS_RESIDUAL, 1, w.zero, b, w, nullptr));
+  TLS_TRY(run_pass(cx, A, PASS_RESIDUAL, 1, w.zero, b, w, nullptr));
   double bb = 0.0;
   TLS_CUDA_TRY(cudaMemcpyAsync(&bb, w.passout + n, 8, cudaMemcpyDeviceToHost, cx.st));
   k_copy<<<(n + 255) / 256, 256, 0, cx.st>>>(w.passout, w.vec.rhs, n);
@@ -767,7 +832,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   }
   cx.launches += 1;
   tr.mark("boot_cgls");
-  TLS_TRY(run_pass(cx, dv, PASS_RESIDUAL, 1, w.x0, b, w, nullptr));     // r_0 (l.227)
+  TLS_TRY(run_pass(cx, A, PASS_RESIDUAL, 1, w.x0, b, w, nullptr));     // r_0 (l.227)
   TLS_TRY(launch_boot_x1(pc, w.passout, w.x0, w.x, cx.st));              // l.229-235
   cx.launches += 1;
   TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
@@ -780,7 +845,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   int bk = -1, brhs = -1, bj = -1;
   for (;; ++k) {
     // a5: residual pass, sigma_k^2, f_k, g_k, psi_k (l.238-245, l.262)
-    TLS_TRY(run_pass(cx, dv, PASS_RESIDUAL, 1, w.x, b, w, nullptr));
+    TLS_TRY(run_pass(cx, A, PASS_RESIDUAL, 1, w.x, b, w, nullptr));
     TLS_TRY(launch_rqi_eval(pc, w.passout, w.x, w.vec, w.S, cx.st));
     cx.launches += 1;
     tr.mark("resid+eval");
@@ -905,12 +970,11 @@ int tls_solve_host(const double* A_host, const double* b_host, int64_t m, int64_
 int tls_colstats(const tls_matrix_t* A, double* colmax, double* sumsq, void* stream, void* ws, size_t ws_bytes) {
   TLS_TRY(check_matrix(A));
   Work w;
-  if (!carve(A, ws, ws_bytes, w, false)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
+  if (!carve_ok(A, ws, ws_bytes, w, false)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
   Ctx cx{static_cast<cudaStream_t>(stream), nullptr};
   const int n = (int)A->n;
-  DenseView dv{A->vals, A->m_local, n, A->ld};
   TLS_CUDA_TRY(cudaMemsetAsync(w.flags, 0, 8 * sizeof(int), cx.st));
-  TLS_TRY(run_pass(cx, dv, PASS_COLSTATS, 2, nullptr, nullptr, w, nullptr));
+  TLS_TRY(run_pass(cx, A, PASS_COLSTATS, 2, nullptr, nullptr, w, nullptr));
   TLS_TRY(launch_scaling(w.colstats, w.colstats + n, n, w.d_tmp, w.d_tmp + n, w.d_tmp + 2 * n, &w.flags[0], cx.st));
   TLS_CUDA_TRY(cudaMemcpyAsync(colmax, w.colstats, (size_t)n * 8, cudaMemcpyDeviceToDevice, cx.st));
   TLS_CUDA_TRY(cudaMemcpyAsync(sumsq, w.d_tmp + 2 * n, 8, cudaMemcpyDeviceToDevice, cx.st));
@@ -921,17 +985,17 @@ int tls_gram(const tls_matrix_t* A, int32_t u_f, const double* d_dev, int32_t K_
              size_t ws_bytes) {
   TLS_TRY(check_matrix(A));
   Work w;
-  if (!carve(A, ws, ws_bytes, w, true)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!carve_ok(A, ws, ws_bytes, w, true)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
+  Ctx cx{static_cast<cudaStream_t>(stream), nullptr};
   const int n = (int)A->n;
-  DenseView dv{A->vals, A->m_local, n, A->ld};
-  TLS_CUDA_TRY(cudaMemsetAsync(w.flags, 0, 8 * sizeof(int), st));
-  k_recip<<<(n + 255) / 256, 256, 0, st>>>(d_dev, w.d_tmp, n);
+  TLS_CUDA_TRY(cudaMemsetAsync(w.flags, 0, 8 * sizeof(int), cx.st));
+  k_recip<<<(n + 255) / 256, 256, 0, cx.st>>>(d_dev, w.d_tmp, n);
   TLS_LAUNCH_CHECK();
-  TLS_TRY(launch_gram(dv, u_f, w.d_tmp, K_t > 0 ? K_t : 64, G_dev, w.gram_ws, w.gram_ws_doubles, &w.flags[1], st, nullptr));
+  TLS_TRY(run_gram(cx, A, u_f, w.d_tmp, K_t > 0 ? K_t : 64, w));
+  TLS_CUDA_TRY(cudaMemcpyAsync(G_dev, w.G, (size_t)n * n * 8, cudaMemcpyDeviceToDevice, cx.st));
   int hf[8];
-  TLS_CUDA_TRY(cudaMemcpyAsync(hf, w.flags, sizeof(hf), cudaMemcpyDeviceToHost, st));
-  TLS_CUDA_TRY(cudaStreamSynchronize(st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(hf, w.flags, sizeof(hf), cudaMemcpyDeviceToHost, cx.st));
+  TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
   return hf[1] ? TLS_RANGE : 0;
 }
 
@@ -940,11 +1004,11 @@ int tls_pass(const tls_matrix_t* A, int32_t mode, int32_t nrhs, const double* q,
   TLS_TRY(check_matrix(A));
   if ((mode != 0 && mode != 1) || nrhs < 1 || nrhs > 2 || (mode == 1 && nrhs != 1)) { set_error("bad pass args"); return TLS_ERR_ARG; }
   Work w;
-  if (!carve(A, ws, ws_bytes, w, false)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
+  if (!carve_ok(A, ws, ws_bytes, w, false)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
   Ctx cx{static_cast<cudaStream_t>(stream), nullptr};
   const int n = (int)A->n;
-  DenseView dv{A->vals, A->m_local, n, A->ld};
-  TLS_TRY(run_pass(cx, dv, mode == 0 ? PASS_OPERATOR : PASS_RESIDUAL, nrhs, q, b, w, nullptr));
+  if (is_csr(A)) TLS_TRY(launch_csc_build(csr_view(A), w.csc, w.csc_scratch, cx.st, &cx.launches));
+  TLS_TRY(run_pass(cx, A, mode == 0 ? PASS_OPERATOR : PASS_RESIDUAL, nrhs, q, b, w, nullptr));
   TLS_CUDA_TRY(cudaMemcpyAsync(v, w.passout, (size_t)nrhs * n * 8, cudaMemcpyDeviceToDevice, cx.st));
   TLS_CUDA_TRY(cudaMemcpyAsync(s, w.passout + (size_t)nrhs * n, 16, cudaMemcpyDeviceToDevice, cx.st));
   return 0;

@@ -34,6 +34,38 @@ int launch_scaling(const double* colmax, const double* sumsq, int n, double* d, 
                    double* normA2, int* flag, cudaStream_t st);
 int launch_round(const double* x, double* y, int64_t n, int prec, cudaStream_t st);
 
+// ---- CSR (k_csr.cu) --------------------------------------------------------------------
+struct CsrView {
+  const int64_t* rowptr;  // m + 1
+  const int32_t* colidx;  // nnz, ascending within a row
+  const double* vals;     // nnz
+  int64_t m;
+  int n;
+  int64_t nnz;
+};
+struct CscView {          // transpose of a CsrView, rows ascending within every column
+  int64_t* colptr;        // n + 1
+  int32_t* rowidx;        // nnz
+  double* vals;           // nnz
+};
+// colstats[0..n) = per-column max |a_ij|, colstats[n] = ||A||_F^2, colstats[n+1..2n) = 0.
+// partials: kCsrRowCTAs doubles.
+int launch_csr_colstats(const CsrView& A, double* colstats, double* partials, cudaStream_t st);
+// G (n x n, full symmetric) = Gram of fl_uf(A D^{-1}); fp16: exact fixed-point sum in ws
+// (csr_gram_ws_bytes), rounded once; with fixed_point_out the limbs are left in ws (two
+// n x n int64 arrays, for an exact all-reduce) and launch_csr_gram_fin converts them.
+size_t csr_gram_ws_bytes(int n);
+int launch_csr_gram(const CsrView& A, int u_f, const double* dinv, double* G, void* ws, size_t ws_bytes,
+                    int* range_flag, cudaStream_t st, int* launches, bool fixed_point_out);
+int launch_csr_gram_fin(const void* ws, int n, double* G, cudaStream_t st);
+size_t csc_scratch_bytes(int64_t m, int n);
+int launch_csc_build(const CsrView& A, CscView C, void* scratch, cudaStream_t st, int* launches);
+size_t csr_pass_partials_doubles();
+// out = [v_0 .. v_{nrhs-1} (stride n), s0, s1] as in launch_pass + launch_reduce;
+// tbuf: nrhs * m doubles.
+int launch_csr_pass(const CsrView& A, const CscView& C, int mode, int nrhs, const double* q, const double* b,
+                    double* tbuf, double* partials, double* out, const int* active, cudaStream_t st);
+
 // ---- Gram (k_gram.cu: CUDA-core fp64/fp32 path; k_gram_tc.cu: tcgen05 path) -------------
 size_t gram_ws_doubles(const DenseView& A, int K_t);   // workspace of either path (doubles)
 bool gram_tc_supported(int u_f, int K_t);

@@ -26,6 +26,13 @@ def shard_rows(m: int, nranks: int, rank: int) -> Tuple[int, int]:
     return lo, hi
 
 
+def shard_csr(rowptr, colidx, vals, lo: int, hi: int):
+    """Rows [lo, hi) of a CSR matrix as a self-contained CSR block (rowptr rebased
+    to 0); works on numpy arrays and torch tensors alike."""
+    e0, e1 = int(rowptr[lo]), int(rowptr[hi])
+    return rowptr[lo:hi + 1] - e0, colidx[e0:e1], vals[e0:e1]
+
+
 def broadcast_unique_id(uid: bytes | None, group=None) -> bytes:
     """Rank 0's 128-byte id to every rank over the default process group."""
     obj = [uid if tdist.get_rank(group) == 0 else None]

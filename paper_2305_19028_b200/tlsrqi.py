@@ -158,6 +158,27 @@ def matrix(A: torch.Tensor, m_global: Optional[int] = None, row_offset: int = 0,
     return M
 
 
+def matrix_csr(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch.Tensor, n: int,
+               m_global: Optional[int] = None, row_offset: int = 0):
+    """tls_matrix_t for a CSR row block on the device: rowptr int64 (m_local + 1,
+    rowptr[0] = 0), colidx int32 (ascending within a row), vals fp64."""
+    assert rowptr.is_cuda and rowptr.dtype == torch.int64 and rowptr.dim() == 1
+    assert colidx.is_cuda and colidx.dtype == torch.int32 and vals.is_cuda and vals.dtype == torch.float64
+    assert colidx.numel() == vals.numel()
+    m = rowptr.numel() - 1
+    M = tls_matrix_t()
+    M.layout = TLS_CSR
+    M.m_local, M.n, M.ld = m, n, 0
+    M.m_global = m if m_global is None else m_global
+    M.row_offset = row_offset
+    M.rowptr = rowptr.data_ptr()
+    M.colidx = colidx.data_ptr() if colidx.numel() else None
+    M.vals = vals.data_ptr() if vals.numel() else None
+    M.nnz_local = vals.numel()
+    M._keep = (rowptr, colidx, vals)
+    return M
+
+
 def dense_operand(A: torch.Tensor) -> torch.Tensor:
     """Row-major fp64 copy with an even leading dimension (pads one zero column if n is odd)."""
     A = A.to(torch.float64)

@@ -267,7 +267,10 @@ def test_sparse_matches_dense():
         assert len(set(cols)) == 7 and (i % Pc.n) in cols and np.all(np.diff(cols) > 0)
     pcs, rs = rqi.solve(As, Pc.b, "fp16")
     pcd, rd = rqi.solve(Ad, Pc.b, "fp16")
-    assert np.array_equal(pcs.Rt, pcd.Rt)
+    # CSR Gram is the exact sum rounded once (R19), the dense one fp32 per 64-row
+    # chunk (R11): R~ agrees to within one fp16 ulp entrywise
+    ulp = np.spacing(np.abs(pcd.Rt).astype(np.float16)).astype(np.float64)
+    assert np.all(np.abs(pcs.Rt - pcd.Rt) <= ulp)
     assert rs.rqi_iters == rd.rqi_iters
     np.testing.assert_allclose(rs.x, rd.x, rtol=1e-12)
     ex = exact.tls_svd(Ad, Pc.b)
@@ -293,3 +296,54 @@ def test_cost_model_equals_sum_of_alg4_line_counts():
     for (m, n, r) in [(10**6, 10**3, 5), (10**4, 10**4, 2000), (100, 60, 8)]:
         s = perfmodel.speedup(m, n, r)
         assert 1.0 <= s <= 4.0
+
+
+# ----------------------------------------------------------------------------- CSR Gram (R19)
+def _tiny_csr(m, n, per_row, seed, integer=False):
+    rng = np.random.default_rng(seed)
+    rows, cols, vals = [], [], []
+    for i in range(m):
+        c = np.sort(rng.choice(n, per_row, replace=False))
+        v = rng.integers(-9, 10, per_row).astype(float) if integer else rng.standard_normal(per_row) * 10.0 ** rng.uniform(-3, 3)
+        rows += [i] * per_row
+        cols += list(c)
+        vals += list(v)
+    A = scipy.sparse.csr_matrix((vals, (rows, cols)), shape=(m, n))
+    A.data[A.data == 0] = 1.0
+    for j in range(n):                      # no empty column
+        if A[:, j].nnz == 0:
+            A[j % m, j] = 1.5
+    return scipy.sparse.csr_matrix(A)
+
+
+def test_csr_gram_fp16_is_exact_sum_rounded_once():
+    """R19 pin: the fp16 CSR Gram equals the exact rational sum of the exact u_f
+    products, rounded once (Fraction arithmetic, independent of the int64 split)."""
+    from fractions import Fraction
+    A = _tiny_csr(60, 7, 3, 11)
+    d, _ = rqi.column_scaling(A)
+    G = rqi.gram_uf(A, d, "fp16")
+    Ah = A.toarray() / d[None, :]
+    Ah = round_to(Ah, "fp16")
+    for j in range(7):
+        for k in range(7):
+            ex = sum((Fraction(float(Ah[i, j])) * Fraction(float(Ah[i, k])) for i in range(60)), Fraction(0))
+            assert G[j, k] == float(ex)
+
+
+def test_csr_gram_integer_inputs_exact():
+    A = _tiny_csr(400, 9, 4, 3, integer=True)
+    d, _ = rqi.column_scaling(A)
+    Ad = A.toarray()
+    exactG = (Ad.T.astype(np.int64) @ Ad.astype(np.int64)).astype(np.float64) / np.outer(d, d)
+    for fmt in ("fp16", "bf16", "fp32", "fp64"):
+        assert np.array_equal(rqi.gram_uf(A, d, fmt), exactG)
+
+
+def test_csr_gram_bf16_within_fp64_summation_bound():
+    A = _tiny_csr(300, 12, 5, 5)
+    d, _ = rqi.column_scaling(A)
+    Ah = round_to(A.toarray() / d[None, :], "bf16")
+    G = rqi.gram_uf(A, d, "bf16")
+    bound = 300 * 2.0 ** -53 * (np.abs(Ah).T @ np.abs(Ah))
+    assert np.all(np.abs(G - Ah.T @ Ah) <= 2 * bound)

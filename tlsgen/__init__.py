@@ -31,7 +31,7 @@ from typing import Optional
 import numpy as np
 
 __all__ = [
-    "DenseProblem", "CsrProblem", "dense_problem", "csr_problem", "config",
+    "DenseProblem", "CsrProblem", "dense_problem", "csr_problem", "ragged_csr", "config",
     "CONFIGS",
 ]
 
@@ -181,6 +181,36 @@ def csr_problem(m: int = 200000, n: int = 2000, per_row: int = 10, eps: float = 
     prod = (vals * x_true[colidx]).reshape(m, per_row + 1).sum(axis=1)
     b = prod + eps * g
     return CsrProblem(name, m, n, rowptr, colidx, vals, b, x_true, eps, seed, u_f)
+
+
+def ragged_csr(m: int, n: int, max_per_row: int, seed: int, eps: float = 1e-3,
+               empty_frac: float = 0.05, name: str = "ragged") -> CsrProblem:
+    """Edge-case CSR stand-in (tests only): row lengths uniform in [0, max_per_row]
+    (a fraction `empty_frac` of rows empty), distinct sorted columns, values N(0,1)
+    scaled by 10^U(-2,2) per row, plus one entry in every column (row j mod m) so
+    no column is empty.  Draw order: lengths, per-row columns, values, scales,
+    x_true, g."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    lens = rng.integers(0, max_per_row + 1, size=m)
+    lens[rng.random(m) < empty_frac] = 0
+    rows = []
+    for i in range(m):
+        rows.append(set(rng.choice(n, int(lens[i]), replace=False).tolist()) if lens[i] else set())
+    for j in range(n):
+        rows[j % m].add(j)
+    lens = np.array([len(r) for r in rows], dtype=np.int64)
+    rowptr = np.zeros(m + 1, dtype=np.int64)
+    rowptr[1:] = np.cumsum(lens)
+    colidx = np.concatenate([np.array(sorted(r), dtype=np.int32) for r in rows if r]).astype(np.int32)
+    vals = rng.standard_normal(int(rowptr[-1]))
+    scale = 10.0 ** rng.uniform(-2, 2, size=m)
+    vals = vals * np.repeat(scale, lens)
+    x_true = rng.standard_normal(n)
+    g = rng.standard_normal(m)
+    prod = np.zeros(m)
+    np.add.at(prod, np.repeat(np.arange(m), lens), vals * x_true[colidx])
+    b = prod + eps * g
+    return CsrProblem(name, m, n, rowptr, colidx, vals, b, x_true, eps, seed)
 
 
 # name -> (m, n, kappa, eps, seed, twin, u_f); cfg3 (CSR) handled separately.
