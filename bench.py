@@ -38,6 +38,8 @@ WORKLOADS = {
              "cfg4 (literal): dense 1048576x1024 fp64, kappa 1e4, b noise 1e-3*N(0,1), u_f fp16"),
     "cfg2w": ("cfg2w", 4096, 512, "bf16", "cfg2w: dense 4096x512 fp64, kappa 1e3, u_f bf16"),
     "cfg5": ("cfg5:k1e4:e1e-6", 65536, 2048, "fp16", "cfg5 cell kappa 1e4 eps 1e-6: dense 65536x2048 fp64, u_f fp16"),
+    "cfg3": ("cfg3", 200000, 2000, "fp16",
+             "cfg3: CSR 200000x2000 fp64, 10 distinct uniform columns + column i mod 2000 per row, u_f fp16"),
 }
 
 
@@ -99,6 +101,8 @@ class ClockSampler:
 def make_problem(wl, device):
     import tlsgen
     cfg, m, n, u_f, _ = WORKLOADS[wl]
+    if cfg == "cfg3":
+        return tlsgen.config(cfg), u_f
     return tlsgen.config(cfg, device=device, keep_factors=False), u_f
 
 
@@ -113,6 +117,8 @@ def oracle_sample(A_np, b_np, u_f, counts, row_scale=16, iters=2):
     from oracle import rqi as orq
     import numpy as np
     m, n = A_np.shape
+    if not isinstance(A_np, np.ndarray):
+        row_scale = 1          # CSR: the oracle factors the whole (28 MB) matrix in seconds
     blk = max(n + 1, m // row_scale)
     t0 = time.perf_counter()
     pc = orq.factor_precond(A_np[:blk], u_f)
@@ -143,8 +149,13 @@ def run_reference(args, rank, world):
     wl = args.workload
     dev = "cuda:0" if torch.cuda.is_available() else "cpu"
     P, u_f = make_problem(wl, dev)
-    A_np = P.A.cpu().numpy() if hasattr(P.A, "cpu") else P.A
-    b_np = P.b.cpu().numpy() if hasattr(P.b, "cpu") else P.b
+    if wl == "cfg3":
+        import scipy.sparse
+        A_np = scipy.sparse.csr_matrix((P.vals, P.colidx, P.rowptr), shape=(P.m, P.n))
+        b_np = P.b
+    else:
+        A_np = P.A.cpu().numpy() if hasattr(P.A, "cpu") else P.A
+        b_np = P.b.cpu().numpy() if hasattr(P.b, "cpu") else P.b
     del P
     # the oracle's own counts on this workload need a full oracle solve (too long);
     # use the counts recorded by the last GPU run when present, else the oracle on
@@ -216,15 +227,30 @@ def main():
     P, u_f = make_problem(wl, f"cuda:{local}")
     m = P.m
     lo, hi = pdist.shard_rows(m, world, rank)
-    A_loc = P.A[lo:hi].clone()
-    b_loc = P.b[lo:hi].clone()
+    csr = wl == "cfg3"
     keep_host = (rank == 0 and world == 1 and not args.no_cpu_baseline)
-    A_full_host = P.A.cpu() if keep_host else None
-    b_full_host = P.b.cpu() if keep_host else None
+    if csr:
+        import scipy.sparse
+        rp, ci, va = pdist.shard_csr(P.rowptr, P.colidx, P.vals, lo, hi)
+        dev = f"cuda:{local}"
+        csr_t = (torch.as_tensor(rp, device=dev), torch.as_tensor(ci, device=dev), torch.as_tensor(va, device=dev))
+        b_loc = torch.as_tensor(P.b[lo:hi], device=dev)
+        A_loc = None
+        A_full_host = scipy.sparse.csr_matrix((P.vals, P.colidx, P.rowptr), shape=(P.m, P.n)) if keep_host else None
+        b_full_host = torch.as_tensor(P.b) if keep_host else None
+        nnz_loc = int(va.size)
+    else:
+        A_loc = P.A[lo:hi].clone()
+        b_loc = P.b[lo:hi].clone()
+        A_full_host = P.A.cpu() if keep_host else None
+        b_full_host = P.b.cpu() if keep_host else None
     del P
     torch.cuda.empty_cache()
     comm = pdist.init_comm(local) if world > 1 else None
-    M = tlsrqi.matrix(A_loc, m_global=m, row_offset=lo)
+    if csr:
+        M = tlsrqi.matrix_csr(*csr_t, n, m_global=m, row_offset=lo)
+    else:
+        M = tlsrqi.matrix(A_loc, m_global=m, row_offset=lo)
     ws = tlsrqi.workspace(M)
     x = torch.empty(n, dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
@@ -280,7 +306,13 @@ def main():
     pcg_per_solve = info["boot_iters"] + sum(a + b for a, b in info["pcg_iters"])
     peak, peak_kind = load_peaks()
     p2 = prof["pass_op2"]
-    bytes_per_pass = 8.0 * (hi - lo) * M.ld
+    if csr:
+        # row phase: rowptr, colidx, vals, t write (2 RHS); column phase: colptr, rowidx, vals,
+        # t gathered once per nonzero (2 RHS) -- the operand is L2-resident (28 MB)
+        ml = hi - lo
+        bytes_per_pass = 8.0 * (ml + 1) + 12.0 * nnz_loc + 16.0 * ml + 8.0 * (n + 1) + 12.0 * nnz_loc + 16.0 * nnz_loc
+    else:
+        bytes_per_pass = 8.0 * (hi - lo) * M.ld
     roof = None
     if p2["count"] > 0:
         avg_ms = p2["ms"] / p2["count"]
@@ -290,7 +322,8 @@ def main():
         if os.path.exists(tpath):
             with open(tpath) as fh:
                 traffic = json.load(fh).get("pass_op2_dram_bytes_per_launch")
-        roof = {"kernel": "k_pass<2,operator> (t = A q, v = A^T t, 2 RHS, one read of A)",
+        roof = {"kernel": ("k_csr_rows<2,operator> + k_csr_cols<2> (t = A q, v = A^T t, 2 RHS; L2-resident operand)"
+                           if csr else "k_pass<2,operator> (t = A q, v = A^T t, 2 RHS, one read of A)"),
                 "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": traffic, "algorithmic_bytes_per_launch": bytes_per_pass,
                 "avg_launch_ms": avg_ms, "launches": p2["count"], "peak_kind": peak_kind}
@@ -298,7 +331,7 @@ def main():
 
     # ---- e2e: the same solve through tls_solve_host from pinned host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not csr:
         A_h = A_loc.cpu().pin_memory()
         b_h = b_loc.cpu().pin_memory()
         x_h = torch.empty(n, dtype=torch.float64).pin_memory()
@@ -336,7 +369,8 @@ def main():
     if keep_host:
         import numpy as np
         counts = (info["rqi_iters"], info["boot_iters"], info["pcg_iters"])
-        t_cpu, sample, parts = oracle_sample(A_full_host.numpy(), b_full_host.numpy(), u_f, counts)
+        t_cpu, sample, parts = oracle_sample(A_full_host if csr else A_full_host.numpy(), b_full_host.numpy(),
+                                             u_f, counts)
         cpu = {"value": t_cpu, "unit": "s", "cores": os.cpu_count(), "kind": "oracle", "sample": sample,
                "parts": parts}
 
@@ -346,7 +380,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "m": m, "n": n, "u_f": u_f, "ld": int(M.ld),
-                       "l2": "inputs larger than L2 (A = %.1f GB)" % (8.0 * m * n / 1e9),
+                       "l2": ("operand L2-resident (CSR, %.0f MB)" % (20.0 * nnz_loc / 1e6) if csr else
+                              "inputs larger than L2 (A = %.1f GB)" % (8.0 * m * n / 1e9)),
                        "parallelism": f"row-shard x{world} (NCCL all-reduce)"},
             "status": info["status_name"], "termination": info["termination_name"],
             "rqi_iters": info["rqi_iters"], "boot_iters": info["boot_iters"], "pcg_iters": info["pcg_iters"],

@@ -289,3 +289,52 @@ def test_cfg5_like_cells(T):
         rc, x, sig, info = T.tls_rqi_pcgtls(M, dev(P.b), R)
         res_or = rqi.rqi_pcgtls_mp(P.A, P.b, pc)
         _check_solve(info, x.cpu().numpy(), sig, res_or)
+
+
+@pytest.mark.parametrize("kappa,eps,fmt", [(1e2, 1e-3, "fp32"), (1e4, 1e-6, "fp16"), (1e2, 1e-1, "bf16")])
+def test_cfg5_full_size_cells(T, kappa, eps, fmt):
+    """BASELINE configs[4] cells at full size (65536 x 2048, generated on the device):
+    the GPU factor + solve against the oracle on the same bytes.  (1e2, 1e-3, fp32)
+    ends STAGNATED at k = 2 under the paper's budget and psi rule; the
+    others converge / break down.  Counts are compared with the oracle run on the
+    GPU's own R~ (the tensor-core Gram is not bit-reproducible)."""
+    P = tlsgen.config(f"cfg5:k{kappa:g}:e{eps:g}", device="cuda", keep_factors=False)
+    M = T.matrix(P.A)
+    rc, R, _ = T.tls_factor_precond(M, fmt)
+    assert rc == 0
+    rc, x, sig, info = T.tls_rqi_pcgtls(M, P.b, R)
+    A = P.A.cpu().numpy()
+    b = P.b.cpu().numpy()
+    Rt, d, nrm = T.tls_precond_export(R)
+    res_same_R = rqi.rqi_pcgtls_mp(A, b, rqi.Precond(Rt, d, fmt, nrm))
+    _check_solve(info, x.cpu().numpy(), sig, res_same_R)
+    if res_same_R.status in (rqi.OK, rqi.STAGNATED):
+        assert _rel(x.cpu().numpy(), res_same_R.x) <= 1e-9
+
+
+@pytest.mark.parametrize("name", ["cfg4w", "cfg4"])
+def test_cfg4_full_size(T, name):
+    """BASELINE configs[3] at full size (2^20 x 1024, 8.6 GB, generated on the device),
+    u_f = fp16 (reading R17), in the launch configuration bench.py times: GPU factor +
+    solve against the oracle's RQI-PCGTLS-MP on the same bytes with the GPU's R~.
+    cfg4w (well-posed twin, R8) converges; the literal cfg4 ends in PCG_BREAKDOWN at
+    k = 1 on both sides."""
+    P = tlsgen.config(name, device="cuda", keep_factors=False)
+    M = T.matrix(P.A)
+    ws = T.workspace(M)
+    rc, R, _ = T.tls_factor_precond(M, "fp16", ws=ws)
+    assert rc == 0
+    rc, x, sig, info = T.tls_rqi_pcgtls(M, P.b, R, ws=ws)
+    Rt, d, nrm = T.tls_precond_export(R)
+    b = P.b.cpu().numpy()
+    A = P.A.cpu().numpy()
+    del P, M, ws
+    torch.cuda.empty_cache()
+    res = rqi.rqi_pcgtls_mp(A, b, rqi.Precond(Rt, d, "fp16", nrm))
+    _check_solve(info, x.cpu().numpy(), sig, res)
+    if name == "cfg4w":
+        assert res.status == rqi.OK
+        # the Rayleigh invariant at the returned x (PAPER.md l.121, l.173): sigma^2 = ||[A,b][x;-1]||^2/(1+||x||^2)
+        assert abs(rqi.certify_sigma(A, b, x.cpu().numpy()) - sig) / sig <= 1e-12
+    else:
+        assert res.status == rqi.PCG_BREAKDOWN and info["breakdown_k"] == 1
