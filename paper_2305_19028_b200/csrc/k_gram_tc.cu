@@ -11,9 +11,15 @@
 //                   (kind::f16, M=128 N=128 K=16, fp32 accumulators in TMEM,
 //                   both operands MN-major straight from the row-major A^)
 //       warps 2-9   epilogue: after every K_t rows, tcgen05.ld the fp32 chunk
-//                   sum and add it to fp64 registers (reading R11: fp32
-//                   accumulation per chunk, fp64 across chunks); two TMEM
-//                   accumulators ping-pong so the MMA never waits for a drain.
+//                   sum (reading R11: the tensor cores accumulate each K_t-row
+//                   chunk in fp32) and add it to an fp32 Kahan-compensated
+//                   register accumulator (FP32 pipe); every `super` chunks the
+//                   compensated sum is flushed into this CTA's fp64 partial
+//                   tile in global memory (L2).  A per-chunk fp32 -> fp64
+//                   conversion (XU pipe, ~16/clk/SM) bound the previous design
+//                   (ncu: XU 65% busy, tensor pipe 12%).  Four TMEM accumulators
+//                   (all 512 columns) rotate so the MMA runs up to three chunks
+//                   ahead of the drain (flushes included).
 //  3. the split partials are summed in fixed order (k_gram_reduce_t).
 #include <cuda.h>
 
@@ -25,6 +31,7 @@ namespace tls {
 constexpr int kTcTile = 128;      // output tile edge (UMMA M = N = 128)
 constexpr int kTcBK = 64;         // rows of A^ per pipeline stage
 constexpr int kTcStages = 4;
+constexpr int kTcAcc = 4;         // TMEM accumulators (4 x 128 columns = all 512): 3 chunks of drain slack
 constexpr int kTcPanel = kTcTile * kTcBK * 2;   // 16 KB: one operand panel (2 TMA boxes of 8 KB)
 constexpr int kTcThreads = 320;
 
@@ -82,40 +89,48 @@ __host__ __device__ constexpr uint32_t idesc_f16(int fmt) {
 
 // ------------------------------------------------------------------------------ 1. A^ = fl_uf(A D^-1)
 template <int PREC>
-__global__ void k_round_scaled(const double* __restrict__ A, int64_t m, int n, int64_t ld, const double* __restrict__ dinv,
-                               uint16_t* __restrict__ Ah, int npad, int* __restrict__ range) {
-  const int groups = npad / 8;  // 8 columns -> one 16-byte store
-  const int64_t tot = m * groups;
+__global__ void __launch_bounds__(256) k_round_scaled(const double* __restrict__ A, int64_t m, int n, int64_t ld,
+                                                      const double* __restrict__ dinv, uint16_t* __restrict__ Ah, int npad,
+                                                      int* __restrict__ range) {
+  // Fully coalesced: a warp reads 32 consecutive column pairs of a row (512 B, one
+  // 16-byte load per lane; ld even and A 16-B aligned) and writes 32 consecutive u_f
+  // pairs (128 B).  Rows are spread over the grid; each thread keeps two pairs in flight.
+  const int pairs = npad / 2;
   int bad = 0;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = e / groups;
-    const int c0 = (int)(e % groups) * 8;
-    uint32_t w[4];
+  for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
+    const double* src = A + row * ld;
+    uint32_t* dst = reinterpret_cast<uint32_t*>(Ah + row * npad);
+    for (int p0 = threadIdx.x; p0 < pairs; p0 += 2 * blockDim.x) {
+      double2 v[2];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint16_t h[2];
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int c = c0 + 2 * k + t;
-        double v = 0.0;
-        if (c < n) {
-          v = round_uf(A[row * ld + c] * dinv[c], PREC);
-          bad |= !isfinite(v);
-        }
-        h[t] = PREC == TLS_FP16 ? enc_f16(v) : enc_b16(v);
+      for (int u = 0; u < 2; ++u) {
+        const int c = 2 * (p0 + u * (int)blockDim.x);
+        if (c + 1 < n) v[u] = __ldcs(reinterpret_cast<const double2*>(src + c));   // streamed once
+        else v[u] = make_double2(c < n ? src[c] : 0.0, 0.0);
       }
-      w[k] = (uint32_t)h[0] | ((uint32_t)h[1] << 16);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int pp = p0 + u * (int)blockDim.x;
+        if (pp >= pairs) break;
+        const int c = 2 * pp;
+        const double x0 = c < n ? v[u].x * dinv[c] : 0.0;
+        const double x1 = c + 1 < n ? v[u].y * dinv[c + 1] : 0.0;
+        const uint16_t h0 = PREC == TLS_FP16 ? f64_to_f16_bits(x0) : f64_to_bf16_bits(x0);   // one RNE rounding
+        const uint16_t h1 = PREC == TLS_FP16 ? f64_to_f16_bits(x1) : f64_to_bf16_bits(x1);
+        const uint32_t lim = PREC == TLS_FP16 ? 0x7c00u : 0x7f80u;                               // inf / nan
+        bad |= ((h0 & 0x7fffu) >= lim) | ((h1 & 0x7fffu) >= lim);
+        dst[pp] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+      }
     }
-    *reinterpret_cast<uint4*>(Ah + row * npad + c0) = make_uint4(w[0], w[1], w[2], w[3]);
   }
   if (bad) atomicExch(range, 1);
 }
 
 // ------------------------------------------------------------------------------ 2. tcgen05 SYRK
-template <int FMT>
+template <int FMT, bool KAHAN>
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchunks, int nsplit, int kpc,
-          double* __restrict__ part) {
+          int super, int epi, double* __restrict__ part) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment for the 128B-swizzled operand panels
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -124,8 +139,8 @@ k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchun
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * kTcStages * kTcPanel);
   uint64_t* empty = full + kTcStages;
   uint64_t* tfull = empty + kTcStages;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + kTcAcc;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + kTcAcc);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int t = blockIdx.x, I = 0;
@@ -141,7 +156,7 @@ k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchun
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kTcAcc; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 8);  // one arrive per epilogue warp
     }
@@ -149,7 +164,7 @@ k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchun
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "r"(256)
+                 "r"(kTcAcc * kTcTile)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -190,8 +205,8 @@ k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchun
       int it = 0;
       for (int c = c0; c < c1; ++c) {
         const int j = c - c0;
-        const int buf = j & 1;
-        if (j >= 2) mbar_wait(&tempty[buf], (uint32_t)((j >> 1) - 1) & 1u);
+        const int buf = j % kTcAcc;
+        if (j >= kTcAcc) mbar_wait(&tempty[buf], (uint32_t)(j / kTcAcc - 1) & 1u);
         tc_fence_after();
         const uint32_t dtm = tmem_base + (uint32_t)(buf * kTcTile);
         const int kb1 = min((c + 1) * kpc, kb_total);
@@ -215,40 +230,71 @@ k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchun
       }
     }
   } else {
-    // ---------------- epilogue: fp32 chunk sums -> fp64 registers
+    // ---------------- epilogue: fp32 chunk sums -> compensated fp32 -> fp64 partial tile
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
     const int half = (warp - 2) >> 2;       // column half: 0 -> cols 0..63, 1 -> 64..127
-    double acc[64];
+    const int row = q * 32 + lane;
+    double* out = part + ((size_t)s * gridDim.x + blockIdx.x) * (kTcTile * kTcTile) + (size_t)row * kTcTile + half * 64;
+    float sm[64], cm[64];
 #pragma unroll
-    for (int i = 0; i < 64; ++i) acc[i] = 0.0;
+    for (int i = 0; i < 64; ++i) { sm[i] = 0.f; cm[i] = 0.f; }
+    int pending = 0;
+    // flush: fire-and-forget fp64 reductions (RED.ADD.F64) into this CTA's partial
+    // tile (zeroed before the launch); each element has exactly one writer thread, so
+    // its adds are applied in program order (deterministic) and the epilogue never
+    // waits for an L2 round trip.
+    auto flush = [&]() {
+#pragma unroll
+      for (int k = 0; k < 64; ++k) {
+        atomicAdd(out + k, KAHAN ? (double)sm[k] - (double)cm[k] : (double)sm[k]);
+        sm[k] = 0.f;
+        cm[k] = 0.f;
+      }
+      pending = 0;
+    };
     for (int c = c0; c < c1; ++c) {
       const int j = c - c0;
-      const int buf = j & 1;
-      mbar_wait(&tfull[buf], (uint32_t)(j >> 1) & 1u);
+      const int buf = j % kTcAcc;
+      mbar_wait(&tfull[buf], (uint32_t)(j / kTcAcc) & 1u);
       tc_fence_after();
-#pragma unroll
-      for (int piece = 0; piece < 2; ++piece) {
-        uint32_t r[32];
-        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kTcTile + half * 64 + piece * 32);
-        TLS_TMEM_LD32(ta, r);
+      uint32_t r0[32], r1[32];
+      const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kTcTile + half * 64);
+      if (epi > 0) {
+        TLS_TMEM_LD32(ta, r0);           // both loads in flight, one wait
+        TLS_TMEM_LD32(ta + 32, r1);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int k = 0; k < 32; ++k) acc[piece * 32 + k] += (double)__uint_as_float(r[k]);
       }
+      // the chunk sum is in registers: hand the TMEM buffer back before the adds
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
-    }
-    const int row = q * 32 + lane;
-    double* out = part + ((size_t)s * gridDim.x + blockIdx.x) * (kTcTile * kTcTile) + (size_t)row * kTcTile + half * 64;
+      if (epi > 1) {
+        if (KAHAN) {
 #pragma unroll
-    for (int k = 0; k < 64; k += 2) *reinterpret_cast<double2*>(out + k) = make_double2(acc[k], acc[k + 1]);
+          for (int k = 0; k < 64; ++k) {        // Kahan: |error| <= 2u sum|x| + O(super u^2)
+            const float x = __uint_as_float(k < 32 ? r0[k] : r1[k - 32]);
+            const float y = __fsub_rn(x, cm[k]);
+            const float t = __fadd_rn(sm[k], y);
+            cm[k] = __fsub_rn(__fsub_rn(t, sm[k]), y);
+            sm[k] = t;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            sm[k] = __fadd_rn(sm[k], __uint_as_float(r0[k]));
+            sm[k + 32] = __fadd_rn(sm[k + 32], __uint_as_float(r1[k]));
+          }
+        }
+      }
+      if (++pending == super) flush();
+    }
+    if (pending) flush();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTcAcc * kTcTile) : "memory");
   }
 }
 
@@ -290,13 +336,25 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// Chunk sums per fp64 flush and the compensation switch (TLS_GRAM_SUPER / TLS_GRAM_KAHAN
+// override the defaults for accuracy experiments, tools/gram_check.py).
+static int gram_super() {
+  const char* e = getenv("TLS_GRAM_SUPER");
+  const int v = e ? atoi(e) : 64;
+  return v < 1 ? 1 : v;
+}
+static int gram_kahan() {
+  const char* e = getenv("TLS_GRAM_KAHAN");
+  return e ? atoi(e) != 0 : 0;
+}
+
 static void tc_shape(int64_t m, int n, int K_t, int& TT, int& ntiles, int& nchunks, int& nsplit) {
   TT = (n + kTcTile - 1) / kTcTile;
   ntiles = TT * (TT + 1) / 2;
   nchunks = (int)((m + K_t - 1) / K_t);
   if (nchunks < 1) nchunks = 1;
-  const int target = 2 * num_sms();
-  nsplit = (target + ntiles - 1) / ntiles;
+  // one wave of persistent-tile CTAs (1 CTA/SM): ntiles * nsplit <= #SMs when possible
+  nsplit = num_sms() / ntiles;
   if (nsplit > nchunks) nsplit = nchunks;
   if (nsplit < 1) nsplit = 1;
 }
@@ -331,9 +389,8 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
   double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + ah_bytes);
   // 1. A^ = fl_uf(A D^-1)
   {
-    const int64_t tot = A.m * (npad / 8);
-    int64_t g = (tot + 255) / 256;
-    const int64_t gmax = (int64_t)num_sms() * 16;
+    int64_t g = A.m;
+    const int64_t gmax = (int64_t)num_sms() * 8;
     if (g > gmax) g = gmax;
     if (u_f == TLS_FP16)
       k_round_scaled<TLS_FP16><<<(int)g, 256, 0, st>>>(A.A, A.m, A.n, A.ld, dinv, Ah, npad, range_flag);
@@ -357,15 +414,21 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
       return TLS_ERR_CUDA;
     }
   }
-  const size_t smem = 2 * kTcStages * kTcPanel + 1024 + 256;
+  const size_t smem = 2 * kTcStages * kTcPanel + 1024 + 512;
   dim3 grid(ntiles, nsplit);
-  if (u_f == TLS_FP16) {
-    TLS_CUDA_TRY(cudaFuncSetAttribute(k_gram_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_gram_tc<0><<<grid, kTcThreads, smem, st>>>(tmap, A.m, TT, nchunks, nsplit, K_t / kTcBK, part);
-  } else {
-    TLS_CUDA_TRY(cudaFuncSetAttribute(k_gram_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_gram_tc<1><<<grid, kTcThreads, smem, st>>>(tmap, A.m, TT, nchunks, nsplit, K_t / kTcBK, part);
-  }
+  auto launch = [&](auto kern) -> int {
+    TLS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const char* ee = getenv("TLS_GRAM_EPI");   // experiment knob: 0 sync only, 1 + TMEM loads, 2 full
+    kern<<<grid, kTcThreads, smem, st>>>(tmap, A.m, TT, nchunks, nsplit, K_t / kTcBK, gram_super(), ee ? atoi(ee) : 2,
+                                         part);
+    return 0;
+  };
+  TLS_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)nsplit * ntiles * kTcTile * kTcTile * 8, st));
+  const bool kahan = gram_kahan();
+  int rc = 0;
+  if (u_f == TLS_FP16) rc = kahan ? launch(k_gram_tc<0, true>) : launch(k_gram_tc<0, false>);
+  else rc = kahan ? launch(k_gram_tc<1, true>) : launch(k_gram_tc<1, false>);
+  if (rc) return rc;
   TLS_LAUNCH_CHECK();
   k_gram_reduce_t<<<ntiles, 256, 0, st>>>(part, ntiles, nsplit, TT, kTcTile, A.n, G);
   TLS_LAUNCH_CHECK();

@@ -58,11 +58,34 @@ __device__ __forceinline__ double round_rne(double x) {
   return sign ? -y : y;
 }
 
+// Hardware conversions: cvt.rn.{f16,bf16,f32}.f64 round the fp64 value ONCE to
+// nearest-even (no intermediate fp32 step for bf16), with gradual underflow and
+// overflow to +-inf -- the same function as round_rne<> above (bit-identical on the
+// parity tests' 4e5 values incl. ties, subnormals and overflow), at one F2F each.
+__device__ __forceinline__ uint16_t f64_to_f16_bits(double x) {
+  uint16_t h;
+  asm("cvt.rn.f16.f64 %0, %1;" : "=h"(h) : "d"(x));
+  return h;
+}
+__device__ __forceinline__ uint16_t f64_to_bf16_bits(double x) {
+  uint16_t h;
+  asm("cvt.rn.bf16.f64 %0, %1;" : "=h"(h) : "d"(x));
+  return h;
+}
+__device__ __forceinline__ double f16_bits_to_f64(uint16_t h) {
+  double d;
+  asm("cvt.f64.f16 %0, %1;" : "=d"(d) : "h"(h));
+  return d;
+}
+__device__ __forceinline__ double bf16_bits_to_f64(uint16_t h) {
+  return (double)__uint_as_float(((uint32_t)h) << 16);
+}
+
 __device__ __forceinline__ double round_uf(double x, int prec) {
   switch (prec) {
-    case TLS_FP16: return round_rne<11, -14, 15>(x);
-    case TLS_BF16: return round_rne<8, -126, 127>(x);
-    case TLS_FP32: return round_rne<24, -126, 127>(x);
+    case TLS_FP16: return f16_bits_to_f64(f64_to_f16_bits(x));
+    case TLS_BF16: return bf16_bits_to_f64(f64_to_bf16_bits(x));
+    case TLS_FP32: return (double)__double2float_rn(x);
     default: return x;
   }
 }
