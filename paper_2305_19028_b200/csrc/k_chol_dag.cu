@@ -1,0 +1,353 @@
+// k_chol_dag.cu — fp64 Cholesky G = R^T R of the u_f Gram (
+// PAPER.md l.206 "Cholesky factorization", l.290-297; reading R10), as ONE
+// persistent kernel executing the tile DAG of the right-looking blocked
+// algorithm on 64 x 64 tiles of the upper triangle:
+//
+//   POTRF(k)       R_kk = chol(G_kk) in shared memory (first non-positive or
+//                  non-finite pivot -> CHOL_BREAKDOWN index), one barrier per column
+//   TRSM(k, j)     R_kj = R_kk^{-T} G_kj by forward substitution   (j > k)
+//   UPDATE(k,i,j)  G_ij -= R_ki^T R_kj                              (k < i <= j)
+//
+// Every CTA (one per SM, co-resident by cooperative launch) fetches the next task
+// of a fixed topological list with an atomic counter and spins on the tile flags
+// its inputs need (release/acquire at gpu scope; tile data read through L2).  The
+// list emits POTRF(k+1) right after the row-(k+1) updates of step k, so the next
+// panel overlaps the rest of step k (one step of lookahead): the critical path is
+// POTRF + TRSM + UPDATE per tile column instead of three dependent launches per
+// step.  The updates of a tile are applied in k order (per-tile counter), so the
+// result is bitwise reproducible.  R overwrites the upper triangle in place.
+#include <vector>
+
+#include "tls_common.cuh"
+#include "tls_kernels.h"
+
+namespace tls {
+
+constexpr int kTB = 64;             // tile edge
+constexpr int kTS = kTB + 1;        // smem row stride (doubles)
+constexpr int kCholThreads = 256;
+
+enum { T_POTRF = 0, T_TRSM = 1, T_UPDATE = 2 };
+
+struct CholCtl {          // device control block (zeroed before the launch)
+  int next;               // task counter
+  int fail;               // 1-based failed pivot (first), 0 = none
+  int pad[2];
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Wait (all threads) until *flag >= want or a breakdown was flagged; returns false on breakdown.
+__device__ bool wait_flag(const int* flag, int want, const CholCtl* ctl) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    int v;
+    while ((v = ld_acquire(flag)) < want) {
+      if (ld_acquire(&ctl->fail) != 0) break;
+    }
+    ok = v >= want;
+  }
+  __syncthreads();
+  const bool r = ok;
+  __syncthreads();
+  return r;
+}
+
+// tile (ti, tj) of G -> smem S[64][65] (zeros outside the matrix; identity padding on the
+// diagonal tile when `pad_identity`)
+__device__ void load_tile(const double* G, int n, int ti, int tj, double* S, bool upper_only, bool pad_identity) {
+  for (int e = threadIdx.x; e < kTB * kTB; e += blockDim.x) {
+    const int i = e >> 6, j = e & 63;
+    const int gi = ti * kTB + i, gj = tj * kTB + j;
+    double v;
+    if (gi < n && gj < n) v = (upper_only && gj < gi) ? 0.0 : __ldcg(G + (size_t)gi * n + gj);
+    else v = (pad_identity && i == j) ? 1.0 : 0.0;
+    S[i * kTS + j] = v;
+  }
+}
+
+__device__ void store_tile(double* G, int n, int ti, int tj, const double* S, bool upper_only) {
+  for (int e = threadIdx.x; e < kTB * kTB; e += blockDim.x) {
+    const int i = e >> 6, j = e & 63;
+    const int gi = ti * kTB + i, gj = tj * kTB + j;
+    if (gi < n && gj < n && (!upper_only || gj >= gi)) __stcg(G + (size_t)gi * n + gj, S[i * kTS + j]);
+  }
+}
+
+// POTRF of the diagonal tile (square-root-free outer-product form, rows scaled by
+// 1/sqrt(d_j) at the end).  Thread t keeps the column strip l = t % 64, rows
+// i = t / 64 + 4r (r < 16) in registers; per column j the final row j is published to
+// shared memory and every thread applies the rank-1 update to its strip (one barrier
+// per column, conflict-free/broadcast shared-memory reads).  S: input upper / output R
+// upper; dr[i] = 1 / R_ii.  Returns the 1-based local failed pivot or 0.
+__device__ int potrf_tile(double* S, double* dr, int nb) {
+  __shared__ int fail;
+  __shared__ double rowj[2][kTB];
+  const int tid = threadIdx.x, l = tid & 63, i0 = tid >> 6;
+  double v[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = S[(i0 + 4 * r) * kTS + l];
+  if (tid == 0) fail = 0;
+  if (tid < kTB) rowj[0][tid] = S[tid];      // row 0 is final from the start
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    const double* rj = rowj[j & 1];
+    const double piv = rj[j];
+    if (!(piv > 0.0) || !isfinite(piv)) {
+      if (tid == 0) fail = j + 1;
+      break;  // uniform: every thread read the same piv
+    }
+    const double dinv = 1.0 / piv;
+    const double sjl = rj[l] * dinv;
+    double mrow[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) mrow[r] = rj[i0 + 4 * r];      // broadcast reads, all in flight
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int i = i0 + 4 * r;
+      if (i > j && l >= i) v[r] = fma(-mrow[r], sjl, v[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if (i0 + 4 * r == j + 1) rowj[(j + 1) & 1][l] = v[r];     // the next pivot row is now final
+    __syncthreads();
+  }
+  const int f = fail;
+  if (f) return f;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) S[(i0 + 4 * r) * kTS + l] = v[r];
+  __syncthreads();
+  __shared__ double rs[kTB];
+  if (tid < kTB) {
+    const double sq = sqrt(S[tid * kTS + tid]);
+    rs[tid] = 1.0 / sq;
+    dr[tid] = rs[tid];
+    S[tid * kTS + tid] = sq;
+  }
+  __syncthreads();
+  for (int e = tid; e < kTB * kTB; e += blockDim.x) {
+    const int i = e >> 6, c = e & 63;
+    if (c > i) S[i * kTS + c] *= rs[i];
+  }
+  __syncthreads();
+  return 0;
+}
+
+// TRSM in smem: B (64 x 64, columns c) <- R^{-T} B by forward substitution, four threads per
+// column (thread q of a column keeps rows l = q (mod 4) in registers; x_i is broadcast from
+// its owner by a shuffle; the remaining rows are updated independently).
+__device__ void trsm_tile(const double* R, const double* dr, double* B) {
+  const int tid = threadIdx.x, c = tid >> 2, q = tid & 3;
+  double g[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) g[t] = B[(4 * t + q) * kTS + c];
+#pragma unroll
+  for (int i = 0; i < kTB; ++i) {
+    const int owner = i & 3, slot = i >> 2;
+    double xi = 0.0;
+    if (q == owner) xi = g[slot] * dr[i];
+    xi = __shfl_sync(0xffffffffu, xi, (tid & 31 & ~3) | owner);
+    if (q == owner) g[slot] = xi;
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int l = 4 * t + q;
+      if (l > i) g[t] = fma(-R[i * kTS + l], xi, g[t]);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 16; ++t) B[(4 * t + q) * kTS + c] = g[t];
+}
+
+// acc[p][q] = sum_i A[i][4ty+p] B[i][tx+16q] (A^T B); B reads are lane-consecutive
+// (conflict-free), A reads are warp broadcasts.
+__device__ __forceinline__ void tile_atb(const double* A, const double* B, double (&acc)[4][4]) {
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  for (int i = 0; i < kTB; ++i) {
+    double a[4], b[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) a[q] = A[i * kTS + 4 * ty + q];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) b[q] = B[i * kTS + tx + 16 * q];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+  }
+}
+
+__global__ void __launch_bounds__(kCholThreads, 1)
+k_chol_dag(double* __restrict__ G, int n, int T, const int4* __restrict__ tasks, int ntasks,
+           double* __restrict__ xinv, int* __restrict__ potrf_done, int* __restrict__ trsm_done,
+           int* __restrict__ upd_done, CholCtl* __restrict__ ctl, int* __restrict__ pivot,
+           unsigned long long* __restrict__ trace) {
+  extern __shared__ double sm[];
+  double* S0 = sm;                  // [64][65]
+  double* S1 = S0 + kTB * kTS;
+  double* S2 = S1 + kTB * kTS;
+  __shared__ int task_idx;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  for (;;) {
+    if (tid == 0) task_idx = atomicAdd(&ctl->next, 1);
+    __syncthreads();
+    const int t = task_idx;
+    __syncthreads();
+    if (t >= ntasks) break;
+    const int4 tk = tasks[t];
+    const int type = tk.x, k = tk.y, i = tk.z, j = tk.w;
+    unsigned long long t0 = 0;
+    if (trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    if (type == T_POTRF) {
+      bool ok = wait_flag(&upd_done[k * T + k], k, ctl);
+      int f = 0;
+      if (ok) {
+        load_tile(G, n, k, k, S0, true, true);
+        __syncthreads();
+        const int nb = min(kTB, n - k * kTB);
+        f = potrf_tile(S0, S1, nb);
+        if (!f) {
+          store_tile(G, n, k, k, S0, true);
+          if (tid < kTB) xinv[(size_t)k * kTB + tid] = S1[tid];
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        if (f) {
+          atomicCAS(&ctl->fail, 0, k * kTB + f);
+          atomicCAS(pivot, 0, k * kTB + f);
+        }
+        __threadfence();
+        st_release(&potrf_done[k], 1);
+      }
+    } else if (type == T_TRSM) {      // R_kj = X_k^T G_kj
+      bool ok = wait_flag(&potrf_done[k], 1, ctl) && wait_flag(&upd_done[k * T + j], k, ctl);
+      if (ok) {
+        load_tile(G, n, k, k, S0, true, true);      // R_kk (upper, identity padding)
+        if (tid < kTB) S2[tid] = __ldcg(xinv + (size_t)k * kTB + tid);
+        load_tile(G, n, k, j, S1, false, false);
+        __syncthreads();
+        trsm_tile(S0, S2, S1);
+        __syncthreads();
+        store_tile(G, n, k, j, S1, false);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        st_release(&trsm_done[k * T + j], 1);
+      }
+    } else {                          // G_ij -= R_ki^T R_kj, applied in k order
+      bool ok = wait_flag(&trsm_done[k * T + i], 1, ctl) && wait_flag(&trsm_done[k * T + j], 1, ctl) &&
+                wait_flag(&upd_done[i * T + j], k, ctl);
+      if (ok) {
+        load_tile(G, n, k, i, S0, false, false);
+        if (j != i) load_tile(G, n, k, j, S1, false, false);
+        load_tile(G, n, i, j, S2, i == j, false);
+        __syncthreads();
+        double acc[4][4] = {};
+        tile_atb(S0, j != i ? S1 : S0, acc);
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) S2[(4 * ty + p) * kTS + tx + 16 * q] -= acc[p][q];
+        __syncthreads();
+        store_tile(G, n, i, j, S2, i == j);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        st_release(&upd_done[i * T + j], k + 1);
+      }
+    }
+    if (trace && tid == 0) {
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      trace[3 * t] = t0;
+      trace[3 * t + 1] = t1;
+      trace[3 * t + 2] = blockIdx.x;
+    }
+  }
+}
+
+// Topological task list with one step of lookahead (file header).
+static const std::vector<int4>& task_list(int T) {
+  static int cached_T = -1;
+  static std::vector<int4> v;
+  if (cached_T == T) return v;
+  v.clear();
+  v.push_back(make_int4(T_POTRF, 0, 0, 0));
+  for (int j = 1; j < T; ++j) v.push_back(make_int4(T_TRSM, 0, 0, j));
+  for (int k = 0; k < T; ++k) {
+    if (k + 1 < T) {
+      for (int j = k + 1; j < T; ++j) v.push_back(make_int4(T_UPDATE, k, k + 1, j));   // row k+1 of step k
+      v.push_back(make_int4(T_POTRF, k + 1, 0, 0));
+      for (int j = k + 2; j < T; ++j) v.push_back(make_int4(T_TRSM, k + 1, 0, j));
+    }
+    for (int i = k + 2; i < T; ++i)
+      for (int j = i; j < T; ++j) v.push_back(make_int4(T_UPDATE, k, i, j));           // rest of step k
+  }
+  cached_T = T;
+  return v;
+}
+
+size_t chol_ws_bytes(int n) {
+  const int T = (n + kTB - 1) / kTB;
+  const size_t tasks = task_list(T).size();
+  return tasks * sizeof(int4) + (size_t)T * kTB * 8 + ((size_t)T + 2 * (size_t)T * T) * sizeof(int) +
+         sizeof(CholCtl) + 1024;
+}
+
+int launch_cholesky(double* G, int n, int* pivot, void* ws, size_t ws_bytes, cudaStream_t st, int* launches) {
+  const int T = (n + kTB - 1) / kTB;
+  const std::vector<int4>& tl = task_list(T);
+  if (ws_bytes < chol_ws_bytes(n)) { set_error("cholesky: workspace too small"); return TLS_ERR_WORKSPACE; }
+  char* p = static_cast<char*>(ws);
+  auto take = [&](size_t bytes) { char* r = p; p += (bytes + 255) & ~(size_t)255; return r; };
+  int4* tasks = reinterpret_cast<int4*>(take(tl.size() * sizeof(int4)));
+  double* xinv = reinterpret_cast<double*>(take((size_t)T * kTB * 8));   // 1 / R_ii per tile
+  int* flags = reinterpret_cast<int*>(take(((size_t)T + 2 * (size_t)T * T) * sizeof(int) + sizeof(CholCtl)));
+  int* potrf_done = flags;
+  int* trsm_done = potrf_done + T;
+  int* upd_done = trsm_done + (size_t)T * T;
+  CholCtl* ctl = reinterpret_cast<CholCtl*>(upd_done + (size_t)T * T);
+  if ((size_t)(p - static_cast<char*>(ws)) > ws_bytes) { set_error("cholesky: workspace too small"); return TLS_ERR_WORKSPACE; }
+  TLS_CUDA_TRY(cudaMemcpyAsync(tasks, tl.data(), tl.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+  TLS_CUDA_TRY(cudaMemsetAsync(flags, 0, ((size_t)T + 2 * (size_t)T * T) * sizeof(int) + sizeof(CholCtl), st));
+  const size_t smem = 3 * kTB * kTS * 8;
+  static bool attr = false;
+  if (!attr) {
+    TLS_CUDA_TRY(cudaFuncSetAttribute(k_chol_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  int ntasks = (int)tl.size();
+  int grid = num_sms();
+  if (grid > ntasks) grid = ntasks;
+  // TLS_CHOL_TRACE=<path>: per-task start/end timestamps (globaltimer ns) and CTA, written
+  // after the kernel as text lines "type k i j start end cta" (diagnostics only)
+  static unsigned long long* trace = nullptr;
+  const char* tpath = getenv("TLS_CHOL_TRACE");
+  if (tpath && !trace) TLS_CUDA_TRY(cudaMalloc(&trace, 3 * sizeof(unsigned long long) * 200000));
+  unsigned long long* tr = tpath ? trace : nullptr;
+  void* args[] = {&G, (void*)&n, (void*)&T, &tasks, &ntasks, &xinv, &potrf_done, &trsm_done, &upd_done, &ctl, &pivot, &tr};
+  TLS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_chol_dag, dim3(grid), dim3(kCholThreads), args, smem, st));
+  if (launches) *launches += 1;
+  if (tr) {
+    std::vector<unsigned long long> h(3 * (size_t)ntasks);
+    TLS_CUDA_TRY(cudaMemcpyAsync(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    TLS_CUDA_TRY(cudaStreamSynchronize(st));
+    FILE* f = fopen(tpath, "w");
+    if (f) {
+      for (int t = 0; t < ntasks; ++t)
+        fprintf(f, "%d %d %d %d %llu %llu %llu\n", tl[t].x, tl[t].y, tl[t].z, tl[t].w, h[3 * t], h[3 * t + 1], h[3 * t + 2]);
+      fclose(f);
+    }
+  }
+  return 0;
+}
+
+}  // namespace tls

@@ -290,6 +290,8 @@ size_t carve(const tls_matrix_t* A, void* ws, size_t bytes, Work& w, bool factor
     w.G = c.take<double>((size_t)n * n);
     // K_t only changes the number of chunks; K_t = 1 gives the largest split count
     w.gram_ws_doubles = csr ? csr_gram_ws_bytes(n) / 8 : gram_ws_doubles(dense_view(A), 1);
+    const size_t chol = (chol_ws_bytes(n) + 7) / 8;                  // the Cholesky reuses it
+    if (w.gram_ws_doubles < chol) w.gram_ws_doubles = chol;
     w.gram_ws = c.take<double>(w.gram_ws_doubles);
   }
   if (ok) *ok = c.ok;
@@ -621,7 +623,7 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
   // a3: Cholesky (replicated on every rank: identical bits)
   {
     ProfScope ps(TLS_PROF_CHOL, cx.st);
-    TLS_TRY(launch_cholesky(w.G, n, &w.flags[2], cx.st, &cx.launches));
+    TLS_TRY(launch_cholesky(w.G, n, &w.flags[2], w.gram_ws, w.gram_ws_doubles * 8, cx.st, &cx.launches));
   }
   tr.mark("cholesky");
   int hflags[8];
@@ -643,7 +645,7 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
   h->normA2_host = hnorm;
   k_fill_scaling<<<(h->dev.npad + 255) / 256, 256, 0, cx.st>>>(h->dev.d, h->dev.dinv, d, dinv, n, h->dev.npad);
   TLS_CUDA_TRY(cudaMemcpyAsync(h->dev.normA2, normA2, sizeof(double), cudaMemcpyDeviceToDevice, cx.st));
-  int rc = launch_pack_R(w.G, n, h->dev, &w.flags[1], cx.st, &cx.launches);
+  int rc = launch_pack_R(w.G, n, 0, h->dev, &w.flags[1], cx.st, &cx.launches);
   cx.launches += 1;  // k_fill_scaling
   if (rc) { tls_precond_destroy(h); return rc; }
   tr.mark("pack");
@@ -683,7 +685,7 @@ int tls_precond_import(int64_t n, int32_t u_f, const double* Rt_host, const doub
   TLS_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
   k_fill_scaling<<<(h->dev.npad + 255) / 256, 256, 0, st>>>(h->dev.d, h->dev.dinv, tmp + (size_t)n * n,
                                                            tmp + (size_t)n * n + n, (int)n, h->dev.npad);
-  int rc = launch_pack_R(tmp, (int)n, h->dev, flag, st, nullptr);
+  int rc = launch_pack_R(tmp, (int)n, 0, h->dev, flag, st, nullptr);
   int hflag = 0;
   TLS_CUDA_TRY(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   TLS_CUDA_TRY(cudaStreamSynchronize(st));

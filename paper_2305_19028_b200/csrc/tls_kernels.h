@@ -76,9 +76,11 @@ int launch_gram(const DenseView& A, int u_f, const double* dinv, int K_t, double
                 size_t ws_doubles, int* range_flag, cudaStream_t st, int* launches);
 
 // ---- Cholesky and R~ packing (k_chol.cu) -----------------------------------------------
-// In-place upper Cholesky of G (n x n, row-major, only the upper triangle is used).
-// *pivot = 1-based index of the first failed pivot (0 if none).
-int launch_cholesky(double* G, int n, int* pivot, cudaStream_t st, int* launches);
+// Cholesky G = R^T R (n x n row-major, input and output R in the upper triangle; the
+// lower triangle is not touched) by the tile-DAG kernel of k_chol_dag.cu.  *pivot =
+// 1-based index of the first failed pivot (0 if none).  ws: >= chol_ws_bytes(n).
+size_t chol_ws_bytes(int n);
+int launch_cholesky(double* G, int n, int* pivot, void* ws, size_t ws_bytes, cudaStream_t st, int* launches);
 // R~ = fl_uf(R) into the handle layouts; *range = 1 on overflow or a zero diagonal.
 struct PrecondDev {
   int n, npad, u_f;
@@ -90,7 +92,8 @@ struct PrecondDev {
   double* dinv;     // npad
   double* normA2;   // 1 (device)
 };
-int launch_pack_R(const double* R, int ldR, PrecondDev& pc, int* range, cudaStream_t st,
+// lower = 0: R upper (R[i][j], j >= i, row-major); lower = 1: R^T in the lower triangle.
+int launch_pack_R(const double* R, int ldR, int lower, PrecondDev& pc, int* range, cudaStream_t st,
                   int* launches);
 size_t precond_bytes(int n, int u_f);
 
