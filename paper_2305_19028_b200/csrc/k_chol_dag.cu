@@ -81,49 +81,116 @@ __device__ void store_tile(double* G, int n, int ti, int tj, const double* S, bo
   }
 }
 
-// POTRF of the diagonal tile (square-root-free outer-product form, rows scaled by
-// 1/sqrt(d_j) at the end).  Thread t keeps the column strip l = t % 64, rows
-// i = t / 64 + 4r (r < 16) in registers; per column j the final row j is published to
-// shared memory and every thread applies the rank-1 update to its strip (one barrier
-// per column, conflict-free/broadcast shared-memory reads).  S: input upper / output R
-// upper; dr[i] = 1 / R_ii.  Returns the 1-based local failed pivot or 0.
+// POTRF of the diagonal tile, blocked by 16 (square-root-free form U = D R with
+// d_i = U_ii; A_ij -= sum_k U_ki U_kj / d_k; rows scaled by 1/sqrt(d_i) at the end).
+// For each 16-block: (1) the 16 x 16 diagonal block, one element per thread in a
+// register, one barrier per column; (2) the multipliers F_ji = U_ji / d_j and the
+// block row to the right by per-column substitution; (3) the rank-16 update of the
+// trailing upper triangle.  S: input upper / output R upper; dr[i] = 1 / R_ii.
+// Returns the 1-based local failed pivot or 0.
+#ifdef POTRF_TRACE
+#define PMARK(k) do { if (threadIdx.x == 0) g_marks[k] = clock64(); } while (0)
+#else
+#define PMARK(k) do {} while (0)
+#endif
 __device__ int potrf_tile(double* S, double* dr, int nb) {
   __shared__ int fail;
-  __shared__ double rowj[2][kTB];
-  const int tid = threadIdx.x, l = tid & 63, i0 = tid >> 6;
-  double v[16];
-#pragma unroll
-  for (int r = 0; r < 16; ++r) v[r] = S[(i0 + 4 * r) * kTS + l];
+  __shared__ double rowb[2][16];
+  __shared__ double F[16][kTB + 1];      // multipliers of the current block: F[j][i] = U_ji / d_j
+  const int tid = threadIdx.x;
   if (tid == 0) fail = 0;
-  if (tid < kTB) rowj[0][tid] = S[tid];      // row 0 is final from the start
   __syncthreads();
-  for (int j = 0; j < nb; ++j) {
-    const double* rj = rowj[j & 1];
-    const double piv = rj[j];
-    if (!(piv > 0.0) || !isfinite(piv)) {
-      if (tid == 0) fail = j + 1;
-      break;  // uniform: every thread read the same piv
+  PMARK(0);
+  for (int o = 0; o < kTB; o += 16) {
+    // (1) diagonal block: warp 0, lane t owns column t of the block in registers;
+    // row jj of the block is read from lane ii by shuffles (no block barriers)
+    if (tid < 32) {
+      const int t = tid & 15;
+      double v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = S[(o + i) * kTS + o + t];
+      int f = 0;
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        const double piv = __shfl_sync(0xffffffffu, v[jj], jj);
+        if (o + jj < nb) {
+          if (!(piv > 0.0) || !isfinite(piv)) { f = o + jj + 1; break; }
+          const double dinv = 1.0 / piv;
+          const double sjt = v[jj];
+#pragma unroll
+          for (int ii = jj + 1; ii < 16; ++ii) {
+            const double m = __shfl_sync(0xffffffffu, v[jj], ii) * dinv;
+            if (t >= ii) v[ii] = fma(-m, sjt, v[ii]);
+          }
+        }
+      }
+      if (tid < 16) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (i <= t) S[(o + i) * kTS + o + t] = v[i];
+      }
+      if (tid == 0 && f) fail = f;
     }
-    const double dinv = 1.0 / piv;
-    const double sjl = rj[l] * dinv;
-    double mrow[16];
-#pragma unroll
-    for (int r = 0; r < 16; ++r) mrow[r] = rj[i0 + 4 * r];      // broadcast reads, all in flight
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const int i = i0 + 4 * r;
-      if (i > j && l >= i) v[r] = fma(-mrow[r], sjl, v[r]);
-    }
-#pragma unroll
-    for (int r = 0; r < 16; ++r)
-      if (i0 + 4 * r == j + 1) rowj[(j + 1) & 1][l] = v[r];     // the next pivot row is now final
     __syncthreads();
+    PMARK(1 + (o / 16) * 4);
+    if (fail) break;
+    // (2) multipliers of the block and the block row to its right (columns c >= o + 16)
+    for (int e = tid; e < 16 * kTB; e += blockDim.x) {
+      const int jj = e >> 6, c = e & 63;
+      const double d = S[(o + jj) * kTS + o + jj];
+      F[jj][c] = (c > o + jj && o + jj < nb) ? S[(o + jj) * kTS + c] / d : 0.0;   // inside the block for now
+    }
+    __syncthreads();
+    const int w = kTB - o - 16;                 // columns to the right
+    if (tid < w) {
+      const int c = o + 16 + tid;
+      double u[16];
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) u[jj] = S[(o + jj) * kTS + c];
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj)
+#pragma unroll
+        for (int ii = jj + 1; ii < 16; ++ii) u[ii] = fma(-F[jj][o + ii], u[jj], u[ii]);
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) S[(o + jj) * kTS + c] = u[jj];
+    }
+    __syncthreads();
+    PMARK(2 + (o / 16) * 4);
+    if (w == 0) break;
+    // multipliers for the columns right of the block (final U rows of the block)
+    for (int e = tid; e < 16 * w; e += blockDim.x) {
+      const int jj = e / w, c = o + 16 + e % w;
+      F[jj][c] = (o + jj < nb) ? S[(o + jj) * kTS + c] / S[(o + jj) * kTS + o + jj] : 0.0;
+    }
+    __syncthreads();
+    PMARK(3 + (o / 16) * 4);
+    // (3) trailing update: S_ic -= sum_jj F[jj][i] U[jj][c], o+16 <= i <= c (4 rows at a time)
+    {
+      const int c = o + 16 + (tid & 63);
+      if (c < kTB) {
+        double uc[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) uc[jj] = S[(o + jj) * kTS + c];
+        for (int i = o + 16 + (tid >> 6); i <= c; i += 16) {
+          double acc[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acc[r] = (i + 4 * r <= c) ? S[(i + 4 * r) * kTS + c] : 0.0;
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[r] = fma(-F[jj][min(i + 4 * r, kTB - 1)], uc[jj], acc[r]);
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if (i + 4 * r <= c) S[(i + 4 * r) * kTS + c] = acc[r];
+        }
+      }
+    }
+    __syncthreads();
+    PMARK(4 + (o / 16) * 4);
   }
+  __syncthreads();
   const int f = fail;
   if (f) return f;
-#pragma unroll
-  for (int r = 0; r < 16; ++r) S[(i0 + 4 * r) * kTS + l] = v[r];
-  __syncthreads();
   __shared__ double rs[kTB];
   if (tid < kTB) {
     const double sq = sqrt(S[tid * kTS + tid]);
