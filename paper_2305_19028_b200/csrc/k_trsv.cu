@@ -114,7 +114,8 @@ __device__ __forceinline__ TrsvSm trsv_carve(int npad) {
 // each solve completes exactly one phase of every barrier).  All threads call it.
 __device__ __forceinline__ void trsv_init(const TrsvSm& sm, int npad) {
   for (int i = threadIdx.x; i < (npad >> 5); i += blockDim.x) mbar_init(&sm.bar[i], 1);
-  __syncthreads();
+  if (threadIdx.x == 0) fence_mbar_init();
+  cluster_sync_all();   // the cluster's CTAs may address these barriers from now on
 }
 
 __device__ __forceinline__ void stage_dinv_warp(double* dst, const double* src) {
@@ -159,9 +160,17 @@ __device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / CPR, cpos = lane % CPR;
   const int NB = npad >> 5;
+  const int C = (int)cluster_nctarank(), cr = (int)cluster_ctarank();
   const uint32_t ph = sm.phase;
-  __syncthreads();  // y is filled
-  if (warp < NB) {
+  // arm every block barrier for this solve: one local arrival + the 256 bytes of the
+  // solution block, written by its owner CTA with st.async (complete_tx); the cluster
+  // barrier makes sure every CTA is armed (and its y filled) before anyone sends
+  for (int i = threadIdx.x; i < NB; i += blockDim.x) mbar_arrive_expect_tx(&sm.bar[i], 256);
+  cluster_sync_all();
+  // block u (solve order) is owned by CTA u % C, warp (u / C) % kTW
+  const int first = cr + C * warp;
+  const int ustep = C * kTW;
+  if (first < NB) {
     double* Dw = sm.D + warp * 1024;
     double* ysw = sm.ys + warp * 32;
     auto real = [&](int u) { return BACK ? NB - 1 - u : u; };
@@ -171,19 +180,21 @@ __device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv
       for (int k = 0; k < NV; ++k) raw[k] = __ldg(reinterpret_cast<const uint4*>(base + (size_t)k * RPI * npad));
     };
     int total = 0;
-    for (int u = warp; u < NB; u += kTW) total += u;
-    stage_dinv_warp(Dw, Dinv + (size_t)real(warp) * 1024);
-    int ui = warp, ci = 0;
-    if (ui == 0) ui += kTW;
+    for (int u = first; u < NB; u += ustep) total += u;
+    stage_dinv_warp(Dw, Dinv + (size_t)real(first) * 1024);
+    int ui = first, ci = 0;
+    if (ui == 0) ui += ustep;
     uint4 raw[DP][NV];
 #pragma unroll
     for (int s = 0; s < DP; ++s) {
       if (s < total) {
         issue(ui, ci, raw[s]);
-        if (++ci == ui) { ui += kTW; ci = 0; }
+        if (++ci == ui) { ui += ustep; ci = 0; }
       }
     }
-    int uc = warp, cc = 0;
+    // remote (cluster) addresses of this lane's y element and of the barriers are formed per block
+    const uint32_t y_base = smem_u32(sm.y), bar_base = smem_u32(sm.bar);
+    int uc = first, cc = 0;
     double acc[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) acc[k] = 0.0;
@@ -209,10 +220,12 @@ __device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv
         x0 = fma(Dw[l * 32 + lane], ysw[l], x0);
         x1 = fma(Dw[(l + 1) * 32 + lane], ysw[l + 1], x1);
       }
-      sm.y[o + lane] = x0 + x1;
+      const double xv = x0 + x1;
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.bar[uc]);
-      uc += kTW;
+      // publish x_u to every CTA of the cluster (including this one)
+      const uint32_t ya = y_base + (uint32_t)(o + lane) * 8u, ba = bar_base + (uint32_t)uc * 8u;
+      for (int r = 0; r < C; ++r) st_async_f64(mapa_shared(ya, (uint32_t)r), xv, mapa_shared(ba, (uint32_t)r));
+      uc += ustep;
       cc = 0;
       if (uc < NB) stage_dinv_warp(Dw, Dinv + (size_t)real(uc) * 1024);
     };
@@ -221,7 +234,7 @@ __device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv
 #pragma unroll
       for (int s = 0; s < DP; ++s) {
         if (kb + s < total) {
-          mbar_wait_spin(&sm.bar[cc], ph);
+          mbar_wait_cluster(&sm.bar[cc], ph);
           double xv[EPC];
           const double2* xp = reinterpret_cast<const double2*>(sm.y + 32 * real(cc) + cpos * EPC);
 #pragma unroll
@@ -236,24 +249,30 @@ __device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv
             for (int e = 0; e < EPC; ++e) acc[k] = fma(chunk_get<T>(raw[s][k], e), xv[e], acc[k]);
           if (kb + s + DP < total) {
             issue(ui, ci, raw[s]);
-            if (++ci == ui) { ui += kTW; ci = 0; }
+            if (++ci == ui) { ui += ustep; ci = 0; }
           }
           if (++cc == uc) solve();
         }
       }
     }
   }
+  // every solution block (also the ones other CTAs own) must be in this CTA's y
+  for (int i = threadIdx.x; i < NB; i += blockDim.x) mbar_wait_cluster(&sm.bar[i], ph);
   sm.phase ^= 1u;
   __syncthreads();
 }
 
 // ---------------------------------------------------------------- plain apply (API / tests)
-// One CTA per right-hand side r (blockIdx.x).
+// One cluster of kTC CTAs per right-hand side r.  Every CTA of a cluster holds the whole
+// vector and computes the same values; only cluster rank 0 writes global memory.
+constexpr int kTC = 4;   // CTAs (SMs) per solve
+
 template <typename T>
 __global__ void __launch_bounds__(kTW * 32) k_precond_apply(PrecondDev pc, int trans, double* __restrict__ Y, int ldY) {
   TrsvSm sm = trsv_carve(pc.npad);
   trsv_init(sm, pc.npad);
-  const int n = pc.n, npad = pc.npad, r = blockIdx.x;
+  const int n = pc.n, npad = pc.npad, r = blockIdx.x / (int)cluster_nctarank();
+  const bool rank0 = cluster_ctarank() == 0;
   for (int i = threadIdx.x; i < npad; i += blockDim.x) {
     double v = i < n ? Y[(size_t)r * ldY + i] : 0.0;
     if (trans) v *= pc.dinv[i];
@@ -261,24 +280,26 @@ __global__ void __launch_bounds__(kTW * 32) k_precond_apply(PrecondDev pc, int t
   }
   if (trans) trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, npad, sm);
   else trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, npad, sm);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    double v = sm.y[i];
-    if (!trans) v *= pc.dinv[i];
-    Y[(size_t)r * ldY + i] = v;
-  }
+  if (rank0)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double v = sm.y[i];
+      if (!trans) v *= pc.dinv[i];
+      Y[(size_t)r * ldY + i] = v;
+    }
 }
 
 // ---------------------------------------------------------------- PCGTLS (Alg. 3)
-// One CTA per right-hand side r = blockIdx.x (the two solves of an RQI step are
-// independent until the RQI update).  Vectors in global memory have stride n
-// (q feeds the pass over A directly).
+// One cluster per right-hand side r (the two solves of an RQI step are independent
+// until the RQI update).  Vectors in global memory have stride n (q feeds the pass
+// over A directly).
 template <typename T>
 __global__ void __launch_bounds__(kTW * 32) k_pcg_init(PrecondDev pc, int nrhs, PcgVecs v, PcgState* __restrict__ S) {
   TrsvSm sm = trsv_carve(pc.npad);
   trsv_init(sm, pc.npad);
-  const int n = pc.n, npad = pc.npad, tid = threadIdx.x, r = blockIdx.x;
+  const int n = pc.n, npad = pc.npad, tid = threadIdx.x, r = blockIdx.x / (int)cluster_nctarank();
+  const bool rank0 = cluster_ctarank() == 0;
   if (r >= nrhs) {                 // the unused RHS slot of a 1-RHS solve
-    if (tid == 0) {
+    if (rank0 && tid == 0) {
       S->active[r] = 0; S->count[r] = 0; S->brk[r] = 0; S->brk_j[r] = -1; S->iter[r] = 0;
       S->eta[r] = S->eta0[r] = S->qq[r] = 0.0;
       S->delta_min[r] = __longlong_as_double(0x7ff0000000000000ll);
@@ -292,9 +313,11 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_init(PrecondDev pc, int nrhs, 
   double e = 0.0;
   for (int i = tid; i < n; i += blockDim.x) {
     const double s = sm.y[i];
-    v.s[off + i] = s;
-    v.p[off + i] = s;
-    v.omega[off + i] = 0.0;
+    if (rank0) {
+      v.s[off + i] = s;
+      v.p[off + i] = s;
+      v.omega[off + i] = 0.0;
+    }
     e = fma(s, s, e);
   }
   const double eta = block_sum(e, sm.red);
@@ -303,11 +326,11 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_init(PrecondDev pc, int nrhs, 
   e = 0.0;
   for (int i = tid; i < n; i += blockDim.x) {
     const double q = sm.y[i] * pc.dinv[i];
-    v.q[off + i] = q;
+    if (rank0) v.q[off + i] = q;
     e = fma(q, q, e);
   }
   const double qq = block_sum(e, sm.red);
-  if (tid == 0) {
+  if (rank0 && tid == 0) {
     S->eta[r] = eta;
     S->eta0[r] = eta;
     S->qq[r] = qq;
@@ -320,38 +343,53 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_init(PrecondDev pc, int nrhs, 
   }
 }
 
-// One PCGTLS iteration of RHS r = blockIdx.x after the pass t = A q_r,
-// v_r = A^T t_r, tau_r = t_r^T t_r (passout = [v_0 .. v_{nrhs-1} (stride n), tau_0, tau_1]).
+// One PCGTLS iteration of RHS r after the pass t = A q_r, v_r = A^T t_r, tau_r = t_r^T t_r
+// (passout = [v_0 .. v_{nrhs-1} (stride n), tau_0, tau_1]).  Every CTA of the cluster
+// reads its inputs before rank 0 writes anything (cluster barriers), so the replicas
+// take identical decisions.
+constexpr int kVecPerThread = 8;   // npad <= kTW * 32 * 8 = 4096
 template <typename T>
 __global__ void __launch_bounds__(kTW * 32) k_pcg_step(PrecondDev pc, PcgVecs v, const double* __restrict__ passout,
                                                        PcgState* __restrict__ S, int nrhs, int rule, int next_q) {
-  __shared__ double s_alpha, s_beta;
-  __shared__ int s_upd, s_cont;
-  const int r = blockIdx.x;
-  if (r >= nrhs || S->active[r] == 0) return;
+  __shared__ double s_alpha, s_beta, s_delta;
+  __shared__ int s_upd, s_cont, s_brk, s_exit;
   TrsvSm sm = trsv_carve(pc.npad);
   trsv_init(sm, pc.npad);
+  const int r = blockIdx.x / (int)cluster_nctarank();
+  const bool rank0 = cluster_ctarank() == 0;
+  if (r >= nrhs || S->active[r] == 0) return;
   const int n = pc.n, npad = pc.npad, tid = threadIdx.x;
   const size_t off = (size_t)r * n;
   const double sig2 = S->sigma2;
   if (tid == 0) {
     s_upd = 0;
+    s_brk = 0;
+    s_exit = 0;
     s_alpha = 0.0;
     const double tau = passout[(size_t)nrhs * n + r];
     const double delta = tau - sig2 * S->qq[r];            // l.194 with the operator of l.324
-    S->delta_min[r] = fmin(S->delta_min[r], delta);
+    s_delta = delta;
     if (!isfinite(delta) || delta == 0.0) {                 // loop guard l.192 (R3)
-      S->active[r] = 0;
+      s_exit = 1;
     } else if (delta < 0.0 && rule == 0) {                  // breakdown (R3)
-      S->active[r] = 0;
-      S->brk[r] = 1;
-      S->brk_j[r] = S->iter[r];
+      s_exit = 1;
+      s_brk = 1;
     } else {
       s_alpha = S->eta[r] / delta;                          // l.195
       s_upd = 1;
     }
   }
-  __syncthreads();
+  const int iter0 = S->iter[r];
+  const double eta_old = S->eta[r], eta0 = S->eta0[r], tol2 = S->tol2, dmin = S->delta_min[r];
+  const int count0 = S->count[r];
+  cluster_sync_all();   // every CTA has read S before rank 0 updates it
+  if (rank0 && tid == 0) {
+    S->delta_min[r] = fmin(dmin, s_delta);
+    if (s_exit) {
+      S->active[r] = 0;
+      if (s_brk) { S->brk[r] = 1; S->brk_j[r] = iter0; }
+    }
+  }
   if (!s_upd) return;
   const double al = s_alpha;
   // omega += alpha q (l.196); y = D^{-1}(A^T t - sigma^2 q) for w = P^{-T}(...) (R1)
@@ -359,55 +397,71 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_step(PrecondDev pc, PcgVecs v,
     double yv = 0.0;
     if (i < n) {
       const double q = v.q[off + i];
-      v.omega[off + i] = fma(al, q, v.omega[off + i]);
+      if (rank0) v.omega[off + i] = fma(al, q, v.omega[off + i]);
       yv = (passout[off + i] - sig2 * q) * pc.dinv[i];
     }
     sm.y[i] = yv;
   }
   trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, npad, sm);
-  // s -= alpha w (l.198), eta' = ||s||^2 (l.199)
+  // s -= alpha w (l.198), eta' = ||s||^2 (l.199); kept in registers until every CTA has read s, p
+  double sn[kVecPerThread], pn[kVecPerThread];
   double e = 0.0;
-  for (int i = tid; i < n; i += blockDim.x) {
-    const double s = fma(-al, sm.y[i], v.s[off + i]);
-    v.s[off + i] = s;
-    e = fma(s, s, e);
+#pragma unroll
+  for (int k = 0; k < kVecPerThread; ++k) {
+    const int i = tid + k * (int)blockDim.x;
+    sn[k] = 0.0;
+    if (i < n) {
+      sn[k] = fma(-al, sm.y[i], v.s[off + i]);
+      e = fma(sn[k], sn[k], e);
+    }
   }
   const double etan = block_sum(e, sm.red);
   if (tid == 0) {
     s_cont = 0;
-    S->count[r] += 1;
-    S->iter[r] += 1;
-    if (etan <= S->tol2 * S->eta0[r]) {                     // early exit (R3)
-      S->active[r] = 0;
-    } else {
-      s_beta = etan / S->eta[r];                            // l.200
-      S->eta[r] = etan;
+    if (!(etan <= tol2 * eta0)) {                           // early exit (R3)
+      s_beta = etan / eta_old;                              // l.200
       s_cont = 1;
     }
   }
   __syncthreads();
-  if (!s_cont) return;
-  // p = s + beta p (l.201)
+  const bool cont = s_cont;
   const double be = s_beta;
-  for (int i = tid; i < npad; i += blockDim.x) {
-    double pv = 0.0;
-    if (i < n) {
-      pv = fma(be, v.p[off + i], v.s[off + i]);
-      v.p[off + i] = pv;
-    }
-    sm.y[i] = pv;
+  // p = s + beta p (l.201)
+#pragma unroll
+  for (int k = 0; k < kVecPerThread; ++k) {
+    const int i = tid + k * (int)blockDim.x;
+    pn[k] = 0.0;
+    if (cont && i < n) pn[k] = fma(be, v.p[off + i], sn[k]);
+    if (i < npad) sm.y[i] = pn[k];
   }
-  if (!next_q) return;
+  cluster_sync_all();   // every CTA has read the old s and p
+  if (rank0) {
+#pragma unroll
+    for (int k = 0; k < kVecPerThread; ++k) {
+      const int i = tid + k * (int)blockDim.x;
+      if (i < n) {
+        v.s[off + i] = sn[k];
+        if (cont) v.p[off + i] = pn[k];
+      }
+    }
+    if (tid == 0) {
+      S->count[r] = count0 + 1;
+      S->iter[r] = iter0 + 1;
+      if (cont) S->eta[r] = etan;
+      else S->active[r] = 0;
+    }
+  }
+  if (!cont || !next_q) return;
   // next q = P^{-1} p (l.193 of the next iteration)
   trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, npad, sm);
   e = 0.0;
   for (int i = tid; i < n; i += blockDim.x) {
     const double q = sm.y[i] * pc.dinv[i];
-    v.q[off + i] = q;
+    if (rank0) v.q[off + i] = q;
     e = fma(q, q, e);
   }
   const double qq = block_sum(e, sm.red);
-  if (tid == 0) S->qq[r] = qq;
+  if (rank0 && tid == 0) S->qq[r] = qq;
 }
 
 // ---------------------------------------------------------------- RQI (Alg. 4)
@@ -477,7 +531,8 @@ __global__ void __launch_bounds__(kTW * 32) k_boot_x1(PrecondDev pc, const doubl
   const double sig0 = passout[n] / (1.0 + xx);
   trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, npad, sm);
   trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, npad, sm);
-  for (int i = tid; i < n; i += blockDim.x) x1[i] = fma(sig0, sm.y[i] * pc.dinv[i], x0[i]);
+  if (cluster_ctarank() == 0)
+    for (int i = tid; i < n; i += blockDim.x) x1[i] = fma(sig0, sm.y[i] * pc.dinv[i], x0[i]);
 }
 
 // ---------------------------------------------------------------- launchers
@@ -495,38 +550,46 @@ static int set_smem(F kern, size_t bytes) {
     default: { using T = double; __VA_ARGS__; } break;      \
   }
 
+// kTC-CTA clusters (one per right-hand side) of the single-CTA TRSV kernels
+template <typename... KArgs, typename... Args>
+static int launch_cluster(void (*kern)(KArgs...), int clusters, size_t smem, cudaStream_t st, Args... args) {
+  TLS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(clusters * kTC);
+  cfg.blockDim = dim3(kTW * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kTC;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  TLS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
+  return 0;
+}
+
 int launch_precond_apply(const PrecondDev& pc, int trans, int nrhs, double* Y, int ldY, cudaStream_t st) {
   const size_t sm = trsv_smem(pc.npad);
   int rc = 0;
-  TLS_DISPATCH_UF(pc.u_f, {
-    if ((rc = set_smem(k_precond_apply<T>, sm))) return rc;
-    k_precond_apply<T><<<nrhs, kTW * 32, sm, st>>>(pc, trans, Y, ldY);
-  });
-  TLS_LAUNCH_CHECK();
-  return 0;
+  TLS_DISPATCH_UF(pc.u_f, { rc = launch_cluster(k_precond_apply<T>, nrhs, sm, st, pc, trans, Y, ldY); });
+  return rc;
 }
 
 int launch_pcg_init(const PrecondDev& pc, int nrhs, PcgVecs v, PcgState* S, cudaStream_t st) {
   const size_t sm = trsv_smem(pc.npad);
   int rc = 0;
-  TLS_DISPATCH_UF(pc.u_f, {
-    if ((rc = set_smem(k_pcg_init<T>, sm))) return rc;
-    k_pcg_init<T><<<2, kTW * 32, sm, st>>>(pc, nrhs, v, S);
-  });
-  TLS_LAUNCH_CHECK();
-  return 0;
+  TLS_DISPATCH_UF(pc.u_f, { rc = launch_cluster(k_pcg_init<T>, 2, sm, st, pc, nrhs, v, S); });
+  return rc;
 }
 
 int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgState* S, int nrhs, int rule,
                     int next_q, cudaStream_t st) {
   const size_t sm = trsv_smem(pc.npad);
   int rc = 0;
-  TLS_DISPATCH_UF(pc.u_f, {
-    if ((rc = set_smem(k_pcg_step<T>, sm))) return rc;
-    k_pcg_step<T><<<nrhs, kTW * 32, sm, st>>>(pc, v, passout, S, nrhs, rule, next_q);
-  });
-  TLS_LAUNCH_CHECK();
-  return 0;
+  TLS_DISPATCH_UF(pc.u_f, { rc = launch_cluster(k_pcg_step<T>, nrhs, sm, st, pc, v, passout, S, nrhs, rule, next_q); });
+  return rc;
 }
 
 int launch_rqi_eval(const PrecondDev& pc, const double* passout, const double* x, PcgVecs v, PcgState* S,
@@ -546,12 +609,8 @@ int launch_rqi_update(const PrecondDev& pc, PcgVecs v, const PcgState* S, double
 int launch_boot_x1(const PrecondDev& pc, const double* passout_r0, const double* x0, double* x1, cudaStream_t st) {
   const size_t sm = trsv_smem(pc.npad);
   int rc = 0;
-  TLS_DISPATCH_UF(pc.u_f, {
-    if ((rc = set_smem(k_boot_x1<T>, sm))) return rc;
-    k_boot_x1<T><<<1, kTW * 32, sm, st>>>(pc, passout_r0, x0, x1);
-  });
-  TLS_LAUNCH_CHECK();
-  return 0;
+  TLS_DISPATCH_UF(pc.u_f, { rc = launch_cluster(k_boot_x1<T>, 1, sm, st, pc, passout_r0, x0, x1); });
+  return rc;
 }
 
 }  // namespace tls
