@@ -304,6 +304,7 @@ def main():
 
     info = infos[-1]
     pcg_per_solve = info["boot_iters"] + sum(a + b for a, b in info["pcg_iters"])
+    a_passes = 3 + info["boot_iters"] + 1 + info["rqi_iters"] + sum(max(a, b) for a, b in info["pcg_iters"])
     peak, peak_kind = load_peaks()
     p2 = prof["pass_op2"]
     if csr:
@@ -386,8 +387,11 @@ def main():
             "status": info["status_name"], "termination": info["termination_name"],
             "rqi_iters": info["rqi_iters"], "boot_iters": info["boot_iters"], "pcg_iters": info["pcg_iters"],
             "sigma": sig, "pcg_iters_per_s": pcg_per_solve / tts,
-            "passes_per_step": passes / args.steps,
-            "a_passes_per_s": passes / args.steps / tts,
+            # passes over A that do work: colstats + Gram read + setup + bootstrap CGLS + r_0
+            # + one residual pass per RQI step + one batched operator pass per PCG iteration
+            "a_passes_per_step": a_passes,
+            "pass_launches_per_step": passes / args.steps,
+            "a_passes_per_s": a_passes / tts,
             "roofline": roof, "kernel_share": kshare,
             "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
         }

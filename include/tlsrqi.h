@@ -102,7 +102,9 @@ typedef struct {
   int32_t boot;           /* 0: x_LS by preconditioned CGLS (R5) [0]; 1: semi-normal */
   int32_t boot_max;       /* [200] */
   double boot_tol;        /* [1e-8] */
-  int32_t op_variant;     /* 0: A-in-loop operator (R1) [0]; other values unsupported */
+  int32_t op_variant;     /* 0: A-in-loop operator (R1) [0]; 1: the paper's A-free Alg. 3 as printed
+                             (delta = p^T p - sigma^2 q^T q, w = p - sigma^2 P^{-T} q;
+                             no pass over A inside PCGTLS; the sigma = 0 bootstrap stays A-in-loop) */
   int32_t breakdown_rule; /* 0: delta < 0 is a breakdown (R3) [0]; 1: only delta == 0 stops */
   int32_t gram_chunk;     /* K_t rows per fp32 accumulation chunk (R11) [64]; multiple of 64 for the tensor-core path */
   int32_t reserved[5];

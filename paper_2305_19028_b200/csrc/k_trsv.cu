@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_init(PrecondDev pc, int nrhs, 
   if (r >= nrhs) {                 // the unused RHS slot of a 1-RHS solve
     if (rank0 && tid == 0) {
       S->active[r] = 0; S->count[r] = 0; S->brk[r] = 0; S->brk_j[r] = -1; S->iter[r] = 0;
-      S->eta[r] = S->eta0[r] = S->qq[r] = 0.0;
+      S->eta[r] = S->eta0[r] = S->qq[r] = S->pp[r] = 0.0;
       S->delta_min[r] = __longlong_as_double(0x7ff0000000000000ll);
     }
     return;
@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_init(PrecondDev pc, int nrhs, 
     S->eta[r] = eta;
     S->eta0[r] = eta;
     S->qq[r] = qq;
+    S->pp[r] = eta;            // p_0 = s_0
     S->delta_min[r] = __longlong_as_double(0x7ff0000000000000ll);
     S->active[r] = eta > 0.0;
     S->count[r] = 0;
@@ -350,7 +351,8 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_init(PrecondDev pc, int nrhs, 
 constexpr int kVecPerThread = 8;   // npad <= kTW * 32 * 8 = 4096
 template <typename T>
 __global__ void __launch_bounds__(kTW * 32) k_pcg_step(PrecondDev pc, PcgVecs v, const double* __restrict__ passout,
-                                                       PcgState* __restrict__ S, int nrhs, int rule, int next_q) {
+                                                       PcgState* __restrict__ S, int nrhs, int rule, int next_q,
+                                                       int variant) {
   __shared__ double s_alpha, s_beta, s_delta;
   __shared__ int s_upd, s_cont, s_brk, s_exit;
   TrsvSm sm = trsv_carve(pc.npad);
@@ -366,8 +368,10 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_step(PrecondDev pc, PcgVecs v,
     s_brk = 0;
     s_exit = 0;
     s_alpha = 0.0;
-    const double tau = passout[(size_t)nrhs * n + r];
-    const double delta = tau - sig2 * S->qq[r];            // l.194 with the operator of l.324
+    // l.194: delta = p^T C p = t^T t - sigma^2 q^T q with the operator of l.324 (variant 0),
+    // or p^T p - sigma^2 q^T q as printed (variant 1, the exact-R identity of l.206)
+    const double tau = variant == 0 ? passout[(size_t)nrhs * n + r] : S->pp[r];
+    const double delta = tau - sig2 * S->qq[r];
     s_delta = delta;
     if (!isfinite(delta) || delta == 0.0) {                 // loop guard l.192 (R3)
       s_exit = 1;
@@ -398,7 +402,8 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_step(PrecondDev pc, PcgVecs v,
     if (i < n) {
       const double q = v.q[off + i];
       if (rank0) v.omega[off + i] = fma(al, q, v.omega[off + i]);
-      yv = (passout[off + i] - sig2 * q) * pc.dinv[i];
+      // variant 0: w = P^{-T}(A^T t - sigma^2 q); variant 1: solve P^{-T} q (l.197)
+      yv = (variant == 0 ? passout[off + i] - sig2 * q : q) * pc.dinv[i];
     }
     sm.y[i] = yv;
   }
@@ -411,7 +416,9 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_step(PrecondDev pc, PcgVecs v,
     const int i = tid + k * (int)blockDim.x;
     sn[k] = 0.0;
     if (i < n) {
-      sn[k] = fma(-al, sm.y[i], v.s[off + i]);
+      // w = solve result (variant 0) or p - sigma^2 P^{-T} q (variant 1, l.197-198)
+      const double w = variant == 0 ? sm.y[i] : fma(-sig2, sm.y[i], v.p[off + i]);
+      sn[k] = fma(-al, w, v.s[off + i]);
       e = fma(sn[k], sn[k], e);
     }
   }
@@ -427,13 +434,16 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_step(PrecondDev pc, PcgVecs v,
   const bool cont = s_cont;
   const double be = s_beta;
   // p = s + beta p (l.201)
+  double ppl = 0.0;
 #pragma unroll
   for (int k = 0; k < kVecPerThread; ++k) {
     const int i = tid + k * (int)blockDim.x;
     pn[k] = 0.0;
     if (cont && i < n) pn[k] = fma(be, v.p[off + i], sn[k]);
     if (i < npad) sm.y[i] = pn[k];
+    ppl = fma(pn[k], pn[k], ppl);
   }
+  const double ppn = block_sum(ppl, sm.red);
   cluster_sync_all();   // every CTA has read the old s and p
   if (rank0) {
 #pragma unroll
@@ -447,7 +457,7 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_step(PrecondDev pc, PcgVecs v,
     if (tid == 0) {
       S->count[r] = count0 + 1;
       S->iter[r] = iter0 + 1;
-      if (cont) S->eta[r] = etan;
+      if (cont) { S->eta[r] = etan; S->pp[r] = ppn; }
       else S->active[r] = 0;
     }
   }
@@ -585,10 +595,11 @@ int launch_pcg_init(const PrecondDev& pc, int nrhs, PcgVecs v, PcgState* S, cuda
 }
 
 int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgState* S, int nrhs, int rule,
-                    int next_q, cudaStream_t st) {
+                    int next_q, int variant, cudaStream_t st) {
   const size_t sm = trsv_smem(pc.npad);
   int rc = 0;
-  TLS_DISPATCH_UF(pc.u_f, { rc = launch_cluster(k_pcg_step<T>, nrhs, sm, st, pc, v, passout, S, nrhs, rule, next_q); });
+  TLS_DISPATCH_UF(pc.u_f, { rc = launch_cluster(k_pcg_step<T>, nrhs, sm, st, pc, v, passout, S, nrhs, rule, next_q,
+                                                variant); });
   return rc;
 }
 

@@ -756,7 +756,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   if (!R || R->dev.n != A->n || !x_out || (A->m_local > 0 && !b)) { set_error("bad rqi args"); return TLS_ERR_ARG; }
   tls_rqi_opts_t o;
   if (opts) o = *opts; else tls_rqi_opts_default(&o);
-  if (o.op_variant != 0) { set_error("op_variant 1 (paper A-free PCGTLS) not in this build"); return TLS_ERR_UNSUPPORTED; }
+  if (o.op_variant != 0 && o.op_variant != 1) { set_error("op_variant must be 0 (A-in-loop) or 1 (paper Alg. 3)"); return TLS_ERR_ARG; }
   if (o.max_outer < 1) o.max_outer = 1;
   Work w;
   if (!carve_ok(A, ws, ws_bytes, w, false)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
@@ -784,12 +784,15 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   };
   // PCG iterations j = 0..budget-1 with device-side predication; with a large
   // budget the host polls the activity flags every 8 iterations.
-  auto pcg_loop = [&](int nrhs, int budget) -> int {
+  // variant 0: one batched operator pass over A per iteration (R1); variant 1: the
+  // paper's A-free Alg. 3 (no pass).  The sigma = 0 bootstrap always uses variant 0.
+  auto pcg_loop = [&](int nrhs, int budget, int variant) -> int {
     for (int j = 0; j < budget; ++j) {
-      TLS_TRY(run_pass(cx, A, PASS_OPERATOR, nrhs, w.vec.q, nullptr, w, w.S->active));
+      if (variant == 0) TLS_TRY(run_pass(cx, A, PASS_OPERATOR, nrhs, w.vec.q, nullptr, w, w.S->active));
       {
         ProfScope ps(TLS_PROF_PCG_STEP, cx.st);
-        TLS_TRY(launch_pcg_step(pc, w.vec, w.passout, w.S, nrhs, o.breakdown_rule, j + 1 < budget ? 1 : 0, cx.st));
+        TLS_TRY(launch_pcg_step(pc, w.vec, w.passout, w.S, nrhs, o.breakdown_rule, j + 1 < budget ? 1 : 0, variant,
+                                cx.st));
       }
       cx.launches += 1;
       if (budget > 16 && (j % 8) == 7) {
@@ -822,7 +825,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
       TLS_TRY(launch_pcg_init(pc, 1, w.vec, w.S, cx.st));
     }
     cx.launches += 1;
-    TLS_TRY(pcg_loop(1, o.boot_max));
+    TLS_TRY(pcg_loop(1, o.boot_max, 0));
     TLS_TRY(read_state());
     boot_iters = hS.count[0];
     k_copy<<<(n + 255) / 256, 256, 0, cx.st>>>(w.vec.omega, w.x0, n);
@@ -881,7 +884,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
     }
     cx.launches += 1;
     tr.mark("pcg_init");
-    TLS_TRY(pcg_loop(2, budget));
+    TLS_TRY(pcg_loop(2, budget, o.op_variant));
     tr.mark("pcg_loop");
     TLS_TRY(read_state());
     pcgc.push_back(hS.count[0]);

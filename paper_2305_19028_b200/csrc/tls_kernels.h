@@ -99,7 +99,7 @@ size_t precond_bytes(int n, int u_f);
 
 // ---- triangular solves, PCG and RQI vector kernels (k_trsv.cu) -------------------------
 struct PcgState {
-  double eta[2], eta0[2], qq[2], delta_min[2];
+  double eta[2], eta0[2], qq[2], pp[2], delta_min[2];
   double sigma2, g, psi, xx, tol2;
   int active[2], count[2], brk[2], brk_j[2];
   int iter[2];    // iteration index j of the next step, per RHS
@@ -111,8 +111,11 @@ int launch_precond_apply(const PrecondDev& pc, int trans, int nrhs, double* Y, i
                          cudaStream_t st);
 int launch_pcg_init(const PrecondDev& pc, int nrhs, PcgVecs v, PcgState* S, cudaStream_t st);
 // One CTA per RHS; an RHS whose active flag is 0 is left untouched.
+// variant 0: A-in-loop operator (R1; passout = the operator pass); variant 1: the
+// paper's A-free Alg. 3 (delta = p^T p - sigma^2 q^T q, w = p - sigma^2 P^{-T} q;
+// passout unused).
 int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgState* S, int nrhs,
-                    int breakdown_rule, int compute_next_q, cudaStream_t st);
+                    int breakdown_rule, int compute_next_q, int variant, cudaStream_t st);
 // step record: sigma2, f (stored as rhs0 = -f), g, psi; copies x into rhs1.
 int launch_rqi_eval(const PrecondDev& pc, const double* passout, const double* x, PcgVecs v,
                     PcgState* S, cudaStream_t st);

@@ -338,3 +338,20 @@ def test_cfg4_full_size(T, name):
         assert abs(rqi.certify_sigma(A, b, x.cpu().numpy()) - sig) / sig <= 1e-12
     else:
         assert res.status == rqi.PCG_BREAKDOWN and info["breakdown_k"] == 1
+
+
+@pytest.mark.parametrize("name,fmt", [("cfg1", "fp16"), ("cfg1", "bf16"), ("cfg2w", "fp16"), ("cfg2w", "bf16"),
+                                      ("cfg2w", "fp64")])
+def test_rqi_parity_paper_operator(T, name, fmt):
+    """op_variant = 1: the paper's A-free Alg. 3 on
+    the GPU against the oracle's `paper` variant with the same R~: identical status,
+    termination, RQI and PCG counts; x, sigma to the north_star tolerances when converged."""
+    P = tlsgen.config(name)
+    pc = rqi.factor_precond(P.A, fmt)
+    res_or = rqi.rqi_pcgtls_mp(P.A, P.b, pc, opts=rqi.RqiOptions(op_variant=1))
+    R = T.tls_precond_import(pc.Rt, pc.d, pc.normA2, fmt)
+    rc, x, sig, info = T.tls_rqi_pcgtls(T.matrix(dev(P.A)), dev(P.b), R,
+                                        opts=T.tls_rqi_opts_default(op_variant=1))
+    _check_solve(info, x.cpu().numpy(), sig, res_or)
+    for a, b in zip(info["sigma2_trace"], res_or.sigma2_trace):
+        assert a == pytest.approx(b, rel=1e-9)

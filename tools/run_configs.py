@@ -26,12 +26,13 @@ from paper_2305_19028_b200 import tlsrqi as T
 UROUND = {"fp16": 2.0 ** -11, "bf16": 2.0 ** -8, "fp32": 2.0 ** -24, "fp64": 2.0 ** -53}
 
 
-def run(M, b, u_f, reps, ws):
+def run(M, b, u_f, reps, ws, op_variant=0):
+    opts = T.tls_rqi_opts_default(op_variant=op_variant)
     def once():
         rc, R, fi = T.tls_factor_precond(M, u_f, ws=ws)
         if R is None:
             return rc, None, None, fi, None
-        rc2, x, sig, info = T.tls_rqi_pcgtls(M, b, R, ws=ws)
+        rc2, x, sig, info = T.tls_rqi_pcgtls(M, b, R, ws=ws, opts=opts)
         return rc2, x, sig, fi, info
     once()
     times = []
@@ -46,7 +47,7 @@ def run(M, b, u_f, reps, ws):
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) / 1e3)
     rc, x, sig, fi, info = out
-    rec = {"u_f": u_f, "tts_s": statistics.median(times), "status": T.STATUS.get(rc, rc)}
+    rec = {"u_f": u_f, "op_variant": op_variant, "tts_s": statistics.median(times), "status": T.STATUS.get(rc, rc)}
     if info is None:
         rec.update({"chol_pivot": fi["chol_pivot"], "factor_status": fi["status_name"]})
         return rec, None
@@ -56,13 +57,13 @@ def run(M, b, u_f, reps, ws):
     return rec, x
 
 
-def dense(P, u_f, reps):
+def dense(P, u_f, reps, op_variant=0):
     A = P.A if torch.is_tensor(P.A) else torch.as_tensor(P.A)
     A = A.to("cuda")
     b = (P.b if torch.is_tensor(P.b) else torch.as_tensor(P.b)).to("cuda")
     M = T.matrix(A)
     ws = T.workspace(M)
-    rec, x = run(M, b, u_f, reps, ws)
+    rec, x = run(M, b, u_f, reps, ws, op_variant)
     rec.update({"m": int(A.shape[0]), "n": int(A.shape[1])})
     return rec
 
@@ -87,6 +88,11 @@ def main():
         P = tlsgen.config(name, device=dev, keep_factors=False) if dev == "cuda" else tlsgen.config(name)
         for u_f in ([P.u_f, "bf16"] if name.startswith("cfg4") else [P.u_f]):
             rec = dense(P, u_f, args.reps)
+            rec["config"] = name
+            res["runs"].append(rec)
+            print(json.dumps(rec), flush=True)
+        if name in ("cfg1", "cfg2w", "cfg4w"):     # the paper's A-free operator
+            rec = dense(P, P.u_f, args.reps, op_variant=1)
             rec["config"] = name
             res["runs"].append(rec)
             print(json.dumps(rec), flush=True)
