@@ -54,7 +54,84 @@ size_t pass_partials_doubles(const DenseView& A) {
   return (size_t)pass_grid(A) * (size_t)(2 * A.n + 2);
 }
 
-template <int NRHS, int MODE, int CPT>
+// One group of RB rows of the current stage: row dot products t_r = a_i . q_r (thread
+// partials over its column chunks, warp transpose-reduce, one shared-memory exchange
+// across the consumer warps), then v_r += t_r a_i.  FULL: all RB rows and all column
+// chunks exist (no predicates).  `stt` = this thread's first element of row rb.
+template <int NRHS, int MODE, int CPT, int RB, bool FULL>
+__device__ __forceinline__ void pass_group(const double* __restrict__ stt, int64_t ld, int rb, int rows, int64_t rs,
+                                           const double* __restrict__ b, const double2 (&qr)[NRHS][CPT],
+                                           double2 (&acc)[NRHS][CPT], const bool (&okc)[CPT], const bool (&ok1)[CPT],
+                                           double* red, double* tfin, int warp, int lane, int tid, double& sacc,
+                                           double& sacc2) {
+  constexpr int V = RB * NRHS;
+  double2 a[RB][CPT];
+  double part[V];
+  // residual mode: the thread that finishes row (rb + tid) loads b_i now, so the load is in
+  // flight during the dot products instead of between the two barriers
+  double bpre = 0.0;
+  if (MODE == PASS_RESIDUAL && tid < V && (FULL || rb + tid < rows)) bpre = b[rs + rb + tid];
+#pragma unroll
+  for (int rr = 0; rr < RB; ++rr) {
+    const double2* rowp = reinterpret_cast<const double2*>(stt + (size_t)rr * ld);
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      if (FULL) {
+        a[rr][c] = rowp[c * kPassConsumers];
+      } else {
+        double2 v = make_double2(0.0, 0.0);
+        if (rb + rr < rows && okc[c]) {
+          v = rowp[c * kPassConsumers];
+          if (!ok1[c]) v.y = 0.0;
+        }
+        a[rr][c] = v;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) {
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        d0 = fma(a[rr][c].x, qr[r][c].x, d0);
+        d1 = fma(a[rr][c].y, qr[r][c].y, d1);
+      }
+      part[rr * NRHS + r] = d0 + d1;
+    }
+  }
+  warp_transpose_reduce<V>(part, lane);
+  if ((lane & (32 / V - 1)) == 0) red[warp * 16 + transpose_reduce_index<V>(lane)] = part[0];
+  named_bar_sync(1, kPassConsumers);
+  if (tid < V) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kPassWarps; ++w) t += red[w * 16 + tid];
+    const int row = rb + tid / NRHS;
+    if (!FULL && row >= rows) {
+      t = 0.0;
+    } else if (MODE == PASS_RESIDUAL) {
+      const double bi = bpre;   // NRHS == 1: row = rb + tid
+      t = bi - t;
+      sacc2 = fma(bi, t, sacc2);
+    }
+    sacc = fma(t, t, sacc);
+    tfin[tid] = t;
+  }
+  named_bar_sync(1, kPassConsumers);
+#pragma unroll
+  for (int rr = 0; rr < RB; ++rr) {
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) {
+      const double t = tfin[rr * NRHS + r];
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        acc[r][c].x = fma(t, a[rr][c].x, acc[r][c].x);
+        acc[r][c].y = fma(t, a[rr][c].y, acc[r][c].y);
+      }
+    }
+  }
+}
+
+template <int NRHS, int MODE, int CPT, bool FC>
 __global__ void __launch_bounds__(kPassThreads, 1)
 k_pass(const double* __restrict__ A, int64_t m, int n, int64_t ld, int rps,
        const double* __restrict__ q, const double* __restrict__ b,
@@ -102,7 +179,7 @@ k_pass(const double* __restrict__ A, int64_t m, int n, int64_t ld, int rps,
   }
 
   // ---------------- consumers
-  constexpr int RB = (CPT >= 8) ? 1 : 8 / CPT;  // rows per reduction group
+  constexpr int RB = (CPT >= 8) ? 1 : 8 / CPT;  // rows per reduction group (divides rows per stage)
   constexpr int V = RB * NRHS;
   const int nchunks = (n + 1) >> 1;
 
@@ -150,65 +227,16 @@ k_pass(const double* __restrict__ A, int64_t m, int n, int64_t ld, int rps,
         }
       }
     } else {
-      for (int rb = 0; rb < rows; rb += RB) {
-        double2 a[RB][CPT];
-        double part[V];
-#pragma unroll
-        for (int rr = 0; rr < RB; ++rr) {
-          const bool rv = rb + rr < rows;
-          const double2* rowp = reinterpret_cast<const double2*>(st + (size_t)(rb + rr) * ld);
-#pragma unroll
-          for (int c = 0; c < CPT; ++c) {
-            double2 v = make_double2(0.0, 0.0);
-            if (rv && okc[c]) {
-              v = rowp[tid + c * kPassConsumers];
-              if (!ok1[c]) v.y = 0.0;
-            }
-            a[rr][c] = v;
-          }
-#pragma unroll
-          for (int r = 0; r < NRHS; ++r) {
-            double d = 0.0;
-#pragma unroll
-            for (int c = 0; c < CPT; ++c) {
-              d = fma(a[rr][c].x, qr[r][c].x, d);
-              d = fma(a[rr][c].y, qr[r][c].y, d);
-            }
-            part[rr * NRHS + r] = d;
-          }
-        }
-        warp_transpose_reduce<V>(part, lane);
-        if ((lane & (32 / V - 1)) == 0) red[warp * 16 + transpose_reduce_index<V>(lane)] = part[0];
-        named_bar_sync(1, kPassConsumers);
-        if (tid < V) {
-          double t = 0.0;
-#pragma unroll
-          for (int w = 0; w < kPassWarps; ++w) t += red[w * 16 + tid];
-          const int row = rb + tid / NRHS;
-          if (row >= rows) {
-            t = 0.0;
-          } else if (MODE == PASS_RESIDUAL) {
-            const double bi = b[rs + row];
-            t = bi - t;
-            sacc2 = fma(bi, t, sacc2);
-          }
-          sacc = fma(t, t, sacc);
-          tfin[tid] = t;
-        }
-        named_bar_sync(1, kPassConsumers);
-#pragma unroll
-        for (int rr = 0; rr < RB; ++rr) {
-#pragma unroll
-          for (int r = 0; r < NRHS; ++r) {
-            const double t = tfin[rr * NRHS + r];
-#pragma unroll
-            for (int c = 0; c < CPT; ++c) {
-              acc[r][c].x = fma(t, a[rr][c].x, acc[r][c].x);
-              acc[r][c].y = fma(t, a[rr][c].y, acc[r][c].y);
-            }
-          }
-        }
+      // full row groups without predicates (FC: every column chunk exists), then the tail
+      int rb = 0;
+      if (FC) {
+        for (; rb + RB <= rows; rb += RB)
+          pass_group<NRHS, MODE, CPT, RB, true>(st + (size_t)rb * ld + 2 * tid, ld, rb, rows, rs, b, qr, acc, okc, ok1,
+                                               red, tfin, warp, lane, tid, sacc, sacc2);
       }
+      for (; rb < rows; rb += RB)
+        pass_group<NRHS, MODE, CPT, RB, false>(st + (size_t)rb * ld + 2 * tid, ld, rb, rows, rs, b, qr, acc, okc, ok1,
+                                              red, tfin, warp, lane, tid, sacc, sacc2);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -251,11 +279,13 @@ k_pass(const double* __restrict__ A, int64_t m, int n, int64_t ld, int rps,
 template <int NRHS, int MODE, int CPT>
 static int launch_pass_t(const DenseView& A, const double* q, const double* b, double* partials,
                          int W, const int* active, cudaStream_t st, int G) {
-  auto kern = k_pass<NRHS, MODE, CPT>;
-  static bool attr = false;
-  if (!attr) {
+  // FC: n fills every thread's CPT column chunks exactly (n = 2 * CPT * consumers)
+  const bool fc = (A.n == 2 * CPT * kPassConsumers);
+  auto kern = fc ? k_pass<NRHS, MODE, CPT, true> : k_pass<NRHS, MODE, CPT, false>;
+  static bool attr[2] = {false, false};
+  if (!attr[fc]) {
     TLS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem));
-    attr = true;
+    attr[fc] = true;
   }
   kern<<<G, kPassThreads, kPassSmem, st>>>(A.A, A.m, A.n, A.ld, rows_per_stage(A), q, b, partials, W,
                                            active);

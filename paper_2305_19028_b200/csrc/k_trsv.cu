@@ -304,6 +304,9 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_init(PrecondDev pc, int nrhs, 
       S->eta[r] = S->eta0[r] = S->qq[r] = S->pp[r] = 0.0;
       S->delta_min[r] = __longlong_as_double(0x7ff0000000000000ll);
     }
+    // the unused q slot is read by the (2-RHS) operator pass: keep it zero
+    if (rank0)
+      for (int i = tid; i < pc.n; i += blockDim.x) v.q[(size_t)r * pc.n + i] = 0.0;
     return;
   }
   const size_t off = (size_t)r * n;
@@ -352,7 +355,7 @@ constexpr int kVecPerThread = 8;   // npad <= kTW * 32 * 8 = 4096
 template <typename T>
 __global__ void __launch_bounds__(kTW * 32) k_pcg_step(PrecondDev pc, PcgVecs v, const double* __restrict__ passout,
                                                        PcgState* __restrict__ S, int nrhs, int rule, int next_q,
-                                                       int variant) {
+                                                       int variant, int pass_nrhs) {
   __shared__ double s_alpha, s_beta, s_delta;
   __shared__ int s_upd, s_cont, s_brk, s_exit;
   TrsvSm sm = trsv_carve(pc.npad);
@@ -370,7 +373,7 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_step(PrecondDev pc, PcgVecs v,
     s_alpha = 0.0;
     // l.194: delta = p^T C p = t^T t - sigma^2 q^T q with the operator of l.324 (variant 0),
     // or p^T p - sigma^2 q^T q as printed (variant 1, the exact-R identity of l.206)
-    const double tau = variant == 0 ? passout[(size_t)nrhs * n + r] : S->pp[r];
+    const double tau = variant == 0 ? passout[(size_t)pass_nrhs * n + r] : S->pp[r];
     const double delta = tau - sig2 * S->qq[r];
     s_delta = delta;
     if (!isfinite(delta) || delta == 0.0) {                 // loop guard l.192 (R3)
@@ -595,11 +598,11 @@ int launch_pcg_init(const PrecondDev& pc, int nrhs, PcgVecs v, PcgState* S, cuda
 }
 
 int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgState* S, int nrhs, int rule,
-                    int next_q, int variant, cudaStream_t st) {
+                    int next_q, int variant, int pass_nrhs, cudaStream_t st) {
   const size_t sm = trsv_smem(pc.npad);
   int rc = 0;
   TLS_DISPATCH_UF(pc.u_f, { rc = launch_cluster(k_pcg_step<T>, nrhs, sm, st, pc, v, passout, S, nrhs, rule, next_q,
-                                                variant); });
+                                                variant, pass_nrhs); });
   return rc;
 }
 

@@ -788,11 +788,14 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   // paper's A-free Alg. 3 (no pass).  The sigma = 0 bootstrap always uses variant 0.
   auto pcg_loop = [&](int nrhs, int budget, int variant) -> int {
     for (int j = 0; j < budget; ++j) {
-      if (variant == 0) TLS_TRY(run_pass(cx, A, PASS_OPERATOR, nrhs, w.vec.q, nullptr, w, w.S->active));
+      // the 2-RHS dense kernel is faster than the 1-RHS one at the same bytes (measured, see
+      // DESIGN §6): a 1-RHS solve passes its q with the second slot held at zero
+      const int pass_rhs = (nrhs == 1 && !is_csr(A)) ? 2 : nrhs;
+      if (variant == 0) TLS_TRY(run_pass(cx, A, PASS_OPERATOR, pass_rhs, w.vec.q, nullptr, w, w.S->active));
       {
         ProfScope ps(TLS_PROF_PCG_STEP, cx.st);
         TLS_TRY(launch_pcg_step(pc, w.vec, w.passout, w.S, nrhs, o.breakdown_rule, j + 1 < budget ? 1 : 0, variant,
-                                cx.st));
+                                pass_rhs, cx.st));
       }
       cx.launches += 1;
       if (budget > 16 && (j % 8) == 7) {

@@ -114,8 +114,9 @@ int launch_pcg_init(const PrecondDev& pc, int nrhs, PcgVecs v, PcgState* S, cuda
 // variant 0: A-in-loop operator (R1; passout = the operator pass); variant 1: the
 // paper's A-free Alg. 3 (delta = p^T p - sigma^2 q^T q, w = p - sigma^2 P^{-T} q;
 // passout unused).
+// pass_nrhs: the RHS count of the operator pass that filled passout (layout [v_0..v_{pass_nrhs-1}, tau..]).
 int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgState* S, int nrhs,
-                    int breakdown_rule, int compute_next_q, int variant, cudaStream_t st);
+                    int breakdown_rule, int compute_next_q, int variant, int pass_nrhs, cudaStream_t st);
 // step record: sigma2, f (stored as rhs0 = -f), g, psi; copies x into rhs1.
 int launch_rqi_eval(const PrecondDev& pc, const double* passout, const double* x, PcgVecs v,
                     PcgState* S, cudaStream_t st);
