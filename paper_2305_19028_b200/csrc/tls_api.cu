@@ -85,7 +85,7 @@ struct tls_precond_s {
 };
 
 static int allreduce(tls_comm_t comm, double* buf, size_t count, int op, cudaStream_t st) {
-  if (comm == nullptr || comm->nranks <= 1 || count == 0) return 0;
+  if (comm == nullptr || comm->comm == nullptr || count == 0) return 0;
   NcclApi* api = nccl_api();
   const int r = api->AllReduce(buf, buf, count, ncclFloat64, op, comm->comm, st);
   if (r != ncclSuccess) {
@@ -97,7 +97,7 @@ static int allreduce(tls_comm_t comm, double* buf, size_t count, int op, cudaStr
 
 // int64 sum (exact, order-free): the fixed-point limbs of the CSR fp16 Gram
 static int allreduce_i64(tls_comm_t comm, void* buf, size_t count, cudaStream_t st) {
-  if (comm == nullptr || comm->nranks <= 1 || count == 0) return 0;
+  if (comm == nullptr || comm->comm == nullptr || count == 0) return 0;
   NcclApi* api = nccl_api();
   const int r = api->AllReduce(buf, buf, count, ncclInt64, ncclSum, comm->comm, st);
   if (r != ncclSuccess) {
@@ -393,7 +393,7 @@ int run_gram(Ctx& cx, const tls_matrix_t* A, int u_f, const double* dinv, int K_
   const int n = (int)A->n;
   ProfScope ps(TLS_PROF_GRAM, cx.st);
   if (is_csr(A)) {
-    const bool ranks = cx.comm != nullptr && cx.comm->nranks > 1;
+    const bool ranks = cx.comm != nullptr && cx.comm->comm != nullptr;
     if (u_f == TLS_FP16 && ranks) {
       // exact fixed-point limbs are summed over ranks as int64 (exact, order-free), then rounded once
       TLS_TRY(launch_csr_gram(csr_view(A), u_f, dinv, w.G, w.gram_ws, w.gram_ws_doubles * 8, &w.flags[1], cx.st,
@@ -561,7 +561,10 @@ int tls_comm_init(int nranks, int rank, const void* id_host, int device, tls_com
   if (!out || nranks < 1 || rank < 0 || rank >= nranks) { set_error("bad comm args"); return TLS_ERR_ARG; }
   TLS_CUDA_TRY(cudaSetDevice(device));
   tls_comm_s* c = new tls_comm_s{nullptr, nranks, rank, device};
-  if (nranks > 1) {
+  // one rank needs no communicator; TLS_FORCE_NCCL=1 creates one anyway so that every
+  // all-reduce of the solve goes through NCCL (single-GPU test of the multi-GPU path)
+  const char* force = getenv("TLS_FORCE_NCCL");
+  if (nranks > 1 || (force && force[0] == '1')) {
     NcclApi* api = nccl_api();
     if (!api) { delete c; set_error("libnccl.so.2 not loadable"); return TLS_ERR_NCCL; }
     ncclUniqueId id;

@@ -355,3 +355,53 @@ def test_rqi_parity_paper_operator(T, name, fmt):
     _check_solve(info, x.cpu().numpy(), sig, res_or)
     for a, b in zip(info["sigma2_trace"], res_or.sigma2_trace):
         assert a == pytest.approx(b, rel=1e-9)
+
+
+def test_nccl_path_single_rank(T, monkeypatch):
+    """The multi-GPU plumbing on one GPU: a real 1-rank NCCL communicator
+    (TLS_FORCE_NCCL=1) routes every all-reduce of the factor and the solve (column
+    max/sums, Gram, the 2n+2 / n+2 pass results, the CSR int64 Gram limbs) through
+    ncclAllReduce; with one rank the results must be bitwise those of comm = NULL."""
+    monkeypatch.setenv("TLS_FORCE_NCCL", "1")
+    uid = T.tls_comm_get_unique_id()
+    comm = T.tls_comm_init(1, 0, uid, torch.cuda.current_device())
+    try:
+        P = tlsgen.config("cfg2w")
+        M = T.matrix(dev(P.A))
+        b = dev(P.b)
+        rc0, R0, _ = T.tls_factor_precond(M, "bf16")
+        _, x0, s0, i0 = T.tls_rqi_pcgtls(M, b, R0)
+        rc1, R1, _ = T.tls_factor_precond(M, "bf16", comm=comm)
+        _, x1, s1, i1 = T.tls_rqi_pcgtls(M, b, R1, comm=comm)
+        assert torch.equal(x0, x1) and s0 == s1 and i0["pcg_iters"] == i1["pcg_iters"]
+        Pc = tlsgen.csr_problem(m=20000, n=300, per_row=10, seed=3)
+        Mc = T.matrix_csr(torch.as_tensor(Pc.rowptr, device="cuda"), torch.as_tensor(Pc.colidx, device="cuda"),
+                          torch.as_tensor(Pc.vals, device="cuda"), Pc.n)
+        bc = dev(Pc.b)
+        _, Rc0, _ = T.tls_factor_precond(Mc, "fp16")
+        _, xc0, sc0, _ = T.tls_rqi_pcgtls(Mc, bc, Rc0)
+        _, Rc1, _ = T.tls_factor_precond(Mc, "fp16", comm=comm)
+        _, xc1, sc1, _ = T.tls_rqi_pcgtls(Mc, bc, Rc1, comm=comm)
+        assert torch.equal(xc0, xc1) and sc0 == sc1
+    finally:
+        T.tls_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("m,n,fmt", [(2, 1, "fp16"), (40, 1, "fp64"), (300, 37, "bf16"), (97, 33, "fp16"),
+                                     (5000, 65, "fp32")])
+def test_edge_shapes_end_to_end(T, m, n, fmt):
+    """Degenerate and ragged shapes through the whole path (n = 1, m = n + 1, odd n with a
+    padded column in the operand, n one past a tile / block edge): status, counts, x and
+    sigma against the oracle on the GPU's own R~, and against the SVD."""
+    rng = np.random.default_rng(m * 7 + n)
+    A = rng.standard_normal((m, n)) * np.logspace(0, -1, n)[None, :]
+    b = A @ rng.standard_normal(n) + 1e-3 * rng.standard_normal(m) / np.sqrt(m)
+    Ad = T.dense_operand(dev(A))
+    M = T.matrix(Ad, n=n)
+    rc, R, _ = T.tls_factor_precond(M, fmt)
+    assert rc == 0
+    rc, x, sig, info = T.tls_rqi_pcgtls(M, dev(b), R)
+    Rt, d, nrm = T.tls_precond_export(R)
+    res = rqi.rqi_pcgtls_mp(A, b, rqi.Precond(Rt, d, fmt, nrm))
+    ex = exact.tls_svd(A, b)
+    _check_solve(info, x.cpu().numpy(), sig, res, ex if res.status == rqi.OK else None)
