@@ -25,10 +25,16 @@ static void gram_shape(const DenseView& A, int K_t, int& TT, int& ntiles, int& n
   if (nsplit < 1) nsplit = 1;
 }
 
+static void gram_shape_f64(const DenseView& A, int& TT, int& ntiles, int& nsplit);
+constexpr int kGT2_ = 128;
 size_t gram_ws_doubles(const DenseView& A, int K_t) {
   int TT, nt, nc, ns;
   gram_shape(A, K_t, TT, nt, nc, ns);
-  const size_t cc = (size_t)ns * nt * kGT * kGT;
+  int T2, nt2, ns2;
+  gram_shape_f64(A, T2, nt2, ns2);
+  size_t cc = (size_t)ns * nt * kGT * kGT;
+  const size_t c2 = (size_t)ns2 * nt2 * kGT2_ * kGT2_;
+  if (c2 > cc) cc = c2;
   const size_t tc = (gram_tc_ws_bytes(A.m, A.n, 64) + 7) / 8;
   return cc > tc ? cc : tc;
 }
@@ -118,17 +124,110 @@ k_gram_cc(const double* __restrict__ A, int64_t m, int n, int64_t ld, const doub
     for (int j = 0; j < 4; ++j) out[(ty * 4 + i) * kGT + tx * 4 + j] = dacc[i][j];
 }
 
-// Sum the split partials in fixed order; write the tile and its mirror image.
-__global__ void k_gram_reduce(const double* __restrict__ part, int ntiles, int nsplit, int TT, int n,
-                              double* __restrict__ G) {
+// u_f in {fp32, fp64}: the products of u_f values are accumulated in fp64 throughout
+// (R10: no fp32 level), so the chunk structure is irrelevant and each CTA sums its
+// whole row split.  128 x 128 upper tiles, 8 x 8 fp64 accumulators per thread, 16-row
+// K-steps staged in shared memory with the next step's global loads (16-byte, rounded
+// to u_f on the fly) in flight during the current step's 16 x 64 DFMAs.
+constexpr int kGT2 = 128, kGK2 = 16, kGP2 = kGT2 + 4;
+template <int PREC>
+__global__ void __launch_bounds__(256, 1)
+k_gram_f64(const double* __restrict__ A, int64_t m, int n, int64_t ld, const double* __restrict__ dinv,
+           int nsplit, int TT, double* __restrict__ part, int* __restrict__ range) {
+  __shared__ __align__(16) double As[kGK2][kGP2];
+  __shared__ __align__(16) double Bs[kGK2][kGP2];
   int t = blockIdx.x, I = 0;
   while (t >= TT - I) { t -= TT - I; ++I; }
   const int J = I + t;
-  for (int e = threadIdx.x; e < kGT * kGT; e += blockDim.x) {
-    const int i = e / kGT, j = e % kGT;
-    const int gi = I * kGT + i, gj = J * kGT + j;
+  const bool diag = (I == J);
+  const int s = blockIdx.y;
+  const int64_t rb = m * s / nsplit, re = m * (s + 1) / nsplit;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int I0 = I * kGT2, J0 = J * kGT2;
+  // staging map: thread -> (row lr = tid / 16, columns lc + 16 q): lanes read consecutive
+  // doubles from global and write consecutive shared-memory words (no bank conflicts)
+  const int lr = tid >> 4, lc = tid & 15;
+  double acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  int bad = 0;
+  // raw fp64 loads of the next step are kept in registers and only rounded (and scaled)
+  // when they are staged, so the loads stay in flight during the current step's math
+  double pa[8], pb[8];
+  auto fetch = [&](int64_t r) {
+    const int64_t row = r + lr;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int ca = I0 + lc + 16 * q, cb = J0 + lc + 16 * q;
+      pa[q] = (row < re && ca < n) ? __ldcs(A + row * ld + ca) : 0.0;
+      pb[q] = (!diag && row < re && cb < n) ? __ldcs(A + row * ld + cb) : 0.0;
+    }
+  };
+  if (rb < re) fetch(rb);
+  for (int64_t r = rb; r < re; r += kGK2) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int ca = I0 + lc + 16 * q, cb = J0 + lc + 16 * q;
+      const double va = ca < n ? round_uf(pa[q] * dinv[ca], PREC) : 0.0;
+      bad |= !isfinite(va);
+      As[lr][lc + 16 * q] = va;
+      if (!diag) {
+        const double vb = cb < n ? round_uf(pb[q] * dinv[cb], PREC) : 0.0;
+        bad |= !isfinite(vb);
+        Bs[lr][lc + 16 * q] = vb;
+      }
+    }
+    __syncthreads();
+    if (r + kGK2 < re) fetch(r + kGK2);       // next step's loads overlap this step's math
+    const double(*Bp)[kGP2] = diag ? As : Bs;
+#pragma unroll 4
+    for (int k = 0; k < kGK2; ++k) {
+      double a[8], bv[8];
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        const double2 t2 = *reinterpret_cast<const double2*>(&As[k][ty * 8 + i]);
+        a[i] = t2.x;
+        a[i + 1] = t2.y;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) bv[j] = Bp[k][tx + 16 * j];      // consecutive lanes, no conflicts
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  if (bad) atomicExch(range, 1);
+  double* out = part + ((size_t)s * gridDim.x + blockIdx.x) * (kGT2 * kGT2);
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) out[(ty * 8 + i) * kGT2 + tx + 16 * j] = acc[i][j];
+}
+
+static void gram_shape_f64(const DenseView& A, int& TT, int& ntiles, int& nsplit) {
+  TT = (A.n + kGT2 - 1) / kGT2;
+  ntiles = TT * (TT + 1) / 2;
+  const int64_t steps = (A.m + kGK2 - 1) / kGK2;
+  nsplit = (int)((2 * (int64_t)num_sms() + ntiles - 1) / ntiles);
+  if (nsplit > steps) nsplit = (int)steps;
+  if (nsplit < 1) nsplit = 1;
+}
+
+// Sum the split partials in fixed order; write the tile and its mirror image.
+__global__ void k_gram_reduce(const double* __restrict__ part, int ntiles, int nsplit, int TT, int n,
+                              double* __restrict__ G, int tile) {
+  int t = blockIdx.x, I = 0;
+  while (t >= TT - I) { t -= TT - I; ++I; }
+  const int J = I + t;
+  for (int e = threadIdx.x; e < tile * tile; e += blockDim.x) {
+    const int i = e / tile, j = e % tile;
+    const int gi = I * tile + i, gj = J * tile + j;
     double acc = 0.0;
-    for (int s = 0; s < nsplit; ++s) acc += part[((size_t)s * ntiles + blockIdx.x) * (kGT * kGT) + e];
+    for (int s = 0; s < nsplit; ++s) acc += part[((size_t)s * ntiles + blockIdx.x) * (tile * tile) + e];
     if (gi < n && gj < n) {
       G[(size_t)gi * n + gj] = acc;
       G[(size_t)gj * n + gi] = acc;
@@ -141,6 +240,24 @@ int launch_gram(const DenseView& A, int u_f, const double* dinv, int K_t, double
   if (K_t < 1) K_t = 64;
   if (gram_tc_supported(u_f, K_t))
     return launch_gram_tc(A, u_f, dinv, K_t, G, ws, ws_doubles * 8, range_flag, st, launches);
+  if (u_f == TLS_FP32 || u_f == TLS_FP64) {
+    int TT, ntiles, nsplit;
+    gram_shape_f64(A, TT, ntiles, nsplit);
+    if ((size_t)nsplit * ntiles * kGT2 * kGT2 > ws_doubles) {
+      set_error("gram: workspace too small");
+      return TLS_ERR_WORKSPACE;
+    }
+    dim3 grid(ntiles, nsplit);
+    if (u_f == TLS_FP32)
+      k_gram_f64<TLS_FP32><<<grid, 256, 0, st>>>(A.A, A.m, A.n, A.ld, dinv, nsplit, TT, ws, range_flag);
+    else
+      k_gram_f64<TLS_FP64><<<grid, 256, 0, st>>>(A.A, A.m, A.n, A.ld, dinv, nsplit, TT, ws, range_flag);
+    TLS_LAUNCH_CHECK();
+    k_gram_reduce<<<ntiles, 256, 0, st>>>(ws, ntiles, nsplit, TT, A.n, G, kGT2);
+    TLS_LAUNCH_CHECK();
+    if (launches) *launches += 2;
+    return 0;
+  }
   int TT, ntiles, nchunks, nsplit;
   gram_shape(A, K_t, TT, ntiles, nchunks, nsplit);
   if ((size_t)nsplit * ntiles * kGT * kGT > ws_doubles) {
@@ -163,7 +280,7 @@ int launch_gram(const DenseView& A, int u_f, const double* dinv, int K_t, double
       break;
   }
   TLS_LAUNCH_CHECK();
-  k_gram_reduce<<<ntiles, 256, 0, st>>>(ws, ntiles, nsplit, TT, A.n, G);
+  k_gram_reduce<<<ntiles, 256, 0, st>>>(ws, ntiles, nsplit, TT, A.n, G, kGT);
   TLS_LAUNCH_CHECK();
   if (launches) *launches += 2;
   return 0;
