@@ -199,6 +199,7 @@ def main():
     ap.add_argument("--workload", default="cfg4w", choices=sorted(WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-control", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -374,6 +375,29 @@ def main():
         with open(os.path.join(ROOT, "profiles", f"counts_{wl}.json"), "w") as fh:
             json.dump({"K": info["rqi_iters"], "B0": info["boot_iters"], "pcg": info["pcg_iters"]}, fh)
 
+    # the uniform-precision control of the paper's comparison (SURVEY
+    # §8(d)): the same solve with u_f = fp64 (exact R, fp64 Gram on CUDA cores), timed the
+    # same way; its TTS over ours is the measured mixed-precision speedup on B200
+    control = None
+    if not args.no_control and world == 1 and not csr:
+        def step64():
+            rc, R, fi = tlsrqi.tls_factor_precond(M, "fp64", comm=comm, stream=stream, ws=ws)
+            rc, _, sig, inf = tlsrqi.tls_rqi_pcgtls(M, b_loc, R, comm=comm, stream=stream, ws=ws, x_out=x)
+            return inf
+        step64()
+        torch.cuda.synchronize()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(3):
+            inf64 = step64()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        t64 = g0.elapsed_time(g1) / 3 / 1e3
+        control = {"u_f": "fp64", "tts_s": t64, "status": inf64["status_name"], "rqi_iters": inf64["rqi_iters"],
+                   "boot_iters": inf64["boot_iters"], "pcg_iters": inf64["pcg_iters"],
+                   "measured_speedup_of_uf": t64 / tts}
+
     cpu = None
     if keep_host:
         import numpy as np
@@ -382,6 +406,14 @@ def main():
                                              u_f, counts)
         cpu = {"value": t_cpu, "unit": "s", "cores": os.cpu_count(), "kind": "oracle", "sample": sample,
                "parts": parts}
+        # the paper's flop model (oracle/perfmodel.py), "model only, no
+        # hardware", at this (m, n, r = RQI steps): paper weights (u, u_p, u_q) = (fp64, fp32,
+        # fp16) and the build's (fp64, fp64, u_f)
+        from oracle import perfmodel
+        cpu["paper_model_speedup"] = {
+            "r": info["rqi_iters"],
+            "paper_weights_fp64_fp32_fp16": perfmodel.speedup(m, n, info["rqi_iters"], "fp64", "fp32", "fp16"),
+            "build_weights_fp64_fp64_uf": perfmodel.speedup(m, n, info["rqi_iters"], "fp64", "fp64", u_f)}
 
     if rank == 0:
         line = {
@@ -402,6 +434,7 @@ def main():
             "a_passes_per_s": a_passes / tts,
             "roofline": roof, "kernel_share": kshare,
             "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
+            "uniform_fp64_control": control,
         }
         print(json.dumps(line), flush=True)
     if comm:
