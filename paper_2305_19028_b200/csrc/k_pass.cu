@@ -20,11 +20,16 @@ namespace tls {
 
 constexpr int kPassConsumers = 256;
 constexpr int kPassWarps = kPassConsumers / 32;
-constexpr int kPassThreads = kPassConsumers + 32;
+constexpr int kPassThreads = kPassConsumers + 32;   // one consumer set
+constexpr int kPassNS = 2;                             // max consumer sets (even / odd stages)
+// consumer sets per instantiation (measured): the 1-RHS passes (residual, 1-RHS operator)
+// gain from two sets; the 2-RHS operator pass is register-limited with two (96 regs).
+template <int NRHS> constexpr int pass_sets() { return NRHS == 1 ? 2 : 1; }
+constexpr int kPassRedDoubles = kPassWarps * 16 + 16 + 32;   // red + tfin + sred of one set
 constexpr int kPassStages = 6;
 constexpr int kPassStageBytes = 32 * 1024;
 constexpr size_t kPassSmem = (size_t)kPassStages * kPassStageBytes + 2 * kPassStages * 8 +
-                             (kPassWarps * 16 + 16 + 32) * 8;
+                             (size_t)kPassNS * kPassRedDoubles * 8;
 
 static int g_num_sms = 0;
 int num_sms() {
@@ -51,7 +56,7 @@ int pass_grid(const DenseView& A) {
 }
 
 size_t pass_partials_doubles(const DenseView& A) {
-  return (size_t)pass_grid(A) * (size_t)(2 * A.n + 2);
+  return (size_t)pass_grid(A) * kPassNS * (size_t)(2 * A.n + 2);
 }
 
 // One group of RB rows of the current stage: row dot products t_r = a_i . q_r (thread
@@ -63,7 +68,7 @@ __device__ __forceinline__ void pass_group(const double* __restrict__ stt, int64
                                            const double* __restrict__ b, const double2 (&qr)[NRHS][CPT],
                                            double2 (&acc)[NRHS][CPT], const bool (&okc)[CPT], const bool (&ok1)[CPT],
                                            double* red, double* tfin, int warp, int lane, int tid, double& sacc,
-                                           double& sacc2) {
+                                           double& sacc2, int bar) {
   constexpr int V = RB * NRHS;
   double2 a[RB][CPT];
   double part[V];
@@ -100,7 +105,7 @@ __device__ __forceinline__ void pass_group(const double* __restrict__ stt, int64
   }
   warp_transpose_reduce<V>(part, lane);
   if ((lane & (32 / V - 1)) == 0) red[warp * 16 + transpose_reduce_index<V>(lane)] = part[0];
-  named_bar_sync(1, kPassConsumers);
+  named_bar_sync(bar, kPassConsumers);
   if (tid < V) {
     double t = 0.0;
 #pragma unroll
@@ -116,7 +121,7 @@ __device__ __forceinline__ void pass_group(const double* __restrict__ stt, int64
     sacc = fma(t, t, sacc);
     tfin[tid] = t;
   }
-  named_bar_sync(1, kPassConsumers);
+  named_bar_sync(bar, kPassConsumers);
 #pragma unroll
   for (int rr = 0; rr < RB; ++rr) {
 #pragma unroll
@@ -131,8 +136,11 @@ __device__ __forceinline__ void pass_group(const double* __restrict__ stt, int64
   }
 }
 
-template <int NRHS, int MODE, int CPT, bool FC>
-__global__ void __launch_bounds__(kPassThreads, 1)
+// NS consumer sets of 8 warps take alternate stages (latency: a set's two barriers per
+// row group serialise its stage, two sets overlap them); each set keeps its own v
+// accumulators and writes its own partial row (the reduce sums grid * NS rows).
+template <int NRHS, int MODE, int CPT, bool FC, int NS>
+__global__ void __launch_bounds__(NS * kPassConsumers + 32, 1)
 k_pass(const double* __restrict__ A, int64_t m, int n, int64_t ld, int rps,
        const double* __restrict__ q, const double* __restrict__ b,
        double* __restrict__ partials, int W, const int* __restrict__ active) {
@@ -141,27 +149,29 @@ k_pass(const double* __restrict__ A, int64_t m, int n, int64_t ld, int rps,
   double* ring = reinterpret_cast<double*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kPassStages * kPassStageBytes);
   uint64_t* empty = full + kPassStages;
-  double* red = reinterpret_cast<double*>(empty + kPassStages);  // [warps][16]
+  const int warp_all = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int set = warp_all / kPassWarps;                         // NS for the producer warp
+  double* red = reinterpret_cast<double*>(empty + kPassStages) + (size_t)(set < NS ? set : 0) * kPassRedDoubles;
   double* tfin = red + kPassWarps * 16;                           // [16]
   double* sred = tfin + 16;                                       // [32]
   constexpr int kStageDoubles = kPassStageBytes / 8;
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x - set * kPassConsumers, warp = warp_all - set * kPassWarps;
+  const int bar = 1 + set;
   const int64_t G = gridDim.x;
   const int64_t r0 = m * (int64_t)blockIdx.x / G;
   const int64_t r1 = m * (int64_t)(blockIdx.x + 1) / G;
   const int nst = (int)((r1 - r0 + rps - 1) / rps);
 
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     for (int s = 0; s < kPassStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kPassWarps);
+      mbar_init(&empty[s], kPassWarps);   // the 8 warps of the set that consumes the stage
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == kPassWarps) {  // ---------------- producer: TMA bulk copies of row blocks
+  if (set == NS) {  // ---------------- producer: TMA bulk copies of row blocks
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       for (int it = 0; it < nst; ++it) {
@@ -204,7 +214,7 @@ k_pass(const double* __restrict__ A, int64_t m, int n, int64_t ld, int rps,
   }
   double sacc = 0.0, sacc2 = 0.0;
 
-  for (int it = 0; it < nst; ++it) {
+  for (int it = set; it < nst; it += NS) {
     const int s = it % kPassStages;
     const uint32_t ph = (uint32_t)(it / kPassStages) & 1u;
     mbar_wait(&full[s], ph);
@@ -232,18 +242,18 @@ k_pass(const double* __restrict__ A, int64_t m, int n, int64_t ld, int rps,
       if (FC) {
         for (; rb + RB <= rows; rb += RB)
           pass_group<NRHS, MODE, CPT, RB, true>(st + (size_t)rb * ld + 2 * tid, ld, rb, rows, rs, b, qr, acc, okc, ok1,
-                                               red, tfin, warp, lane, tid, sacc, sacc2);
+                                               red, tfin, warp, lane, tid, sacc, sacc2, bar);
       }
       for (; rb < rows; rb += RB)
         pass_group<NRHS, MODE, CPT, RB, false>(st + (size_t)rb * ld + 2 * tid, ld, rb, rows, rs, b, qr, acc, okc, ok1,
-                                              red, tfin, warp, lane, tid, sacc, sacc2);
+                                              red, tfin, warp, lane, tid, sacc, sacc2, bar);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
-  // ---------------- write this CTA's partial
-  double* out = partials + (size_t)blockIdx.x * W;
+  // ---------------- write this set's partial
+  double* out = partials + ((size_t)blockIdx.x * NS + set) * W;
 #pragma unroll
   for (int r = 0; r < NRHS; ++r) {
 #pragma unroll
@@ -259,7 +269,7 @@ k_pass(const double* __restrict__ A, int64_t m, int n, int64_t ld, int rps,
       sred[tid] = tid < V ? sacc : 0.0;
       sred[16 + tid] = tid < V ? sacc2 : 0.0;
     }
-    named_bar_sync(1, kPassConsumers);
+    named_bar_sync(bar, kPassConsumers);
     if (tid == 0) {
       double s0 = 0.0, s1 = 0.0;
       for (int i = 0; i < V; ++i) {
@@ -281,14 +291,15 @@ static int launch_pass_t(const DenseView& A, const double* q, const double* b, d
                          int W, const int* active, cudaStream_t st, int G) {
   // FC: n fills every thread's CPT column chunks exactly (n = 2 * CPT * consumers)
   const bool fc = (A.n == 2 * CPT * kPassConsumers);
-  auto kern = fc ? k_pass<NRHS, MODE, CPT, true> : k_pass<NRHS, MODE, CPT, false>;
+  constexpr int NS = pass_sets<NRHS>();
+  auto kern = fc ? k_pass<NRHS, MODE, CPT, true, NS> : k_pass<NRHS, MODE, CPT, false, NS>;
   static bool attr[2] = {false, false};
   if (!attr[fc]) {
     TLS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem));
     attr[fc] = true;
   }
-  kern<<<G, kPassThreads, kPassSmem, st>>>(A.A, A.m, A.n, A.ld, rows_per_stage(A), q, b, partials, W,
-                                           active);
+  kern<<<G, NS * kPassConsumers + 32, kPassSmem, st>>>(A.A, A.m, A.n, A.ld, rows_per_stage(A), q, b, partials,
+                                                             W, active);
   TLS_LAUNCH_CHECK();
   return 0;
 }
@@ -310,7 +321,8 @@ int launch_pass(const DenseView& A, int mode, int nrhs, const double* q, const d
     return TLS_ERR_UNSUPPORTED;
   }
   const int G = pass_grid(A);
-  if (grid_out) *grid_out = G;
+  // partial rows for the fixed-order reduce: one per consumer set
+  if (grid_out) *grid_out = G * ((mode != PASS_COLSTATS && (mode == PASS_RESIDUAL || nrhs == 1)) ? 2 : 1);
   if (A.m == 0) return 0;
   if (mode == PASS_COLSTATS)
     return launch_pass_cpt<2, PASS_COLSTATS>(A, q, b, partials, 2 * A.n, active, st, G);
