@@ -57,10 +57,52 @@ __global__ void __launch_bounds__(32) k_diag_inv(const T* __restrict__ Rrow, int
   }
 }
 
+// The coupling blocks of the look-ahead solve (k_trsv.cu): with solve order u, block x_u =
+// z_u - E_u x_{u-1} where z_u = D_u (y_u - all tile updates except the last) and E_u = D_u
+// T_{u,u-1}.  Back (R~ x = y, previous block in solve order = real block kb+1):
+// E = R~_kk^{-1} R~_{kb,kb+1}; forward (R~^T x = y, previous = kb-1): E = R~_kk^{-T} R~_{kb-1,kb}^T.
+// Stored [l][i] = E[i][l] (lane i reads consecutive words).  Computed once per R~ in fp64
+// from the exact upcasts.
+template <typename T>
+__global__ void __launch_bounds__(32) k_e_blocks(const T* __restrict__ Rrow, int npad, const double* __restrict__ DinvB,
+                                                  const double* __restrict__ DinvF, double* __restrict__ EB,
+                                                  double* __restrict__ EF) {
+  __shared__ double Tt[32][33];
+  const int kb = blockIdx.x, i = threadIdx.x, NB = npad / 32;
+  const int o = kb * 32;
+  // back: E[i][j] = sum_l D_B[i][l] R[o + l][o + 32 + j],  D_B[i][l] = DinvB[kb][l][i]
+  double* E = EB + (size_t)kb * 1024;
+  if (kb + 1 < NB) {
+    for (int l = 0; l < 32; ++l) Tt[l][i] = dec<T>(Rrow[(size_t)(o + l) * npad + o + 32 + i]);
+    __syncwarp();
+    for (int j = 0; j < 32; ++j) {
+      double acc = 0.0;
+      for (int l = 0; l < 32; ++l) acc = fma(DinvB[(size_t)kb * 1024 + l * 32 + i], Tt[l][j], acc);
+      E[j * 32 + i] = acc;
+    }
+  } else {
+    for (int j = 0; j < 32; ++j) E[j * 32 + i] = 0.0;
+  }
+  __syncwarp();
+  // forward: E[i][j] = sum_l D_F[i][l] R[o - 32 + j][o + l],  D_F[i][l] = DinvF[kb][l][i]
+  E = EF + (size_t)kb * 1024;
+  if (kb > 0) {
+    for (int j = 0; j < 32; ++j) Tt[j][i] = dec<T>(Rrow[(size_t)(o - 32 + j) * npad + o + i]);   // Tt[j][l]
+    __syncwarp();
+    for (int j = 0; j < 32; ++j) {
+      double acc = 0.0;
+      for (int l = 0; l < 32; ++l) acc = fma(DinvF[(size_t)kb * 1024 + l * 32 + i], Tt[j][l], acc);
+      E[j * 32 + i] = acc;
+    }
+  } else {
+    for (int j = 0; j < 32; ++j) E[j * 32 + i] = 0.0;
+  }
+}
+
 size_t precond_bytes(int n, int u_f) {
   const int npad = (n + 31) / 32 * 32;
   const size_t es = (u_f == TLS_FP64) ? 8 : (u_f == TLS_FP32 ? 4 : 2);
-  return 2 * (size_t)npad * npad * es + 2 * (size_t)npad * 32 * 8 + 2 * (size_t)npad * 8 + 256;
+  return 2 * (size_t)npad * npad * es + 4 * (size_t)npad * 32 * 8 + 2 * (size_t)npad * 8 + 256;
 }
 
 template <typename T>
@@ -73,6 +115,7 @@ static int pack_t(const double* R, int ldR, int lower, PrecondDev& pc, int* rang
     TLS_LAUNCH_CHECK();
   }
   k_diag_inv<T><<<pc.npad / 32, 32, 0, st>>>((const T*)pc.Rrow, pc.npad, pc.DinvB, pc.DinvF);
+  k_e_blocks<T><<<pc.npad / 32, 32, 0, st>>>((const T*)pc.Rrow, pc.npad, pc.DinvB, pc.DinvF, pc.EB, pc.EF);
   TLS_LAUNCH_CHECK();
   return 0;
 }
@@ -85,7 +128,7 @@ int launch_pack_R(const double* R, int ldR, int lower, PrecondDev& pc, int* rang
     case TLS_FP32: rc = pack_t<float>(R, ldR, lower, pc, range, st); break;
     default: rc = pack_t<double>(R, ldR, lower, pc, range, st); break;
   }
-  if (launches) *launches += (R != nullptr) ? 2 : 1;
+  if (launches) *launches += (R != nullptr) ? 3 : 2;
   return rc;
 }
 

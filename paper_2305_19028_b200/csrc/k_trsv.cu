@@ -82,21 +82,21 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // so the loads overlap the wait for x.  The critical path per block row is one
 // tile update plus one 32 x 32 solve; the other tile updates of all warps run
 // concurrently with it.
-constexpr int kTW = 16;  // warps of a TRSV CTA
+constexpr int kTW = 8;   // warps of a TRSV CTA
 
 template <typename T> struct TileDP { static constexpr int v = SegTraits<T>::NV <= 4 ? 4 : (SegTraits<T>::NV <= 8 ? 2 : 1); };
 
 struct TrsvSm {
   uint32_t phase; // parity of the barrier phase the next solve completes (one phase per solve)
   double* y;      // [npad] right-hand side in, solution out (in place)
-  double* D;      // [kTW][1024] per-warp slot for the inverse of the diagonal block
+  double* D;      // [kTW][2048] per-warp slot: inverse of the diagonal block, then its E block
   double* ys;     // [kTW][32] per-warp scratch of the block solve
   uint64_t* bar;  // [NB] x_u published
   double* red;    // [32] block_sum scratch
 };
 // dynamic smem of a TRSV CTA
 static size_t trsv_smem(int npad) {
-  return (size_t)npad * 8 + (size_t)kTW * 1024 * 8 + (size_t)kTW * 32 * 8 + (size_t)(npad / 32) * 8 + 32 * 8;
+  return (size_t)npad * 8 + (size_t)kTW * 2048 * 8 + (size_t)kTW * 32 * 8 + (size_t)(npad / 32) * 8 + 32 * 8;
 }
 __device__ __forceinline__ TrsvSm trsv_carve(int npad) {
   extern __shared__ __align__(16) double tsm[];
@@ -104,7 +104,7 @@ __device__ __forceinline__ TrsvSm trsv_carve(int npad) {
   s.phase = 0;
   s.y = tsm;
   s.D = s.y + npad;
-  s.ys = s.D + kTW * 1024;
+  s.ys = s.D + kTW * 2048;
   s.red = s.ys + kTW * 32;
   s.bar = reinterpret_cast<uint64_t*>(s.red + 32);
   return s;
@@ -118,10 +118,12 @@ __device__ __forceinline__ void trsv_init(const TrsvSm& sm, int npad) {
   cluster_sync_all();   // the cluster's CTAs may address these barriers from now on
 }
 
-__device__ __forceinline__ void stage_dinv_warp(double* dst, const double* src) {
+__device__ __forceinline__ void stage_dinv_warp(double* dst, const double* src, const double* esrc) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int k = 0; k < 16; ++k) cp_async16(dst + (k * 32 + lane) * 2, src + (k * 32 + lane) * 2);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) cp_async16(dst + 1024 + (k * 32 + lane) * 2, esrc + (k * 32 + lane) * 2);
   cp_async_commit();
 }
 
@@ -153,8 +155,15 @@ template <> __device__ __forceinline__ double chunk_get<double>(const uint4& u, 
 // each lane accumulates, per k, a partial dot product over its chunk's columns; the
 // partials of a row are combined across its CPR lanes only when the block is solved.
 // All threads of the CTA must call it (after trsv_init); ends with __syncthreads().
+// Look-ahead form of each block solve (k_e_blocks in k_chol.cu): the owner accumulates
+// the tile updates of block u from every solution block except the last one in solve
+// order, forms z_u = D_u (y_u - acc) while x_{u-1} is still being solved elsewhere, and
+// once x_{u-1} arrives computes x_u = z_u - E_u x_{u-1}, E_u = D_u T_{u,u-1}: a single
+// 32 x 32 product on the critical path instead of a tile update, a cross-lane row
+// reduction and the diagonal solve.
 template <typename T, bool BACK>
-__device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv, int npad, TrsvSm& sm) {
+__device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv, const double* __restrict__ Eblk,
+                        int npad, TrsvSm& sm) {
   constexpr int NV = SegTraits<T>::NV, DP = TileDP<T>::v;
   constexpr int CPR = NV, RPI = 32 / CPR, EPC = 16 / (int)sizeof(T);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -167,11 +176,13 @@ __device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv
   // barrier makes sure every CTA is armed (and its y filled) before anyone sends
   for (int i = threadIdx.x; i < NB; i += blockDim.x) mbar_arrive_expect_tx(&sm.bar[i], 256);
   cluster_sync_all();
-  // block u (solve order) is owned by CTA u % C, warp (u / C) % kTW
+  // block u (solve order) is owned by CTA u % C, warp (u / C) % kTW; its tiles are
+  // (u, 0 .. u-2) -- the coupling to u-1 is the E block
   const int first = cr + C * warp;
   const int ustep = C * kTW;
   if (first < NB) {
-    double* Dw = sm.D + warp * 1024;
+    double* Dw = sm.D + warp * 2048;
+    double* Ew = Dw + 1024;
     double* ysw = sm.ys + warp * 32;
     auto real = [&](int u) { return BACK ? NB - 1 - u : u; };
     auto issue = [&](int ui, int ci, uint4 (&raw)[NV]) {
@@ -179,20 +190,23 @@ __device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv
 #pragma unroll
       for (int k = 0; k < NV; ++k) raw[k] = __ldg(reinterpret_cast<const uint4*>(base + (size_t)k * RPI * npad));
     };
+    auto ntiles = [](int u) { return u >= 1 ? u - 1 : 0; };
     int total = 0;
-    for (int u = first; u < NB; u += ustep) total += u;
-    stage_dinv_warp(Dw, Dinv + (size_t)real(first) * 1024);
+    for (int u = first; u < NB; u += ustep) total += ntiles(u);
+    stage_dinv_warp(Dw, Dinv + (size_t)real(first) * 1024, Eblk + (size_t)real(first) * 1024);
     int ui = first, ci = 0;
-    if (ui == 0) ui += ustep;
+    while (ui < NB && ntiles(ui) == 0) ui += ustep;
     uint4 raw[DP][NV];
 #pragma unroll
     for (int s = 0; s < DP; ++s) {
       if (s < total) {
         issue(ui, ci, raw[s]);
-        if (++ci == ui) { ui += ustep; ci = 0; }
+        if (++ci == ntiles(ui)) {
+          ci = 0;
+          do { ui += ustep; } while (ui < NB && ntiles(ui) == 0);
+        }
       }
     }
-    // remote (cluster) addresses of this lane's y element and of the barriers are formed per block
     const uint32_t y_base = smem_u32(sm.y), bar_base = smem_u32(sm.bar);
     int uc = first, cc = 0;
     double acc[NV];
@@ -214,22 +228,33 @@ __device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv
       ysw[lane] = sm.y[o + lane] - mine;
       cp_async_wait<0>();
       __syncwarp();
-      double x0 = 0.0, x1 = 0.0;
+      double z0 = 0.0, z1 = 0.0;
 #pragma unroll
       for (int l = 0; l < 32; l += 2) {
-        x0 = fma(Dw[l * 32 + lane], ysw[l], x0);
-        x1 = fma(Dw[(l + 1) * 32 + lane], ysw[l + 1], x1);
+        z0 = fma(Dw[l * 32 + lane], ysw[l], z0);
+        z1 = fma(Dw[(l + 1) * 32 + lane], ysw[l + 1], z1);
       }
-      const double xv = x0 + x1;
+      double xv = z0 + z1;
+      if (uc >= 1) {                                     // x_u = z_u - E_u x_{u-1}
+        mbar_wait_cluster(&sm.bar[uc - 1], ph);
+        const double* xp = sm.y + 32 * real(uc - 1);
+        double e0 = 0.0, e1 = 0.0;
+#pragma unroll
+        for (int l = 0; l < 32; l += 2) {
+          e0 = fma(Ew[l * 32 + lane], xp[l], e0);
+          e1 = fma(Ew[(l + 1) * 32 + lane], xp[l + 1], e1);
+        }
+        xv -= e0 + e1;
+      }
       __syncwarp();
       // publish x_u to every CTA of the cluster (including this one)
       const uint32_t ya = y_base + (uint32_t)(o + lane) * 8u, ba = bar_base + (uint32_t)uc * 8u;
       for (int r = 0; r < C; ++r) st_async_f64(mapa_shared(ya, (uint32_t)r), xv, mapa_shared(ba, (uint32_t)r));
       uc += ustep;
       cc = 0;
-      if (uc < NB) stage_dinv_warp(Dw, Dinv + (size_t)real(uc) * 1024);
+      if (uc < NB) stage_dinv_warp(Dw, Dinv + (size_t)real(uc) * 1024, Eblk + (size_t)real(uc) * 1024);
     };
-    if (uc == 0) solve();
+    while (uc < NB && ntiles(uc) == 0) solve();
     for (int kb = 0; kb < total; kb += DP) {
 #pragma unroll
       for (int s = 0; s < DP; ++s) {
@@ -249,9 +274,15 @@ __device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv
             for (int e = 0; e < EPC; ++e) acc[k] = fma(chunk_get<T>(raw[s][k], e), xv[e], acc[k]);
           if (kb + s + DP < total) {
             issue(ui, ci, raw[s]);
-            if (++ci == ui) { ui += ustep; ci = 0; }
+            if (++ci == ntiles(ui)) {
+              ci = 0;
+              do { ui += ustep; } while (ui < NB && ntiles(ui) == 0);
+            }
           }
-          if (++cc == uc) solve();
+          if (++cc == ntiles(uc)) {
+            solve();
+            while (uc < NB && ntiles(uc) == 0) solve();
+          }
         }
       }
     }
@@ -265,10 +296,18 @@ __device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv
 // ---------------------------------------------------------------- plain apply (API / tests)
 // One cluster of kTC CTAs per right-hand side r.  Every CTA of a cluster holds the whole
 // vector and computes the same values; only cluster rank 0 writes global memory.
-constexpr int kTC = 4;   // CTAs (SMs) per solve
+constexpr int kTC = 8;   // CTAs (SMs) per solve, the portable cluster maximum (TLS_TRSV_CLUSTER overrides)
+static int trsv_cluster() {
+  static const int c = [] {
+    const char* e = getenv("TLS_TRSV_CLUSTER");
+    const int v = e ? atoi(e) : kTC;
+    return (v == 1 || v == 2 || v == 4 || v == 8) ? v : kTC;
+  }();
+  return c;
+}
 
 template <typename T>
-__global__ void __launch_bounds__(kTW * 32) k_precond_apply(PrecondDev pc, int trans, double* __restrict__ Y, int ldY) {
+__global__ void __launch_bounds__(kTW * 32, 1) k_precond_apply(PrecondDev pc, int trans, double* __restrict__ Y, int ldY) {
   TrsvSm sm = trsv_carve(pc.npad);
   trsv_init(sm, pc.npad);
   const int n = pc.n, npad = pc.npad, r = blockIdx.x / (int)cluster_nctarank();
@@ -278,8 +317,8 @@ __global__ void __launch_bounds__(kTW * 32) k_precond_apply(PrecondDev pc, int t
     if (trans) v *= pc.dinv[i];
     sm.y[i] = v;
   }
-  if (trans) trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, npad, sm);
-  else trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, npad, sm);
+  if (trans) trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, pc.EF, npad, sm);
+  else trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, pc.EB, npad, sm);
   if (rank0)
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       double v = sm.y[i];
@@ -293,7 +332,7 @@ __global__ void __launch_bounds__(kTW * 32) k_precond_apply(PrecondDev pc, int t
 // until the RQI update).  Vectors in global memory have stride n (q feeds the pass
 // over A directly).
 template <typename T>
-__global__ void __launch_bounds__(kTW * 32) k_pcg_init(PrecondDev pc, int nrhs, PcgVecs v, PcgState* __restrict__ S) {
+__global__ void __launch_bounds__(kTW * 32, 1) k_pcg_init(PrecondDev pc, int nrhs, PcgVecs v, PcgState* __restrict__ S) {
   TrsvSm sm = trsv_carve(pc.npad);
   trsv_init(sm, pc.npad);
   const int n = pc.n, npad = pc.npad, tid = threadIdx.x, r = blockIdx.x / (int)cluster_nctarank();
@@ -312,7 +351,7 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_init(PrecondDev pc, int nrhs, 
   const size_t off = (size_t)r * n;
   // l.191: s_0 = p_0 = P^{-T} f, eta_0 = ||s_0||^2, omega_0 = 0
   for (int i = tid; i < npad; i += blockDim.x) sm.y[i] = i < n ? v.rhs[off + i] * pc.dinv[i] : 0.0;
-  trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, npad, sm);
+  trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, pc.EF, npad, sm);
   double e = 0.0;
   for (int i = tid; i < n; i += blockDim.x) {
     const double s = sm.y[i];
@@ -325,7 +364,7 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_init(PrecondDev pc, int nrhs, 
   }
   const double eta = block_sum(e, sm.red);
   // first q = P^{-1} p (l.193)
-  trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, npad, sm);
+  trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, pc.EB, npad, sm);
   e = 0.0;
   for (int i = tid; i < n; i += blockDim.x) {
     const double q = sm.y[i] * pc.dinv[i];
@@ -351,9 +390,9 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_init(PrecondDev pc, int nrhs, 
 // (passout = [v_0 .. v_{nrhs-1} (stride n), tau_0, tau_1]).  Every CTA of the cluster
 // reads its inputs before rank 0 writes anything (cluster barriers), so the replicas
 // take identical decisions.
-constexpr int kVecPerThread = 8;   // npad <= kTW * 32 * 8 = 4096
+constexpr int kVecPerThread = 16;  // npad <= kTW * 32 * 16 = 4096
 template <typename T>
-__global__ void __launch_bounds__(kTW * 32) k_pcg_step(PrecondDev pc, PcgVecs v, const double* __restrict__ passout,
+__global__ void __launch_bounds__(kTW * 32, 1) k_pcg_step(PrecondDev pc, PcgVecs v, const double* __restrict__ passout,
                                                        PcgState* __restrict__ S, int nrhs, int rule, int next_q,
                                                        int variant, int pass_nrhs) {
   __shared__ double s_alpha, s_beta, s_delta;
@@ -410,7 +449,7 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_step(PrecondDev pc, PcgVecs v,
     }
     sm.y[i] = yv;
   }
-  trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, npad, sm);
+  trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, pc.EF, npad, sm);
   // s -= alpha w (l.198), eta' = ||s||^2 (l.199); kept in registers until every CTA has read s, p
   double sn[kVecPerThread], pn[kVecPerThread];
   double e = 0.0;
@@ -466,7 +505,7 @@ __global__ void __launch_bounds__(kTW * 32) k_pcg_step(PrecondDev pc, PcgVecs v,
   }
   if (!cont || !next_q) return;
   // next q = P^{-1} p (l.193 of the next iteration)
-  trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, npad, sm);
+  trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, pc.EB, npad, sm);
   e = 0.0;
   for (int i = tid; i < n; i += blockDim.x) {
     const double q = sm.y[i] * pc.dinv[i];
@@ -529,7 +568,7 @@ __global__ void __launch_bounds__(kTT) k_rqi_update(int n, PcgVecs v, const PcgS
 
 // l.227-235: sigma_0^2 = r_0^T r_0/(1 + x_0^T x_0); u_0 = P^{-1} P^{-T} x_0 (R9); x_1 = x_0 + sigma_0^2 u_0.
 template <typename T>
-__global__ void __launch_bounds__(kTW * 32) k_boot_x1(PrecondDev pc, const double* __restrict__ passout,
+__global__ void __launch_bounds__(kTW * 32, 1) k_boot_x1(PrecondDev pc, const double* __restrict__ passout,
                                                       const double* __restrict__ x0, double* __restrict__ x1) {
   TrsvSm sm = trsv_carve(pc.npad);
   trsv_init(sm, pc.npad);
@@ -542,8 +581,8 @@ __global__ void __launch_bounds__(kTW * 32) k_boot_x1(PrecondDev pc, const doubl
   }
   const double xx = block_sum(e, sm.red);
   const double sig0 = passout[n] / (1.0 + xx);
-  trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, npad, sm);
-  trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, npad, sm);
+  trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, pc.EF, npad, sm);
+  trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, pc.EB, npad, sm);
   if (cluster_ctarank() == 0)
     for (int i = tid; i < n; i += blockDim.x) x1[i] = fma(sig0, sm.y[i] * pc.dinv[i], x0[i]);
 }
@@ -568,13 +607,14 @@ template <typename... KArgs, typename... Args>
 static int launch_cluster(void (*kern)(KArgs...), int clusters, size_t smem, cudaStream_t st, Args... args) {
   TLS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(clusters * kTC);
+  const int C = trsv_cluster();
+  cfg.gridDim = dim3(clusters * C);
   cfg.blockDim = dim3(kTW * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = kTC;
+  at[0].val.clusterDim.x = C;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;

@@ -471,6 +471,8 @@ int alloc_precond(int n, int u_f, tls_precond_t* out) {
   d.RTrow = p; p += (size_t)npad * npad * es;
   d.DinvB = reinterpret_cast<double*>(p); p += (size_t)npad * 32 * 8;
   d.DinvF = reinterpret_cast<double*>(p); p += (size_t)npad * 32 * 8;
+  d.EB = reinterpret_cast<double*>(p); p += (size_t)npad * 32 * 8;
+  d.EF = reinterpret_cast<double*>(p); p += (size_t)npad * 32 * 8;
   d.d = reinterpret_cast<double*>(p); p += (size_t)npad * 8;
   d.dinv = reinterpret_cast<double*>(p); p += (size_t)npad * 8;
   d.normA2 = reinterpret_cast<double*>(p);

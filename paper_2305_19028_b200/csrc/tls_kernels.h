@@ -88,6 +88,8 @@ struct PrecondDev {
   void* RTrow;      // npad x npad u_f, row-major R~^T
   double* DinvB;    // (npad/32) blocks of 32x32: DinvB[kb][l][i] = (R~_kk^{-1})[i][l]
   double* DinvF;    // (npad/32) blocks of 32x32: DinvF[kb][l][i] = (R~_kk^{-1})[l][i]
+  double* EB;       // (npad/32) blocks: EB[kb][l][i] = (R~_kk^{-1} R~_{k,k+1})[i][l]     (back solve)
+  double* EF;       // (npad/32) blocks: EF[kb][l][i] = (R~_kk^{-T} R~_{k-1,k}^T)[i][l]  (forward solve)
   double* d;        // npad (1 on padding)
   double* dinv;     // npad
   double* normA2;   // 1 (device)
