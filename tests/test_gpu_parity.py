@@ -405,3 +405,43 @@ def test_edge_shapes_end_to_end(T, m, n, fmt):
     res = rqi.rqi_pcgtls_mp(A, b, rqi.Precond(Rt, d, fmt, nrm))
     ex = exact.tls_svd(A, b)
     _check_solve(info, x.cpu().numpy(), sig, res, ex if res.status == rqi.OK else None)
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_virtual_row_shards(T, P):
+    """Row sharding on one GPU: every per-rank quantity the library
+    all-reduces -- column max / sums of squares, the u_f Gram, the operator and
+    residual pass results -- computed on P contiguous row blocks (dist.shard_rows)
+    and combined (sum; max for the column maxima) equals the unsharded computation."""
+    from paper_2305_19028_b200.dist import shard_rows
+    P_ = tlsgen.config("cfg2w")
+    A, b = P_.A, P_.b
+    m, n = A.shape
+    rng = np.random.default_rng(P)
+    q = rng.standard_normal((2, n))
+    x = rng.standard_normal(n)
+    M = T.matrix(dev(A))
+    cm_full, ss_full = T.tls_colstats(M)
+    d = torch.ldexp(torch.ones_like(cm_full), torch.frexp(cm_full)[1] - 1)
+    _, G_full = T.tls_gram(M, "fp16", d)
+    v_full, s_full = T.tls_pass(M, 0, dev(q))
+    vr_full, sr_full = T.tls_pass(M, 1, dev(x), dev(b))
+    cm = None; ss = 0.0; G = 0.0; v = 0.0; s = 0.0; vr = 0.0; sr = 0.0
+    for r in range(P):
+        lo, hi = shard_rows(m, P, r)
+        Mr = T.matrix(dev(A[lo:hi]), m_global=m, row_offset=lo)
+        c_r, s_r = T.tls_colstats(Mr)
+        cm = c_r if cm is None else torch.maximum(cm, c_r)
+        ss += float(s_r)
+        G = G + T.tls_gram(Mr, "fp16", d)[1]
+        v_r, sv_r = T.tls_pass(Mr, 0, dev(q))
+        v = v + v_r; s = s + sv_r
+        w_r, sw_r = T.tls_pass(Mr, 1, dev(x), dev(b[lo:hi]))
+        vr = vr + w_r; sr = sr + sw_r
+    assert torch.equal(cm, cm_full)
+    assert ss == pytest.approx(float(ss_full), rel=1e-13)
+    assert float((G - G_full).abs().max() / G_full.abs().max()) < 1e-6     # fp32 chunk sums regroup at shard edges
+    assert float((v - v_full).norm() / v_full.norm()) < 1e-13
+    assert float((s - s_full).abs().max() / s_full.abs().max()) < 1e-13
+    assert float((vr - vr_full).norm() / vr_full.norm()) < 1e-13
+    assert float((sr[0] - sr_full[0]).abs() / sr_full[0].abs()) < 1e-13
