@@ -24,7 +24,10 @@ constexpr int kPassThreads = kPassConsumers + 32;   // one consumer set
 constexpr int kPassNS = 2;                             // max consumer sets (even / odd stages)
 // consumer sets per instantiation (measured): the 1-RHS passes (residual, 1-RHS operator)
 // gain from two sets; the 2-RHS operator pass is register-limited with two (96 regs).
-template <int NRHS> constexpr int pass_sets() { return NRHS == 1 ? 2 : 1; }
+// (measured per shape, tools/time_pass.py); the column-statistics pass uses one set
+constexpr int pass_sets_rt(int nrhs, int mode, int cpt) {
+  return (mode != 2 /*PASS_COLSTATS*/ && (nrhs == 1 || cpt == 1)) ? 2 : 1;
+}
 constexpr int kPassRedDoubles = kPassWarps * 16 + 16 + 32;   // red + tfin + sred of one set
 constexpr int kPassStages = 6;
 constexpr int kPassStageBytes = 32 * 1024;
@@ -189,7 +192,9 @@ k_pass(const double* __restrict__ A, int64_t m, int n, int64_t ld, int rps,
   }
 
   // ---------------- consumers
-  constexpr int RB = (CPT >= 8) ? 1 : 8 / CPT;  // rows per reduction group (divides rows per stage)
+  // rows per reduction group (divides rows per stage); two consumer sets with 2 RHS halve it
+  // to stay within the 96-register budget of the 17-warp CTA
+  constexpr int RB = ((CPT >= 8) ? 1 : 8 / CPT) / ((NS == 2 && NRHS == 2 && CPT < 8) ? 2 : 1);
   constexpr int V = RB * NRHS;
   const int nchunks = (n + 1) >> 1;
 
@@ -291,7 +296,7 @@ static int launch_pass_t(const DenseView& A, const double* q, const double* b, d
                          int W, const int* active, cudaStream_t st, int G) {
   // FC: n fills every thread's CPT column chunks exactly (n = 2 * CPT * consumers)
   const bool fc = (A.n == 2 * CPT * kPassConsumers);
-  constexpr int NS = pass_sets<NRHS>();
+  constexpr int NS = pass_sets_rt(NRHS, MODE, CPT);
   auto kern = fc ? k_pass<NRHS, MODE, CPT, true, NS> : k_pass<NRHS, MODE, CPT, false, NS>;
   static bool attr[2] = {false, false};
   if (!attr[fc]) {
@@ -321,8 +326,12 @@ int launch_pass(const DenseView& A, int mode, int nrhs, const double* q, const d
     return TLS_ERR_UNSUPPORTED;
   }
   const int G = pass_grid(A);
-  // partial rows for the fixed-order reduce: one per consumer set
-  if (grid_out) *grid_out = G * ((mode != PASS_COLSTATS && (mode == PASS_RESIDUAL || nrhs == 1)) ? 2 : 1);
+  // partial rows for the fixed-order reduce: one per consumer set (pass_sets_rt of the
+  // instantiation launch_pass_cpt picks)
+  const int chunks = (A.n + 1) / 2;
+  const int cpt = chunks <= kPassConsumers ? 1 : chunks <= 2 * kPassConsumers ? 2 : chunks <= 4 * kPassConsumers ? 4 : 8;
+  const int kn = mode == PASS_COLSTATS ? 2 : (mode == PASS_RESIDUAL ? 1 : nrhs);
+  if (grid_out) *grid_out = G * pass_sets_rt(kn, mode, cpt);
   if (A.m == 0) return 0;
   if (mode == PASS_COLSTATS)
     return launch_pass_cpt<2, PASS_COLSTATS>(A, q, b, partials, 2 * A.n, active, st, G);
