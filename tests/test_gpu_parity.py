@@ -445,3 +445,21 @@ def test_virtual_row_shards(T, P):
     assert float((s - s_full).abs().max() / s_full.abs().max()) < 1e-13
     assert float((vr - vr_full).norm() / vr_full.norm()) < 1e-13
     assert float((sr[0] - sr_full[0]).abs() / sr_full[0].abs()) < 1e-13
+
+
+@pytest.mark.parametrize("opt", [dict(budget_rule=1), dict(stop_rule=1), dict(breakdown_rule=1), dict(boot=1),
+                                 dict(max_outer=2), dict(polish=0), dict(tol_inner=1e-6), dict(boot_tol=1e-4)])
+def test_rqi_options_parity(T, opt):
+    """Every tls_rqi_opts_t switch (include/tlsrqi.h) against the oracle's RqiOptions on the
+    same R~ (cfg1 with u_f fp16; cfg2w bf16 for the budget rule): identical status,
+    termination, RQI/PCG/bootstrap counts and sigma^2 trajectory; x, sigma to tolerance."""
+    name, fmt = ("cfg2w", "bf16") if "budget_rule" in opt else ("cfg1", "fp16")
+    P = tlsgen.config(name)
+    pc = rqi.factor_precond(P.A, fmt)
+    res = rqi.rqi_pcgtls_mp(P.A, P.b, pc, opts=rqi.RqiOptions(**opt))
+    R = T.tls_precond_import(pc.Rt, pc.d, pc.normA2, fmt)
+    rc, x, sig, info = T.tls_rqi_pcgtls(T.matrix(dev(P.A)), dev(P.b), R, opts=T.tls_rqi_opts_default(**opt))
+    _check_solve(info, x.cpu().numpy(), sig, res)
+    assert info["boot_iters"] == res.boot_iters
+    for a, b in zip(info["sigma2_trace"], res.sigma2_trace):
+        assert a == pytest.approx(b, rel=1e-9)
