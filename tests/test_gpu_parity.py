@@ -191,11 +191,20 @@ def test_precond_apply_vs_oracle(T, fmt, n):
 
 
 # ----------------------------------------------------------------------------- a4-a9 RQI
-def _check_solve(res_gpu, x_gpu, sig_gpu, res_or, ex=None, strict_boot=True):
+def _check_solve(res_gpu, x_gpu, sig_gpu, res_or, ex=None, strict_boot=True, pcg_slack=0):
+    """north_star parity: same status, termination and RQI count; PCG counts equal
+    (pcg_slack = 0) or within +-pcg_slack per solve per step (the north_star's +-2, used
+    where an inner solve can end on the tol_inner test at the fp64 floor, a decision
+    the summation order can move); x to 1e-9, sigma to 1e-12."""
     assert res_gpu["status"] == res_or.status
     assert res_gpu["termination"] == res_or.termination
     assert res_gpu["rqi_iters"] == res_or.rqi_iters
-    assert res_gpu["pcg_iters"] == [tuple(p) for p in res_or.pcg_iters]
+    if pcg_slack == 0:
+        assert res_gpu["pcg_iters"] == [tuple(p) for p in res_or.pcg_iters]
+    else:
+        assert len(res_gpu["pcg_iters"]) == len(res_or.pcg_iters)
+        for a, b in zip(res_gpu["pcg_iters"], res_or.pcg_iters):
+            assert abs(a[0] - b[0]) <= pcg_slack and abs(a[1] - b[1]) <= pcg_slack
     if strict_boot:
         assert abs(res_gpu["boot_iters"] - res_or.boot_iters) <= 2
     if res_or.status == rqi.OK:
@@ -462,4 +471,30 @@ def test_rqi_options_parity(T, opt):
     _check_solve(info, x.cpu().numpy(), sig, res)
     assert info["boot_iters"] == res.boot_iters
     for a, b in zip(info["sigma2_trace"], res.sigma2_trace):
+        assert a == pytest.approx(b, rel=1e-9)
+
+
+@pytest.mark.parametrize("name", tlsgen.PAPER_PROBLEMS)
+@pytest.mark.parametrize("fmt", ["fp16", "bf16", "fp32", "fp64"])
+def test_paper_sec4_problems(T, name, fmt):
+    """The paper's five §4 problems through
+    the whole GPU path: status, termination, RQI/PCG counts against the oracle run on
+    the GPU's own R~, x and sigma against it (and the SVD when OK); then the oracle's
+    R~ imported for a count-and-trajectory parity independent of the Gram."""
+    P = tlsgen.paper_problem(name)
+    M = T.matrix(T.dense_operand(dev(P.A)), n=P.n)
+    rc, R, finfo = T.tls_factor_precond(M, fmt)
+    assert rc == 0
+    rc, x, sig, info = T.tls_rqi_pcgtls(M, dev(P.b), R)
+    Rt, d, nrm = T.tls_precond_export(R)
+    res_same_R = rqi.rqi_pcgtls_mp(P.A, P.b, rqi.Precond(Rt, d, fmt, nrm))
+    ex = exact.tls_svd(P.A, P.b)
+    _check_solve(info, x.cpu().numpy(), sig, res_same_R, ex if res_same_R.status == rqi.OK else None,
+                 pcg_slack=2)
+    pc = rqi.factor_precond(P.A, fmt)
+    res_or = rqi.rqi_pcgtls_mp(P.A, P.b, pc)
+    R2 = T.tls_precond_import(pc.Rt, pc.d, pc.normA2, fmt)
+    rc, x2, sig2, info2 = T.tls_rqi_pcgtls(M, dev(P.b), R2)
+    _check_solve(info2, x2.cpu().numpy(), sig2, res_or, pcg_slack=2)
+    for a, b in zip(info2["sigma2_trace"], res_or.sigma2_trace):
         assert a == pytest.approx(b, rel=1e-9)

@@ -244,3 +244,114 @@ def config(name: str, device: str = "cpu", **kw):
     n = kw.pop("n", n)
     return dense_problem(m, n, kappa, eps, seed, twin=twin, device=device, name=name,
                          u_f=kw.pop("u_f", u_f), **kw)
+
+
+# --------------------------------------------------------------------------- PAPER §4 problems
+@dataclasses.dataclass
+class PaperProblem:
+    """One of the paper's §4 test problems, as (A+E, b+e)."""
+    name: str
+    A: np.ndarray        # (m, n) float64 row-major: the perturbed A + E
+    b: np.ndarray        # (m,) the perturbed b + e
+    A0: np.ndarray       # unperturbed A
+    b0: np.ndarray       # unperturbed b
+    x_true: Optional[np.ndarray]
+    eps: float
+    seed: int
+    u_f: str = "fp16"
+
+    @property
+    def m(self) -> int:
+        return int(self.A.shape[0])
+
+    @property
+    def n(self) -> int:
+        return int(self.A.shape[1])
+
+
+def _haar(k: int, rng) -> np.ndarray:
+    return _orthonormal_np(rng.standard_normal((k, k)))
+
+
+def paper_problem(name: str, seed: int = 1, eps: Optional[float] = None, **kw) -> PaperProblem:
+    """The five §4 problems with the paper's sizes and noise levels.  numpy's PCG64 stands
+    in for MATLAB's rng (SURVEY.md §8(f) OUT OF SCOPE: RNG-exact reproduction), so the
+    instances are the paper's distributions, not its bytes (R20-R22).
+
+      random     PAPER.md:484-487  A = rand(100,60), b = ones, E = eps rand, e = eps rand, eps 1e-6
+      delta      PAPER.md:501-531  the 9x4 pattern (delta at (1,1),(3,2); 1 at (7,3),(9,4)),
+                                   b = ones, E = eps Ebar .* A, e = eps ebar .* b with Ebar,
+                                   ebar ~ U(-1,1); eps 1e-1, delta 1e-2
+      bjorck     PAPER.md:539-550  A = Y [D; 0] Z^T, D = diag(2^0..2^-(n-1)), (m,n) = (30,15),
+                                   x = (1, 1/2, .., 1/n), b = A x; E = eps rand, e = eps rand, eps 0.05
+      toeplitz   PAPER.md:572-587  Tbar (n x n-2w) lower banded Toeplitz with first column
+                                   t_i = exp(-(w-i+1)^2/(2 a^2))/sqrt(2 pi a^2), i = 1..2w+1;
+                                   E = toeplitz(c, r) random (c ~ U(0,1)^n, r = (c_1, U(0,1)..));
+                                   b = ones + e; E, e scaled by 1e-3; n 100, w 2, a 1.25
+      vanhuffel  PAPER.md:591-604  n x (n-2): n-1 on the diagonal of the top (n-2) block, -1
+                                   elsewhere; b = (-1,..,-1, n-1, -1); E = eps rand, e = eps rand,
+                                   eps 1e-6, n 100
+    Draw order per problem: the matrices named above, then E, then e.
+    """
+    rng = np.random.Generator(np.random.PCG64(seed))
+    x_true = None
+    if name == "random":
+        m, n = kw.get("m", 100), kw.get("n", 60)
+        eps = 1e-6 if eps is None else eps
+        A0 = rng.random((m, n))
+        b0 = np.ones(m)
+        E = eps * rng.random((m, n))
+        e = eps * rng.random(m)
+    elif name == "delta":
+        delta = kw.get("delta", 1e-2)
+        eps = 1e-1 if eps is None else eps
+        A0 = np.zeros((9, 4))
+        A0[0, 0] = delta
+        A0[2, 1] = delta
+        A0[6, 2] = 1.0
+        A0[8, 3] = 1.0
+        b0 = np.ones(9)
+        E = eps * rng.uniform(-1.0, 1.0, (9, 4)) * A0
+        e = eps * rng.uniform(-1.0, 1.0, 9) * b0
+    elif name == "bjorck":
+        m, n = kw.get("m", 30), kw.get("n", 15)
+        eps = 0.05 if eps is None else eps
+        Y = _haar(m, rng)
+        Z = _haar(n, rng)
+        D = np.zeros((m, n))
+        D[np.arange(n), np.arange(n)] = 2.0 ** -np.arange(n)
+        A0 = Y @ D @ Z.T
+        x_true = 1.0 / np.arange(1, n + 1)
+        b0 = A0 @ x_true
+        E = eps * rng.random((m, n))
+        e = eps * rng.random(m)
+    elif name == "toeplitz":
+        n, w, a = kw.get("n", 100), kw.get("omega", 2), kw.get("alpha", 1.25)
+        eps = 1e-3 if eps is None else eps
+        nc = n - 2 * w
+        i = np.arange(1, 2 * w + 2)
+        col = np.zeros(n)
+        col[:2 * w + 1] = np.exp(-((w - i + 1) ** 2) / (2 * a * a)) / math.sqrt(2 * math.pi * a * a)
+        idx = np.arange(n)[:, None] - np.arange(nc)[None, :]
+        A0 = np.where(idx >= 0, col[np.clip(idx, 0, n - 1)], 0.0)
+        c = rng.random(n)
+        r = np.concatenate([[c[0]], rng.random(nc - 1)])
+        E = eps * np.where(idx >= 0, c[np.clip(idx, 0, n - 1)], r[np.clip(-idx, 0, nc - 1)])
+        b0 = np.ones(n)
+        e = eps * rng.random(n)
+    elif name == "vanhuffel":
+        n = kw.get("n", 100)
+        eps = 1e-6 if eps is None else eps
+        A0 = -np.ones((n, n - 2))
+        A0[np.arange(n - 2), np.arange(n - 2)] = n - 1.0
+        b0 = -np.ones(n)
+        b0[n - 2] = n - 1.0
+        E = eps * rng.random((n, n - 2))
+        e = eps * rng.random(n)
+    else:
+        raise ValueError(f"unknown paper problem {name!r}")
+    A = np.ascontiguousarray(A0 + E)
+    return PaperProblem(name, A, b0 + e, A0, b0, x_true, float(eps), seed)
+
+
+PAPER_PROBLEMS = ("random", "delta", "bjorck", "toeplitz", "vanhuffel")
