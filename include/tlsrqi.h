@@ -107,7 +107,12 @@ typedef struct {
                              no pass over A inside PCGTLS; the sigma = 0 bootstrap stays A-in-loop) */
   int32_t breakdown_rule; /* 0: delta < 0 is a breakdown (R3) [0]; 1: only delta == 0 stops */
   int32_t gram_chunk;     /* K_t rows per fp32 accumulation chunk (R11) [64]; multiple of 64 for the tensor-core path */
-  int32_t reserved[5];
+  int32_t u_p;            /* precision of the PCGTLS operator A^T A q of the RQI's inner solves (R23):
+                             0 or TLS_FP64 [0]; TLS_FP32 = the paper's experimental setting u_p = single
+                              on an fp32 copy of A made by the solve and kept in the
+                             precond handle (4 m_local ld32 bytes, dense A, n <= 2048, op_variant 0).
+                             The bootstrap, the residual passes and all n-vector work stay fp64. */
+  int32_t reserved[4];
 } tls_rqi_opts_t;
 
 /* Results.  pcg_iters (2*max_outer ints), sigma2_trace, psi_trace
@@ -198,6 +203,11 @@ TLS_API int tls_gram(const tls_matrix_t* A, int32_t u_f, const double* d_dev, in
 TLS_API int tls_pass(const tls_matrix_t* A, int32_t mode, int32_t nrhs, const double* q_dev,
              const double* b_dev, double* v_dev, double* s_dev, void* stream, void* ws_dev,
              size_t ws_bytes);
+/* a7 with u_p = fp32 (R23): the 2-RHS operator pass on R's fp32 copy of this A (made on
+ * first use): t_r = fl32(A) fl32(q_r) and v_r = fl32(A)^T t_r accumulated in fp32, s[r] =
+ * t_r^T t_r in fp64.  q_dev, v_dev: 2 x n fp64; s_dev: 2 doubles. */
+TLS_API int tls_pass_fp32(const tls_matrix_t* A, tls_precond_t R, const double* q_dev, double* v_dev,
+                          double* s_dev, void* stream, void* ws_dev, size_t ws_bytes);
 /* a6: Y_dev (nrhs x n) <- P^{-1} Y (trans = 0: D^{-1} R~^{-1} Y, back substitution)
  * or P^{-T} Y (trans = 1: R~^{-T} D^{-1} Y, forward substitution), nrhs in {1,2}. */
 TLS_API int tls_precond_apply(const tls_precond_t R, int32_t trans, int32_t nrhs, double* Y_dev,
@@ -217,7 +227,8 @@ enum {
   TLS_PROF_PCG_STEP = 6,  /* fused PCG step: fwd solve + recurrences + back solve (a6, a8) */
   TLS_PROF_PCG_INIT = 7,  /* PCG initialisation: fwd + back solve (a6) */
   TLS_PROF_REDUCE = 8,    /* fixed-order partial reductions */
-  TLS_PROF_NCAT = 9
+  TLS_PROF_PASS_OP2_FP32 = 9, /* operator pass on the fp32 copy of A (u_p = fp32, R23) */
+  TLS_PROF_NCAT = 10
 };
 /* Enable (1) or disable (0) timing; both reset the accumulated totals. */
 TLS_API int tls_profile_enable(int on);

@@ -200,8 +200,20 @@ class PcgResult:
     delta_min: float = math.inf
 
 
+def operator_fp32(A32, q: np.ndarray):
+    """The A-in-loop operator at u_p = fp32 (reading R23; PAPER.md l.480-482 run PCGTLS
+    in single): q rounded to fp32 (RNE), t = A32 q and v = A32^T t each accumulated in
+    fp32 (numpy's float32 matrix-vector products), t^T t in fp64 of the fp32 t.
+    Returns (t^T t, v) in fp64."""
+    q32 = q.astype(np.float32)
+    t = np.asarray(A32 @ q32, dtype=np.float32).reshape(-1)
+    t64 = t.astype(np.float64)
+    v = np.asarray(A32.T @ t, dtype=np.float32).reshape(-1).astype(np.float64)
+    return float(t64 @ t64), v
+
+
 def pcgtls(A, pc: Precond, sigma2: float, f: np.ndarray, l: int, tol_inner: float,
-           variant: str = "A", breakdown_rule: str = "spec") -> PcgResult:
+           variant: str = "A", breakdown_rule: str = "spec", A32=None) -> PcgResult:
     """l-step PCGTLS for (A^T A - sigma^2 I) omega = f (Alg. 3, l.186-204).
 
     variant "A" (default, reading R1): the preconditioned operator
@@ -212,7 +224,9 @@ def pcgtls(A, pc: Precond, sigma2: float, f: np.ndarray, l: int, tol_inner: floa
     delta = p^T p - sigma^2 q^T q (l.194), w = p - sigma^2 P^{-T} q (l.197-198).
     Loop guard (R3): delta non-finite or zero stops before the update (l.192);
     delta < 0 is a breakdown under the "spec" rule; at most l updates (R3);
-    early exit after an update when eta_{j+1} <= tol_inner^2 eta_0."""
+    early exit after an update when eta_{j+1} <= tol_inner^2 eta_0.
+    A32 (variant "A" only): the fp32 copy of A; the operator then runs at u_p = fp32
+    (operator_fp32, R23) and everything else stays fp64."""
     n = f.shape[0]
     omega = np.zeros(n)                        # l.191
     s = apply_PinvT(pc, f)
@@ -224,7 +238,10 @@ def pcgtls(A, pc: Precond, sigma2: float, f: np.ndarray, l: int, tol_inner: floa
         return res
     for j in range(l):                         # l.192
         q = apply_Pinv(pc, p)                  # l.193
-        if variant == "A":
+        if variant == "A" and A32 is not None:
+            tt, v = operator_fp32(A32, q)
+            delta = tt - sigma2 * float(q @ q)
+        elif variant == "A":
             t = matvec(A, q)
             delta = float(t @ t) - sigma2 * float(q @ q)
         else:
@@ -237,7 +254,9 @@ def pcgtls(A, pc: Precond, sigma2: float, f: np.ndarray, l: int, tol_inner: floa
             break
         alpha = eta / delta                    # l.195
         omega = omega + alpha * q              # l.196
-        if variant == "A":
+        if variant == "A" and A32 is not None:
+            w = apply_PinvT(pc, v - sigma2 * q)
+        elif variant == "A":
             w = apply_PinvT(pc, rmatvec(A, t) - sigma2 * q)
         else:
             w = p - sigma2 * apply_PinvT(pc, q)            # l.197
@@ -268,6 +287,7 @@ class RqiOptions:
     op_variant: int = 0        # 0: A-in-loop (R1); 1: paper Alg. 3
     breakdown_rule: int = 0    # 0: delta <= 0 stops (spec); 1: delta == 0 only (paper)
     gram_chunk: int = 64
+    u_p: str = "fp64"          # operator precision of the RQI's inner solves (R23): "fp64" | "fp32"
 
 
 @dataclasses.dataclass
@@ -319,6 +339,7 @@ def rqi_pcgtls_mp(A, b: np.ndarray, pc: Precond, tol: float = 1e-14,
     rule = "spec" if o.breakdown_rule == 0 else "paper"
     tol_in = tol if o.tol_inner <= 0 else o.tol_inner
     n = A.shape[1]
+    A32 = A.astype(np.float32) if (o.u_p == "fp32" and variant == "A") else None   # fl32(A), RNE
     if pc.status != OK:
         return RqiResult(np.zeros(n), math.nan, pc.status, T_BREAKDOWN, 0, 0, [], [], [])
     passes = 0
@@ -377,8 +398,8 @@ def rqi_pcgtls_mp(A, b: np.ndarray, pc: Precond, tol: float = 1e-14,
             res.x, res.sigma, res.status, res.termination = x, math.sqrt(sig2), MAX_OUTER, T_MAX_OUTER
             break
         budget = k + 1 if o.budget_rule == 0 else 400
-        ra = pcgtls(A, pc, sig2, -f, budget, tol_in, variant, rule)     # l.246
-        rb = pcgtls(A, pc, sig2, x, budget, tol_in, variant, rule)      # l.252
+        ra = pcgtls(A, pc, sig2, -f, budget, tol_in, variant, rule, A32)     # l.246
+        rb = pcgtls(A, pc, sig2, x, budget, tol_in, variant, rule, A32)      # l.252
         if variant == "A":
             passes += ra.count + rb.count + (ra.breakdown or ra.count < budget) + (rb.breakdown or rb.count < budget)
         res.pcg_iters.append((ra.count, rb.count))

@@ -82,6 +82,12 @@ struct tls_precond_s {
   size_t bytes;
   int device;
   double normA2_host;
+  // u_p = fp32 (R23): fl32 copy of the local row block of A, made by the first solve that
+  // asks for it and kept for later solves on the same block (keyed by pointer and shape)
+  float* a32 = nullptr;
+  size_t a32_bytes = 0;
+  const double* a32_src = nullptr;
+  int64_t a32_m = -1, a32_ld = -1;
 };
 
 static int allreduce(tls_comm_t comm, double* buf, size_t count, int op, cudaStream_t st) {
@@ -385,6 +391,66 @@ int run_pass(Ctx& cx, const tls_matrix_t* A, int mode, int nrhs, const double* q
   } else {
     TLS_TRY(allreduce(cx.comm, out, W, ncclSum, cx.st));
   }
+  return 0;
+}
+
+// One spare fp32-copy buffer kept by tls_precond_destroy for the next handle (a fresh
+// cudaMalloc/cudaFree of the 4 GiB copy per solve would stall the stream).
+struct A32Spare { int device = -1; size_t bytes = 0; float* ptr = nullptr; };
+static A32Spare& a32_spare() {
+  static A32Spare s;
+  return s;
+}
+
+// The fl32 copy of the dense local block held by the handle (R23): (re)made when missing
+// or made for another block.  The only allocation outside alloc_precond; freed with R.
+int ensure_a32(Ctx& cx, const tls_matrix_t* A, tls_precond_t R) {
+  if (is_csr(A)) { set_error("u_p = fp32 needs a dense A"); return TLS_ERR_UNSUPPORTED; }
+  if (A->n > 2048) { set_error("u_p = fp32 needs n <= 2048"); return TLS_ERR_UNSUPPORTED; }
+  if (R->a32 && R->a32_src == A->vals && R->a32_m == A->m_local && R->a32_ld == A->ld) return 0;
+  const size_t bytes = (size_t)A->m_local * p32_ld((int)A->n) * 4 + 256;
+  if (R->a32_bytes < bytes) {
+    if (R->a32) { cudaStreamSynchronize(cx.st); cudaFree(R->a32); R->a32 = nullptr; R->a32_bytes = 0; }
+    A32Spare& sp = a32_spare();
+    if (sp.ptr && sp.device == R->device && sp.bytes >= bytes) {
+      R->a32 = sp.ptr;
+      R->a32_bytes = sp.bytes;
+      sp.ptr = nullptr;
+    }
+  }
+  if (R->a32_bytes < bytes) {
+    const cudaError_t e = cudaMalloc(&R->a32, bytes);
+    if (e != cudaSuccess) { set_error("cudaMalloc(A32 %zu B): %s", bytes, cudaGetErrorString(e)); return TLS_ERR_CUDA; }
+    R->a32_bytes = bytes;
+  }
+  TLS_TRY(launch_round32(dense_view(A), R->a32, cx.st));
+  R->a32_src = A->vals;
+  R->a32_m = A->m_local;
+  R->a32_ld = A->ld;
+  cx.launches += 1;
+  cx.passes += 1;
+  return 0;
+}
+
+// 2-RHS operator pass over the fp32 copy (u_p = fp32, k_pass32.cu) into w.passout.
+int run_pass32(Ctx& cx, const tls_matrix_t* A, tls_precond_t R, const double* q, Work& w, const int* active) {
+  const int n = (int)A->n;
+  const int W = 2 * n + 2;
+  const DenseView dv = dense_view(A);
+  int G = 1;
+  {
+    ProfScope ps(TLS_PROF_PASS_OP2_FP32, cx.st);
+    TLS_TRY(launch_pass32(dv, R->a32, q, w.partials, active, cx.st, &G));
+  }
+  if (dv.m > 0) {
+    ProfScope ps(TLS_PROF_REDUCE, cx.st);
+    TLS_TRY(launch_reduce(w.partials, G, W, 0, w.passout, active, cx.st));
+    cx.launches += 2;
+  } else {
+    TLS_CUDA_TRY(cudaMemsetAsync(w.passout, 0, (size_t)W * 8, cx.st));
+  }
+  cx.passes += 1;
+  TLS_TRY(allreduce(cx.comm, w.passout, W, ncclSum, cx.st));
   return 0;
 }
 
@@ -739,6 +805,16 @@ int tls_precond_export(tls_precond_t R, double* Rt_host, double* d_host, double*
 
 void tls_precond_destroy(tls_precond_t R) {
   if (!R) return;
+  if (R->a32) {
+    cudaDeviceSynchronize();
+    A32Spare& sp = a32_spare();
+    if (sp.ptr == nullptr || sp.bytes < R->a32_bytes) {
+      if (sp.ptr) cudaFree(sp.ptr);
+      sp = A32Spare{R->device, R->a32_bytes, R->a32};
+    } else {
+      cudaFree(R->a32);
+    }
+  }
   if (R->base) {
     auto& pool = precond_pool();
     if (pool.size() < 8) {
@@ -762,6 +838,8 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   tls_rqi_opts_t o;
   if (opts) o = *opts; else tls_rqi_opts_default(&o);
   if (o.op_variant != 0 && o.op_variant != 1) { set_error("op_variant must be 0 (A-in-loop) or 1 (paper Alg. 3)"); return TLS_ERR_ARG; }
+  if (o.u_p != 0 && o.u_p != TLS_FP64 && o.u_p != TLS_FP32) { set_error("u_p must be TLS_FP64 (or 0) or TLS_FP32"); return TLS_ERR_UNSUPPORTED; }
+  const bool up32 = o.u_p == TLS_FP32 && o.op_variant == 0;
   if (o.max_outer < 1) o.max_outer = 1;
   Work w;
   if (!carve_ok(A, ws, ws_bytes, w, false)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
@@ -769,6 +847,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   const int n = (int)A->n;
   const PrecondDev& pc = R->dev;
   if (is_csr(A)) TLS_TRY(launch_csc_build(csr_view(A), w.csc, w.csc_scratch, cx.st, &cx.launches));
+  if (up32) TLS_TRY(ensure_a32(cx, A, R));
   const double tol_in = o.tol_inner > 0 ? o.tol_inner : tol;
   PcgState hS;
 
@@ -791,12 +870,15 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   // budget the host polls the activity flags every 8 iterations.
   // variant 0: one batched operator pass over A per iteration (R1); variant 1: the
   // paper's A-free Alg. 3 (no pass).  The sigma = 0 bootstrap always uses variant 0.
-  auto pcg_loop = [&](int nrhs, int budget, int variant) -> int {
+  // fp32: the RQI's inner solves run their operator pass on the fp32 copy (u_p, R23);
+  // the sigma = 0 bootstrap stays fp64 (R5: x_LS to 1e-8).
+  auto pcg_loop = [&](int nrhs, int budget, int variant, bool fp32) -> int {
     for (int j = 0; j < budget; ++j) {
       // the 2-RHS dense kernel is faster than the 1-RHS one at the same bytes (measured, see
       // DESIGN §6): a 1-RHS solve passes its q with the second slot held at zero
       const int pass_rhs = (nrhs == 1 && !is_csr(A)) ? 2 : nrhs;
-      if (variant == 0) TLS_TRY(run_pass(cx, A, PASS_OPERATOR, pass_rhs, w.vec.q, nullptr, w, w.S->active));
+      if (variant == 0 && fp32) TLS_TRY(run_pass32(cx, A, R, w.vec.q, w, w.S->active));
+      else if (variant == 0) TLS_TRY(run_pass(cx, A, PASS_OPERATOR, pass_rhs, w.vec.q, nullptr, w, w.S->active));
       {
         ProfScope ps(TLS_PROF_PCG_STEP, cx.st);
         TLS_TRY(launch_pcg_step(pc, w.vec, w.passout, w.S, nrhs, o.breakdown_rule, j + 1 < budget ? 1 : 0, variant,
@@ -833,7 +915,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
       TLS_TRY(launch_pcg_init(pc, 1, w.vec, w.S, cx.st));
     }
     cx.launches += 1;
-    TLS_TRY(pcg_loop(1, o.boot_max, 0));
+    TLS_TRY(pcg_loop(1, o.boot_max, 0, false));
     TLS_TRY(read_state());
     boot_iters = hS.count[0];
     k_copy<<<(n + 255) / 256, 256, 0, cx.st>>>(w.vec.omega, w.x0, n);
@@ -892,7 +974,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
     }
     cx.launches += 1;
     tr.mark("pcg_init");
-    TLS_TRY(pcg_loop(2, budget, o.op_variant));
+    TLS_TRY(pcg_loop(2, budget, o.op_variant, up32));
     tr.mark("pcg_loop");
     TLS_TRY(read_state());
     pcgc.push_back(hS.count[0]);
@@ -1024,6 +1106,21 @@ int tls_pass(const tls_matrix_t* A, int32_t mode, int32_t nrhs, const double* q,
   TLS_TRY(run_pass(cx, A, mode == 0 ? PASS_OPERATOR : PASS_RESIDUAL, nrhs, q, b, w, nullptr));
   TLS_CUDA_TRY(cudaMemcpyAsync(v, w.passout, (size_t)nrhs * n * 8, cudaMemcpyDeviceToDevice, cx.st));
   TLS_CUDA_TRY(cudaMemcpyAsync(s, w.passout + (size_t)nrhs * n, 16, cudaMemcpyDeviceToDevice, cx.st));
+  return 0;
+}
+
+int tls_pass_fp32(const tls_matrix_t* A, tls_precond_t R, const double* q, double* v, double* s, void* stream,
+                  void* ws, size_t ws_bytes) {
+  TLS_TRY(check_matrix(A));
+  if (!R || R->dev.n != A->n) { set_error("bad handle"); return TLS_ERR_ARG; }
+  Work w;
+  if (!carve_ok(A, ws, ws_bytes, w, false)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
+  Ctx cx{static_cast<cudaStream_t>(stream), nullptr};
+  const int n = (int)A->n;
+  TLS_TRY(ensure_a32(cx, A, R));
+  TLS_TRY(run_pass32(cx, A, R, q, w, nullptr));
+  TLS_CUDA_TRY(cudaMemcpyAsync(v, w.passout, (size_t)2 * n * 8, cudaMemcpyDeviceToDevice, cx.st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(s, w.passout + (size_t)2 * n, 16, cudaMemcpyDeviceToDevice, cx.st));
   return 0;
 }
 

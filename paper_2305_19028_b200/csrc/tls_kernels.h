@@ -25,6 +25,12 @@ size_t pass_partials_doubles(const DenseView& A);
 // `active` (may be NULL): int[2] of PCG activity flags; the kernel is a no-op when both are 0.
 int launch_pass(const DenseView& A, int mode, int nrhs, const double* q, const double* b,
                 double* partials, const int* active, cudaStream_t st, int* grid_out);
+// u_p = fp32 operator pass (k_pass32.cu, R23): A32 = fl32(A) row-major with ld32 = p32_ld(n);
+// 2 RHS, writes grid x (2n + 2) partials like launch_pass (grid <= pass_partials rows).
+int p32_ld(int n);
+int launch_round32(const DenseView& A, float* A32, cudaStream_t st);
+int launch_pass32(const DenseView& A, const float* A32, const double* q, double* partials, const int* active,
+                  cudaStream_t st, int* grid_out);
 // out[w] = sum_g partials[g][w] (max for w < nmax), fixed order.
 int launch_reduce(const double* partials, int G, int W, int nmax, double* out, const int* active,
                   cudaStream_t st);

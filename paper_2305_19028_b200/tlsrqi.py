@@ -37,8 +37,8 @@ class tls_rqi_opts_t(C.Structure):
     _fields_ = [("budget_rule", C.c_int32), ("stop_rule", C.c_int32), ("max_outer", C.c_int32),
                 ("polish", C.c_int32), ("tol_inner", C.c_double), ("boot", C.c_int32),
                 ("boot_max", C.c_int32), ("boot_tol", C.c_double), ("op_variant", C.c_int32),
-                ("breakdown_rule", C.c_int32), ("gram_chunk", C.c_int32),
-                ("reserved", C.c_int32 * 5)]
+                ("breakdown_rule", C.c_int32), ("gram_chunk", C.c_int32), ("u_p", C.c_int32),
+                ("reserved", C.c_int32 * 4)]
 
 
 class tls_info_t(C.Structure):
@@ -85,6 +85,7 @@ def lib() -> C.CDLL:
         "tls_colstats": (C.c_int, [M, VP, VP, VP, VP, SZ]),
         "tls_gram": (C.c_int, [M, I32, VP, I32, VP, VP, VP, SZ]),
         "tls_pass": (C.c_int, [M, I32, I32, VP, VP, VP, VP, VP, VP, SZ]),
+        "tls_pass_fp32": (C.c_int, [M, VP, VP, VP, VP, VP, VP, SZ]),
         "tls_precond_apply": (C.c_int, [VP, I32, I32, VP, VP]),
         "tls_round": (C.c_int, [VP, VP, I64, I32, VP]),
         "tls_profile_enable": (C.c_int, [C.c_int]),
@@ -102,10 +103,10 @@ EXPORTED = ["tls_abi_version", "tls_rqi_opts_default", "tls_status_string", "tls
             "tls_comm_get_unique_id", "tls_comm_init", "tls_comm_destroy", "tls_workspace_size",
             "tls_factor_precond", "tls_precond_import", "tls_precond_export", "tls_precond_destroy",
             "tls_rqi_pcgtls", "tls_solve_host_bytes", "tls_solve_host", "tls_colstats", "tls_gram",
-            "tls_pass", "tls_precond_apply", "tls_round", "tls_profile_enable", "tls_profile_read"]
+            "tls_pass", "tls_pass_fp32", "tls_precond_apply", "tls_round", "tls_profile_enable", "tls_profile_read"]
 
 PROF_CATS = ["pass_op2", "pass_op1", "pass_resid", "colstats", "gram", "chol", "pcg_step",
-             "pcg_init", "reduce"]
+             "pcg_init", "reduce", "pass_op2_fp32"]
 
 
 class TlsError(RuntimeError):
@@ -139,6 +140,8 @@ def tls_rqi_opts_default(**over) -> tls_rqi_opts_t:
     o = tls_rqi_opts_t()
     lib().tls_rqi_opts_default(C.byref(o))
     for k, v in over.items():
+        if k == "u_p" and isinstance(v, str):      # "fp64" / "fp32" (R23)
+            v = PREC[v]
         setattr(o, k, v)
     return o
 
@@ -357,6 +360,17 @@ def tls_pass(M: tls_matrix_t, mode: int, q: torch.Tensor, b: Optional[torch.Tens
     s = torch.empty(2, dtype=torch.float64, device="cuda")
     _check(lib().tls_pass(C.byref(M), mode, nrhs, _ptr(q.contiguous()), _ptr(b), _ptr(v), _ptr(s),
                           _stream(stream), _ptr(ws), ws.numel()), "tls_pass")
+    return v, s
+
+
+def tls_pass_fp32(M: tls_matrix_t, R: "Precond", q: torch.Tensor, stream=None, ws=None):
+    """u_p = fp32 operator pass (R23) on R's fp32 copy of A: q (2 x n) -> (v, s)."""
+    if ws is None:
+        ws = workspace(M)
+    v = torch.empty((2, int(M.n)), dtype=torch.float64, device="cuda")
+    s = torch.empty(2, dtype=torch.float64, device="cuda")
+    _check(lib().tls_pass_fp32(C.byref(M), C.c_void_p(R.handle), _ptr(q.contiguous()), _ptr(v), _ptr(s),
+                               _stream(stream), _ptr(ws), ws.numel()), "tls_pass_fp32")
     return v, s
 
 

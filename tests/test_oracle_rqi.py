@@ -347,3 +347,47 @@ def test_csr_gram_bf16_within_fp64_summation_bound():
     G = rqi.gram_uf(A, d, "bf16")
     bound = 300 * 2.0 ** -53 * (np.abs(Ah).T @ np.abs(Ah))
     assert np.all(np.abs(G - Ah.T @ Ah) <= 2 * bound)
+
+
+# ----------------------------------------------------------------------------- u_p = fp32 (R23)
+def test_operator_fp32_within_fp32_bound():
+    """operator_fp32 (R23): v and t^T t lie within the closed-form fp32 accumulation
+    bound around the exact product of the fp32-rounded data (gamma_k = k u/(1 - k u),
+    u = 2^-24), and they are NOT the fp64 result (the arithmetic really is fp32)."""
+    rng = np.random.default_rng(11)
+    m, n = 3000, 300
+    A = rng.standard_normal((m, n)) * np.logspace(0, -2, n)
+    q = rng.standard_normal(n)
+    A32 = A.astype(np.float32)
+    tt, v = rqi.operator_fp32(A32, q)
+    Ae = A32.astype(np.float64)
+    qe = q.astype(np.float32).astype(np.float64)
+    t_ex = Ae @ qe
+    u = 2.0 ** -24
+    g = lambda k: k * u / (1 - k * u)
+    tb = g(n) * (np.abs(Ae) @ np.abs(qe))                    # |t32 - t_ex| bound
+    t32 = (A32 @ q.astype(np.float32)).astype(np.float64)
+    assert np.all(np.abs(t32 - t_ex) <= tb)
+    vb = g(m) * (np.abs(Ae).T @ np.abs(t32)) + np.abs(Ae).T @ tb
+    v_ex = Ae.T @ t_ex
+    assert np.all(np.abs(v - v_ex) <= vb)
+    assert abs(tt - float(t_ex @ t_ex)) <= 2.0 * float(np.abs(t_ex) @ tb) + 1e-300
+    v64 = A.T @ (A @ q)
+    assert np.max(np.abs(v - v64) / np.abs(v64).max()) > 1e-9      # fp32 arithmetic happened
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2w", "random", "delta", "toeplitz", "vanhuffel"])
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+def test_up_fp32_suffices(name, fmt):
+    """with u = fp64, single precision for the PCG (u_p) 'was
+    sufficient for all included examples': the same status and RQI count as u_p = fp64
+    and the limiting accuracy of the SVD."""
+    P = tlsgen.config(name) if name.startswith("cfg") else tlsgen.paper_problem(name)
+    ex = exact.tls_svd(P.A, P.b)
+    pc = rqi.factor_precond(P.A, fmt)
+    r64 = rqi.rqi_pcgtls_mp(P.A, P.b, pc)
+    r32 = rqi.rqi_pcgtls_mp(P.A, P.b, pc, opts=rqi.RqiOptions(u_p="fp32"))
+    assert r32.status == r64.status == rqi.OK
+    assert r32.rqi_iters == r64.rqi_iters
+    assert np.linalg.norm(r32.x - ex.x) / np.linalg.norm(ex.x) <= 1e-12
+    assert abs(r32.sigma - ex.sigma) / ex.sigma <= 1e-12
