@@ -27,7 +27,7 @@ constexpr int kTB = 64;             // tile edge
 constexpr int kTS = kTB + 1;        // smem row stride (doubles)
 constexpr int kCholThreads = 256;
 
-enum { T_POTRF = 0, T_TRSM = 1, T_UPDATE = 2 };
+enum { T_POTRF = 0, T_TRSM = 1, T_UPDATE = 2, T_DIAG = 3 };
 
 struct CholCtl {          // device control block (zeroed before the launch)
   int next;               // task counter
@@ -62,14 +62,23 @@ __device__ bool wait_flag(const int* flag, int want, const CholCtl* ctl) {
 
 // tile (ti, tj) of G -> smem S[64][65] (zeros outside the matrix; identity padding on the
 // diagonal tile when `pad_identity`)
+// All 16 loads of a thread are issued before the first shared-memory store (one L2 round
+// trip per tile instead of 16 dependent ones: measured 9.2 -> see DESIGN §6).
 __device__ void load_tile(const double* G, int n, int ti, int tj, double* S, bool upper_only, bool pad_identity) {
-  for (int e = threadIdx.x; e < kTB * kTB; e += blockDim.x) {
+  constexpr int kPer = kTB * kTB / kCholThreads;
+  double v[kPer];
+#pragma unroll
+  for (int r = 0; r < kPer; ++r) {
+    const int e = threadIdx.x + r * kCholThreads;
     const int i = e >> 6, j = e & 63;
     const int gi = ti * kTB + i, gj = tj * kTB + j;
-    double v;
-    if (gi < n && gj < n) v = (upper_only && gj < gi) ? 0.0 : __ldcg(G + (size_t)gi * n + gj);
-    else v = (pad_identity && i == j) ? 1.0 : 0.0;
-    S[i * kTS + j] = v;
+    if (gi < n && gj < n) v[r] = (upper_only && gj < gi) ? 0.0 : __ldcg(G + (size_t)gi * n + gj);
+    else v[r] = (pad_identity && i == j) ? 1.0 : 0.0;
+  }
+#pragma unroll
+  for (int r = 0; r < kPer; ++r) {
+    const int e = threadIdx.x + r * kCholThreads;
+    S[(e >> 6) * kTS + (e & 63)] = v[r];
   }
 }
 
@@ -93,10 +102,24 @@ __device__ void store_tile(double* G, int n, int ti, int tj, const double* S, bo
 #else
 #define PMARK(k) do {} while (0)
 #endif
+// 1/x for a positive normal pivot: MUFU.RCP64H seed and two Newton steps (~1 ulp).  The
+// pivots sit on the factorization's critical path; per 16-pivot diagonal block this is
+// 4.5k cycles against 5.3k for the IEEE division routine and 7.2k for an fp32 seed
+// (tools/micro/diag16.cu).
+__device__ __forceinline__ double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 __device__ int potrf_tile(double* S, double* dr, int nb) {
   __shared__ int fail;
   __shared__ double rowb[2][16];
   __shared__ double F[16][kTB + 1];      // multipliers of the current block: F[j][i] = U_ji / d_j
+  __shared__ double bdinv[16];           // 1 / d_j of the current block
   const int tid = threadIdx.x;
   if (tid == 0) fail = 0;
   __syncthreads();
@@ -110,17 +133,21 @@ __device__ int potrf_tile(double* S, double* dr, int nb) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = S[(o + i) * kTS + o + t];
       int f = 0;
+      // no `break`: a loop exit kept the loop rolled and v[] in local memory (measured)
 #pragma unroll
       for (int jj = 0; jj < 16; ++jj) {
         const double piv = __shfl_sync(0xffffffffu, v[jj], jj);
-        if (o + jj < nb) {
-          if (!(piv > 0.0) || !isfinite(piv)) { f = o + jj + 1; break; }
-          const double dinv = 1.0 / piv;
-          const double sjt = v[jj];
+        if (o + jj < nb && f == 0) {
+          if (!(piv > 0.0 && piv < INFINITY)) {      // non-positive, NaN or +inf pivot
+            f = o + jj + 1;
+          } else {
+            const double dinv = rcp_fast(piv);
+            const double sjt = v[jj];
 #pragma unroll
-          for (int ii = jj + 1; ii < 16; ++ii) {
-            const double m = __shfl_sync(0xffffffffu, v[jj], ii) * dinv;
-            if (t >= ii) v[ii] = fma(-m, sjt, v[ii]);
+            for (int ii = jj + 1; ii < 16; ++ii) {
+              const double m = __shfl_sync(0xffffffffu, v[jj], ii) * dinv;
+              if (t >= ii) v[ii] = fma(-m, sjt, v[ii]);
+            }
           }
         }
       }
@@ -128,6 +155,8 @@ __device__ int potrf_tile(double* S, double* dr, int nb) {
 #pragma unroll
         for (int i = 0; i < 16; ++i)
           if (i <= t) S[(o + i) * kTS + o + t] = v[i];
+        // d_t, read back (indexing v[t] with the lane index would put v[] in local memory)
+        bdinv[t] = rcp_fast(S[(o + t) * kTS + o + t]);
       }
       if (tid == 0 && f) fail = f;
     }
@@ -137,8 +166,7 @@ __device__ int potrf_tile(double* S, double* dr, int nb) {
     // (2) multipliers of the block and the block row to its right (columns c >= o + 16)
     for (int e = tid; e < 16 * kTB; e += blockDim.x) {
       const int jj = e >> 6, c = e & 63;
-      const double d = S[(o + jj) * kTS + o + jj];
-      F[jj][c] = (c > o + jj && o + jj < nb) ? S[(o + jj) * kTS + c] / d : 0.0;   // inside the block for now
+      F[jj][c] = (c > o + jj && o + jj < nb) ? S[(o + jj) * kTS + c] * bdinv[jj] : 0.0;   // inside the block for now
     }
     __syncthreads();
     const int w = kTB - o - 16;                 // columns to the right
@@ -160,7 +188,7 @@ __device__ int potrf_tile(double* S, double* dr, int nb) {
     // multipliers for the columns right of the block (final U rows of the block)
     for (int e = tid; e < 16 * w; e += blockDim.x) {
       const int jj = e / w, c = o + 16 + e % w;
-      F[jj][c] = (o + jj < nb) ? S[(o + jj) * kTS + c] / S[(o + jj) * kTS + o + jj] : 0.0;
+      F[jj][c] = (o + jj < nb) ? S[(o + jj) * kTS + c] * bdinv[jj] : 0.0;
     }
     __syncthreads();
     PMARK(3 + (o / 16) * 4);
@@ -194,7 +222,7 @@ __device__ int potrf_tile(double* S, double* dr, int nb) {
   __shared__ double rs[kTB];
   if (tid < kTB) {
     const double sq = sqrt(S[tid * kTS + tid]);
-    rs[tid] = 1.0 / sq;
+    rs[tid] = rcp_fast(sq);
     dr[tid] = rs[tid];
     S[tid * kTS + tid] = sq;
   }
@@ -236,6 +264,7 @@ __device__ void trsm_tile(const double* R, const double* dr, double* B) {
 // (conflict-free), A reads are warp broadcasts.
 __device__ __forceinline__ void tile_atb(const double* A, const double* B, double (&acc)[4][4]) {
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+#pragma unroll 4
   for (int i = 0; i < kTB; ++i) {
     double a[4], b[4];
 #pragma unroll
@@ -270,14 +299,19 @@ k_chol_dag(double* __restrict__ G, int n, int T, const int4* __restrict__ tasks,
     const int type = tk.x, k = tk.y, i = tk.z, j = tk.w;
     unsigned long long t0 = 0;
     if (trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    unsigned long long tready = 0, tload = 0, tcomp = 0;
+#define TSTAMP(v) do { if (trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v)); } while (0)
     if (type == T_POTRF) {
       bool ok = wait_flag(&upd_done[k * T + k], k, ctl);
+      if (trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tready));
       int f = 0;
       if (ok) {
         load_tile(G, n, k, k, S0, true, true);
         __syncthreads();
+        TSTAMP(tload);
         const int nb = min(kTB, n - k * kTB);
         f = potrf_tile(S0, S1, nb);
+        TSTAMP(tcomp);
         if (!f) {
           store_tile(G, n, k, k, S0, true);
           if (tid < kTB) xinv[(size_t)k * kTB + tid] = S1[tid];
@@ -294,13 +328,16 @@ k_chol_dag(double* __restrict__ G, int n, int T, const int4* __restrict__ tasks,
       }
     } else if (type == T_TRSM) {      // R_kj = X_k^T G_kj
       bool ok = wait_flag(&potrf_done[k], 1, ctl) && wait_flag(&upd_done[k * T + j], k, ctl);
+      if (trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tready));
       if (ok) {
         load_tile(G, n, k, k, S0, true, true);      // R_kk (upper, identity padding)
         if (tid < kTB) S2[tid] = __ldcg(xinv + (size_t)k * kTB + tid);
         load_tile(G, n, k, j, S1, false, false);
         __syncthreads();
+        TSTAMP(tload);
         trsm_tile(S0, S2, S1);
         __syncthreads();
+        TSTAMP(tcomp);
         store_tile(G, n, k, j, S1, false);
       }
       __syncthreads();
@@ -308,14 +345,67 @@ k_chol_dag(double* __restrict__ G, int n, int T, const int4* __restrict__ tasks,
         __threadfence();
         st_release(&trsm_done[k * T + j], 1);
       }
+    } else if (type == T_DIAG) {
+      // TRSM(k, k+1), then UPDATE(k, k+1, k+1) and POTRF(k+1) on the tile still in shared
+      // memory: the factorization's critical path without two store/flag/load hops
+      const int jn = k + 1;
+      __shared__ double drk[kTB], drj[kTB];
+      bool ok = wait_flag(&potrf_done[k], 1, ctl) && wait_flag(&upd_done[k * T + jn], k, ctl);
+      TSTAMP(tready);
+      if (ok) {
+        load_tile(G, n, k, k, S0, true, true);
+        if (tid < kTB) drk[tid] = __ldcg(xinv + (size_t)k * kTB + tid);
+        load_tile(G, n, k, jn, S1, false, false);
+        __syncthreads();
+        trsm_tile(S0, drk, S1);
+        __syncthreads();
+        store_tile(G, n, k, jn, S1, false);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        st_release(&trsm_done[k * T + jn], 1);
+      }
+      ok = ok && wait_flag(&upd_done[jn * T + jn], k, ctl);
+      TSTAMP(tload);
+      int f = 0;
+      if (ok) {
+        load_tile(G, n, jn, jn, S2, true, true);
+        __syncthreads();
+        double acc[4][4] = {};
+        tile_atb(S1, S1, acc);
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) S2[(4 * ty + p) * kTS + tx + 16 * q] -= acc[p][q];
+        __syncthreads();
+        f = potrf_tile(S2, drj, min(kTB, n - jn * kTB));
+        TSTAMP(tcomp);
+        if (!f) {
+          store_tile(G, n, jn, jn, S2, true);
+          if (tid < kTB) xinv[(size_t)jn * kTB + tid] = drj[tid];
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        if (f) {
+          atomicCAS(&ctl->fail, 0, jn * kTB + f);
+          atomicCAS(pivot, 0, jn * kTB + f);
+        }
+        __threadfence();
+        st_release(&upd_done[jn * T + jn], k + 1);
+        st_release(&potrf_done[jn], 1);
+      }
     } else {                          // G_ij -= R_ki^T R_kj, applied in k order
       bool ok = wait_flag(&trsm_done[k * T + i], 1, ctl) && wait_flag(&trsm_done[k * T + j], 1, ctl) &&
                 wait_flag(&upd_done[i * T + j], k, ctl);
+      if (trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tready));
       if (ok) {
         load_tile(G, n, k, i, S0, false, false);
         if (j != i) load_tile(G, n, k, j, S1, false, false);
         load_tile(G, n, i, j, S2, i == j, false);
         __syncthreads();
+        TSTAMP(tload);
         double acc[4][4] = {};
         tile_atb(S0, j != i ? S1 : S0, acc);
 #pragma unroll
@@ -323,6 +413,7 @@ k_chol_dag(double* __restrict__ G, int n, int T, const int4* __restrict__ tasks,
 #pragma unroll
           for (int q = 0; q < 4; ++q) S2[(4 * ty + p) * kTS + tx + 16 * q] -= acc[p][q];
         __syncthreads();
+        TSTAMP(tcomp);
         store_tile(G, n, i, j, S2, i == j);
       }
       __syncthreads();
@@ -334,9 +425,12 @@ k_chol_dag(double* __restrict__ G, int n, int T, const int4* __restrict__ tasks,
     if (trace && tid == 0) {
       unsigned long long t1;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-      trace[3 * t] = t0;
-      trace[3 * t + 1] = t1;
-      trace[3 * t + 2] = blockIdx.x;
+      trace[6 * t] = t0;
+      trace[6 * t + 1] = tready;
+      trace[6 * t + 2] = tload;
+      trace[6 * t + 3] = tcomp;
+      trace[6 * t + 4] = t1;
+      trace[6 * t + 5] = blockIdx.x;
     }
   }
 }
@@ -346,17 +440,22 @@ static const std::vector<int4>& task_list(int T) {
   static int cached_T = -1;
   static std::vector<int4> v;
   if (cached_T == T) return v;
+  // DIAG(k) = TRSM(k, k+1) + UPDATE(k, k+1, k+1) + POTRF(k+1) (kernel comment).  Every
+  // task's inputs come from tasks earlier in the list, so in-order fetching cannot deadlock.
   v.clear();
   v.push_back(make_int4(T_POTRF, 0, 0, 0));
-  for (int j = 1; j < T; ++j) v.push_back(make_int4(T_TRSM, 0, 0, j));
-  for (int k = 0; k < T; ++k) {
-    if (k + 1 < T) {
-      for (int j = k + 1; j < T; ++j) v.push_back(make_int4(T_UPDATE, k, k + 1, j));   // row k+1 of step k
-      v.push_back(make_int4(T_POTRF, k + 1, 0, 0));
-      for (int j = k + 2; j < T; ++j) v.push_back(make_int4(T_TRSM, k + 1, 0, j));
+  if (T > 1) v.push_back(make_int4(T_DIAG, 0, 0, 1));
+  for (int j = 2; j < T; ++j) v.push_back(make_int4(T_TRSM, 0, 0, j));
+  for (int k = 0; k + 1 < T; ++k) {
+    for (int j = k + 2; j < T; ++j) v.push_back(make_int4(T_UPDATE, k, k + 1, j));     // row k+1 of step k
+    if (k + 2 < T) {
+      v.push_back(make_int4(T_UPDATE, k, k + 2, k + 2));                               // DIAG(k+1) needs it
+      v.push_back(make_int4(T_DIAG, k + 1, 0, k + 2));
+      for (int j = k + 3; j < T; ++j) v.push_back(make_int4(T_TRSM, k + 1, 0, j));
     }
     for (int i = k + 2; i < T; ++i)
-      for (int j = i; j < T; ++j) v.push_back(make_int4(T_UPDATE, k, i, j));           // rest of step k
+      for (int j = i; j < T; ++j)
+        if (!(i == k + 2 && j == k + 2)) v.push_back(make_int4(T_UPDATE, k, i, j));   // rest of step k
   }
   cached_T = T;
   return v;
@@ -395,22 +494,24 @@ int launch_cholesky(double* G, int n, int* pivot, void* ws, size_t ws_bytes, cud
   int grid = num_sms();
   if (grid > ntasks) grid = ntasks;
   // TLS_CHOL_TRACE=<path>: per-task start/end timestamps (globaltimer ns) and CTA, written
-  // after the kernel as text lines "type k i j start end cta" (diagnostics only)
+  // after the kernel as text lines "type k i j start ready loaded computed end cta"
+  // (diagnostics only)
   static unsigned long long* trace = nullptr;
   const char* tpath = getenv("TLS_CHOL_TRACE");
-  if (tpath && !trace) TLS_CUDA_TRY(cudaMalloc(&trace, 3 * sizeof(unsigned long long) * 200000));
+  if (tpath && !trace) TLS_CUDA_TRY(cudaMalloc(&trace, 6 * sizeof(unsigned long long) * 200000));
   unsigned long long* tr = tpath ? trace : nullptr;
   void* args[] = {&G, (void*)&n, (void*)&T, &tasks, &ntasks, &xinv, &potrf_done, &trsm_done, &upd_done, &ctl, &pivot, &tr};
   TLS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_chol_dag, dim3(grid), dim3(kCholThreads), args, smem, st));
   if (launches) *launches += 1;
   if (tr) {
-    std::vector<unsigned long long> h(3 * (size_t)ntasks);
+    std::vector<unsigned long long> h(6 * (size_t)ntasks);
     TLS_CUDA_TRY(cudaMemcpyAsync(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost, st));
     TLS_CUDA_TRY(cudaStreamSynchronize(st));
     FILE* f = fopen(tpath, "w");
     if (f) {
       for (int t = 0; t < ntasks; ++t)
-        fprintf(f, "%d %d %d %d %llu %llu %llu\n", tl[t].x, tl[t].y, tl[t].z, tl[t].w, h[3 * t], h[3 * t + 1], h[3 * t + 2]);
+        fprintf(f, "%d %d %d %d %llu %llu %llu %llu %llu %llu\n", tl[t].x, tl[t].y, tl[t].z, tl[t].w, h[6 * t],
+                h[6 * t + 1], h[6 * t + 2], h[6 * t + 3], h[6 * t + 4], h[6 * t + 5]);
       fclose(f);
     }
   }

@@ -325,6 +325,11 @@ int launch_pass(const DenseView& A, int mode, int nrhs, const double* q, const d
     set_error("dense pass: need n <= %d and even ld >= n", kMaxDenseN);
     return TLS_ERR_UNSUPPORTED;
   }
+  // TLS_PASS_TEAM=1: the team-per-row layout of k_pass32.cu for the fp64 operator (2 RHS)
+  // and residual passes (A/B switch)
+  static const int team = [] { const char* e = getenv("TLS_PASS_TEAM"); return e ? atoi(e) : 0; }();
+  if (team && A.n <= 2048 && (mode == PASS_RESIDUAL || (mode == PASS_OPERATOR && nrhs == 2)))
+    return launch_pass_team(A, mode, q, b, partials, active, st, grid_out);
   const int G = pass_grid(A);
   // partial rows for the fixed-order reduce: one per consumer set (pass_sets_rt of the
   // instantiation launch_pass_cpt picks)

@@ -31,6 +31,9 @@ int p32_ld(int n);
 int launch_round32(const DenseView& A, float* A32, cudaStream_t st);
 int launch_pass32(const DenseView& A, const float* A32, const double* q, double* partials, const int* active,
                   cudaStream_t st, int* grid_out);
+// fp64 operator (2 RHS) / residual passes in k_pass32.cu's team-per-row layout.
+int launch_pass_team(const DenseView& A, int mode, const double* q, const double* b, double* partials,
+                     const int* active, cudaStream_t st, int* grid_out);
 // out[w] = sum_g partials[g][w] (max for w < nmax), fixed order.
 int launch_reduce(const double* partials, int G, int W, int nmax, double* out, const int* active,
                   cudaStream_t st);

@@ -12,10 +12,10 @@ for m, n in ((1 << 20, 1024), (1 << 16, 2048), (1 << 19, 512)):
         tlsrqi.tls_pass(M, args[0], args[1], args[2], ws=ws)
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(10):
+        for _ in range(30):
             tlsrqi.tls_pass(M, args[0], args[1], args[2], ws=ws)
         e1.record(); torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / 10
-        print(f"m={m} n={n} {name:5s}: {ms:.3f} ms  {8 * m * n / ms / 1e9:7.1f} GB/s (incl. reduce + copy-out)", flush=True)
+        ms = e0.elapsed_time(e1) / 30
+        print(f"m={m} n={n} {name:5s}: {ms:.3f} ms  {8 * m * n / ms / 1e9:7.2f} TB/s (incl. reduce + copy-out)", flush=True)
     del A, M, ws
     torch.cuda.empty_cache()
