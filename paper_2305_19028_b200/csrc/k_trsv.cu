@@ -547,6 +547,7 @@ __global__ void __launch_bounds__(kTT) k_rqi_eval(int n, const double* __restric
 // z = x + omega_a (l.248); beta = (z^T f - g)/(z^T x + 1) (l.250); x' = z + beta omega_b (l.254).
 __global__ void __launch_bounds__(kTT) k_rqi_update(int n, PcgVecs v, const PcgState* __restrict__ S,
                                                      double* __restrict__ x, double* __restrict__ x_prev) {
+  if (S->brk[0] | S->brk[1]) return;   // PCG breakdown: the host returns x_k (read with the next state)
   __shared__ double red[32];
   const int tid = threadIdx.x;
   double zf = 0.0, zx = 0.0;

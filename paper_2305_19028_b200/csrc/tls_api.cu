@@ -342,6 +342,11 @@ __global__ void k_recip(const double* __restrict__ d, double* __restrict__ dinv,
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dinv[i] = 1.0 / d[i];
 }
 
+__global__ void k_set_state(PcgState* S, int set_sigma, double sigma2, double tol2) {
+  if (set_sigma) S->sigma2 = sigma2;
+  S->tol2 = tol2;
+}
+
 __global__ void k_copy(const double* __restrict__ a, double* __restrict__ b, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
 }
@@ -697,38 +702,35 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
     TLS_TRY(launch_cholesky(w.G, n, &w.flags[2], w.gram_ws, w.gram_ws_doubles * 8, cx.st, &cx.launches));
   }
   tr.mark("cholesky");
+  // R~ is packed before the host looks at any flag: one synchronisation per factorization
+  // (flags: [0] zero column, [1] A^ out of u_f range, [2] Cholesky pivot, [3] R~ out of range)
+  tls_precond_t h = nullptr;
+  TLS_TRY(alloc_precond(n, u_f, &h));
+  tr.mark("alloc");
+  k_fill_scaling<<<(h->dev.npad + 255) / 256, 256, 0, cx.st>>>(h->dev.d, h->dev.dinv, d, dinv, n, h->dev.npad);
+  TLS_CUDA_TRY(cudaMemcpyAsync(h->dev.normA2, normA2, sizeof(double), cudaMemcpyDeviceToDevice, cx.st));
+  int rc = launch_pack_R(w.G, n, 0, h->dev, &w.flags[3], cx.st, &cx.launches);
+  cx.launches += 1;  // k_fill_scaling
+  if (rc) { tls_precond_destroy(h); return rc; }
+  tr.mark("pack");
   int hflags[8];
   double hnorm = 0.0;
   TLS_CUDA_TRY(cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, cx.st));
   TLS_CUDA_TRY(cudaMemcpyAsync(&hnorm, normA2, sizeof(double), cudaMemcpyDeviceToHost, cx.st));
   TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+  tr.mark("sync");
   if (info) { info->passes = cx.passes; info->launches = cx.launches; }
-  if (hflags[0]) { set_error("A has a zero or non-finite column (rank deficient)"); return TLS_ERR_ARG; }
-  if (hflags[1]) { if (info) info->status = TLS_RANGE; return TLS_RANGE; }
-  if (hflags[2]) {
-    if (info) { info->status = TLS_CHOL_BREAKDOWN; info->chol_pivot = hflags[2]; }
-    return TLS_CHOL_BREAKDOWN;
-  }
-  tr.mark("sync1");
-  tls_precond_t h = nullptr;
-  TLS_TRY(alloc_precond(n, u_f, &h));
-  tr.mark("alloc");
-  h->normA2_host = hnorm;
-  k_fill_scaling<<<(h->dev.npad + 255) / 256, 256, 0, cx.st>>>(h->dev.d, h->dev.dinv, d, dinv, n, h->dev.npad);
-  TLS_CUDA_TRY(cudaMemcpyAsync(h->dev.normA2, normA2, sizeof(double), cudaMemcpyDeviceToDevice, cx.st));
-  int rc = launch_pack_R(w.G, n, 0, h->dev, &w.flags[1], cx.st, &cx.launches);
-  cx.launches += 1;  // k_fill_scaling
-  if (rc) { tls_precond_destroy(h); return rc; }
-  tr.mark("pack");
-  TLS_CUDA_TRY(cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, cx.st));
-  TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
-  tr.mark("sync2");
-  if (info) { info->passes = cx.passes; info->launches = cx.launches; }
-  if (hflags[1]) {
+  int st = 0;
+  if (hflags[0]) { set_error("A has a zero or non-finite column (rank deficient)"); st = TLS_ERR_ARG; }
+  else if (hflags[1]) st = TLS_RANGE;
+  else if (hflags[2]) { st = TLS_CHOL_BREAKDOWN; if (info) info->chol_pivot = hflags[2]; }
+  else if (hflags[3]) st = TLS_RANGE;
+  if (st) {
     tls_precond_destroy(h);
-    if (info) info->status = TLS_RANGE;
-    return TLS_RANGE;
+    if (info && st > 0) info->status = st;
+    return st;
   }
+  h->normA2_host = hnorm;
   *R_out = h;
   return 0;
 }
@@ -851,14 +853,12 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   const double tol_in = o.tol_inner > 0 ? o.tol_inner : tol;
   PcgState hS;
 
-  auto set_state_scalars = [&](double sigma2, double tol2) -> int {
-    // host -> device: sigma^2 for PCG and the early-exit threshold (small pageable copies)
-    static thread_local double buf[2];
-    buf[0] = sigma2;
-    buf[1] = tol2;
-    TLS_CUDA_TRY(cudaMemcpyAsync(&w.S->sigma2, &buf[0], 8, cudaMemcpyHostToDevice, cx.st));
-    TLS_CUDA_TRY(cudaMemcpyAsync(&w.S->tol2, &buf[1], 8, cudaMemcpyHostToDevice, cx.st));
-    TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+  // sigma^2 (bootstrap only: the RQI steps take k_rqi_eval's device value) and the early-exit
+  // threshold, written by a one-thread kernel: no host synchronisation
+  auto set_state_scalars = [&](bool set_sigma, double sigma2, double tol2) -> int {
+    k_set_state<<<1, 1, 0, cx.st>>>(w.S, set_sigma ? 1 : 0, sigma2, tol2);
+    cx.launches += 1;
+    TLS_LAUNCH_CHECK();
     return 0;
   };
   auto read_state = [&]() -> int {
@@ -901,23 +901,21 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   TLS_CUDA_TRY(cudaMemsetAsync(w.vec.rhs, 0, 2 * (size_t)n * 8, cx.st));
   // setup (a1): h = A^T b, b^T b from the residual pass at x = 0
   TLS_TRY(run_pass(cx, A, PASS_RESIDUAL, 1, w.zero, b, w, nullptr));
-  double bb = 0.0;
-  TLS_CUDA_TRY(cudaMemcpyAsync(&bb, w.passout + n, 8, cudaMemcpyDeviceToHost, cx.st));
+  // b^T b stays on the device (read with the first RQI state) and A^T b becomes the CGLS RHS
+  TLS_CUDA_TRY(cudaMemcpyAsync(&w.S->bb, w.passout + n, 8, cudaMemcpyDeviceToDevice, cx.st));
   k_copy<<<(n + 255) / 256, 256, 0, cx.st>>>(w.passout, w.vec.rhs, n);
   cx.launches += 1;
   tr.mark("setup");
   // a4: bootstrap x_0 = x_LS (R5)
   int boot_iters = 0;
   if (o.boot == 0) {
-    TLS_TRY(set_state_scalars(0.0, o.boot_tol * o.boot_tol));
+    TLS_TRY(set_state_scalars(true, 0.0, o.boot_tol * o.boot_tol));
     {
       ProfScope ps(TLS_PROF_PCG_INIT, cx.st);
       TLS_TRY(launch_pcg_init(pc, 1, w.vec, w.S, cx.st));
     }
     cx.launches += 1;
-    TLS_TRY(pcg_loop(1, o.boot_max, 0, false));
-    TLS_TRY(read_state());
-    boot_iters = hS.count[0];
+    TLS_TRY(pcg_loop(1, o.boot_max, 0, false));   // its count is read with the first RQI state
     k_copy<<<(n + 255) / 256, 256, 0, cx.st>>>(w.vec.omega, w.x0, n);
   } else {
     k_copy<<<(n + 255) / 256, 256, 0, cx.st>>>(w.vec.rhs, w.x0, n);
@@ -930,14 +928,17 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   TLS_TRY(run_pass(cx, A, PASS_RESIDUAL, 1, w.x0, b, w, nullptr));     // r_0 (l.227)
   TLS_TRY(launch_boot_x1(pc, w.passout, w.x0, w.x, cx.st));              // l.229-235
   cx.launches += 1;
-  TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
-  const double normAb2 = R->normA2_host + bb;
+  TLS_TRY(set_state_scalars(false, 0.0, tol_in * tol_in));
+  double normAb2 = NAN;
 
   std::vector<double> s2tr, psitr;
   std::vector<int> pcgc;
   int status = TLS_OK, term = TLS_TERM_NONE, k = 1, crossed = 0, use_prev = 0;
   double psi_prev = 0.0, sig2_prev = NAN, sig2_ret = NAN;
   int bk = -1, brhs = -1, bj = -1;
+  // ONE host synchronisation per RQI step: the state read after the residual pass also
+  // returns the previous step's PCG counts and breakdown flags (k_rqi_update is a no-op
+  // after a breakdown, so x is still x_{k-1}; the residual evaluation at it is discarded)
   for (;; ++k) {
     // a5: residual pass, sigma_k^2, f_k, g_k, psi_k (l.238-245, l.262)
     TLS_TRY(run_pass(cx, A, PASS_RESIDUAL, 1, w.x, b, w, nullptr));
@@ -946,6 +947,23 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
     tr.mark("resid+eval");
     TLS_TRY(read_state());
     tr.mark("read_state");
+    if (k == 1) {
+      if (o.boot == 0) boot_iters = hS.count[0];
+      normAb2 = R->normA2_host + hS.bb;
+    } else {
+      pcgc.push_back(hS.count[0]);
+      pcgc.push_back(hS.count[1]);
+      if (hS.brk[0] || hS.brk[1]) {                                // R3, R18 (step k - 1)
+        status = TLS_PCG_BREAKDOWN;
+        term = TLS_TERM_BREAKDOWN;
+        --k;
+        bk = k;
+        brhs = hS.brk[0] ? 0 : 1;
+        bj = hS.brk_j[brhs];
+        sig2_ret = sig2_prev;
+        break;
+      }
+    }
     const double sig2 = hS.sigma2, psi = hS.psi;
     s2tr.push_back(sig2);
     psitr.push_back(psi);
@@ -967,7 +985,6 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
     if (k > o.max_outer) { status = TLS_MAX_OUTER; term = TLS_TERM_MAX_OUTER; sig2_ret = sig2; break; }
     // a6-a8: the two PCGTLS solves, batched (l.246, l.252)
     const int budget = o.budget_rule == 0 ? k + 1 : 400;
-    TLS_TRY(set_state_scalars(sig2, tol_in * tol_in));
     {
       ProfScope ps(TLS_PROF_PCG_INIT, cx.st);
       TLS_TRY(launch_pcg_init(pc, 2, w.vec, w.S, cx.st));
@@ -976,19 +993,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
     tr.mark("pcg_init");
     TLS_TRY(pcg_loop(2, budget, o.op_variant, up32));
     tr.mark("pcg_loop");
-    TLS_TRY(read_state());
-    pcgc.push_back(hS.count[0]);
-    pcgc.push_back(hS.count[1]);
-    if (hS.brk[0] || hS.brk[1]) {                                  // R3, R18
-      status = TLS_PCG_BREAKDOWN;
-      term = TLS_TERM_BREAKDOWN;
-      bk = k;
-      brhs = hS.brk[0] ? 0 : 1;
-      bj = hS.brk_j[brhs];
-      sig2_ret = sig2;
-      break;
-    }
-    // a9: z, beta_k, x_{k+1} (l.248-255)
+    // a9: z, beta_k, x_{k+1} (l.248-255); skipped on the device after a PCG breakdown
     TLS_TRY(launch_rqi_update(pc, w.vec, w.S, w.x, w.x_prev, cx.st));
     cx.launches += 1;
     psi_prev = psi;

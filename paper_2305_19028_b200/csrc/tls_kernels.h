@@ -114,6 +114,7 @@ struct PcgState {
   double sigma2, g, psi, xx, tol2;
   int active[2], count[2], brk[2], brk_j[2];
   int iter[2];    // iteration index j of the next step, per RHS
+  double bb;      // b^T b of the local rows (all-reduced), from the setup pass
 };
 struct PcgVecs {  // device, each [2][npad]
   double *omega, *s, *p, *q, *rhs;
