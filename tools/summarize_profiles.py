@@ -61,7 +61,12 @@ KEYS = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
 for rep, dst, title in (("k_pass_full.ncu-rep", f"{tag}_ncu_k_pass_op2_full.txt",
                          "ncu --set full -k regex:k_pass -s 2 -c 1 python tools/prof_pass.py (2^20 x 1024, 2 RHS)"),
                         ("pcg_step.ncu-rep", f"{tag}_ncu_k_pcg_step.txt",
-                         "ncu --set full -k regex:k_pcg_step -s 40 -c 1 (bench cfg4w, n=1024 fp16, 8-CTA cluster per RHS)")):
+                         "ncu --set full -k regex:k_pcg_step -s 40 -c 1 (bench cfg4w, n=1024 fp16, 8-CTA cluster per RHS)"),
+                        ("k_pass32_full.ncu-rep", f"{tag}_ncu_k_pass32_full.txt",
+                         "ncu --set full -k regex:k_pass_team -s 2 -c 1 python tools/time_pass32.py (u_p = fp32 operator "
+                         "pass, 2^20 x 1024 fp32 copy of A, 2 RHS; algorithmic 4.295 GB)"),
+                        ("chol_full.ncu-rep", f"{tag}_ncu_k_chol_dag.txt",
+                         "ncu --set full -k regex:k_chol_dag -s 1 -c 1 python tools/time_chol.py (tile-DAG Cholesky, n = 1024)")):
     path = os.path.join(G, rep)
     if not os.path.exists(path):
         continue
