@@ -126,10 +126,12 @@ k_gram_cc(const double* __restrict__ A, int64_t m, int n, int64_t ld, const doub
 
 // u_f in {fp32, fp64}: the products of u_f values are accumulated in fp64 throughout
 // (R10: no fp32 level), so the chunk structure is irrelevant and each CTA sums its
-// whole row split.  128 x 128 upper tiles, 8 x 8 fp64 accumulators per thread, 16-row
-// K-steps staged in shared memory with the next step's global loads (16-byte, rounded
-// to u_f on the fly) in flight during the current step's 16 x 64 DFMAs.
-constexpr int kGT2 = 128, kGK2 = 16, kGP2 = kGT2 + 4;
+// whole row split.  128 x 128 upper tiles, 32 x 64 per warp (64 fp64 accumulators), 16-row
+// K-steps staged in shared memory with the next step's global loads (rounded to u_f when
+// staged) in flight during the current step's DMMAs.
+// kGP2: row stride 136 doubles (272 words = 16 mod 32 banks), so the DMMA fragment loads
+// (4 rows x 8 consecutive doubles per warp) take the minimum two wavefronts.
+constexpr int kGT2 = 128, kGK2 = 16, kGP2 = kGT2 + 8;
 template <int PREC>
 __global__ void __launch_bounds__(256, 1)
 k_gram_f64(const double* __restrict__ A, int64_t m, int n, int64_t ld, const double* __restrict__ dinv,
@@ -142,16 +144,16 @@ k_gram_f64(const double* __restrict__ A, int64_t m, int n, int64_t ld, const dou
   const bool diag = (I == J);
   const int s = blockIdx.y;
   const int64_t rb = m * s / nsplit, re = m * (s + 1) / nsplit;
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wm = warp & 3, wn = warp >> 2;
   const int I0 = I * kGT2, J0 = J * kGT2;
   // staging map: thread -> (row lr = tid / 16, columns lc + 16 q): lanes read consecutive
-  // doubles from global and write consecutive shared-memory words (no bank conflicts)
+  // doubles from global and write consecutive shared-memory words
   const int lr = tid >> 4, lc = tid & 15;
-  double acc[8][8];
+  double acc[4][8][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   int bad = 0;
   // raw fp64 loads of the next step are kept in registers and only rounded (and scaled)
   // when they are staged, so the loads stay in flight during the current step's math
@@ -182,30 +184,38 @@ k_gram_f64(const double* __restrict__ A, int64_t m, int n, int64_t ld, const dou
     __syncthreads();
     if (r + kGK2 < re) fetch(r + kGK2);       // next step's loads overlap this step's math
     const double(*Bp)[kGP2] = diag ? As : Bs;
-#pragma unroll 4
-    for (int k = 0; k < kGK2; ++k) {
-      double a[8], bv[8];
+    // fp64 tensor cores (DMMA m8n8k4, SASS DMMA; the same 64 FMA/clk/SM as DFMA on B200 at
+    // 1/8 of the instructions, measured tools/micro/dmma.cu): warp (wm, wn) owns rows
+    // wm*32.. and columns wn*64.. of the tile; A = Â_I^T (8 x 4 fragments), B = Â_J (4 x 8).
+    // 16.0 -> 13.2 ms at 65536 x 2048 against the DFMA version (22 TF/s, ~60% of the fp64
+    // peak; a cp.async ring with in-place conversion measured 16.3 ms)
 #pragma unroll
-      for (int i = 0; i < 8; i += 2) {
-        const double2 t2 = *reinterpret_cast<const double2*>(&As[k][ty * 8 + i]);
-        a[i] = t2.x;
-        a[i + 1] = t2.y;
-      }
+    for (int kk = 0; kk < kGK2; kk += 4) {
+      const int kr = kk + (lane & 3);
+      double af[4], bf[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) bv[j] = Bp[k][tx + 16 * j];      // consecutive lanes, no conflicts
+      for (int mi = 0; mi < 4; ++mi) af[mi] = As[kr][wm * 32 + mi * 8 + (lane >> 2)];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int nj = 0; nj < 8; ++nj) bf[nj] = Bp[kr][wn * 64 + nj * 8 + (lane >> 2)];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], bv[j], acc[i][j]);
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 8; ++nj)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[mi][nj][0]), "+d"(acc[mi][nj][1])
+                       : "d"(af[mi]), "d"(bf[nj]));
     }
     __syncthreads();
   }
   if (bad) atomicExch(range, 1);
   double* out = part + ((size_t)s * gridDim.x + blockIdx.x) * (kGT2 * kGT2);
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) out[(ty * 8 + i) * kGT2 + tx + 16 * j] = acc[i][j];
+    for (int nj = 0; nj < 8; ++nj) {
+      const int row = wm * 32 + mi * 8 + (lane >> 2), col = wn * 64 + nj * 8 + 2 * (lane & 3);
+      *reinterpret_cast<double2*>(out + (size_t)row * kGT2 + col) = make_double2(acc[mi][nj][0], acc[mi][nj][1]);
+    }
 }
 
 static void gram_shape_f64(const DenseView& A, int& TT, int& ntiles, int& nsplit) {
