@@ -438,6 +438,41 @@ def main():
                               "achieved_gbs": 4.0 * (hi - lo) * n / (avg32 * 1e-3) / 1e9,
                               "frac": 4.0 * (hi - lo) * n / (avg32 * 1e-3) / 1e9 / peak}}
 
+    # the explicit-inverse preconditioner application (R24; the default when sharded over
+    # several ranks): same factorization, PCG steps on W = R~^{-1} over every SM
+    winv = None
+    if not args.no_control:
+        ow = tlsrqi.tls_rqi_opts_default(precond_apply=2)
+
+        def stepw():
+            rc, R, fi = tlsrqi.tls_factor_precond(M, u_f, comm=comm, stream=stream, ws=ws)
+            rc, _, sgw, inf = tlsrqi.tls_rqi_pcgtls(M, b_loc, R, comm=comm, stream=stream, ws=ws, x_out=x, opts=ow)
+            return inf, sgw
+        stepw()
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+        tlsrqi.tls_profile_enable(True)
+        k0 = torch.cuda.Event(enable_timing=True)
+        k1 = torch.cuda.Event(enable_timing=True)
+        k0.record(stream)
+        for _ in range(args.steps):
+            infw, sgw = stepw()
+        k1.record(stream)
+        torch.cuda.synchronize()
+        pw = tlsrqi.tls_profile_read()
+        tlsrqi.tls_profile_enable(False)
+        tw = k0.elapsed_time(k1) / args.steps
+        if world > 1:
+            t = torch.tensor([tw], dtype=torch.float64, device="cuda")
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            tw = float(t.item())
+        winv = {"precond_apply": "explicit inverse (R24)", "tts_s": tw / 1e3, "status": infw["status_name"],
+                "rqi_iters": infw["rqi_iters"], "boot_iters": infw["boot_iters"], "pcg_iters": infw["pcg_iters"],
+                "sigma_rel_diff": abs(sgw - sig) / sig, "speedup_vs_substitution": tts / (tw / 1e3),
+                "pcg_step_us": 1e3 * pw["pcg_step"]["ms"] / max(1, pw["pcg_step"]["count"]),
+                "pcg_step_us_substitution": 1e3 * prof["pcg_step"]["ms"] / max(1, prof["pcg_step"]["count"])}
+
     cpu = None
     if keep_host:
         import numpy as np
@@ -476,6 +511,7 @@ def main():
             "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
             "uniform_fp64_control": control,
             "paper_precision_up_fp32": up32,
+            "precond_inverse": winv,
         }
         print(json.dumps(line), flush=True)
     if comm:

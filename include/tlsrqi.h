@@ -112,7 +112,12 @@ typedef struct {
                               on an fp32 copy of A made by the solve and kept in the
                              precond handle (4 m_local ld32 bytes, dense A, n <= 2048, op_variant 0).
                              The bootstrap, the residual passes and all n-vector work stay fp64. */
-  int32_t reserved[4];
+  int32_t precond_apply;  /* how q = P^{-1} p and w = P^{-T} y are applied (R24): 1 = forward/back
+                             substitution with the stored R~ ("Forward/Backward Subs",
+                             l.427); 2 = products with W = R~^{-1} formed once per handle in fp64 (npad^2
+                             doubles owned by the handle); 0 = auto [0]: 2 when comm has several ranks,
+                             else 1 */
+  int32_t reserved[3];
 } tls_rqi_opts_t;
 
 /* Results.  pcg_iters (2*max_outer ints), sigma2_trace, psi_trace
@@ -209,7 +214,9 @@ TLS_API int tls_pass(const tls_matrix_t* A, int32_t mode, int32_t nrhs, const do
 TLS_API int tls_pass_fp32(const tls_matrix_t* A, tls_precond_t R, const double* q_dev, double* v_dev,
                           double* s_dev, void* stream, void* ws_dev, size_t ws_bytes);
 /* a6: Y_dev (nrhs x n) <- P^{-1} Y (trans = 0: D^{-1} R~^{-1} Y, back substitution)
- * or P^{-T} Y (trans = 1: R~^{-T} D^{-1} Y, forward substitution), nrhs in {1,2}. */
+ * or P^{-T} Y (trans = 1: R~^{-T} D^{-1} Y, forward substitution), nrhs in {1,2}.
+ * trans | 2: the same maps through the explicit inverse W = R~^{-1} (R24; W is formed
+ * once and kept by the handle). */
 TLS_API int tls_precond_apply(const tls_precond_t R, int32_t trans, int32_t nrhs, double* Y_dev,
                       void* stream);
 /* fl_uf rounding of n fp64 values (reading R4), for bit-exact parity tests. */

@@ -156,6 +156,7 @@ class Precond:
     chol_pivot: int = 0  # 1-based index of the first failed pivot (CHOL_BREAKDOWN)
     G: Optional[np.ndarray] = None
     R: Optional[np.ndarray] = None
+    W: Optional[np.ndarray] = None   # explicit inverse of R~ when the solve applies it (R24)
 
 
 def factor_precond(A, u_f: str, K_t: int = 64, keep: bool = False) -> Precond:
@@ -179,14 +180,26 @@ def factor_precond(A, u_f: str, K_t: int = 64, keep: bool = False) -> Precond:
     return Precond(Rt, d, u_f, normA2, OK, 0, G if keep else None, R if keep else None)
 
 
+def with_inverse(pc: Precond) -> Precond:
+    """The same preconditioner applied through W = R~^{-1}, formed once in fp64 by
+    triangular solves against the identity (reading R24: tls_rqi_opts_t.precond_apply = 2)."""
+    W = scipy.linalg.solve_triangular(pc.Rt, np.eye(pc.Rt.shape[0]), lower=False)
+    return dataclasses.replace(pc, W=np.triu(W))
+
+
 def apply_Pinv(pc: Precond, y: np.ndarray) -> np.ndarray:
     """P^{-1} y = D^{-1} (R~^{-1} y): back substitution (PAPER.md Alg. 3 l.193;
-    Table 1 "Forward/Backward Subs", l.427)."""
+    Table 1 "Forward/Backward Subs", l.427), or D^{-1} (W y) with the explicit inverse (R24)."""
+    if pc.W is not None:
+        return (pc.W @ y) / pc.d
     return scipy.linalg.solve_triangular(pc.Rt, y, lower=False) / pc.d
 
 
 def apply_PinvT(pc: Precond, y: np.ndarray) -> np.ndarray:
-    """P^{-T} y = R~^{-T} (D^{-1} y): forward substitution (Alg. 3 l.191, l.197)."""
+    """P^{-T} y = R~^{-T} (D^{-1} y): forward substitution (Alg. 3 l.191, l.197), or
+    W^T (D^{-1} y) with the explicit inverse (R24)."""
+    if pc.W is not None:
+        return pc.W.T @ (y / pc.d)
     return scipy.linalg.solve_triangular(pc.Rt, y / pc.d, trans="T", lower=False)
 
 
@@ -288,6 +301,7 @@ class RqiOptions:
     breakdown_rule: int = 0    # 0: delta <= 0 stops (spec); 1: delta == 0 only (paper)
     gram_chunk: int = 64
     u_p: str = "fp64"          # operator precision of the RQI's inner solves (R23): "fp64" | "fp32"
+    precond_apply: int = 0     # R24: 1 substitution, 2 explicit inverse, 0 auto (= 1 in this one-process oracle)
 
 
 @dataclasses.dataclass
@@ -342,6 +356,8 @@ def rqi_pcgtls_mp(A, b: np.ndarray, pc: Precond, tol: float = 1e-14,
     A32 = A.astype(np.float32) if (o.u_p == "fp32" and variant == "A") else None   # fl32(A), RNE
     if pc.status != OK:
         return RqiResult(np.zeros(n), math.nan, pc.status, T_BREAKDOWN, 0, 0, [], [], [])
+    if o.precond_apply == 2 and pc.W is None:
+        pc = with_inverse(pc)
     passes = 0
     normAb2 = pc.normA2 + float(b @ b)
     h = rmatvec(A, b)                          # A^T b (setup pass)

@@ -18,6 +18,8 @@
 // fused into k_pcg_step around the forward solve, followed by the next
 // iteration's back solve; the RQI updates of Alg. 4 (l.238-255) live in
 // k_rqi_eval / k_rqi_update / k_boot_x1.  All reductions are fixed-order.
+#include <cooperative_groups.h>
+
 #include "tls_common.cuh"
 #include "tls_kernels.h"
 
@@ -293,6 +295,442 @@ __device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- explicit-inverse apply (R24)
+__device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+
+// y <- W^T y (BACK = false, the forward solve R~^T x = y) or W y (BACK = true, the back
+// solve R~ x = y) with W = R~^{-1} formed once in fp64 (k_trtri; npad x npad row-major,
+// zero below the diagonal).  A cluster-wide GEMV: CTA c of the cluster computes the 32-row
+// (32-column) chunks q = c, c + C, ... of the result, coalesced over W's rows, and stores
+// them into every CTA's staging buffer through DSMEM; no block-by-block dependency chain.
+// Same contract as trsv_ws: every CTA calls it with the same y and gets the same result.
+template <bool BACK>
+__device__ void wgemv(const double* __restrict__ W, int npad, TrsvSm& sm) {
+  const int C = (int)cluster_nctarank(), cr = (int)cluster_ctarank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NB = npad >> 5;
+  double* out = sm.D;                 // [npad] result staging (the TRSV slots are unused here)
+  double* part = sm.D + 2048;         // [kTW][32] column partials
+  const uint32_t out_base = smem_u32(out);
+  cluster_sync_all();                 // no CTA is still reading a previous result from `out`
+  for (int q = cr; q < NB; q += C) {
+    if (BACK) {
+      // rows 32q + warp + kTW k: x_i = sum_{j >= 32q} W_ij y_j (W_ij = 0 for j < i)
+      for (int k = 0; k < 32 / kTW; ++k) {
+        const int i = 32 * q + warp + kTW * k;
+        const double* Wi = W + (size_t)i * npad;
+        double a0 = 0.0, a1 = 0.0;
+        int j = 32 * q + lane;
+        for (; j + 32 < npad; j += 64) {
+          a0 = fma(__ldg(Wi + j), sm.y[j], a0);
+          a1 = fma(__ldg(Wi + j + 32), sm.y[j + 32], a1);
+        }
+        if (j < npad) a0 = fma(__ldg(Wi + j), sm.y[j], a0);
+        const double acc = warp_sum(a0 + a1);
+        if (lane < C) st_cluster_f64(mapa_shared(out_base + (uint32_t)i * 8u, (uint32_t)lane), acc);
+      }
+    } else {
+      // columns j = 32q + lane: x_j = sum_{i < 32q + 32} W_ij y_i, rows split over the warps
+      const int j = 32 * q + lane;
+      double a0 = 0.0, a1 = 0.0;
+      int i = warp;
+      for (; i + kTW < 32 * q + 32; i += 2 * kTW) {
+        a0 = fma(__ldg(W + (size_t)i * npad + j), sm.y[i], a0);
+        a1 = fma(__ldg(W + (size_t)(i + kTW) * npad + j), sm.y[i + kTW], a1);
+      }
+      if (i < 32 * q + 32) a0 = fma(__ldg(W + (size_t)i * npad + j), sm.y[i], a0);
+      part[warp * 32 + lane] = a0 + a1;
+      __syncthreads();
+      if (warp == 0) {
+        double acc = 0.0;
+#pragma unroll
+        for (int w = 0; w < kTW; ++w) acc += part[w * 32 + lane];
+        for (int r = 0; r < C; ++r) st_cluster_f64(mapa_shared(out_base + (uint32_t)j * 8u, (uint32_t)r), acc);
+      }
+      __syncthreads();
+    }
+  }
+  cluster_sync_all();                 // every chunk has landed in every CTA
+  for (int i = tid; i < npad; i += blockDim.x) sm.y[i] = out[i];
+  __syncthreads();
+}
+
+// The preconditioner solves of every kernel below: substitution with the stored R~ (the
+// default, a6 as specified) or the explicit inverse when the solve provides one (pc.W).
+template <typename T, bool BACK>
+__device__ __forceinline__ void pre_apply(const PrecondDev& pc, TrsvSm& sm) {
+  if (pc.W != nullptr) wgemv<BACK>(pc.W, pc.npad, sm);
+  else if (BACK) trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, pc.EB, pc.npad, sm);
+  else trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, pc.EF, pc.npad, sm);
+}
+
+// W = R~^{-1} by block columns (R24): W_JJ = R~_JJ^{-1} (the DinvB blocks), then for
+// I = J-1 .. 0: W_IJ = -R~_II^{-1} sum_{K=I+1..J} R~_IK W_KJ.  CTA (J, c) owns 4 columns of
+// block column J and keeps their strip of W in shared memory.  Warp w takes the blocks
+// K = I+1+w, I+1+w+8, ...; lane r multiplies the 32-element segment of row 32I+r of R~_IK
+// (one vector load, the next one in flight) into the strip; the 8 warp partials are summed
+// in fixed order and the 32 x 32 inverse is applied.  W, WT zeroed beforehand; WT = W^T.
+template <typename T>
+__global__ void __launch_bounds__(256) k_trtri(PrecondDev pc, double* __restrict__ W, double* __restrict__ WT) {
+  constexpr int NV = SegTraits<T>::NV;
+  extern __shared__ double wsm[];
+  const int npad = pc.npad;
+  const int J = blockIdx.x >> 3, c0 = (blockIdx.x & 7) * 4;
+  double* Wc = wsm;                          // [npad][4]
+  double* Tp = Wc + (size_t)npad * 4;        // [8][32][4] partials
+  double* Tf = Tp + 8 * 32 * 4;              // [32][4]
+  const int tid = threadIdx.x, w = tid >> 5, r = tid & 31;
+  const T* R = reinterpret_cast<const T*>(pc.Rrow);
+  if (tid < 128) {                           // DinvB[kb][l][i] = (R~_kk^{-1})[i][l]
+    const int rr = tid >> 2, cc = tid & 3;
+    const double v = pc.DinvB[(size_t)J * 1024 + (c0 + cc) * 32 + rr];
+    Wc[(32 * J + rr) * 4 + cc] = v;
+    W[(size_t)(32 * J + rr) * npad + 32 * J + c0 + cc] = v;
+    WT[(size_t)(32 * J + c0 + cc) * npad + 32 * J + rr] = v;
+  }
+  __syncthreads();
+  for (int I = J - 1; I >= 0; --I) {
+    const T* Rr = R + (size_t)(32 * I + r) * npad;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    uint4 cur[NV], nxt[NV];
+    int K = I + 1 + w;
+    if (K <= J) seg_load<T>(Rr + 32 * K, cur);
+    for (; K <= J; K += 8) {
+      if (K + 8 <= J) seg_load<T>(Rr + 32 * (K + 8), nxt);
+      const double* wk = Wc + (size_t)(32 * K) * 4;
+#pragma unroll
+      for (int l = 0; l < 32; ++l) {
+        const double rv = seg_get<T>(cur, l);
+        const double4 wv = *reinterpret_cast<const double4*>(wk + 4 * l);
+        a[0] = fma(rv, wv.x, a[0]);
+        a[1] = fma(rv, wv.y, a[1]);
+        a[2] = fma(rv, wv.z, a[2]);
+        a[3] = fma(rv, wv.w, a[3]);
+      }
+#pragma unroll
+      for (int k = 0; k < NV; ++k) cur[k] = nxt[k];
+    }
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) Tp[(w * 32 + r) * 4 + cc] = a[cc];
+    __syncthreads();
+    if (tid < 128) {
+      const int rr = tid >> 2, cc = tid & 3;
+      double t = 0.0;
+#pragma unroll
+      for (int h = 0; h < 8; ++h) t += Tp[(h * 32 + rr) * 4 + cc];
+      Tf[rr * 4 + cc] = t;
+    }
+    __syncthreads();
+    if (tid < 128) {
+      const int rr = tid >> 2, cc = tid & 3;
+      double s = 0.0;
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) s = fma(pc.DinvB[(size_t)I * 1024 + l * 32 + rr], Tf[l * 4 + cc], s);
+      Wc[(32 * I + rr) * 4 + cc] = -s;
+      W[(size_t)(32 * I + rr) * npad + 32 * J + c0 + cc] = -s;
+      WT[(size_t)(32 * J + c0 + cc) * npad + 32 * I + rr] = -s;
+    }
+    __syncthreads();
+  }
+}
+
+
+// ---------------------------------------------------------------- explicit-inverse PCG (R24)
+// With W = R~^{-1} the two preconditioner solves of a PCG step are products with W^T and W
+// that every SM can share (the substitutions are a dependency chain on one 8-CTA cluster):
+//   k_wgemv_grid  rows of WT (forward) or W (back) against the staged vectors of the active
+//                 right-hand sides, one warp per row, both RHS in the same read of the row;
+//   k_wpcg_*_mid  the n-vector recurrences of Alg. 3 (l.194-201), one CTA per RHS, with the
+//                 same decisions, state updates and fixed-order reductions as k_pcg_step.
+// mode 0: s = p = W^T (D^{-1} rhs), omega = 0 (pcg_init); mode 1: w = W^T y with
+// y = D^{-1}(A^T t - sigma^2 q) (variant 0) or D^{-1} q (variant 1); mode 2: q = D^{-1} W p.
+constexpr int kWG = 256;
+__global__ void __launch_bounds__(kWG) k_wgemv_grid(PrecondDev pc, PcgVecs v, const double* __restrict__ passout,
+                                                   const PcgState* __restrict__ S, int nrhs, int mode, int variant,
+                                                   int all) {
+  extern __shared__ double vin[];       // [2][npad]
+  const int n = pc.n, npad = pc.npad, tid = threadIdx.x, lane = tid & 31;
+  bool act[2];
+  for (int r = 0; r < 2; ++r) act[r] = r < nrhs && (all || S->active[r] != 0);
+  if (!act[0] && !act[1]) return;
+  const double sig2 = S->sigma2;
+  for (int r = 0; r < 2; ++r) {
+    if (!act[r]) continue;
+    const size_t off = (size_t)r * n;
+    for (int j = tid; j < npad; j += kWG) {
+      double x = 0.0;
+      if (j < n) {
+        if (mode == 0) x = v.rhs[off + j] * pc.dinv[j];
+        else if (mode == 1) x = (variant == 0 ? passout[off + j] - sig2 * v.q[off + j] : v.q[off + j]) * pc.dinv[j];
+        else x = v.p[off + j];
+      }
+      vin[(size_t)r * npad + j] = x;
+    }
+  }
+  __syncthreads();
+  const double* M = mode == 2 ? pc.W : pc.WT;
+  const int nw = gridDim.x * (kWG / 32);
+  for (int i = blockIdx.x * (kWG / 32) + (tid >> 5); i < n; i += nw) {
+    const double* Mi = M + (size_t)i * npad;
+    // upper rows (W) from the 32-aligned chunk of the diagonal on; lower rows (WT) up to it
+    const int j0 = mode == 2 ? (i & ~31) : 0, j1 = mode == 2 ? npad : ((i | 31) + 1);
+    double a0 = 0.0, a1 = 0.0;
+    for (int j = j0 + lane; j < j1; j += 32) {
+      const double m = __ldg(Mi + j);
+      if (act[0]) a0 = fma(m, vin[j], a0);
+      if (act[1]) a1 = fma(m, vin[npad + j], a1);
+    }
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    if (lane < 2 && act[lane]) {
+      const double a = lane == 0 ? a0 : a1;
+      const size_t o = (size_t)lane * n + i;
+      if (mode == 0) { v.s[o] = a; v.p[o] = a; v.omega[o] = 0.0; }
+      else if (mode == 1) v.w[o] = a;
+      else v.q[o] = a * pc.dinv[i];
+    }
+  }
+}
+
+// One PCG step on the explicit inverse as ONE cooperative kernel over every SM (R24):
+//   A  w = W^T y, rows of WT spread over the grid               -> grid barrier
+//   B  every CTA forms the same delta, alpha, s', eta', beta, p' (fixed-order sums)
+//                                                                -> grid barrier
+//   C  CTA 0 writes s, p and the state; q = D^{-1} W p' spread over the grid.
+// Same decisions, updates and state as k_pcg_step.
+__global__ void __launch_bounds__(kWG) k_wpcg_step_coop(PrecondDev pc, PcgVecs v, const double* __restrict__ passout,
+                                                       PcgState* __restrict__ S, int nrhs, int rule, int next_q,
+                                                       int variant, int pass_nrhs) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double wsh[];
+  const int n = pc.n, npad = pc.npad, tid = threadIdx.x, lane = tid & 31;
+  double* vin = wsh;                    // [2][npad]: y, later p'
+  double* snb = wsh + 2 * (size_t)npad; // [2][npad]: s'
+  __shared__ double red[32];
+  __shared__ double s_al[2], s_be[2], s_dl[2], s_qq[2], s_eta[2], s_pp[2];
+  __shared__ int s_upd[2], s_cont[2], s_brk[2];
+  bool act[2];
+  for (int r = 0; r < 2; ++r) act[r] = r < nrhs && S->active[r] != 0;
+  if (!act[0] && !act[1]) return;       // uniform over the grid
+  const double sig2 = S->sigma2;
+  // ---- A
+  for (int r = 0; r < 2; ++r) {
+    if (!act[r]) continue;
+    const size_t off = (size_t)r * n;
+    for (int j = tid; j < npad; j += kWG)
+      vin[(size_t)r * npad + j] =
+          j < n ? (variant == 0 ? passout[off + j] - sig2 * v.q[off + j] : v.q[off + j]) * pc.dinv[j] : 0.0;
+  }
+  __syncthreads();
+  const int nw = gridDim.x * (kWG / 32);
+  for (int i = blockIdx.x * (kWG / 32) + (tid >> 5); i < n; i += nw) {
+    const double* Mi = pc.WT + (size_t)i * npad;
+    double a0 = 0.0, a1 = 0.0;
+    for (int j = lane; j <= (i | 31); j += 32) {
+      const double m = __ldg(Mi + j);
+      if (act[0]) a0 = fma(m, vin[j], a0);
+      if (act[1]) a1 = fma(m, vin[npad + j], a1);
+    }
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    if (lane < 2 && act[lane]) v.w[(size_t)lane * n + i] = lane == 0 ? a0 : a1;
+  }
+  grid.sync();
+  // ---- B (redundant in every CTA)
+  for (int r = 0; r < 2; ++r) {
+    if (!act[r]) continue;
+    const size_t off = (size_t)r * n;
+    double e = 0.0;
+    for (int i = tid; i < n; i += kWG) e = fma(v.q[off + i], v.q[off + i], e);
+    const double qq = block_sum(e, red);
+    if (tid == 0) {
+      s_qq[r] = qq;
+      s_upd[r] = 0;
+      s_brk[r] = 0;
+      s_al[r] = 0.0;
+      const double tau = variant == 0 ? passout[(size_t)pass_nrhs * n + r] : S->pp[r];
+      const double delta = tau - sig2 * qq;                     // l.194 (R1)
+      s_dl[r] = delta;
+      if (!isfinite(delta) || delta == 0.0) {                   // loop guard l.192 (R3)
+      } else if (delta < 0.0 && rule == 0) {                    // breakdown (R3)
+        s_brk[r] = 1;
+      } else {
+        s_al[r] = S->eta[r] / delta;                            // l.195
+        s_upd[r] = 1;
+      }
+    }
+    __syncthreads();
+    s_cont[r] = 0;
+    if (!s_upd[r]) continue;
+    const double al = s_al[r];
+    e = 0.0;
+    for (int i = tid; i < n; i += kWG) {
+      const double q = v.q[off + i];
+      if (blockIdx.x == 0) v.omega[off + i] = fma(al, q, v.omega[off + i]);   // l.196 (only CTA 0 reads omega)
+      const double w = variant == 0 ? v.w[off + i] : fma(-sig2, v.w[off + i], v.p[off + i]);   // l.197
+      const double sn = fma(-al, w, v.s[off + i]);             // l.198
+      snb[(size_t)r * npad + i] = sn;
+      e = fma(sn, sn, e);
+    }
+    const double etan = block_sum(e, red);                      // l.199
+    __syncthreads();
+    if (tid == 0) {
+      s_eta[r] = etan;
+      if (!(etan <= S->tol2 * S->eta0[r])) { s_be[r] = etan / S->eta[r]; s_cont[r] = 1; }   // R3; l.200
+    }
+    __syncthreads();
+    e = 0.0;
+    if (s_cont[r]) {
+      const double be = s_be[r];
+      for (int i = tid; i < npad; i += kWG) {
+        const double pn = i < n ? fma(be, v.p[off + i], snb[(size_t)r * npad + i]) : 0.0;   // l.201
+        vin[(size_t)r * npad + i] = pn;
+        e = fma(pn, pn, e);
+      }
+    }
+    const double ppn = block_sum(e, red);
+    if (tid == 0) s_pp[r] = ppn;
+    __syncthreads();
+  }
+  grid.sync();                          // every CTA has read the old q, s, p
+  // ---- C
+  if (blockIdx.x == 0) {
+    for (int r = 0; r < 2; ++r) {
+      if (!act[r]) continue;
+      const size_t off = (size_t)r * n;
+      if (s_upd[r])
+        for (int i = tid; i < n; i += kWG) {
+          v.s[off + i] = snb[(size_t)r * npad + i];
+          if (s_cont[r]) v.p[off + i] = vin[(size_t)r * npad + i];
+        }
+      if (tid == 0) {
+        S->delta_min[r] = fmin(S->delta_min[r], s_dl[r]);
+        S->qq[r] = s_qq[r];
+        if (!s_upd[r]) {
+          S->active[r] = 0;
+          if (s_brk[r]) { S->brk[r] = 1; S->brk_j[r] = S->iter[r]; }
+        } else {
+          S->count[r] += 1;
+          S->iter[r] += 1;
+          if (s_cont[r]) { S->eta[r] = s_eta[r]; S->pp[r] = s_pp[r]; }
+          else S->active[r] = 0;
+        }
+      }
+    }
+  }
+  if (!next_q) return;
+  bool nq[2];
+  for (int r = 0; r < 2; ++r) nq[r] = act[r] && s_cont[r];
+  if (!nq[0] && !nq[1]) return;
+  for (int i = blockIdx.x * (kWG / 32) + (tid >> 5); i < n; i += nw) {
+    const double* Mi = pc.W + (size_t)i * npad;
+    double a0 = 0.0, a1 = 0.0;
+    for (int j = (i & ~31) + lane; j < npad; j += 32) {
+      const double m = __ldg(Mi + j);
+      if (nq[0]) a0 = fma(m, vin[j], a0);
+      if (nq[1]) a1 = fma(m, vin[npad + j], a1);
+    }
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    if (lane < 2 && nq[lane]) v.q[(size_t)lane * n + i] = (lane == 0 ? a0 : a1) * pc.dinv[i];
+  }
+}
+
+// pcg_init's recurrence part (k_pcg_init after its forward solve): eta_0, the state.
+__global__ void __launch_bounds__(kTT) k_wpcg_init_mid(PrecondDev pc, int nrhs, PcgVecs v, PcgState* __restrict__ S) {
+  __shared__ double red[32];
+  const int r = blockIdx.x, n = pc.n, tid = threadIdx.x;
+  if (r >= nrhs) {                      // the unused RHS slot of a 1-RHS solve
+    if (tid == 0) {
+      S->active[r] = 0; S->count[r] = 0; S->brk[r] = 0; S->brk_j[r] = -1; S->iter[r] = 0;
+      S->eta[r] = S->eta0[r] = S->qq[r] = S->pp[r] = 0.0;
+      S->delta_min[r] = __longlong_as_double(0x7ff0000000000000ll);
+    }
+    for (int i = tid; i < n; i += kTT) v.q[(size_t)r * n + i] = 0.0;
+    return;
+  }
+  double e = 0.0;
+  for (int i = tid; i < n; i += kTT) e = fma(v.s[(size_t)r * n + i], v.s[(size_t)r * n + i], e);
+  const double eta = block_sum(e, red);
+  if (tid == 0) {
+    S->eta[r] = eta; S->eta0[r] = eta; S->pp[r] = eta;
+    S->delta_min[r] = __longlong_as_double(0x7ff0000000000000ll);
+    S->active[r] = eta > 0.0; S->count[r] = 0; S->brk[r] = 0; S->brk_j[r] = -1; S->iter[r] = 0;
+  }
+}
+
+// k_pcg_step between its two solves (same decisions and updates, R3): delta, alpha, omega,
+// s, eta', beta, p; q^T q of the current q is formed here (fixed order).
+__global__ void __launch_bounds__(kTT) k_wpcg_step_mid(PrecondDev pc, PcgVecs v, const double* __restrict__ passout,
+                                                      PcgState* __restrict__ S, int nrhs, int rule, int variant,
+                                                      int pass_nrhs) {
+  __shared__ double red[32];
+  __shared__ double s_alpha, s_beta;
+  __shared__ int s_upd, s_cont;
+  const int r = blockIdx.x, n = pc.n, tid = threadIdx.x;
+  if (r >= nrhs || S->active[r] == 0) return;
+  const size_t off = (size_t)r * n;
+  const double sig2 = S->sigma2;
+  double e = 0.0;
+  for (int i = tid; i < n; i += kTT) e = fma(v.q[off + i], v.q[off + i], e);
+  const double qq = block_sum(e, red);
+  const int iter0 = S->iter[r], count0 = S->count[r];
+  const double eta_old = S->eta[r], eta0 = S->eta0[r], tol2 = S->tol2;
+  if (tid == 0) {
+    s_upd = 0;
+    s_alpha = 0.0;
+    const double tau = variant == 0 ? passout[(size_t)pass_nrhs * n + r] : S->pp[r];
+    const double delta = tau - sig2 * qq;                       // l.194 (R1)
+    S->delta_min[r] = fmin(S->delta_min[r], delta);
+    S->qq[r] = qq;
+    if (!isfinite(delta) || delta == 0.0) {                     // loop guard l.192 (R3)
+      S->active[r] = 0;
+    } else if (delta < 0.0 && rule == 0) {                      // breakdown (R3)
+      S->active[r] = 0; S->brk[r] = 1; S->brk_j[r] = iter0;
+    } else {
+      s_alpha = eta_old / delta;                                // l.195
+      s_upd = 1;
+    }
+  }
+  __syncthreads();
+  if (!s_upd) return;
+  const double al = s_alpha;
+  e = 0.0;
+  for (int i = tid; i < n; i += kTT) {
+    const double q = v.q[off + i];
+    v.omega[off + i] = fma(al, q, v.omega[off + i]);           // l.196
+    const double w = variant == 0 ? v.w[off + i] : fma(-sig2, v.w[off + i], v.p[off + i]);   // l.197
+    const double sn = fma(-al, w, v.s[off + i]);               // l.198
+    v.s[off + i] = sn;
+    e = fma(sn, sn, e);
+  }
+  const double etan = block_sum(e, red);                        // l.199
+  if (tid == 0) {
+    s_cont = 0;
+    if (!(etan <= tol2 * eta0)) { s_beta = etan / eta_old; s_cont = 1; }   // early exit (R3); l.200
+  }
+  __syncthreads();
+  const bool cont = s_cont;
+  const double be = s_beta;
+  e = 0.0;
+  if (cont)
+    for (int i = tid; i < n; i += kTT) {
+      const double pn = fma(be, v.p[off + i], v.s[off + i]);   // l.201
+      v.p[off + i] = pn;
+      e = fma(pn, pn, e);
+    }
+  const double ppn = block_sum(e, red);
+  if (tid == 0) {
+    S->count[r] = count0 + 1;
+    S->iter[r] = iter0 + 1;
+    if (cont) { S->eta[r] = etan; S->pp[r] = ppn; }
+    else S->active[r] = 0;
+  }
+}
+
 // ---------------------------------------------------------------- plain apply (API / tests)
 // One cluster of kTC CTAs per right-hand side r.  Every CTA of a cluster holds the whole
 // vector and computes the same values; only cluster rank 0 writes global memory.
@@ -317,8 +755,8 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_precond_apply(PrecondDev pc, in
     if (trans) v *= pc.dinv[i];
     sm.y[i] = v;
   }
-  if (trans) trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, pc.EF, npad, sm);
-  else trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, pc.EB, npad, sm);
+  if (trans) pre_apply<T, false>(pc, sm);
+  else pre_apply<T, true>(pc, sm);
   if (rank0)
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       double v = sm.y[i];
@@ -351,7 +789,7 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_init(PrecondDev pc, int nrh
   const size_t off = (size_t)r * n;
   // l.191: s_0 = p_0 = P^{-T} f, eta_0 = ||s_0||^2, omega_0 = 0
   for (int i = tid; i < npad; i += blockDim.x) sm.y[i] = i < n ? v.rhs[off + i] * pc.dinv[i] : 0.0;
-  trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, pc.EF, npad, sm);
+  pre_apply<T, false>(pc, sm);
   double e = 0.0;
   for (int i = tid; i < n; i += blockDim.x) {
     const double s = sm.y[i];
@@ -364,7 +802,7 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_init(PrecondDev pc, int nrh
   }
   const double eta = block_sum(e, sm.red);
   // first q = P^{-1} p (l.193)
-  trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, pc.EB, npad, sm);
+  pre_apply<T, true>(pc, sm);
   e = 0.0;
   for (int i = tid; i < n; i += blockDim.x) {
     const double q = sm.y[i] * pc.dinv[i];
@@ -449,7 +887,7 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_step(PrecondDev pc, PcgVecs
     }
     sm.y[i] = yv;
   }
-  trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, pc.EF, npad, sm);
+  pre_apply<T, false>(pc, sm);
   // s -= alpha w (l.198), eta' = ||s||^2 (l.199); kept in registers until every CTA has read s, p
   double sn[kVecPerThread], pn[kVecPerThread];
   double e = 0.0;
@@ -505,7 +943,7 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_step(PrecondDev pc, PcgVecs
   }
   if (!cont || !next_q) return;
   // next q = P^{-1} p (l.193 of the next iteration)
-  trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, pc.EB, npad, sm);
+  pre_apply<T, true>(pc, sm);
   e = 0.0;
   for (int i = tid; i < n; i += blockDim.x) {
     const double q = sm.y[i] * pc.dinv[i];
@@ -582,8 +1020,8 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_boot_x1(PrecondDev pc, const do
   }
   const double xx = block_sum(e, sm.red);
   const double sig0 = passout[n] / (1.0 + xx);
-  trsv_ws<T, false>((const T*)pc.RTrow, pc.DinvF, pc.EF, npad, sm);
-  trsv_ws<T, true>((const T*)pc.Rrow, pc.DinvB, pc.EB, npad, sm);
+  pre_apply<T, false>(pc, sm);
+  pre_apply<T, true>(pc, sm);
   if (cluster_ctarank() == 0)
     for (int i = tid; i < n; i += blockDim.x) x1[i] = fma(sig0, sm.y[i] * pc.dinv[i], x0[i]);
 }
@@ -631,7 +1069,29 @@ int launch_precond_apply(const PrecondDev& pc, int trans, int nrhs, double* Y, i
   return rc;
 }
 
+static int wgemv_grid_launch(const PrecondDev& pc, PcgVecs v, const double* passout, const PcgState* S, int nrhs,
+                             int mode, int variant, int all, cudaStream_t st) {
+  const size_t smem = 2 * (size_t)pc.npad * 8;
+  static size_t attr = 0;
+  if (attr < smem) {
+    TLS_CUDA_TRY(cudaFuncSetAttribute(k_wgemv_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  int g = (pc.n + kWG / 32 - 1) / (kWG / 32);
+  if (g > num_sms()) g = num_sms();
+  k_wgemv_grid<<<g, kWG, smem, st>>>(pc, v, passout, S, nrhs, mode, variant, all);
+  TLS_LAUNCH_CHECK();
+  return 0;
+}
+
 int launch_pcg_init(const PrecondDev& pc, int nrhs, PcgVecs v, PcgState* S, cudaStream_t st) {
+  if (pc.W != nullptr) {                 // R24: three kernels, no substitution chain
+    int rc = wgemv_grid_launch(pc, v, nullptr, S, nrhs, 0, 0, 1, st);
+    if (rc) return rc;
+    k_wpcg_init_mid<<<2, kTT, 0, st>>>(pc, nrhs, v, S);
+    TLS_LAUNCH_CHECK();
+    return wgemv_grid_launch(pc, v, nullptr, S, nrhs, 2, 0, 1, st);
+  }
   const size_t sm = trsv_smem(pc.npad);
   int rc = 0;
   TLS_DISPATCH_UF(pc.u_f, { rc = launch_cluster(k_pcg_init<T>, 2, sm, st, pc, nrhs, v, S); });
@@ -640,6 +1100,19 @@ int launch_pcg_init(const PrecondDev& pc, int nrhs, PcgVecs v, PcgState* S, cuda
 
 int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgState* S, int nrhs, int rule,
                     int next_q, int variant, int pass_nrhs, cudaStream_t st) {
+  if (pc.W != nullptr) {                 // R24: one cooperative kernel over every SM
+    const size_t smem = 4 * (size_t)pc.npad * 8;
+    static size_t attr = 0;
+    if (attr < smem) {
+      TLS_CUDA_TRY(cudaFuncSetAttribute(k_wpcg_step_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    int g = (pc.n + kWG / 32 - 1) / (kWG / 32);
+    if (g > num_sms()) g = num_sms();
+    void* args[] = {(void*)&pc, &v, (void*)&passout, &S, &nrhs, &rule, &next_q, &variant, &pass_nrhs};
+    TLS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_wpcg_step_coop, dim3(g), dim3(kWG), args, smem, st));
+    return 0;
+  }
   const size_t sm = trsv_smem(pc.npad);
   int rc = 0;
   TLS_DISPATCH_UF(pc.u_f, { rc = launch_cluster(k_pcg_step<T>, nrhs, sm, st, pc, v, passout, S, nrhs, rule, next_q,
@@ -665,6 +1138,23 @@ int launch_boot_x1(const PrecondDev& pc, const double* passout_r0, const double*
   const size_t sm = trsv_smem(pc.npad);
   int rc = 0;
   TLS_DISPATCH_UF(pc.u_f, { rc = launch_cluster(k_boot_x1<T>, 1, sm, st, pc, passout_r0, x0, x1); });
+  return rc;
+}
+
+int launch_trtri(const PrecondDev& pc, double* W, double* WT, cudaStream_t st) {
+  const size_t smem = (size_t)pc.npad * 4 * 8 + 9 * 32 * 4 * 8;
+  TLS_CUDA_TRY(cudaMemsetAsync(W, 0, (size_t)pc.npad * pc.npad * 8, st));
+  TLS_CUDA_TRY(cudaMemsetAsync(WT, 0, (size_t)pc.npad * pc.npad * 8, st));
+  int rc = 0;
+  TLS_DISPATCH_UF(pc.u_f, {
+    static size_t attr = 0;
+    if (attr < smem) {
+      TLS_CUDA_TRY(cudaFuncSetAttribute(k_trtri<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    k_trtri<T><<<(pc.npad / 32) * 8, 256, smem, st>>>(pc, W, WT);
+  });
+  TLS_LAUNCH_CHECK();
   return rc;
 }
 

@@ -88,6 +88,8 @@ struct tls_precond_s {
   size_t a32_bytes = 0;
   const double* a32_src = nullptr;
   int64_t a32_m = -1, a32_ld = -1;
+  // explicit inverse W = R~^{-1} and W^T (R24), made by the first solve that applies it
+  double* winv = nullptr;
 };
 
 static int allreduce(tls_comm_t comm, double* buf, size_t count, int op, cudaStream_t st) {
@@ -272,6 +274,7 @@ size_t carve(const tls_matrix_t* A, void* ws, size_t bytes, Work& w, bool factor
   w.vec.p = c.take<double>(2 * (size_t)n);
   w.vec.q = c.take<double>(2 * (size_t)n);
   w.vec.rhs = c.take<double>(2 * (size_t)n);
+  w.vec.w = c.take<double>(2 * (size_t)n);
   w.x = c.take<double>(n);
   w.x_prev = c.take<double>(n);
   w.x0 = c.take<double>(n);
@@ -434,6 +437,28 @@ int ensure_a32(Ctx& cx, const tls_matrix_t* A, tls_precond_t R) {
   R->a32_ld = A->ld;
   cx.launches += 1;
   cx.passes += 1;
+  return 0;
+}
+
+// W = R~^{-1} in fp64 for the explicit-inverse preconditioner application (R24).
+static A32Spare& winv_spare() {   // one spare W buffer, reused by the next handle (see a32_spare)
+  static A32Spare s;
+  return s;
+}
+
+int ensure_winv(Ctx& cx, tls_precond_t R) {
+  if (R->winv) return 0;
+  const size_t bytes = 2 * (size_t)R->dev.npad * R->dev.npad * 8;
+  A32Spare& sp = winv_spare();
+  if (sp.ptr && sp.device == R->device && sp.bytes == bytes) {
+    R->winv = reinterpret_cast<double*>(sp.ptr);
+    sp.ptr = nullptr;
+  } else {
+    const cudaError_t e = cudaMalloc(&R->winv, bytes);
+    if (e != cudaSuccess) { R->winv = nullptr; set_error("cudaMalloc(W %zu B): %s", bytes, cudaGetErrorString(e)); return TLS_ERR_CUDA; }
+  }
+  TLS_TRY(launch_trtri(R->dev, R->winv, R->winv + (size_t)R->dev.npad * R->dev.npad, cx.st));
+  cx.launches += 1;
   return 0;
 }
 
@@ -807,6 +832,12 @@ int tls_precond_export(tls_precond_t R, double* Rt_host, double* d_host, double*
 
 void tls_precond_destroy(tls_precond_t R) {
   if (!R) return;
+  if (R->winv) {
+    cudaDeviceSynchronize();
+    A32Spare& sp = winv_spare();
+    if (sp.ptr) cudaFree(sp.ptr);
+    sp = A32Spare{R->device, 2 * (size_t)R->dev.npad * R->dev.npad * 8, reinterpret_cast<float*>(R->winv)};
+  }
   if (R->a32) {
     cudaDeviceSynchronize();
     A32Spare& sp = a32_spare();
@@ -842,12 +873,19 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   if (o.op_variant != 0 && o.op_variant != 1) { set_error("op_variant must be 0 (A-in-loop) or 1 (paper Alg. 3)"); return TLS_ERR_ARG; }
   if (o.u_p != 0 && o.u_p != TLS_FP64 && o.u_p != TLS_FP32) { set_error("u_p must be TLS_FP64 (or 0) or TLS_FP32"); return TLS_ERR_UNSUPPORTED; }
   const bool up32 = o.u_p == TLS_FP32 && o.op_variant == 0;
+  if (o.precond_apply < 0 || o.precond_apply > 2) { set_error("precond_apply must be 0 (auto), 1 or 2"); return TLS_ERR_ARG; }
+  // R24: substitution (1) or the explicit inverse (2); auto (0) = the inverse only when the
+  // solve is sharded over several ranks, where the replicated solves are the serial part
+  const bool multi = comm != nullptr && comm->nranks > 1;
+  const bool use_w = o.precond_apply == 2 || (o.precond_apply == 0 && multi);
   if (o.max_outer < 1) o.max_outer = 1;
   Work w;
   if (!carve_ok(A, ws, ws_bytes, w, false)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
   Ctx cx{static_cast<cudaStream_t>(stream), comm};
   const int n = (int)A->n;
-  const PrecondDev& pc = R->dev;
+  if (use_w) TLS_TRY(ensure_winv(cx, R));
+  PrecondDev pc = R->dev;
+  if (use_w) { pc.W = R->winv; pc.WT = R->winv + (size_t)pc.npad * pc.npad; }
   if (is_csr(A)) TLS_TRY(launch_csc_build(csr_view(A), w.csc, w.csc_scratch, cx.st, &cx.launches));
   if (up32) TLS_TRY(ensure_a32(cx, A, R));
   const double tol_in = o.tol_inner > 0 ? o.tol_inner : tol;
@@ -1130,8 +1168,15 @@ int tls_pass_fp32(const tls_matrix_t* A, tls_precond_t R, const double* q, doubl
 }
 
 int tls_precond_apply(const tls_precond_t R, int32_t trans, int32_t nrhs, double* Y, void* stream) {
-  if (!R || nrhs < 1 || nrhs > 2 || !Y) { set_error("bad apply args"); return TLS_ERR_ARG; }
-  return launch_precond_apply(R->dev, trans ? 1 : 0, nrhs, Y, R->dev.n, static_cast<cudaStream_t>(stream));
+  if (!R || nrhs < 1 || nrhs > 2 || !Y || trans < 0 || trans > 3) { set_error("bad apply args"); return TLS_ERR_ARG; }
+  Ctx cx{static_cast<cudaStream_t>(stream), nullptr};
+  PrecondDev pc = R->dev;
+  if (trans & 2) {                      // through the explicit inverse (R24)
+    TLS_TRY(ensure_winv(cx, R));
+    pc.W = R->winv;
+    pc.WT = R->winv + (size_t)pc.npad * pc.npad;
+  }
+  return launch_precond_apply(pc, trans & 1, nrhs, Y, R->dev.n, cx.st);
 }
 
 int tls_round(const double* x, double* y, int64_t n, int32_t prec, void* stream) {

@@ -102,7 +102,11 @@ struct PrecondDev {
   double* d;        // npad (1 on padding)
   double* dinv;     // npad
   double* normA2;   // 1 (device)
+  const double* W = nullptr;   // explicit inverse R~^{-1} (fp64 npad x npad, upper) when the solve applies it (R24)
+  const double* WT = nullptr;  // its transpose (lower), so both products run over contiguous rows
 };
+// W = R~^{-1} and WT = W^T (k_trtri in k_trsv.cu): npad x npad fp64 each, zeroed by the launcher.
+int launch_trtri(const PrecondDev& pc, double* W, double* WT, cudaStream_t st);
 // lower = 0: R upper (R[i][j], j >= i, row-major); lower = 1: R^T in the lower triangle.
 int launch_pack_R(const double* R, int ldR, int lower, PrecondDev& pc, int* range, cudaStream_t st,
                   int* launches);
@@ -116,8 +120,9 @@ struct PcgState {
   int iter[2];    // iteration index j of the next step, per RHS
   double bb;      // b^T b of the local rows (all-reduced), from the setup pass
 };
-struct PcgVecs {  // device, each [2][npad]
+struct PcgVecs {  // device, each [2][n] (RHS r at offset r * n)
   double *omega, *s, *p, *q, *rhs;
+  double* w;      // P^{-T}-solve result of a step (explicit-inverse path, R24)
 };
 int launch_precond_apply(const PrecondDev& pc, int trans, int nrhs, double* Y, int ldY,
                          cudaStream_t st);

@@ -38,7 +38,7 @@ class tls_rqi_opts_t(C.Structure):
                 ("polish", C.c_int32), ("tol_inner", C.c_double), ("boot", C.c_int32),
                 ("boot_max", C.c_int32), ("boot_tol", C.c_double), ("op_variant", C.c_int32),
                 ("breakdown_rule", C.c_int32), ("gram_chunk", C.c_int32), ("u_p", C.c_int32),
-                ("reserved", C.c_int32 * 4)]
+                ("precond_apply", C.c_int32), ("reserved", C.c_int32 * 3)]
 
 
 class tls_info_t(C.Structure):
@@ -375,7 +375,8 @@ def tls_pass_fp32(M: tls_matrix_t, R: "Precond", q: torch.Tensor, stream=None, w
 
 
 def tls_precond_apply(R: Precond, trans: int, Y: torch.Tensor, stream=None) -> torch.Tensor:
-    """In place: Y (nrhs x n) <- P^{-1} Y (trans 0) or P^{-T} Y (trans 1)."""
+    """In place: Y (nrhs x n) <- P^{-1} Y (trans 0) or P^{-T} Y (trans 1); trans | 2 applies
+    them through the explicit inverse W = R~^{-1} (R24)."""
     nrhs = 1 if Y.dim() == 1 else Y.shape[0]
     assert Y.is_contiguous()
     _check(lib().tls_precond_apply(C.c_void_p(R.handle), trans, nrhs, _ptr(Y), _stream(stream)),

@@ -391,3 +391,35 @@ def test_up_fp32_suffices(name, fmt):
     assert r32.rqi_iters == r64.rqi_iters
     assert np.linalg.norm(r32.x - ex.x) / np.linalg.norm(ex.x) <= 1e-12
     assert abs(r32.sigma - ex.sigma) / ex.sigma <= 1e-12
+
+
+# ----------------------------------------------------------------------------- explicit inverse (R24)
+def test_explicit_inverse_apply():
+    """with_inverse (R24): W R~ = I, and P^{-1}, P^{-T} through W equal the substitutions
+    to kappa(R~) u (the operator is the same linear map; only the rounding differs)."""
+    P = tlsgen.config("cfg2w")
+    pc = rqi.factor_precond(P.A, "bf16")
+    pw = rqi.with_inverse(pc)
+    n = pc.Rt.shape[0]
+    assert np.allclose(pw.W @ pc.Rt, np.eye(n), atol=1e-12)
+    assert np.array_equal(np.tril(pw.W, -1), np.zeros((n, n)))
+    kap = np.linalg.cond(pc.Rt)
+    y = np.random.default_rng(3).standard_normal(n)
+    for f in (rqi.apply_Pinv, rqi.apply_PinvT):
+        a, b = f(pc, y), f(pw, y)
+        assert np.linalg.norm(a - b) <= 10 * kap * 2.0 ** -53 * np.linalg.norm(a)
+
+
+@pytest.mark.parametrize("name,fmt", [("cfg1", "fp16"), ("cfg2w", "bf16"), ("cfg2w", "fp16")])
+def test_explicit_inverse_same_solve(name, fmt):
+    """The solve through W: the same status, RQI and PCG counts as substitution, and the
+    SVD's x and sigma."""
+    P = tlsgen.config(name)
+    ex = exact.tls_svd(P.A, P.b)
+    pc = rqi.factor_precond(P.A, fmt)
+    r1 = rqi.rqi_pcgtls_mp(P.A, P.b, pc)
+    r2 = rqi.rqi_pcgtls_mp(P.A, P.b, pc, opts=rqi.RqiOptions(precond_apply=2))
+    assert (r2.status, r2.termination, r2.rqi_iters, r2.pcg_iters) == (r1.status, r1.termination, r1.rqi_iters, r1.pcg_iters)
+    assert abs(r2.boot_iters - r1.boot_iters) <= 1
+    assert np.linalg.norm(r2.x - ex.x) / np.linalg.norm(ex.x) <= 1e-12
+    assert abs(r2.sigma - ex.sigma) / ex.sigma <= 1e-12
