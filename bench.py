@@ -265,41 +265,58 @@ def main():
 
     for _ in range(args.warmup):
         fi, info, sig = step()
-    tlsrqi.tls_profile_enable(True)
-    sampler = ClockSampler(local)
+
+    def timed():
+        tlsrqi.tls_profile_enable(True)
+        sampler = ClockSampler(local)
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        launches = 0
+        passes = 0
+        infos = []
+        dbg = os.environ.get("BENCH_DEBUG") == "1"
+        for _ in range(args.steps):
+            if dbg:
+                ev_a = torch.cuda.Event(enable_timing=True); ev_a.record(stream); th = time.perf_counter()
+            fi, info, sig = step()
+            if dbg:
+                ev_b = torch.cuda.Event(enable_timing=True); ev_b.record(stream); ev_b.synchronize()
+                print(f"[bench] step device {ev_a.elapsed_time(ev_b):.2f} ms host {1e3 * (time.perf_counter() - th):.2f} ms",
+                      file=sys.stderr, flush=True)
+            launches += fi["launches"] + info["launches"]
+            passes += fi["passes"] + info["passes"]
+            infos.append(info)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            tdist.barrier()
+        clocks = sampler.stop()
+        prof = tlsrqi.tls_profile_read()
+        tlsrqi.tls_profile_enable(False)
+        ms_total = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            ms_total = float(t.item())
+        return ms_total, launches, passes, infos, clocks, prof, sig
+
+    # a run that saw hardware or thermal slowdown is measured once more (timing rules);
+    # the decision is all-reduced so every rank repeats together
+    BAD = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    ms_total, launches, passes, infos, clocks, prof, sig = timed()
+    bad = 1.0 if BAD & set(clocks.get("reasons", [])) else 0.0
     if world > 1:
-        tdist.barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    launches = 0
-    passes = 0
-    infos = []
-    dbg = os.environ.get("BENCH_DEBUG") == "1"
-    for _ in range(args.steps):
-        if dbg:
-            ev_a = torch.cuda.Event(enable_timing=True); ev_a.record(stream); th = time.perf_counter()
-        fi, info, sig = step()
-        if dbg:
-            ev_b = torch.cuda.Event(enable_timing=True); ev_b.record(stream); ev_b.synchronize()
-            print(f"[bench] step device {ev_a.elapsed_time(ev_b):.2f} ms host {1e3 * (time.perf_counter() - th):.2f} ms",
-                  file=sys.stderr, flush=True)
-        launches += fi["launches"] + info["launches"]
-        passes += fi["passes"] + info["passes"]
-        infos.append(info)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        tdist.barrier()
-    clocks = sampler.stop()
-    prof = tlsrqi.tls_profile_read()
-    tlsrqi.tls_profile_enable(False)
-    ms_total = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        t = torch.tensor([bad], dtype=torch.float64, device="cuda")
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        ms_total = float(t.item())
+        bad = float(t.item())
+    if bad:
+        first = clocks
+        ms_total, launches, passes, infos, clocks, prof, sig = timed()
+        clocks = dict(clocks, remeasured_after=first)
     ms_step = ms_total / args.steps
     tts = ms_step / 1e3
 
