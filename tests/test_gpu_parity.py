@@ -111,7 +111,7 @@ def test_gram_within_accumulation_bound(T, fmt, m, n, path, monkeypatch):
     if path == "cc":
         monkeypatch.setenv("TLS_GRAM", "cc")
     elif fmt in ("fp32", "fp64"):
-        pytest.skip("fp32/fp64 Gram has only the fp64 CUDA-core path")
+        pytest.skip("the fp32/fp64 Gram has a single path (fp64 tensor cores, k_gram_f64)")
     P = _problem(m, n)
     d, _ = rqi.column_scaling(P.A)
     rc, G = T.tls_gram(T.matrix(T.dense_operand(dev(P.A))), fmt, dev(d), 2048)
