@@ -355,6 +355,21 @@ def main():
                 "avg_launch_ms": avg_ms, "launches": p2["count"], "working_launches": working,
                 "peak_kind": peak_kind}
     kshare = {k: v["ms"] / ms_total for k, v in prof.items() if v["count"]}
+    # context for `frac`: a plain streaming read of the same operand (torch's column sum,
+    # no arithmetic to speak of) timed right after the step loop, in the same clock /
+    # power state; the copy-based peak of MEASURED_PEAKS.json is a short burst
+    if roof is not None and not csr:
+        A_loc.sum(0)
+        torch.cuda.synchronize()
+        r0 = torch.cuda.Event(enable_timing=True)
+        r1 = torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        for _ in range(20):
+            A_loc.sum(0)
+        r1.record(stream)
+        torch.cuda.synchronize()
+        roof["plain_read_gbs_same_state"] = bytes_per_pass / (r0.elapsed_time(r1) / 20 * 1e-3) / 1e9
+        roof["frac_of_plain_read"] = roof["achieved"] / roof["plain_read_gbs_same_state"]
 
     # ---- e2e: the same solve through tls_solve_host from pinned host buffers
     e2e = None
