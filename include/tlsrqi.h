@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define TLSRQI_ABI_VERSION 1
+#define TLSRQI_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define TLS_API __attribute__((visibility("default")))
@@ -117,7 +117,10 @@ typedef struct {
                              l.427); 2 = products with W = R~^{-1} formed once per handle in fp64 (npad^2
                              doubles owned by the handle); 0 = auto [0]: 2 when comm has several ranks,
                              else 1 */
-  int32_t reserved[3];
+  int32_t certify;        /* 1: after the solve, sigma_certified = sqrt(||b - A x||^2 / (1 + ||x||^2)) with
+                             every residual and sum by Dot2 (compensated; one more pass over A;
+                             SURVEY §8(c) c2 step 8); 0 [0]: skipped, sigma_certified = NaN */
+  int32_t reserved[2];
 } tls_rqi_opts_t;
 
 /* Results.  pcg_iters (2*max_outer ints), sigma2_trace, psi_trace
@@ -134,7 +137,8 @@ typedef struct {
   int64_t passes;         /* passes over A made by the call */
   int32_t launches;       /* kernels launched by the call (this library's kernels only) */
   int32_t pcg_steps;      /* RQI steps whose PCGTLS counts are in pcg_iters */
-  int32_t reserved[4];
+  double sigma_certified; /* compensated sigma of the returned x (opts.certify), else NaN */
+  int32_t reserved[2];
 } tls_info_t;
 
 TLS_API int tls_abi_version(void);

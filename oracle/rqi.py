@@ -436,12 +436,55 @@ def rqi_pcgtls_mp(A, b: np.ndarray, pc: Precond, tol: float = 1e-14,
     return res
 
 
+def _two_sum(a, b):
+    """Knuth's TwoSum: s + e = a + b exactly (s = fl(a + b))."""
+    s = a + b
+    bb = s - a
+    return s, (a - (s - bb)) + (b - bb)
+
+
+def _split(a):
+    """Veltkamp split of fp64 values into 26 + 27 significant bits."""
+    c = 134217729.0 * a        # 2^27 + 1
+    hi = c - (c - a)
+    return hi, a - hi
+
+
+def _two_prod(a, b):
+    """Dekker's TwoProduct: p + e = a * b exactly (p = fl(a * b)), without an fma."""
+    p = a * b
+    ah, al = _split(a)
+    bh, bl = _split(b)
+    return p, al * bl - (((p - ah * bh) - al * bh) - ah * bl)
+
+
+def dot2_rows(terms_a, terms_b):
+    """Dot2 (Ogita, Rump & Oishi 2005, Alg. 5.3) of each row of two (rows x k) arrays,
+    summed left to right: as accurate as the dot product in twice fp64 rounded once."""
+    s = np.zeros(terms_a.shape[0])
+    c = np.zeros(terms_a.shape[0])
+    for j in range(terms_a.shape[1]):
+        p, e = _two_prod(terms_a[:, j], terms_b[:, j])
+        s, q = _two_sum(s, p)
+        c = c + (q + e)
+    return s + c
+
+
 def certify_sigma(A, b: np.ndarray, x: np.ndarray) -> float:
-    """sigma = sqrt(||b - A x||^2 / (1 + ||x||^2)) with exactly rounded sums
-    (math.fsum), the compensated final certificate."""
-    Ax = matvec(A, x)
-    r = b - Ax
-    return math.sqrt(math.fsum(r * r) / (1.0 + math.fsum(x * x)))
+    """The final certificate: sigma = sqrt(||b - A x||^2 /
+    (1 + ||x||^2)) with r_i = b_i - a_i . x, ||r||^2 and ||x||^2 each formed by Dot2
+    (compensated products and sums), then one fp64 square root of the quotient."""
+    if _is_sparse(A):
+        A = A.toarray()
+    A = np.asarray(A, dtype=np.float64)
+    m, n = A.shape
+    # r_i = Dot2 over the n + 1 terms (b_i * 1) + sum_j (-a_ij) x_j
+    ta = np.concatenate([b[:, None], -A], axis=1)
+    tb = np.concatenate([np.ones((m, 1)), np.broadcast_to(x, (m, n))], axis=1)
+    r = dot2_rows(ta, tb)
+    rho = dot2_rows(r[None, :], r[None, :])[0]
+    xx = dot2_rows(x[None, :], x[None, :])[0]
+    return math.sqrt(rho / (1.0 + xx))
 
 
 def solve(A, b, u_f: str, tol: float = 1e-14, opts: Optional[RqiOptions] = None):

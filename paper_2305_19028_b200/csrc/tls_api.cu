@@ -523,6 +523,7 @@ void fill_info_defaults(tls_info_t* info) {
   info->passes = 0;
   info->launches = 0;
   info->pcg_steps = 0;
+  info->sigma_certified = NAN;
 }
 
 // Device buffers of destroyed handles are kept for reuse (keyed by device and size):
@@ -1039,8 +1040,20 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   }
   k_copy<<<(n + 255) / 256, 256, 0, cx.st>>>(use_prev ? w.x_prev : w.x, x_out, n);
   cx.launches += 1;
+  double cert[3] = {NAN, 0.0, 0.0};
+  if (o.certify) {                       // compensated certificate (c2 step 8): one more pass
+    const DenseView dv = is_csr(A) ? DenseView{} : dense_view(A);
+    const CsrView cv = is_csr(A) ? csr_view(A) : CsrView{};
+    TLS_TRY(launch_certify(is_csr(A) ? nullptr : &dv, is_csr(A) ? &cv : nullptr, b, x_out, n, w.partials, w.passout,
+                           cx.st));
+    TLS_TRY(allreduce(cx.comm, w.passout, 2, ncclSum, cx.st));
+    TLS_CUDA_TRY(cudaMemcpyAsync(cert, w.passout, sizeof(cert), cudaMemcpyDeviceToHost, cx.st));
+    cx.launches += 2;
+    cx.passes += 1;
+  }
   TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
   TLS_LAUNCH_CHECK();
+  if (info && o.certify) info->sigma_certified = std::sqrt((cert[0] + cert[1]) / (1.0 + cert[2]));
   if (sigma_out) *sigma_out = std::sqrt(sig2_ret);
   if (info) {
     info->status = status;

@@ -143,4 +143,10 @@ int launch_rqi_update(const PrecondDev& pc, PcgVecs v, const PcgState* S, double
 int launch_boot_x1(const PrecondDev& pc, const double* passout_r0, const double* x0, double* x1,
                    cudaStream_t st);
 
+// compensated certificate (k_certify.cu): out[0..1] = Dot2 pair of ||b - A x||^2 over the
+// local rows, out[2] = ||x||^2; part: certify_grid() x 2 doubles of scratch.
+int certify_grid();
+int launch_certify(const DenseView* D, const CsrView* S, const double* b, const double* x, int n, double* part,
+                   double* out, cudaStream_t st);
+
 }  // namespace tls

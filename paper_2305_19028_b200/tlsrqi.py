@@ -38,7 +38,7 @@ class tls_rqi_opts_t(C.Structure):
                 ("polish", C.c_int32), ("tol_inner", C.c_double), ("boot", C.c_int32),
                 ("boot_max", C.c_int32), ("boot_tol", C.c_double), ("op_variant", C.c_int32),
                 ("breakdown_rule", C.c_int32), ("gram_chunk", C.c_int32), ("u_p", C.c_int32),
-                ("precond_apply", C.c_int32), ("reserved", C.c_int32 * 3)]
+                ("precond_apply", C.c_int32), ("certify", C.c_int32), ("reserved", C.c_int32 * 2)]
 
 
 class tls_info_t(C.Structure):
@@ -48,7 +48,7 @@ class tls_info_t(C.Structure):
                 ("breakdown_k", C.c_int32), ("breakdown_rhs", C.c_int32),
                 ("breakdown_j", C.c_int32), ("chol_pivot", C.c_int32), ("sigma2", C.c_double),
                 ("passes", C.c_int64), ("launches", C.c_int32), ("pcg_steps", C.c_int32),
-                ("reserved", C.c_int32 * 4)]
+                ("sigma_certified", C.c_double), ("reserved", C.c_int32 * 2)]
 
 
 _lib = None
@@ -229,6 +229,7 @@ def _info_dict(info: tls_info_t, bufs) -> dict:
         "breakdown_k": int(info.breakdown_k), "breakdown_rhs": int(info.breakdown_rhs),
         "breakdown_j": int(info.breakdown_j), "chol_pivot": int(info.chol_pivot),
         "sigma2": float(info.sigma2), "passes": int(info.passes), "launches": int(info.launches),
+        "sigma_certified": float(info.sigma_certified),
     }
 
 

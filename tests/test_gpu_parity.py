@@ -498,3 +498,30 @@ def test_paper_sec4_problems(T, name, fmt):
     _check_solve(info2, x2.cpu().numpy(), sig2, res_or, pcg_slack=2)
     for a, b in zip(info2["sigma2_trace"], res_or.sigma2_trace):
         assert a == pytest.approx(b, rel=1e-9)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2w", "vanhuffel", "cfg3"])
+def test_certified_sigma(T, name):
+    """opts.certify: the GPU's Dot2 certificate of the returned x
+    equals the oracle's certify_sigma of the same x to a few ulps (both twice-fp64
+    accurate, different summation orders), and the SVD's sigma to the solve's accuracy."""
+    if name == "cfg3":
+        P = tlsgen.config("cfg3", m=20000, n=500)
+        A = P.to_dense()
+        M = T.matrix_csr(torch.as_tensor(P.rowptr, device="cuda"), torch.as_tensor(P.colidx, device="cuda"),
+                         torch.as_tensor(P.vals, device="cuda"), P.n)
+    else:
+        P = tlsgen.config(name) if name.startswith("cfg") else tlsgen.paper_problem(name)
+        A = P.A
+        M = T.matrix(T.dense_operand(dev(A)), n=A.shape[1])
+    rc, R, _ = T.tls_factor_precond(M, "fp16")
+    rc, x, sig, info = T.tls_rqi_pcgtls(M, dev(P.b), R, opts=T.tls_rqi_opts_default(certify=1))
+    assert info["status"] == rqi.OK
+    sc = info["sigma_certified"]
+    ref = rqi.certify_sigma(A, np.asarray(P.b), x.cpu().numpy())
+    assert abs(sc - ref) / ref <= 1e-14
+    assert abs(sc - sig) / sig <= 1e-12
+    if A.shape[0] * A.shape[1] <= 4096 * 512:
+        assert abs(sc - exact.tls_svd(A, np.asarray(P.b)).sigma) / sc <= 1e-11
+    rc, x2, sig2, info2 = T.tls_rqi_pcgtls(M, dev(P.b), R)
+    assert math.isnan(info2["sigma_certified"])

@@ -423,3 +423,33 @@ def test_explicit_inverse_same_solve(name, fmt):
     assert abs(r2.boot_iters - r1.boot_iters) <= 1
     assert np.linalg.norm(r2.x - ex.x) / np.linalg.norm(ex.x) <= 1e-12
     assert abs(r2.sigma - ex.sigma) / ex.sigma <= 1e-12
+
+
+# ----------------------------------------------------------------------------- certificate
+def test_dot2_against_exact_rationals():
+    """dot2_rows (Dot2): within one rounding of the exact rational dot product (plus the
+    Dot2 bound's u^2 cond term), on sums with heavy cancellation where plain fp64 fails."""
+    from fractions import Fraction
+    rng = np.random.default_rng(21)
+    k = 40
+    a = rng.standard_normal((8, k)) * 10.0 ** rng.integers(-8, 8, (8, k))
+    b = rng.standard_normal((8, k))
+    a[:, -1] = -(a[:, :-1] * b[:, :-1]).sum(axis=1) / b[:, -1]      # near-cancellation
+    got = rqi.dot2_rows(a, b)
+    for i in range(8):
+        ex = sum(Fraction(float(a[i, j])) * Fraction(float(b[i, j])) for j in range(k))
+        absd = sum(abs(Fraction(float(a[i, j])) * Fraction(float(b[i, j]))) for j in range(k))
+        err = abs(Fraction(float(got[i])) - ex)
+        assert err <= Fraction(2.0 ** -53) * abs(ex) + Fraction(4 * k * k) * Fraction(2.0 ** -106) * absd
+
+
+def test_certify_sigma_exact_on_consistent_pair():
+    """certify_sigma on the SPEC.md:213 2x2 TLS closed form (sigma^2 = 3 - sqrt(5),
+    x = (sqrt(5) - 1)/2) and on a consistent system (sigma = 0 at x_true)."""
+    A = np.array([[2.0], [0.0]])          # tests/golden/tls_2x2.txt (SPEC.md:213-214)
+    b = np.array([1.0, 1.0])
+    x = np.array([(math.sqrt(5.0) - 1.0) / 2.0])
+    s = rqi.certify_sigma(A, b, x)
+    assert s * s == pytest.approx(3.0 - math.sqrt(5.0), rel=1e-14)
+    P = tlsgen.paper_problem("bjorck", eps=0.0)
+    assert rqi.certify_sigma(P.A, P.b, P.x_true) < 1e-15
