@@ -177,7 +177,8 @@ TLS_API int tls_precond_export(tls_precond_t R, double* Rt_host, double* d_host,
 TLS_API void tls_precond_destroy(tls_precond_t R);
 
 /* ---- the RQI-PCGTLS-MP solve (§8 rows a4-a9) ----
- * u and u_r must be TLS_FP64 (north_star); tol is the primary stop
+ * R must come from this A (same n and, for a factored handle, the same m_global; else
+ * TLS_ERR_ARG).  u and u_r must be TLS_FP64 (north_star); tol is the primary stop
  * psi_k <= tol ||[A,b]||_F^2 (R6).  x_out_dev (n fp64) receives the returned
  * iterate on every rank, *sigma_out_host = sqrt(sigma^2) of that iterate. */
 TLS_API int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b_local_dev, const tls_precond_t R,

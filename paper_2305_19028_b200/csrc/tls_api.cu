@@ -90,6 +90,8 @@ struct tls_precond_s {
   int64_t a32_m = -1, a32_ld = -1;
   // explicit inverse W = R~^{-1} and W^T (R24), made by the first solve that applies it
   double* winv = nullptr;
+  // fingerprint of the factored A: global row count; -1 for imported handles
+  int64_t m_global = -1;
 };
 
 static int allreduce(tls_comm_t comm, double* buf, size_t count, int op, cudaStream_t st) {
@@ -757,6 +759,7 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
     return st;
   }
   h->normA2_host = hnorm;
+  h->m_global = A->m_global;
   *R_out = h;
   return 0;
 }
@@ -869,6 +872,11 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   TLS_TRY(check_matrix(A));
   if (u != TLS_FP64 || u_r != TLS_FP64) { set_error("u and u_r must be TLS_FP64 in this build"); return TLS_ERR_UNSUPPORTED; }
   if (!R || R->dev.n != A->n || !x_out || (A->m_local > 0 && !b)) { set_error("bad rqi args"); return TLS_ERR_ARG; }
+  if (R->m_global >= 0 && R->m_global != A->m_global) {
+    set_error("the preconditioner was factored from a %lld-row A, not this %lld-row one", (long long)R->m_global,
+              (long long)A->m_global);
+    return TLS_ERR_ARG;
+  }
   tls_rqi_opts_t o;
   if (opts) o = *opts; else tls_rqi_opts_default(&o);
   if (o.op_variant != 0 && o.op_variant != 1) { set_error("op_variant must be 0 (A-in-loop) or 1 (paper Alg. 3)"); return TLS_ERR_ARG; }

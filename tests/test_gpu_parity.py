@@ -525,3 +525,13 @@ def test_certified_sigma(T, name):
         assert abs(sc - exact.tls_svd(A, np.asarray(P.b)).sigma) / sc <= 1e-11
     rc, x2, sig2, info2 = T.tls_rqi_pcgtls(M, dev(P.b), R)
     assert math.isnan(info2["sigma_certified"])
+
+
+def test_handle_fingerprint(T):
+    """A handle factored from one A is refused for an A of another shape."""
+    P = tlsgen.config("cfg1")
+    M = T.matrix(dev(P.A))
+    rc, R, _ = T.tls_factor_precond(M, "fp16")
+    M2 = T.matrix(dev(P.A[:150]))
+    with pytest.raises(T.TlsError):
+        T.tls_rqi_pcgtls(M2, dev(P.b[:150]), R)
