@@ -407,6 +407,15 @@ def main():
         with open(os.path.join(ROOT, "profiles", f"counts_{wl}.json"), "w") as fh:
             json.dump({"K": info["rqi_iters"], "B0": info["boot_iters"], "pcg": info["pcg_iters"]}, fh)
 
+    # TTS as a model: the step's passes over A at the HBM peak plus the
+    # measured time of everything that is not a pass (Gram, Cholesky, PCG steps, ...)
+    pass_cats = ("pass_op2", "pass_op1", "pass_resid", "colstats", "pass_op2_fp32", "reduce")
+    non_pass_ms = sum(v["ms"] for k, v in prof.items() if k not in pass_cats) / args.steps
+    passes_at_peak_ms = a_passes * bytes_per_pass / (peak * 1e9) * 1e3
+    tts_model = {"a_passes": a_passes, "passes_at_peak_ms": passes_at_peak_ms,
+                 "measured_non_pass_ms": non_pass_ms, "model_ms": passes_at_peak_ms + non_pass_ms,
+                 "measured_ms": ms_step}
+
     # the uniform-precision control of the paper's comparison (SURVEY
     # §8(d)): the same solve with u_f = fp64 (exact R, fp64 Gram on CUDA cores), timed the
     # same way; its TTS over ours is the measured mixed-precision speedup on B200
@@ -539,7 +548,7 @@ def main():
             "a_passes_per_step": a_passes,
             "pass_launches_per_step": passes / args.steps,
             "a_passes_per_s": a_passes / tts,
-            "roofline": roof, "kernel_share": kshare,
+            "roofline": roof, "kernel_share": kshare, "tts_model": tts_model,
             "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
             "uniform_fp64_control": control,
             "paper_precision_up_fp32": up32,
