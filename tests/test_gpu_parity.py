@@ -535,3 +535,40 @@ def test_handle_fingerprint(T):
     M2 = T.matrix(dev(P.A[:150]))
     with pytest.raises(T.TlsError):
         T.tls_rqi_pcgtls(M2, dev(P.b[:150]), R)
+
+
+def test_empty_row_block(T):
+    """A rank with no rows (m_local = 0, more ranks than rows): every pass, the Gram, the
+    column statistics and the u_p = fp32 pass return zeros (max: 0) without touching A."""
+    P_ = tlsgen.config("cfg1")
+    m, n = P_.A.shape
+    E = torch.zeros((0, n), dtype=torch.float64, device="cuda")
+    M = T.matrix(E, m_global=m, row_offset=m)
+    cm, ss = T.tls_colstats(M)
+    assert float(cm.abs().max()) == 0.0 and float(ss) == 0.0
+    d = torch.ones(n, dtype=torch.float64, device="cuda")
+    assert float(T.tls_gram(M, "fp16", d)[1].abs().max()) == 0.0
+    q = torch.ones((2, n), dtype=torch.float64, device="cuda")
+    v, s = T.tls_pass(M, 0, q)
+    assert float(v.abs().max()) == 0.0 and float(s.abs().max()) == 0.0
+    v, s = T.tls_pass(M, 1, q[0], torch.zeros(0, dtype=torch.float64, device="cuda"))
+    assert float(v.abs().max()) == 0.0 and float(s.abs().max()) == 0.0
+    R = T.tls_precond_import(np.eye(n), np.ones(n), 1.0, "fp64")
+    v, s = T.tls_pass_fp32(M, R, q)
+    assert float(v.abs().max()) == 0.0 and float(s.abs().max()) == 0.0
+
+
+def test_empty_row_block_csr(T):
+    """The same for a CSR rank with no rows (rowptr = [0], no entries)."""
+    n = 50
+    rp = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ci = torch.zeros(0, dtype=torch.int32, device="cuda")
+    va = torch.zeros(0, dtype=torch.float64, device="cuda")
+    M = T.matrix_csr(rp, ci, va, n, m_global=200, row_offset=200)
+    cm, ss = T.tls_colstats(M)
+    assert float(cm.abs().max()) == 0.0 and float(ss) == 0.0
+    d = torch.ones(n, dtype=torch.float64, device="cuda")
+    assert float(T.tls_gram(M, "fp16", d)[1].abs().max()) == 0.0
+    q = torch.ones((2, n), dtype=torch.float64, device="cuda")
+    v, s = T.tls_pass(M, 0, q)
+    assert float(v.abs().max()) == 0.0 and float(s.abs().max()) == 0.0
