@@ -11,6 +11,8 @@ from __future__ import annotations
 
 import dataclasses
 
+import math
+
 import numpy as np
 
 
@@ -84,6 +86,42 @@ def constraints(A: np.ndarray, ex: TlsExact) -> dict:
     gap = 1.0 - ex.sigma ** 2 / ex.sigma_A_min ** 2
     return {"kappa": kappa, "kappa_F": kappa_F, "gap": gap,
             "constr1": 1.0 / kappa, "constr2": gap / kappa_F}
+
+
+def constraint_report(m: int, n: int, sigma_A: np.ndarray, sigma: float, normF: float,
+                      lam_min_H: float, c: float = 1.0) -> dict:
+    """All the factorization-precision constraints of PAPER.md §3.1 (l.270-391), c = 1
+    (reading R13), from the singular values of A, sigma_{n+1}, ||A||_F and lambda_min(H):
+      D1  u_q < 1/(c m n^{3/2} kappa)              QR: R^ nonsingular (l.279-281)
+      D2  u_q < 1/(c m^{1/2} n^{3/4} kappa)        the probabilistic version (l.283-286)
+      D3  u_q <~ 1/kappa                           constr1 (l.287-288)
+      D4  u_q <= 1/(20 n^{3/2} kappa^2)            Cholesky of fl(A^T A), Wilkinson (l.290-294)
+      D5  u_q <~ 1/kappa^2                         its heuristic (l.295-296)
+      D6  u_q < lmin(H)/((2 lmin(H) + n)(n + 1))   scaled Cholesky, H = D^{-1} fl(A^TA) D^{-1} (l.298-304)
+      D7  sqrt(m) g_mn kappa_F < gap, g_mn = c m n u/(1 - c m n u): positive-definite C^ (l.364-378)
+      D8  u_q <~ gap / kappa_F                     constr2 (l.386-387)
+    with gap = 1 - sigma_{n+1}^2/sigma'_n^2 and kappa_F = ||A||_F / sigma'_n."""
+    smax, smin = float(np.max(sigma_A)), float(np.min(sigma_A))
+    kappa = smax / smin
+    kappa_F = normF / smin
+    gap = 1.0 - sigma * sigma / (smin * smin)
+    g = gap / (math.sqrt(m) * kappa_F)           # D7: c m n u / (1 - c m n u) < g
+    return {"kappa": kappa, "kappa_F": kappa_F, "gap": gap,
+            "D1": 1.0 / (c * m * n ** 1.5 * kappa),
+            "D2": 1.0 / (c * math.sqrt(m) * n ** 0.75 * kappa),
+            "D3": 1.0 / kappa,
+            "D4": 1.0 / (20.0 * n ** 1.5 * kappa * kappa),
+            "D5": 1.0 / (kappa * kappa),
+            "D6": lam_min_H / ((2.0 * lam_min_H + n) * (n + 1)),
+            "D7": (g / (c * m * n * (1.0 + g))) if g > 0 else 0.0,
+            "D8": gap / kappa_F}
+
+
+def lam_min_H(A: np.ndarray) -> float:
+    """lambda_min of H = D^{-1} A^T A D^{-1}, D = diag(A^T A)^{1/2}."""
+    G = A.T @ A
+    dd = 1.0 / np.sqrt(np.diag(G))
+    return float(np.linalg.eigvalsh(G * dd[:, None] * dd[None, :])[0])
 
 
 def rayleigh_sigma2(A: np.ndarray, b: np.ndarray, x: np.ndarray) -> float:

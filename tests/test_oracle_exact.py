@@ -93,3 +93,28 @@ def test_literal_cfg2_nearly_nongeneric():
     assert e.kappa_tls > 1e6 and ew.kappa_tls < 1e4
     cons = exact.constraints(P.A, e)
     assert cons["gap"] < 1e-2
+
+
+def test_constraint_report_closed_forms():
+    """constraint_report (§3.1 D1-D8) on cases with closed forms: orthogonal
+    columns of different norms give H = I, so D6 = 1/((2 + n)(n + 1)); D3/D5/D1/D2/D4 are
+    the printed powers of kappa; D7 solves c m n u/(1 - c m n u) = gap/(sqrt(m) kappa_F)
+    exactly at its value; D8 = constr2 of exact.constraints."""
+    m, n = 50, 6
+    Q, _ = np.linalg.qr(np.random.default_rng(1).standard_normal((m, n)))
+    A = Q * np.array([1.0, 2.0, 4.0, 8.0, 16.0, 32.0])
+    assert exact.lam_min_H(A) == pytest.approx(1.0, rel=1e-12)
+    b = A @ np.ones(n) + 0.1 * np.random.default_rng(2).standard_normal(m)
+    ex = exact.tls_svd(A, b)
+    sA = np.linalg.svd(A, compute_uv=False)
+    r = exact.constraint_report(m, n, sA, ex.sigma, float(np.linalg.norm(A)), exact.lam_min_H(A))
+    kap = 32.0
+    assert r["kappa"] == pytest.approx(kap, rel=1e-12)
+    assert r["D3"] == pytest.approx(1 / kap) and r["D5"] == pytest.approx(1 / kap ** 2)
+    assert r["D1"] == pytest.approx(1 / (m * n ** 1.5 * kap)) and r["D2"] == pytest.approx(1 / (m ** 0.5 * n ** 0.75 * kap))
+    assert r["D4"] == pytest.approx(1 / (20 * n ** 1.5 * kap ** 2))
+    assert r["D6"] == pytest.approx(1.0 / ((2.0 + n) * (n + 1)), rel=1e-12)
+    u = r["D7"]
+    gmn = m * n * u / (1 - m * n * u)
+    assert np.sqrt(m) * gmn * r["kappa_F"] == pytest.approx(r["gap"], rel=1e-12)
+    assert r["D8"] == pytest.approx(exact.constraints(A, ex)["constr2"], rel=1e-14)

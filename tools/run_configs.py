@@ -108,15 +108,32 @@ def main():
         res["runs"].append(rec)
         print(json.dumps(rec), flush=True)
     if want("cfg5"):
+        from oracle import exact
         for kappa in (1e2, 1e4, 1e6, 1e8):
             for eps in (1e-6, 1e-3, 1e-1):
                 P = tlsgen.config(f"cfg5:k{kappa:g}:e{eps:g}", device="cuda", keep_factors=False)
+                # the paper's constraint report D1-D8 (§3.1, oracle/exact.py) of this cell:
+                # singular values from the construction, sigma_{n+1} from the SVD of the R factor of
+                # [A, b], lambda_min(H) from the fp64 Gram (all on the GPU, not timed)
+                Ab = torch.cat([P.A, P.b[:, None]], dim=1)
+                Rab = torch.linalg.qr(Ab, mode="r")[1]
+                sig_np1 = float(torch.linalg.svdvals(Rab)[-1])
+                del Ab, Rab
+                G = P.A.T @ P.A
+                dd = 1.0 / torch.sqrt(torch.diagonal(G))
+                lmin = float(torch.linalg.eigvalsh(G * dd[:, None] * dd[None, :])[0])
+                del G
+                s = P.s
+                report = exact.constraint_report(P.m, P.n, s, sig_np1, float(np.linalg.norm(s)), lmin)
                 for u_f in ("fp16", "bf16", "fp32", "fp64"):
                     rec = dense(P, u_f, 1)
                     u = UROUND[u_f]
                     # constr1: u_f * kappa(A) <~ 1 for the factorization
                     rec.update({"config": "cfg5", "kappa": kappa, "eps": eps,
-                                "uf_times_kappa": u * kappa, "constr1_ok": u * kappa < 1.0})
+                                "uf_times_kappa": u * kappa, "constr1_ok": u * kappa < 1.0,
+                                "constraint_report": report,
+                                "bounds_met": [k for k in ("D1", "D2", "D3", "D4", "D5", "D6", "D7", "D8")
+                                               if u <= report[k]]})
                     sig = rec.get("sigma")
                     if sig is not None and math.isfinite(sig):
                         s_n = 1.0 / kappa
