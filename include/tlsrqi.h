@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define TLSRQI_ABI_VERSION 2
+#define TLSRQI_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define TLS_API __attribute__((visibility("default")))
@@ -138,7 +138,8 @@ typedef struct {
   int32_t launches;       /* kernels launched by the call (this library's kernels only) */
   int32_t pcg_steps;      /* RQI steps whose PCGTLS counts are in pcg_iters */
   double sigma_certified; /* compensated sigma of the returned x (opts.certify), else NaN */
-  int32_t reserved[2];
+  double* delta_min_trace;/* optional [2*(k-1)]: smallest curvature delta_j = p_j^T C p_j seen by solve (a) and
+                             (b) at each RQI step (the per-step trace of SURVEY §8(c) c2 step 9) */
 } tls_info_t;
 
 TLS_API int tls_abi_version(void);

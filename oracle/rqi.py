@@ -319,6 +319,7 @@ class RqiResult:
     breakdown_rhs: int = -1
     breakdown_j: int = -1
     passes: int = 0            # passes over A (unbatched) for perf accounting
+    delta_min_trace: List[tuple] = dataclasses.field(default_factory=list)   # c2 step 9
 
 
 def newton_residual(A, b: np.ndarray, x: np.ndarray):
@@ -419,6 +420,7 @@ def rqi_pcgtls_mp(A, b: np.ndarray, pc: Precond, tol: float = 1e-14,
         if variant == "A":
             passes += ra.count + rb.count + (ra.breakdown or ra.count < budget) + (rb.breakdown or rb.count < budget)
         res.pcg_iters.append((ra.count, rb.count))
+        res.delta_min_trace.append((ra.delta_min, rb.delta_min))
         if ra.breakdown or rb.breakdown:
             res.x, res.sigma = x, math.sqrt(sig2)
             res.status, res.termination = PCG_BREAKDOWN, T_BREAKDOWN

@@ -980,6 +980,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
 
   std::vector<double> s2tr, psitr;
   std::vector<int> pcgc;
+  std::vector<double> dmin;
   int status = TLS_OK, term = TLS_TERM_NONE, k = 1, crossed = 0, use_prev = 0;
   double psi_prev = 0.0, sig2_prev = NAN, sig2_ret = NAN;
   int bk = -1, brhs = -1, bj = -1;
@@ -1000,6 +1001,8 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
     } else {
       pcgc.push_back(hS.count[0]);
       pcgc.push_back(hS.count[1]);
+      dmin.push_back(hS.delta_min[0]);
+      dmin.push_back(hS.delta_min[1]);
       if (hS.brk[0] || hS.brk[1]) {                                // R3, R18 (step k - 1)
         status = TLS_PCG_BREAKDOWN;
         term = TLS_TERM_BREAKDOWN;
@@ -1081,6 +1084,8 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
       for (size_t i = 0; i < s2tr.size() && i < (size_t)o.max_outer + 1; ++i) info->sigma2_trace[i] = s2tr[i];
     if (info->psi_trace)
       for (size_t i = 0; i < psitr.size() && i < (size_t)o.max_outer + 1; ++i) info->psi_trace[i] = psitr[i];
+    if (info->delta_min_trace)
+      for (size_t i = 0; i < dmin.size() && i < 2 * (size_t)o.max_outer; ++i) info->delta_min_trace[i] = dmin[i];
   }
   return status;
 }

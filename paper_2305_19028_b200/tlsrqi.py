@@ -48,7 +48,7 @@ class tls_info_t(C.Structure):
                 ("breakdown_k", C.c_int32), ("breakdown_rhs", C.c_int32),
                 ("breakdown_j", C.c_int32), ("chol_pivot", C.c_int32), ("sigma2", C.c_double),
                 ("passes", C.c_int64), ("launches", C.c_int32), ("pcg_steps", C.c_int32),
-                ("sigma_certified", C.c_double), ("reserved", C.c_int32 * 2)]
+                ("sigma_certified", C.c_double), ("delta_min_trace", C.POINTER(C.c_double))]
 
 
 _lib = None
@@ -210,14 +210,16 @@ def _info(max_outer: int):
     pcg = (C.c_int32 * (2 * max_outer + 2))()
     s2 = (C.c_double * (max_outer + 2))()
     ps = (C.c_double * (max_outer + 2))()
+    dm = (C.c_double * (2 * max_outer + 2))()
     info.pcg_iters = C.cast(pcg, C.POINTER(C.c_int32))
     info.sigma2_trace = C.cast(s2, C.POINTER(C.c_double))
     info.psi_trace = C.cast(ps, C.POINTER(C.c_double))
-    return info, (pcg, s2, ps)
+    info.delta_min_trace = C.cast(dm, C.POINTER(C.c_double))
+    return info, (pcg, s2, ps, dm)
 
 
 def _info_dict(info: tls_info_t, bufs) -> dict:
-    pcg, s2, ps = bufs
+    pcg, s2, ps, dm = bufs
     k = max(int(info.rqi_iters), 0)
     npcg = max(int(info.pcg_steps), 0)
     return {
@@ -230,6 +232,7 @@ def _info_dict(info: tls_info_t, bufs) -> dict:
         "breakdown_j": int(info.breakdown_j), "chol_pivot": int(info.chol_pivot),
         "sigma2": float(info.sigma2), "passes": int(info.passes), "launches": int(info.launches),
         "sigma_certified": float(info.sigma_certified),
+        "delta_min_trace": [(dm[2 * i], dm[2 * i + 1]) for i in range(npcg)],
     }
 
 

@@ -572,3 +572,18 @@ def test_empty_row_block_csr(T):
     q = torch.ones((2, n), dtype=torch.float64, device="cuda")
     v, s = T.tls_pass(M, 0, q)
     assert float(v.abs().max()) == 0.0 and float(s.abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("name,fmt", [("cfg1", "fp16"), ("cfg2w", "bf16"), ("cfg2w", "fp64")])
+def test_delta_min_trace(T, name, fmt):
+    """The per-step trace of SURVEY §8(c) c2 step 9 includes delta_min of each PCGTLS
+    solve: GPU and oracle (same R~) agree per step and RHS to 1e-9 relative."""
+    P = tlsgen.config(name)
+    pc = rqi.factor_precond(P.A, fmt)
+    res = rqi.rqi_pcgtls_mp(P.A, P.b, pc)
+    R = T.tls_precond_import(pc.Rt, pc.d, pc.normA2, fmt)
+    rc, x, sig, info = T.tls_rqi_pcgtls(T.matrix(dev(P.A)), dev(P.b), R)
+    assert len(info["delta_min_trace"]) == len(res.delta_min_trace) > 0
+    for g, o in zip(info["delta_min_trace"], res.delta_min_trace):
+        for r in range(2):
+            assert g[r] == pytest.approx(o[r], rel=1e-9)
