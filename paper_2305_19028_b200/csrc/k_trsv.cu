@@ -368,19 +368,22 @@ __device__ __forceinline__ void pre_apply(const PrecondDev& pc, TrsvSm& sm) {
 
 // W = R~^{-1} by block columns (R24): W_JJ = R~_JJ^{-1} (the DinvB blocks), then for
 // I = J-1 .. 0: W_IJ = -R~_II^{-1} sum_{K=I+1..J} R~_IK W_KJ.  CTA (J, c) owns 4 columns of
-// block column J and keeps their strip of W in shared memory.  Warp w takes the blocks
+// block column J and keeps their strip of W in shared memory (DinvB_I staged by cp.async).  Warp w takes the blocks
 // K = I+1+w, I+1+w+8, ...; lane r multiplies the 32-element segment of row 32I+r of R~_IK
 // (one vector load, the next one in flight) into the strip; the 8 warp partials are summed
 // in fixed order and the 32 x 32 inverse is applied.  W, WT zeroed beforehand; WT = W^T.
+constexpr int kTriW = 8, kTriT = kTriW * 32;   // warps of k_trtri: warp w takes every 8th block K (16 measured slower)
+
 template <typename T>
-__global__ void __launch_bounds__(256) k_trtri(PrecondDev pc, double* __restrict__ W, double* __restrict__ WT) {
+__global__ void __launch_bounds__(kTriT) k_trtri(PrecondDev pc, double* __restrict__ W, double* __restrict__ WT) {
   constexpr int NV = SegTraits<T>::NV;
   extern __shared__ double wsm[];
   const int npad = pc.npad;
   const int J = blockIdx.x >> 3, c0 = (blockIdx.x & 7) * 4;
   double* Wc = wsm;                          // [npad][4]
-  double* Tp = Wc + (size_t)npad * 4;        // [8][32][4] partials
-  double* Tf = Tp + 8 * 32 * 4;              // [32][4]
+  double* Tp = Wc + (size_t)npad * 4;        // [kTriW][32][4] partials
+  double* Tf = Tp + kTriW * 32 * 4;          // [32][4]
+  double* Di = Tf + 32 * 4;                  // [1024] DinvB block of the current I (staged by cp.async)
   const int tid = threadIdx.x, w = tid >> 5, r = tid & 31;
   const T* R = reinterpret_cast<const T*>(pc.Rrow);
   if (tid < 128) {                           // DinvB[kb][l][i] = (R~_kk^{-1})[i][l]
@@ -392,13 +395,17 @@ __global__ void __launch_bounds__(256) k_trtri(PrecondDev pc, double* __restrict
   }
   __syncthreads();
   for (int I = J - 1; I >= 0; --I) {
+    // the 32 x 32 inverse of block I arrives while the products are formed
+#pragma unroll
+    for (int k = tid; k < 512; k += kTriT) cp_async16(Di + 2 * k, pc.DinvB + (size_t)I * 1024 + 2 * k);
+    cp_async_commit();
     const T* Rr = R + (size_t)(32 * I + r) * npad;
     double a[4] = {0.0, 0.0, 0.0, 0.0};
     uint4 cur[NV], nxt[NV];
     int K = I + 1 + w;
     if (K <= J) seg_load<T>(Rr + 32 * K, cur);
-    for (; K <= J; K += 8) {
-      if (K + 8 <= J) seg_load<T>(Rr + 32 * (K + 8), nxt);
+    for (; K <= J; K += kTriW) {
+      if (K + kTriW <= J) seg_load<T>(Rr + 32 * (K + kTriW), nxt);
       const double* wk = Wc + (size_t)(32 * K) * 4;
 #pragma unroll
       for (int l = 0; l < 32; ++l) {
@@ -414,12 +421,13 @@ __global__ void __launch_bounds__(256) k_trtri(PrecondDev pc, double* __restrict
     }
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) Tp[(w * 32 + r) * 4 + cc] = a[cc];
+    cp_async_wait<0>();
     __syncthreads();
     if (tid < 128) {
       const int rr = tid >> 2, cc = tid & 3;
       double t = 0.0;
 #pragma unroll
-      for (int h = 0; h < 8; ++h) t += Tp[(h * 32 + rr) * 4 + cc];
+      for (int h = 0; h < kTriW; ++h) t += Tp[(h * 32 + rr) * 4 + cc];
       Tf[rr * 4 + cc] = t;
     }
     __syncthreads();
@@ -427,7 +435,7 @@ __global__ void __launch_bounds__(256) k_trtri(PrecondDev pc, double* __restrict
       const int rr = tid >> 2, cc = tid & 3;
       double s = 0.0;
 #pragma unroll 8
-      for (int l = 0; l < 32; ++l) s = fma(pc.DinvB[(size_t)I * 1024 + l * 32 + rr], Tf[l * 4 + cc], s);
+      for (int l = 0; l < 32; ++l) s = fma(Di[l * 32 + rr], Tf[l * 4 + cc], s);
       Wc[(32 * I + rr) * 4 + cc] = -s;
       W[(size_t)(32 * I + rr) * npad + 32 * J + c0 + cc] = -s;
       WT[(size_t)(32 * J + c0 + cc) * npad + 32 * I + rr] = -s;
@@ -1142,7 +1150,7 @@ int launch_boot_x1(const PrecondDev& pc, const double* passout_r0, const double*
 }
 
 int launch_trtri(const PrecondDev& pc, double* W, double* WT, cudaStream_t st) {
-  const size_t smem = (size_t)pc.npad * 4 * 8 + 9 * 32 * 4 * 8;
+  const size_t smem = (size_t)pc.npad * 4 * 8 + (kTriW + 1) * 32 * 4 * 8 + 1024 * 8;
   TLS_CUDA_TRY(cudaMemsetAsync(W, 0, (size_t)pc.npad * pc.npad * 8, st));
   TLS_CUDA_TRY(cudaMemsetAsync(WT, 0, (size_t)pc.npad * pc.npad * 8, st));
   int rc = 0;
@@ -1152,7 +1160,7 @@ int launch_trtri(const PrecondDev& pc, double* W, double* WT, cudaStream_t st) {
       TLS_CUDA_TRY(cudaFuncSetAttribute(k_trtri<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr = smem;
     }
-    k_trtri<T><<<(pc.npad / 32) * 8, 256, smem, st>>>(pc, W, WT);
+    k_trtri<T><<<(pc.npad / 32) * 8, kTriT, smem, st>>>(pc, W, WT);
   });
   TLS_LAUNCH_CHECK();
   return rc;
