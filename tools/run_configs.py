@@ -26,8 +26,11 @@ from paper_2305_19028_b200 import tlsrqi as T
 UROUND = {"fp16": 2.0 ** -11, "bf16": 2.0 ** -8, "fp32": 2.0 ** -24, "fp64": 2.0 ** -53}
 
 
+EXTRA = {}   # --opts k=v,... applied to every solve (e.g. u_p=2,precond_apply=2)
+
+
 def run(M, b, u_f, reps, ws, op_variant=0):
-    opts = T.tls_rqi_opts_default(op_variant=op_variant)
+    opts = T.tls_rqi_opts_default(op_variant=op_variant, **EXTRA)
     def once():
         rc, R, fi = T.tls_factor_precond(M, u_f, ws=ws)
         if R is None:
@@ -73,10 +76,14 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--out", default="gpurun_out/configs.json")
+    ap.add_argument("--opts", default="", help="tls_rqi_opts_t overrides, e.g. u_p=2,precond_apply=2")
     args = ap.parse_args()
+    for kv in filter(None, args.opts.split(",")):
+        k, v = kv.split("=")
+        EXTRA[k] = float(v) if "." in v or "e" in v else int(v)
     only = set(args.only.split(",")) if args.only else None
     res = {"gpu": torch.cuda.get_device_name(0), "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
-           "runs": []}
+           "opts": EXTRA, "runs": []}
 
     def want(k):
         return only is None or k in only
