@@ -123,6 +123,10 @@ def oracle_sample(A_np, b_np, u_f, counts, row_scale=16, iters=2):
     t0 = time.perf_counter()
     pc = orq.factor_precond(A_np[:blk], u_f)
     t_factor = (time.perf_counter() - t0) * (m / blk)
+    if pc.status != orq.OK:
+        # the row sample can be too short for a positive definite u_f Gram (small m): time the
+        # iterations with an identity R~ instead (their cost does not depend on R~'s values)
+        pc = orq.Precond(np.eye(n), np.ones(n), u_f, 1.0)
     f = np.ones(n)
     t0 = time.perf_counter()
     orq.pcgtls(A_np, pc, 0.0, f, iters, 0.0, "A")
