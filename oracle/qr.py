@@ -1,0 +1,54 @@
+"""Householder QR computed in a low precision u_q (oracle; TEST INFRASTRUCTURE ONLY, see
+oracle/__init__.py).  Groundwork for SURVEY §8(f) NEXT-2: the paper's preferred
+preconditioner is the R factor of a Householder QR of A computed in precision u_q
+("Compute A = Q[R 0]^T in u_q", l.276-288); the GPU path of
+this round uses the Cholesky of the u_f Gram instead (DESIGN R10).
+
+The arithmetic follows the textbook algorithm (Golub & Van Loan Alg. 5.1.1 / Higham
+§19.1) with every elementary vector operation rounded to u_q, the way the paper's
+`chop` simulation rounds every operation (SPEC.md householder_qr):
+for j = 0 .. n-1 (x = A[j:, j]):
+    sigma = fl(||x||)             (dot product rounded, then a rounded square root)
+    alpha = -sign(x_0) sigma       (the sign that avoids cancellation)
+    v = x - alpha e_0, rounded;   beta = fl(2 / fl(v^T v))
+    A[j:, j:] -= v (beta (v^T A[j:, j:]))   each of the three steps rounded
+and R is the upper triangle with its rows' signs flipped so that diag(R) >= 0 (SPEC.md
+"Sign convention").  Q is never formed.  Reading (R25): inner products are accumulated
+in fp64 and rounded once (a wide accumulator, as on tensor cores), every elementwise
+operation is rounded on its own.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .rounding import round_to
+
+
+def householder_qr_r(A: np.ndarray, fmt: str) -> np.ndarray:
+    """R (n x n, upper, diag >= 0) of the Householder QR of A with every operation
+    rounded to fmt.  A is first rounded to fmt.  Raises ZeroDivisionError on an exactly
+    zero column (rank deficiency, SPEC.md householder_qr errors)."""
+    rd = lambda x: round_to(np.asarray(x, dtype=np.float64), fmt)
+    W = rd(np.array(A, dtype=np.float64, copy=True))
+    m, n = W.shape
+    if m < n:
+        raise ValueError("householder_qr_r needs m >= n")
+    for j in range(n):
+        x = W[j:, j]
+        sigma = float(rd(np.sqrt(rd(np.dot(x, x)))))
+        if sigma == 0.0:
+            raise ZeroDivisionError(f"zero column {j}")
+        alpha = -sigma if x[0] >= 0 else sigma
+        v = x.copy()
+        v[0] = float(rd(x[0] - alpha))
+        vv = float(rd(np.dot(v, v)))
+        beta = float(rd(2.0 / vv))
+        # W[j:, j:] -= v (beta (v^T W[j:, j:]))
+        wT = rd(v @ W[j:, j:])
+        wT = rd(beta * wT)
+        W[j:, j:] = rd(W[j:, j:] - rd(np.outer(v, wT)))
+        W[j, j] = alpha
+        W[j + 1:, j] = 0.0
+    R = np.triu(W[:n, :n])
+    sgn = np.where(np.diag(R) < 0, -1.0, 1.0)
+    return R * sgn[:, None]

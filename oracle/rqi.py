@@ -159,6 +159,24 @@ class Precond:
     W: Optional[np.ndarray] = None   # explicit inverse of R~ when the solve applies it (R24)
 
 
+def factor_precond_qr(A, u_f: str) -> Precond:
+    """The paper's preferred preconditioner: R~ = the R factor
+    of a Householder QR of A D^{-1} computed with every operation in u_f (oracle/qr.py,
+    reading R25), the same power-of-two scaling D as the Cholesky route.  Oracle only in
+    this round (the GPU path factors the Gram)."""
+    from .qr import householder_qr_r
+    A_d = A.toarray() if _is_sparse(A) else np.asarray(A)
+    n = A_d.shape[1]
+    d, normA2 = column_scaling(A)
+    try:
+        Rt = householder_qr_r(A_d / d, u_f)
+    except ZeroDivisionError:
+        return Precond(np.zeros((n, n)), d, u_f, normA2, CHOL_BREAKDOWN, 1)
+    if not np.all(np.isfinite(Rt)) or np.any(np.diag(Rt) == 0):
+        return Precond(Rt, d, u_f, normA2, RANGE)
+    return Precond(Rt, d, u_f, normA2, OK)
+
+
 def factor_precond(A, u_f: str, K_t: int = 64, keep: bool = False) -> Precond:
     """tls_factor_precond: scaling, u_f Gram, fp64 Cholesky G = R^T R (LAPACK
     dpotrf, upper), R~ = fl_uf(R)  (PAPER.md l.231 with the Cholesky route of

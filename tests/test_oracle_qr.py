@@ -1,0 +1,73 @@
+"""Pins of oracle/qr.py (Householder QR in u_q; SURVEY §8(f) NEXT-2 groundwork):
+SPEC.md's worked examples, LAPACK agreement in fp64, the Gram residual bound in low
+precision, and the paper's point that QR depends on kappa where the Gram Cholesky
+depends on kappa^2."""
+import numpy as np
+import pytest
+
+from oracle.qr import householder_qr_r
+from oracle.rounding import round_to, unit_roundoff
+
+
+def test_spec_examples():
+    """SPEC.md householder_qr examples: QR(I_n) = I_n; QR([3;4]) = [5]."""
+    assert np.array_equal(householder_qr_r(np.eye(5), "fp64"), np.eye(5))
+    assert householder_qr_r(np.array([[3.0], [4.0]]), "fp64")[0, 0] == 5.0
+
+
+def test_fp64_matches_lapack():
+    """In fp64 the R factor equals LAPACK's (numpy.linalg.qr) up to row signs."""
+    rng = np.random.default_rng(4)
+    A = rng.standard_normal((20, 10))
+    R = householder_qr_r(A, "fp64")
+    Rl = np.linalg.qr(A, mode="r")
+    Rl = Rl * np.where(np.diag(Rl) < 0, -1.0, 1.0)[:, None]
+    assert np.allclose(R, Rl, rtol=1e-13, atol=1e-13)
+    assert np.all(np.diag(R) >= 0)
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16", "fp32"])
+def test_gram_residual_bound(fmt):
+    """SPEC.md invariant 'QR residual <= 10 m n u' in Gram form (Q is not formed):
+    ||R^T R - Ah^T Ah||_F <= 10 m n u ||Ah||_F^2 with Ah = fl(A)."""
+    rng = np.random.default_rng(5)
+    m, n = 60, 12
+    A = round_to(rng.standard_normal((m, n)), fmt)
+    R = householder_qr_r(A, fmt)
+    u = unit_roundoff(fmt)
+    assert np.linalg.norm(R.T @ R - A.T @ A) <= 10 * m * n * u * np.linalg.norm(A) ** 2
+
+
+def test_qr_needs_kappa_where_cholesky_needs_kappa_squared():
+    """PAPER.md l.276-297 / SPEC.md cholesky_scaled example: with kappa(A)^2 > 1/u_fp16
+    but u_fp16 kappa(A) < 1, the Cholesky of the fp16-rounded Gram fl(A^T A) (the unscaled
+    pathway) breaks down while the fp16 Householder R is nonsingular and preconditions A
+    (kappa(A R^{-1}) small)."""
+    rng = np.random.default_rng(6)
+    m, n = 80, 10
+    U, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    kappa = 300.0                      # kappa^2 = 9e4 > 1/u = 2048; u kappa = 0.15
+    A = (U * np.logspace(0, -np.log10(kappa), n)) @ V.T
+    G16 = round_to(round_to(A, "fp16").T @ round_to(A, "fp16"), "fp16")
+    with pytest.raises(np.linalg.LinAlgError):
+        np.linalg.cholesky(G16)
+    R = householder_qr_r(A, "fp16")
+    assert np.min(np.abs(np.diag(R))) > 0
+    assert np.linalg.cond(A @ np.linalg.inv(R)) < 10.0
+
+
+@pytest.mark.parametrize("name", ["cfg1", "random", "vanhuffel", "toeplitz"])
+def test_rqi_with_qr_preconditioner(name):
+    """RQI-PCGTLS-MP with the paper's own preconditioner (fp16 Householder R, PAPER.md
+    l.231) reaches the SVD's x and sigma like the Cholesky route does."""
+    import tlsgen
+    from oracle import exact, rqi
+    P = tlsgen.config(name) if name.startswith("cfg") else tlsgen.paper_problem(name)
+    ex = exact.tls_svd(P.A, P.b)
+    pc = rqi.factor_precond_qr(P.A, "fp16")
+    assert pc.status == rqi.OK
+    r = rqi.rqi_pcgtls_mp(P.A, P.b, pc)
+    assert r.status == rqi.OK
+    assert np.linalg.norm(r.x - ex.x) / np.linalg.norm(ex.x) <= 1e-12
+    assert abs(r.sigma - ex.sigma) / ex.sigma <= 1e-12
