@@ -108,3 +108,54 @@ def test_row_sharded_passes_world2():
         assert r["normA2_rel"] < 1e-14
         for k in ("op_rel_0", "op_rel_1", "tau_rel_0", "tau_rel_1", "resid_rel", "rho_rel"):
             assert r[k] < 1e-13, (k, r[k])
+
+
+class _LVec(np.ndarray):
+    """A rank's rows of an m-vector: the inner product of two of them is all-reduced."""
+
+    def __matmul__(self, other):
+        return float(_allreduce(np.array([np.dot(np.asarray(self), np.asarray(other))]))[0])
+
+
+def _solve_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        P = tlsgen.config("cfg2w", m=1024, n=96)
+        A, b = P.A, P.b
+        m, n = A.shape
+        pc = rqi.factor_precond(A, "fp16")          # replicated factorization of the reduced Gram
+        ref = rqi.rqi_pcgtls_mp(A, b, pc)
+        lo, hi = shard_rows(m, world, rank)
+        Al = np.ascontiguousarray(A[lo:hi])
+        bl = np.ascontiguousarray(b[lo:hi]).view(_LVec)
+        # the library's sharded structure: A q and b - A x stay local, A^T t and every
+        # inner product of m-vectors are all-reduced, all n-vector work is replicated
+        rqi.matvec = lambda _A, x: np.asarray(Al @ np.asarray(x)).view(_LVec)
+        rqi.rmatvec = lambda _A, t: _allreduce(Al.T @ np.asarray(t))
+        res = rqi.rqi_pcgtls_mp(Al, bl, pc)
+        xs = [torch.zeros(n, dtype=torch.float64) for _ in range(world)]
+        tdist.all_gather(xs, torch.from_numpy(np.asarray(res.x, dtype=np.float64)))
+        out[rank] = {"same": (res.status, res.termination, res.rqi_iters, res.boot_iters, res.pcg_iters) ==
+                             (ref.status, ref.termination, ref.rqi_iters, ref.boot_iters, ref.pcg_iters),
+                     "x_rel": float(np.linalg.norm(res.x - ref.x) / np.linalg.norm(ref.x)),
+                     "sig_rel": abs(res.sigma - ref.sigma) / ref.sigma,
+                     "replicas": all(torch.equal(xs[0], v) for v in xs)}
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_row_sharded_solve_world2():
+    """The whole RQI-PCGTLS-MP solve on two row shards over gloo (the N > 1 structure of
+    SURVEY §8(e)) gives the unsharded oracle's status and counts, x and sigma to roundoff,
+    and bit-identical x on both ranks."""
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_solve_worker, args=(world, port, out), nprocs=world, join=True)
+    for rank in range(world):
+        r = out[rank]
+        assert r["same"] and r["replicas"]
+        assert r["x_rel"] < 1e-12 and r["sig_rel"] < 1e-13
