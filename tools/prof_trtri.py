@@ -1,5 +1,6 @@
+"""Profiling driver: forming W = R~^{-1} (k_trtri) for n = 1024 and 2048 through tls_precond_apply.  Used under ncu."""
 import os, sys
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, tlsgen
 from paper_2305_19028_b200 import tlsrqi as T
 for n in (1024, 2048):
