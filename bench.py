@@ -411,6 +411,15 @@ def main():
         with open(os.path.join(ROOT, "profiles", f"counts_{wl}.json"), "w") as fh:
             json.dump({"K": info["rqi_iters"], "B0": info["boot_iters"], "pcg": info["pcg_iters"]}, fh)
 
+    # the compensated certificate of the returned x (c2 step 8), one extra untimed solve
+    rc_c, R_c, _ = tlsrqi.tls_factor_precond(M, u_f, comm=comm, stream=stream, ws=ws)
+    sig_cert = None
+    if R_c is not None:
+        _, _, _, inf_c = tlsrqi.tls_rqi_pcgtls(M, b_loc, R_c, comm=comm, stream=stream, ws=ws, x_out=x,
+                                               opts=tlsrqi.tls_rqi_opts_default(certify=1))
+        sig_cert = inf_c["sigma_certified"]
+        del R_c
+
     # TTS as a model: the step's passes over A at the HBM peak plus the
     # measured time of everything that is not a pass (Gram, Cholesky, PCG steps, ...)
     pass_cats = ("pass_op2", "pass_op1", "pass_resid", "colstats", "pass_op2_fp32", "reduce")
@@ -546,7 +555,7 @@ def main():
                        "parallelism": f"row-shard x{world} (NCCL all-reduce)"},
             "status": info["status_name"], "termination": info["termination_name"],
             "rqi_iters": info["rqi_iters"], "boot_iters": info["boot_iters"], "pcg_iters": info["pcg_iters"],
-            "sigma": sig, "pcg_iters_per_s": pcg_per_solve / tts,
+            "sigma": sig, "sigma_certified": sig_cert, "pcg_iters_per_s": pcg_per_solve / tts,
             # passes over A that do work: colstats + Gram read + setup + bootstrap CGLS + r_0
             # + one residual pass per RQI step + one batched operator pass per PCG iteration
             "a_passes_per_step": a_passes,
