@@ -63,3 +63,35 @@ def test_argument_validation_without_gpu(L):
     assert L.tls_workspace_size(C.byref(M), 50) == 0
     M.ld, M.vals = 4, 256
     assert L.tls_workspace_size(C.byref(M), 50) > 0
+
+
+def test_ctypes_layouts_equal_the_c_compiler(L, tmp_path):
+    """The binding's ctypes structures have the sizes and field offsets that gcc gives the
+    header's structs (the ABI of include/tlsrqi.h, checked without a GPU)."""
+    import shutil
+    import subprocess
+    from paper_2305_19028_b200 import tlsrqi
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    structs = {"tls_matrix_t": tlsrqi.tls_matrix_t, "tls_rqi_opts_t": tlsrqi.tls_rqi_opts_t,
+               "tls_info_t": tlsrqi.tls_info_t}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "tlsrqi.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'  printf("{name} size %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'  printf("{name} {f} %zu\\n", offsetof({name}, {f}));')
+    lines.append(f'  printf("abi %d\\n", TLSRQI_ABI_VERSION);')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = {}
+    for ln in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        *k, v = ln.split()
+        got[" ".join(k)] = int(v)
+    for name, cls in structs.items():
+        assert got[f"{name} size"] == C.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert got[f"{name} {f}"] == getattr(cls, f).offset, (name, f)
+    assert got["abi"] == L.tls_abi_version()
