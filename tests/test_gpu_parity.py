@@ -587,3 +587,33 @@ def test_delta_min_trace(T, name, fmt):
     for g, o in zip(info["delta_min_trace"], res.delta_min_trace):
         for r in range(2):
             assert g[r] == pytest.approx(o[r], rel=1e-9)
+
+
+@pytest.mark.parametrize("opt", [dict(certify=1), dict(precond_apply=2), dict(u_p=2)])
+def test_solve_host_with_options(T, opt):
+    """The host-buffer end-to-end entry takes the same options as the device path and gives
+    the same status, counts, x and sigma (and the certificate)."""
+    P = tlsgen.config("cfg2w")
+    A_h = torch.as_tensor(P.A).pin_memory()
+    b_h = torch.as_tensor(P.b).pin_memory()
+    o = T.tls_rqi_opts_default(**opt)
+    rc, x, sig, info = T.tls_solve_host(A_h, b_h, "bf16", opts=o)
+    M = T.matrix(dev(P.A))
+    rc2, R, _ = T.tls_factor_precond(M, "bf16")
+    rc2, x2, sig2, info2 = T.tls_rqi_pcgtls(M, dev(P.b), R, opts=o)
+    assert rc == rc2 == 0
+    assert info["rqi_iters"] == info2["rqi_iters"] and info["pcg_iters"] == info2["pcg_iters"]
+    assert _rel(x.numpy(), x2.cpu().numpy()) <= 1e-12 and abs(sig - sig2) / sig2 <= 1e-13
+    if "certify" in opt:
+        assert abs(info["sigma_certified"] - sig) / sig <= 1e-12
+
+
+def test_up_fp32_refuses_csr(T):
+    """u_p = fp32 needs the dense fp32 copy: a CSR A is refused with ERR_UNSUPPORTED."""
+    P = tlsgen.config("cfg3", m=2000, n=100)
+    M = T.matrix_csr(torch.as_tensor(P.rowptr, device="cuda"), torch.as_tensor(P.colidx, device="cuda"),
+                     torch.as_tensor(P.vals, device="cuda"), P.n)
+    rc, R, _ = T.tls_factor_precond(M, "fp16")
+    with pytest.raises(T.TlsError) as e:
+        T.tls_rqi_pcgtls(M, torch.as_tensor(P.b, device="cuda"), R, opts=T.tls_rqi_opts_default(u_p=2))
+    assert e.value.rc == -5
