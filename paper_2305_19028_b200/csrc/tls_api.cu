@@ -932,7 +932,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
                                 pass_rhs, cx.st));
       }
       cx.launches += 1;
-      if (budget > 16 && (j % 8) == 7) {
+      if (budget > 16 && (j == 3 || (j % 8) == 7)) {   // first poll early: small bootstraps skip no-op launches
         int act[2] = {0, 0};
         TLS_CUDA_TRY(cudaMemcpyAsync(act, w.S->active, sizeof(act), cudaMemcpyDeviceToHost, cx.st));
         TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
