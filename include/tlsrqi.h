@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define TLSRQI_ABI_VERSION 3
+#define TLSRQI_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define TLS_API __attribute__((visibility("default")))
@@ -167,6 +167,20 @@ TLS_API size_t tls_workspace_size(const tls_matrix_t* A, int32_t max_outer);
 TLS_API int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t* opts,
                        tls_comm_t comm, void* stream, void* ws_dev, size_t ws_bytes,
                        tls_precond_t* R_out, tls_info_t* info);
+
+/* ---- the paper's preferred preconditioner: Householder QR in u_f ----
+ * PAPER.md l.215-218 and Alg. 4 l.231 "Compute A = Q[R 0]^T in u_q"; reading R25.
+ * R~ = the R factor (diag >= 0) of a Householder QR of fl_uf(A D^{-1}), with the same D
+ * and ||A||_F^2 as tls_factor_precond; every elementwise operation is rounded to u_f, inner
+ * products are accumulated in fp64 and rounded once.  The returned handle is used exactly
+ * like a Cholesky one.  Dense A on one GPU only (CSR, or a comm of more than one rank:
+ * TLS_ERR_ARG).  ws_dev: ws_bytes >= tls_qr_workspace_size(A, u_f) bytes (it holds an m x n
+ * fp32 -- fp64 for u_f = TLS_FP64 -- working copy of A).  A column that becomes exactly zero
+ * in u_f: TLS_CHOL_BREAKDOWN, info->chol_pivot = its 1-based index, *R_out = NULL.
+ * A reflector overflowing u_f: TLS_RANGE. */
+TLS_API size_t tls_qr_workspace_size(const tls_matrix_t* A, int32_t u_f);
+TLS_API int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, void* stream, void* ws_dev,
+                                  size_t ws_bytes, tls_precond_t* R_out, tls_info_t* info);
 
 /* Handle from host data (tests: import the oracle's R~ to isolate PCG/RQI
  * parity).  Rt_host: n x n row-major upper-triangular values already

@@ -24,6 +24,14 @@ import numpy as np
 from .rounding import round_to
 
 
+class ZeroColumn(ZeroDivisionError):
+    """Column `col` (0-based) is exactly zero below its diagonal position in fmt."""
+
+    def __init__(self, col: int):
+        super().__init__(f"zero column {col}")
+        self.col = col
+
+
 def householder_qr_r(A: np.ndarray, fmt: str) -> np.ndarray:
     """R (n x n, upper, diag >= 0) of the Householder QR of A with every operation
     rounded to fmt.  A is first rounded to fmt.  Raises ZeroDivisionError on an exactly
@@ -37,7 +45,7 @@ def householder_qr_r(A: np.ndarray, fmt: str) -> np.ndarray:
         x = W[j:, j]
         sigma = float(rd(np.sqrt(rd(np.dot(x, x)))))
         if sigma == 0.0:
-            raise ZeroDivisionError(f"zero column {j}")
+            raise ZeroColumn(j)
         alpha = -sigma if x[0] >= 0 else sigma
         v = x.copy()
         v[0] = float(rd(x[0] - alpha))

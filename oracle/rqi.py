@@ -170,8 +170,8 @@ def factor_precond_qr(A, u_f: str) -> Precond:
     d, normA2 = column_scaling(A)
     try:
         Rt = householder_qr_r(A_d / d, u_f)
-    except ZeroDivisionError:
-        return Precond(np.zeros((n, n)), d, u_f, normA2, CHOL_BREAKDOWN, 1)
+    except ZeroDivisionError as e:   # 1-based index of the vanishing column (tlsrqi.h chol_pivot)
+        return Precond(np.zeros((n, n)), d, u_f, normA2, CHOL_BREAKDOWN, getattr(e, "col", 0) + 1)
     if not np.all(np.isfinite(Rt)) or np.any(np.diag(Rt) == 0):
         return Precond(Rt, d, u_f, normA2, RANGE)
     return Precond(Rt, d, u_f, normA2, OK)

@@ -1,0 +1,280 @@
+// k_qr.cu — the paper's preferred preconditioner on the GPU: R~ = the R factor of a
+// Householder QR of A D^{-1} computed in u_f (PAPER.md l.215-218,
+// l.231 "Compute A = Q[R 0]^T in u_q", l.276-288; reading R25).
+//
+// Arithmetic (R25): every elementwise operation is rounded to u_f on its own, inner
+// products are accumulated in fp64 and rounded once (a wide accumulator).  Per column j
+// (x = W[j:, j]):
+//     sigma = fl(sqrt(fl(x^T x))),  alpha = -sign(x_0) sigma,  v = x - alpha e_0 (v_0 rounded),
+//     beta = fl(2 / fl(v^T v)),     w^T = fl(beta fl(v^T W[j:, j+1:])),
+//     W[j:, j+1:] = fl(W - fl(v w^T))                      (each product and difference rounded)
+// and R row j = sign(alpha) [alpha, W[j, j+1:]] (diag(R) >= 0).
+//
+// B200 design: W = fl_uf(A D^{-1}) lives row-major in HBM as fp32 (exact for fp16/bf16/fp32
+// values) or fp64 (u_f = fp64).  One column costs ONE streaming pass over the trailing
+// matrix: k_qr_step updates rows >= j with column j's reflector and, in the same pass,
+// accumulates the fp64 partial inner products of the NEXT column (x'^T x' and x'^T W')
+// per CTA, so column j+1's reflector needs no second pass; k_qr_fin reduces those partials
+// (fixed order, deterministic), forms the column's scalars and w^T.  2 launches per column.
+#include "tls_common.cuh"
+#include "tls_kernels.h"
+
+namespace tls {
+
+namespace {
+constexpr int kQrThreads = 256;
+
+template <typename T> __device__ __forceinline__ T qr_store(double v);
+template <> __device__ __forceinline__ float qr_store<float>(double v) { return (float)v; }   // exact: v in u_f
+template <> __device__ __forceinline__ double qr_store<double>(double v) { return v; }
+
+// scal[j]: {alpha, v_0, sigma, beta}
+// One pass.  LOAD: W = fl_uf(A D^{-1}) and the partials of column 0.  Otherwise: apply
+// column j's reflector to rows >= j, columns > j, write R row j, and accumulate the partials
+// of column c = j + 1 over rows > c: partP[b][k] = sum_i x'_i W'[i][k] for k >= c (k = c is
+// the tail x'^T x' of the column below its diagonal).
+// A CTA owns RB rows; it runs `teams` rows at a time, one team of TG threads per row (CPT
+// columns per thread, k = c + tl + q TG), with the next row of each team loaded before the
+// current one is stored.  Team partials are combined in shared memory in team order.
+template <typename T, bool LOAD, int CPT>
+__device__ __forceinline__ void qr_load_row(const T* __restrict__ W, const double* __restrict__ A, int64_t lda,
+                                            int64_t i, int n, int j, int c, int tl, int TG, double (&dst)[CPT],
+                                            double& sj, double& sc) {
+  if (LOAD) {
+    const double* src = A + i * lda;
+    sc = src[0];
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      const int k = c + tl + q * TG;
+      dst[q] = k < n ? src[k] : 0.0;
+    }
+  } else {
+    const T* src = W + i * (int64_t)n;
+    sj = (i == j) ? 0.0 : (double)src[j];
+    sc = c < n ? (double)src[c] : 0.0;
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      const int k = c + tl + q * TG;
+      dst[q] = k < n ? (double)src[k] : 0.0;
+    }
+  }
+}
+
+template <typename T, bool LOAD, int CPT>
+__global__ void __launch_bounds__(kQrThreads) k_qr_step(T* __restrict__ W, const double* __restrict__ A, int64_t lda,
+                                                         const double* __restrict__ dinv, int64_t m, int n, int j,
+                                                         int RB, int bfirst, int TG, int prec,
+                                                         const double* __restrict__ wT,
+                                                         const double* __restrict__ scal, double* __restrict__ partP,
+                                                         double* __restrict__ G, const int* __restrict__ dead) {
+  extern __shared__ double qsm[];
+  if (!LOAD && *dead) return;
+  const int c = j + 1;
+  const int ncols = n - c;
+  const int64_t rs = LOAD ? 0 : j;
+  const int b = bfirst + (int)blockIdx.x;
+  int64_t r0 = (int64_t)b * RB;
+  const int64_t r1 = min(m, r0 + RB);
+  if (r1 <= rs) return;                 // rows all above: k_qr_fin does not read this CTA
+  if (r0 < rs) r0 = rs;
+  const int t = threadIdx.x, tm = t / TG, tl = t % TG, teams = blockDim.x / TG;
+  double wk[CPT], acc[CPT], cur[CPT], nxt[CPT];
+  const double alpha = LOAD ? 0.0 : scal[4 * j + 0];
+  const double v0 = LOAD ? 0.0 : scal[4 * j + 1];
+  const double wc = LOAD ? dinv[0] : (c < n ? wT[c] : 0.0);     // LOAD: the scale of column 0
+#pragma unroll
+  for (int q = 0; q < CPT; ++q) {
+    const int k = c + tl + q * TG;
+    wk[q] = k < n ? (LOAD ? dinv[k] : wT[k]) : 0.0;             // LOAD: the column scales
+    acc[q] = 0.0;
+  }
+  int64_t i = r0 + tm;
+  bool have = i < r1;
+  double nj = 0.0, nc = 0.0;
+  if (have) qr_load_row<T, LOAD, CPT>(W, A, lda, i, n, j, c, tl, TG, nxt, nj, nc);
+  while (have) {
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) cur[q] = nxt[q];
+    const double cj = nj, cc = nc;
+    const int64_t inext = i + teams;
+    const bool hn = inext < r1;
+    if (hn) qr_load_row<T, LOAD, CPT>(W, A, lda, inext, n, j, c, tl, TG, nxt, nj, nc);
+    T* row = W + i * (int64_t)n;
+    double xc, vi = 0.0;   // xc: new value of column c in this row (same bits in every thread)
+    if (LOAD) {
+      xc = round_uf(cc * wc, prec);
+    } else {
+      vi = (i == j) ? v0 : cj;
+      xc = round_uf(cc - round_uf(vi * wc, prec), prec);
+    }
+    const bool accum = i > c;
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      const int k = c + tl + q * TG;
+      if (k < n) {
+        const double nv = LOAD ? round_uf(cur[q] * wk[q], prec)
+                               : round_uf(cur[q] - round_uf(vi * wk[q], prec), prec);
+        row[k] = qr_store<T>(nv);
+        if (accum) acc[q] = fma(xc, nv, acc[q]);
+        if (!LOAD && i == j) G[(int64_t)j * n + k] = alpha < 0.0 ? -nv : nv;
+      }
+    }
+    i = inext;
+    have = hn;
+  }
+  if (teams == 1) {
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      const int k = c + tl + q * TG;
+      if (k < n) partP[(int64_t)b * n + k] = acc[q];
+    }
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < CPT; ++q) {
+    const int kk = tl + q * TG;
+    if (kk < ncols) qsm[tm * ncols + kk] = acc[q];
+  }
+  __syncthreads();
+  for (int kk = t; kk < ncols; kk += blockDim.x) {
+    double sum = 0.0;
+    for (int u = 0; u < teams; ++u) sum += qsm[u * ncols + kk];
+    partP[(int64_t)b * n + c + kk] = sum;
+  }
+}
+
+// Column j's scalars and w^T from the partials the previous pass left (CTAs b >= b0 wrote).
+// A CTA reduces 32 columns: warp w sums partial rows b = b0 + w (mod 8), then the 8 warp
+// sums are added in warp order (deterministic).
+template <typename T>
+__global__ void __launch_bounds__(kQrThreads) k_qr_fin(const T* __restrict__ W, int n, int j, int b0, int nb, int prec,
+                                                        const double* __restrict__ partP, double* __restrict__ wT,
+                                                        double* __restrict__ scal, double* __restrict__ G,
+                                                        int* __restrict__ qflags) {
+  __shared__ double red[32];
+  __shared__ double cs[8][32];
+  if (qflags[0]) return;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  double tl = 0.0;
+  for (int b = b0 + t; b < nb; b += kQrThreads) tl += partP[(int64_t)b * n + j];
+  const double tail = block_sum(tl, red);                      // fixed order: same bits in every CTA
+  const double x0 = (double)W[(int64_t)j * n + j];
+  const double sigma = round_uf(sqrt(round_uf(fma(x0, x0, tail), prec)), prec);
+  if (!(sigma > 0.0)) {                                        // zero (or non-finite) column in u_f
+    if (blockIdx.x == 0 && t == 0) { qflags[0] = 1; qflags[1] = j + 1; }
+    return;
+  }
+  const double alpha = x0 >= 0.0 ? -sigma : sigma;
+  const double v0 = round_uf(x0 - alpha, prec);
+  const double vv = round_uf(fma(v0, v0, tail), prec);
+  const double beta = round_uf(2.0 / vv, prec);
+  const int k = j + 1 + blockIdx.x * 32 + lane;
+  double s0 = 0.0, s1 = 0.0;
+  if (k < n) {
+    int b = b0 + warp;
+    for (; b + 8 < nb; b += 16) {
+      s0 += partP[(int64_t)b * n + k];
+      s1 += partP[(int64_t)(b + 8) * n + k];
+    }
+    if (b < nb) s0 += partP[(int64_t)b * n + k];
+  }
+  cs[warp][lane] = s0 + s1;
+  __syncthreads();
+  if (warp == 0 && k < n) {
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += cs[u][lane];
+    const double w = round_uf(fma(v0, (double)W[(int64_t)j * n + k], s), prec);
+    wT[k] = round_uf(beta * w, prec);
+  }
+  if (blockIdx.x == 0 && t == 0) {
+    scal[4 * j + 0] = alpha;
+    scal[4 * j + 1] = v0;
+    scal[4 * j + 2] = sigma;
+    scal[4 * j + 3] = beta;
+    G[(int64_t)j * n + j] = sigma;                              // |alpha|: diag(R) >= 0
+  }
+}
+
+// Team size for a pass over `ncols` columns with CPT columns per thread.
+inline int qr_team(int ncols, int cpt) {
+  int tg = (ncols + cpt - 1) / cpt;
+  tg = (tg + 31) / 32 * 32;
+  if (tg < 32) tg = 32;
+  return tg > kQrThreads ? kQrThreads : tg;
+}
+
+template <typename T, bool LOAD, int CPT>
+int qr_step_launch(T* W, const DenseView& A, const double* dinv, int j, int RB, int bfirst, int nblk, int u_f,
+                   const double* wT, const double* scal, double* partP, double* G, const int* qflags, cudaStream_t st) {
+  const int n = A.n;
+  const int ncols = n - (j + 1);
+  const int TG = qr_team(ncols, CPT);
+  const int teams = kQrThreads / TG;
+  const size_t smem = teams > 1 ? (size_t)teams * ncols * sizeof(double) : 0;
+  k_qr_step<T, LOAD, CPT><<<nblk, teams * TG, smem, st>>>(W, A.A, A.ld, dinv, A.m, n, j, RB, bfirst, TG, u_f, wT,
+                                                          scal, partP, G, qflags);
+  TLS_LAUNCH_CHECK();
+  return 0;
+}
+
+template <typename T, int CPT>
+int qr_t(const DenseView& A, int u_f, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
+         int* qflags, double* G, cudaStream_t st, int* launches) {
+  const int n = A.n;
+  const int64_t m = A.m;
+  const int RB = qr_rows_per_cta(m, n);
+  const int nb = (int)((m + RB - 1) / RB);
+  T* W = static_cast<T*>(Wbuf);
+  int rc = qr_step_launch<T, true, CPT>(W, A, dinv, -1, RB, 0, nb, u_f, nullptr, nullptr, partP, G, qflags, st);
+  if (rc) return rc;
+  int nl = 1;
+  for (int j = 0; j < n; ++j) {
+    // partials of column j were written by the pass with first row max(j - 1, 0)
+    const int b0 = (int)((j > 0 ? j - 1 : 0) / RB);
+    const int nf = (n - j - 1 + 31) / 32;
+    k_qr_fin<T><<<nf > 0 ? nf : 1, kQrThreads, 0, st>>>(W, n, j, b0, nb, u_f, partP, wT, scal, G, qflags);
+    ++nl;
+    if (j + 1 < n) {
+      const int bs = (int)(j / RB);       // CTAs whose rows are all < j would exit at once: not launched
+      rc = qr_step_launch<T, false, CPT>(W, A, dinv, j, RB, bs, nb - bs, u_f, wT, scal, partP, G, qflags, st);
+      if (rc) return rc;
+      ++nl;
+    }
+  }
+  TLS_LAUNCH_CHECK();
+  if (launches) *launches += nl;
+  return 0;
+}
+
+template <typename T>
+int qr_dispatch(const DenseView& A, int u_f, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
+                int* qflags, double* G, cudaStream_t st, int* launches) {
+  if (A.n <= 4 * kQrThreads) return qr_t<T, 4>(A, u_f, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
+  if (A.n <= 8 * kQrThreads) return qr_t<T, 8>(A, u_f, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
+  return qr_t<T, 16>(A, u_f, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
+}
+}  // namespace
+
+int qr_rows_per_cta(int64_t m, int n) {
+  const int64_t want = (n > 8 * kQrThreads ? 1 : 2) * 148;   // resident CTAs: one wave
+  int64_t rb = (m + want - 1) / want;
+  if (rb < 32) rb = 32;
+  return (int)rb;
+}
+
+size_t qr_work_bytes(int64_t m, int n, int u_f) {
+  const int RB = qr_rows_per_cta(m, n);
+  const int64_t nb = (m + RB - 1) / RB;
+  const size_t es = (u_f == TLS_FP64) ? 8 : 4;
+  return (size_t)m * n * es + (size_t)nb * n * 8 + (size_t)n * 8 + 4 * (size_t)n * 8 + 5 * 256;
+}
+
+int launch_qr(const DenseView& A, int u_f, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
+              int* qflags, double* G, cudaStream_t st, int* launches) {
+  if (A.n > kMaxDenseN) { set_error("QR: n > %d", kMaxDenseN); return TLS_ERR_ARG; }
+  if (u_f == TLS_FP64) return qr_dispatch<double>(A, u_f, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
+  return qr_dispatch<float>(A, u_f, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
+}
+
+}  // namespace tls

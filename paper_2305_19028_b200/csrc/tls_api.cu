@@ -764,6 +764,87 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
   return 0;
 }
 
+size_t tls_qr_workspace_size(const tls_matrix_t* A, int32_t u_f) {
+  if (check_matrix(A) != 0 || is_csr(A) || u_f < TLS_FP16 || u_f > TLS_FP64) return 0;
+  return ws_need(A, false) + (size_t)A->n * A->n * 8 + 256 + qr_work_bytes(A->m_local, (int)A->n, u_f);
+}
+
+int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, void* stream, void* ws,
+                          size_t ws_bytes, tls_precond_t* R_out, tls_info_t* info) {
+  fill_info_defaults(info);
+  if (R_out) *R_out = nullptr;
+  TLS_TRY(check_matrix(A));
+  if (!R_out || u_f < TLS_FP16 || u_f > TLS_FP64) { set_error("bad u_f or R_out"); return TLS_ERR_ARG; }
+  if (is_csr(A)) { set_error("the QR preconditioner takes a dense A"); return TLS_ERR_ARG; }
+  if (comm != nullptr && comm->nranks > 1) { set_error("the QR preconditioner is single-GPU in this build"); return TLS_ERR_ARG; }
+  const size_t need = tls_qr_workspace_size(A, u_f);
+  Work w;
+  if (ws == nullptr || ws_bytes < need || !carve_ok(A, ws, ws_bytes, w, false)) {
+    set_error("workspace too small (need %zu)", need);
+    return TLS_ERR_WORKSPACE;
+  }
+  const int n = (int)A->n;
+  const size_t base = ws_need(A, false);
+  Carver c{static_cast<char*>(ws) + base, ws_bytes - base};
+  double* G = c.take<double>((size_t)n * n);
+  const int RB = qr_rows_per_cta(A->m_local, n);
+  const int64_t nb = (A->m_local + RB - 1) / RB;
+  void* Wq = c.take<char>((size_t)A->m_local * n * (u_f == TLS_FP64 ? 8 : 4));
+  double* partP = c.take<double>((size_t)nb * n);
+  double* wT = c.take<double>((size_t)n);
+  double* scal = c.take<double>(4 * (size_t)n);
+  int* qflags = c.take<int>(4);
+  if (!c.ok) { set_error("workspace too small (need %zu)", need); return TLS_ERR_WORKSPACE; }
+  Ctx cx{static_cast<cudaStream_t>(stream), comm};
+  Tracer tr(cx.st);
+  tr.mark("qr:start");
+  TLS_CUDA_TRY(cudaMemsetAsync(w.flags, 0, 8 * sizeof(int), cx.st));
+  TLS_CUDA_TRY(cudaMemsetAsync(qflags, 0, 4 * sizeof(int), cx.st));
+  TLS_CUDA_TRY(cudaMemsetAsync(G, 0, (size_t)n * n * 8, cx.st));
+  // the same D = powers of two and ||A||_F^2 as the Cholesky route (R2)
+  TLS_TRY(run_pass(cx, A, PASS_COLSTATS, 2, nullptr, nullptr, w, nullptr));
+  double* d = w.d_tmp;
+  double* dinv = w.d_tmp + n;
+  double* normA2 = w.d_tmp + 2 * n;
+  TLS_TRY(launch_scaling(w.colstats, w.colstats + n, n, d, dinv, normA2, &w.flags[0], cx.st));
+  cx.launches += 1;
+  tr.mark("colstats");
+  {
+    ProfScope ps(TLS_PROF_CHOL, cx.st);
+    TLS_TRY(launch_qr(dense_view(A), u_f, dinv, Wq, partP, wT, scal, qflags, G, cx.st, &cx.launches));
+  }
+  cx.passes += n + 1;
+  tr.mark("qr");
+  tls_precond_t h = nullptr;
+  TLS_TRY(alloc_precond(n, u_f, &h));
+  k_fill_scaling<<<(h->dev.npad + 255) / 256, 256, 0, cx.st>>>(h->dev.d, h->dev.dinv, d, dinv, n, h->dev.npad);
+  TLS_CUDA_TRY(cudaMemcpyAsync(h->dev.normA2, normA2, sizeof(double), cudaMemcpyDeviceToDevice, cx.st));
+  int rc = launch_pack_R(G, n, 0, h->dev, &w.flags[3], cx.st, &cx.launches);
+  cx.launches += 1;
+  if (rc) { tls_precond_destroy(h); return rc; }
+  int hflags[8], hq[4];
+  double hnorm = 0.0;
+  TLS_CUDA_TRY(cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, cx.st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(hq, qflags, sizeof(hq), cudaMemcpyDeviceToHost, cx.st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(&hnorm, normA2, sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+  TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+  tr.mark("sync");
+  if (info) { info->passes = cx.passes; info->launches = cx.launches; }
+  int st = 0;
+  if (hflags[0]) { set_error("A has a zero or non-finite column (rank deficient)"); st = TLS_ERR_ARG; }
+  else if (hq[0]) { st = TLS_CHOL_BREAKDOWN; if (info) info->chol_pivot = hq[1]; }
+  else if (hflags[3]) st = TLS_RANGE;
+  if (st) {
+    tls_precond_destroy(h);
+    if (info && st > 0) info->status = st;
+    return st;
+  }
+  h->normA2_host = hnorm;
+  h->m_global = A->m_global;
+  *R_out = h;
+  return 0;
+}
+
 int tls_precond_import(int64_t n, int32_t u_f, const double* Rt_host, const double* d_host, double normA2,
                        void* stream, tls_precond_t* out) {
   if (!out || n < 1 || n > kMaxDenseN || !Rt_host || !d_host || u_f < TLS_FP16 || u_f > TLS_FP64) {

@@ -74,6 +74,8 @@ def lib() -> C.CDLL:
         "tls_comm_destroy": (C.c_int, [VP]),
         "tls_workspace_size": (SZ, [M, I32]),
         "tls_factor_precond": (C.c_int, [M, I32, P(tls_rqi_opts_t), VP, VP, VP, SZ, P(VP), P(tls_info_t)]),
+        "tls_qr_workspace_size": (SZ, [M, I32]),
+        "tls_factor_precond_qr": (C.c_int, [M, I32, VP, VP, VP, SZ, P(VP), P(tls_info_t)]),
         "tls_precond_import": (C.c_int, [I64, I32, VP, VP, D, VP, P(VP)]),
         "tls_precond_export": (C.c_int, [VP, VP, VP, P(D)]),
         "tls_precond_destroy": (None, [VP]),
@@ -101,7 +103,7 @@ def lib() -> C.CDLL:
 
 EXPORTED = ["tls_abi_version", "tls_rqi_opts_default", "tls_status_string", "tls_last_error",
             "tls_comm_get_unique_id", "tls_comm_init", "tls_comm_destroy", "tls_workspace_size",
-            "tls_factor_precond", "tls_precond_import", "tls_precond_export", "tls_precond_destroy",
+            "tls_factor_precond", "tls_qr_workspace_size", "tls_factor_precond_qr", "tls_precond_import", "tls_precond_export", "tls_precond_destroy",
             "tls_rqi_pcgtls", "tls_solve_host_bytes", "tls_solve_host", "tls_colstats", "tls_gram",
             "tls_pass", "tls_pass_fp32", "tls_precond_apply", "tls_round", "tls_profile_enable", "tls_profile_read"]
 
@@ -262,6 +264,22 @@ def tls_factor_precond(M: tls_matrix_t, u_f, opts: Optional[tls_rqi_opts_t] = No
     _check(rc, "tls_factor_precond")
     d = _info_dict(info, bufs)
     return rc, (Precond(R.value, int(M.n), uf) if R.value else None), d
+
+
+def tls_factor_precond_qr(M: tls_matrix_t, u_f, comm=None, stream=None, ws: Optional[torch.Tensor] = None):
+    """Householder-QR preconditioner in u_f (NEXT-2, R25).  Returns (status, Precond or None, info dict)."""
+    uf = PREC[u_f] if isinstance(u_f, str) else int(u_f)
+    if ws is None:
+        nbytes = int(lib().tls_qr_workspace_size(C.byref(M), uf))
+        if nbytes == 0:
+            raise TlsError(-1, "tls_qr_workspace_size")
+        ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    R = C.c_void_p()
+    info, bufs = _info(50)
+    rc = lib().tls_factor_precond_qr(C.byref(M), uf, C.c_void_p(comm) if comm else None, _stream(stream),
+                                     _ptr(ws), ws.numel(), C.byref(R), C.byref(info))
+    _check(rc, "tls_factor_precond_qr")
+    return rc, (Precond(R.value, int(M.n), uf) if R.value else None), _info_dict(info, bufs)
 
 
 def tls_precond_import(Rt, d, normA2: float, u_f, stream=None) -> Precond:

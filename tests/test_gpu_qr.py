@@ -1,0 +1,155 @@
+"""GPU parity of the Householder-QR preconditioner in u_f (PAPER.md
+l.215-218, l.231; reading R25) against oracle/qr.py through the C ABI.
+
+What is compared, and why not bit for bit: both sides round every elementwise operation
+to u_f in the same order and take the same sign decisions; only the fp64 inner products
+(x^T x, v^T W) are summed in a different order before their single rounding to u_f.  So
+  - D and ||A||_F^2: bit-exact / 1e-14 (the Cholesky route's own pass);
+  - R~: each entry agrees to a few u_f ulps (a rounded inner product can land on the
+    other side of a u_f rounding boundary, and that difference then propagates through
+    the remaining columns like any other rounding error of the factorization); the bound
+    written below is the QR backward-error bound the oracle is pinned to (test_oracle_qr:
+    ||R^T R - Ah^T Ah||_F <= 10 m n u ||Ah||_F^2) applied to the GPU's R~, plus a normwise
+    distance to the oracle's R~ within the same bound's forward image (kappa(Ah) times it);
+  - a solve with the GPU's QR R~: the north_star tolerances against the oracle run on the
+    same R~ (x 1e-9, sigma 1e-12, same RQI count, PCG counts equal) and against the SVD.
+"""
+import numpy as np
+import pytest
+import torch
+
+import tlsgen
+from oracle import exact, rqi
+from oracle.rounding import round_to, unit_roundoff
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+
+@pytest.fixture(scope="module")
+def T():
+    from paper_2305_19028_b200 import tlsrqi
+    tlsrqi.lib()
+    return tlsrqi
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+
+
+def _mat(T, A):
+    """tls_matrix_t of A with an even leading dimension (the ABI's dense layout); returns the
+    device tensor too, which must stay alive while the matrix is used."""
+    m, n = A.shape
+    Ap = np.zeros((m, n + (n & 1)))
+    Ap[:, :n] = A
+    t = dev(Ap)
+    return T.matrix(t, n=n), t
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300))
+
+
+def _problem(m, n, kappa, seed, spread=True):
+    rng = np.random.default_rng(seed)
+    U, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    s = np.logspace(0, -np.log10(kappa), n)
+    A = (U * s) @ V.T
+    # column scales spread over several binades so that D is not the identity
+    if spread:
+        A = A * np.exp2(rng.integers(-6, 7, n))[None, :]
+    x = rng.standard_normal(n)
+    b = A @ x + 1e-3 * rng.standard_normal(m) * np.linalg.norm(A @ x) / np.sqrt(m)
+    return A, b
+
+
+CASES = [  # (m, n, kappa, u_f): tiles of 256 columns per thread sweep, ragged tails, all formats
+    (200, 20, 1e2, "fp16"), (333, 47, 1e2, "bf16"), (777, 67, 1e3, "fp32"), (257, 31, 1e3, "fp64"),
+    (600, 300, 1e2, "fp16"), (1100, 530, 1e2, "bf16")]
+
+
+@pytest.mark.parametrize("m,n,kappa,fmt", CASES)
+def test_qr_factor_parity(T, m, n, kappa, fmt):
+    A, _ = _problem(m, n, kappa, seed=m + n)
+    pc = rqi.factor_precond_qr(A, fmt)
+    assert pc.status == rqi.OK
+    M, keep = _mat(T, A)
+    rc, R, info = T.tls_factor_precond_qr(M, fmt)
+    assert rc == 0 and R is not None
+    Rt, d, nrm = T.tls_precond_export(R)
+    assert np.array_equal(d, pc.d)
+    assert nrm == pytest.approx(pc.normA2, rel=1e-14)
+    assert np.array_equal(np.tril(Rt, -1), np.zeros_like(Rt))
+    assert np.all(np.diag(Rt) > 0)
+    assert np.array_equal(round_to(Rt, fmt), Rt)                 # stored in u_f
+    u = unit_roundoff(fmt)
+    Ah = round_to(A / d, fmt)
+    bound = 10 * m * n * u * np.linalg.norm(Ah) ** 2
+    assert np.linalg.norm(Rt.T @ Rt - Ah.T @ Ah) <= bound         # backward error (pinned bound)
+    kap = np.linalg.cond(Ah)
+    assert _rel(Rt, pc.Rt) <= 10 * m * n * u * kap
+
+
+@pytest.mark.parametrize("m,n,kappa,fmt", [(200, 20, 1e2, "fp16"), (777, 67, 1e3, "bf16"), (5000, 1100, 1e2, "fp16"),
+                                           (1100, 530, 1e2, "fp16")])
+def test_qr_solve_parity(T, m, n, kappa, fmt):
+    """RQI-PCGTLS-MP preconditioned by the GPU's QR R~ against the oracle on the same R~."""
+    A, b = _problem(m, n, kappa, seed=7 * m + n, spread=False)   # sigma_n(A) >> sigma_{n+1}: a TLS solution exists
+    M, keep = _mat(T, A)
+    rc, R, _ = T.tls_factor_precond_qr(M, fmt)
+    assert rc == 0
+    rc, x, sig, info = T.tls_rqi_pcgtls(M, dev(b), R)
+    Rt, d, nrm = T.tls_precond_export(R)
+    Ah = round_to(A / d, fmt)      # backward error of the GPU's QR (the bound the oracle is pinned to)
+    assert np.linalg.norm(Rt.T @ Rt - Ah.T @ Ah) <= 10 * m * n * unit_roundoff(fmt) * np.linalg.norm(Ah) ** 2
+    res = rqi.rqi_pcgtls_mp(A, b, rqi.Precond(Rt, d, fmt, nrm))
+    ex = exact.tls_svd(A, b)
+    assert info["status"] == res.status == rqi.OK
+    assert info["rqi_iters"] == res.rqi_iters
+    assert info["pcg_iters"] == [tuple(p) for p in res.pcg_iters]
+    assert _rel(x.cpu().numpy(), res.x) <= 1e-9
+    assert abs(sig - res.sigma) / res.sigma <= 1e-12
+    assert _rel(x.cpu().numpy(), ex.x) <= 1e-9
+
+
+def test_qr_cfg1_paper_workload(T):
+    """cfg1 (BASELINE configs[0]) with the paper's preferred preconditioner, u_f = fp16."""
+    P = tlsgen.config("cfg1")
+    M = T.matrix(dev(P.A))
+    rc, R, _ = T.tls_factor_precond_qr(M, "fp16")
+    assert rc == 0
+    Rt, d, nrm = T.tls_precond_export(R)
+    pc = rqi.factor_precond_qr(P.A, "fp16")
+    assert _rel(Rt, pc.Rt) <= 1e-2
+    rc, x, sig, info = T.tls_rqi_pcgtls(M, dev(P.b), R)
+    ex = exact.tls_svd(P.A, P.b)
+    assert _rel(x.cpu().numpy(), ex.x) <= 1e-9
+    assert abs(sig - ex.sigma) / ex.sigma <= 1e-11
+
+
+def test_qr_zero_column_breakdown(T):
+    """Column 1 equals 2 x column 0 = 2 e_0: after the power-of-two scaling both are e_0, the
+    first reflector maps column 1 to -e_0 exactly, and column 1 is exactly zero below the
+    diagonal.  Both sides report the 1-based pivot 2."""
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((64, 8))
+    A[:, 0] = 0.0
+    A[0, 0] = 1.0
+    A[:, 1] = 2.0 * A[:, 0]
+    for fmt in ("fp16", "fp32", "fp64"):
+        pc = rqi.factor_precond_qr(A, fmt)
+        assert pc.status == rqi.CHOL_BREAKDOWN and pc.chol_pivot == 2
+        rc, R, info = T.tls_factor_precond_qr(T.matrix(dev(A)), fmt)
+        assert R is None
+        assert rc == rqi.CHOL_BREAKDOWN
+        assert info["chol_pivot"] == pc.chol_pivot
+
+
+def test_qr_refuses_csr_and_reports_workspace(T):
+    A, _ = _problem(64, 8, 10.0, seed=1)
+    M = T.matrix(dev(A))
+    assert T.lib().tls_qr_workspace_size(M, 0) >= 64 * 8 * 4
+    with pytest.raises(T.TlsError):
+        T.tls_factor_precond_qr(M, "fp16", ws=torch.empty(16, dtype=torch.uint8, device="cuda"))

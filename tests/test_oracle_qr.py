@@ -71,3 +71,22 @@ def test_rqi_with_qr_preconditioner(name):
     assert r.status == rqi.OK
     assert np.linalg.norm(r.x - ex.x) / np.linalg.norm(ex.x) <= 1e-12
     assert abs(r.sigma - ex.sigma) / ex.sigma <= 1e-12
+
+
+def test_zero_column_reports_its_pivot():
+    """Column 1 = 2 x column 0 = 2 e_0: the first reflector (sigma = 1, alpha = -1, v = 2 e_0,
+    beta = 1/2) maps the scaled column 1 (= e_0) to -e_0 exactly, so column 1 vanishes below
+    its diagonal: CHOL_BREAKDOWN with the 1-based pivot 2 in every format."""
+    from oracle import rqi
+    from oracle.qr import ZeroColumn, householder_qr_r
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((64, 8))
+    A[:, 0] = 0.0
+    A[0, 0] = 1.0
+    A[:, 1] = 2.0 * A[:, 0]
+    for fmt in ("fp16", "bf16", "fp32", "fp64"):
+        with pytest.raises(ZeroColumn) as e:
+            householder_qr_r(A / np.array([1.0, 2.0] + [1.0] * 6), fmt)
+        assert e.value.col == 1
+        pc = rqi.factor_precond_qr(A, fmt)
+        assert pc.status == rqi.CHOL_BREAKDOWN and pc.chol_pivot == 2
