@@ -16,6 +16,8 @@
 // accumulates the fp64 partial inner products of the NEXT column (x'^T x' and x'^T W')
 // per CTA, so column j+1's reflector needs no second pass; k_qr_fin reduces those partials
 // (fixed order, deterministic), forms the column's scalars and w^T.  2 launches per column.
+#include <cuda_bf16.h>
+
 #include "tls_common.cuh"
 #include "tls_kernels.h"
 
@@ -23,6 +25,13 @@ namespace tls {
 
 namespace {
 constexpr int kQrThreads = 256;
+
+// Round an fp32 value to u_f (fp16 / bf16 hardware conversions; identity for fp32).
+template <int PREC> __device__ __forceinline__ float qr_rdf(float x) {
+  if constexpr (PREC == TLS_FP16) return __half2float(__float2half_rn(x));
+  else if constexpr (PREC == TLS_BF16) return __bfloat162float(__float2bfloat16_rn(x));
+  else return x;
+}
 
 template <typename T> __device__ __forceinline__ T qr_store(double v);
 template <> __device__ __forceinline__ float qr_store<float>(double v) { return (float)v; }   // exact: v in u_f
@@ -36,34 +45,32 @@ template <> __device__ __forceinline__ double qr_store<double>(double v) { retur
 // A CTA owns RB rows; it runs `teams` rows at a time, one team of TG threads per row (CPT
 // columns per thread, k = c + tl + q TG), with the next row of each team loaded before the
 // current one is stored.  Team partials are combined in shared memory in team order.
+template <typename T, bool LOAD> struct QrSrc { using type = T; };
+template <typename T> struct QrSrc<T, true> { using type = double; };   // LOAD reads A itself
+
+// Loads of the next row keep the storage type: nothing waits on them until the row is used.
 template <typename T, bool LOAD, int CPT>
 __device__ __forceinline__ void qr_load_row(const T* __restrict__ W, const double* __restrict__ A, int64_t lda,
-                                            int64_t i, int n, int j, int c, int tl, int TG, double (&dst)[CPT],
-                                            double& sj, double& sc) {
-  if (LOAD) {
-    const double* src = A + i * lda;
-    sc = src[0];
+                                            int64_t i, int n, int ldw, int j, int c, int tl, int TG,
+                                            typename QrSrc<T, LOAD>::type (&dst)[CPT],
+                                            typename QrSrc<T, LOAD>::type& sj, typename QrSrc<T, LOAD>::type& sc) {
+  using S = typename QrSrc<T, LOAD>::type;
+  const S* src;
+  if constexpr (LOAD) src = A + i * lda;
+  else src = W + i * (int64_t)ldw;
+  if (!LOAD) sj = (i == j) ? S(0) : src[j];
+  sc = c < n ? src[c] : S(0);
 #pragma unroll
-    for (int q = 0; q < CPT; ++q) {
-      const int k = c + tl + q * TG;
-      dst[q] = k < n ? src[k] : 0.0;
-    }
-  } else {
-    const T* src = W + i * (int64_t)n;
-    sj = (i == j) ? 0.0 : (double)src[j];
-    sc = c < n ? (double)src[c] : 0.0;
-#pragma unroll
-    for (int q = 0; q < CPT; ++q) {
-      const int k = c + tl + q * TG;
-      dst[q] = k < n ? (double)src[k] : 0.0;
-    }
+  for (int q = 0; q < CPT; ++q) {
+    const int k = c + tl + q * TG;
+    dst[q] = k < n ? src[k] : S(0);
   }
 }
 
-template <typename T, bool LOAD, int CPT>
-__global__ void __launch_bounds__(kQrThreads) k_qr_step(T* __restrict__ W, const double* __restrict__ A, int64_t lda,
-                                                         const double* __restrict__ dinv, int64_t m, int n, int j,
-                                                         int RB, int bfirst, int TG, int prec,
+template <typename T, bool LOAD, int CPT, int PREC>
+__global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step(T* __restrict__ W, const double* __restrict__ A, int64_t lda,
+                                                         const double* __restrict__ dinv, int64_t m, int n, int ldw, int j,
+                                                         int RB, int bfirst, int TG,
                                                          const double* __restrict__ wT,
                                                          const double* __restrict__ scal, double* __restrict__ partP,
                                                          double* __restrict__ G, const int* __restrict__ dead) {
@@ -78,7 +85,10 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_step(T* __restrict__ W, const
   if (r1 <= rs) return;                 // rows all above: k_qr_fin does not read this CTA
   if (r0 < rs) r0 = rs;
   const int t = threadIdx.x, tm = t / TG, tl = t % TG, teams = blockDim.x / TG;
-  double wk[CPT], acc[CPT], cur[CPT], nxt[CPT];
+  using S = typename QrSrc<T, LOAD>::type;
+  constexpr int prec = PREC;
+  double wk[CPT], acc[CPT];
+  S cur[CPT], nxt[CPT];
   const double alpha = LOAD ? 0.0 : scal[4 * j + 0];
   const double v0 = LOAD ? 0.0 : scal[4 * j + 1];
   const double wc = LOAD ? dinv[0] : (c < n ? wT[c] : 0.0);     // LOAD: the scale of column 0
@@ -90,33 +100,56 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_step(T* __restrict__ W, const
   }
   int64_t i = r0 + tm;
   bool have = i < r1;
-  double nj = 0.0, nc = 0.0;
-  if (have) qr_load_row<T, LOAD, CPT>(W, A, lda, i, n, j, c, tl, TG, nxt, nj, nc);
+  S nj = S(0), nc = S(0);
+  if (have) qr_load_row<T, LOAD, CPT>(W, A, lda, i, n, ldw, j, c, tl, TG, nxt, nj, nc);
   while (have) {
 #pragma unroll
     for (int q = 0; q < CPT; ++q) cur[q] = nxt[q];
-    const double cj = nj, cc = nc;
+    const double cj = (double)nj, cc = (double)nc;
     const int64_t inext = i + teams;
     const bool hn = inext < r1;
-    if (hn) qr_load_row<T, LOAD, CPT>(W, A, lda, inext, n, j, c, tl, TG, nxt, nj, nc);
-    T* row = W + i * (int64_t)n;
-    double xc, vi = 0.0;   // xc: new value of column c in this row (same bits in every thread)
-    if (LOAD) {
-      xc = round_uf(cc * wc, prec);
-    } else {
-      vi = (i == j) ? v0 : cj;
-      xc = round_uf(cc - round_uf(vi * wc, prec), prec);
-    }
+    if (hn) qr_load_row<T, LOAD, CPT>(W, A, lda, inext, n, ldw, j, c, tl, TG, nxt, nj, nc);
+    T* row = W + i * (int64_t)ldw;
     const bool accum = i > c;
+    if (LOAD && tl < ldw - n) row[n + tl] = T(0);      // padding columns of the working copy
+    if constexpr (!LOAD && PREC != TLS_FP64) {
+      // fp32 arithmetic, bit-identical to the fp64-then-round of the oracle: the products of
+      // two u_f values are exact in fp32 (fp16: 22 bits, bf16: 16) or correctly rounded
+      // (u_f = fp32), and a difference rounded to fp32 and then to u_f equals the difference
+      // rounded once to u_f, as fp32's 24 bits >= 2p + 2 for p = 11 and 8 (double rounding is
+      // innocuous; R25).  Conversions then stay off the XU pipe (packed F2FP / HADD2).
+      const float vf = (i == j) ? (float)v0 : (float)cj;
+      const float xf = qr_rdf<PREC>(__fsub_rn((float)cc, qr_rdf<PREC>(__fmul_rn(vf, (float)wc))));
+      const double xd = (double)xf;
 #pragma unroll
-    for (int q = 0; q < CPT; ++q) {
-      const int k = c + tl + q * TG;
-      if (k < n) {
-        const double nv = LOAD ? round_uf(cur[q] * wk[q], prec)
-                               : round_uf(cur[q] - round_uf(vi * wk[q], prec), prec);
-        row[k] = qr_store<T>(nv);
-        if (accum) acc[q] = fma(xc, nv, acc[q]);
-        if (!LOAD && i == j) G[(int64_t)j * n + k] = alpha < 0.0 ? -nv : nv;
+      for (int q = 0; q < CPT; ++q) {
+        const int k = c + tl + q * TG;
+        if (k < n) {
+          const float nf = qr_rdf<PREC>(__fsub_rn((float)cur[q], qr_rdf<PREC>(__fmul_rn(vf, (float)wk[q]))));
+          row[k] = nf;
+          if (accum) acc[q] = fma(xd, (double)nf, acc[q]);
+          if (i == j) G[(int64_t)j * n + k] = alpha < 0.0 ? -(double)nf : (double)nf;
+        }
+      }
+    } else {
+      double xc, vi = 0.0;   // xc: new value of column c in this row (same bits in every thread)
+      if (LOAD) {
+        xc = round_uf(cc * wc, prec);
+      } else {
+        vi = (i == j) ? v0 : cj;
+        xc = round_uf(__dsub_rn(cc, round_uf(__dmul_rn(vi, wc), prec)), prec);
+      }
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        const int k = c + tl + q * TG;
+        if (k < n) {
+          const double cv = (double)cur[q];
+          const double nv = LOAD ? round_uf(cv * wk[q], prec)
+                                 : round_uf(__dsub_rn(cv, round_uf(__dmul_rn(vi, wk[q]), prec)), prec);
+          row[k] = qr_store<T>(nv);
+          if (accum) acc[q] = fma(xc, nv, acc[q]);
+          if (!LOAD && i == j) G[(int64_t)j * n + k] = alpha < 0.0 ? -nv : nv;
+        }
       }
     }
     i = inext;
@@ -143,22 +176,136 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_step(T* __restrict__ W, const
   }
 }
 
+// The update pass on the fp32 working copy (u_f = fp16 / bf16 / fp32), 16-byte accesses:
+// thread tl owns the 4-column groups g = tl + q TG starting at the aligned column c0 = c & ~3
+// (ldw is a multiple of 4).  Columns k < c and k >= n carry w_k = 0, so they are rewritten
+// with their own values (rd(x - rd(v 0)) = x) and need no masks.
+template <int CPT, int PREC>
+__global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step_v4(
+    float* __restrict__ W, int64_t m, int n, int ldw, int j, int RB, int bfirst, int TG,
+    const double* __restrict__ wT, const double* __restrict__ scal, double* __restrict__ partP,
+    double* __restrict__ G, const int* __restrict__ dead) {
+  constexpr int GPT = CPT / 4;
+  extern __shared__ double qsm[];
+  if (*dead) return;
+  const int c = j + 1, c0 = c & ~3;
+  const int ngroups = (ldw - c0) >> 2;
+  const int b = bfirst + (int)blockIdx.x;
+  int64_t r0 = (int64_t)b * RB;
+  const int64_t r1 = min(m, r0 + RB);
+  if (r1 <= j) return;
+  if (r0 < j) r0 = j;
+  const int t = threadIdx.x, tm = t / TG, tl = t % TG, teams = blockDim.x / TG;
+  const double alpha = scal[4 * j + 0];
+  const float v0f = (float)scal[4 * j + 1];
+  const float wcf = (float)wT[c];
+  float wk[CPT];
+  double acc[CPT];
+#pragma unroll
+  for (int q = 0; q < GPT; ++q) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int k = c0 + 4 * (tl + q * TG) + e;
+      wk[4 * q + e] = (k >= c && k < n) ? (float)wT[k] : 0.f;
+      acc[4 * q + e] = 0.0;
+    }
+  }
+  float4 cur[GPT], nxt[GPT];
+  float nj = 0.f, nc = 0.f;
+  int64_t i = r0 + tm;
+  bool have = i < r1;
+  auto load = [&](int64_t ii) {   // the next row of this team, in flight while row i is updated
+    const float* src = W + ii * (int64_t)ldw;
+    nj = src[j];
+    nc = src[c];
+#pragma unroll
+    for (int q = 0; q < GPT; ++q) {
+      const int g = tl + q * TG;
+      if (g < ngroups) nxt[q] = *reinterpret_cast<const float4*>(src + c0 + 4 * g);
+    }
+  };
+  if (have) load(i);
+  while (have) {
+#pragma unroll
+    for (int q = 0; q < GPT; ++q) cur[q] = nxt[q];
+    const float cj = nj, cc = nc;
+    const int64_t inext = i + teams;
+    const bool hn = inext < r1;
+    if (hn) load(inext);
+    float* row = W + i * (int64_t)ldw;
+    const float vf = (i == j) ? v0f : cj;
+    const double xd = (double)qr_rdf<PREC>(__fsub_rn(cc, qr_rdf<PREC>(__fmul_rn(vf, wcf))));
+    const bool accum = i > c;
+#pragma unroll
+    for (int q = 0; q < GPT; ++q) {
+      const int g = tl + q * TG;
+      if (g < ngroups) {
+        float x[4] = {cur[q].x, cur[q].y, cur[q].z, cur[q].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          x[e] = qr_rdf<PREC>(__fsub_rn(x[e], qr_rdf<PREC>(__fmul_rn(vf, wk[4 * q + e]))));
+          if (accum) acc[4 * q + e] = fma(xd, (double)x[e], acc[4 * q + e]);
+        }
+        *reinterpret_cast<float4*>(row + c0 + 4 * g) = make_float4(x[0], x[1], x[2], x[3]);
+        if (i == j) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int k = c0 + 4 * g + e;
+            if (k >= c && k < n) G[(int64_t)j * n + k] = alpha < 0.0 ? -(double)x[e] : (double)x[e];
+          }
+        }
+      }
+    }
+    i = inext;
+    have = hn;
+  }
+  const int ncv = ngroups * 4;
+  if (teams > 1) {
+#pragma unroll
+    for (int q = 0; q < GPT; ++q) {
+      const int g = tl + q * TG;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (g < ngroups) qsm[tm * ncv + 4 * g + e] = acc[4 * q + e];
+    }
+    __syncthreads();
+    for (int kk = t; kk < ncv; kk += blockDim.x) {
+      const int k = c0 + kk;
+      if (k < c || k >= n) continue;
+      double sum = 0.0;
+      for (int u = 0; u < teams; ++u) sum += qsm[u * ncv + kk];
+      partP[(int64_t)b * n + k] = sum;
+    }
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < GPT; ++q) {
+    const int g = tl + q * TG;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int k = c0 + 4 * g + e;
+      if (g < ngroups && k >= c && k < n) partP[(int64_t)b * n + k] = acc[4 * q + e];
+    }
+  }
+}
+
 // Column j's scalars and w^T from the partials the previous pass left (CTAs b >= b0 wrote).
 // A CTA reduces 32 columns: warp w sums partial rows b = b0 + w (mod 8), then the 8 warp
 // sums are added in warp order (deterministic).
-template <typename T>
-__global__ void __launch_bounds__(kQrThreads) k_qr_fin(const T* __restrict__ W, int n, int j, int b0, int nb, int prec,
+template <typename T, int PREC>
+__global__ void __launch_bounds__(kQrThreads) k_qr_fin(const T* __restrict__ W, int n, int ldw, int j, int b0, int nb,
                                                         const double* __restrict__ partP, double* __restrict__ wT,
                                                         double* __restrict__ scal, double* __restrict__ G,
                                                         int* __restrict__ qflags) {
   __shared__ double red[32];
   __shared__ double cs[8][32];
+  constexpr int prec = PREC;
   if (qflags[0]) return;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   double tl = 0.0;
   for (int b = b0 + t; b < nb; b += kQrThreads) tl += partP[(int64_t)b * n + j];
   const double tail = block_sum(tl, red);                      // fixed order: same bits in every CTA
-  const double x0 = (double)W[(int64_t)j * n + j];
+  const double x0 = (double)W[(int64_t)j * ldw + j];
   const double sigma = round_uf(sqrt(round_uf(fma(x0, x0, tail), prec)), prec);
   if (!(sigma > 0.0)) {                                        // zero (or non-finite) column in u_f
     if (blockIdx.x == 0 && t == 0) { qflags[0] = 1; qflags[1] = j + 1; }
@@ -184,7 +331,7 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_fin(const T* __restrict__ W, 
     double s = 0.0;
 #pragma unroll
     for (int u = 0; u < 8; ++u) s += cs[u][lane];
-    const double w = round_uf(fma(v0, (double)W[(int64_t)j * n + k], s), prec);
+    const double w = round_uf(fma(v0, (double)W[(int64_t)j * ldw + k], s), prec);
     wT[k] = round_uf(beta * w, prec);
   }
   if (blockIdx.x == 0 && t == 0) {
@@ -204,40 +351,51 @@ inline int qr_team(int ncols, int cpt) {
   return tg > kQrThreads ? kQrThreads : tg;
 }
 
-template <typename T, bool LOAD, int CPT>
-int qr_step_launch(T* W, const DenseView& A, const double* dinv, int j, int RB, int bfirst, int nblk, int u_f,
+template <typename T, bool LOAD, int CPT, int PREC>
+int qr_step_launch(T* W, const DenseView& A, int ldw, const double* dinv, int j, int RB, int bfirst, int nblk,
                    const double* wT, const double* scal, double* partP, double* G, const int* qflags, cudaStream_t st) {
   const int n = A.n;
-  const int ncols = n - (j + 1);
-  const int TG = qr_team(ncols, CPT);
-  const int teams = kQrThreads / TG;
-  const size_t smem = teams > 1 ? (size_t)teams * ncols * sizeof(double) : 0;
-  k_qr_step<T, LOAD, CPT><<<nblk, teams * TG, smem, st>>>(W, A.A, A.ld, dinv, A.m, n, j, RB, bfirst, TG, u_f, wT,
-                                                          scal, partP, G, qflags);
+  if constexpr (!LOAD && sizeof(T) == 4) {
+    const int c0 = (j + 1) & ~3;
+    const int ngroups = (ldw - c0) / 4;
+    const int TG = qr_team(ngroups, CPT / 4);
+    const int teams = kQrThreads / TG;
+    const size_t smem = teams > 1 ? (size_t)teams * ngroups * 4 * sizeof(double) : 0;
+    k_qr_step_v4<CPT, PREC><<<nblk, teams * TG, smem, st>>>(reinterpret_cast<float*>(W), A.m, n, ldw, j, RB, bfirst,
+                                                            TG, wT, scal, partP, G, qflags);
+  } else {
+    const int ncols = n - (j + 1);
+    const int TG = qr_team(ncols, CPT);
+    const int teams = kQrThreads / TG;
+    const size_t smem = teams > 1 ? (size_t)teams * ncols * sizeof(double) : 0;
+    k_qr_step<T, LOAD, CPT, PREC><<<nblk, teams * TG, smem, st>>>(W, A.A, A.ld, dinv, A.m, n, ldw, j, RB, bfirst, TG,
+                                                                  wT, scal, partP, G, qflags);
+  }
   TLS_LAUNCH_CHECK();
   return 0;
 }
 
-template <typename T, int CPT>
-int qr_t(const DenseView& A, int u_f, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
+template <typename T, int CPT, int PREC>
+int qr_t(const DenseView& A, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
          int* qflags, double* G, cudaStream_t st, int* launches) {
   const int n = A.n;
   const int64_t m = A.m;
   const int RB = qr_rows_per_cta(m, n);
   const int nb = (int)((m + RB - 1) / RB);
   T* W = static_cast<T*>(Wbuf);
-  int rc = qr_step_launch<T, true, CPT>(W, A, dinv, -1, RB, 0, nb, u_f, nullptr, nullptr, partP, G, qflags, st);
+  const int ldw = qr_ldw(n, PREC);
+  int rc = qr_step_launch<T, true, CPT, PREC>(W, A, ldw, dinv, -1, RB, 0, nb, nullptr, nullptr, partP, G, qflags, st);
   if (rc) return rc;
   int nl = 1;
   for (int j = 0; j < n; ++j) {
     // partials of column j were written by the pass with first row max(j - 1, 0)
     const int b0 = (int)((j > 0 ? j - 1 : 0) / RB);
     const int nf = (n - j - 1 + 31) / 32;
-    k_qr_fin<T><<<nf > 0 ? nf : 1, kQrThreads, 0, st>>>(W, n, j, b0, nb, u_f, partP, wT, scal, G, qflags);
+    k_qr_fin<T, PREC><<<nf > 0 ? nf : 1, kQrThreads, 0, st>>>(W, n, ldw, j, b0, nb, partP, wT, scal, G, qflags);
     ++nl;
     if (j + 1 < n) {
       const int bs = (int)(j / RB);       // CTAs whose rows are all < j would exit at once: not launched
-      rc = qr_step_launch<T, false, CPT>(W, A, dinv, j, RB, bs, nb - bs, u_f, wT, scal, partP, G, qflags, st);
+      rc = qr_step_launch<T, false, CPT, PREC>(W, A, ldw, dinv, j, RB, bs, nb - bs, wT, scal, partP, G, qflags, st);
       if (rc) return rc;
       ++nl;
     }
@@ -247,12 +405,12 @@ int qr_t(const DenseView& A, int u_f, const double* dinv, void* Wbuf, double* pa
   return 0;
 }
 
-template <typename T>
-int qr_dispatch(const DenseView& A, int u_f, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
+template <typename T, int PREC>
+int qr_dispatch(const DenseView& A, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
                 int* qflags, double* G, cudaStream_t st, int* launches) {
-  if (A.n <= 4 * kQrThreads) return qr_t<T, 4>(A, u_f, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
-  if (A.n <= 8 * kQrThreads) return qr_t<T, 8>(A, u_f, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
-  return qr_t<T, 16>(A, u_f, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
+  if (A.n <= 4 * kQrThreads) return qr_t<T, 4, PREC>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
+  if (A.n <= 8 * kQrThreads) return qr_t<T, 8, PREC>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
+  return qr_t<T, 16, PREC>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
 }
 }  // namespace
 
@@ -263,18 +421,24 @@ int qr_rows_per_cta(int64_t m, int n) {
   return (int)rb;
 }
 
+int qr_ldw(int n, int u_f) { return u_f == TLS_FP64 ? n : (n + 3) / 4 * 4; }
+
 size_t qr_work_bytes(int64_t m, int n, int u_f) {
   const int RB = qr_rows_per_cta(m, n);
   const int64_t nb = (m + RB - 1) / RB;
   const size_t es = (u_f == TLS_FP64) ? 8 : 4;
-  return (size_t)m * n * es + (size_t)nb * n * 8 + (size_t)n * 8 + 4 * (size_t)n * 8 + 5 * 256;
+  return (size_t)m * qr_ldw(n, u_f) * es + (size_t)nb * n * 8 + (size_t)n * 8 + 4 * (size_t)n * 8 + 5 * 256;
 }
 
 int launch_qr(const DenseView& A, int u_f, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
               int* qflags, double* G, cudaStream_t st, int* launches) {
   if (A.n > kMaxDenseN) { set_error("QR: n > %d", kMaxDenseN); return TLS_ERR_ARG; }
-  if (u_f == TLS_FP64) return qr_dispatch<double>(A, u_f, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
-  return qr_dispatch<float>(A, u_f, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
+  switch (u_f) {
+    case TLS_FP16: return qr_dispatch<float, TLS_FP16>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
+    case TLS_BF16: return qr_dispatch<float, TLS_BF16>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
+    case TLS_FP32: return qr_dispatch<float, TLS_FP32>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
+    default: return qr_dispatch<double, TLS_FP64>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
+  }
 }
 
 }  // namespace tls

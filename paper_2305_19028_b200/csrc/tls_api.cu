@@ -789,7 +789,7 @@ int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, v
   double* G = c.take<double>((size_t)n * n);
   const int RB = qr_rows_per_cta(A->m_local, n);
   const int64_t nb = (A->m_local + RB - 1) / RB;
-  void* Wq = c.take<char>((size_t)A->m_local * n * (u_f == TLS_FP64 ? 8 : 4));
+  void* Wq = c.take<char>((size_t)A->m_local * qr_ldw(n, u_f) * (u_f == TLS_FP64 ? 8 : 4));
   double* partP = c.take<double>((size_t)nb * n);
   double* wT = c.take<double>((size_t)n);
   double* scal = c.take<double>(4 * (size_t)n);
