@@ -153,3 +153,36 @@ def test_qr_refuses_csr_and_reports_workspace(T):
     assert T.lib().tls_qr_workspace_size(M, 0) >= 64 * 8 * 4
     with pytest.raises(T.TlsError):
         T.tls_factor_precond_qr(M, "fp16", ws=torch.empty(16, dtype=torch.uint8, device="cuda"))
+
+
+@pytest.mark.parametrize("name", tlsgen.PAPER_PROBLEMS)
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+def test_paper_sec4_problems_qr(T, name, fmt):
+    """The paper's §4 problems with the QR preconditioner it prefers (E5
+    compares it with the Cholesky one): the GPU's QR R~ against the oracle's, and the solve
+    on the GPU's R~ against the oracle on the same R~ (PCG counts within the north_star's +-2)."""
+    P = tlsgen.paper_problem(name)
+    M = T.matrix(T.dense_operand(dev(P.A)), n=P.n)
+    pc = rqi.factor_precond_qr(P.A, fmt)
+    rc, R, finfo = T.tls_factor_precond_qr(M, fmt)
+    assert rc == pc.status
+    if rc != 0:
+        assert finfo["chol_pivot"] == pc.chol_pivot
+        return
+    Rt, d, nrm = T.tls_precond_export(R)
+    m, n = P.A.shape
+    Ah = round_to(P.A / d, fmt)
+    assert np.linalg.norm(Rt.T @ Rt - Ah.T @ Ah) <= 10 * m * n * unit_roundoff(fmt) * np.linalg.norm(Ah) ** 2
+    assert _rel(Rt, pc.Rt) <= 10 * m * n * unit_roundoff(fmt) * np.linalg.cond(Ah)
+    rc, x, sig, info = T.tls_rqi_pcgtls(M, dev(P.b), R)
+    res = rqi.rqi_pcgtls_mp(P.A, P.b, rqi.Precond(Rt, d, fmt, nrm))
+    assert info["status"] == res.status
+    assert info["rqi_iters"] == res.rqi_iters
+    assert len(info["pcg_iters"]) == len(res.pcg_iters)
+    for a, b in zip(info["pcg_iters"], res.pcg_iters):
+        assert abs(a[0] - b[0]) <= 2 and abs(a[1] - b[1]) <= 2
+    if res.status == rqi.OK:
+        ex = exact.tls_svd(P.A, P.b)
+        assert _rel(x.cpu().numpy(), res.x) <= 1e-9
+        assert abs(sig - res.sigma) / res.sigma <= 1e-12
+        assert _rel(x.cpu().numpy(), ex.x) <= 1e-9
