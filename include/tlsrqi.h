@@ -169,16 +169,23 @@ TLS_API int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi
                        tls_precond_t* R_out, tls_info_t* info);
 
 /* ---- the paper's preferred preconditioner: Householder QR in u_f ----
- * PAPER.md l.215-218 and Alg. 4 l.231 "Compute A = Q[R 0]^T in u_q"; reading R25.
+ * PAPER.md l.215-218 and Alg. 4 l.231 "Compute A = Q[R 0]^T in u_q"; readings R25, R26.
  * R~ = the R factor (diag >= 0) of a Householder QR of fl_uf(A D^{-1}), with the same D
  * and ||A||_F^2 as tls_factor_precond; every elementwise operation is rounded to u_f, inner
  * products are accumulated in fp64 and rounded once.  The returned handle is used exactly
- * like a Cholesky one.  Dense A on one GPU only (CSR, or a comm of more than one rank:
- * TLS_ERR_ARG).  ws_dev: ws_bytes >= tls_qr_workspace_size(A, u_f) bytes (it holds an m x n
- * fp32 -- fp64 for u_f = TLS_FP64 -- working copy of A).  A column that becomes exactly zero
- * in u_f: TLS_CHOL_BREAKDOWN, info->chol_pivot = its 1-based index, *R_out = NULL.
- * A reflector overflowing u_f: TLS_RANGE. */
-TLS_API size_t tls_qr_workspace_size(const tls_matrix_t* A, int32_t u_f);
+ * like a Cholesky one.  Dense A only (CSR: TLS_ERR_ARG).
+ * Row-sharded A (comm with nranks > 1) or TSQR leaves (environment TLS_QR_LEAVES = k,
+ * default 1: each rank's rows split into k contiguous blocks [s m/k, (s+1) m/k)): every
+ * leaf is factored as above, the leaf R's are stacked in rank-major, leaf order (the
+ * stack all-reduced over the ranks; each rank fills only its own slots), and R~ is the R
+ * factor of the stack, computed the same way without further scaling (R26).  Every leaf
+ * needs >= n rows (else TLS_ERR_ARG).  R~ is identical on every rank.
+ * ws_dev: ws_bytes >= tls_qr_workspace_size(A, u_f, nranks) bytes (it holds an m_local x n
+ * fp32 -- fp64 for u_f = TLS_FP64 -- working copy of the rows, and for TSQR the stack and
+ * its working copy).  A column that becomes exactly zero in u_f: TLS_CHOL_BREAKDOWN,
+ * info->chol_pivot = its 1-based index (within the leaf or stack factorization where it
+ * happened), *R_out = NULL.  A reflector overflowing u_f: TLS_RANGE. */
+TLS_API size_t tls_qr_workspace_size(const tls_matrix_t* A, int32_t u_f, int32_t nranks);
 TLS_API int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, void* stream, void* ws_dev,
                                   size_t ws_bytes, tls_precond_t* R_out, tls_info_t* info);
 

@@ -60,3 +60,20 @@ def householder_qr_r(A: np.ndarray, fmt: str) -> np.ndarray:
     R = np.triu(W[:n, :n])
     sgn = np.where(np.diag(R) < 0, -1.0, 1.0)
     return R * sgn[:, None]
+
+
+def tsqr_r(A: np.ndarray, row_blocks, fmt: str) -> np.ndarray:
+    """TSQR (tall-skinny QR, reading R26): the R factors of the row blocks A[r0:r1] (each a
+    Householder QR in fmt, householder_qr_r) stacked in block order, then the R factor of that
+    stack, again by householder_qr_r.  In exact arithmetic this is the R of A (diag >= 0):
+    A = diag(Q_b) [R_1; ...; R_B] and [R_1; ...; R_B] = Q' R.  One block is the plain QR."""
+    if len(row_blocks) == 1:
+        r0, r1 = row_blocks[0]
+        return householder_qr_r(A[r0:r1], fmt)
+    return householder_qr_r(np.vstack([householder_qr_r(A[r0:r1], fmt) for r0, r1 in row_blocks]), fmt)
+
+
+def even_row_blocks(m: int, k: int):
+    """k contiguous row ranges [s m // k, (s + 1) m // k): the split of a row block into k
+    TSQR leaves (tlsrqi.h tls_factor_precond_qr)."""
+    return [(s * m // k, (s + 1) * m // k) for s in range(k)]

@@ -159,17 +159,18 @@ class Precond:
     W: Optional[np.ndarray] = None   # explicit inverse of R~ when the solve applies it (R24)
 
 
-def factor_precond_qr(A, u_f: str) -> Precond:
+def factor_precond_qr(A, u_f: str, row_blocks=None) -> Precond:
     """The paper's preferred preconditioner: R~ = the R factor
     of a Householder QR of A D^{-1} computed with every operation in u_f (oracle/qr.py,
-    reading R25), the same power-of-two scaling D as the Cholesky route.  Oracle only in
-    this round (the GPU path factors the Gram)."""
-    from .qr import householder_qr_r
+    reading R25), the same power-of-two scaling D as the Cholesky route (SURVEY §8(f)
+    NEXT-2; GPU: tls_factor_precond_qr).  row_blocks: the TSQR leaves (R26)."""
+    from .qr import householder_qr_r, tsqr_r
     A_d = A.toarray() if _is_sparse(A) else np.asarray(A)
     n = A_d.shape[1]
     d, normA2 = column_scaling(A)
     try:
-        Rt = householder_qr_r(A_d / d, u_f)
+        # row_blocks: the TSQR leaves of a row-sharded A (R26); None = one block
+        Rt = householder_qr_r(A_d / d, u_f) if row_blocks is None else tsqr_r(A_d / d, row_blocks, u_f)
     except ZeroDivisionError as e:   # 1-based index of the vanishing column (tlsrqi.h chol_pivot)
         return Precond(np.zeros((n, n)), d, u_f, normA2, CHOL_BREAKDOWN, getattr(e, "col", 0) + 1)
     if not np.all(np.isfinite(Rt)) or np.any(np.diag(Rt) == 0):

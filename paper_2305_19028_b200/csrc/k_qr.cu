@@ -91,11 +91,11 @@ __global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step(T* __
   S cur[CPT], nxt[CPT];
   const double alpha = LOAD ? 0.0 : scal[4 * j + 0];
   const double v0 = LOAD ? 0.0 : scal[4 * j + 1];
-  const double wc = LOAD ? dinv[0] : (c < n ? wT[c] : 0.0);     // LOAD: the scale of column 0
+  const double wc = LOAD ? (dinv ? dinv[0] : 1.0) : (c < n ? wT[c] : 0.0);   // LOAD: the scale of column 0
 #pragma unroll
   for (int q = 0; q < CPT; ++q) {
     const int k = c + tl + q * TG;
-    wk[q] = k < n ? (LOAD ? dinv[k] : wT[k]) : 0.0;             // LOAD: the column scales
+    wk[q] = k < n ? (LOAD ? (dinv ? dinv[k] : 1.0) : wT[k]) : 0.0;   // LOAD: the column scales (none: 1)
     acc[q] = 0.0;
   }
   int64_t i = r0 + tm;

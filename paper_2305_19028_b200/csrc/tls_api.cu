@@ -764,9 +764,60 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
   return 0;
 }
 
-size_t tls_qr_workspace_size(const tls_matrix_t* A, int32_t u_f) {
-  if (check_matrix(A) != 0 || is_csr(A) || u_f < TLS_FP16 || u_f > TLS_FP64) return 0;
-  return ws_need(A, false) + (size_t)A->n * A->n * 8 + 256 + qr_work_bytes(A->m_local, (int)A->n, u_f);
+namespace {
+// TSQR leaves per rank (R26): TLS_QR_LEAVES, default 1.  The tree is leaves -> one stack
+// factorization; > 1 on one GPU runs the same code path as a row-sharded factorization.
+int qr_leaves() {
+  const char* e = getenv("TLS_QR_LEAVES");
+  const int k = e ? atoi(e) : 1;
+  return k < 1 ? 1 : (k > 64 ? 64 : k);
+}
+
+struct QrBufs {
+  double* G = nullptr;      // n x n R of the last factorization (lower part zero)
+  void* W1 = nullptr;       // working copy of the local rows
+  double* part1 = nullptr;
+  double* S = nullptr;      // (leaves x n) x n stack of leaf R's
+  void* W2 = nullptr;       // working copy of the stack
+  double* part2 = nullptr;
+  double* wT = nullptr;
+  double* scal = nullptr;
+  int* qflags = nullptr;
+};
+
+size_t qr_partials(int64_t m, int n) {
+  const int RB = qr_rows_per_cta(m, n);
+  return (size_t)((m + RB - 1) / RB) * n;
+}
+
+// Carves (or, with ws == nullptr, measures) the QR buffers after the solve workspace.
+size_t carve_qr(const tls_matrix_t* A, int u_f, int nleaf, void* ws, size_t bytes, QrBufs& q, bool* ok) {
+  const int n = (int)A->n;
+  const size_t base = ws_need(A, false);
+  Carver c{ws ? static_cast<char*>(ws) + base : nullptr, (ws && bytes > base) ? bytes - base : 0};
+  const size_t es = (u_f == TLS_FP64) ? 8 : 4;
+  const size_t ldw = (size_t)qr_ldw(n, u_f);
+  q.G = c.take<double>((size_t)n * n);
+  q.W1 = c.take<char>((size_t)A->m_local * ldw * es);
+  q.part1 = c.take<double>(qr_partials(A->m_local, n));
+  if (nleaf > 1) {
+    const int64_t ms = (int64_t)nleaf * n;
+    q.S = c.take<double>((size_t)ms * n);
+    q.W2 = c.take<char>((size_t)ms * ldw * es);
+    q.part2 = c.take<double>(qr_partials(ms, n));
+  }
+  q.wT = c.take<double>((size_t)n);
+  q.scal = c.take<double>(4 * (size_t)n);
+  q.qflags = c.take<int>(4);
+  if (ok) *ok = c.ok && ws != nullptr;
+  return base + c.off;
+}
+}  // namespace
+
+size_t tls_qr_workspace_size(const tls_matrix_t* A, int32_t u_f, int32_t nranks) {
+  if (check_matrix(A) != 0 || is_csr(A) || u_f < TLS_FP16 || u_f > TLS_FP64 || nranks < 1) return 0;
+  QrBufs q;
+  return carve_qr(A, u_f, nranks * qr_leaves(), nullptr, 0, q, nullptr);
 }
 
 int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, void* stream, void* ws,
@@ -776,32 +827,30 @@ int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, v
   TLS_TRY(check_matrix(A));
   if (!R_out || u_f < TLS_FP16 || u_f > TLS_FP64) { set_error("bad u_f or R_out"); return TLS_ERR_ARG; }
   if (is_csr(A)) { set_error("the QR preconditioner takes a dense A"); return TLS_ERR_ARG; }
-  if (comm != nullptr && comm->nranks > 1) { set_error("the QR preconditioner is single-GPU in this build"); return TLS_ERR_ARG; }
-  const size_t need = tls_qr_workspace_size(A, u_f);
+  const int n = (int)A->n;
+  const int P = comm ? comm->nranks : 1;
+  const int rank = comm ? comm->rank : 0;
+  const int sub = qr_leaves();
+  const int nleaf = P * sub;
+  if (nleaf > 1 && A->m_local / sub < n) {
+    set_error("TSQR: every leaf needs >= n rows (m_local = %lld, %d leaves per rank, n = %d)",
+              (long long)A->m_local, sub, n);
+    return TLS_ERR_ARG;
+  }
   Work w;
-  if (ws == nullptr || ws_bytes < need || !carve_ok(A, ws, ws_bytes, w, false)) {
+  QrBufs q;
+  bool ok = false;
+  const size_t need = carve_qr(A, u_f, nleaf, ws, ws_bytes, q, &ok);
+  if (!ok || ws_bytes < need || !carve_ok(A, ws, ws_bytes, w, false)) {
     set_error("workspace too small (need %zu)", need);
     return TLS_ERR_WORKSPACE;
   }
-  const int n = (int)A->n;
-  const size_t base = ws_need(A, false);
-  Carver c{static_cast<char*>(ws) + base, ws_bytes - base};
-  double* G = c.take<double>((size_t)n * n);
-  const int RB = qr_rows_per_cta(A->m_local, n);
-  const int64_t nb = (A->m_local + RB - 1) / RB;
-  void* Wq = c.take<char>((size_t)A->m_local * qr_ldw(n, u_f) * (u_f == TLS_FP64 ? 8 : 4));
-  double* partP = c.take<double>((size_t)nb * n);
-  double* wT = c.take<double>((size_t)n);
-  double* scal = c.take<double>(4 * (size_t)n);
-  int* qflags = c.take<int>(4);
-  if (!c.ok) { set_error("workspace too small (need %zu)", need); return TLS_ERR_WORKSPACE; }
   Ctx cx{static_cast<cudaStream_t>(stream), comm};
   Tracer tr(cx.st);
   tr.mark("qr:start");
   TLS_CUDA_TRY(cudaMemsetAsync(w.flags, 0, 8 * sizeof(int), cx.st));
-  TLS_CUDA_TRY(cudaMemsetAsync(qflags, 0, 4 * sizeof(int), cx.st));
-  TLS_CUDA_TRY(cudaMemsetAsync(G, 0, (size_t)n * n * 8, cx.st));
-  // the same D = powers of two and ||A||_F^2 as the Cholesky route (R2)
+  TLS_CUDA_TRY(cudaMemsetAsync(q.qflags, 0, 4 * sizeof(int), cx.st));
+  // the same D = powers of two and ||A||_F^2 as the Cholesky route (R2), all-reduced
   TLS_TRY(run_pass(cx, A, PASS_COLSTATS, 2, nullptr, nullptr, w, nullptr));
   double* d = w.d_tmp;
   double* dinv = w.d_tmp + n;
@@ -811,21 +860,42 @@ int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, v
   tr.mark("colstats");
   {
     ProfScope ps(TLS_PROF_CHOL, cx.st);
-    TLS_TRY(launch_qr(dense_view(A), u_f, dinv, Wq, partP, wT, scal, qflags, G, cx.st, &cx.launches));
+    if (nleaf == 1) {
+      TLS_CUDA_TRY(cudaMemsetAsync(q.G, 0, (size_t)n * n * 8, cx.st));
+      TLS_TRY(launch_qr(dense_view(A), u_f, dinv, q.W1, q.part1, q.wT, q.scal, q.qflags, q.G, cx.st, &cx.launches));
+      cx.passes += n + 1;
+    } else {
+      // TSQR (R26): leaf R's of this rank's row blocks into their slots of the stack,
+      // the stack summed over ranks (all other slots are zero: exact), then its R.
+      TLS_CUDA_TRY(cudaMemsetAsync(q.S, 0, (size_t)nleaf * n * n * 8, cx.st));
+      const int64_t ml = A->m_local;
+      for (int s = 0; s < sub; ++s) {
+        const int64_t r0 = s * ml / sub, r1 = (s + 1) * ml / sub;
+        DenseView leaf{A->vals + r0 * A->ld, r1 - r0, n, A->ld};
+        TLS_CUDA_TRY(cudaMemsetAsync(q.G, 0, (size_t)n * n * 8, cx.st));
+        TLS_TRY(launch_qr(leaf, u_f, dinv, q.W1, q.part1, q.wT, q.scal, q.qflags, q.G, cx.st, &cx.launches));
+        TLS_CUDA_TRY(cudaMemcpyAsync(q.S + (size_t)(rank * sub + s) * n * n, q.G, (size_t)n * n * 8,
+                                     cudaMemcpyDeviceToDevice, cx.st));
+        cx.passes += n + 1;
+      }
+      if (P > 1) TLS_TRY(allreduce(comm, q.S, (size_t)nleaf * n * n, ncclSum, cx.st));
+      TLS_CUDA_TRY(cudaMemsetAsync(q.G, 0, (size_t)n * n * 8, cx.st));
+      DenseView stack{q.S, (int64_t)nleaf * n, n, n};
+      TLS_TRY(launch_qr(stack, u_f, nullptr, q.W2, q.part2, q.wT, q.scal, q.qflags, q.G, cx.st, &cx.launches));
+    }
   }
-  cx.passes += n + 1;
   tr.mark("qr");
   tls_precond_t h = nullptr;
   TLS_TRY(alloc_precond(n, u_f, &h));
   k_fill_scaling<<<(h->dev.npad + 255) / 256, 256, 0, cx.st>>>(h->dev.d, h->dev.dinv, d, dinv, n, h->dev.npad);
   TLS_CUDA_TRY(cudaMemcpyAsync(h->dev.normA2, normA2, sizeof(double), cudaMemcpyDeviceToDevice, cx.st));
-  int rc = launch_pack_R(G, n, 0, h->dev, &w.flags[3], cx.st, &cx.launches);
+  int rc = launch_pack_R(q.G, n, 0, h->dev, &w.flags[3], cx.st, &cx.launches);
   cx.launches += 1;
   if (rc) { tls_precond_destroy(h); return rc; }
   int hflags[8], hq[4];
   double hnorm = 0.0;
   TLS_CUDA_TRY(cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, cx.st));
-  TLS_CUDA_TRY(cudaMemcpyAsync(hq, qflags, sizeof(hq), cudaMemcpyDeviceToHost, cx.st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(hq, q.qflags, sizeof(hq), cudaMemcpyDeviceToHost, cx.st));
   TLS_CUDA_TRY(cudaMemcpyAsync(&hnorm, normA2, sizeof(double), cudaMemcpyDeviceToHost, cx.st));
   TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
   tr.mark("sync");

@@ -153,6 +153,7 @@ int launch_certify(const DenseView* D, const CsrView* S, const double* b, const 
 int qr_rows_per_cta(int64_t m, int n);
 int qr_ldw(int n, int u_f);                        // row stride of the working copy
 size_t qr_work_bytes(int64_t m, int n, int u_f);   // W copy + partials + w^T + scalars + flags
+// dinv == nullptr: no scaling (the TSQR stack of already scaled leaf R's)
 int launch_qr(const DenseView& A, int u_f, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
               int* qflags, double* G, cudaStream_t st, int* launches);
 

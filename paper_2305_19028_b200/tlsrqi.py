@@ -74,7 +74,7 @@ def lib() -> C.CDLL:
         "tls_comm_destroy": (C.c_int, [VP]),
         "tls_workspace_size": (SZ, [M, I32]),
         "tls_factor_precond": (C.c_int, [M, I32, P(tls_rqi_opts_t), VP, VP, VP, SZ, P(VP), P(tls_info_t)]),
-        "tls_qr_workspace_size": (SZ, [M, I32]),
+        "tls_qr_workspace_size": (SZ, [M, I32, I32]),
         "tls_factor_precond_qr": (C.c_int, [M, I32, VP, VP, VP, SZ, P(VP), P(tls_info_t)]),
         "tls_precond_import": (C.c_int, [I64, I32, VP, VP, D, VP, P(VP)]),
         "tls_precond_export": (C.c_int, [VP, VP, VP, P(D)]),
@@ -266,11 +266,13 @@ def tls_factor_precond(M: tls_matrix_t, u_f, opts: Optional[tls_rqi_opts_t] = No
     return rc, (Precond(R.value, int(M.n), uf) if R.value else None), d
 
 
-def tls_factor_precond_qr(M: tls_matrix_t, u_f, comm=None, stream=None, ws: Optional[torch.Tensor] = None):
-    """Householder-QR preconditioner in u_f (NEXT-2, R25).  Returns (status, Precond or None, info dict)."""
+def tls_factor_precond_qr(M: tls_matrix_t, u_f, comm=None, stream=None, ws: Optional[torch.Tensor] = None,
+                          nranks: int = 1):
+    """Householder-QR preconditioner in u_f (NEXT-2, R25; TSQR over ranks / TLS_QR_LEAVES, R26).
+    Returns (status, Precond or None, info dict)."""
     uf = PREC[u_f] if isinstance(u_f, str) else int(u_f)
     if ws is None:
-        nbytes = int(lib().tls_qr_workspace_size(C.byref(M), uf))
+        nbytes = int(lib().tls_qr_workspace_size(C.byref(M), uf, nranks))
         if nbytes == 0:
             raise TlsError(-1, "tls_qr_workspace_size")
         ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")

@@ -159,3 +159,45 @@ def test_row_sharded_solve_world2():
         r = out[rank]
         assert r["same"] and r["replicas"]
         assert r["x_rel"] < 1e-12 and r["sig_rel"] < 1e-13
+
+
+def _tsqr_worker(rank, world, port, out):
+    """The exchange of the row-sharded QR preconditioner (tls_factor_precond_qr, R26): each
+    rank factors its own rows (D from the all-reduced column maxima), writes its R into its
+    slot of a zeroed (world n) x n stack, the stack is sum-all-reduced (every other slot is
+    zero, so the sum is exact), and every rank factors the stack."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.qr import householder_qr_r
+        P = tlsgen.config("cfg1")
+        A = P.A
+        m, n = A.shape
+        lo, hi = shard_rows(m, world, rank)
+        cm = _allreduce(np.max(np.abs(A[lo:hi]), axis=0), tdist.ReduceOp.MAX)
+        d = np.exp2(np.floor(np.log2(cm)))
+        S = np.zeros((world * n, n))
+        S[rank * n:(rank + 1) * n] = householder_qr_r(A[lo:hi] / d, "fp16")
+        S = _allreduce(S)
+        R = householder_qr_r(S, "fp16")
+        pc = rqi.factor_precond_qr(A, "fp16", row_blocks=[shard_rows(m, world, r) for r in range(world)])
+        allR = [torch.zeros(n * n, dtype=torch.float64) for _ in range(world)]
+        tdist.all_gather(allR, torch.from_numpy(R.ravel().copy()))
+        out[rank] = {"equal_oracle": bool(np.array_equal(R, pc.Rt)), "d_equal": bool(np.array_equal(d, pc.d)),
+                     "replicas": all(np.array_equal(allR[0].numpy(), t.numpy()) for t in allR)}
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_row_sharded_qr_preconditioner_world2():
+    """The TSQR exchange on two gloo ranks reproduces the oracle's TSQR with the shards as
+    leaves bit for bit, identically on both ranks."""
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_tsqr_worker, args=(world, port, out), nprocs=world, join=True)
+    for rank in range(world):
+        r = out[rank]
+        assert r["equal_oracle"] and r["d_equal"] and r["replicas"]

@@ -150,7 +150,8 @@ def test_qr_zero_column_breakdown(T):
 def test_qr_refuses_csr_and_reports_workspace(T):
     A, _ = _problem(64, 8, 10.0, seed=1)
     M = T.matrix(dev(A))
-    assert T.lib().tls_qr_workspace_size(M, 0) >= 64 * 8 * 4
+    assert T.lib().tls_qr_workspace_size(M, 0, 1) >= 64 * 8 * 4
+    assert T.lib().tls_qr_workspace_size(M, 0, 2) > T.lib().tls_qr_workspace_size(M, 0, 1)   # + the TSQR stack
     with pytest.raises(T.TlsError):
         T.tls_factor_precond_qr(M, "fp16", ws=torch.empty(16, dtype=torch.uint8, device="cuda"))
 
@@ -186,3 +187,40 @@ def test_paper_sec4_problems_qr(T, name, fmt):
         assert _rel(x.cpu().numpy(), res.x) <= 1e-9
         assert abs(sig - res.sigma) / res.sigma <= 1e-12
         assert _rel(x.cpu().numpy(), ex.x) <= 1e-9
+
+
+@pytest.mark.parametrize("leaves,m,n,fmt", [(2, 200, 20, "fp16"), (3, 777, 67, "bf16"), (4, 1200, 270, "fp16"),
+                                            (2, 300, 31, "fp64")])
+def test_qr_tsqr_leaves(T, monkeypatch, leaves, m, n, fmt):
+    """TSQR (R26) through the same code path a row-sharded factorization takes, on one GPU:
+    TLS_QR_LEAVES = k splits the rows into k leaves.  Against the oracle's tsqr_r on the same
+    leaves (bounds as in test_qr_factor_parity, two levels), then a solve on that R~."""
+    from oracle.qr import even_row_blocks
+    monkeypatch.setenv("TLS_QR_LEAVES", str(leaves))
+    A, b = _problem(m, n, 1e2, seed=3 * m + n, spread=False)
+    M, keep = _mat(T, A)
+    rc, R, info = T.tls_factor_precond_qr(M, fmt)
+    assert rc == 0
+    pc = rqi.factor_precond_qr(A, fmt, row_blocks=even_row_blocks(m, leaves))
+    Rt, d, nrm = T.tls_precond_export(R)
+    assert np.array_equal(d, pc.d)
+    assert np.all(np.diag(Rt) > 0) and np.array_equal(round_to(Rt, fmt), Rt)
+    u = unit_roundoff(fmt)
+    Ah = round_to(A / d, fmt)
+    assert np.linalg.norm(Rt.T @ Rt - Ah.T @ Ah) <= 2 * 10 * m * n * u * np.linalg.norm(Ah) ** 2
+    assert _rel(Rt, pc.Rt) <= 2 * 10 * m * n * u * np.linalg.cond(Ah)
+    rc, x, sig, info = T.tls_rqi_pcgtls(M, dev(b), R)
+    res = rqi.rqi_pcgtls_mp(A, b, rqi.Precond(Rt, d, fmt, nrm))
+    assert info["status"] == res.status == rqi.OK
+    assert info["rqi_iters"] == res.rqi_iters
+    assert info["pcg_iters"] == [tuple(p) for p in res.pcg_iters]
+    assert _rel(x.cpu().numpy(), res.x) <= 1e-9
+    assert abs(sig - res.sigma) / res.sigma <= 1e-12
+
+
+def test_qr_tsqr_leaf_too_short(T, monkeypatch):
+    monkeypatch.setenv("TLS_QR_LEAVES", "8")
+    A, _ = _problem(100, 20, 10.0, seed=2)
+    M, keep = _mat(T, A)
+    with pytest.raises(T.TlsError):
+        T.tls_factor_precond_qr(M, "fp16")

@@ -90,3 +90,35 @@ def test_zero_column_reports_its_pivot():
         assert e.value.col == 1
         pc = rqi.factor_precond_qr(A, fmt)
         assert pc.status == rqi.CHOL_BREAKDOWN and pc.chol_pivot == 2
+
+
+def test_tsqr_fp64_equals_lapack_r():
+    """TSQR (R26) in fp64: the R of the stacked leaf R's is LAPACK's R of the whole A up to
+    row signs (A = diag(Q_b)[R_1; ...; R_B], [R_1; ...; R_B] = Q'R), for 1, 2, 3 and 5 leaves;
+    a dropped or duplicated leaf changes R^T R = A^T A and fails."""
+    from oracle.qr import even_row_blocks, tsqr_r
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((97, 9))
+    R0 = np.linalg.qr(A, mode="r")
+    R0 = R0 * np.where(np.diag(R0) < 0, -1.0, 1.0)[:, None]
+    for k in (1, 2, 3, 5):
+        R = tsqr_r(A, even_row_blocks(97, k), "fp64")
+        assert np.max(np.abs(R - R0)) <= 1e-13 * np.max(np.abs(R0))
+    # the leaves cover the rows exactly once
+    for m, k in ((97, 5), (4096, 3), (10, 10)):
+        bl = even_row_blocks(m, k)
+        assert bl[0][0] == 0 and bl[-1][1] == m and all(a[1] == b[0] for a, b in zip(bl, bl[1:]))
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16", "fp32"])
+def test_tsqr_backward_error_bound(fmt):
+    """Two levels of Householder QR in fmt: ||R^T R - Ah^T Ah||_F <= 2 x 10 m n u ||Ah||_F^2
+    (each level's Gram residual bound, the leaf one applied block by block)."""
+    from oracle.qr import even_row_blocks, tsqr_r
+    rng = np.random.default_rng(5)
+    m, n = 300, 12
+    A = round_to(rng.standard_normal((m, n)) * np.logspace(0, -1, n)[None, :], fmt)
+    R = tsqr_r(A, even_row_blocks(m, 3), fmt)
+    u = unit_roundoff(fmt)
+    assert np.all(np.diag(R) > 0)
+    assert np.linalg.norm(R.T @ R - A.T @ A) <= 2 * 10 * m * n * u * np.linalg.norm(A) ** 2
