@@ -11,7 +11,8 @@ REPS = [("k_pass<2,op> fp64 operator pass (a7)", "profiles/r01_k_pass_full.ncu-r
         ("k_chol_dag (a3, n=1024)", "profiles/r01_chol_full.ncu-rep"),
         ("k_pcg_step (a6+a8, 8-CTA cluster)", "profiles/r01_pcg_step.ncu-rep"),
         ("k_csr_rows (a7 CSR, cfg3)", "profiles/r01_k_csr_rows.ncu-rep"),
-        ("k_csr_cols (a7 CSR, cfg3)", "profiles/r01_k_csr_cols.ncu-rep")]
+        ("k_csr_cols (a7 CSR, cfg3)", "profiles/r01_k_csr_cols.ncu-rep"),
+        ("k_qr_step_v4 (NEXT-2 QR, 65536x2048, j=600)", "profiles/r01_ncu_qr_step_v4.ncu-rep")]
 def raw(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
