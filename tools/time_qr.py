@@ -14,7 +14,7 @@ for m, n in shapes:
         torch.logspace(0, -2, n, dtype=torch.float64, device="cuda")[None, :]
     M = tlsrqi.matrix(A)
     for fmt in ("fp16", "bf16"):
-        wq = torch.empty(int(tlsrqi.lib().tls_qr_workspace_size(M, tlsrqi.PREC[fmt])), dtype=torch.uint8, device="cuda")
+        wq = torch.empty(int(tlsrqi.lib().tls_qr_workspace_size(M, tlsrqi.PREC[fmt], 1)), dtype=torch.uint8, device="cuda")
         wc = tlsrqi.workspace(M)
         out = {}
         for name, fn in (("qr", lambda: tlsrqi.tls_factor_precond_qr(M, fmt, ws=wq)),
