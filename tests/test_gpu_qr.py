@@ -224,3 +224,30 @@ def test_qr_tsqr_leaf_too_short(T, monkeypatch):
     M, keep = _mat(T, A)
     with pytest.raises(T.TlsError):
         T.tls_factor_precond_qr(M, "fp16")
+
+
+@pytest.mark.parametrize("m,n,fmt", [(5, 1, "fp16"), (2300, 2100, "fp16"), (4200, 4096, "bf16")])
+def test_qr_extreme_widths(T, m, n, fmt):
+    """n = 1 (no update pass at all) and n > 2048 (16 columns per thread; n = 4096 is the
+    largest dense n): the R~ the GPU returns is a QR factor of fl(A D^{-1}) within the pinned
+    backward-error bound, upper with a positive diagonal, in u_f; then a solve on it matches
+    the oracle run on the same R~."""
+    A, b = _problem(m, n, 10.0, seed=m + 7 * n, spread=False)
+    M, keep = _mat(T, A)
+    rc, R, _ = T.tls_factor_precond_qr(M, fmt)
+    assert rc == 0
+    Rt, d, nrm = T.tls_precond_export(R)
+    assert np.array_equal(np.tril(Rt, -1), np.zeros_like(Rt)) and np.all(np.diag(Rt) > 0)
+    assert np.array_equal(round_to(Rt, fmt), Rt)
+    Ah = round_to(A / d, fmt)
+    assert np.linalg.norm(Rt.T @ Rt - Ah.T @ Ah) <= 10 * m * n * unit_roundoff(fmt) * np.linalg.norm(Ah) ** 2
+    if n == 1:
+        assert Rt[0, 0] == pytest.approx(np.linalg.norm(Ah), rel=2 * unit_roundoff(fmt))
+        return
+    rc, x, sig, info = T.tls_rqi_pcgtls(M, dev(b), R)
+    res = rqi.rqi_pcgtls_mp(A, b, rqi.Precond(Rt, d, fmt, nrm))
+    assert info["status"] == res.status
+    assert info["rqi_iters"] == res.rqi_iters
+    if res.status == rqi.OK:
+        assert _rel(x.cpu().numpy(), res.x) <= 1e-9
+        assert abs(sig - res.sigma) / res.sigma <= 1e-12
