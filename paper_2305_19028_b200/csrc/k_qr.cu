@@ -17,6 +17,7 @@
 // per CTA, so column j+1's reflector needs no second pass; k_qr_fin reduces those partials
 // (fixed order, deterministic), forms the column's scalars and w^T.  2 launches per column.
 #include <cuda_bf16.h>
+#include <cstdlib>
 
 #include "tls_common.cuh"
 #include "tls_kernels.h"
@@ -75,6 +76,9 @@ __global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step(T* __
                                                          const double* __restrict__ scal, double* __restrict__ partP,
                                                          double* __restrict__ G, const int* __restrict__ dead) {
   extern __shared__ double qsm[];
+  // programmatic dependent launch: wait for the predecessor's writes before reading anything;
+  // the next kernel is released after the row loop (below)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (!LOAD && *dead) return;
   const int c = j + 1;
   const int ncols = n - c;
@@ -155,6 +159,7 @@ __global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step(T* __
     i = inext;
     have = hn;
   }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (teams == 1) {
 #pragma unroll
     for (int q = 0; q < CPT; ++q) {
@@ -187,6 +192,9 @@ __global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step_v4(
     double* __restrict__ G, const int* __restrict__ dead) {
   constexpr int GPT = CPT / 4;
   extern __shared__ double qsm[];
+  // programmatic dependent launch: wait for the predecessor's writes before reading anything;
+  // the next kernel is released after the row loop (below)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (*dead) return;
   const int c = j + 1, c0 = c & ~3;
   const int ngroups = (ldw - c0) >> 2;
@@ -259,6 +267,7 @@ __global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step_v4(
     i = inext;
     have = hn;
   }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int ncv = ngroups * 4;
   if (teams > 1) {
 #pragma unroll
@@ -298,6 +307,10 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_fin(const T* __restrict__ W, 
                                                         double* __restrict__ scal, double* __restrict__ G,
                                                         int* __restrict__ qflags) {
   __shared__ double red[32];
+  // programmatic dependent launch: the next kernel of the chain may be scheduled now; this
+  // one waits for its predecessor's writes before reading anything
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ double cs[8][32];
   constexpr int prec = PREC;
   if (qflags[0]) return;
@@ -343,6 +356,29 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_fin(const T* __restrict__ W, 
   }
 }
 
+// Launch with programmatic stream serialisation (PDL): the kernels of the per-column chain
+// overlap their launch with the tail of the previous one (each waits on griddepcontrol).
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool pdl = [] { const char* e = getenv("TLS_QR_PDL"); return !(e && e[0] == '0'); }();
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k, args...);
+  if (e != cudaSuccess) {
+    set_error("k_qr launch: %s", cudaGetErrorString(e));
+    return TLS_ERR_CUDA;
+  }
+  return 0;
+}
+
 // Team size for a pass over `ncols` columns with CPT columns per thread.
 inline int qr_team(int ncols, int cpt) {
   int tg = (ncols + cpt - 1) / cpt;
@@ -361,18 +397,16 @@ int qr_step_launch(T* W, const DenseView& A, int ldw, const double* dinv, int j,
     const int TG = qr_team(ngroups, CPT / 4);
     const int teams = kQrThreads / TG;
     const size_t smem = teams > 1 ? (size_t)teams * ngroups * 4 * sizeof(double) : 0;
-    k_qr_step_v4<CPT, PREC><<<nblk, teams * TG, smem, st>>>(reinterpret_cast<float*>(W), A.m, n, ldw, j, RB, bfirst,
-                                                            TG, wT, scal, partP, G, qflags);
+    return launch_pdl(k_qr_step_v4<CPT, PREC>, nblk, teams * TG, smem, st, reinterpret_cast<float*>(W), A.m, n, ldw,
+                      j, RB, bfirst, TG, wT, scal, partP, G, qflags);
   } else {
     const int ncols = n - (j + 1);
     const int TG = qr_team(ncols, CPT);
     const int teams = kQrThreads / TG;
     const size_t smem = teams > 1 ? (size_t)teams * ncols * sizeof(double) : 0;
-    k_qr_step<T, LOAD, CPT, PREC><<<nblk, teams * TG, smem, st>>>(W, A.A, A.ld, dinv, A.m, n, ldw, j, RB, bfirst, TG,
-                                                                  wT, scal, partP, G, qflags);
+    return launch_pdl(k_qr_step<T, LOAD, CPT, PREC>, nblk, teams * TG, smem, st, W, A.A, A.ld, dinv, A.m, n, ldw, j,
+                      RB, bfirst, TG, wT, scal, partP, G, qflags);
   }
-  TLS_LAUNCH_CHECK();
-  return 0;
 }
 
 template <typename T, int CPT, int PREC>
@@ -391,7 +425,9 @@ int qr_t(const DenseView& A, const double* dinv, void* Wbuf, double* partP, doub
     // partials of column j were written by the pass with first row max(j - 1, 0)
     const int b0 = (int)((j > 0 ? j - 1 : 0) / RB);
     const int nf = (n - j - 1 + 31) / 32;
-    k_qr_fin<T, PREC><<<nf > 0 ? nf : 1, kQrThreads, 0, st>>>(W, n, ldw, j, b0, nb, partP, wT, scal, G, qflags);
+    rc = launch_pdl(k_qr_fin<T, PREC>, nf > 0 ? nf : 1, kQrThreads, 0, st, (const T*)W, n, ldw, j, b0, nb,
+                    (const double*)partP, wT, scal, G, qflags);
+    if (rc) return rc;
     ++nl;
     if (j + 1 < n) {
       const int bs = (int)(j / RB);       // CTAs whose rows are all < j would exit at once: not launched
