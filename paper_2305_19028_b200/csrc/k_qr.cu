@@ -16,6 +16,7 @@
 // accumulates the fp64 partial inner products of the NEXT column (x'^T x' and x'^T W')
 // per CTA, so column j+1's reflector needs no second pass; k_qr_fin reduces those partials
 // (fixed order, deterministic), forms the column's scalars and w^T.  2 launches per column.
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 #include <cstdlib>
 
@@ -23,6 +24,7 @@
 #include "tls_kernels.h"
 
 namespace tls {
+namespace cg = cooperative_groups;
 
 namespace {
 constexpr int kQrThreads = 256;
@@ -37,6 +39,14 @@ template <int PREC> __device__ __forceinline__ float qr_rdf(float x) {
 template <typename T> __device__ __forceinline__ T qr_store(double v);
 template <> __device__ __forceinline__ float qr_store<float>(double v) { return (float)v; }   // exact: v in u_f
 template <> __device__ __forceinline__ double qr_store<double>(double v) { return v; }
+
+// Team size for a pass over `ncols` columns with CPT columns per thread.
+__host__ __device__ inline int qr_team(int ncols, int cpt) {
+  int tg = (ncols + cpt - 1) / cpt;
+  tg = (tg + 31) / 32 * 32;
+  if (tg < 32) tg = 32;
+  return tg > kQrThreads ? kQrThreads : tg;
+}
 
 // scal[j]: {alpha, v_0, sigma, beta}
 // One pass.  LOAD: W = fl_uf(A D^{-1}) and the partials of column 0.  Otherwise: apply
@@ -185,25 +195,21 @@ __global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step(T* __
 // thread tl owns the 4-column groups g = tl + q TG starting at the aligned column c0 = c & ~3
 // (ldw is a multiple of 4).  Columns k < c and k >= n carry w_k = 0, so they are rewritten
 // with their own values (rd(x - rd(v 0)) = x) and need no masks.
+// Row block b's share of column j's update pass (the body of k_qr_step_v4 and of one column
+// of k_qr_coop); `teams` teams of TG threads, threads beyond teams x TG only join the combine.
 template <int CPT, int PREC>
-__global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step_v4(
-    float* __restrict__ W, int64_t m, int n, int ldw, int j, int RB, int bfirst, int TG,
-    const double* __restrict__ wT, const double* __restrict__ scal, double* __restrict__ partP,
-    double* __restrict__ G, const int* __restrict__ dead) {
+__device__ __forceinline__ void qr_update_v4(float* __restrict__ W, int64_t m, int n, int ldw, int j, int RB, int b,
+                                             int TG, int teams, const double* __restrict__ wT,
+                                             const double* __restrict__ scal, double* __restrict__ partP,
+                                             double* __restrict__ G, double* qsm, bool pdl_release) {
   constexpr int GPT = CPT / 4;
-  extern __shared__ double qsm[];
-  // programmatic dependent launch: wait for the predecessor's writes before reading anything;
-  // the next kernel is released after the row loop (below)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (*dead) return;
   const int c = j + 1, c0 = c & ~3;
   const int ngroups = (ldw - c0) >> 2;
-  const int b = bfirst + (int)blockIdx.x;
   int64_t r0 = (int64_t)b * RB;
   const int64_t r1 = min(m, r0 + RB);
   if (r1 <= j) return;
   if (r0 < j) r0 = j;
-  const int t = threadIdx.x, tm = t / TG, tl = t % TG, teams = blockDim.x / TG;
+  const int t = threadIdx.x, tm = t / TG, tl = t % TG;
   const double alpha = scal[4 * j + 0];
   const float v0f = (float)scal[4 * j + 1];
   const float wcf = (float)wT[c];
@@ -221,7 +227,7 @@ __global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step_v4(
   float4 cur[GPT], nxt[GPT];
   float nj = 0.f, nc = 0.f;
   int64_t i = r0 + tm;
-  bool have = i < r1;
+  bool have = tm < teams && i < r1;
   auto load = [&](int64_t ii) {   // the next row of this team, in flight while row i is updated
     const float* src = W + ii * (int64_t)ldw;
     nj = src[j];
@@ -267,7 +273,7 @@ __global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step_v4(
     i = inext;
     have = hn;
   }
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (pdl_release) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int ncv = ngroups * 4;
   if (teams > 1) {
 #pragma unroll
@@ -275,10 +281,10 @@ __global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step_v4(
       const int g = tl + q * TG;
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (g < ngroups) qsm[tm * ncv + 4 * g + e] = acc[4 * q + e];
+        if (tm < teams && g < ngroups) qsm[tm * ncv + 4 * g + e] = acc[4 * q + e];
     }
     __syncthreads();
-    for (int kk = t; kk < ncv; kk += blockDim.x) {
+    for (int kk = t; kk < ncv; kk += blockDim.x) {   // (teams x ncv doubles of qsm)
       const int k = c0 + kk;
       if (k < c || k >= n) continue;
       double sum = 0.0;
@@ -293,8 +299,101 @@ __global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step_v4(
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int k = c0 + 4 * g + e;
-      if (g < ngroups && k >= c && k < n) partP[(int64_t)b * n + k] = acc[4 * q + e];
+      if (tm < teams && g < ngroups && k >= c && k < n) partP[(int64_t)b * n + k] = acc[4 * q + e];
     }
+  }
+}
+
+template <int CPT, int PREC>
+__global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step_v4(
+    float* __restrict__ W, int64_t m, int n, int ldw, int j, int RB, int bfirst, int TG,
+    const double* __restrict__ wT, const double* __restrict__ scal, double* __restrict__ partP,
+    double* __restrict__ G, const int* __restrict__ dead) {
+  extern __shared__ double qsm[];
+  // programmatic dependent launch: wait for the predecessor's writes before reading anything;
+  // the next kernel is released after the row loop
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (*dead) return;
+  qr_update_v4<CPT, PREC>(W, m, n, ldw, j, RB, bfirst + (int)blockIdx.x, TG, (int)blockDim.x / TG, wT, scal, partP, G,
+                          qsm, true);
+}
+
+// ---------------------------------------------------------------- one persistent kernel
+// The whole column loop of the fp32 working copy in ONE cooperative launch (all CTAs
+// resident): per column, every CTA forms the column's scalars from the partials (same bits
+// in every CTA), reduces its slice of w^T, grid barrier, its rows' update pass (with the next
+// column's partials), grid barrier.  Replaces 2 launches per column and k_qr_fin's latency,
+// but measured slower than the PDL chain, so it is opt-in (TLS_QR_COOP=1).
+template <int PREC>
+__device__ __forceinline__ bool qr_fin_coop(const float* __restrict__ W, int n, int ldw, int j, int b0, int nb,
+                                            const double* __restrict__ partP, double* __restrict__ wT,
+                                            double* __restrict__ scal, double* __restrict__ G,
+                                            int* __restrict__ qflags, double* red, double* cs) {
+  constexpr int prec = PREC;
+  const int t = threadIdx.x;
+  double tl = 0.0;
+  for (int b = b0 + t; b < nb; b += kQrThreads) tl += partP[(int64_t)b * n + j];
+  const double tail = block_sum(tl, red);                      // fixed order: same bits in every CTA
+  const double x0 = (double)W[(int64_t)j * ldw + j];
+  const double sigma = round_uf(sqrt(round_uf(fma(x0, x0, tail), prec)), prec);
+  if (!(sigma > 0.0)) {
+    if (blockIdx.x == 0 && t == 0) { qflags[0] = 1; qflags[1] = j + 1; }
+    return false;
+  }
+  const double alpha = x0 >= 0.0 ? -sigma : sigma;
+  const double v0 = round_uf(x0 - alpha, prec);
+  const double vv = round_uf(fma(v0, v0, tail), prec);
+  const double beta = round_uf(2.0 / vv, prec);
+  // this CTA's slice of columns; 8 columns at a time, 32 row groups per column
+  const int nk = n - j - 1;
+  const int S = (nk + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int kbeg = j + 1 + (int)blockIdx.x * S, kend = min(n, kbeg + S);
+  const int l8 = t & 7, grp = t >> 3;
+  for (int k0 = kbeg; k0 < kend; k0 += 8) {
+    const int k = k0 + l8;
+    double sum = 0.0;
+    if (k < kend)
+      for (int b = b0 + grp; b < nb; b += 32) sum += partP[(int64_t)b * n + k];
+    cs[grp * 8 + l8] = sum;
+    __syncthreads();
+    if (t < 8 && k0 + t < kend) {
+      double tot = 0.0;
+      for (int g = 0; g < 32; ++g) tot += cs[g * 8 + t];
+      const int kk = k0 + t;
+      const double w = round_uf(fma(v0, (double)W[(int64_t)j * ldw + kk], tot), prec);
+      wT[kk] = round_uf(beta * w, prec);
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && t == 0) {
+    scal[4 * j + 0] = alpha;
+    scal[4 * j + 1] = v0;
+    scal[4 * j + 2] = sigma;
+    scal[4 * j + 3] = beta;
+    G[(int64_t)j * n + j] = sigma;
+  }
+  return true;
+}
+
+template <int CPT, int PREC>
+__global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_coop(
+    float* __restrict__ W, int64_t m, int n, int ldw, int RB, int nb, double* __restrict__ partP,
+    double* __restrict__ wT, double* __restrict__ scal, double* __restrict__ G, int* __restrict__ qflags) {
+  extern __shared__ double qsm[];
+  __shared__ double red[32];
+  __shared__ double cs[kQrThreads];
+  cg::grid_group grid = cg::this_grid();
+  for (int j = 0; j < n; ++j) {
+    const int b0 = (j > 0 ? j - 1 : 0) / RB;
+    // sigma is computed identically in every CTA, so a zero column ends every CTA's loop
+    if (!qr_fin_coop<PREC>(W, n, ldw, j, b0, nb, partP, wT, scal, G, qflags, red, cs)) break;
+    grid.sync();
+    if (j + 1 == n) break;
+    const int ngroups = (ldw - ((j + 1) & ~3)) >> 2;
+    const int TG = qr_team(ngroups, CPT / 4);
+    qr_update_v4<CPT, PREC>(W, m, n, ldw, j, RB, (int)blockIdx.x, TG, kQrThreads / TG, wT, scal, partP, G, qsm,
+                            false);
+    grid.sync();
   }
 }
 
@@ -379,13 +478,6 @@ int launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, 
   return 0;
 }
 
-// Team size for a pass over `ncols` columns with CPT columns per thread.
-inline int qr_team(int ncols, int cpt) {
-  int tg = (ncols + cpt - 1) / cpt;
-  tg = (tg + 31) / 32 * 32;
-  if (tg < 32) tg = 32;
-  return tg > kQrThreads ? kQrThreads : tg;
-}
 
 template <typename T, bool LOAD, int CPT, int PREC>
 int qr_step_launch(T* W, const DenseView& A, int ldw, const double* dinv, int j, int RB, int bfirst, int nblk,
@@ -421,6 +513,31 @@ int qr_t(const DenseView& A, const double* dinv, void* Wbuf, double* partP, doub
   int rc = qr_step_launch<T, true, CPT, PREC>(W, A, ldw, dinv, -1, RB, 0, nb, nullptr, nullptr, partP, G, qflags, st);
   if (rc) return rc;
   int nl = 1;
+  if constexpr (sizeof(T) == 4) {
+    // opt-in (TLS_QR_COOP=1): measured slower than the PDL chain (4096 x 512: 6.8 vs 5.0 ms,
+    // 65536 x 2048: 442 vs 314 ms), like the other cooperative streaming passes
+    const char* ce = getenv("TLS_QR_COOP");
+    const bool coop_env = ce && ce[0] == '1';
+    const size_t smem = (size_t)kQrThreads * CPT * sizeof(double);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (coop_env && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_qr_coop<CPT, PREC>, kQrThreads, smem) ==
+                        cudaSuccess && per_sm * sms >= nb) {
+      float* Wf = reinterpret_cast<float*>(W);
+      int64_t mm = m;
+      int nn = n, ll = ldw, rb = RB, nbb = nb;
+      void* args[] = {&Wf, &mm, &nn, &ll, &rb, &nbb, &partP, &wT, &scal, &G, &qflags};
+      const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_qr_coop<CPT, PREC>, dim3(nb), dim3(kQrThreads),
+                                                        args, smem, st);
+      if (e != cudaSuccess) {
+        set_error("k_qr_coop launch: %s", cudaGetErrorString(e));
+        return TLS_ERR_CUDA;
+      }
+      if (launches) *launches += nl + 1;
+      return 0;
+    }
+  }
   for (int j = 0; j < n; ++j) {
     // partials of column j were written by the pass with first row max(j - 1, 0)
     const int b0 = (int)((j > 0 ? j - 1 : 0) / RB);

@@ -251,3 +251,24 @@ def test_qr_extreme_widths(T, m, n, fmt):
     if res.status == rqi.OK:
         assert _rel(x.cpu().numpy(), res.x) <= 1e-9
         assert abs(sig - res.sigma) / res.sigma <= 1e-12
+
+
+@pytest.mark.parametrize("m,n,fmt", [(777, 67, "bf16"), (1100, 530, "fp16")])
+def test_qr_persistent_kernel_variant(T, monkeypatch, m, n, fmt):
+    """TLS_QR_COOP=1: the whole column loop in one cooperative kernel (k_qr_coop, opt-in);
+    same bounds against the oracle as the default launch chain, and a solve on its R~."""
+    monkeypatch.setenv("TLS_QR_COOP", "1")
+    A, b = _problem(m, n, 1e2, seed=m + n, spread=False)
+    M, keep = _mat(T, A)
+    rc, R, info = T.tls_factor_precond_qr(M, fmt)
+    assert rc == 0 and info["launches"] < 20
+    Rt, d, nrm = T.tls_precond_export(R)
+    pc = rqi.factor_precond_qr(A, fmt)
+    u = unit_roundoff(fmt)
+    Ah = round_to(A / d, fmt)
+    assert np.linalg.norm(Rt.T @ Rt - Ah.T @ Ah) <= 10 * m * n * u * np.linalg.norm(Ah) ** 2
+    assert _rel(Rt, pc.Rt) <= 10 * m * n * u * np.linalg.cond(Ah)
+    rc, x, sig, sinfo = T.tls_rqi_pcgtls(M, dev(b), R)
+    res = rqi.rqi_pcgtls_mp(A, b, rqi.Precond(Rt, d, fmt, nrm))
+    assert sinfo["status"] == res.status == rqi.OK and sinfo["rqi_iters"] == res.rqi_iters
+    assert _rel(x.cpu().numpy(), res.x) <= 1e-9
