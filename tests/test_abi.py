@@ -95,3 +95,22 @@ def test_ctypes_layouts_equal_the_c_compiler(L, tmp_path):
         for f, _ in cls._fields_:
             assert got[f"{name} {f}"] == getattr(cls, f).offset, (name, f)
     assert got["abi"] == L.tls_abi_version()
+
+
+def test_qr_workspace_size_without_gpu(L, monkeypatch):
+    """tls_qr_workspace_size (host only): 0 for CSR, a bad u_f or nranks < 1; otherwise at
+    least the fp32 (fp64 for u_f = fp64) working copy, and more with a TSQR stack (nranks or
+    TLS_QR_LEAVES > 1)."""
+    from paper_2305_19028_b200 import tlsrqi
+    M = tlsrqi.tls_matrix_t()
+    M.layout, M.n, M.m_local, M.m_global, M.ld, M.vals = 0, 64, 1000, 1000, 64, 256
+    s16 = L.tls_qr_workspace_size(C.byref(M), 0, 1)
+    s64 = L.tls_qr_workspace_size(C.byref(M), 3, 1)
+    assert s16 >= 1000 * 64 * 4 and s64 >= 1000 * 64 * 8 and s64 > s16
+    assert L.tls_qr_workspace_size(C.byref(M), 0, 4) >= s16 + 4 * 64 * 64 * 8
+    assert L.tls_qr_workspace_size(C.byref(M), 7, 1) == 0
+    assert L.tls_qr_workspace_size(C.byref(M), 0, 0) == 0
+    monkeypatch.setenv("TLS_QR_LEAVES", "3")
+    assert L.tls_qr_workspace_size(C.byref(M), 0, 1) >= s16 + 3 * 64 * 64 * 8
+    M.layout = 1
+    assert L.tls_qr_workspace_size(C.byref(M), 0, 1) == 0
