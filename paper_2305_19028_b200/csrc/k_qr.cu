@@ -28,6 +28,8 @@ namespace cg = cooperative_groups;
 
 namespace {
 constexpr int kQrThreads = 256;
+// update-pass CTA size: one CTA per SM, 512 threads (<= 8 columns per thread) or 256 (16)
+template <int CPT> constexpr int qr_step_threads() { return CPT >= 16 ? 256 : 512; }
 
 // Round an fp32 value to u_f (fp16 / bf16 hardware conversions; identity for fp32).
 template <int PREC> __device__ __forceinline__ float qr_rdf(float x) {
@@ -79,7 +81,7 @@ __device__ __forceinline__ void qr_load_row(const T* __restrict__ W, const doubl
 }
 
 template <typename T, bool LOAD, int CPT, int PREC>
-__global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step(T* __restrict__ W, const double* __restrict__ A, int64_t lda,
+__global__ void __launch_bounds__(qr_step_threads<CPT>(), 1) k_qr_step(T* __restrict__ W, const double* __restrict__ A, int64_t lda,
                                                          const double* __restrict__ dinv, int64_t m, int n, int ldw, int j,
                                                          int RB, int bfirst, int TG,
                                                          const double* __restrict__ wT,
@@ -305,7 +307,7 @@ __device__ __forceinline__ void qr_update_v4(float* __restrict__ W, int64_t m, i
 }
 
 template <int CPT, int PREC>
-__global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_step_v4(
+__global__ void __launch_bounds__(qr_step_threads<CPT>(), 1) k_qr_step_v4(
     float* __restrict__ W, int64_t m, int n, int ldw, int j, int RB, int bfirst, int TG,
     const double* __restrict__ wT, const double* __restrict__ scal, double* __restrict__ partP,
     double* __restrict__ G, const int* __restrict__ dead) {
@@ -487,14 +489,14 @@ int qr_step_launch(T* W, const DenseView& A, int ldw, const double* dinv, int j,
     const int c0 = (j + 1) & ~3;
     const int ngroups = (ldw - c0) / 4;
     const int TG = qr_team(ngroups, CPT / 4);
-    const int teams = kQrThreads / TG;
+    const int teams = qr_step_threads<CPT>() / TG;
     const size_t smem = teams > 1 ? (size_t)teams * ngroups * 4 * sizeof(double) : 0;
     return launch_pdl(k_qr_step_v4<CPT, PREC>, nblk, teams * TG, smem, st, reinterpret_cast<float*>(W), A.m, n, ldw,
                       j, RB, bfirst, TG, wT, scal, partP, G, qflags);
   } else {
     const int ncols = n - (j + 1);
     const int TG = qr_team(ncols, CPT);
-    const int teams = kQrThreads / TG;
+    const int teams = qr_step_threads<CPT>() / TG;
     const size_t smem = teams > 1 ? (size_t)teams * ncols * sizeof(double) : 0;
     return launch_pdl(k_qr_step<T, LOAD, CPT, PREC>, nblk, teams * TG, smem, st, W, A.A, A.ld, dinv, A.m, n, ldw, j,
                       RB, bfirst, TG, wT, scal, partP, G, qflags);
@@ -568,7 +570,8 @@ int qr_dispatch(const DenseView& A, const double* dinv, void* Wbuf, double* part
 }  // namespace
 
 int qr_rows_per_cta(int64_t m, int n) {
-  const int64_t want = (n > 8 * kQrThreads ? 1 : 2) * 148;   // resident CTAs: one wave
+  (void)n;
+  const int64_t want = 148;   // one update-pass CTA per SM (qr_step_threads)
   int64_t rb = (m + want - 1) / want;
   if (rb < 32) rb = 32;
   return (int)rb;
