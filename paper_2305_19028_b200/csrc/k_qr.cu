@@ -29,7 +29,7 @@ namespace cg = cooperative_groups;
 namespace {
 constexpr int kQrThreads = 256;
 // update-pass CTA size: one CTA per SM, 512 threads (<= 8 columns per thread) or 256 (16)
-template <int CPT> constexpr int qr_step_threads() { return CPT >= 16 ? 256 : 512; }
+template <int CPT> __host__ __device__ constexpr int qr_step_threads() { return CPT >= 16 ? 256 : 512; }
 
 // Round an fp32 value to u_f (fp16 / bf16 hardware conversions; identity for fp32).
 template <int PREC> __device__ __forceinline__ float qr_rdf(float x) {
@@ -334,7 +334,7 @@ __device__ __forceinline__ bool qr_fin_coop(const float* __restrict__ W, int n, 
   constexpr int prec = PREC;
   const int t = threadIdx.x;
   double tl = 0.0;
-  for (int b = b0 + t; b < nb; b += kQrThreads) tl += partP[(int64_t)b * n + j];
+  for (int b = b0 + t; b < nb; b += (int)blockDim.x) tl += partP[(int64_t)b * n + j];
   const double tail = block_sum(tl, red);                      // fixed order: same bits in every CTA
   const double x0 = (double)W[(int64_t)j * ldw + j];
   const double sigma = round_uf(sqrt(round_uf(fma(x0, x0, tail), prec)), prec);
@@ -350,17 +350,17 @@ __device__ __forceinline__ bool qr_fin_coop(const float* __restrict__ W, int n, 
   const int nk = n - j - 1;
   const int S = (nk + (int)gridDim.x - 1) / (int)gridDim.x;
   const int kbeg = j + 1 + (int)blockIdx.x * S, kend = min(n, kbeg + S);
-  const int l8 = t & 7, grp = t >> 3;
+  const int l8 = t & 7, grp = t >> 3, ngrp = (int)blockDim.x >> 3;
   for (int k0 = kbeg; k0 < kend; k0 += 8) {
     const int k = k0 + l8;
     double sum = 0.0;
     if (k < kend)
-      for (int b = b0 + grp; b < nb; b += 32) sum += partP[(int64_t)b * n + k];
+      for (int b = b0 + grp; b < nb; b += ngrp) sum += partP[(int64_t)b * n + k];
     cs[grp * 8 + l8] = sum;
     __syncthreads();
     if (t < 8 && k0 + t < kend) {
       double tot = 0.0;
-      for (int g = 0; g < 32; ++g) tot += cs[g * 8 + t];
+      for (int g = 0; g < ngrp; ++g) tot += cs[g * 8 + t];
       const int kk = k0 + t;
       const double w = round_uf(fma(v0, (double)W[(int64_t)j * ldw + kk], tot), prec);
       wT[kk] = round_uf(beta * w, prec);
@@ -378,12 +378,12 @@ __device__ __forceinline__ bool qr_fin_coop(const float* __restrict__ W, int n, 
 }
 
 template <int CPT, int PREC>
-__global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_coop(
+__global__ void __launch_bounds__(qr_step_threads<CPT>(), 1) k_qr_coop(
     float* __restrict__ W, int64_t m, int n, int ldw, int RB, int nb, double* __restrict__ partP,
     double* __restrict__ wT, double* __restrict__ scal, double* __restrict__ G, int* __restrict__ qflags) {
   extern __shared__ double qsm[];
   __shared__ double red[32];
-  __shared__ double cs[kQrThreads];
+  __shared__ double cs[qr_step_threads<CPT>()];
   cg::grid_group grid = cg::this_grid();
   for (int j = 0; j < n; ++j) {
     const int b0 = (j > 0 ? j - 1 : 0) / RB;
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(kQrThreads, CPT >= 16 ? 1 : 2) k_qr_coop(
     if (j + 1 == n) break;
     const int ngroups = (ldw - ((j + 1) & ~3)) >> 2;
     const int TG = qr_team(ngroups, CPT / 4);
-    qr_update_v4<CPT, PREC>(W, m, n, ldw, j, RB, (int)blockIdx.x, TG, kQrThreads / TG, wT, scal, partP, G, qsm,
+    qr_update_v4<CPT, PREC>(W, m, n, ldw, j, RB, (int)blockIdx.x, TG, qr_step_threads<CPT>() / TG, wT, scal, partP, G, qsm,
                             false);
     grid.sync();
   }
@@ -516,21 +516,21 @@ int qr_t(const DenseView& A, const double* dinv, void* Wbuf, double* partP, doub
   if (rc) return rc;
   int nl = 1;
   if constexpr (sizeof(T) == 4) {
-    // opt-in (TLS_QR_COOP=1): measured slower than the PDL chain (4096 x 512: 6.8 vs 5.0 ms,
-    // 65536 x 2048: 442 vs 314 ms), like the other cooperative streaming passes
+    // opt-in (TLS_QR_COOP=1): measured slower than the PDL chain (4096 x 512: 5.4 vs 4.4 ms,
+    // 65536 x 2048: 418 vs 301 ms), like the other cooperative streaming passes
     const char* ce = getenv("TLS_QR_COOP");
     const bool coop_env = ce && ce[0] == '1';
-    const size_t smem = (size_t)kQrThreads * CPT * sizeof(double);
+    const size_t smem = (size_t)qr_step_threads<CPT>() * CPT * sizeof(double);
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (coop_env && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_qr_coop<CPT, PREC>, kQrThreads, smem) ==
+    if (coop_env && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_qr_coop<CPT, PREC>, qr_step_threads<CPT>(), smem) ==
                         cudaSuccess && per_sm * sms >= nb) {
       float* Wf = reinterpret_cast<float*>(W);
       int64_t mm = m;
       int nn = n, ll = ldw, rb = RB, nbb = nb;
       void* args[] = {&Wf, &mm, &nn, &ll, &rb, &nbb, &partP, &wT, &scal, &G, &qflags};
-      const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_qr_coop<CPT, PREC>, dim3(nb), dim3(kQrThreads),
+      const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_qr_coop<CPT, PREC>, dim3(nb), dim3(qr_step_threads<CPT>()),
                                                         args, smem, st);
       if (e != cudaSuccess) {
         set_error("k_qr_coop launch: %s", cudaGetErrorString(e));
