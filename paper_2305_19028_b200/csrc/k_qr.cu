@@ -338,7 +338,7 @@ __device__ __forceinline__ bool qr_fin_coop(const float* __restrict__ W, int n, 
   const double tail = block_sum(tl, red);                      // fixed order: same bits in every CTA
   const double x0 = (double)W[(int64_t)j * ldw + j];
   const double sigma = round_uf(sqrt(round_uf(fma(x0, x0, tail), prec)), prec);
-  if (!(sigma > 0.0)) {
+  if (sigma == 0.0) {
     if (blockIdx.x == 0 && t == 0) { qflags[0] = 1; qflags[1] = j + 1; }
     return false;
   }
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_fin(const T* __restrict__ W, 
   const double tail = block_sum(tl, red);                      // fixed order: same bits in every CTA
   const double x0 = (double)W[(int64_t)j * ldw + j];
   const double sigma = round_uf(sqrt(round_uf(fma(x0, x0, tail), prec)), prec);
-  if (!(sigma > 0.0)) {                                        // zero (or non-finite) column in u_f
+  if (sigma == 0.0) {        // zero column in u_f (an overflowed inf/NaN goes on, as in the oracle: TLS_RANGE)
     if (blockIdx.x == 0 && t == 0) { qflags[0] = 1; qflags[1] = j + 1; }
     return;
   }

@@ -272,3 +272,25 @@ def test_qr_persistent_kernel_variant(T, monkeypatch, m, n, fmt):
     res = rqi.rqi_pcgtls_mp(A, b, rqi.Precond(Rt, d, fmt, nrm))
     assert sinfo["status"] == res.status == rqi.OK and sinfo["rqi_iters"] == res.rqi_iters
     assert _rel(x.cpu().numpy(), res.x) <= 1e-9
+
+
+def test_qr_fp16_norm_overflow_is_range(T):
+    """A tall column whose squared norm exceeds fp16's range (70000 entries in [1/2, 1) after
+    the power-of-two scaling: x^T x > 65504) overflows when the inner product is rounded to
+    fp16 (R25).  The oracle carries the inf/NaN through and reports RANGE; so must the GPU (not
+    a zero-column breakdown).  bf16 has fp32's range and factors the same matrix."""
+    import warnings
+    rng = np.random.default_rng(0)
+    A = rng.uniform(0.5, 1.0, (70000, 4))
+    M, keep = _mat(T, A)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        pc16 = rqi.factor_precond_qr(A, "fp16")
+    assert pc16.status == rqi.RANGE
+    rc, R, info = T.tls_factor_precond_qr(M, "fp16")
+    assert rc == rqi.RANGE and R is None
+    pcb = rqi.factor_precond_qr(A, "bf16")
+    rc, R, info = T.tls_factor_precond_qr(M, "bf16")
+    assert rc == pcb.status == 0
+    Rt, d, nrm = T.tls_precond_export(R)
+    assert _rel(Rt, pcb.Rt) <= 10 * 70000 * 4 * unit_roundoff("bf16") * np.linalg.cond(round_to(A / d, "bf16"))
