@@ -176,9 +176,10 @@ TLS_API int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi
  * like a Cholesky one.  Dense A only (CSR: TLS_ERR_ARG).
  * Row-sharded A (comm with nranks > 1) or TSQR leaves (environment TLS_QR_LEAVES = k,
  * default 1: each rank's rows split into k contiguous blocks [s m/k, (s+1) m/k)): every
- * leaf is factored as above, the leaf R's are stacked in rank-major, leaf order (the
- * stack all-reduced over the ranks; each rank fills only its own slots), and R~ is the R
- * factor of the stack, computed the same way without further scaling (R26).  Every leaf
+ * leaf is factored as above, the leaf R's are stacked row-interleaved (row i of leaf L =
+ * rank * k + s at stack row i * leaves + L; the stack all-reduced over the ranks, each rank
+ * filling only its own rows), and R~ is the R factor of the stack, computed the same way
+ * without further scaling and skipping the stack rows that are still zero (R26).  Every leaf
  * needs >= n rows (else TLS_ERR_ARG).  R~ is identical on every rank.
  * ws_dev: ws_bytes >= tls_qr_workspace_size(A, u_f, nranks) bytes (it holds an m_local x n
  * fp32 -- fp64 for u_f = TLS_FP64 -- working copy of the rows, and for TSQR the stack and

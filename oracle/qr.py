@@ -63,14 +63,22 @@ def householder_qr_r(A: np.ndarray, fmt: str) -> np.ndarray:
 
 
 def tsqr_r(A: np.ndarray, row_blocks, fmt: str) -> np.ndarray:
-    """TSQR (tall-skinny QR, reading R26): the R factors of the row blocks A[r0:r1] (each a
-    Householder QR in fmt, householder_qr_r) stacked in block order, then the R factor of that
-    stack, again by householder_qr_r.  In exact arithmetic this is the R of A (diag >= 0):
-    A = diag(Q_b) [R_1; ...; R_B] and [R_1; ...; R_B] = Q' R.  One block is the plain QR."""
+    """TSQR (tall-skinny QR, reading R26): the R factors R_b of the row blocks A[r0:r1] (each a
+    Householder QR in fmt, householder_qr_r) stacked row-interleaved -- stack row i B + b is
+    row i of R_b -- then the R factor of that stack, again by householder_qr_r.  In exact
+    arithmetic this is the R of A (diag >= 0): A = diag(Q_b) Pi S and S = Q' R for the row
+    permutation Pi.  The interleaving puts every row whose first nonzero is in column i
+    before those starting later, so the stack's column j only involves its first (j+1) B rows
+    (the rest are zero and stay zero).  One block is the plain QR."""
     if len(row_blocks) == 1:
         r0, r1 = row_blocks[0]
         return householder_qr_r(A[r0:r1], fmt)
-    return householder_qr_r(np.vstack([householder_qr_r(A[r0:r1], fmt) for r0, r1 in row_blocks]), fmt)
+    Rs = [householder_qr_r(A[r0:r1], fmt) for r0, r1 in row_blocks]
+    B, n = len(Rs), A.shape[1]
+    S = np.zeros((B * n, n))
+    for b, R in enumerate(Rs):
+        S[b::B] = R
+    return householder_qr_r(S, fmt)
 
 
 def even_row_blocks(m: int, k: int):

@@ -18,6 +18,7 @@
 // (fixed order, deterministic), forms the column's scalars and w^T.  2 launches per column.
 #include <cooperative_groups.h>
 #include <cuda_bf16.h>
+#include <algorithm>
 #include <cstdlib>
 
 #include "tls_common.cuh"
@@ -505,7 +506,7 @@ int qr_step_launch(T* W, const DenseView& A, int ldw, const double* dinv, int j,
 
 template <typename T, int CPT, int PREC>
 int qr_t(const DenseView& A, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
-         int* qflags, double* G, cudaStream_t st, int* launches) {
+         int* qflags, double* G, cudaStream_t st, int* launches, int row_stride) {
   const int n = A.n;
   const int64_t m = A.m;
   const int RB = qr_rows_per_cta(m, n);
@@ -540,17 +541,24 @@ int qr_t(const DenseView& A, const double* dinv, void* Wbuf, double* partP, doub
       return 0;
     }
   }
+  // row_stride > 0 (the row-interleaved TSQR stack, R26): rows >= (j + 2) row_stride are zero in
+  // columns j and j + 1, so the pass of column j stops there (bit-identical: they add zeros)
+  auto m_act = [&](int j) -> int64_t { return row_stride > 0 ? std::min(m, (int64_t)(j + 2) * row_stride) : m; };
   for (int j = 0; j < n; ++j) {
     // partials of column j were written by the pass with first row max(j - 1, 0)
     const int b0 = (int)((j > 0 ? j - 1 : 0) / RB);
+    const int nbj = j == 0 ? nb : (int)((m_act(j - 1) + RB - 1) / RB);   // CTAs that wrote them
     const int nf = (n - j - 1 + 31) / 32;
-    rc = launch_pdl(k_qr_fin<T, PREC>, nf > 0 ? nf : 1, kQrThreads, 0, st, (const T*)W, n, ldw, j, b0, nb,
+    rc = launch_pdl(k_qr_fin<T, PREC>, nf > 0 ? nf : 1, kQrThreads, 0, st, (const T*)W, n, ldw, j, b0, nbj,
                     (const double*)partP, wT, scal, G, qflags);
     if (rc) return rc;
     ++nl;
     if (j + 1 < n) {
       const int bs = (int)(j / RB);       // CTAs whose rows are all < j would exit at once: not launched
-      rc = qr_step_launch<T, false, CPT, PREC>(W, A, ldw, dinv, j, RB, bs, nb - bs, wT, scal, partP, G, qflags, st);
+      DenseView Aj = A;
+      Aj.m = m_act(j);
+      const int nbu = (int)((Aj.m + RB - 1) / RB);
+      rc = qr_step_launch<T, false, CPT, PREC>(W, Aj, ldw, dinv, j, RB, bs, nbu - bs, wT, scal, partP, G, qflags, st);
       if (rc) return rc;
       ++nl;
     }
@@ -562,10 +570,10 @@ int qr_t(const DenseView& A, const double* dinv, void* Wbuf, double* partP, doub
 
 template <typename T, int PREC>
 int qr_dispatch(const DenseView& A, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
-                int* qflags, double* G, cudaStream_t st, int* launches) {
-  if (A.n <= 4 * kQrThreads) return qr_t<T, 4, PREC>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
-  if (A.n <= 8 * kQrThreads) return qr_t<T, 8, PREC>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
-  return qr_t<T, 16, PREC>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
+                int* qflags, double* G, cudaStream_t st, int* launches, int rs) {
+  if (A.n <= 4 * kQrThreads) return qr_t<T, 4, PREC>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, rs);
+  if (A.n <= 8 * kQrThreads) return qr_t<T, 8, PREC>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, rs);
+  return qr_t<T, 16, PREC>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, rs);
 }
 }  // namespace
 
@@ -587,13 +595,13 @@ size_t qr_work_bytes(int64_t m, int n, int u_f) {
 }
 
 int launch_qr(const DenseView& A, int u_f, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
-              int* qflags, double* G, cudaStream_t st, int* launches) {
+              int* qflags, double* G, cudaStream_t st, int* launches, int row_stride) {
   if (A.n > kMaxDenseN) { set_error("QR: n > %d", kMaxDenseN); return TLS_ERR_ARG; }
   switch (u_f) {
-    case TLS_FP16: return qr_dispatch<float, TLS_FP16>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
-    case TLS_BF16: return qr_dispatch<float, TLS_BF16>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
-    case TLS_FP32: return qr_dispatch<float, TLS_FP32>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
-    default: return qr_dispatch<double, TLS_FP64>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches);
+    case TLS_FP16: return qr_dispatch<float, TLS_FP16>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, row_stride);
+    case TLS_BF16: return qr_dispatch<float, TLS_BF16>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, row_stride);
+    case TLS_FP32: return qr_dispatch<float, TLS_FP32>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, row_stride);
+    default: return qr_dispatch<double, TLS_FP64>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, row_stride);
   }
 }
 

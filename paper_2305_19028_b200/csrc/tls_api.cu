@@ -865,8 +865,8 @@ int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, v
       TLS_TRY(launch_qr(dense_view(A), u_f, dinv, q.W1, q.part1, q.wT, q.scal, q.qflags, q.G, cx.st, &cx.launches));
       cx.passes += n + 1;
     } else {
-      // TSQR (R26): leaf R's of this rank's row blocks into their slots of the stack,
-      // the stack summed over ranks (all other slots are zero: exact), then its R.
+      // TSQR (R26): leaf R's of this rank's row blocks into their rows of the row-interleaved
+      // stack, the stack summed over ranks (all other rows are zero: exact), then its R.
       TLS_CUDA_TRY(cudaMemsetAsync(q.S, 0, (size_t)nleaf * n * n * 8, cx.st));
       const int64_t ml = A->m_local;
       for (int s = 0; s < sub; ++s) {
@@ -874,14 +874,15 @@ int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, v
         DenseView leaf{A->vals + r0 * A->ld, r1 - r0, n, A->ld};
         TLS_CUDA_TRY(cudaMemsetAsync(q.G, 0, (size_t)n * n * 8, cx.st));
         TLS_TRY(launch_qr(leaf, u_f, dinv, q.W1, q.part1, q.wT, q.scal, q.qflags, q.G, cx.st, &cx.launches));
-        TLS_CUDA_TRY(cudaMemcpyAsync(q.S + (size_t)(rank * sub + s) * n * n, q.G, (size_t)n * n * 8,
-                                     cudaMemcpyDeviceToDevice, cx.st));
+        // row i of leaf L goes to stack row i nleaf + L (row-interleaved, R26)
+        TLS_CUDA_TRY(cudaMemcpy2DAsync(q.S + (size_t)(rank * sub + s) * n, (size_t)nleaf * n * 8, q.G, (size_t)n * 8,
+                                       (size_t)n * 8, (size_t)n, cudaMemcpyDeviceToDevice, cx.st));
         cx.passes += n + 1;
       }
       if (P > 1) TLS_TRY(allreduce(comm, q.S, (size_t)nleaf * n * n, ncclSum, cx.st));
       TLS_CUDA_TRY(cudaMemsetAsync(q.G, 0, (size_t)n * n * 8, cx.st));
       DenseView stack{q.S, (int64_t)nleaf * n, n, n};
-      TLS_TRY(launch_qr(stack, u_f, nullptr, q.W2, q.part2, q.wT, q.scal, q.qflags, q.G, cx.st, &cx.launches));
+      TLS_TRY(launch_qr(stack, u_f, nullptr, q.W2, q.part2, q.wT, q.scal, q.qflags, q.G, cx.st, &cx.launches, nleaf));
     }
   }
   tr.mark("qr");

@@ -154,7 +154,9 @@ int qr_rows_per_cta(int64_t m, int n);
 int qr_ldw(int n, int u_f);                        // row stride of the working copy
 size_t qr_work_bytes(int64_t m, int n, int u_f);   // W copy + partials + w^T + scalars + flags
 // dinv == nullptr: no scaling (the TSQR stack of already scaled leaf R's)
+// row_stride > 0: A is the row-interleaved TSQR stack of row_stride leaf R's (rows >= (j+2)
+// row_stride are zero in columns j, j+1 and are skipped, R26)
 int launch_qr(const DenseView& A, int u_f, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
-              int* qflags, double* G, cudaStream_t st, int* launches);
+              int* qflags, double* G, cudaStream_t st, int* launches, int row_stride = 0);
 
 }  // namespace tls

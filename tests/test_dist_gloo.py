@@ -164,8 +164,9 @@ def test_row_sharded_solve_world2():
 def _tsqr_worker(rank, world, port, out):
     """The exchange of the row-sharded QR preconditioner (tls_factor_precond_qr, R26): each
     rank factors its own rows (D from the all-reduced column maxima), writes its R into its
-    slot of a zeroed (world n) x n stack, the stack is sum-all-reduced (every other slot is
-    zero, so the sum is exact), and every rank factors the stack."""
+    rows of a zeroed (world n) x n stack (row i of rank p's R at stack row i world + p), the
+    stack is sum-all-reduced (every other slot is zero, so the sum is exact), and every rank
+    factors the stack."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     tdist.init_process_group("gloo", rank=rank, world_size=world)
@@ -178,7 +179,7 @@ def _tsqr_worker(rank, world, port, out):
         cm = _allreduce(np.max(np.abs(A[lo:hi]), axis=0), tdist.ReduceOp.MAX)
         d = np.exp2(np.floor(np.log2(cm)))
         S = np.zeros((world * n, n))
-        S[rank * n:(rank + 1) * n] = householder_qr_r(A[lo:hi] / d, "fp16")
+        S[rank::world] = householder_qr_r(A[lo:hi] / d, "fp16")      # row-interleaved slots (R26)
         S = _allreduce(S)
         R = householder_qr_r(S, "fp16")
         pc = rqi.factor_precond_qr(A, "fp16", row_blocks=[shard_rows(m, world, r) for r in range(world)])
