@@ -269,6 +269,7 @@ def tls_factor_precond(M: tls_matrix_t, u_f, opts: Optional[tls_rqi_opts_t] = No
 def tls_factor_precond_qr(M: tls_matrix_t, u_f, comm=None, stream=None, ws: Optional[torch.Tensor] = None,
                           nranks: int = 1):
     """Householder-QR preconditioner in u_f (NEXT-2, R25; TSQR over ranks / TLS_QR_LEAVES, R26).
+    nranks: the size of `comm` (it sizes the TSQR stack in the workspace when ws is None).
     Returns (status, Precond or None, info dict)."""
     uf = PREC[u_f] if isinstance(u_f, str) else int(u_f)
     if ws is None:
