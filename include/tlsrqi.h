@@ -185,7 +185,11 @@ TLS_API int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi
  * fp32 -- fp64 for u_f = TLS_FP64 -- working copy of the rows, and for TSQR the stack and
  * its working copy).  A column that becomes exactly zero in u_f: TLS_CHOL_BREAKDOWN,
  * info->chol_pivot = its 1-based index (within the leaf or stack factorization where it
- * happened), *R_out = NULL.  A reflector overflowing u_f: TLS_RANGE. */
+ * happened), *R_out = NULL.  An inner product or reflector overflowing u_f (e.g. a column
+ * with x^T x > 65504 in fp16): TLS_RANGE, *R_out = NULL.  The stream is synchronised once at
+ * the end; the environment knobs TLS_QR_PDL=0 (plain launches) and TLS_QR_COOP=1 (one
+ * cooperative kernel for the column loop) select measured-slower variants for comparison.
+ * tls_qr_workspace_size returns 0 for CSR, a bad u_f or nranks < 1. */
 TLS_API size_t tls_qr_workspace_size(const tls_matrix_t* A, int32_t u_f, int32_t nranks);
 TLS_API int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, void* stream, void* ws_dev,
                                   size_t ws_bytes, tls_precond_t* R_out, tls_info_t* info);
