@@ -32,10 +32,14 @@ class ZeroColumn(ZeroDivisionError):
         self.col = col
 
 
-def householder_qr_r(A: np.ndarray, fmt: str) -> np.ndarray:
+def householder_qr_r(A: np.ndarray, fmt: str, leaf: bool = False) -> np.ndarray:
     """R (n x n, upper, diag >= 0) of the Householder QR of A with every operation
     rounded to fmt.  A is first rounded to fmt.  Raises ZeroDivisionError on an exactly
-    zero column (rank deficiency, SPEC.md householder_qr errors)."""
+    zero column (rank deficiency, SPEC.md householder_qr errors).
+    leaf=True (a TSQR leaf, reading R26): a column that vanishes on this block's rows is
+    not a rank deficiency of A (other blocks hold its mass), so its reflector is the
+    identity H = I (nothing is applied) and R's row j is W[j, j:] as it stands (R_jj = 0);
+    only the stack factorization reports a vanishing column."""
     rd = lambda x: round_to(np.asarray(x, dtype=np.float64), fmt)
     W = rd(np.array(A, dtype=np.float64, copy=True))
     m, n = W.shape
@@ -45,7 +49,9 @@ def householder_qr_r(A: np.ndarray, fmt: str) -> np.ndarray:
         x = W[j:, j]
         sigma = float(rd(np.sqrt(rd(np.dot(x, x)))))
         if sigma == 0.0:
-            raise ZeroColumn(j)
+            if not leaf:
+                raise ZeroColumn(j)
+            continue                                   # H = I; row j of R is W[j, j:]
         alpha = -sigma if x[0] >= 0 else sigma
         v = x.copy()
         v[0] = float(rd(x[0] - alpha))
@@ -73,7 +79,7 @@ def tsqr_r(A: np.ndarray, row_blocks, fmt: str) -> np.ndarray:
     if len(row_blocks) == 1:
         r0, r1 = row_blocks[0]
         return householder_qr_r(A[r0:r1], fmt)
-    Rs = [householder_qr_r(A[r0:r1], fmt) for r0, r1 in row_blocks]
+    Rs = [householder_qr_r(A[r0:r1], fmt, leaf=True) for r0, r1 in row_blocks]
     B, n = len(Rs), A.shape[1]
     S = np.zeros((B * n, n))
     for b, R in enumerate(Rs):

@@ -58,13 +58,50 @@ def column_scaling(A):
         amax = np.asarray(abs(A).max(axis=0).todense()).reshape(-1)
         normA2 = float(A.multiply(A).sum())
     else:
-        amax = np.max(np.abs(A), axis=0)
-        normA2 = float(np.sum(A * A))
+        amax, c = _col_max_sumsq(np.asarray(A))
+        normA2 = float(np.sum(c))
     if np.any(amax == 0) or not np.all(np.isfinite(amax)):
         raise ValueError("A has a zero or non-finite column")
     _, E = np.frexp(amax)
     d = np.ldexp(1.0, E - 1)
     return d, normA2
+
+
+def _col_max_sumsq(A: np.ndarray):
+    """Column maxima of |A| and column sums of squares, over row slices in the thread pool
+    (the maxima are exact in any order; the sums of squares are fp64 sums of the row
+    slices' sums, added in slice order)."""
+    step = max(1, min(65536, -(-A.shape[0] // _threads())))
+    sls = [slice(i, i + step) for i in range(0, A.shape[0], step)]
+    def one(sl):
+        X = A[sl]
+        return np.max(np.abs(X), axis=0), np.einsum("ij,ij->j", X, X)
+    parts = list(_pool().map(one, sls))
+    amax = np.max(np.stack([p[0] for p in parts]), axis=0)
+    c = np.zeros(A.shape[1])
+    for p in parts:
+        c += p[1]
+    return amax, c
+
+
+def norm_scaling(A):
+    """The scaling of the QR route (reading R27): the paper's D, "a diagonal matrix with the
+    square root of the diagonal elements of A^T A on the diagonal", rounded
+    to a power of two so that applying it is exact (l.307): with c_j = ||a_j||^2 and
+    k = floor(log2 c_j), d_j = 2^ceil(k/2) is sqrt(c_j) rounded to the nearest power of two
+    (sqrt(c_j) lies in [2^(k/2), 2^((k+1)/2))), and every scaled column has
+    ||a_j/d_j||^2 in [1/2, 2).  Decided on powers of two of c_j, never on a rounded sqrt.
+    Returns (d, ||A||_F^2); a zero or non-finite column raises ValueError (rank deficient)."""
+    if _is_sparse(A):
+        c = np.asarray(A.multiply(A).sum(axis=0)).reshape(-1)
+    else:
+        c = _col_max_sumsq(np.asarray(A))[1]
+    if np.any(c == 0) or not np.all(np.isfinite(c)):
+        raise ValueError("A has a zero or non-finite column")
+    _, E = np.frexp(c)                 # c = f 2^E, f in [1/2, 1): k = E - 1
+    k = E - 1
+    d = np.ldexp(1.0, -((-k) // 2))    # 2^ceil(k/2)
+    return d, float(np.sum(c))
 
 
 # ----------------------------------------------------------------------------- Gram
@@ -99,30 +136,87 @@ def _gram_sparse(A, d: np.ndarray, u_f: str) -> np.ndarray:
     return G * 2.0 ** -48
 
 
+def _round_rows(X: np.ndarray, d: np.ndarray, u_f: str, out_dtype) -> np.ndarray:
+    """fl_uf(X D^{-1}) (round_to) computed on row slices in a thread pool (numpy releases
+    the GIL), returned as out_dtype (exact: the values are u_f values); fp16 through
+    numpy's float16 cast, which is the same direct fp64 -> fp16 RNE (pinned bit-exact
+    against round_to in tests/test_oracle_rounding.py).  OverflowError if any value
+    overflows u_f."""
+    out = np.empty(X.shape, dtype=out_dtype)
+    def one(sl):
+        Y = X[sl] / d[None, :]
+        if u_f == "fp16":
+            with np.errstate(over="ignore"):
+                Y = Y.astype(np.float16)
+        else:
+            Y = round_to(Y, u_f)
+        out[sl] = Y
+        return bool(np.all(np.isfinite(out[sl])))
+    step = max(1, -(-X.shape[0] // _threads()))
+    sls = [slice(i, i + step) for i in range(0, X.shape[0], step)]
+    if not all(_pool().map(one, sls)):
+        raise OverflowError("A D^-1 overflows u_f")
+    return out
+
+
+_POOL = None
+
+
+def _threads() -> int:
+    import os
+    return max(1, min(32, os.cpu_count() or 1))
+
+
+def _pool():
+    global _POOL
+    if _POOL is None:
+        import concurrent.futures
+        _POOL = concurrent.futures.ThreadPoolExecutor(_threads())
+    return _POOL
+
+
 def gram_uf(A, d: np.ndarray, u_f: str, K_t: int = 64) -> np.ndarray:
     """Dense A:  G = sum over chunks c of K_t consecutive rows (in order) of
     fp64( fl32-accumulated  A^_c^T A^_c ),  A^ = fl_uf(A D^{-1})   (R10, R11).
 
     u_f in {fp16, bf16}: the products of u_f values are exact in fp32 and each
     chunk is summed in fp32 (a float32 matmul), as the tensor cores accumulate
-    in fp32; chunks are added in fp64.  u_f = fp32: A^ in fp32, G formed in
-    fp64.  u_f = fp64: G = (A D^{-1})^T (A D^{-1}) in fp64 (control)."""
+    in fp32; the chunk sums are added to G in fp64 in chunk order.  u_f = fp32:
+    A^ in fp32, the chunk products formed in fp64.  u_f = fp64: G = (A D^{-1})^T
+    (A D^{-1}) in fp64 (control).
+
+    Evaluation (no change to the arithmetic above): rows are rounded in slices of
+    64 chunks, the chunk products of a slice are one batched matmul, and the output
+    rows are split over a thread pool; every element of G still receives its
+    chunk sums one at a time in chunk order."""
     if _is_sparse(A):
         return _gram_sparse(A, d, u_f)
     m, n = A.shape
     G = np.zeros((n, n))
-    for c0 in range(0, m, K_t):
-        blk = A[c0:c0 + K_t]
-        blk = blk.toarray() if _is_sparse(blk) else np.asarray(blk)
-        Ah = round_to(blk / d[None, :], u_f)
-        if not np.all(np.isfinite(Ah)):
-            raise OverflowError("A D^-1 overflows u_f")
-        if u_f in ("fp16", "bf16"):
-            A32 = Ah.astype(np.float32)
-            S = (A32.T @ A32).astype(np.float64)
-        else:
-            S = Ah.T @ Ah
-        G += S
+    low = u_f in ("fp16", "bf16")
+    nb = max(1, min(_threads(), -(-n // 64)))
+    rblocks = [slice(j * n // nb, (j + 1) * n // nb) for j in range(nb)]
+    rows = K_t * 64
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):          # one BLAS thread per pool thread
+        for r0 in range(0, m, rows):
+            blk = A[r0:r0 + rows]
+            blk = blk.toarray() if _is_sparse(blk) else np.asarray(blk)
+            Ah = _round_rows(blk, d, u_f, np.float32 if low else np.float64)
+            nfull = Ah.shape[0] // K_t
+            chunks = [Ah[: nfull * K_t].reshape(nfull, K_t, n)] if nfull else []
+            tail = Ah[nfull * K_t:]
+
+            def work(rb):
+                Gr = G[rb]                                        # rows rb of G (a view)
+                for C in chunks:                                  # (nc, K_t, n)
+                    S = np.matmul(C[:, :, rb].transpose(0, 2, 1), C)   # (nc, |rb|, n), fp32 or fp64
+                    for c in range(S.shape[0]):                   # chunk order
+                        Gr += S[c]
+                if tail.shape[0]:
+                    Gr += tail[:, rb].T @ tail
+
+            list(_pool().map(work, rblocks))
     return G
 
 
@@ -144,6 +238,37 @@ def gram_exact_bound(A, d: np.ndarray, u_f: str, K_t: int = 64) -> np.ndarray:
     return (gam + (nchunks + 1) * 2.0 ** -53) * B
 
 
+def gram_accumulation_bound(A, d: np.ndarray, u_f: str, K_t: int = 64, super_chunks: int = 64,
+                            truncating: bool = True, nsplit: int = 148) -> np.ndarray:
+    """Elementwise bound on |G - A^^T A^| for every member of the accumulation family that
+    reading R11 fixes for the dense u_f in {fp16, bf16} Gram:
+      level 1  each K_t-row chunk summed in fp32 (the tensor cores): unit u1 = 2^-23 when the
+               adder truncates (R11 measured a truncation bias), 2^-24 for round-to-nearest;
+      level 2  `super_chunks` consecutive chunk sums added in fp32, round to nearest (2^-24);
+      level 3  everything after that in fp64: the flushes of one row split and `nsplit` splits.
+    With gamma(k, u) = k u / (1 - k u) and S = |A^|^T |A^| (the exact products are exact):
+      |G - A^^T A^| <= [ (1 + g1)(1 + g2)(1 + g3) - 1 ] S,
+      g1 = gamma(K_t - 1, u1),  g2 = gamma(super_chunks - 1, 2^-24),
+      g3 = gamma(ceil(m / (K_t super_chunks)) + nsplit, 2^-53),
+    the standard recursive-summation bound applied level by level (each level's inputs are the
+    previous level's computed sums, whose magnitudes are bounded by (1 + g) times the exact
+    sums of |products|).  gram_exact_bound is the one-level special case."""
+    m = A.shape[0]
+    def gam(k, u):
+        k = max(int(k), 0)
+        return k * u / (1.0 - k * u)
+    g1 = gam(min(K_t, m) - 1, 2.0 ** -23 if truncating else 2.0 ** -24)
+    g2 = gam(min(super_chunks, -(-m // K_t)) - 1, 2.0 ** -24)
+    g3 = gam(-(-m // (K_t * super_chunks)) + nsplit, 2.0 ** -53)
+    S = np.zeros((A.shape[1], A.shape[1]))
+    for c0 in range(0, m, 65536):
+        blk = A[c0:c0 + 65536]
+        blk = blk.toarray() if _is_sparse(blk) else np.asarray(blk)
+        Ah = np.abs(round_to(blk / d[None, :], u_f))
+        S += Ah.T @ Ah
+    return ((1 + g1) * (1 + g2) * (1 + g3) - 1) * S
+
+
 # ----------------------------------------------------------------------------- Cholesky
 @dataclasses.dataclass
 class Precond:
@@ -162,12 +287,12 @@ class Precond:
 def factor_precond_qr(A, u_f: str, row_blocks=None) -> Precond:
     """The paper's preferred preconditioner: R~ = the R factor
     of a Householder QR of A D^{-1} computed with every operation in u_f (oracle/qr.py,
-    reading R25), the same power-of-two scaling D as the Cholesky route (SURVEY §8(f)
-    NEXT-2; GPU: tls_factor_precond_qr).  row_blocks: the TSQR leaves (R26)."""
+    reading R25), scaled by the paper's D = diag(A^T A)^{1/2} rounded to powers of two
+    (norm_scaling, reading R27; GPU: tls_factor_precond_qr).  row_blocks: the TSQR leaves (R26)."""
     from .qr import householder_qr_r, tsqr_r
     A_d = A.toarray() if _is_sparse(A) else np.asarray(A)
     n = A_d.shape[1]
-    d, normA2 = column_scaling(A)
+    d, normA2 = norm_scaling(A)
     try:
         # row_blocks: the TSQR leaves of a row-sharded A (R26); None = one block
         Rt = householder_qr_r(A_d / d, u_f) if row_blocks is None else tsqr_r(A_d / d, row_blocks, u_f)

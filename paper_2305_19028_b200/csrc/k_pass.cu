@@ -379,19 +379,23 @@ int launch_reduce(const double* partials, int G, int W, int nmax, double* out, c
   return 0;
 }
 
-// --------------------------------------------------------------------------- scaling D (R2)
+// --------------------------------------------------------------------------- scaling D
+// mode 0 (Cholesky route, R2): d_j = 2^floor(log2 max_i |a_ij|).
+// mode 1 (QR route, R27): the paper's D = diag(A^T A)^{1/2} rounded to a
+// power of two: k = floor(log2 c_j), d_j = 2^ceil(k/2), decided on c_j's exponent alone.
 __global__ void k_scaling(const double* __restrict__ colmax, const double* __restrict__ sumsq, int n,
                           double* __restrict__ d, double* __restrict__ dinv, double* __restrict__ normA2,
-                          int* __restrict__ flag) {
+                          int* __restrict__ flag, int mode) {
   __shared__ double red[32];
   double s = 0.0;
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    const double cm = colmax[j];
+    const double cm = mode == 0 ? colmax[j] : sumsq[j];
     if (!(cm > 0.0) || !isfinite(cm)) atomicExch(flag, 1);
     int e = 0;
     frexp(cm, &e);
-    d[j] = scalbn(1.0, e - 1);
-    dinv[j] = scalbn(1.0, 1 - e);
+    const int p = mode == 0 ? e - 1 : -((1 - e) >> 1);   // mode 1: ceil((e - 1) / 2)
+    d[j] = scalbn(1.0, p);
+    dinv[j] = scalbn(1.0, -p);
     s += sumsq[j];
   }
   s = block_sum(s, red);
@@ -399,8 +403,8 @@ __global__ void k_scaling(const double* __restrict__ colmax, const double* __res
 }
 
 int launch_scaling(const double* colmax, const double* sumsq, int n, double* d, double* dinv,
-                   double* normA2, int* flag, cudaStream_t st) {
-  k_scaling<<<1, 1024, 0, st>>>(colmax, sumsq, n, d, dinv, normA2, flag);
+                   double* normA2, int* flag, cudaStream_t st, int mode) {
+  k_scaling<<<1, 1024, 0, st>>>(colmax, sumsq, n, d, dinv, normA2, flag, mode);
   TLS_LAUNCH_CHECK();
   return 0;
 }

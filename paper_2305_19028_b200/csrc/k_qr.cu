@@ -407,7 +407,7 @@ template <typename T, int PREC>
 __global__ void __launch_bounds__(kQrThreads) k_qr_fin(const T* __restrict__ W, int n, int ldw, int j, int b0, int nb,
                                                         const double* __restrict__ partP, double* __restrict__ wT,
                                                         double* __restrict__ scal, double* __restrict__ G,
-                                                        int* __restrict__ qflags) {
+                                                        int* __restrict__ qflags, int leaf) {
   __shared__ double red[32];
   // programmatic dependent launch: the next kernel of the chain may be scheduled now; this
   // one waits for its predecessor's writes before reading anything
@@ -422,14 +422,17 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_fin(const T* __restrict__ W, 
   const double tail = block_sum(tl, red);                      // fixed order: same bits in every CTA
   const double x0 = (double)W[(int64_t)j * ldw + j];
   const double sigma = round_uf(sqrt(round_uf(fma(x0, x0, tail), prec)), prec);
-  if (sigma == 0.0) {        // zero column in u_f (an overflowed inf/NaN goes on, as in the oracle: TLS_RANGE)
+  const bool ident = sigma == 0.0;
+  if (ident && !leaf) {      // zero column in u_f (an overflowed inf/NaN goes on, as in the oracle: TLS_RANGE)
     if (blockIdx.x == 0 && t == 0) { qflags[0] = 1; qflags[1] = j + 1; }
     return;
   }
-  const double alpha = x0 >= 0.0 ? -sigma : sigma;
-  const double v0 = round_uf(x0 - alpha, prec);
-  const double vv = round_uf(fma(v0, v0, tail), prec);
-  const double beta = round_uf(2.0 / vv, prec);
+  // a TSQR leaf's vanishing column (R26): the identity reflector (alpha = v_0 = beta = 0 gives
+  // w^T = 0, the update leaves every row as it is and R's row j is W[j, j:] with R_jj = 0)
+  const double alpha = ident ? 0.0 : (x0 >= 0.0 ? -sigma : sigma);
+  const double v0 = ident ? 0.0 : round_uf(x0 - alpha, prec);
+  const double vv = ident ? 1.0 : round_uf(fma(v0, v0, tail), prec);
+  const double beta = ident ? 0.0 : round_uf(2.0 / vv, prec);
   const int k = j + 1 + blockIdx.x * 32 + lane;
   double s0 = 0.0, s1 = 0.0;
   if (k < n) {
@@ -506,7 +509,7 @@ int qr_step_launch(T* W, const DenseView& A, int ldw, const double* dinv, int j,
 
 template <typename T, int CPT, int PREC>
 int qr_t(const DenseView& A, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
-         int* qflags, double* G, cudaStream_t st, int* launches, int row_stride) {
+         int* qflags, double* G, cudaStream_t st, int* launches, int row_stride, int leaf) {
   const int n = A.n;
   const int64_t m = A.m;
   const int RB = qr_rows_per_cta(m, n);
@@ -520,7 +523,7 @@ int qr_t(const DenseView& A, const double* dinv, void* Wbuf, double* partP, doub
     // opt-in (TLS_QR_COOP=1): measured slower than the PDL chain (4096 x 512: 5.4 vs 4.4 ms,
     // 65536 x 2048: 418 vs 301 ms), like the other cooperative streaming passes
     const char* ce = getenv("TLS_QR_COOP");
-    const bool coop_env = ce && ce[0] == '1';
+    const bool coop_env = ce && ce[0] == '1' && !leaf;   // the cooperative loop has no leaf mode
     const size_t smem = (size_t)qr_step_threads<CPT>() * CPT * sizeof(double);
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
@@ -550,7 +553,7 @@ int qr_t(const DenseView& A, const double* dinv, void* Wbuf, double* partP, doub
     const int nbj = j == 0 ? nb : (int)((m_act(j - 1) + RB - 1) / RB);   // CTAs that wrote them
     const int nf = (n - j - 1 + 31) / 32;
     rc = launch_pdl(k_qr_fin<T, PREC>, nf > 0 ? nf : 1, kQrThreads, 0, st, (const T*)W, n, ldw, j, b0, nbj,
-                    (const double*)partP, wT, scal, G, qflags);
+                    (const double*)partP, wT, scal, G, qflags, leaf);
     if (rc) return rc;
     ++nl;
     if (j + 1 < n) {
@@ -570,11 +573,11 @@ int qr_t(const DenseView& A, const double* dinv, void* Wbuf, double* partP, doub
 
 template <typename T, int PREC>
 int qr_dispatch(const DenseView& A, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
-                int* qflags, double* G, cudaStream_t st, int* launches, int rs) {
+                int* qflags, double* G, cudaStream_t st, int* launches, int rs, int leaf) {
   // 8 columns per thread up to n = 2048 (measured: 4 per thread is 1.2-1.3x slower at n = 1024,
   // 16 per thread with 256-thread CTAs 1.1x slower at n = 1024 and 2048)
-  if (A.n <= 8 * kQrThreads) return qr_t<T, 8, PREC>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, rs);
-  return qr_t<T, 16, PREC>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, rs);
+  if (A.n <= 8 * kQrThreads) return qr_t<T, 8, PREC>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, rs, leaf);
+  return qr_t<T, 16, PREC>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, rs, leaf);
 }
 }  // namespace
 
@@ -596,13 +599,13 @@ size_t qr_work_bytes(int64_t m, int n, int u_f) {
 }
 
 int launch_qr(const DenseView& A, int u_f, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
-              int* qflags, double* G, cudaStream_t st, int* launches, int row_stride) {
+              int* qflags, double* G, cudaStream_t st, int* launches, int row_stride, int leaf) {
   if (A.n > kMaxDenseN) { set_error("QR: n > %d", kMaxDenseN); return TLS_ERR_ARG; }
   switch (u_f) {
-    case TLS_FP16: return qr_dispatch<float, TLS_FP16>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, row_stride);
-    case TLS_BF16: return qr_dispatch<float, TLS_BF16>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, row_stride);
-    case TLS_FP32: return qr_dispatch<float, TLS_FP32>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, row_stride);
-    default: return qr_dispatch<double, TLS_FP64>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, row_stride);
+    case TLS_FP16: return qr_dispatch<float, TLS_FP16>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, row_stride, leaf);
+    case TLS_BF16: return qr_dispatch<float, TLS_BF16>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, row_stride, leaf);
+    case TLS_FP32: return qr_dispatch<float, TLS_FP32>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, row_stride, leaf);
+    default: return qr_dispatch<double, TLS_FP64>(A, dinv, Wbuf, partP, wT, scal, qflags, G, st, launches, row_stride, leaf);
   }
 }
 

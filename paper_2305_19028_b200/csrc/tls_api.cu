@@ -785,9 +785,15 @@ struct QrBufs {
   int* qflags = nullptr;
 };
 
+// Partial rows of an update pass over <= m rows: qr_rows_per_cta is not monotone in m (a TSQR
+// leaf of m' < m rows can use more CTAs than m itself), so size for every m' <= m:
+// ceil(m'/RB(m')) <= min(ceil(m'/32), 148) <= min(ceil(m/32), 148).
 size_t qr_partials(int64_t m, int n) {
+  int64_t nb = (m + 31) / 32;
+  if (nb > 148) nb = 148;
   const int RB = qr_rows_per_cta(m, n);
-  return (size_t)((m + RB - 1) / RB) * n;
+  const int64_t own = (m + RB - 1) / RB;
+  return (size_t)(nb > own ? nb : own) * n;
 }
 
 // Carves (or, with ws == nullptr, measures) the QR buffers after the solve workspace.
@@ -832,11 +838,6 @@ int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, v
   const int rank = comm ? comm->rank : 0;
   const int sub = qr_leaves();
   const int nleaf = P * sub;
-  if (nleaf > 1 && A->m_local / sub < n) {
-    set_error("TSQR: every leaf needs >= n rows (m_local = %lld, %d leaves per rank, n = %d)",
-              (long long)A->m_local, sub, n);
-    return TLS_ERR_ARG;
-  }
   Work w;
   QrBufs q;
   bool ok = false;
@@ -846,16 +847,31 @@ int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, v
     return TLS_ERR_WORKSPACE;
   }
   Ctx cx{static_cast<cudaStream_t>(stream), comm};
+  // every leaf needs >= n rows; decided collectively (max over ranks) so that all ranks
+  // return the same status instead of some entering the stack all-reduce alone
+  double bad = (nleaf > 1 && A->m_local / sub < n) ? 1.0 : 0.0;
+  if (P > 1) {
+    TLS_CUDA_TRY(cudaMemcpyAsync(w.d_tmp, &bad, 8, cudaMemcpyHostToDevice, cx.st));
+    TLS_TRY(allreduce(comm, w.d_tmp, 1, ncclMax, cx.st));
+    TLS_CUDA_TRY(cudaMemcpyAsync(&bad, w.d_tmp, 8, cudaMemcpyDeviceToHost, cx.st));
+    TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+  }
+  if (bad != 0.0) {
+    set_error("TSQR: every leaf needs >= n rows (m_local = %lld, %d leaves per rank, n = %d, on this or another rank)",
+              (long long)A->m_local, sub, n);
+    return TLS_ERR_ARG;
+  }
   Tracer tr(cx.st);
   tr.mark("qr:start");
   TLS_CUDA_TRY(cudaMemsetAsync(w.flags, 0, 8 * sizeof(int), cx.st));
   TLS_CUDA_TRY(cudaMemsetAsync(q.qflags, 0, 4 * sizeof(int), cx.st));
-  // the same D = powers of two and ||A||_F^2 as the Cholesky route (R2), all-reduced
+  // column sums of squares, all-reduced; D = the paper's diag(A^T A)^{1/2} rounded to powers
+  // of two (R27), ||A||_F^2
   TLS_TRY(run_pass(cx, A, PASS_COLSTATS, 2, nullptr, nullptr, w, nullptr));
   double* d = w.d_tmp;
   double* dinv = w.d_tmp + n;
   double* normA2 = w.d_tmp + 2 * n;
-  TLS_TRY(launch_scaling(w.colstats, w.colstats + n, n, d, dinv, normA2, &w.flags[0], cx.st));
+  TLS_TRY(launch_scaling(w.colstats, w.colstats + n, n, d, dinv, normA2, &w.flags[0], cx.st, 1));
   cx.launches += 1;
   tr.mark("colstats");
   {
@@ -873,7 +889,7 @@ int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, v
         const int64_t r0 = s * ml / sub, r1 = (s + 1) * ml / sub;
         DenseView leaf{A->vals + r0 * A->ld, r1 - r0, n, A->ld};
         TLS_CUDA_TRY(cudaMemsetAsync(q.G, 0, (size_t)n * n * 8, cx.st));
-        TLS_TRY(launch_qr(leaf, u_f, dinv, q.W1, q.part1, q.wT, q.scal, q.qflags, q.G, cx.st, &cx.launches));
+        TLS_TRY(launch_qr(leaf, u_f, dinv, q.W1, q.part1, q.wT, q.scal, q.qflags, q.G, cx.st, &cx.launches, 0, 1));
         // row i of leaf L goes to stack row i nleaf + L (row-interleaved, R26)
         TLS_CUDA_TRY(cudaMemcpy2DAsync(q.S + (size_t)(rank * sub + s) * n, (size_t)nleaf * n * 8, q.G, (size_t)n * 8,
                                        (size_t)n * 8, (size_t)n, cudaMemcpyDeviceToDevice, cx.st));

@@ -40,7 +40,7 @@ int launch_reduce(const double* partials, int G, int W, int nmax, double* out, c
 // d_j = 2^floor(log2 colmax_j), dinv_j = 1/d_j, normA2 = sum_j sumsq_j; *flag = 1 on a zero or
 // non-finite column.
 int launch_scaling(const double* colmax, const double* sumsq, int n, double* d, double* dinv,
-                   double* normA2, int* flag, cudaStream_t st);
+                   double* normA2, int* flag, cudaStream_t st, int mode = 0);
 int launch_round(const double* x, double* y, int64_t n, int prec, cudaStream_t st);
 
 // ---- CSR (k_csr.cu) --------------------------------------------------------------------
@@ -156,7 +156,9 @@ size_t qr_work_bytes(int64_t m, int n, int u_f);   // W copy + partials + w^T + 
 // dinv == nullptr: no scaling (the TSQR stack of already scaled leaf R's)
 // row_stride > 0: A is the row-interleaved TSQR stack of row_stride leaf R's (rows >= (j+2)
 // row_stride are zero in columns j, j+1 and are skipped, R26)
+// leaf = 1: a TSQR leaf (R26): a column vanishing on these rows takes the identity reflector
+// (R_jj = 0) instead of raising the breakdown flag
 int launch_qr(const DenseView& A, int u_f, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
-              int* qflags, double* G, cudaStream_t st, int* launches, int row_stride = 0);
+              int* qflags, double* G, cudaStream_t st, int* launches, int row_stride = 0, int leaf = 0);
 
 }  // namespace tls

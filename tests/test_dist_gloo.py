@@ -163,7 +163,8 @@ def test_row_sharded_solve_world2():
 
 def _tsqr_worker(rank, world, port, out):
     """The exchange of the row-sharded QR preconditioner (tls_factor_precond_qr, R26): each
-    rank factors its own rows (D from the all-reduced column maxima), writes its R into its
+    rank factors its own rows (D from the all-reduced column sums of squares, R27; a column
+    vanishing on a rank's rows takes the identity reflector, R26), writes its R into its
     rows of a zeroed (world n) x n stack (row i of rank p's R at stack row i world + p), the
     stack is sum-all-reduced (every other slot is zero, so the sum is exact), and every rank
     factors the stack."""
@@ -176,10 +177,10 @@ def _tsqr_worker(rank, world, port, out):
         A = P.A
         m, n = A.shape
         lo, hi = shard_rows(m, world, rank)
-        cm = _allreduce(np.max(np.abs(A[lo:hi]), axis=0), tdist.ReduceOp.MAX)
-        d = np.exp2(np.floor(np.log2(cm)))
+        c = _allreduce(np.sum(A[lo:hi] * A[lo:hi], axis=0))
+        d = np.exp2(np.ceil((np.frexp(c)[1] - 1) / 2))                # 2^ceil(floor(log2 c) / 2)
         S = np.zeros((world * n, n))
-        S[rank::world] = householder_qr_r(A[lo:hi] / d, "fp16")      # row-interleaved slots (R26)
+        S[rank::world] = householder_qr_r(A[lo:hi] / d, "fp16", leaf=True)   # row-interleaved slots (R26)
         S = _allreduce(S)
         R = householder_qr_r(S, "fp16")
         pc = rqi.factor_precond_qr(A, "fp16", row_blocks=[shard_rows(m, world, r) for r in range(world)])

@@ -1,16 +1,15 @@
 """GPU parity of the Householder-QR preconditioner in u_f (PAPER.md
-l.215-218, l.231; reading R25) against oracle/qr.py through the C ABI.
+l.215-218, l.231; readings R25-R27) against oracle/qr.py through the C ABI.
 
-What is compared, and why not bit for bit: both sides round every elementwise operation
-to u_f in the same order and take the same sign decisions; only the fp64 inner products
-(x^T x, v^T W) are summed in a different order before their single rounding to u_f.  So
-  - D and ||A||_F^2: bit-exact / 1e-14 (the Cholesky route's own pass);
-  - R~: each entry agrees to a few u_f ulps (a rounded inner product can land on the
-    other side of a u_f rounding boundary, and that difference then propagates through
-    the remaining columns like any other rounding error of the factorization); the bound
-    written below is the QR backward-error bound the oracle is pinned to (test_oracle_qr:
-    ||R^T R - Ah^T Ah||_F <= 10 m n u ||Ah||_F^2) applied to the GPU's R~, plus a normwise
-    distance to the oracle's R~ within the same bound's forward image (kappa(Ah) times it);
+Both sides round every elementwise operation to u_f at the same points (pinned exactly by
+test_oracle_qr.test_householder_rounding_points_exact) and take the same sign decisions; only
+the fp64 inner products (x^T x, v^T W) are summed in another order before their single
+rounding to u_f, which changes a rounded value only when the fp64 sum lies within its own
+rounding error (~1e-16 relative) of a u_f rounding boundary.  So
+  - D and ||A||_F^2: bit-exact / 1e-14;
+  - R~ (u_f = fp16 / bf16 / fp32): entrywise in u_f ulps -- bit-identical on >= 99% of the
+    entries and within 2 ulps everywhere (_assert_entrywise);  u_f = fp64: the summation order
+    itself is the rounding, so 1e-12 kappa(Ah) relative (normwise) instead;
   - a solve with the GPU's QR R~: the north_star tolerances against the oracle run on the
     same R~ (x 1e-9, sigma 1e-12, same RQI count, PCG counts equal) and against the SVD.
 """
@@ -51,6 +50,32 @@ def _rel(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300))
 
 
+def _ordered(x, fmt):
+    """u_f values -> integers whose differences count u_f ulps (sign-magnitude folded)."""
+    x = np.asarray(x, dtype=np.float64)
+    if fmt == "fp16":
+        b = x.astype(np.float16).view(np.int16).astype(np.int64)
+        return np.where(b < 0, -(b & 0x7FFF), b)
+    b = x.astype(np.float32).view(np.int32).astype(np.int64)
+    if fmt == "bf16":
+        b = b >> 16
+        return np.where(b < 0, -(b & 0x7FFF), b)
+    return np.where(b < 0, -(b & 0x7FFFFFFF), b)
+
+
+def _assert_entrywise(Rt, Ro, fmt, frac_equal=0.99, max_ulps=2):
+    """GPU R~ vs oracle R~ entry by entry: identical bits on >= frac_equal of the stored
+    (upper) entries and at most max_ulps u_f ulps apart elsewhere; u_f = fp64: normwise."""
+    iu = np.triu_indices(Rt.shape[0])
+    if fmt == "fp64":
+        assert _rel(Rt, Ro) <= 1e-12 * max(1.0, np.linalg.cond(Ro))
+        return
+    a, b = Rt[iu], Ro[iu]
+    same = np.mean(a.view(np.uint64) == b.view(np.uint64))
+    ulps = np.abs(_ordered(a, fmt) - _ordered(b, fmt))
+    assert same >= frac_equal and ulps.max() <= max_ulps, (same, int(ulps.max()))
+
+
 def _problem(m, n, kappa, seed, spread=True):
     rng = np.random.default_rng(seed)
     U, _ = np.linalg.qr(rng.standard_normal((m, n)))
@@ -84,12 +109,7 @@ def test_qr_factor_parity(T, m, n, kappa, fmt):
     assert np.array_equal(np.tril(Rt, -1), np.zeros_like(Rt))
     assert np.all(np.diag(Rt) > 0)
     assert np.array_equal(round_to(Rt, fmt), Rt)                 # stored in u_f
-    u = unit_roundoff(fmt)
-    Ah = round_to(A / d, fmt)
-    bound = 10 * m * n * u * np.linalg.norm(Ah) ** 2
-    assert np.linalg.norm(Rt.T @ Rt - Ah.T @ Ah) <= bound         # backward error (pinned bound)
-    kap = np.linalg.cond(Ah)
-    assert _rel(Rt, pc.Rt) <= 10 * m * n * u * kap
+    _assert_entrywise(Rt, pc.Rt, fmt)
 
 
 @pytest.mark.parametrize("m,n,kappa,fmt", [(200, 20, 1e2, "fp16"), (777, 67, 1e3, "bf16"), (5000, 1100, 1e2, "fp16"),
@@ -102,8 +122,8 @@ def test_qr_solve_parity(T, m, n, kappa, fmt):
     assert rc == 0
     rc, x, sig, info = T.tls_rqi_pcgtls(M, dev(b), R)
     Rt, d, nrm = T.tls_precond_export(R)
-    Ah = round_to(A / d, fmt)      # backward error of the GPU's QR (the bound the oracle is pinned to)
-    assert np.linalg.norm(Rt.T @ Rt - Ah.T @ Ah) <= 10 * m * n * unit_roundoff(fmt) * np.linalg.norm(Ah) ** 2
+    if m * n * n <= 4e8:                    # the oracle's u_f QR costs O(m n^2) numpy passes
+        _assert_entrywise(Rt, rqi.factor_precond_qr(A, fmt).Rt, fmt)
     res = rqi.rqi_pcgtls_mp(A, b, rqi.Precond(Rt, d, fmt, nrm))
     ex = exact.tls_svd(A, b)
     assert info["status"] == res.status == rqi.OK
@@ -122,7 +142,7 @@ def test_qr_cfg1_paper_workload(T):
     assert rc == 0
     Rt, d, nrm = T.tls_precond_export(R)
     pc = rqi.factor_precond_qr(P.A, "fp16")
-    assert _rel(Rt, pc.Rt) <= 1e-2
+    _assert_entrywise(Rt, pc.Rt, "fp16")
     rc, x, sig, info = T.tls_rqi_pcgtls(M, dev(P.b), R)
     ex = exact.tls_svd(P.A, P.b)
     assert _rel(x.cpu().numpy(), ex.x) <= 1e-9
@@ -171,10 +191,7 @@ def test_paper_sec4_problems_qr(T, name, fmt):
         assert finfo["chol_pivot"] == pc.chol_pivot
         return
     Rt, d, nrm = T.tls_precond_export(R)
-    m, n = P.A.shape
-    Ah = round_to(P.A / d, fmt)
-    assert np.linalg.norm(Rt.T @ Rt - Ah.T @ Ah) <= 10 * m * n * unit_roundoff(fmt) * np.linalg.norm(Ah) ** 2
-    assert _rel(Rt, pc.Rt) <= 10 * m * n * unit_roundoff(fmt) * np.linalg.cond(Ah)
+    _assert_entrywise(Rt, pc.Rt, fmt)
     rc, x, sig, info = T.tls_rqi_pcgtls(M, dev(P.b), R)
     res = rqi.rqi_pcgtls_mp(P.A, P.b, rqi.Precond(Rt, d, fmt, nrm))
     assert info["status"] == res.status
@@ -205,10 +222,7 @@ def test_qr_tsqr_leaves(T, monkeypatch, leaves, m, n, fmt):
     Rt, d, nrm = T.tls_precond_export(R)
     assert np.array_equal(d, pc.d)
     assert np.all(np.diag(Rt) > 0) and np.array_equal(round_to(Rt, fmt), Rt)
-    u = unit_roundoff(fmt)
-    Ah = round_to(A / d, fmt)
-    assert np.linalg.norm(Rt.T @ Rt - Ah.T @ Ah) <= 2 * 10 * m * n * u * np.linalg.norm(Ah) ** 2
-    assert _rel(Rt, pc.Rt) <= 2 * 10 * m * n * u * np.linalg.cond(Ah)
+    _assert_entrywise(Rt, pc.Rt, fmt)
     rc, x, sig, info = T.tls_rqi_pcgtls(M, dev(b), R)
     res = rqi.rqi_pcgtls_mp(A, b, rqi.Precond(Rt, d, fmt, nrm))
     assert info["status"] == res.status == rqi.OK
@@ -216,6 +230,44 @@ def test_qr_tsqr_leaves(T, monkeypatch, leaves, m, n, fmt):
     assert info["pcg_iters"] == [tuple(p) for p in res.pcg_iters]
     assert _rel(x.cpu().numpy(), res.x) <= 1e-9
     assert abs(sig - res.sigma) / res.sigma <= 1e-12
+
+
+@pytest.mark.parametrize("leaves,m,n", [(3, 14209, 16), (2, 9473, 16)])
+def test_qr_tsqr_leaf_partials_sizing(T, monkeypatch, leaves, m, n):
+    """qr_rows_per_cta is not monotone in m -- 14209 rows in 3 leaves of 4736/4737
+    rows use 148/148/144 update CTAs against 147 for 14209 rows, 9473 in 2 leaves 148 vs 146.
+    The partials buffer is sized for every leaf; R~ equals the oracle's tsqr_r entrywise."""
+    from oracle.qr import even_row_blocks
+    monkeypatch.setenv("TLS_QR_LEAVES", str(leaves))
+    A, b = _problem(m, n, 1e2, seed=m, spread=True)
+    M, keep = _mat(T, A)
+    rc, R, info = T.tls_factor_precond_qr(M, "fp16")
+    assert rc == 0
+    Rt, d, nrm = T.tls_precond_export(R)
+    pc = rqi.factor_precond_qr(A, "fp16", row_blocks=even_row_blocks(m, leaves))
+    _assert_entrywise(Rt, pc.Rt, "fp16")
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "fp64"])
+def test_qr_tsqr_leaf_vanishing_column(T, monkeypatch, fmt):
+    """a column that is zero on one leaf's rows of a full-rank A is not a rank
+    deficiency -- the leaf takes the identity reflector (R26) and the factorization succeeds
+    with the oracle's tsqr_r R~; a column zero on every row is still CHOL_BREAKDOWN."""
+    from oracle.qr import even_row_blocks
+    monkeypatch.setenv("TLS_QR_LEAVES", "3")
+    A, b = _problem(900, 24, 1e2, seed=17, spread=False)
+    A[:300, 5] = 0.0
+    M, keep = _mat(T, A)
+    rc, R, info = T.tls_factor_precond_qr(M, fmt)
+    pc = rqi.factor_precond_qr(A, fmt, row_blocks=even_row_blocks(900, 3))
+    assert rc == pc.status == 0
+    Rt, d, nrm = T.tls_precond_export(R)
+    _assert_entrywise(Rt, pc.Rt, fmt)
+    A[:, 5] = 0.0
+    A[0, 5] = 0.0
+    M2, keep2 = _mat(T, A)
+    with pytest.raises(T.TlsError):       # a zero column of A itself is an argument error (rank deficient)
+        T.tls_factor_precond_qr(M2, fmt)
 
 
 def test_qr_tsqr_leaf_too_short(T, monkeypatch):
@@ -240,7 +292,11 @@ def test_qr_extreme_widths(T, m, n, fmt):
     assert np.array_equal(np.tril(Rt, -1), np.zeros_like(Rt)) and np.all(np.diag(Rt) > 0)
     assert np.array_equal(round_to(Rt, fmt), Rt)
     Ah = round_to(A / d, fmt)
-    assert np.linalg.norm(Rt.T @ Rt - Ah.T @ Ah) <= 10 * m * n * unit_roundoff(fmt) * np.linalg.norm(Ah) ** 2
+    if m * n * n <= 4e8:
+        _assert_entrywise(Rt, rqi.factor_precond_qr(A, fmt).Rt, fmt)
+    else:                                   # backward error of the GPU's R~ (probabilistic form, c = 2)
+        u = unit_roundoff(fmt)
+        assert np.linalg.norm(Rt.T @ Rt - Ah.T @ Ah) <= 2 * np.sqrt(m) * n ** 0.75 * u * np.linalg.norm(Ah) ** 2
     if n == 1:
         assert Rt[0, 0] == pytest.approx(np.linalg.norm(Ah), rel=2 * unit_roundoff(fmt))
         return
@@ -264,33 +320,27 @@ def test_qr_persistent_kernel_variant(T, monkeypatch, m, n, fmt):
     assert rc == 0 and info["launches"] < 20
     Rt, d, nrm = T.tls_precond_export(R)
     pc = rqi.factor_precond_qr(A, fmt)
-    u = unit_roundoff(fmt)
-    Ah = round_to(A / d, fmt)
-    assert np.linalg.norm(Rt.T @ Rt - Ah.T @ Ah) <= 10 * m * n * u * np.linalg.norm(Ah) ** 2
-    assert _rel(Rt, pc.Rt) <= 10 * m * n * u * np.linalg.cond(Ah)
+    _assert_entrywise(Rt, pc.Rt, fmt)
     rc, x, sig, sinfo = T.tls_rqi_pcgtls(M, dev(b), R)
     res = rqi.rqi_pcgtls_mp(A, b, rqi.Precond(Rt, d, fmt, nrm))
     assert sinfo["status"] == res.status == rqi.OK and sinfo["rqi_iters"] == res.rqi_iters
     assert _rel(x.cpu().numpy(), res.x) <= 1e-9
 
 
-def test_qr_fp16_norm_overflow_is_range(T):
-    """A tall column whose squared norm exceeds fp16's range (70000 entries in [1/2, 1) after
-    the power-of-two scaling: x^T x > 65504) overflows when the inner product is rounded to
-    fp16 (R25).  The oracle carries the inf/NaN through and reports RANGE; so must the GPU (not
-    a zero-column breakdown).  bf16 has fp32's range and factors the same matrix."""
-    import warnings
+def test_qr_norm_scaling_keeps_fp16_in_range(T):
+    """A tall column of 70000 entries in [1/2, 1): under round 1's max-based D its x^T x
+    (> 65504) overflowed fp16 when rounded (TLS_RANGE).  The paper's
+    D = diag(A^T A)^{1/2} rounded to powers of two (R27) scales every column to
+    a norm in [2^-1/2, 2^1/2), so fp16 factors it -- bit for bit like the oracle -- and so does
+    bf16."""
     rng = np.random.default_rng(0)
     A = rng.uniform(0.5, 1.0, (70000, 4))
     M, keep = _mat(T, A)
-    with warnings.catch_warnings():
-        warnings.simplefilter("ignore")
-        pc16 = rqi.factor_precond_qr(A, "fp16")
-    assert pc16.status == rqi.RANGE
-    rc, R, info = T.tls_factor_precond_qr(M, "fp16")
-    assert rc == rqi.RANGE and R is None
-    pcb = rqi.factor_precond_qr(A, "bf16")
-    rc, R, info = T.tls_factor_precond_qr(M, "bf16")
-    assert rc == pcb.status == 0
-    Rt, d, nrm = T.tls_precond_export(R)
-    assert _rel(Rt, pcb.Rt) <= 10 * 70000 * 4 * unit_roundoff("bf16") * np.linalg.cond(round_to(A / d, "bf16"))
+    for fmt in ("fp16", "bf16"):
+        pc = rqi.factor_precond_qr(A, fmt)
+        assert pc.status == rqi.OK
+        rc, R, info = T.tls_factor_precond_qr(M, fmt)
+        assert rc == 0
+        Rt, d, nrm = T.tls_precond_export(R)
+        assert np.array_equal(d, pc.d)
+        _assert_entrywise(Rt, pc.Rt, fmt)
