@@ -11,8 +11,8 @@ kappa 1e4, u_f fp16; reading R8), row-sharded over N GPUs.
 N > 1 is launched by torchrun (one process per GPU, RANK/LOCAL_RANK/WORLD_SIZE
 from the env); times are CUDA events on the solve stream, max over ranks.
 Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle
-(oracle/, the only reference this paper has) on a bounded sample of the same
-workload on the host cores.
+(oracle/, the only reference this paper has): every step is one whole oracle
+solve of the same workload on the host cores (no sample, no extrapolation).
 """
 from __future__ import annotations
 
@@ -107,49 +107,28 @@ def make_problem(wl, device):
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def oracle_sample(A_np, b_np, u_f, counts, row_scale=16, iters=2):
-    """Time the CPU oracle on a bounded sample of the workload and scale it to one
-    whole solve: (1) the oracle preconditioner build on the first m/row_scale rows
-    (its cost is linear in m), x row_scale; (2) `iters` oracle PCGTLS iterations
-    (A-in-loop, one RHS) and one residual evaluation on the FULL A; composed with
-    the iteration counts of the solve (same algorithm, same counts):
-      T = row_scale*t_factor + t_resid*(K + 2) + t_iter*(B0 + sum_k (c_a + c_b))."""
+def oracle_solve_timed(A_np, b_np, u_f):
+    """The CPU oracle as it stands (oracle.rqi.solve: its scaling, fp32-chunked Gram, LAPACK
+    Cholesky and RQI-PCGTLS-MP) timed end to end on the WHOLE workload on the host cores --
+    no row sample, no extrapolation, the oracle's own iteration counts.  Returns
+    (seconds, result, sample description, cores)."""
     from oracle import rqi as orq
-    import numpy as np
-    m, n = A_np.shape
-    if not isinstance(A_np, np.ndarray):
-        row_scale = 1          # CSR: the oracle factors the whole (28 MB) matrix in seconds
-    blk = max(n + 1, m // row_scale)
     t0 = time.perf_counter()
-    pc = orq.factor_precond(A_np[:blk], u_f)
-    t_factor = (time.perf_counter() - t0) * (m / blk)
-    if pc.status != orq.OK:
-        # the row sample can be too short for a positive definite u_f Gram (small m): time the
-        # iterations with an identity R~ instead (their cost does not depend on R~'s values)
-        pc = orq.Precond(np.eye(n), np.ones(n), u_f, 1.0)
-    f = np.ones(n)
-    t0 = time.perf_counter()
-    orq.pcgtls(A_np, pc, 0.0, f, iters, 0.0, "A")
-    t_iter = (time.perf_counter() - t0) / iters
-    x = np.zeros(n)
-    t0 = time.perf_counter()
-    orq.newton_residual(A_np, b_np, x)
-    t_resid = time.perf_counter() - t0
-    K, B0, pcg = counts
-    total = t_factor + t_resid * (K + 2) + t_iter * (B0 + sum(a + b for a, b in pcg))
-    sample = (f"oracle factor on {blk} of {m} rows (x{m / blk:.0f}) + {iters} oracle PCGTLS iterations "
-              f"and 1 residual pass on the full A, composed with the solve's counts K={K}, B0={B0}, "
-              f"PCG={sum(a + b for a, b in pcg)}")
-    return total, sample, {"t_factor_s": t_factor, "t_iter_s": t_iter, "t_resid_s": t_resid}
+    pc, res = orq.solve(A_np, b_np, u_f)
+    t = time.perf_counter() - t0
+    pcg = sum(a + b for a, b in res.pcg_iters)
+    sample = (f"the whole oracle solve (oracle.rqi.solve: factor + RQI-PCGTLS-MP) on the full "
+              f"{A_np.shape[0]}x{A_np.shape[1]} workload, unextrapolated, with the oracle's own counts "
+              f"(status {res.status}, K={res.rqi_iters}, B0={res.boot_iters}, PCG={pcg}, {res.passes} passes over A)")
+    return t, res, sample, orq._threads()
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle as it stands, on the host cores (rank 0 only)."""
+    """--impl reference: the CPU oracle as it stands, on the host cores (rank 0 only): every
+    warm-up and timed step is one whole oracle solve of the workload."""
     if rank != 0:
         return
-    import numpy as np
     import torch
-    from oracle import rqi as orq
     wl = args.workload
     dev = "cuda:0" if torch.cuda.is_available() else "cpu"
     P, u_f = make_problem(wl, dev)
@@ -161,26 +140,15 @@ def run_reference(args, rank, world):
         A_np = P.A.cpu().numpy() if hasattr(P.A, "cpu") else P.A
         b_np = P.b.cpu().numpy() if hasattr(P.b, "cpu") else P.b
     del P
-    # the oracle's own counts on this workload need a full oracle solve (too long);
-    # use the counts recorded by the last GPU run when present, else the oracle on
-    # a 1/16 row block as a stand-in for K and B0
-    counts = None
-    cpath = os.path.join(ROOT, "profiles", f"counts_{wl}.json")
-    if os.path.exists(cpath):
-        with open(cpath) as fh:
-            c = json.load(fh)
-        counts = (c["K"], c["B0"], [tuple(p) for p in c["pcg"]])
-    if counts is None:
-        blk = A_np.shape[0] // 16
-        _, res = orq.solve(A_np[:blk], b_np[:blk], u_f)
-        counts = (res.rqi_iters, res.boot_iters, res.pcg_iters)
+    if dev != "cpu":
+        torch.cuda.empty_cache()
     times = []
     for it in range(args.warmup + args.steps):
-        t, sample, parts = oracle_sample(A_np, b_np, u_f, counts, row_scale=64, iters=1)
+        t, res, sample, cores = oracle_solve_timed(A_np, b_np, u_f)
+        print(f"[reference] step {it}: {t:.2f} s", file=sys.stderr, flush=True)
         if it >= args.warmup:
             times.append(t)
     v = statistics.mean(times)
-    cores = os.cpu_count()
     line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -189,7 +157,8 @@ def run_reference(args, rank, world):
                        "u_f": u_f, "l2": "inputs larger than L2", "parallelism": "host cores"},
             "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "parts": parts}
+            "step_times_s": times, "status": int(res.status), "rqi_iters": res.rqi_iters,
+            "boot_iters": res.boot_iters, "pcg_iters": [list(p) for p in res.pcg_iters]}
     print(json.dumps(line), flush=True)
 
 
@@ -347,15 +316,19 @@ def main():
         working = max(1, min(working, p2["count"]))
         avg_ms = p2["ms"] / working
         ach = bytes_per_pass / (avg_ms * 1e-3) / 1e9
-        traffic = None
+        # DRAM bytes per launch of this kernel from the committed `ncu --set full` capture of the
+        # same launch (profiles/traffic_<workload>.json; ncu cannot run inside the timed region)
+        traffic, traffic_src = None, None
         tpath = os.path.join(ROOT, "profiles", f"traffic_{wl}.json")
         if os.path.exists(tpath):
             with open(tpath) as fh:
-                traffic = json.load(fh).get("pass_op2_dram_bytes_per_launch")
+                tj = json.load(fh)
+            traffic = tj.get("pass_op2_dram_bytes_per_launch")
+            traffic_src = f"committed ncu capture: profiles/traffic_{wl}.json ({tj.get('source', 'ncu --set full')})"
         roof = {"kernel": ("k_csr_rows<2,operator> + k_csr_cols<2> (t = A q, v = A^T t, 2 RHS; L2-resident operand)"
                            if csr else "k_pass<2,operator> (t = A q, v = A^T t, 2 RHS, one read of A)"),
                 "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": traffic, "algorithmic_bytes_per_launch": bytes_per_pass,
+                "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": bytes_per_pass,
                 "avg_launch_ms": avg_ms, "launches": p2["count"], "working_launches": working,
                 "peak_kind": peak_kind}
     kshare = {k: v["ms"] / ms_total for k, v in prof.items() if v["count"]}
@@ -405,11 +378,6 @@ def main():
         e2e = {"value": e_ms / args.steps / 1e3, "unit": "s",
                "h2d_bytes_per_step": int(A_h.numel() * 8 + b_h.numel() * 8),
                "d2h_bytes_per_step": int(n * 8)}
-
-    if rank == 0:
-        os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-        with open(os.path.join(ROOT, "profiles", f"counts_{wl}.json"), "w") as fh:
-            json.dump({"K": info["rqi_iters"], "B0": info["boot_iters"], "pcg": info["pcg_iters"]}, fh)
 
     # the compensated certificate of the returned x (c2 step 8), one extra untimed solve
     rc_c, R_c, _ = tlsrqi.tls_factor_precond(M, u_f, comm=comm, stream=stream, ws=ws)
@@ -530,11 +498,11 @@ def main():
     cpu = None
     if keep_host:
         import numpy as np
-        counts = (info["rqi_iters"], info["boot_iters"], info["pcg_iters"])
-        t_cpu, sample, parts = oracle_sample(A_full_host if csr else A_full_host.numpy(), b_full_host.numpy(),
-                                             u_f, counts)
-        cpu = {"value": t_cpu, "unit": "s", "cores": os.cpu_count(), "kind": "oracle", "sample": sample,
-               "parts": parts}
+        t_cpu, res_cpu, sample, cores = oracle_solve_timed(A_full_host if csr else A_full_host.numpy(),
+                                                           b_full_host.numpy(), u_f)
+        cpu = {"value": t_cpu, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample,
+               "same_counts_as_gpu": (res_cpu.rqi_iters, [tuple(p) for p in res_cpu.pcg_iters]) ==
+                                     (info["rqi_iters"], [tuple(p) for p in info["pcg_iters"]])}
         # the paper's flop model (oracle/perfmodel.py), "model only, no
         # hardware", at this (m, n, r = RQI steps): paper weights (u, u_p, u_q) = (fp64, fp32,
         # fp16) and the build's (fp64, fp64, u_f)

@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define TLSRQI_ABI_VERSION 4
+#define TLSRQI_ABI_VERSION 5
 
 #if defined(__GNUC__)
 #define TLS_API __attribute__((visibility("default")))
@@ -120,7 +120,12 @@ typedef struct {
   int32_t certify;        /* 1: after the solve, sigma_certified = sqrt(||b - A x||^2 / (1 + ||x||^2)) with
                              every residual and sum by Dot2 (compensated; one more pass over A;
                              SURVEY §8(c) c2 step 8); 0 [0]: skipped, sigma_certified = NaN */
-  int32_t reserved[2];
+  int32_t minimal_check;  /* R28: after an OK solve, this many PCGTLS steps at the returned sigma^2 on a fixed
+                             counter-based right-hand side; a curvature delta_j <= 0 shows A^T A - sigma^2 I is
+                             not positive definite (sigma >= sigma'_n: not the TLS solution, PAPER.md
+                             l.266-268) and the status becomes TLS_NOT_MINIMAL (x, sigma and the termination
+                             are kept).  One pass over A per step.  0 [0]: off */
+  int32_t reserved;
 } tls_rqi_opts_t;
 
 /* Results.  pcg_iters (2*max_outer ints), sigma2_trace, psi_trace
@@ -152,6 +157,20 @@ TLS_API const char* tls_last_error(void);
  * torch.distributed) before every rank calls tls_comm_init. */
 TLS_API int tls_comm_get_unique_id(void* id_out_host /* 128 bytes */);
 TLS_API int tls_comm_init(int nranks, int rank, const void* id_host, int device, tls_comm_t* out);
+/* Host-staged communicator for ranks that are processes sharing ONE GPU (PAPER.md has no
+ * multi-GPU design; this exercises the row-sharded path of SURVEY §8(e) on a single device).
+ * Every rank calls it with the same `name` (a POSIX shared-memory name starting with '/',
+ * unique per run: a stale segment of the same name is reused as is) and `slot_bytes` (the
+ * per-rank staging slot, >= 4096 and a multiple of 256; larger all-reduces run in chunks).
+ * Each collective synchronises the caller's stream, exchanges through the segment and sums
+ * the ranks' contributions on the host in rank order 0..P-1, so every rank gets identical
+ * bits; no kernel waits for another rank.  A rank that waits more than 120 s for the others
+ * returns TLS_ERR_NCCL.  Returns after every rank has mapped the segment; rank 0 unlinks it in
+ * tls_comm_destroy (which is collective for this backend). */
+TLS_API int tls_comm_init_shm(int nranks, int rank, const char* name, size_t slot_bytes, int device,
+                              tls_comm_t* out);
+TLS_API int tls_comm_nranks(tls_comm_t comm);   /* 1 for NULL */
+TLS_API int tls_comm_rank(tls_comm_t comm);     /* 0 for NULL */
 TLS_API int tls_comm_destroy(tls_comm_t comm);
 
 /* Workspace bytes for tls_factor_precond and tls_rqi_pcgtls on this A. */

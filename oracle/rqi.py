@@ -446,6 +446,7 @@ class RqiOptions:
     gram_chunk: int = 64
     u_p: str = "fp64"          # operator precision of the RQI's inner solves (R23): "fp64" | "fp32"
     precond_apply: int = 0     # R24: 1 substitution, 2 explicit inverse, 0 auto (= 1 in this one-process oracle)
+    minimal_check: int = 0     # R28: PCG steps of the minimality certificate after an OK solve (0 = off)
 
 
 @dataclasses.dataclass
@@ -464,6 +465,30 @@ class RqiResult:
     breakdown_j: int = -1
     passes: int = 0            # passes over A (unbatched) for perf accounting
     delta_min_trace: List[tuple] = dataclasses.field(default_factory=list)   # c2 step 9
+
+
+def certificate_rhs(n: int) -> np.ndarray:
+    """The fixed right-hand side of the minimality certificate (R28), a counter-based
+    pseudo-random vector both sides generate bit for bit: h_j = (j + 1) * 0x9E3779B97F4A7C15
+    mod 2^64, r_j = (h_j >> 11) 2^-53 - 1/2 (every step exact in fp64)."""
+    h = np.arange(1, n + 1, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+    return (h >> np.uint64(11)).astype(np.float64) * 2.0 ** -53 - 0.5
+
+
+def minimality_certificate(A, pc: Precond, sigma2: float, steps: int):
+    """Is A^T A - sigma^2 I positive definite (x_TLS is unique only if
+    sigma'_n > sigma_{n+1}, and PCGTLS needs A^T A - sigma_k^2 I SPD)?  Reading R28: `steps`
+    iterations of PCGTLS (A-in-loop, l.186-204) at sigma^2 on certificate_rhs with no early
+    exit.  CG's curvatures delta_j = p_j^T C p_j of C = P^{-T}(A^T A - sigma^2 I)P^{-1} are the
+    pivots of the Lanczos tridiagonal T_j, so all delta_j > 0 <=> T_j SPD <=> every Ritz value
+    of C is positive; a delta_j <= 0 exhibits a direction of non-positive curvature, so C -- and
+    by Sylvester's law of inertia A^T A - sigma^2 I -- is not positive definite: sigma >= sigma'_n
+    and (x, sigma) is not the TLS solution (NOT_MINIMAL).  The converse is one-sided: `steps`
+    positive pivots make negative curvature unlikely (Lanczos finds extreme eigenvalues first),
+    not impossible.  Returns (not_minimal, delta_min)."""
+    n = A.shape[1]
+    r = pcgtls(A, pc, sigma2, certificate_rhs(n), steps, 0.0, "A", "spec")
+    return bool(r.breakdown or r.delta_min <= 0.0), r.delta_min
 
 
 def newton_residual(A, b: np.ndarray, x: np.ndarray):
@@ -578,6 +603,11 @@ def rqi_pcgtls_mp(A, b: np.ndarray, pc: Precond, tol: float = 1e-14,
         prev, psi_prev = (x, sig2), psi
         x = x_new
         k += 1
+    if res.status == OK and o.minimal_check > 0:                # R28
+        nm, _ = minimality_certificate(A, pc, res.sigma ** 2, o.minimal_check)
+        passes += o.minimal_check
+        if nm:
+            res.status = NOT_MINIMAL
     res.passes = passes
     return res
 

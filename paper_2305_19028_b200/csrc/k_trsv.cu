@@ -508,9 +508,16 @@ __global__ void __launch_bounds__(kWG) k_wgemv_grid(PrecondDev pc, PcgVecs v, co
 //                                                                -> grid barrier
 //   C  CTA 0 writes s, p and the state; q = D^{-1} W p' spread over the grid.
 // Same decisions, updates and state as k_pcg_step.
-__global__ void __launch_bounds__(kWG) k_wpcg_step_coop(PrecondDev pc, PcgVecs v, const double* __restrict__ passout,
+//   0  (partials != nullptr, NEXT-3) the operator pass's per-CTA partials are reduced here in
+//      k_reduce_partials' fixed order (8 row groups, then the group sums in order: the same
+//      bits), column slices spread over the grid, into passout -> grid barrier.  Saves the
+//      separate reduction launch of every PCG iteration on one rank.
+// passout is not __restrict__: with phase 0 this kernel writes it (pout) before reading it, so
+// its loads must stay coherent (no read-only-path caching across the grid barrier).
+__global__ void __launch_bounds__(kWG) k_wpcg_step_coop(PrecondDev pc, PcgVecs v, const double* passout,
                                                        PcgState* __restrict__ S, int nrhs, int rule, int next_q,
-                                                       int variant, int pass_nrhs) {
+                                                       int variant, int pass_nrhs, const double* __restrict__ partials,
+                                                       int G, double* __restrict__ pout) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double wsh[];
@@ -524,6 +531,28 @@ __global__ void __launch_bounds__(kWG) k_wpcg_step_coop(PrecondDev pc, PcgVecs v
   for (int r = 0; r < 2; ++r) act[r] = r < nrhs && S->active[r] != 0;
   if (!act[0] && !act[1]) return;       // uniform over the grid
   const double sig2 = S->sigma2;
+  if (partials != nullptr) {
+    // ---- 0: passout = fixed-order sum of the G partial rows (k_reduce_partials' order)
+    const int W = pass_nrhs * n + 2;
+    const int tx = tid & 31, grp = tid >> 5;          // 32 columns x 8 row groups per block
+    double* gs = snb;                                   // [8][33] scratch (snb is free until B)
+    for (int cb = blockIdx.x; cb * 32 < W; cb += gridDim.x) {
+      const int w = cb * 32 + tx;
+      const int g0 = G * grp / 8, g1 = G * (grp + 1) / 8;
+      double acc = 0.0;
+      if (w < W)
+        for (int g = g0; g < g1; ++g) acc += partials[(size_t)g * W + w];
+      gs[grp * 33 + tx] = acc;
+      __syncthreads();
+      if (grp == 0 && w < W) {
+        double r = gs[tx];
+        for (int k = 1; k < 8; ++k) r += gs[k * 33 + tx];
+        pout[w] = r;
+      }
+      __syncthreads();
+    }
+    grid.sync();
+  }
   // ---- A
   for (int r = 0; r < 2; ++r) {
     if (!act[r]) continue;
@@ -1107,9 +1136,10 @@ int launch_pcg_init(const PrecondDev& pc, int nrhs, PcgVecs v, PcgState* S, cuda
 }
 
 int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgState* S, int nrhs, int rule,
-                    int next_q, int variant, int pass_nrhs, cudaStream_t st) {
+                    int next_q, int variant, int pass_nrhs, cudaStream_t st, const double* partials, int G) {
   if (pc.W != nullptr) {                 // R24: one cooperative kernel over every SM
-    const size_t smem = 4 * (size_t)pc.npad * 8;
+    const size_t dbl = 4 * (size_t)pc.npad > 2 * (size_t)pc.npad + 264 ? 4 * (size_t)pc.npad : 2 * (size_t)pc.npad + 264;
+    const size_t smem = dbl * 8;
     static size_t attr = 0;
     if (attr < smem) {
       TLS_CUDA_TRY(cudaFuncSetAttribute(k_wpcg_step_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1117,9 +1147,15 @@ int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgS
     }
     int g = (pc.n + kWG / 32 - 1) / (kWG / 32);
     if (g > num_sms()) g = num_sms();
-    void* args[] = {(void*)&pc, &v, (void*)&passout, &S, &nrhs, &rule, &next_q, &variant, &pass_nrhs};
+    double* pout = const_cast<double*>(passout);
+    void* args[] = {(void*)&pc, &v, (void*)&passout, &S, &nrhs, &rule, &next_q, &variant, &pass_nrhs,
+                    (void*)&partials, &G, &pout};
     TLS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_wpcg_step_coop, dim3(g), dim3(kWG), args, smem, st));
     return 0;
+  }
+  if (partials != nullptr) {
+    set_error("launch_pcg_step: the fused reduction needs the explicit-inverse step");
+    return TLS_ERR_ARG;
   }
   const size_t sm = trsv_smem(pc.npad);
   int rc = 0;

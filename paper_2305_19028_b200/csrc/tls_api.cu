@@ -6,6 +6,13 @@
 // inside PCGTLS all control (breakdown, early exit) is device-resident.
 #include <dlfcn.h>
 
+#include <fcntl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -40,7 +47,7 @@ using namespace tls;
 namespace {
 typedef struct ncclComm* ncclComm_t;
 typedef struct { char internal[128]; } ncclUniqueId;
-enum { ncclSuccess = 0 };
+enum { ncclSuccess = 0, ncclInProgress = 7 };
 enum { ncclSum = 0, ncclMax = 2 };
 enum { ncclFloat64 = 8, ncclInt32 = 2, ncclInt64 = 4 };
 struct NcclApi {
@@ -48,6 +55,7 @@ struct NcclApi {
   int (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
   int (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t);
   int (*CommDestroy)(ncclComm_t);
+  int (*CommGetAsyncError)(ncclComm_t, int*);
   const char* (*GetErrorString)(int);
   bool ok = false;
 };
@@ -63,17 +71,39 @@ NcclApi* nccl_api() {
       api.CommInitRank = (int (*)(ncclComm_t*, int, ncclUniqueId, int))dlsym(h, "ncclCommInitRank");
       api.AllReduce = (int (*)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclAllReduce");
       api.CommDestroy = (int (*)(ncclComm_t))dlsym(h, "ncclCommDestroy");
+      api.CommGetAsyncError = (int (*)(ncclComm_t, int*))dlsym(h, "ncclCommGetAsyncError");
       api.GetErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
       api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy;
     }
   }
   return api.ok ? &api : nullptr;
 }
+
+// Host-shm backend: ranks that are processes sharing ONE GPU (tls_comm_init_shm).  Every
+// collective is staged through a POSIX shared-memory segment: a rank copies its buffer to the
+// host (its stream synchronised first), writes it into its own slot, waits at a process-shared
+// barrier, sums ALL ranks' slots in rank order 0..P-1 (every rank computes identical bits),
+// waits at a second barrier (the slots may then be reused) and copies the result back.  No
+// kernel ever waits for another rank (B200_PROFILING.md: kernels spinning on other ranks' flags
+// must not share a GPU), so this backend runs every multi-rank code path of the library --
+// sharded passes, all-reduced Gram, replicated Cholesky, TSQR stack exchange, the
+// explicit-inverse default -- with real per-rank processes on one GPU.  It is a correctness
+// backend; the production path is NCCL over NVLink.
+struct ShmHeader {
+  std::atomic<int64_t> arrive;     // arrivals in the current barrier phase
+  std::atomic<int64_t> phase;      // completed barrier phases
+  int64_t nranks;
+  int64_t slot_bytes;
+};
 }  // namespace
 
 struct tls_comm_s {
   ncclComm_t comm;
   int nranks, rank, device;
+  ShmHeader* shm = nullptr;        // host-shm backend (comm == nullptr)
+  size_t shm_bytes = 0;
+  char shm_name[96] = {0};
+  double* stage = nullptr;         // pinned staging buffer of slot_bytes
 };
 
 struct tls_precond_s {
@@ -90,28 +120,105 @@ struct tls_precond_s {
   int64_t a32_m = -1, a32_ld = -1;
   // explicit inverse W = R~^{-1} and W^T (R24), made by the first solve that applies it
   double* winv = nullptr;
-  // fingerprint of the factored A: global row count; -1 for imported handles
+  // fingerprint of the factored A: global row count (-1 for imported handles)
+  // and the sampled content checksum of this rank's block (k_fingerprint)
   int64_t m_global = -1;
+  double content = 0.0;
+  double a32_content = 0.0;   // the checksum the fp32 copy was made from
 };
 
-static int allreduce(tls_comm_t comm, double* buf, size_t count, int op, cudaStream_t st) {
-  if (comm == nullptr || comm->comm == nullptr || count == 0) return 0;
-  NcclApi* api = nccl_api();
-  const int r = api->AllReduce(buf, buf, count, ncclFloat64, op, comm->comm, st);
-  if (r != ncclSuccess) {
-    set_error("ncclAllReduce: %s", api->GetErrorString ? api->GetErrorString(r) : "error");
-    return TLS_ERR_NCCL;
+namespace {
+bool comm_active(tls_comm_t c) { return c != nullptr && (c->comm != nullptr || c->shm != nullptr); }
+
+char* shm_slot(tls_comm_t c, int r) {
+  return reinterpret_cast<char*>(c->shm) + 256 + (size_t)r * (size_t)c->shm->slot_bytes;
+}
+
+int shm_barrier(tls_comm_t c) {
+  ShmHeader* h = c->shm;
+  const int64_t ph = h->phase.load(std::memory_order_acquire);
+  if (h->arrive.fetch_add(1, std::memory_order_acq_rel) + 1 == h->nranks) {
+    h->arrive.store(0, std::memory_order_relaxed);
+    h->phase.fetch_add(1, std::memory_order_acq_rel);
+    return 0;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (long spin = 0; h->phase.load(std::memory_order_acquire) == ph; ++spin) {
+    if (spin > 1000) sched_yield();
+    if ((spin & 1023) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120)) {
+      set_error("shm barrier: rank %d waited 120 s for the other ranks", c->rank);
+      return TLS_ERR_NCCL;
+    }
   }
   return 0;
 }
 
+// `count` 8-byte elements (double, or int64 when is_int); op = ncclSum / ncclMax
+int shm_allreduce(tls_comm_t c, void* buf, size_t count, int op, bool is_int, cudaStream_t st) {
+  const size_t per = (size_t)c->shm->slot_bytes / 8;
+  char* dev = static_cast<char*>(buf);
+  for (size_t off = 0; off < count; off += per) {
+    const size_t k = count - off < per ? count - off : per;
+    TLS_CUDA_TRY(cudaMemcpyAsync(c->stage, dev + off * 8, k * 8, cudaMemcpyDeviceToHost, st));
+    TLS_CUDA_TRY(cudaStreamSynchronize(st));
+    std::memcpy(shm_slot(c, c->rank), c->stage, k * 8);
+    TLS_TRY(shm_barrier(c));
+    for (size_t i = 0; i < k; ++i) {
+      if (is_int) {
+        int64_t acc = 0;
+        for (int r = 0; r < c->nranks; ++r) acc += reinterpret_cast<const int64_t*>(shm_slot(c, r))[i];
+        reinterpret_cast<int64_t*>(c->stage)[i] = acc;
+      } else {
+        double acc = reinterpret_cast<const double*>(shm_slot(c, 0))[i];
+        for (int r = 1; r < c->nranks; ++r) {                     // rank order 0..P-1
+          const double v = reinterpret_cast<const double*>(shm_slot(c, r))[i];
+          acc = (op == ncclMax) ? (v > acc ? v : acc) : acc + v;
+        }
+        c->stage[i] = acc;
+      }
+    }
+    TLS_TRY(shm_barrier(c));
+    TLS_CUDA_TRY(cudaMemcpyAsync(dev + off * 8, c->stage, k * 8, cudaMemcpyHostToDevice, st));
+    TLS_CUDA_TRY(cudaStreamSynchronize(st));   // the staging buffer is reused by the next chunk
+  }
+  return 0;
+}
+
+int nccl_check(tls_comm_t comm, int r, const char* what) {
+  if (r == ncclSuccess) return 0;
+  NcclApi* api = nccl_api();
+  int aerr = 0;
+  if (api->CommGetAsyncError) api->CommGetAsyncError(comm->comm, &aerr);
+  set_error("%s: %s (async state: %s)", what, api->GetErrorString ? api->GetErrorString(r) : "error",
+            api->GetErrorString ? api->GetErrorString(aerr) : "?");
+  return TLS_ERR_NCCL;
+}
+}  // namespace
+
+static int allreduce(tls_comm_t comm, double* buf, size_t count, int op, cudaStream_t st) {
+  if (!comm_active(comm) || count == 0) return 0;
+  if (comm->shm) return shm_allreduce(comm, buf, count, op, false, st);
+  return nccl_check(comm, nccl_api()->AllReduce(buf, buf, count, ncclFloat64, op, comm->comm, st), "ncclAllReduce");
+}
+
 // int64 sum (exact, order-free): the fixed-point limbs of the CSR fp16 Gram
 static int allreduce_i64(tls_comm_t comm, void* buf, size_t count, cudaStream_t st) {
-  if (comm == nullptr || comm->comm == nullptr || count == 0) return 0;
+  if (!comm_active(comm) || count == 0) return 0;
+  if (comm->shm) return shm_allreduce(comm, buf, count, ncclSum, true, st);
+  return nccl_check(comm, nccl_api()->AllReduce(buf, buf, count, ncclInt64, ncclSum, comm->comm, st),
+                    "ncclAllReduce(int64)");
+}
+
+// An NCCL error raised asynchronously (a peer died, a link fault) surfaces at the end of each
+// top-level call as TLS_ERR_NCCL instead of as a later hang.
+static int comm_async_check(tls_comm_t comm) {
+  if (comm == nullptr || comm->comm == nullptr) return 0;
   NcclApi* api = nccl_api();
-  const int r = api->AllReduce(buf, buf, count, ncclInt64, ncclSum, comm->comm, st);
-  if (r != ncclSuccess) {
-    set_error("ncclAllReduce(int64): %s", api->GetErrorString ? api->GetErrorString(r) : "error");
+  if (!api || !api->CommGetAsyncError) return 0;
+  int aerr = 0;
+  const int r = api->CommGetAsyncError(comm->comm, &aerr);
+  if (r != ncclSuccess || (aerr != ncclSuccess && aerr != ncclInProgress)) {
+    set_error("NCCL asynchronous error: %s", api->GetErrorString ? api->GetErrorString(aerr ? aerr : r) : "error");
     return TLS_ERR_NCCL;
   }
   return 0;
@@ -303,6 +410,8 @@ size_t carve(const tls_matrix_t* A, void* ws, size_t bytes, Work& w, bool factor
     w.gram_ws_doubles = csr ? csr_gram_ws_bytes(n) / 8 : gram_ws_doubles(dense_view(A), 1);
     const size_t chol = (chol_ws_bytes(n) + 7) / 8;                  // the Cholesky reuses it
     if (w.gram_ws_doubles < chol) w.gram_ws_doubles = chol;
+    const size_t packed = (size_t)n * (n + 1) / 2;                    // the packed Gram all-reduce too
+    if (w.gram_ws_doubles < packed) w.gram_ws_doubles = packed;
     w.gram_ws = c.take<double>(w.gram_ws_doubles);
   }
   if (ok) *ok = c.ok;
@@ -343,6 +452,26 @@ int check_matrix(const tls_matrix_t* A) {
   return 0;
 }
 
+// The symmetric Gram's upper triangle (row i: columns i..n-1) packed row by row, n(n+1)/2
+// doubles: what the multi-rank Gram all-reduce moves (half of n^2); unpack mirrors it.
+__device__ __forceinline__ int64_t packed_row_start(int64_t i, int64_t n) { return i * n - i * (i - 1) / 2; }
+__global__ void k_pack_upper(const double* __restrict__ G, double* __restrict__ P, int n) {
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const int64_t o = packed_row_start(i, n) - i;
+    for (int j = i + threadIdx.x; j < n; j += blockDim.x) P[o + j] = G[(int64_t)i * n + j];
+  }
+}
+__global__ void k_unpack_upper(const double* __restrict__ P, double* __restrict__ G, int n) {
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const int64_t o = packed_row_start(i, n) - i;
+    for (int j = i + threadIdx.x; j < n; j += blockDim.x) {
+      const double v = P[o + j];
+      G[(int64_t)i * n + j] = v;
+      G[(int64_t)j * n + i] = v;
+    }
+  }
+}
+
 __global__ void k_recip(const double* __restrict__ d, double* __restrict__ dinv, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dinv[i] = 1.0 / d[i];
 }
@@ -350,6 +479,15 @@ __global__ void k_recip(const double* __restrict__ d, double* __restrict__ dinv,
 __global__ void k_set_state(PcgState* S, int set_sigma, double sigma2, double tol2) {
   if (set_sigma) S->sigma2 = sigma2;
   S->tol2 = tol2;
+}
+
+// The minimality certificate's right-hand side (R28; oracle.rqi.certificate_rhs, same bits):
+// r_j = ((j + 1) * 0x9E3779B97F4A7C15 mod 2^64 >> 11) 2^-53 - 1/2.
+__global__ void k_cert_rhs(double* __restrict__ r, int n) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const unsigned long long h = (unsigned long long)(j + 1) * 0x9E3779B97F4A7C15ull;
+    r[j] = (double)(h >> 11) * 0x1p-53 - 0.5;
+  }
 }
 
 __global__ void k_copy(const double* __restrict__ a, double* __restrict__ b, int64_t n) {
@@ -404,6 +542,19 @@ int run_pass(Ctx& cx, const tls_matrix_t* A, int mode, int nrhs, const double* q
   return 0;
 }
 
+// Sampled content checksum of the local block into *dev (k_fingerprint).
+int run_fingerprint(Ctx& cx, const tls_matrix_t* A, double* dev) {
+  if (is_csr(A)) {
+    const CsrView cv = csr_view(A);
+    TLS_TRY(launch_fingerprint(nullptr, &cv, dev, cx.st));
+  } else {
+    const DenseView dv = dense_view(A);
+    TLS_TRY(launch_fingerprint(&dv, nullptr, dev, cx.st));
+  }
+  cx.launches += 1;
+  return 0;
+}
+
 // One spare fp32-copy buffer kept by tls_precond_destroy for the next handle (a fresh
 // cudaMalloc/cudaFree of the 4 GiB copy per solve would stall the stream).
 struct A32Spare { int device = -1; size_t bytes = 0; float* ptr = nullptr; };
@@ -414,10 +565,13 @@ static A32Spare& a32_spare() {
 
 // The fl32 copy of the dense local block held by the handle (R23): (re)made when missing
 // or made for another block.  The only allocation outside alloc_precond; freed with R.
-int ensure_a32(Ctx& cx, const tls_matrix_t* A, tls_precond_t R) {
+int ensure_a32(Ctx& cx, const tls_matrix_t* A, tls_precond_t R, double content) {
   if (is_csr(A)) { set_error("u_p = fp32 needs a dense A"); return TLS_ERR_UNSUPPORTED; }
   if (A->n > 2048) { set_error("u_p = fp32 needs n <= 2048"); return TLS_ERR_UNSUPPORTED; }
-  if (R->a32 && R->a32_src == A->vals && R->a32_m == A->m_local && R->a32_ld == A->ld) return 0;
+  // reused only for the same block with the same sampled content (an A rewritten in place is
+  // re-rounded)
+  if (R->a32 && R->a32_src == A->vals && R->a32_m == A->m_local && R->a32_ld == A->ld && R->a32_content == content)
+    return 0;
   const size_t bytes = (size_t)A->m_local * p32_ld((int)A->n) * 4 + 256;
   if (R->a32_bytes < bytes) {
     if (R->a32) { cudaStreamSynchronize(cx.st); cudaFree(R->a32); R->a32 = nullptr; R->a32_bytes = 0; }
@@ -437,6 +591,7 @@ int ensure_a32(Ctx& cx, const tls_matrix_t* A, tls_precond_t R) {
   R->a32_src = A->vals;
   R->a32_m = A->m_local;
   R->a32_ld = A->ld;
+  R->a32_content = content;
   cx.launches += 1;
   cx.passes += 1;
   return 0;
@@ -491,7 +646,7 @@ int run_gram(Ctx& cx, const tls_matrix_t* A, int u_f, const double* dinv, int K_
   const int n = (int)A->n;
   ProfScope ps(TLS_PROF_GRAM, cx.st);
   if (is_csr(A)) {
-    const bool ranks = cx.comm != nullptr && cx.comm->comm != nullptr;
+    const bool ranks = comm_active(cx.comm);
     if (u_f == TLS_FP16 && ranks) {
       // exact fixed-point limbs are summed over ranks as int64 (exact, order-free), then rounded once
       TLS_TRY(launch_csr_gram(csr_view(A), u_f, dinv, w.G, w.gram_ws, w.gram_ws_doubles * 8, &w.flags[1], cx.st,
@@ -509,7 +664,16 @@ int run_gram(Ctx& cx, const tls_matrix_t* A, int u_f, const double* dinv, int K_
   } else {
     TLS_CUDA_TRY(cudaMemsetAsync(w.G, 0, (size_t)n * n * 8, cx.st));
   }
-  TLS_TRY(allreduce(cx.comm, w.G, (size_t)n * n, ncclSum, cx.st));
+  if (comm_active(cx.comm)) {
+    // the symmetric Gram travels packed: n(n+1)/2 doubles instead of n^2
+    const int g = n < 4096 ? n : 4096;
+    k_pack_upper<<<g, 256, 0, cx.st>>>(w.G, w.gram_ws, n);
+    TLS_LAUNCH_CHECK();
+    TLS_TRY(allreduce(cx.comm, w.gram_ws, (size_t)n * (n + 1) / 2, ncclSum, cx.st));
+    k_unpack_upper<<<g, 256, 0, cx.st>>>(w.gram_ws, w.G, n);
+    TLS_LAUNCH_CHECK();
+    cx.launches += 2;
+  }
   return 0;
 }
 
@@ -681,12 +845,54 @@ int tls_comm_init(int nranks, int rank, const void* id_host, int device, tls_com
   return 0;
 }
 
+int tls_comm_init_shm(int nranks, int rank, const char* name, size_t slot_bytes, int device, tls_comm_t* out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks || !name || name[0] != '/' || strlen(name) >= 96 ||
+      slot_bytes < 4096 || (slot_bytes & 255)) {
+    set_error("bad shm comm args (name must start with '/', slot_bytes >= 4096 and a multiple of 256)");
+    return TLS_ERR_ARG;
+  }
+  TLS_CUDA_TRY(cudaSetDevice(device));
+  const size_t bytes = 256 + (size_t)nranks * slot_bytes;
+  const int fd = shm_open(name, O_CREAT | O_RDWR, 0600);
+  if (fd < 0) { set_error("shm_open(%s) failed", name); return TLS_ERR_NCCL; }
+  if (ftruncate(fd, (off_t)bytes) != 0) { close(fd); set_error("ftruncate(%s) failed", name); return TLS_ERR_NCCL; }
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) { set_error("mmap(%s) failed", name); return TLS_ERR_NCCL; }
+  tls_comm_s* c = new tls_comm_s{nullptr, nranks, rank, device};
+  c->shm = static_cast<ShmHeader*>(p);
+  c->shm_bytes = bytes;
+  std::snprintf(c->shm_name, sizeof(c->shm_name), "%s", name);
+  // a fresh segment is zero-filled: arrive = phase = 0; every rank writes the same sizes
+  c->shm->nranks = nranks;
+  c->shm->slot_bytes = (int64_t)slot_bytes;
+  if (cudaMallocHost(&c->stage, slot_bytes) != cudaSuccess) {
+    munmap(p, bytes);
+    delete c;
+    set_error("cudaMallocHost(%zu) failed", slot_bytes);
+    return TLS_ERR_CUDA;
+  }
+  const int rc = shm_barrier(c);      // every rank has mapped the segment
+  if (rc) { tls_comm_destroy(c); return rc; }
+  *out = c;
+  return 0;
+}
+
+int tls_comm_nranks(tls_comm_t c) { return c ? c->nranks : 1; }
+int tls_comm_rank(tls_comm_t c) { return c ? c->rank : 0; }
+
 int tls_comm_destroy(tls_comm_t c) {
   if (!c) return 0;
   if (c->comm) {
     NcclApi* api = nccl_api();
     if (api) api->CommDestroy(c->comm);
   }
+  if (c->shm) {
+    shm_barrier(c);                   // nobody still reads a slot
+    munmap(c->shm, c->shm_bytes);
+    if (c->rank == 0) shm_unlink(c->shm_name);
+  }
+  if (c->stage) cudaFreeHost(c->stage);
   delete c;
   return 0;
 }
@@ -740,14 +946,17 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
   int rc = launch_pack_R(w.G, n, 0, h->dev, &w.flags[3], cx.st, &cx.launches);
   cx.launches += 1;  // k_fill_scaling
   if (rc) { tls_precond_destroy(h); return rc; }
+  rc = run_fingerprint(cx, A, normA2 + 1);
+  if (rc) { tls_precond_destroy(h); return rc; }
   tr.mark("pack");
   int hflags[8];
-  double hnorm = 0.0;
+  double hnorm[2] = {0.0, 0.0};
   TLS_CUDA_TRY(cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, cx.st));
-  TLS_CUDA_TRY(cudaMemcpyAsync(&hnorm, normA2, sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(hnorm, normA2, 2 * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
   TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
   tr.mark("sync");
   if (info) { info->passes = cx.passes; info->launches = cx.launches; }
+  { const int arc = comm_async_check(comm); if (arc) { tls_precond_destroy(h); return arc; } }
   int st = 0;
   if (hflags[0]) { set_error("A has a zero or non-finite column (rank deficient)"); st = TLS_ERR_ARG; }
   else if (hflags[1]) st = TLS_RANGE;
@@ -758,8 +967,9 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
     if (info && st > 0) info->status = st;
     return st;
   }
-  h->normA2_host = hnorm;
+  h->normA2_host = hnorm[0];
   h->m_global = A->m_global;
+  h->content = hnorm[1];
   *R_out = h;
   return 0;
 }
@@ -909,14 +1119,17 @@ int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, v
   int rc = launch_pack_R(q.G, n, 0, h->dev, &w.flags[3], cx.st, &cx.launches);
   cx.launches += 1;
   if (rc) { tls_precond_destroy(h); return rc; }
+  rc = run_fingerprint(cx, A, normA2 + 1);
+  if (rc) { tls_precond_destroy(h); return rc; }
   int hflags[8], hq[4];
-  double hnorm = 0.0;
+  double hnorm[2] = {0.0, 0.0};
   TLS_CUDA_TRY(cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, cx.st));
   TLS_CUDA_TRY(cudaMemcpyAsync(hq, q.qflags, sizeof(hq), cudaMemcpyDeviceToHost, cx.st));
-  TLS_CUDA_TRY(cudaMemcpyAsync(&hnorm, normA2, sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(hnorm, normA2, 2 * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
   TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
   tr.mark("sync");
   if (info) { info->passes = cx.passes; info->launches = cx.launches; }
+  { const int arc = comm_async_check(comm); if (arc) { tls_precond_destroy(h); return arc; } }
   int st = 0;
   if (hflags[0]) { set_error("A has a zero or non-finite column (rank deficient)"); st = TLS_ERR_ARG; }
   else if (hq[0]) { st = TLS_CHOL_BREAKDOWN; if (info) info->chol_pivot = hq[1]; }
@@ -926,8 +1139,9 @@ int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, v
     if (info && st > 0) info->status = st;
     return st;
   }
-  h->normA2_host = hnorm;
+  h->normA2_host = hnorm[0];
   h->m_global = A->m_global;
+  h->content = hnorm[1];
   *R_out = h;
   return 0;
 }
@@ -1060,11 +1274,24 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   if (!carve_ok(A, ws, ws_bytes, w, false)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
   Ctx cx{static_cast<cudaStream_t>(stream), comm};
   const int n = (int)A->n;
+  // the handle's fingerprint: this rank's block must have the content it was factored from
+  double content = 0.0;
+  TLS_TRY(run_fingerprint(cx, A, w.d_tmp));
+  TLS_CUDA_TRY(cudaMemcpyAsync(&content, w.d_tmp, sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+  TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+  if (R->m_global >= 0 && !(content == R->content)) {
+    set_error("A's content differs from the matrix the preconditioner was factored from (sampled checksum)");
+    return TLS_ERR_ARG;
+  }
   if (use_w) TLS_TRY(ensure_winv(cx, R));
   PrecondDev pc = R->dev;
   if (use_w) { pc.W = R->winv; pc.WT = R->winv + (size_t)pc.npad * pc.npad; }
+  // the fused reduction (NEXT-3) needs the explicit-inverse step and a single rank;
+  // TLS_FUSE_REDUCE=0 keeps the separate k_reduce_partials launch (A/B measurements)
+  const char* fre = getenv("TLS_FUSE_REDUCE");
+  const bool fuse_reduce = use_w && !comm_active(comm) && !(fre && fre[0] == '0');
   if (is_csr(A)) TLS_TRY(launch_csc_build(csr_view(A), w.csc, w.csc_scratch, cx.st, &cx.launches));
-  if (up32) TLS_TRY(ensure_a32(cx, A, R));
+  if (up32) TLS_TRY(ensure_a32(cx, A, R, content));
   const double tol_in = o.tol_inner > 0 ? o.tol_inner : tol;
   PcgState hS;
 
@@ -1087,17 +1314,26 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   // paper's A-free Alg. 3 (no pass).  The sigma = 0 bootstrap always uses variant 0.
   // fp32: the RQI's inner solves run their operator pass on the fp32 copy (u_p, R23);
   // the sigma = 0 bootstrap stays fp64 (R5: x_LS to 1e-8).
-  auto pcg_loop = [&](int nrhs, int budget, int variant, bool fp32) -> int {
+  auto pcg_loop = [&](int nrhs, int budget, int variant, bool fp32, int rule) -> int {
     for (int j = 0; j < budget; ++j) {
       // the 2-RHS dense kernel is faster than the 1-RHS one at the same bytes (measured, see
       // DESIGN §6): a 1-RHS solve passes its q with the second slot held at zero
       const int pass_rhs = (nrhs == 1 && !is_csr(A)) ? 2 : nrhs;
-      if (variant == 0 && fp32) TLS_TRY(run_pass32(cx, A, R, w.vec.q, w, w.S->active));
+      // NEXT-3: on one rank the explicit-inverse step reduces the dense pass's partials itself
+      // (no separate reduction launch); with ranks the reduced sums go through the all-reduce
+      const bool fold = fuse_reduce && variant == 0 && !fp32 && !is_csr(A) && A->m_local > 0;
+      int G = 0;
+      if (fold) {
+        ProfScope ps(TLS_PROF_PASS_OP2, cx.st);
+        TLS_TRY(launch_pass(dense_view(A), PASS_OPERATOR, pass_rhs, w.vec.q, nullptr, w.partials, w.S->active, cx.st, &G));
+        cx.launches += 1;
+        cx.passes += 1;
+      } else if (variant == 0 && fp32) TLS_TRY(run_pass32(cx, A, R, w.vec.q, w, w.S->active));
       else if (variant == 0) TLS_TRY(run_pass(cx, A, PASS_OPERATOR, pass_rhs, w.vec.q, nullptr, w, w.S->active));
       {
         ProfScope ps(TLS_PROF_PCG_STEP, cx.st);
-        TLS_TRY(launch_pcg_step(pc, w.vec, w.passout, w.S, nrhs, o.breakdown_rule, j + 1 < budget ? 1 : 0, variant,
-                                pass_rhs, cx.st));
+        TLS_TRY(launch_pcg_step(pc, w.vec, w.passout, w.S, nrhs, rule, j + 1 < budget ? 1 : 0, variant,
+                                pass_rhs, cx.st, fold ? w.partials : nullptr, G));
       }
       cx.launches += 1;
       if (budget > 16 && (j == 3 || (j % 8) == 7)) {   // first poll early: small bootstraps skip no-op launches
@@ -1130,7 +1366,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
       TLS_TRY(launch_pcg_init(pc, 1, w.vec, w.S, cx.st));
     }
     cx.launches += 1;
-    TLS_TRY(pcg_loop(1, o.boot_max, 0, false));   // its count is read with the first RQI state
+    TLS_TRY(pcg_loop(1, o.boot_max, 0, false, o.breakdown_rule));   // its count is read with the first RQI state
     k_copy<<<(n + 255) / 256, 256, 0, cx.st>>>(w.vec.omega, w.x0, n);
   } else {
     k_copy<<<(n + 255) / 256, 256, 0, cx.st>>>(w.vec.rhs, w.x0, n);
@@ -1209,7 +1445,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
     }
     cx.launches += 1;
     tr.mark("pcg_init");
-    TLS_TRY(pcg_loop(2, budget, o.op_variant, up32));
+    TLS_TRY(pcg_loop(2, budget, o.op_variant, up32, o.breakdown_rule));
     tr.mark("pcg_loop");
     // a9: z, beta_k, x_{k+1} (l.248-255); skipped on the device after a PCG breakdown
     TLS_TRY(launch_rqi_update(pc, w.vec, w.S, w.x, w.x_prev, cx.st));
@@ -1219,6 +1455,17 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   }
   k_copy<<<(n + 255) / 256, 256, 0, cx.st>>>(use_prev ? w.x_prev : w.x, x_out, n);
   cx.launches += 1;
+  if (status == TLS_OK && o.minimal_check > 0) {
+    // R28: PCGTLS at the returned sigma^2 on the fixed certificate RHS, SPEC breakdown rule,
+    // no early exit; any delta_j <= 0 means A^T A - sigma^2 I is not positive definite
+    k_cert_rhs<<<(n + 255) / 256, 256, 0, cx.st>>>(w.vec.rhs, n);
+    TLS_TRY(set_state_scalars(true, sig2_ret, 0.0));
+    TLS_TRY(launch_pcg_init(pc, 1, w.vec, w.S, cx.st));
+    cx.launches += 2;
+    TLS_TRY(pcg_loop(1, o.minimal_check, 0, false, 0));
+    TLS_TRY(read_state());
+    if (hS.brk[0] || !(hS.delta_min[0] > 0.0)) status = TLS_NOT_MINIMAL;
+  }
   double cert[3] = {NAN, 0.0, 0.0};
   if (o.certify) {                       // compensated certificate (c2 step 8): one more pass
     const DenseView dv = is_csr(A) ? DenseView{} : dense_view(A);
@@ -1232,6 +1479,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   }
   TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
   TLS_LAUNCH_CHECK();
+  TLS_TRY(comm_async_check(comm));
   if (info && o.certify) info->sigma_certified = std::sqrt((cert[0] + cert[1]) / (1.0 + cert[2]));
   if (sigma_out) *sigma_out = std::sqrt(sig2_ret);
   if (info) {
@@ -1354,7 +1602,11 @@ int tls_pass_fp32(const tls_matrix_t* A, tls_precond_t R, const double* q, doubl
   if (!carve_ok(A, ws, ws_bytes, w, false)) { set_error("workspace too small"); return TLS_ERR_WORKSPACE; }
   Ctx cx{static_cast<cudaStream_t>(stream), nullptr};
   const int n = (int)A->n;
-  TLS_TRY(ensure_a32(cx, A, R));
+  double content = 0.0;
+  TLS_TRY(run_fingerprint(cx, A, w.d_tmp));
+  TLS_CUDA_TRY(cudaMemcpyAsync(&content, w.d_tmp, sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+  TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+  TLS_TRY(ensure_a32(cx, A, R, content));
   TLS_TRY(run_pass32(cx, A, R, q, w, nullptr));
   TLS_CUDA_TRY(cudaMemcpyAsync(v, w.passout, (size_t)2 * n * 8, cudaMemcpyDeviceToDevice, cx.st));
   TLS_CUDA_TRY(cudaMemcpyAsync(s, w.passout + (size_t)2 * n, 16, cudaMemcpyDeviceToDevice, cx.st));

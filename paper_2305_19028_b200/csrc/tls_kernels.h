@@ -52,6 +52,9 @@ struct CsrView {
   int n;
   int64_t nnz;
 };
+// sampled content checksum of a local block (k_pass.cu): 256 evenly spread rows
+int launch_fingerprint(const DenseView* dv, const CsrView* cv, double* out, cudaStream_t st);
+
 struct CscView {          // transpose of a CsrView, rows ascending within every column
   int64_t* colptr;        // n + 1
   int32_t* rowidx;        // nnz
@@ -132,8 +135,11 @@ int launch_pcg_init(const PrecondDev& pc, int nrhs, PcgVecs v, PcgState* S, cuda
 // paper's A-free Alg. 3 (delta = p^T p - sigma^2 q^T q, w = p - sigma^2 P^{-T} q;
 // passout unused).
 // pass_nrhs: the RHS count of the operator pass that filled passout (layout [v_0..v_{pass_nrhs-1}, tau..]).
+// partials != nullptr (explicit-inverse step only, NEXT-3): passout is computed in the step's
+// first phase from the G per-CTA partial rows of the operator pass (k_reduce_partials' order).
 int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgState* S, int nrhs,
-                    int breakdown_rule, int compute_next_q, int variant, int pass_nrhs, cudaStream_t st);
+                    int breakdown_rule, int compute_next_q, int variant, int pass_nrhs, cudaStream_t st,
+                    const double* partials = nullptr, int G = 0);
 // step record: sigma2, f (stored as rhs0 = -f), g, psi; copies x into rhs1.
 int launch_rqi_eval(const PrecondDev& pc, const double* passout, const double* x, PcgVecs v,
                     PcgState* S, cudaStream_t st);

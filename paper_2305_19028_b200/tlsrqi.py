@@ -38,7 +38,8 @@ class tls_rqi_opts_t(C.Structure):
                 ("polish", C.c_int32), ("tol_inner", C.c_double), ("boot", C.c_int32),
                 ("boot_max", C.c_int32), ("boot_tol", C.c_double), ("op_variant", C.c_int32),
                 ("breakdown_rule", C.c_int32), ("gram_chunk", C.c_int32), ("u_p", C.c_int32),
-                ("precond_apply", C.c_int32), ("certify", C.c_int32), ("reserved", C.c_int32 * 2)]
+                ("precond_apply", C.c_int32), ("certify", C.c_int32), ("minimal_check", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class tls_info_t(C.Structure):
@@ -72,6 +73,9 @@ def lib() -> C.CDLL:
         "tls_comm_get_unique_id": (C.c_int, [VP]),
         "tls_comm_init": (C.c_int, [C.c_int, C.c_int, VP, C.c_int, P(VP)]),
         "tls_comm_destroy": (C.c_int, [VP]),
+        "tls_comm_init_shm": (C.c_int, [C.c_int, C.c_int, C.c_char_p, SZ, C.c_int, P(VP)]),
+        "tls_comm_nranks": (C.c_int, [VP]),
+        "tls_comm_rank": (C.c_int, [VP]),
         "tls_workspace_size": (SZ, [M, I32]),
         "tls_factor_precond": (C.c_int, [M, I32, P(tls_rqi_opts_t), VP, VP, VP, SZ, P(VP), P(tls_info_t)]),
         "tls_qr_workspace_size": (SZ, [M, I32, I32]),
@@ -102,7 +106,8 @@ def lib() -> C.CDLL:
 
 
 EXPORTED = ["tls_abi_version", "tls_rqi_opts_default", "tls_status_string", "tls_last_error",
-            "tls_comm_get_unique_id", "tls_comm_init", "tls_comm_destroy", "tls_workspace_size",
+            "tls_comm_get_unique_id", "tls_comm_init", "tls_comm_init_shm", "tls_comm_nranks", "tls_comm_rank",
+            "tls_comm_destroy", "tls_workspace_size",
             "tls_factor_precond", "tls_qr_workspace_size", "tls_factor_precond_qr", "tls_precond_import", "tls_precond_export", "tls_precond_destroy",
             "tls_rqi_pcgtls", "tls_solve_host_bytes", "tls_solve_host", "tls_colstats", "tls_gram",
             "tls_pass", "tls_pass_fp32", "tls_precond_apply", "tls_round", "tls_profile_enable", "tls_profile_read"]
@@ -267,11 +272,14 @@ def tls_factor_precond(M: tls_matrix_t, u_f, opts: Optional[tls_rqi_opts_t] = No
 
 
 def tls_factor_precond_qr(M: tls_matrix_t, u_f, comm=None, stream=None, ws: Optional[torch.Tensor] = None,
-                          nranks: int = 1):
+                          nranks: Optional[int] = None):
     """Householder-QR preconditioner in u_f (NEXT-2, R25; TSQR over ranks / TLS_QR_LEAVES, R26).
-    nranks: the size of `comm` (it sizes the TSQR stack in the workspace when ws is None).
+    nranks: sizes the TSQR stack in the workspace when ws is None; default: the size of
+    `comm` (tls_comm_nranks), 1 without one.
     Returns (status, Precond or None, info dict)."""
     uf = PREC[u_f] if isinstance(u_f, str) else int(u_f)
+    if nranks is None:
+        nranks = int(lib().tls_comm_nranks(C.c_void_p(comm) if comm else None))
     if ws is None:
         nbytes = int(lib().tls_qr_workspace_size(C.byref(M), uf, nranks))
         if nbytes == 0:
@@ -427,6 +435,17 @@ def tls_comm_init(nranks: int, rank: int, uid: bytes, device: int) -> int:
     buf = (C.c_char * 128).from_buffer_copy(uid)
     _check(lib().tls_comm_init(nranks, rank, buf, device, C.byref(h)), "tls_comm_init")
     return h.value
+
+
+def tls_comm_init_shm(nranks: int, rank: int, name: str, device: int, slot_bytes: int = 1 << 22) -> int:
+    """Host-staged communicator for ranks sharing one GPU (tlsrqi.h tls_comm_init_shm)."""
+    h = C.c_void_p()
+    _check(lib().tls_comm_init_shm(nranks, rank, name.encode(), slot_bytes, device, C.byref(h)), "tls_comm_init_shm")
+    return h.value
+
+
+def tls_comm_nranks(comm) -> int:
+    return int(lib().tls_comm_nranks(C.c_void_p(comm) if comm else None))
 
 
 def tls_comm_destroy(comm: int) -> None:

@@ -33,7 +33,7 @@ def test_exports_every_header_symbol(L):
 
 def test_host_entry_points(L):
     from paper_2305_19028_b200 import tlsrqi
-    assert L.tls_abi_version() == 4
+    assert L.tls_abi_version() == 5
     for code, name in tlsrqi.STATUS.items():
         assert tlsrqi.tls_status_string(code) == name
     o = tlsrqi.tls_rqi_opts_default()
@@ -58,7 +58,7 @@ def test_argument_validation_without_gpu(L):
     assert L.tls_workspace_size(C.byref(M), 50) == 0
     M.layout = 1
     M.m_global = 10
-    assert L.tls_workspace_size(C.byref(M), 50) == 0             # CSR not in this build
+    assert L.tls_workspace_size(C.byref(M), 50) == 0             # CSR without rowptr / colidx / vals
     M.layout, M.ld = 0, 5                                        # odd ld
     assert L.tls_workspace_size(C.byref(M), 50) == 0
     M.ld, M.vals = 4, 256

@@ -453,3 +453,48 @@ def test_certify_sigma_exact_on_consistent_pair():
     assert s * s == pytest.approx(3.0 - math.sqrt(5.0), rel=1e-14)
     P = tlsgen.paper_problem("bjorck", eps=0.0)
     assert rqi.certify_sigma(P.A, P.b, P.x_true) < 1e-15
+
+
+# ----------------------------------------------------------------------------- R28 certificate
+def test_certificate_rhs_is_the_counter_based_vector():
+    """r_j = ((j + 1) * 0x9E3779B97F4A7C15 mod 2^64 >> 11) 2^-53 - 1/2, recomputed with Python
+    integers and exact rationals (the GPU generates the same bits, k_cert_rhs)."""
+    from fractions import Fraction
+    r = rqi.certificate_rhs(300)
+    for j in range(300):
+        h = ((j + 1) * 0x9E3779B97F4A7C15) % (1 << 64)
+        assert Fraction(r[j]) == Fraction(h >> 11, 1 << 53) - Fraction(1, 2)
+
+
+@pytest.mark.parametrize("u_f", ["fp16", "fp64"])
+def test_minimality_certificate_against_closed_form(u_f):
+    """A = U diag(s) V^T with s_n = 1e-2 known by construction: A^T A - sigma^2 I is positive
+    definite iff sigma < s_n.  The certificate must accept sigma = 0.9 s_n
+    and 0.5 s_n and reject sigma = 1.1 s_n, between s_n and s_{n-1}, and above s_1."""
+    P = tlsgen.dense_problem(600, 30, 1e2, 1e-3, 12, twin=True)
+    s = np.linalg.svd(P.A, compute_uv=False)
+    pc = rqi.factor_precond(P.A, u_f)
+    for sig, want in [(0.5 * s[-1], False), (0.9 * s[-1], False), (1.1 * s[-1], True),
+                      (0.5 * (s[-1] + s[-2]), True), (2.0 * s[0], True)]:
+        nm, dmin = rqi.minimality_certificate(P.A, pc, sig * sig, 10)
+        assert nm == want, (sig / s[-1], dmin)
+
+
+def test_not_minimal_reported_for_a_converged_non_minimal_pair():
+    """A nearly non-generic problem (literal noise 1e-1 at kappa 1e2: sigma_{n+1} ~ sigma'_n)
+    with the paper's breakdown rule and an until-tol budget: RQI converges (tol crossing) to a
+    singular pair of [A, b] ABOVE sigma'_n -- an eigenpair, not the TLS solution.  With
+    minimal_check the status is NOT_MINIMAL, and the SVD confirms sigma > sigma'_n; the same
+    options on well-posed problems (cfg1, cfg2w) keep OK with sigma < sigma'_n."""
+    P = tlsgen.dense_problem(400, 40, 1e2, 1e-1, 2, twin=False)
+    sn = np.linalg.svd(P.A, compute_uv=False)[-1]
+    o = rqi.RqiOptions(breakdown_rule=1, budget_rule=1, minimal_check=10)
+    _, res = rqi.solve(P.A, P.b, "fp64", opts=o)
+    assert res.status == rqi.NOT_MINIMAL and res.termination == rqi.T_CONVERGED_TOL
+    assert res.sigma > sn
+    _, res0 = rqi.solve(P.A, P.b, "fp64", opts=rqi.RqiOptions(breakdown_rule=1, budget_rule=1))
+    assert res0.status == rqi.OK and res0.sigma == res.sigma          # the check changes only the status
+    for name in ("cfg1", "cfg2w"):
+        Q = tlsgen.config(name)
+        _, r = rqi.solve(Q.A, Q.b, Q.u_f, opts=rqi.RqiOptions(minimal_check=10))
+        assert r.status == rqi.OK and r.sigma < np.linalg.svd(Q.A, compute_uv=False)[-1]

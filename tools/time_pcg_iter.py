@@ -1,0 +1,70 @@
+"""Non-pass time of one PCG iteration (NEXT-3): a solve on a SHORT A (m = 8192 rows, n = 1024,
+so the operator pass is ~10 us) with budget_rule = until tol and a loose tol, timed with CUDA
+events around the whole PCG loop; per iteration = loop time / iterations, minus the pass
+kernel's own event-timed duration.  Compares the substitution step (k_pcg_step, 8-CTA
+clusters), the explicit-inverse step with the separate reduction (TLS_FUSE_REDUCE=0) and the
+fused step (reduction folded into k_wpcg_step_coop).
+
+  python tools/time_pcg_iter.py [--n 1024] [--m 8192]
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def one(mode, m, n):
+    import numpy as np
+    import torch
+    import tlsgen
+    from paper_2305_19028_b200 import tlsrqi as T
+    torch.cuda.set_device(0)
+    P = tlsgen.dense_problem(m, n, 1e2, 1e-3, 3, twin=True, device="cuda", keep_factors=False)
+    M = T.matrix(P.A)
+    ws = T.workspace(M)
+    rc, R, _ = T.tls_factor_precond(M, "fp16", ws=ws)
+    pa = 1 if mode == "subst" else 2
+    o = T.tls_rqi_opts_default(precond_apply=pa, boot_max=400, boot_tol=1e-300)   # bootstrap = 400 iterations
+    o.max_outer = 1
+    for _ in range(2):
+        T.tls_rqi_pcgtls(M, P.b, R, opts=o, ws=ws)
+    torch.cuda.synchronize()
+    T.tls_profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rc, x, sig, info = T.tls_rqi_pcgtls(M, P.b, R, opts=o, ws=ws)
+    e1.record()
+    torch.cuda.synchronize()
+    prof = T.tls_profile_read()
+    T.tls_profile_enable(False)
+    total_ms = e0.elapsed_time(e1)
+    it = info["boot_iters"]
+    pass_ms = prof["pass_op2"]["ms"]
+    return {"mode": mode, "m": m, "n": n, "boot_iters": it, "solve_ms": total_ms,
+            "pass_us_per_iter": 1e3 * pass_ms / max(1, prof["pass_op2"]["count"]),
+            "step_us_per_iter": 1e3 * prof["pcg_step"]["ms"] / max(1, prof["pcg_step"]["count"]),
+            "reduce_us_per_iter": 1e3 * prof["reduce"]["ms"] / max(1, prof["reduce"]["count"]),
+            "per_iter_us": 1e3 * total_ms / max(1, it)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--m", type=int, default=8192)
+    ap.add_argument("--mode", default="")
+    args = ap.parse_args()
+    if args.mode:
+        print(json.dumps(one(args.mode, args.m, args.n)))
+        return
+    for mode, env in (("subst", {}), ("winv_sep", {"TLS_FUSE_REDUCE": "0"}), ("winv_fused", {})):
+        e = dict(os.environ, **env)
+        out = subprocess.run([sys.executable, __file__, "--mode", mode, "--m", str(args.m), "--n", str(args.n)],
+                             env=e, capture_output=True, text=True)
+        print(out.stdout.strip() or out.stderr[-2000:], flush=True)
+
+
+if __name__ == "__main__":
+    main()
