@@ -298,6 +298,277 @@ k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchun
   }
 }
 
+// ------------------------------------------------------------------------------ 2'. fused rounding + SYRK
+// k_gram_fused: steps 1 and 2 in ONE cooperative launch, with A^ never written to HBM.
+// Every CTA of split s (one per upper 128-tile) also runs 4 converter warps: the 64-row blocks
+// of the split are rounded cooperatively -- unit u = (row r, 64-column chunk q) of a block goes
+// to CTA u mod ntiles, converter warp (u / ntiles) mod 4 -- from fp64 A (TMA bulk copies into a
+// per-warp staging ring, converted in registers with the hardware cvt.rn: the same single RNE
+// rounding as k_round_scaled) into a small L2-resident ring of kFzRing blocks per split, from
+// which the tile's TMA producer loads its 128B-swizzled panels exactly as k_gram_tc does.
+// Hand-off through two monotonic counters per ring slot (gpu-scope release/acquire, proxy
+// fences for the generic-store -> TMA-load path):
+//   ready[s][slot]  += 1 per converter warp and block   (consumer waits (gen+1) * ntiles * 4)
+//   done[s][slot]   += 1 per tile CTA once its TMA of the block landed
+//                                                       (converter waits gen * ntiles to reuse)
+// All CTAs are co-resident (cooperative launch, one CTA per SM), so the spin waits progress; a
+// wait that exceeds ~1 s of spinning sets *err and proceeds (the host reports TLS_ERR_CUDA).
+// HBM traffic: one read of A (8 m n bytes); the ring stays in L2.  The MMA issuer and the
+// epilogue (fp32 chunk sums, K_t rows per TMEM chunk, reading R11) are k_gram_tc's.
+constexpr int kFzRing = 8;
+constexpr int kFzConvWarps = 4;
+constexpr int kFzThreads = kTcThreads + 32 * kFzConvWarps;
+constexpr int kFzSlots = 32;                       // staging slots per converter warp
+constexpr int kFzUnit = 512;                       // one unit: 64 fp64 of one row
+constexpr size_t kFzSmem = 2 * kTcStages * kTcPanel + (size_t)kFzConvWarps * kFzSlots * kFzUnit + 2048 + 1024;
+
+struct FzArgs {
+  const double* A;
+  int64_t ld;
+  int n;
+  const double* dinv;
+  uint16_t* ring;       // [nsplit][kFzRing][64][npad64]
+  int npad64;
+  int* ready;           // [nsplit][kFzRing]
+  int* done;            // [nsplit][kFzRing]
+  int* err;
+  int* range;
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_geq(const int* p, int target, int* err) {
+  for (long it = 0; ld_acquire(p) < target; ++it) {
+    if (it > (1L << 24)) { atomicExch(err, 1); return; }
+    __nanosleep(64);
+  }
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(kFzThreads, 1)
+k_gram_fused(const __grid_constant__ CUtensorMap tmap, FzArgs fz, int64_t m, int TT, int nchunks, int nsplit,
+             int kpc, int super, double* __restrict__ part) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* panA = smem;
+  unsigned char* panB = smem + kTcStages * kTcPanel;
+  unsigned char* stg = smem + 2 * kTcStages * kTcPanel;                          // [4 warps][32][512 B]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + (size_t)kFzConvWarps * kFzSlots * kFzUnit);
+  uint64_t* empty = full + kTcStages;
+  uint64_t* tfull = empty + kTcStages;
+  uint64_t* tempty = tfull + kTcAcc;
+  uint64_t* cbar = tempty + kTcAcc;                                              // [4][32]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(cbar + kFzConvWarps * kFzSlots);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = gridDim.x;
+  int t = blockIdx.x, I = 0;
+  while (t >= TT - I) { t -= TT - I; ++I; }
+  const int J = I + t;
+  const bool diag = (I == J);
+  const int s = blockIdx.y;
+  const int c0 = (int)((int64_t)nchunks * s / nsplit), c1 = (int)((int64_t)nchunks * (s + 1) / nsplit);
+  const int kb_total = (int)((m + kTcBK - 1) / kTcBK);
+  const int kb_begin = c0 * kpc, kb_end = min(c1 * kpc, kb_total);
+  const int nblk = kb_end > kb_begin ? kb_end - kb_begin : 0;
+  int* ready = fz.ready + s * kFzRing;
+  int* done = fz.done + s * kFzRing;
+  const int conv_per_block = ntiles * kFzConvWarps;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTcStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < kTcAcc; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
+    for (int i = 0; i < kFzConvWarps * kFzSlots; ++i) mbar_init(&cbar[i], 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(kTcAcc * kTcTile)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp >= 10) {
+    // ---------------- converters: fp64 A -> fl_uf(A D^-1) into the L2 ring
+    const int cw = warp - 10;
+    const int ncq = (fz.n + 63) / 64;
+    const int nunits = 64 * ncq;
+    const int u0 = blockIdx.x + ntiles * cw;
+    const int mine = nunits > u0 ? (nunits - 1 - u0) / conv_per_block + 1 : 0;
+    const int64_t total = (int64_t)nblk * mine;
+    unsigned char* my = stg + (size_t)cw * kFzSlots * kFzUnit;
+    uint64_t* mb = cbar + cw * kFzSlots;
+    const uint64_t pol = policy_evict_first();
+    // unit index k of block l -> (row, chunk) and whether it needs data
+    auto unit_of = [&](int64_t seq, int& l, int& r, int& q, int64_t& row) {
+      l = (int)(seq / mine);
+      const int u = u0 + (int)(seq % mine) * conv_per_block;
+      r = u / ncq;
+      q = u % ncq;
+      row = (int64_t)(kb_begin + l) * kTcBK + r;
+    };
+    auto issue = [&](int64_t seq) {             // lane 0: bulk copy of unit `seq` into its slot
+      int l, r, q;
+      int64_t row;
+      unit_of(seq, l, r, q, row);
+      uint64_t* bar = &mb[seq % kFzSlots];
+      if (row < m) {
+        int cols = (int)(fz.ld - 64 * q);
+        if (cols > 64) cols = 64;
+        mbar_arrive_expect_tx(bar, (uint32_t)cols * 8);
+        bulk_g2s(my + (seq % kFzSlots) * kFzUnit, fz.A + row * fz.ld + 64 * q, (uint32_t)cols * 8, bar, pol);
+      } else {
+        mbar_arrive(bar);                       // a padding row: nothing to load
+      }
+    };
+    if (lane == 0)
+      for (int64_t k = 0; k < total && k < kFzSlots; ++k) issue(k);
+    int bad = 0;
+    int64_t seq = 0;
+    for (int l = 0; l < nblk; ++l) {
+      const int slot = l % kFzRing;
+      const int gen = l / kFzRing;
+      if (lane == 0 && gen > 0) wait_geq(&done[slot], gen * ntiles, fz.err);   // consumers released it
+      __syncwarp();
+      uint16_t* rb = fz.ring + ((size_t)(s * kFzRing + slot) * kTcBK) * fz.npad64;
+      for (int k = 0; k < mine; ++k, ++seq) {
+        int ll, r, q;
+        int64_t row;
+        unit_of(seq, ll, r, q, row);
+        mbar_wait(&mb[seq % kFzSlots], (uint32_t)(seq / kFzSlots) & 1u);
+        const int c = 64 * q + 2 * lane;
+        double x0 = 0.0, x1 = 0.0;
+        if (row < m) {
+          const double2 v = *reinterpret_cast<const double2*>(my + (seq % kFzSlots) * kFzUnit + 16 * lane);
+          x0 = c < fz.n ? v.x * fz.dinv[c] : 0.0;
+          x1 = c + 1 < fz.n ? v.y * fz.dinv[c + 1] : 0.0;
+        }
+        __syncwarp();                           // every lane read the slot: it may be refilled
+        if (lane == 0 && seq + kFzSlots < total) issue(seq + kFzSlots);
+        const uint16_t h0 = FMT == 0 ? f64_to_f16_bits(x0) : f64_to_bf16_bits(x0);
+        const uint16_t h1 = FMT == 0 ? f64_to_f16_bits(x1) : f64_to_bf16_bits(x1);
+        const uint32_t lim = FMT == 0 ? 0x7c00u : 0x7f80u;
+        bad |= ((h0 & 0x7fffu) >= lim) | ((h1 & 0x7fffu) >= lim);
+        if (c < fz.npad64)
+          *reinterpret_cast<uint32_t*>(rb + (size_t)r * fz.npad64 + c) = (uint32_t)h0 | ((uint32_t)h1 << 16);
+      }
+      // publish this warp's share of block l: generic stores -> visible to the TMA (async proxy)
+      fence_proxy_async_global();
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(&ready[slot], 1);
+    }
+    if (bad) atomicExch(fz.range, 1);
+  } else if (warp == 0) {
+    // ---------------- TMA producer (ring -> swizzled panels)
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      const uint32_t bytes = diag ? kTcPanel : 2 * kTcPanel;
+      for (int l = 0; l < nblk; ++l) {
+        const int st = l % kTcStages;
+        const uint32_t ph = (uint32_t)(l / kTcStages) & 1u;
+        if (l >= kTcStages) mbar_wait(&empty[st], ph ^ 1u);
+        wait_geq(&ready[l % kFzRing], (l / kFzRing + 1) * conv_per_block, fz.err);
+        fence_proxy_async_global();
+        mbar_arrive_expect_tx(&full[st], bytes);
+        const int row = (s * kFzRing + l % kFzRing) * kTcBK;
+        unsigned char* a = panA + st * kTcPanel;
+        tma_load_2d(a, &tmap, I * kTcTile, row, &full[st]);
+        tma_load_2d(a + kTcPanel / 2, &tmap, I * kTcTile + 64, row, &full[st]);
+        if (!diag) {
+          unsigned char* b = panB + st * kTcPanel;
+          tma_load_2d(b, &tmap, J * kTcTile, row, &full[st]);
+          tma_load_2d(b + kTcPanel / 2, &tmap, J * kTcTile + 64, row, &full[st]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread), k_gram_tc's loop over the split's chunks
+    if (lane == 0) {
+      const uint32_t idesc = idesc_f16(FMT);
+      int l = 0;
+      for (int c = c0; c < c1; ++c) {
+        const int j = c - c0;
+        const int buf = j % kTcAcc;
+        if (j >= kTcAcc) mbar_wait(&tempty[buf], (uint32_t)(j / kTcAcc - 1) & 1u);
+        tc_fence_after();
+        const uint32_t dtm = tmem_base + (uint32_t)(buf * kTcTile);
+        const int kb1 = min((c + 1) * kpc, kb_total);
+        for (int kb = c * kpc; kb < kb1; ++kb, ++l) {
+          const int st = l % kTcStages;
+          mbar_wait(&full[st], (uint32_t)(l / kTcStages) & 1u);
+          atomicAdd(&done[l % kFzRing], 1);     // the panels of block l are in shared memory
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(panA + st * kTcPanel);
+          const uint32_t b0 = smem_u32((diag ? panA : panB) + st * kTcPanel);
+#pragma unroll
+          for (int kk = 0; kk < kTcBK / 16; ++kk) {
+            const uint64_t ad = sw128_desc(a0 + kk * 2048, kTcPanel / 2, 1024);
+            const uint64_t bd = sw128_desc(b0 + kk * 2048, kTcPanel / 2, 1024);
+            tc_mma_f16(dtm, ad, bd, idesc, (kb > c * kpc || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty[st]);
+        }
+        tc_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2-9): k_gram_tc's, draining 32 columns at a time
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int row = q * 32 + lane;
+    double* out = part + ((size_t)s * gridDim.x + blockIdx.x) * (kTcTile * kTcTile) + (size_t)row * kTcTile + half * 64;
+    float sm[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) sm[i] = 0.f;
+    int pending = 0;
+    for (int c = c0; c < c1; ++c) {
+      const int j = c - c0;
+      const int buf = j % kTcAcc;
+      mbar_wait(&tfull[buf], (uint32_t)(j / kTcAcc) & 1u);
+      tc_fence_after();
+      const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kTcTile + half * 64);
+      uint32_t r0[32];
+      TLS_TMEM_LD32(ta, r0);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int k = 0; k < 32; ++k) sm[k] = __fadd_rn(sm[k], __uint_as_float(r0[k]));
+      TLS_TMEM_LD32(ta + 32, r0);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+#pragma unroll
+      for (int k = 0; k < 32; ++k) sm[k + 32] = __fadd_rn(sm[k + 32], __uint_as_float(r0[k]));
+      if (++pending == super) {
+#pragma unroll
+        for (int k = 0; k < 64; ++k) { atomicAdd(out + k, (double)sm[k]); sm[k] = 0.f; }
+        pending = 0;
+      }
+    }
+    if (pending) {
+#pragma unroll
+      for (int k = 0; k < 64; ++k) atomicAdd(out + k, (double)sm[k]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTcAcc * kTcTile) : "memory");
+  }
+}
+
 // ------------------------------------------------------------------------------ 3. split reduction
 __global__ void k_gram_reduce_t(const double* __restrict__ part, int ntiles, int nsplit, int TT, int tile, int n,
                                 double* __restrict__ G) {
@@ -367,12 +638,27 @@ bool gram_tc_supported(int u_f, int K_t) {
   return encode_fn() != nullptr;
 }
 
+// The fused path's ring (kFzRing 64-row blocks of A^ per split, rows of round64(n) 16-bit
+// values) plus its counters; used in place of the A^ buffer of the two-kernel path.
+static size_t fz_ring_bytes(int n, int nsplit) {
+  const int npad64 = (n + 63) / 64 * 64;
+  return (size_t)nsplit * kFzRing * kTcBK * npad64 * 2 + 2 * (size_t)nsplit * kFzRing * 4 + 256;
+}
+
 size_t gram_tc_ws_bytes(int64_t m, int n, int K_t) {
   int TT, ntiles, nchunks, nsplit;
   tc_shape(m, n, K_t < kTcBK ? kTcBK : K_t, TT, ntiles, nchunks, nsplit);
   const int npad = (n + 7) / 8 * 8;
-  const size_t ah = ((size_t)m * npad * 2 + 1023) & ~(size_t)1023;
+  size_t ah = ((size_t)m * npad * 2 + 1023) & ~(size_t)1023;
+  const size_t fz = (fz_ring_bytes(n, nsplit) + 1023) & ~(size_t)1023;
+  if (fz > ah) ah = fz;
   return ah + (size_t)nsplit * ntiles * kTcTile * kTcTile * 8;
+}
+
+// TLS_GRAM_FUSED=0 selects the two-kernel path (k_round_scaled + k_gram_tc) for comparisons.
+static bool gram_fused_enabled() {
+  const char* e = getenv("TLS_GRAM_FUSED");
+  return !(e && e[0] == '0');
 }
 
 int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, double* G, void* ws, size_t ws_bytes,
@@ -386,7 +672,59 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
     return TLS_ERR_WORKSPACE;
   }
   uint16_t* Ah = static_cast<uint16_t*>(ws);
-  double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + ah_bytes);
+  size_t a_region = ah_bytes;
+  {
+    const size_t fz = (fz_ring_bytes(A.n, nsplit) + 1023) & ~(size_t)1023;
+    if (fz > a_region) a_region = fz;
+  }
+  double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + a_region);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (gram_fused_enabled() && ntiles * nsplit <= sms) {
+    // ---- fused: rounding inside the tensor-core kernel, A^ only in an L2-resident ring
+    const int npad64 = (A.n + 63) / 64 * 64;
+    FzArgs fz;
+    fz.A = A.A;
+    fz.ld = A.ld;
+    fz.n = A.n;
+    fz.dinv = dinv;
+    fz.ring = Ah;
+    fz.npad64 = npad64;
+    fz.ready = reinterpret_cast<int*>(reinterpret_cast<char*>(Ah) + (size_t)nsplit * kFzRing * kTcBK * npad64 * 2);
+    fz.done = fz.ready + nsplit * kFzRing;
+    fz.err = range_flag + 3;            // the factor's flags[4]: a ring hand-off timed out
+    fz.range = range_flag;
+    TLS_CUDA_TRY(cudaMemsetAsync(fz.ready, 0, 2 * (size_t)nsplit * kFzRing * 4, st));
+    CUtensorMap rmap;
+    const cuuint64_t dims[2] = {(cuuint64_t)npad64, (cuuint64_t)nsplit * kFzRing * kTcBK};
+    const cuuint64_t strides[1] = {(cuuint64_t)npad64 * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)kTcBK};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&rmap, u_f == TLS_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                   2, Ah, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled (ring) failed (%d)", (int)r);
+      return TLS_ERR_CUDA;
+    }
+    TLS_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)nsplit * ntiles * kTcTile * kTcTile * 8, st));
+    auto kern = u_f == TLS_FP16 ? k_gram_fused<0> : k_gram_fused<1>;
+    TLS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFzSmem));
+    int per_sm = 0;
+    TLS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFzThreads, kFzSmem));
+    if (per_sm >= 1) {
+      int64_t mm = A.m;
+      int tt = TT, nc = nchunks, ns = nsplit, kpc = K_t / kTcBK, sup = gram_super();
+      void* args[] = {(void*)&rmap, &fz, &mm, &tt, &nc, &ns, &kpc, &sup, &part};
+      TLS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(ntiles, nsplit), dim3(kFzThreads), args, kFzSmem, st));
+      k_gram_reduce_t<<<ntiles, 256, 0, st>>>(part, ntiles, nsplit, TT, kTcTile, A.n, G);
+      TLS_LAUNCH_CHECK();
+      if (launches) *launches += 2;
+      return 0;
+    }
+  }
   // 1. A^ = fl_uf(A D^-1)
   {
     int64_t g = A.m;

@@ -16,16 +16,16 @@
 // accumulates the fp64 partial inner products of the NEXT column (x'^T x' and x'^T W')
 // per CTA, so column j+1's reflector needs no second pass; k_qr_fin reduces those partials
 // (fixed order, deterministic), forms the column's scalars and w^T.  2 launches per column.
-#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "tls_common.cuh"
 #include "tls_kernels.h"
 
 namespace tls {
-namespace cg = cooperative_groups;
 
 namespace {
 constexpr int kQrThreads = 256;
@@ -126,6 +126,8 @@ __global__ void __launch_bounds__(qr_step_threads<CPT>(), 1) k_qr_step(T* __rest
     const int64_t inext = i + teams;
     const bool hn = inext < r1;
     if (hn) qr_load_row<T, LOAD, CPT>(W, A, lda, inext, n, ldw, j, c, tl, TG, nxt, nj, nc);
+    // in-place update by a multi-warp team: see qr_update_v4 (the LOAD pass reads A, not W)
+    if (!LOAD && TG > 32) asm volatile("bar.sync %0, %1;" ::"r"(1 + tm), "r"(TG) : "memory");
     T* row = W + i * (int64_t)ldw;
     const bool accum = i > c;
     if (LOAD && tl < ldw - n) row[n + tl] = T(0);      // padding columns of the working copy
@@ -198,8 +200,8 @@ __global__ void __launch_bounds__(qr_step_threads<CPT>(), 1) k_qr_step(T* __rest
 // thread tl owns the 4-column groups g = tl + q TG starting at the aligned column c0 = c & ~3
 // (ldw is a multiple of 4).  Columns k < c and k >= n carry w_k = 0, so they are rewritten
 // with their own values (rd(x - rd(v 0)) = x) and need no masks.
-// Row block b's share of column j's update pass (the body of k_qr_step_v4 and of one column
-// of k_qr_coop); `teams` teams of TG threads, threads beyond teams x TG only join the combine.
+// Row block b's share of column j's update pass (the body of k_qr_step_v4); `teams` teams of
+// TG threads, threads beyond teams x TG only join the combine.
 template <int CPT, int PREC>
 __device__ __forceinline__ void qr_update_v4(float* __restrict__ W, int64_t m, int n, int ldw, int j, int RB, int b,
                                              int TG, int teams, const double* __restrict__ wT,
@@ -249,6 +251,13 @@ __device__ __forceinline__ void qr_update_v4(float* __restrict__ W, int64_t m, i
     const int64_t inext = i + teams;
     const bool hn = inext < r1;
     if (hn) load(inext);
+    // A team of several warps updates a row in place, and every thread reads the row's column c
+    // (old value) while the thread owning column c's group writes its new value: all of the
+    // team's loads of row `inext` must be performed before any store to it (one iteration
+    // later).  bar.sync orders them (its participants' prior accesses are performed first).
+    // A one-warp team needs none.  (Without it, teams of 3 warps -- n >= ~520 -- read
+    // already-updated column-c values: round 1's QR differed from the oracle there.)
+    if (TG > 32) asm volatile("bar.sync %0, %1;" ::"r"(1 + tm), "r"(TG) : "memory");
     float* row = W + i * (int64_t)ldw;
     const float vf = (i == j) ? v0f : cj;
     const double xd = (double)qr_rdf<PREC>(__fsub_rn(cc, qr_rdf<PREC>(__fmul_rn(vf, wcf))));
@@ -319,85 +328,6 @@ __global__ void __launch_bounds__(qr_step_threads<CPT>(), 1) k_qr_step_v4(
   if (*dead) return;
   qr_update_v4<CPT, PREC>(W, m, n, ldw, j, RB, bfirst + (int)blockIdx.x, TG, (int)blockDim.x / TG, wT, scal, partP, G,
                           qsm, true);
-}
-
-// ---------------------------------------------------------------- one persistent kernel
-// The whole column loop of the fp32 working copy in ONE cooperative launch (all CTAs
-// resident): per column, every CTA forms the column's scalars from the partials (same bits
-// in every CTA), reduces its slice of w^T, grid barrier, its rows' update pass (with the next
-// column's partials), grid barrier.  Replaces 2 launches per column and k_qr_fin's latency,
-// but measured slower than the PDL chain, so it is opt-in (TLS_QR_COOP=1).
-template <int PREC>
-__device__ __forceinline__ bool qr_fin_coop(const float* __restrict__ W, int n, int ldw, int j, int b0, int nb,
-                                            const double* __restrict__ partP, double* __restrict__ wT,
-                                            double* __restrict__ scal, double* __restrict__ G,
-                                            int* __restrict__ qflags, double* red, double* cs) {
-  constexpr int prec = PREC;
-  const int t = threadIdx.x;
-  double tl = 0.0;
-  for (int b = b0 + t; b < nb; b += (int)blockDim.x) tl += partP[(int64_t)b * n + j];
-  const double tail = block_sum(tl, red);                      // fixed order: same bits in every CTA
-  const double x0 = (double)W[(int64_t)j * ldw + j];
-  const double sigma = round_uf(sqrt(round_uf(fma(x0, x0, tail), prec)), prec);
-  if (sigma == 0.0) {
-    if (blockIdx.x == 0 && t == 0) { qflags[0] = 1; qflags[1] = j + 1; }
-    return false;
-  }
-  const double alpha = x0 >= 0.0 ? -sigma : sigma;
-  const double v0 = round_uf(x0 - alpha, prec);
-  const double vv = round_uf(fma(v0, v0, tail), prec);
-  const double beta = round_uf(2.0 / vv, prec);
-  // this CTA's slice of columns; 8 columns at a time, 32 row groups per column
-  const int nk = n - j - 1;
-  const int S = (nk + (int)gridDim.x - 1) / (int)gridDim.x;
-  const int kbeg = j + 1 + (int)blockIdx.x * S, kend = min(n, kbeg + S);
-  const int l8 = t & 7, grp = t >> 3, ngrp = (int)blockDim.x >> 3;
-  for (int k0 = kbeg; k0 < kend; k0 += 8) {
-    const int k = k0 + l8;
-    double sum = 0.0;
-    if (k < kend)
-      for (int b = b0 + grp; b < nb; b += ngrp) sum += partP[(int64_t)b * n + k];
-    cs[grp * 8 + l8] = sum;
-    __syncthreads();
-    if (t < 8 && k0 + t < kend) {
-      double tot = 0.0;
-      for (int g = 0; g < ngrp; ++g) tot += cs[g * 8 + t];
-      const int kk = k0 + t;
-      const double w = round_uf(fma(v0, (double)W[(int64_t)j * ldw + kk], tot), prec);
-      wT[kk] = round_uf(beta * w, prec);
-    }
-    __syncthreads();
-  }
-  if (blockIdx.x == 0 && t == 0) {
-    scal[4 * j + 0] = alpha;
-    scal[4 * j + 1] = v0;
-    scal[4 * j + 2] = sigma;
-    scal[4 * j + 3] = beta;
-    G[(int64_t)j * n + j] = sigma;
-  }
-  return true;
-}
-
-template <int CPT, int PREC>
-__global__ void __launch_bounds__(qr_step_threads<CPT>(), 1) k_qr_coop(
-    float* __restrict__ W, int64_t m, int n, int ldw, int RB, int nb, double* __restrict__ partP,
-    double* __restrict__ wT, double* __restrict__ scal, double* __restrict__ G, int* __restrict__ qflags) {
-  extern __shared__ double qsm[];
-  __shared__ double red[32];
-  __shared__ double cs[qr_step_threads<CPT>()];
-  cg::grid_group grid = cg::this_grid();
-  for (int j = 0; j < n; ++j) {
-    const int b0 = (j > 0 ? j - 1 : 0) / RB;
-    // sigma is computed identically in every CTA, so a zero column ends every CTA's loop
-    if (!qr_fin_coop<PREC>(W, n, ldw, j, b0, nb, partP, wT, scal, G, qflags, red, cs)) break;
-    grid.sync();
-    if (j + 1 == n) break;
-    const int ngroups = (ldw - ((j + 1) & ~3)) >> 2;
-    const int TG = qr_team(ngroups, CPT / 4);
-    qr_update_v4<CPT, PREC>(W, m, n, ldw, j, RB, (int)blockIdx.x, TG, qr_step_threads<CPT>() / TG, wT, scal, partP, G, qsm,
-                            false);
-    grid.sync();
-  }
 }
 
 // Column j's scalars and w^T from the partials the previous pass left (CTAs b >= b0 wrote).
@@ -519,35 +449,37 @@ int qr_t(const DenseView& A, const double* dinv, void* Wbuf, double* partP, doub
   int rc = qr_step_launch<T, true, CPT, PREC>(W, A, ldw, dinv, -1, RB, 0, nb, nullptr, nullptr, partP, G, qflags, st);
   if (rc) return rc;
   int nl = 1;
-  if constexpr (sizeof(T) == 4) {
-    // opt-in (TLS_QR_COOP=1): measured slower than the PDL chain (4096 x 512: 5.4 vs 4.4 ms,
-    // 65536 x 2048: 418 vs 301 ms), like the other cooperative streaming passes
-    const char* ce = getenv("TLS_QR_COOP");
-    const bool coop_env = ce && ce[0] == '1' && !leaf;   // the cooperative loop has no leaf mode
-    const size_t smem = (size_t)qr_step_threads<CPT>() * CPT * sizeof(double);
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (coop_env && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_qr_coop<CPT, PREC>, qr_step_threads<CPT>(), smem) ==
-                        cudaSuccess && per_sm * sms >= nb) {
-      float* Wf = reinterpret_cast<float*>(W);
-      int64_t mm = m;
-      int nn = n, ll = ldw, rb = RB, nbb = nb;
-      void* args[] = {&Wf, &mm, &nn, &ll, &rb, &nbb, &partP, &wT, &scal, &G, &qflags};
-      const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_qr_coop<CPT, PREC>, dim3(nb), dim3(qr_step_threads<CPT>()),
-                                                        args, smem, st);
-      if (e != cudaSuccess) {
-        set_error("k_qr_coop launch: %s", cudaGetErrorString(e));
-        return TLS_ERR_CUDA;
-      }
-      if (launches) *launches += nl + 1;
-      return 0;
-    }
-  }
   // row_stride > 0 (the row-interleaved TSQR stack, R26): rows >= (j + 2) row_stride are zero in
   // columns j and j + 1, so the pass of column j stops there (bit-identical: they add zeros)
   auto m_act = [&](int j) -> int64_t { return row_stride > 0 ? std::min(m, (int64_t)(j + 2) * row_stride) : m; };
+  // debugging aid: TLS_QR_STOP=J ends the loop after column J's update pass and, with
+  // TLS_QR_DUMP=path, writes the working copy, w^T, the scalars and the partials to path
+  const char* stop_e = getenv("TLS_QR_STOP");
+  const int stop_j = stop_e ? atoi(stop_e) : -1;
   for (int j = 0; j < n; ++j) {
+    if (stop_j >= 0 && j > stop_j) {
+      const char* path = getenv("TLS_QR_DUMP");
+      if (path) {
+        cudaStreamSynchronize(st);
+        std::vector<char> hw((size_t)m * ldw * sizeof(T));
+        std::vector<double> hwt(n), hs(4 * (size_t)n), hp((size_t)nb * n);
+        cudaMemcpy(hw.data(), W, hw.size(), cudaMemcpyDeviceToHost);
+        cudaMemcpy(hwt.data(), wT, n * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(hs.data(), scal, 4 * (size_t)n * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(hp.data(), partP, (size_t)nb * n * 8, cudaMemcpyDeviceToHost);
+        FILE* f = fopen(path, "wb");
+        if (f) {
+          const int64_t hdr[5] = {m, n, ldw, nb, (int64_t)sizeof(T)};
+          fwrite(hdr, 8, 5, f);
+          fwrite(hw.data(), 1, hw.size(), f);
+          fwrite(hwt.data(), 8, n, f);
+          fwrite(hs.data(), 8, 4 * (size_t)n, f);
+          fwrite(hp.data(), 8, (size_t)nb * n, f);
+          fclose(f);
+        }
+      }
+      break;
+    }
     // partials of column j were written by the pass with first row max(j - 1, 0)
     const int b0 = (int)((j > 0 ? j - 1 : 0) / RB);
     const int nbj = j == 0 ? nb : (int)((m_act(j - 1) + RB - 1) / RB);   // CTAs that wrote them

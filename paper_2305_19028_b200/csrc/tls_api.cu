@@ -958,7 +958,8 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
   if (info) { info->passes = cx.passes; info->launches = cx.launches; }
   { const int arc = comm_async_check(comm); if (arc) { tls_precond_destroy(h); return arc; } }
   int st = 0;
-  if (hflags[0]) { set_error("A has a zero or non-finite column (rank deficient)"); st = TLS_ERR_ARG; }
+  if (hflags[4]) { set_error("k_gram_fused: a ring hand-off timed out"); st = TLS_ERR_CUDA; }
+  else if (hflags[0]) { set_error("A has a zero or non-finite column (rank deficient)"); st = TLS_ERR_ARG; }
   else if (hflags[1]) st = TLS_RANGE;
   else if (hflags[2]) { st = TLS_CHOL_BREAKDOWN; if (info) info->chol_pivot = hflags[2]; }
   else if (hflags[3]) st = TLS_RANGE;
@@ -1576,6 +1577,7 @@ int tls_gram(const tls_matrix_t* A, int32_t u_f, const double* d_dev, int32_t K_
   int hf[8];
   TLS_CUDA_TRY(cudaMemcpyAsync(hf, w.flags, sizeof(hf), cudaMemcpyDeviceToHost, cx.st));
   TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+  if (hf[4]) { set_error("k_gram_fused: a ring hand-off timed out"); return TLS_ERR_CUDA; }
   return hf[1] ? TLS_RANGE : 0;
 }
 

@@ -1,6 +1,6 @@
 """Where does the GPU's u_f Householder QR first differ from oracle.qr?  For each case prints
 the first row j of R~ that differs, the differing columns and values, and the oracle's and
-the GPU's diagonal there.  Run under several environments (TLS_QR_PDL=0, TLS_QR_COOP=1).
+the GPU's diagonal there.  Run under several environments (TLS_QR_PDL=0).
 
   python tools/qr_diff.py
 """
@@ -42,7 +42,7 @@ def main():
         iu = np.triu_indices(n)
         frac = float(np.mean(Rt[iu] == pc.Rt[iu]))
         rows = [j for j in range(n) if not np.array_equal(Rt[j], pc.Rt[j])]
-        msg = f"{m}x{n} {fmt} env PDL={os.environ.get('TLS_QR_PDL', '1')} COOP={os.environ.get('TLS_QR_COOP', '0')}: " \
+        msg = f"{m}x{n} {fmt} env PDL={os.environ.get('TLS_QR_PDL', '1')}: " \
               f"d equal {same_d}, identical {frac:.4f}"
         if rows:
             j = rows[0]
