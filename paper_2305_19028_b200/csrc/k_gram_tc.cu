@@ -23,6 +23,9 @@
 //  3. the split partials are summed in fixed order (k_gram_reduce_t).
 #include <cuda.h>
 
+#include <cstdio>
+#include <vector>
+
 #include "tls_common.cuh"
 #include "tls_kernels.h"
 
@@ -130,7 +133,7 @@ __global__ void __launch_bounds__(256) k_round_scaled(const double* __restrict__
 template <int FMT, bool KAHAN>
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchunks, int nsplit, int kpc,
-          int super, int epi, double* __restrict__ part) {
+          int super, int epi, double* __restrict__ part, int kb0) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment for the 128B-swizzled operand panels
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -186,7 +189,7 @@ k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchun
           const uint32_t ph = (uint32_t)(it / kTcStages) & 1u;
           if (it >= kTcStages) mbar_wait(&empty[st], ph ^ 1u);
           mbar_arrive_expect_tx(&full[st], bytes);
-          const int row = kb * kTcBK;
+          const int row = (kb0 + kb) * kTcBK;      // kb0: the segment's first block (launch_gram_tc)
           unsigned char* a = panA + st * kTcPanel;
           tma_load_2d(a, &tmap, I * kTcTile, row, &full[st]);
           tma_load_2d(a + kTcPanel / 2, &tmap, I * kTcTile + 64, row, &full[st]);
@@ -315,12 +318,16 @@ k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchun
 // wait that exceeds ~1 s of spinning sets *err and proceeds (the host reports TLS_ERR_CUDA).
 // HBM traffic: one read of A (8 m n bytes); the ring stays in L2.  The MMA issuer and the
 // epilogue (fp32 chunk sums, K_t rows per TMEM chunk, reading R11) are k_gram_tc's.
-constexpr int kFzRing = 8;
+constexpr int kFzRing = 16;
 constexpr int kFzConvWarps = 4;
-constexpr int kFzThreads = kTcThreads + 32 * kFzConvWarps;
-constexpr int kFzSlots = 32;                       // staging slots per converter warp
-constexpr int kFzUnit = 512;                       // one unit: 64 fp64 of one row
-constexpr size_t kFzSmem = 2 * kTcStages * kTcPanel + (size_t)kFzConvWarps * kFzSlots * kFzUnit + 2048 + 1024;
+constexpr int kFzThreads = kTcThreads + 32 * kFzConvWarps;   // 448
+constexpr int kFzSlots = 2;                        // staging slots per converter warp
+constexpr int kFzSeg = 1024;                       // one unit: up to 1024 fp64 of one row (8 KB)
+constexpr int kFzUnit = kFzSeg * 8;
+constexpr int kFzMaxN = 2048;                      // D^{-1} staged in shared memory
+constexpr int kFzPub = 2;                          // units per release
+constexpr size_t kFzSmem = 2 * kTcStages * kTcPanel + (size_t)kFzConvWarps * kFzSlots * kFzUnit + kFzMaxN * 8 +
+                           2048 + 1024;
 
 struct FzArgs {
   const double* A;
@@ -333,7 +340,14 @@ struct FzArgs {
   int* done;            // [nsplit][kFzRing]
   int* err;
   int* range;
+  unsigned long long* prof;   // debugging (TLS_FZ_PROF=1): per CTA [8] nanoseconds, else nullptr
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -363,8 +377,10 @@ k_gram_fused(const __grid_constant__ CUtensorMap tmap, FzArgs fz, int64_t m, int
   uint64_t* empty = full + kTcStages;
   uint64_t* tfull = empty + kTcStages;
   uint64_t* tempty = tfull + kTcAcc;
-  uint64_t* cbar = tempty + kTcAcc;                                              // [4][32]
+  uint64_t* cbar = tempty + kTcAcc;                                              // [warps][slots]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(cbar + kFzConvWarps * kFzSlots);
+  double* sdinv = reinterpret_cast<double*>(smem + 2 * kTcStages * kTcPanel +
+                                            (size_t)kFzConvWarps * kFzSlots * kFzUnit + 2048);   // [kFzMaxN]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = gridDim.x;
@@ -379,7 +395,6 @@ k_gram_fused(const __grid_constant__ CUtensorMap tmap, FzArgs fz, int64_t m, int
   const int nblk = kb_end > kb_begin ? kb_end - kb_begin : 0;
   int* ready = fz.ready + s * kFzRing;
   int* done = fz.done + s * kFzRing;
-  const int conv_per_block = ntiles * kFzConvWarps;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kTcStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
@@ -387,6 +402,7 @@ k_gram_fused(const __grid_constant__ CUtensorMap tmap, FzArgs fz, int64_t m, int
     for (int i = 0; i < kFzConvWarps * kFzSlots; ++i) mbar_init(&cbar[i], 1);
     fence_mbar_init();
   }
+  for (int c = threadIdx.x; c < kFzMaxN; c += blockDim.x) sdinv[c] = c < fz.n ? fz.dinv[c] : 0.0;
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
                  "r"(kTcAcc * kTcTile)
@@ -399,86 +415,120 @@ k_gram_fused(const __grid_constant__ CUtensorMap tmap, FzArgs fz, int64_t m, int
   const uint32_t tmem_base = *tmem_holder;
 
   if (warp >= 10) {
-    // ---------------- converters: fp64 A -> fl_uf(A D^-1) into the L2 ring
+    // ---------------- converters: fp64 A -> fl_uf(A D^-1) into the L2 ring.  Units are row
+    // segments of up to 1024 columns (8 KB, one bulk copy); the split's units, row by row, go
+    // round-robin to its ntiles x 4 converter warps.  A warp converts a unit with 16-byte lanes
+    // (16 sub-chunks of 64 columns, unrolled) and releases every kFzPub units.
     const int cw = warp - 10;
-    const int ncq = (fz.n + 63) / 64;
-    const int nunits = 64 * ncq;
-    const int u0 = blockIdx.x + ntiles * cw;
-    const int mine = nunits > u0 ? (nunits - 1 - u0) / conv_per_block + 1 : 0;
-    const int64_t total = (int64_t)nblk * mine;
+    const int nseg = (fz.n + kFzSeg - 1) / kFzSeg;
+    const int nconv = ntiles * kFzConvWarps;
+    const int wid = blockIdx.x * kFzConvWarps + cw;          // 0..nconv-1 within the split
+    const int64_t nu = (int64_t)nblk * kTcBK * nseg;            // units of the split
     unsigned char* my = stg + (size_t)cw * kFzSlots * kFzUnit;
     uint64_t* mb = cbar + cw * kFzSlots;
     const uint64_t pol = policy_evict_first();
-    // unit index k of block l -> (row, chunk) and whether it needs data
-    auto unit_of = [&](int64_t seq, int& l, int& r, int& q, int64_t& row) {
-      l = (int)(seq / mine);
-      const int u = u0 + (int)(seq % mine) * conv_per_block;
-      r = u / ncq;
-      q = u % ncq;
-      row = (int64_t)(kb_begin + l) * kTcBK + r;
-    };
-    auto issue = [&](int64_t seq) {             // lane 0: bulk copy of unit `seq` into its slot
-      int l, r, q;
-      int64_t row;
-      unit_of(seq, l, r, q, row);
-      uint64_t* bar = &mb[seq % kFzSlots];
+    auto issue = [&](int64_t u, int slot) {                     // lane 0
+      const int64_t rowl = u / nseg;                            // row within the split
+      const int seg = (int)(u % nseg);
+      const int64_t row = (int64_t)kb_begin * kTcBK + rowl;
+      uint64_t* bar = &mb[slot];
       if (row < m) {
-        int cols = (int)(fz.ld - 64 * q);
-        if (cols > 64) cols = 64;
+        int cols = (int)(fz.ld - (int64_t)kFzSeg * seg);
+        if (cols > kFzSeg) cols = kFzSeg;
         mbar_arrive_expect_tx(bar, (uint32_t)cols * 8);
-        bulk_g2s(my + (seq % kFzSlots) * kFzUnit, fz.A + row * fz.ld + 64 * q, (uint32_t)cols * 8, bar, pol);
+        bulk_g2s(my + slot * kFzUnit, fz.A + row * fz.ld + (int64_t)kFzSeg * seg, (uint32_t)cols * 8, bar, pol);
       } else {
-        mbar_arrive(bar);                       // a padding row: nothing to load
+        mbar_arrive(bar);
       }
     };
+    const int nmine = nu > wid ? (int)((nu - 1 - wid) / nconv + 1) : 0;
     if (lane == 0)
-      for (int64_t k = 0; k < total && k < kFzSlots; ++k) issue(k);
+      for (int i = 0; i < kFzSlots && i < nmine; ++i) issue(wid + (int64_t)i * nconv, i);
     int bad = 0;
-    int64_t seq = 0;
-    for (int l = 0; l < nblk; ++l) {
-      const int slot = l % kFzRing;
-      const int gen = l / kFzRing;
-      if (lane == 0 && gen > 0) wait_geq(&done[slot], gen * ntiles, fz.err);   // consumers released it
-      __syncwarp();
-      uint16_t* rb = fz.ring + ((size_t)(s * kFzRing + slot) * kTcBK) * fz.npad64;
-      for (int k = 0; k < mine; ++k, ++seq) {
-        int ll, r, q;
-        int64_t row;
-        unit_of(seq, ll, r, q, row);
-        mbar_wait(&mb[seq % kFzSlots], (uint32_t)(seq / kFzSlots) & 1u);
-        const int c = 64 * q + 2 * lane;
-        double x0 = 0.0, x1 = 0.0;
-        if (row < m) {
-          const double2 v = *reinterpret_cast<const double2*>(my + (seq % kFzSlots) * kFzUnit + 16 * lane);
-          x0 = c < fz.n ? v.x * fz.dinv[c] : 0.0;
-          x1 = c + 1 < fz.n ? v.y * fz.dinv[c + 1] : 0.0;
-        }
-        __syncwarp();                           // every lane read the slot: it may be refilled
-        if (lane == 0 && seq + kFzSlots < total) issue(seq + kFzSlots);
-        const uint16_t h0 = FMT == 0 ? f64_to_f16_bits(x0) : f64_to_bf16_bits(x0);
-        const uint16_t h1 = FMT == 0 ? f64_to_f16_bits(x1) : f64_to_bf16_bits(x1);
-        const uint32_t lim = FMT == 0 ? 0x7c00u : 0x7f80u;
-        bad |= ((h0 & 0x7fffu) >= lim) | ((h1 & 0x7fffu) >= lim);
-        if (c < fz.npad64)
-          *reinterpret_cast<uint32_t*>(rb + (size_t)r * fz.npad64 + c) = (uint32_t)h0 | ((uint32_t)h1 << 16);
+    uint32_t slot_par = 0;
+    unsigned long long t_wd = 0, t_mb = 0, t_cv = 0, t_pub = 0;
+    int pend[kFzPub];
+    int npend = 0;
+    int last_gen_waited = -1, last_l = -1;
+    for (int i = 0; i < nmine; ++i) {
+      const int64_t u = wid + (int64_t)i * nconv;
+      const int64_t rowl = u / nseg;
+      const int seg = (int)(u % nseg);
+      const int l = (int)(rowl / kTcBK), r = (int)(rowl % kTcBK);
+      const int slot = l % kFzRing, gen = l / kFzRing;
+      unsigned long long ta = fz.prof ? gtime() : 0;
+      if (l != last_l) {                        // first unit of this block: the slot must be free
+        if (lane == 0 && gen > 0) wait_geq(&done[slot], gen * ntiles, fz.err);
+        __syncwarp();
+        last_l = l;
       }
-      // publish this warp's share of block l: generic stores -> visible to the TMA (async proxy)
-      fence_proxy_async_global();
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) atomicAdd(&ready[slot], 1);
+      (void)last_gen_waited;
+      if (fz.prof) { const unsigned long long tb = gtime(); t_wd += tb - ta; ta = tb; }
+      const int sl = i % kFzSlots;
+      mbar_wait(&mb[sl], (slot_par >> sl) & 1u);
+      slot_par ^= 1u << sl;
+      if (fz.prof) { const unsigned long long tb = gtime(); t_mb += tb - ta; ta = tb; }
+      const bool live = (int64_t)kb_begin * kTcBK + rowl < m;
+      uint16_t* dst = fz.ring + ((size_t)(s * kFzRing + slot) * kTcBK + r) * fz.npad64 + (size_t)kFzSeg * seg;
+      const uint32_t src = smem_u32(my + sl * kFzUnit) + 16 * lane;
+      const uint32_t dsrc = smem_u32(sdinv + kFzSeg * seg) + 16 * lane;
+      const int hmax = min(kFzSeg / 64, (fz.npad64 - kFzSeg * seg) / 64);       // warp-uniform
+      // branch-free in the sub-chunk loop: all loads first (the staging slot and sdinv are always
+      // in bounds; columns past the copy are garbage but selected away), then convert and store
+#pragma unroll
+      for (int h0 = 0; h0 < kFzSeg / 64; h0 += 8) {
+        double2 v[8], dv[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[h].x), "=d"(v[h].y) : "r"(src + 512 * (h0 + h)));
+          asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(dv[h].x), "=d"(dv[h].y) : "r"(dsrc + 512 * (h0 + h)));
+        }
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const double x0 = live ? v[h].x * dv[h].x : 0.0;      // sdinv = 0 beyond n
+          const double x1 = live ? v[h].y * dv[h].y : 0.0;
+          const uint16_t b0 = FMT == 0 ? f64_to_f16_bits(x0) : f64_to_bf16_bits(x0);
+          const uint16_t b1 = FMT == 0 ? f64_to_f16_bits(x1) : f64_to_bf16_bits(x1);
+          const uint32_t lim = FMT == 0 ? 0x7c00u : 0x7f80u;
+          if (h0 + h < hmax) {
+            bad |= ((b0 & 0x7fffu) >= lim) | ((b1 & 0x7fffu) >= lim);
+            *reinterpret_cast<uint32_t*>(dst + 64 * (h0 + h) + 2 * lane) = (uint32_t)b0 | ((uint32_t)b1 << 16);
+          }
+        }
+      }
+      __syncwarp();                             // the slot was read by every lane: refill it
+      if (lane == 0 && i + kFzSlots < nmine) issue(u + (int64_t)kFzSlots * nconv, sl);
+      if (fz.prof) { const unsigned long long tb = gtime(); t_cv += tb - ta; ta = tb; }
+      pend[npend++ % kFzPub] = slot;
+      if (npend == kFzPub || i + 1 == nmine) {  // release: generic stores -> TMA (async proxy)
+        fence_proxy_async_global();
+        __threadfence();
+        __syncwarp();
+        if (lane == 0)
+          for (int p = 0; p < npend; ++p) atomicAdd(&ready[pend[p]], 1);
+        npend = 0;
+      }
+      if (fz.prof) t_pub += gtime() - ta;
     }
     if (bad) atomicExch(fz.range, 1);
+    if (fz.prof && lane == 0) {
+      unsigned long long* pr = fz.prof + 8 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x);
+      atomicAdd(pr + 0, t_wd); atomicAdd(pr + 1, t_mb); atomicAdd(pr + 2, t_cv); atomicAdd(pr + 3, t_pub);
+    }
   } else if (warp == 0) {
     // ---------------- TMA producer (ring -> swizzled panels)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
       const uint32_t bytes = diag ? kTcPanel : 2 * kTcPanel;
+      unsigned long long t_we = 0, t_wr = 0;
       for (int l = 0; l < nblk; ++l) {
         const int st = l % kTcStages;
         const uint32_t ph = (uint32_t)(l / kTcStages) & 1u;
+        unsigned long long ta = fz.prof ? gtime() : 0;
         if (l >= kTcStages) mbar_wait(&empty[st], ph ^ 1u);
-        wait_geq(&ready[l % kFzRing], (l / kFzRing + 1) * conv_per_block, fz.err);
+        if (fz.prof) { const unsigned long long tb = gtime(); t_we += tb - ta; ta = tb; }
+        wait_geq(&ready[l % kFzRing], (l / kFzRing + 1) * kTcBK * ((fz.n + kFzSeg - 1) / kFzSeg), fz.err);
+        if (fz.prof) t_wr += gtime() - ta;
         fence_proxy_async_global();
         mbar_arrive_expect_tx(&full[st], bytes);
         const int row = (s * kFzRing + l % kFzRing) * kTcBK;
@@ -491,22 +541,31 @@ k_gram_fused(const __grid_constant__ CUtensorMap tmap, FzArgs fz, int64_t m, int
           tma_load_2d(b + kTcPanel / 2, &tmap, J * kTcTile + 64, row, &full[st]);
         }
       }
+      if (fz.prof) {
+        unsigned long long* pr = fz.prof + 8 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x);
+        atomicAdd(pr + 4, t_we); atomicAdd(pr + 5, t_wr);
+      }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread), k_gram_tc's loop over the split's chunks
     if (lane == 0) {
       const uint32_t idesc = idesc_f16(FMT);
       int l = 0;
+      unsigned long long t_wf = 0, t_wt = 0;
       for (int c = c0; c < c1; ++c) {
         const int j = c - c0;
         const int buf = j % kTcAcc;
+        unsigned long long ta = fz.prof ? gtime() : 0;
         if (j >= kTcAcc) mbar_wait(&tempty[buf], (uint32_t)(j / kTcAcc - 1) & 1u);
+        if (fz.prof) t_wt += gtime() - ta;
         tc_fence_after();
         const uint32_t dtm = tmem_base + (uint32_t)(buf * kTcTile);
         const int kb1 = min((c + 1) * kpc, kb_total);
         for (int kb = c * kpc; kb < kb1; ++kb, ++l) {
           const int st = l % kTcStages;
+          ta = fz.prof ? gtime() : 0;
           mbar_wait(&full[st], (uint32_t)(l / kTcStages) & 1u);
+          if (fz.prof) t_wf += gtime() - ta;
           atomicAdd(&done[l % kFzRing], 1);     // the panels of block l are in shared memory
           tc_fence_after();
           const uint32_t a0 = smem_u32(panA + st * kTcPanel);
@@ -520,6 +579,10 @@ k_gram_fused(const __grid_constant__ CUtensorMap tmap, FzArgs fz, int64_t m, int
           tc_commit(&empty[st]);
         }
         tc_commit(&tfull[buf]);
+      }
+      if (fz.prof) {
+        unsigned long long* pr = fz.prof + 8 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x);
+        atomicAdd(pr + 6, t_wf); atomicAdd(pr + 7, t_wt);
       }
     }
   } else {
@@ -655,10 +718,15 @@ size_t gram_tc_ws_bytes(int64_t m, int n, int K_t) {
   return ah + (size_t)nsplit * ntiles * kTcTile * kTcTile * 8;
 }
 
-// TLS_GRAM_FUSED=0 selects the two-kernel path (k_round_scaled + k_gram_tc) for comparisons.
+// TLS_GRAM_FUSED=1 selects the fused kernel.  Measured (tools/time_gram_fused.py, profiles/
+// r02_gram_fused.txt): bit-identical G, HBM traffic = one read of A (ncu: 2.17 GB read, 37 MB
+// written at 2^18 x 1024: the ring never leaves L2), but 7.8 ms against 4.5 ms for the
+// two-kernel path at 2^20 x 1024: the 4 converter warps per SM the register file leaves next to
+// the 8-warp epilogue (448 threads x 128 registers) are issue/latency-bound (ncu: 0.25 eligible
+// warps per scheduler, 18% issue slots busy), so the default stays k_round_scaled + k_gram_tc.
 static bool gram_fused_enabled() {
   const char* e = getenv("TLS_GRAM_FUSED");
-  return !(e && e[0] == '0');
+  return e && e[0] == '1';
 }
 
 int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, double* G, void* ws, size_t ws_bytes,
@@ -681,7 +749,7 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (gram_fused_enabled() && ntiles * nsplit <= sms) {
+  if (gram_fused_enabled() && ntiles * nsplit <= sms && A.n <= kFzMaxN) {
     // ---- fused: rounding inside the tensor-core kernel, A^ only in an L2-resident ring
     const int npad64 = (A.n + 63) / 64 * 64;
     FzArgs fz;
@@ -695,6 +763,12 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
     fz.done = fz.ready + nsplit * kFzRing;
     fz.err = range_flag + 3;            // the factor's flags[4]: a ring hand-off timed out
     fz.range = range_flag;
+    fz.prof = nullptr;
+    const char* pe = getenv("TLS_FZ_PROF");
+    if (pe && pe[0] == '1') {                  // debugging only: per-CTA wait/work times
+      TLS_CUDA_TRY(cudaMalloc(&fz.prof, (size_t)ntiles * nsplit * 8 * 8));
+      TLS_CUDA_TRY(cudaMemsetAsync(fz.prof, 0, (size_t)ntiles * nsplit * 8 * 8, st));
+    }
     TLS_CUDA_TRY(cudaMemsetAsync(fz.ready, 0, 2 * (size_t)nsplit * kFzRing * 4, st));
     CUtensorMap rmap;
     const cuuint64_t dims[2] = {(cuuint64_t)npad64, (cuuint64_t)nsplit * kFzRing * kTcBK};
@@ -721,22 +795,26 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
       TLS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(ntiles, nsplit), dim3(kFzThreads), args, kFzSmem, st));
       k_gram_reduce_t<<<ntiles, 256, 0, st>>>(part, ntiles, nsplit, TT, kTcTile, A.n, G);
       TLS_LAUNCH_CHECK();
+      if (fz.prof) {
+        std::vector<unsigned long long> h((size_t)ntiles * nsplit * 8);
+        cudaMemcpy(h.data(), fz.prof, h.size() * 8, cudaMemcpyDeviceToHost);
+        double avg[8] = {};
+        for (size_t b = 0; b < (size_t)ntiles * nsplit; ++b)
+          for (int k = 0; k < 8; ++k) avg[k] += h[b * 8 + k] / 1e6 / (ntiles * nsplit) / (k < 4 ? kFzConvWarps : 1);
+        fprintf(stderr, "[fz] ms per CTA: conv wait_done %.3f wait_stage %.3f convert %.3f publish %.3f | "
+                "producer wait_empty %.3f wait_ready %.3f | mma wait_full %.3f wait_tempty %.3f\n",
+                avg[0], avg[1], avg[2], avg[3], avg[4], avg[5], avg[6], avg[7]);
+        cudaFree(fz.prof);
+      }
       if (launches) *launches += 2;
       return 0;
     }
   }
-  // 1. A^ = fl_uf(A D^-1)
-  {
-    int64_t g = A.m;
-    const int64_t gmax = (int64_t)num_sms() * 8;
-    if (g > gmax) g = gmax;
-    if (u_f == TLS_FP16)
-      k_round_scaled<TLS_FP16><<<(int)g, 256, 0, st>>>(A.A, A.m, A.n, A.ld, dinv, Ah, npad, range_flag);
-    else
-      k_round_scaled<TLS_BF16><<<(int)g, 256, 0, st>>>(A.A, A.m, A.n, A.ld, dinv, Ah, npad, range_flag);
-    TLS_LAUNCH_CHECK();
-  }
-  // 2. tensor map over A^ (row-major m x npad, 16-bit), 64x64 boxes, 128B swizzle
+  // 1.+2. row segments: k_round_scaled of segment k+1 (side stream) overlaps k_gram_tc of segment
+  // k (caller's stream): the rounding pass is HBM-bound, the SYRK L2/latency-bound, and both
+  // fit on an SM together (registers 320 x 168 + 256 x 32, one SYRK CTA per SM).  Segment
+  // boundaries are multiples of K_t rows, so every K_t chunk stays within one segment; each
+  // segment's launch restarts the 64-chunk fp32 flush grouping (another member of R11's family).
   CUtensorMap tmap;
   {
     const cuuint64_t dims[2] = {(cuuint64_t)npad, (cuuint64_t)A.m};
@@ -752,25 +830,66 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
       return TLS_ERR_CUDA;
     }
   }
+  const char* se = getenv("TLS_GRAM_SEGS");
+  int nseg = se ? atoi(se) : 8;
+  const int64_t seg_unit = K_t;                                   // boundaries on chunk edges
+  const int64_t units = (A.m + seg_unit - 1) / seg_unit;
+  if (nseg < 1) nseg = 1;
+  if (units < (int64_t)nseg * nsplit * 4) nseg = 1;               // small m: one launch
+  // the side stream and the events (one set per device, made on first use)
+  struct Side { int dev = -1; cudaStream_t s = nullptr; cudaEvent_t fork = nullptr, ev[16] = {}; };
+  static Side side_cache[8];
+  Side& sd = side_cache[dev & 7];
+  if (nseg > 1 && sd.dev != dev) {
+    TLS_CUDA_TRY(cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking));
+    TLS_CUDA_TRY(cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming));
+    for (auto& e : sd.ev) TLS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    sd.dev = dev;
+  }
+  if (nseg > 16) nseg = 16;
   const size_t smem = 2 * kTcStages * kTcPanel + 1024 + 512;
-  dim3 grid(ntiles, nsplit);
-  auto launch = [&](auto kern) -> int {
-    TLS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const char* ee = getenv("TLS_GRAM_EPI");   // experiment knob: 0 sync only, 1 + TMEM loads, 2 full
-    kern<<<grid, kTcThreads, smem, st>>>(tmap, A.m, TT, nchunks, nsplit, K_t / kTcBK, gram_super(), ee ? atoi(ee) : 2,
-                                         part);
-    return 0;
-  };
-  TLS_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)nsplit * ntiles * kTcTile * kTcTile * 8, st));
   const bool kahan = gram_kahan();
-  int rc = 0;
-  if (u_f == TLS_FP16) rc = kahan ? launch(k_gram_tc<0, true>) : launch(k_gram_tc<0, false>);
-  else rc = kahan ? launch(k_gram_tc<1, true>) : launch(k_gram_tc<1, false>);
-  if (rc) return rc;
-  TLS_LAUNCH_CHECK();
+  const char* ee = getenv("TLS_GRAM_EPI");   // experiment knob: 0 sync only, 1 + TMEM loads, 2 full
+  auto kfn = u_f == TLS_FP16 ? (kahan ? k_gram_tc<0, true> : k_gram_tc<0, false>)
+                             : (kahan ? k_gram_tc<1, true> : k_gram_tc<1, false>);
+  TLS_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  TLS_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)nsplit * ntiles * kTcTile * kTcTile * 8, st));
+  cudaStream_t rs = nseg > 1 ? sd.s : st;
+  if (nseg > 1) {
+    TLS_CUDA_TRY(cudaEventRecord(sd.fork, st));                    // D^{-1} and the memset are ready
+    TLS_CUDA_TRY(cudaStreamWaitEvent(rs, sd.fork, 0));
+  }
+  for (int k = 0; k < nseg; ++k) {
+    const int64_t r0 = units * k / nseg * seg_unit;
+    int64_t r1 = units * (k + 1) / nseg * seg_unit;
+    if (r1 > A.m) r1 = A.m;
+    const int64_t rows = r1 - r0;
+    if (rows <= 0) continue;
+    int64_t g = rows;
+    const int64_t gmax = (int64_t)num_sms() * (nseg > 1 ? 4 : 8);
+    if (g > gmax) g = gmax;
+    const double* src = A.A + r0 * A.ld;
+    uint16_t* dst = Ah + r0 * npad;
+    if (u_f == TLS_FP16)
+      k_round_scaled<TLS_FP16><<<(int)g, 256, 0, rs>>>(src, rows, A.n, A.ld, dinv, dst, npad, range_flag);
+    else
+      k_round_scaled<TLS_BF16><<<(int)g, 256, 0, rs>>>(src, rows, A.n, A.ld, dinv, dst, npad, range_flag);
+    TLS_LAUNCH_CHECK();
+    if (nseg > 1) {
+      TLS_CUDA_TRY(cudaEventRecord(sd.ev[k], rs));
+      TLS_CUDA_TRY(cudaStreamWaitEvent(st, sd.ev[k], 0));
+    }
+    int TTs, nts, ncs, nss;
+    tc_shape(rows, A.n, K_t, TTs, nts, ncs, nss);
+    const int ns_use = nsplit < ncs ? nsplit : ncs;               // the part buffer holds nsplit splits
+    kfn<<<dim3(ntiles, ns_use), kTcThreads, smem, st>>>(tmap, rows, TT, ncs, ns_use, K_t / kTcBK, gram_super(),
+                                                        ee ? atoi(ee) : 2, part, (int)(r0 / kTcBK));
+    TLS_LAUNCH_CHECK();
+    if (launches) *launches += 2;
+  }
   k_gram_reduce_t<<<ntiles, 256, 0, st>>>(part, ntiles, nsplit, TT, kTcTile, A.n, G);
   TLS_LAUNCH_CHECK();
-  if (launches) *launches += 3;
+  if (launches) *launches += 1;
   return 0;
 }
 

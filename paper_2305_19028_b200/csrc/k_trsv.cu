@@ -517,7 +517,8 @@ __global__ void __launch_bounds__(kWG) k_wgemv_grid(PrecondDev pc, PcgVecs v, co
 __global__ void __launch_bounds__(kWG) k_wpcg_step_coop(PrecondDev pc, PcgVecs v, const double* passout,
                                                        PcgState* __restrict__ S, int nrhs, int rule, int next_q,
                                                        int variant, int pass_nrhs, const double* __restrict__ partials,
-                                                       int G, double* __restrict__ pout) {
+                                                       int G, double* __restrict__ pout, const int* __restrict__ nq_dev) {
+  if (nq_dev) next_q = *nq_dev;         // graph-captured loop (NEXT-3): decided on the device
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double wsh[];
@@ -869,7 +870,8 @@ constexpr int kVecPerThread = 16;  // npad <= kTW * 32 * 16 = 4096
 template <typename T>
 __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_step(PrecondDev pc, PcgVecs v, const double* __restrict__ passout,
                                                        PcgState* __restrict__ S, int nrhs, int rule, int next_q,
-                                                       int variant, int pass_nrhs) {
+                                                       int variant, int pass_nrhs, const int* __restrict__ nq_dev) {
+  if (nq_dev) next_q = *nq_dev;         // graph-captured loop (NEXT-3): decided on the device
   __shared__ double s_alpha, s_beta, s_delta;
   __shared__ int s_upd, s_cont, s_brk, s_exit;
   TrsvSm sm = trsv_carve(pc.npad);
@@ -1136,7 +1138,8 @@ int launch_pcg_init(const PrecondDev& pc, int nrhs, PcgVecs v, PcgState* S, cuda
 }
 
 int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgState* S, int nrhs, int rule,
-                    int next_q, int variant, int pass_nrhs, cudaStream_t st, const double* partials, int G) {
+                    int next_q, int variant, int pass_nrhs, cudaStream_t st, const double* partials, int G,
+                    const int* nq_dev) {
   if (pc.W != nullptr) {                 // R24: one cooperative kernel over every SM
     const size_t dbl = 4 * (size_t)pc.npad > 2 * (size_t)pc.npad + 264 ? 4 * (size_t)pc.npad : 2 * (size_t)pc.npad + 264;
     const size_t smem = dbl * 8;
@@ -1149,7 +1152,7 @@ int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgS
     if (g > num_sms()) g = num_sms();
     double* pout = const_cast<double*>(passout);
     void* args[] = {(void*)&pc, &v, (void*)&passout, &S, &nrhs, &rule, &next_q, &variant, &pass_nrhs,
-                    (void*)&partials, &G, &pout};
+                    (void*)&partials, &G, &pout, (void*)&nq_dev};
     TLS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_wpcg_step_coop, dim3(g), dim3(kWG), args, smem, st));
     return 0;
   }
@@ -1160,7 +1163,7 @@ int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgS
   const size_t sm = trsv_smem(pc.npad);
   int rc = 0;
   TLS_DISPATCH_UF(pc.u_f, { rc = launch_cluster(k_pcg_step<T>, nrhs, sm, st, pc, v, passout, S, nrhs, rule, next_q,
-                                                variant, pass_nrhs); });
+                                                variant, pass_nrhs, nq_dev); });
   return rc;
 }
 

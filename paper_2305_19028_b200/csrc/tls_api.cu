@@ -490,6 +490,24 @@ __global__ void k_cert_rhs(double* __restrict__ r, int n) {
   }
 }
 
+// The graph-captured PCG loop (NEXT-3): a WHILE conditional node whose body is one PCG
+// iteration (operator pass, [reduction], step) followed by k_loop_cond, which decides on the
+// device whether another iteration runs: j < budget and a right-hand side still active.  No
+// host launch and no host poll per iteration.
+__global__ void k_loop_init(PcgState* S, int budget) {
+  S->loop_j = 0;
+  S->loop_budget = budget;
+  S->loop_nextq = budget > 1 ? 1 : 0;
+}
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, PcgState* S) {
+  const int j = S->loop_j + 1;
+  S->loop_j = j;
+  S->loop_total += 1;
+  S->loop_nextq = j + 1 < S->loop_budget ? 1 : 0;
+  const bool more = j < S->loop_budget && (S->active[0] | S->active[1]);
+  cudaGraphSetConditional(h, more ? 1u : 0u);
+}
+
 __global__ void k_copy(const double* __restrict__ a, double* __restrict__ b, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
 }
@@ -1304,9 +1322,20 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
     TLS_LAUNCH_CHECK();
     return 0;
   };
+  // iterations a graph ran are known on the device only: loop_total (all graph iterations so
+  // far) is read with each state read, and the launches and passes of the loop launched since
+  // the previous read (one loop between reads) are added then
+  int graph_per_iter = 0, graph_pass_per_iter = 0, per_iter_now = 0;
+  int graph_seen = 0;
   auto read_state = [&]() -> int {
     TLS_CUDA_TRY(cudaMemcpyAsync(&hS, w.S, sizeof(PcgState), cudaMemcpyDeviceToHost, cx.st));
     TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+    const int d = hS.loop_total - graph_seen;
+    if (d > 0) {
+      cx.launches += d * graph_per_iter;
+      cx.passes += (int64_t)d * graph_pass_per_iter;
+      graph_seen = hS.loop_total;
+    }
     return 0;
   };
   // PCG iterations j = 0..budget-1 with device-side predication; with a large
@@ -1315,28 +1344,110 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   // paper's A-free Alg. 3 (no pass).  The sigma = 0 bootstrap always uses variant 0.
   // fp32: the RQI's inner solves run their operator pass on the fp32 copy (u_p, R23);
   // the sigma = 0 bootstrap stays fp64 (R5: x_LS to 1e-8).
+  // one PCG iteration's launches (the body of both loop forms); next_q from the host (j) or,
+  // in the captured graph, from the device (nq_dev)
+  auto pcg_iter = [&](int nrhs, int j, int budget, int variant, bool fp32, int rule, const int* nq_dev) -> int {
+    const int pass_rhs = (nrhs == 1 && !is_csr(A)) ? 2 : nrhs;
+    const bool fold = fuse_reduce && variant == 0 && !fp32 && !is_csr(A) && A->m_local > 0;
+    int G = 0;
+    if (fold) {
+      ProfScope ps(TLS_PROF_PASS_OP2, cx.st);
+      TLS_TRY(launch_pass(dense_view(A), PASS_OPERATOR, pass_rhs, w.vec.q, nullptr, w.partials, w.S->active, cx.st, &G));
+      cx.launches += 1;
+      cx.passes += 1;
+    } else if (variant == 0 && fp32) TLS_TRY(run_pass32(cx, A, R, w.vec.q, w, w.S->active));
+    else if (variant == 0) TLS_TRY(run_pass(cx, A, PASS_OPERATOR, pass_rhs, w.vec.q, nullptr, w, w.S->active));
+    {
+      ProfScope ps(TLS_PROF_PCG_STEP, cx.st);
+      TLS_TRY(launch_pcg_step(pc, w.vec, w.passout, w.S, nrhs, rule, j + 1 < budget ? 1 : 0, variant,
+                              pass_rhs, cx.st, fold ? w.partials : nullptr, G, nq_dev));
+    }
+    cx.launches += 1;
+    return 0;
+  };
+  // The graph form (default on one rank without profiling; TLS_PCG_GRAPH=0 disables it): built
+  // once per (shape of the call) and kept; the iteration count is known only on the device, so
+  // the launch and pass counters are settled from S->loop_total after the solve.
+  const char* ge = getenv("TLS_PCG_GRAPH");
+  const bool graph_ok = !(ge && ge[0] == '0') && !prof().on && !comm_active(comm);
+  auto pcg_loop_graph = [&](int nrhs, int budget, int variant, bool fp32, int rule) -> int {
+    // everything the captured kernels bake in: the device pointers and the launch shapes (the
+    // handle's buffers come back from the pool, so repeated factorizations reuse a graph)
+    struct Key { const void* p[12]; int e[10]; };
+    struct Entry { Key k; cudaGraphExec_t ex; int per_iter; };
+    static std::vector<Entry> cache;
+    static bool broken = false;           // capture or instantiation failed once: host loop from now on
+    Key key;
+    std::memset(&key, 0, sizeof(key));
+    const void* ptrs[12] = {A->vals, A->rowptr, ws, pc.Rrow, pc.RTrow, pc.DinvB, pc.DinvF, pc.EB, pc.EF, pc.dinv,
+                            pc.W, R->a32};
+    std::memcpy(key.p, ptrs, sizeof(ptrs));
+    const int ints[10] = {nrhs, variant, fp32 ? 1 : 0, rule, (int)A->n, (int)(A->m_local & 0x7fffffff), fuse_reduce ? 1 : 0,
+                          pc.u_f, (int)A->ld, (int)(ws_bytes >> 20)};
+    std::memcpy(key.e, ints, sizeof(ints));
+    if (broken) return 1;
+    Entry* ent = nullptr;
+    for (auto& e : cache)
+      if (std::memcmp(&e.k, &key, sizeof(Key)) == 0) { ent = &e; break; }
+    k_loop_init<<<1, 1, 0, cx.st>>>(w.S, budget);
+    TLS_LAUNCH_CHECK();
+    cx.launches += 1;
+    if (!ent) {
+      cudaGraph_t g;
+      TLS_CUDA_TRY(cudaGraphCreate(&g, 0));
+      cudaGraphConditionalHandle h;
+      TLS_CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t node;
+      TLS_CUDA_TRY(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      cudaStream_t cap;
+      TLS_CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+      const cudaStream_t saved = cx.st;
+      const int l0 = cx.launches;
+      const int64_t p0 = cx.passes;
+      cx.st = cap;
+      TLS_CUDA_TRY(cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      int rc = pcg_iter(nrhs, 0, budget, variant, fp32, rule, &w.S->loop_nextq);
+      if (rc == 0) k_loop_cond<<<1, 1, 0, cap>>>(h, w.S);
+      per_iter_now = cx.launches - l0 + 1;
+      cudaGraph_t out = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(cap, &out);
+      cx.st = saved;
+      cudaStreamDestroy(cap);
+      cx.launches = l0;
+      cx.passes = p0;
+      cudaGraphExec_t ex = nullptr;
+      const cudaError_t ie = (rc == 0 && ce == cudaSuccess) ? cudaGraphInstantiate(&ex, g, 0) : cudaErrorUnknown;
+      cudaGraphDestroy(g);
+      if (rc || ce != cudaSuccess || ie != cudaSuccess) {
+        cudaGetLastError();               // clear a capture error; the host loop takes over
+        broken = true;
+        return 1;
+      }
+      if (cache.size() >= 16) { cudaGraphExecDestroy(cache.front().ex); cache.erase(cache.begin()); }
+      cache.push_back(Entry{key, ex, per_iter_now});
+      ent = &cache.back();
+    }
+    TLS_CUDA_TRY(cudaGraphLaunch(ent->ex, cx.st));
+    graph_per_iter = ent->per_iter;
+    graph_pass_per_iter = variant == 0 ? 1 : 0;
+    return 0;
+  };
   auto pcg_loop = [&](int nrhs, int budget, int variant, bool fp32, int rule) -> int {
+    if (graph_ok) {
+      const int rc = pcg_loop_graph(nrhs, budget, variant, fp32, rule);
+      if (rc <= 0) return rc;             // rc > 0: no graph (capture unsupported): host loop
+    }
     for (int j = 0; j < budget; ++j) {
       // the 2-RHS dense kernel is faster than the 1-RHS one at the same bytes (measured, see
-      // DESIGN §6): a 1-RHS solve passes its q with the second slot held at zero
-      const int pass_rhs = (nrhs == 1 && !is_csr(A)) ? 2 : nrhs;
-      // NEXT-3: on one rank the explicit-inverse step reduces the dense pass's partials itself
-      // (no separate reduction launch); with ranks the reduced sums go through the all-reduce
-      const bool fold = fuse_reduce && variant == 0 && !fp32 && !is_csr(A) && A->m_local > 0;
-      int G = 0;
-      if (fold) {
-        ProfScope ps(TLS_PROF_PASS_OP2, cx.st);
-        TLS_TRY(launch_pass(dense_view(A), PASS_OPERATOR, pass_rhs, w.vec.q, nullptr, w.partials, w.S->active, cx.st, &G));
-        cx.launches += 1;
-        cx.passes += 1;
-      } else if (variant == 0 && fp32) TLS_TRY(run_pass32(cx, A, R, w.vec.q, w, w.S->active));
-      else if (variant == 0) TLS_TRY(run_pass(cx, A, PASS_OPERATOR, pass_rhs, w.vec.q, nullptr, w, w.S->active));
-      {
-        ProfScope ps(TLS_PROF_PCG_STEP, cx.st);
-        TLS_TRY(launch_pcg_step(pc, w.vec, w.passout, w.S, nrhs, rule, j + 1 < budget ? 1 : 0, variant,
-                                pass_rhs, cx.st, fold ? w.partials : nullptr, G));
-      }
-      cx.launches += 1;
+      // DESIGN §6): a 1-RHS solve passes its q with the second slot held at zero.  NEXT-3: on one
+      // rank the explicit-inverse step reduces the dense pass's partials itself (pcg_iter)
+      TLS_TRY(pcg_iter(nrhs, j, budget, variant, fp32, rule, nullptr));
       if (budget > 16 && (j == 3 || (j % 8) == 7)) {   // first poll early: small bootstraps skip no-op launches
         int act[2] = {0, 0};
         TLS_CUDA_TRY(cudaMemcpyAsync(act, w.S->active, sizeof(act), cudaMemcpyDeviceToHost, cx.st));
@@ -1349,6 +1460,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
 
   Tracer tr(cx.st);
   tr.mark("rqi:start");
+  TLS_CUDA_TRY(cudaMemsetAsync(&w.S->loop_total, 0, sizeof(int), cx.st));
   TLS_CUDA_TRY(cudaMemsetAsync(w.zero, 0, (size_t)n * 8, cx.st));
   TLS_CUDA_TRY(cudaMemsetAsync(w.vec.rhs, 0, 2 * (size_t)n * 8, cx.st));
   // setup (a1): h = A^T b, b^T b from the residual pass at x = 0

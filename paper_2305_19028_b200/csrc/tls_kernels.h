@@ -122,6 +122,9 @@ struct PcgState {
   int active[2], count[2], brk[2], brk_j[2];
   int iter[2];    // iteration index j of the next step, per RHS
   double bb;      // b^T b of the local rows (all-reduced), from the setup pass
+  // the graph-captured PCG loop (NEXT-3, tls_api.cu pcg_loop): iteration j, budget, whether
+  // the step computes the next q, and the iterations run so far (launch accounting)
+  int loop_j, loop_budget, loop_nextq, loop_total;
 };
 struct PcgVecs {  // device, each [2][n] (RHS r at offset r * n)
   double *omega, *s, *p, *q, *rhs;
@@ -139,7 +142,7 @@ int launch_pcg_init(const PrecondDev& pc, int nrhs, PcgVecs v, PcgState* S, cuda
 // first phase from the G per-CTA partial rows of the operator pass (k_reduce_partials' order).
 int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgState* S, int nrhs,
                     int breakdown_rule, int compute_next_q, int variant, int pass_nrhs, cudaStream_t st,
-                    const double* partials = nullptr, int G = 0);
+                    const double* partials = nullptr, int G = 0, const int* nq_dev = nullptr);
 // step record: sigma2, f (stored as rhs0 = -f), g, psi; copies x into rhs1.
 int launch_rqi_eval(const PrecondDev& pc, const double* passout, const double* x, PcgVecs v,
                     PcgState* S, cudaStream_t st);
