@@ -45,6 +45,12 @@ int num_sms() {
   return g_num_sms;
 }
 
+// Programmatic dependent launch of the passes and the PCG steps (NEXT-3; TLS_PDL=0 disables).
+bool pass_pdl() {
+  static const bool on = [] { const char* e = getenv("TLS_PDL"); return !(e && e[0] == '0'); }();
+  return on;
+}
+
 static int rows_per_stage(const DenseView& A) {
   int64_t r = kPassStageBytes / (A.ld * 8);
   return (int)(r < 1 ? 1 : r);
@@ -147,6 +153,10 @@ __global__ void __launch_bounds__(NS * kPassConsumers + 32, 1)
 k_pass(const double* __restrict__ A, int64_t m, int n, int64_t ld, int rps,
        const double* __restrict__ q, const double* __restrict__ b,
        double* __restrict__ partials, int W, const int* __restrict__ active) {
+  // launched with programmatic stream serialization after a PCG step (NEXT-3): everything
+  // below reads the step's results (active, q), so wait for it first; the launch itself (CTA
+  // rasterisation, shared-memory carve-out) overlaps the step's tail.  A no-op otherwise.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (active != nullptr && (active[0] | active[1]) == 0) return;
   extern __shared__ __align__(128) unsigned char smem[];
   double* ring = reinterpret_cast<double*>(smem);
@@ -303,6 +313,20 @@ static int launch_pass_t(const DenseView& A, const double* q, const double* b, d
     TLS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPassSmem));
     attr[fc] = true;
   }
+  if (pass_pdl()) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(NS * kPassConsumers + 32);
+    cfg.dynamicSmemBytes = kPassSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    TLS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A.A, A.m, A.n, A.ld, rows_per_stage(A), q, b, partials, W, active));
+    return 0;
+  }
   kern<<<G, NS * kPassConsumers + 32, kPassSmem, st>>>(A.A, A.m, A.n, A.ld, rows_per_stage(A), q, b, partials,
                                                              W, active);
   TLS_LAUNCH_CHECK();
@@ -420,33 +444,38 @@ __device__ __forceinline__ double fp_weight(int64_t j) {
   const uint64_t h = (uint64_t)(j + 1) * 0x9E3779B97F4A7C15ull;
   return 1.0 + (double)(h >> 40) * 0x1p-24;
 }
-__global__ void k_fingerprint(const double* __restrict__ A, int64_t m, int n, int64_t ld,
-                              const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
-                              double* __restrict__ out) {
-  __shared__ double part[256];
-  const int t = threadIdx.x;
+// One CTA per sampled row (coalesced), the row's weighted sum by a fixed-order block
+// reduction into part[r]; k_fingerprint_fin adds the 256 row sums in order.
+__global__ void __launch_bounds__(256) k_fingerprint(const double* __restrict__ A, int64_t m, int n, int64_t ld,
+                                                     const int64_t* __restrict__ rowptr,
+                                                     const int32_t* __restrict__ colidx, double* __restrict__ part) {
+  __shared__ double red[32];
+  const int r = blockIdx.x, t = threadIdx.x;
   double acc = 0.0;
-  if (m > 0 && (m >= 256 || t < m)) {
-    const int64_t i = m >= 256 ? (int64_t)t * (m - 1) / 255 : t;
+  if (m > 0 && (m >= 256 || r < m)) {
+    const int64_t i = m >= 256 ? (int64_t)r * (m - 1) / 255 : r;
     if (rowptr) {
-      for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k)
+      for (int64_t k = rowptr[i] + t; k < rowptr[i + 1]; k += blockDim.x)
         acc += A[k] * fp_weight(colidx[k]) + (double)colidx[k] * 0x1p-20;
     } else {
-      for (int j = 0; j < n; ++j) acc += A[i * ld + j] * fp_weight(j);
+      for (int j = t; j < n; j += blockDim.x) acc += A[i * ld + j] * fp_weight(j);
     }
   }
-  part[t] = acc;
-  __syncthreads();
-  if (t == 0) {
+  acc = block_sum(acc, red);
+  if (t == 0) part[r] = acc;
+}
+__global__ void k_fingerprint_fin(const double* __restrict__ part, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
     double s = 0.0;
     for (int u = 0; u < 256; ++u) s += part[u];
     out[0] = s;
   }
 }
 
-int launch_fingerprint(const DenseView* dv, const CsrView* cv, double* out, cudaStream_t st) {
-  if (cv) k_fingerprint<<<1, 256, 0, st>>>(cv->vals, cv->m, cv->n, 0, cv->rowptr, cv->colidx, out);
-  else k_fingerprint<<<1, 256, 0, st>>>(dv->A, dv->m, dv->n, dv->ld, nullptr, nullptr, out);
+int launch_fingerprint(const DenseView* dv, const CsrView* cv, double* out, double* scratch, cudaStream_t st) {
+  if (cv) k_fingerprint<<<256, 256, 0, st>>>(cv->vals, cv->m, cv->n, 0, cv->rowptr, cv->colidx, scratch);
+  else k_fingerprint<<<256, 256, 0, st>>>(dv->A, dv->m, dv->n, dv->ld, nullptr, nullptr, scratch);
+  k_fingerprint_fin<<<1, 32, 0, st>>>(scratch, out);
   TLS_LAUNCH_CHECK();
   return 0;
 }

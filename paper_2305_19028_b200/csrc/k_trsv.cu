@@ -518,6 +518,10 @@ __global__ void __launch_bounds__(kWG) k_wpcg_step_coop(PrecondDev pc, PcgVecs v
                                                        PcgState* __restrict__ S, int nrhs, int rule, int next_q,
                                                        int variant, int pass_nrhs, const double* __restrict__ partials,
                                                        int G, double* __restrict__ pout, const int* __restrict__ nq_dev) {
+  // programmatic dependent launch (NEXT-3): wait for the operator pass, release the next pass
+  // at once (it waits for this grid's completion before reading anything)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (nq_dev) next_q = *nq_dev;         // graph-captured loop (NEXT-3): decided on the device
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -1151,9 +1155,20 @@ int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgS
     int g = (pc.n + kWG / 32 - 1) / (kWG / 32);
     if (g > num_sms()) g = num_sms();
     double* pout = const_cast<double*>(passout);
-    void* args[] = {(void*)&pc, &v, (void*)&passout, &S, &nrhs, &rule, &next_q, &variant, &pass_nrhs,
-                    (void*)&partials, &G, &pout, (void*)&nq_dev};
-    TLS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_wpcg_step_coop, dim3(g), dim3(kWG), args, smem, st));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(kWG);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pass_pdl() ? 2 : 1;
+    TLS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_wpcg_step_coop, pc, v, passout, S, nrhs, rule, next_q, variant, pass_nrhs,
+                                    partials, G, pout, nq_dev));
     return 0;
   }
   if (partials != nullptr) {

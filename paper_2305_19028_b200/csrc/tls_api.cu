@@ -375,7 +375,7 @@ size_t carve(const tls_matrix_t* A, void* ws, size_t bytes, Work& w, bool factor
   const bool csr = is_csr(A);
   Carver c{static_cast<char*>(ws), ws ? bytes : 0};
   const size_t npart = csr ? csr_pass_partials_doubles() : pass_partials_doubles(dense_view(A));
-  w.partials = c.take<double>(npart);
+  w.partials = c.take<double>(npart > 256 ? npart : 256);   // also the fingerprint's 256 row sums
   w.passout = c.take<double>(2 * (size_t)n + 2);
   w.colstats = c.take<double>(2 * (size_t)n);
   w.vec.omega = c.take<double>(2 * (size_t)n);
@@ -560,16 +560,16 @@ int run_pass(Ctx& cx, const tls_matrix_t* A, int mode, int nrhs, const double* q
   return 0;
 }
 
-// Sampled content checksum of the local block into *dev (k_fingerprint).
-int run_fingerprint(Ctx& cx, const tls_matrix_t* A, double* dev) {
+// Sampled content checksum of the local block into *dev (k_fingerprint); scratch: 256 doubles.
+int run_fingerprint(Ctx& cx, const tls_matrix_t* A, double* dev, double* scratch) {
   if (is_csr(A)) {
     const CsrView cv = csr_view(A);
-    TLS_TRY(launch_fingerprint(nullptr, &cv, dev, cx.st));
+    TLS_TRY(launch_fingerprint(nullptr, &cv, dev, scratch, cx.st));
   } else {
     const DenseView dv = dense_view(A);
-    TLS_TRY(launch_fingerprint(&dv, nullptr, dev, cx.st));
+    TLS_TRY(launch_fingerprint(&dv, nullptr, dev, scratch, cx.st));
   }
-  cx.launches += 1;
+  cx.launches += 2;
   return 0;
 }
 
@@ -964,7 +964,7 @@ int tls_factor_precond(const tls_matrix_t* A, int32_t u_f, const tls_rqi_opts_t*
   int rc = launch_pack_R(w.G, n, 0, h->dev, &w.flags[3], cx.st, &cx.launches);
   cx.launches += 1;  // k_fill_scaling
   if (rc) { tls_precond_destroy(h); return rc; }
-  rc = run_fingerprint(cx, A, normA2 + 1);
+  rc = run_fingerprint(cx, A, normA2 + 1, w.partials);
   if (rc) { tls_precond_destroy(h); return rc; }
   tr.mark("pack");
   int hflags[8];
@@ -1138,7 +1138,7 @@ int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, v
   int rc = launch_pack_R(q.G, n, 0, h->dev, &w.flags[3], cx.st, &cx.launches);
   cx.launches += 1;
   if (rc) { tls_precond_destroy(h); return rc; }
-  rc = run_fingerprint(cx, A, normA2 + 1);
+  rc = run_fingerprint(cx, A, normA2 + 1, w.partials);
   if (rc) { tls_precond_destroy(h); return rc; }
   int hflags[8], hq[4];
   double hnorm[2] = {0.0, 0.0};
@@ -1295,7 +1295,7 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   const int n = (int)A->n;
   // the handle's fingerprint: this rank's block must have the content it was factored from
   double content = 0.0;
-  TLS_TRY(run_fingerprint(cx, A, w.d_tmp));
+  TLS_TRY(run_fingerprint(cx, A, w.d_tmp, w.partials));
   TLS_CUDA_TRY(cudaMemcpyAsync(&content, w.d_tmp, sizeof(double), cudaMemcpyDeviceToHost, cx.st));
   TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
   if (R->m_global >= 0 && !(content == R->content)) {
@@ -1717,7 +1717,7 @@ int tls_pass_fp32(const tls_matrix_t* A, tls_precond_t R, const double* q, doubl
   Ctx cx{static_cast<cudaStream_t>(stream), nullptr};
   const int n = (int)A->n;
   double content = 0.0;
-  TLS_TRY(run_fingerprint(cx, A, w.d_tmp));
+  TLS_TRY(run_fingerprint(cx, A, w.d_tmp, w.partials));
   TLS_CUDA_TRY(cudaMemcpyAsync(&content, w.d_tmp, sizeof(double), cudaMemcpyDeviceToHost, cx.st));
   TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
   TLS_TRY(ensure_a32(cx, A, R, content));

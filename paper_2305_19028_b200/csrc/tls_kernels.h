@@ -9,6 +9,7 @@ namespace tls {
 constexpr int kMaxDenseN = 4096;   // register-resident column ownership in k_pass (CPT <= 8)
 
 int num_sms();
+bool pass_pdl();   // programmatic dependent launch of passes and PCG steps (TLS_PDL=0: off)
 
 // ---- streaming passes over A (k_pass.cu) ---------------------------------------------
 enum PassMode { PASS_OPERATOR = 0, PASS_RESIDUAL = 1, PASS_COLSTATS = 2 };
@@ -52,8 +53,8 @@ struct CsrView {
   int n;
   int64_t nnz;
 };
-// sampled content checksum of a local block (k_pass.cu): 256 evenly spread rows
-int launch_fingerprint(const DenseView* dv, const CsrView* cv, double* out, cudaStream_t st);
+// sampled content checksum of a local block (k_pass.cu): 256 evenly spread rows; scratch: 256 doubles
+int launch_fingerprint(const DenseView* dv, const CsrView* cv, double* out, double* scratch, cudaStream_t st);
 
 struct CscView {          // transpose of a CsrView, rows ascending within every column
   int64_t* colptr;        // n + 1

@@ -730,3 +730,23 @@ def test_fingerprint_refuses_a_rewritten_A(T):
     q32 = q.cpu().numpy().astype(np.float32).astype(np.float64)
     ref = A2.T @ (A2 @ q32[0])
     assert _rel(v2[0].cpu().numpy(), ref) < 1e-5 and _rel(v1[0].cpu().numpy(), ref) > 1e-5
+
+
+@pytest.mark.parametrize("name,fmt,pa", [("cfg2w", "bf16", 1), ("cfg2w", "fp16", 2), ("cfg1", "fp16", 1)])
+def test_graph_loop_equals_host_loop(T, monkeypatch, name, fmt, pa):
+    """NEXT-3: the PCG loop captured as a CUDA graph (a WHILE conditional node whose body is one
+    iteration; the trip decision is made on the device by k_loop_cond) runs the same kernels in
+    the same order as the host loop: bit-identical x, sigma, counts and sigma^2 trace."""
+    P = tlsgen.config(name)
+    M = T.matrix(dev(P.A))
+    b = dev(P.b)
+    rc, R, _ = T.tls_factor_precond(M, fmt)
+    o = T.tls_rqi_opts_default(precond_apply=pa)
+    out = {}
+    for g in ("0", "1"):
+        monkeypatch.setenv("TLS_PCG_GRAPH", g)
+        rc, x, sig, info = T.tls_rqi_pcgtls(M, b, R, opts=o)
+        out[g] = (x.cpu().numpy().view(np.uint64).copy(), sig, info)
+    assert np.array_equal(out["0"][0], out["1"][0]) and out["0"][1] == out["1"][1]
+    for k in ("status", "termination", "rqi_iters", "boot_iters", "pcg_iters", "sigma2_trace", "passes"):
+        assert out["0"][2][k] == out["1"][2][k], k

@@ -122,5 +122,6 @@ def test_fused_gram_bitwise_reproducible(T, monkeypatch):
             ref = _bits(G)
         assert np.array_equal(_bits(G), ref)
     monkeypatch.setenv("TLS_GRAM_FUSED", "0")
+    monkeypatch.setenv("TLS_GRAM_SEGS", "1")          # the unsegmented two-kernel path: same chunking
     rc, G0 = T.tls_gram(M, "fp16", d, 64, ws=ws)
     assert np.array_equal(_bits(G0), ref)            # and equal to the two-kernel path

@@ -51,7 +51,8 @@ def one(mode, m, n):
     it = info["boot_iters"]
     pass_us = 1e3 * prof["pass_op2"]["ms"] / max(1, prof["pass_op2"]["count"])
     per_iter = 1e3 * total_ms / max(1, it)
-    return {"mode": mode, "graph": os.environ.get("TLS_PCG_GRAPH", "1") != "0", "m": m, "n": n, "boot_iters": it,
+    return {"mode": mode, "graph": os.environ.get("TLS_PCG_GRAPH", "1") != "0", "pdl": os.environ.get("TLS_PDL", "1") != "0",
+            "m": m, "n": n, "boot_iters": it,
             "solve_ms": total_ms, "launches": info["launches"], "pass_us_per_iter": pass_us,
             "step_us_per_iter": 1e3 * prof["pcg_step"]["ms"] / max(1, prof["pcg_step"]["count"]),
             "reduce_us_per_iter": 1e3 * prof["reduce"]["ms"] / max(1, prof["reduce"]["count"]),
@@ -67,8 +68,10 @@ def main():
     if args.mode:
         print(json.dumps(one(args.mode, args.m, args.n)))
         return
-    for mode, env in (("subst", {"TLS_PCG_GRAPH": "0"}), ("subst", {}), ("winv_sep", {"TLS_FUSE_REDUCE": "0", "TLS_PCG_GRAPH": "0"}),
-                      ("winv_fused", {"TLS_PCG_GRAPH": "0"}), ("winv_fused", {})):
+    for mode, env in (("subst", {"TLS_PCG_GRAPH": "0", "TLS_PDL": "0"}), ("subst", {"TLS_PDL": "0"}), ("subst", {}),
+                      ("winv_sep", {"TLS_FUSE_REDUCE": "0", "TLS_PCG_GRAPH": "0", "TLS_PDL": "0"}),
+                      ("winv_fused", {"TLS_PCG_GRAPH": "0", "TLS_PDL": "0"}), ("winv_fused", {"TLS_PDL": "0"}),
+                      ("winv_fused", {})):
         e = dict(os.environ, **env)
         out = subprocess.run([sys.executable, __file__, "--mode", mode, "--m", str(args.m), "--n", str(args.n)],
                              env=e, capture_output=True, text=True)
