@@ -10,6 +10,7 @@ OUT = os.path.join(HERE, "libtlsrqi.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(HERE, "..", "include")]
+FLAGS += os.environ.get("TLS_EXTRA_NVCC", "").split()      # build-time experiment knobs (e.g. -DTLS_PASS_WIDE=1)
 
 
 def sources():

@@ -748,5 +748,8 @@ def test_graph_loop_equals_host_loop(T, monkeypatch, name, fmt, pa):
         rc, x, sig, info = T.tls_rqi_pcgtls(M, b, R, opts=o)
         out[g] = (x.cpu().numpy().view(np.uint64).copy(), sig, info)
     assert np.array_equal(out["0"][0], out["1"][0]) and out["0"][1] == out["1"][1]
-    for k in ("status", "termination", "rqi_iters", "boot_iters", "pcg_iters", "sigma2_trace", "passes"):
+    for k in ("status", "termination", "rqi_iters", "boot_iters", "pcg_iters", "sigma2_trace"):
         assert out["0"][2][k] == out["1"][2][k], k
+    # passes: the host loop counts every launched pass, also those an inactive PCG makes a no-op;
+    # the graph counts the iterations it ran (the device stops the loop)
+    assert out["1"][2]["passes"] <= out["0"][2]["passes"]
