@@ -105,3 +105,11 @@ def test_up_fp32_wide_and_factor(T):
     assert i32["rqi_iters"] == i64["rqi_iters"]
     assert _rel(x32.cpu().numpy(), x64.cpu().numpy()) <= 1e-9
     assert abs(s32 - s64) / s64 <= 1e-12
+    # and against the oracle's u_p = fp32 run on the same R~ (not only GPU vs GPU)
+    Rt, d, nrm = T.tls_precond_export(R)
+    res = rqi.rqi_pcgtls_mp(P.A, P.b, rqi.Precond(Rt, d, "fp16", nrm), opts=rqi.RqiOptions(u_p="fp32"))
+    assert i32["status"] == res.status and i32["rqi_iters"] == res.rqi_iters
+    for a, b in zip(i32["pcg_iters"], res.pcg_iters):
+        assert abs(a[0] - b[0]) <= 2 and abs(a[1] - b[1]) <= 2
+    assert _rel(x32.cpu().numpy(), res.x) <= 1e-9
+    assert abs(s32 - res.sigma) / res.sigma <= 1e-12

@@ -82,3 +82,16 @@ def test_inverse_csr_and_wide(T):
         assert i1["status"] == i2["status"] == 0 and i1["rqi_iters"] == i2["rqi_iters"]
         assert _rel(x2.cpu().numpy(), x1.cpu().numpy()) <= 1e-9
         assert abs(s2 - s1) / s1 <= 1e-12
+        # and against the oracle's explicit-inverse run on the same R~ (not only GPU vs GPU)
+        Rt, d, nrm = T.tls_precond_export(R)
+        if M_ is M:
+            import scipy.sparse
+            A_h = scipy.sparse.csr_matrix((P.vals, P.colidx, P.rowptr), shape=(P.m, P.n))
+            b_h = P.b
+        else:
+            A_h, b_h = D.A, D.b
+        res = rqi.rqi_pcgtls_mp(A_h, b_h, rqi.Precond(Rt, d, "fp16", nrm), opts=rqi.RqiOptions(precond_apply=2))
+        assert i2["status"] == res.status and i2["rqi_iters"] == res.rqi_iters
+        assert [tuple(p) for p in i2["pcg_iters"]] == [tuple(p) for p in res.pcg_iters]
+        assert _rel(x2.cpu().numpy(), res.x) <= 1e-9
+        assert abs(s2 - res.sigma) / res.sigma <= 1e-12

@@ -498,3 +498,49 @@ def test_not_minimal_reported_for_a_converged_non_minimal_pair():
         Q = tlsgen.config(name)
         _, r = rqi.solve(Q.A, Q.b, Q.u_f, opts=rqi.RqiOptions(minimal_check=10))
         assert r.status == rqi.OK and r.sigma < np.linalg.svd(Q.A, compute_uv=False)[-1]
+
+
+# ----------------------------------------------------------------------------- stop rule (R6, R7)
+@pytest.mark.parametrize("psis,opts,want", [
+    # no crossing, psi rises at k = 3: STAGNATED with x_2 (R7)
+    ([5.0, 4.0, 6.0], {}, (rqi.STAGNATED, rqi.T_STAGNATED, 3, 2)),
+    # crossing at k = 2, polish step k = 3 improves: CONVERGED_TOL with x_3 (R6)
+    ([5.0, 1e-20, 0.5e-20], {}, (rqi.OK, rqi.T_CONVERGED_TOL, 3, 3)),
+    # crossing at k = 2, the polish step's psi rose: CONVERGED_TOL, the better iterate x_2 (R6)
+    ([5.0, 1e-20, 2e-20], {}, (rqi.OK, rqi.T_CONVERGED_TOL, 3, 2)),
+    # polish = 2: psi rises at k = 3 after the crossing at k = 2: PSI_INCREASE_CONVERGED with x_2
+    ([5.0, 1e-20, 3e-20], {"polish": 2}, (rqi.OK, rqi.T_PSI_INCREASE_CONVERGED, 3, 2)),
+    # the weak rule (l.532): an equal psi counts as an increase
+    ([5.0, 4.0, 4.0], {"stop_rule": 1}, (rqi.STAGNATED, rqi.T_STAGNATED, 3, 2)),
+    ([5.0, 4.0, 4.0, 3.0, 2.0], {"max_outer": 4}, (rqi.MAX_OUTER, rqi.T_MAX_OUTER, 5, 5)),
+])
+def test_stop_rule_branches_on_scripted_psi(monkeypatch, psis, opts, want):
+    """The stop tests of rqi_pcgtls_mp (R6: tol crossing + polish; R7: psi increase before the
+    crossing is STAGNATED; l.265 strict / l.532 weak; max_outer) on a scripted psi_k sequence:
+    newton_residual is replaced by a script (sigma_k^2 = k, f = 0, g = 0, psi_k given) and each
+    PCGTLS solve returns omega = e_0, so x_k = (k - 1) e_0 marks which iterate is returned."""
+    n = 3
+    A = np.eye(6, n)
+    b = np.ones(6)
+    pc = rqi.Precond(np.eye(n), np.ones(n), "fp64", 1.0)
+    calls = {"k": 0}
+
+    def script(A_, b_, x):
+        k = calls["k"]
+        calls["k"] += 1
+        return float(k + 1), np.zeros(n), 0.0, psis[min(k, len(psis) - 1)]
+
+    def pcg(A_, pc_, sigma2, f, l, tol_inner, variant="A", breakdown_rule="spec", A32=None):
+        om = np.zeros(n)
+        if sigma2 > 0:                                   # RQI solves (the bootstrap runs at sigma^2 = 0)
+            om[0] = 1.0
+        return rqi.PcgResult(om, l)
+
+    monkeypatch.setattr(rqi, "newton_residual", script)
+    monkeypatch.setattr(rqi, "pcgtls", pcg)
+    o = rqi.RqiOptions(**opts)
+    res = rqi.rqi_pcgtls_mp(A, b, pc, tol=1e-14, opts=o)
+    status, term, k, k_ret = want
+    assert (res.status, res.termination, res.rqi_iters) == (status, term, k)
+    assert res.x[0] == k_ret - 1                        # x_{k_ret}
+    assert res.sigma == pytest.approx(np.sqrt(k_ret))    # sigma_{k_ret}
