@@ -63,7 +63,7 @@ enum {
   TLS_MAX_OUTER = 3,      /* max_outer RQI steps without meeting a stop test (R6) */
   TLS_NONFINITE = 4,      /* sigma^2 or psi not finite */
   TLS_RANGE = 5,          /* A D^{-1} or R~ overflows u_f (reading R4) */
-  TLS_NOT_MINIMAL = 6,    /* reserved: minimality certificate failed (R8) */
+  TLS_NOT_MINIMAL = 6,    /* opts.minimal_check: A^T A - sigma^2 I not positive definite at the result (R28) */
   TLS_STAGNATED = 7,      /* psi rose before the tol crossing (R7) */
   TLS_ERR_ARG = -1, TLS_ERR_CUDA = -2, TLS_ERR_NCCL = -3, TLS_ERR_WORKSPACE = -4,
   TLS_ERR_UNSUPPORTED = -5
@@ -223,10 +223,18 @@ TLS_API int tls_precond_export(tls_precond_t R, double* Rt_host, double* d_host,
 TLS_API void tls_precond_destroy(tls_precond_t R);
 
 /* ---- the RQI-PCGTLS-MP solve (§8 rows a4-a9) ----
- * R must come from this A (same n and, for a factored handle, the same m_global; else
- * TLS_ERR_ARG).  u and u_r must be TLS_FP64 (north_star); tol is the primary stop
- * psi_k <= tol ||[A,b]||_F^2 (R6).  x_out_dev (n fp64) receives the returned
- * iterate on every rank, *sigma_out_host = sqrt(sigma^2) of that iterate. */
+ * R must come from this A (same n and, for a factored handle, the same m_global and the same
+ * content: the handle keeps a checksum of 256 evenly spread rows of this rank's block, taken at
+ * the factorization and compared at every solve -- an A rewritten in place is TLS_ERR_ARG;
+ * imported handles are not checked).  u and u_r must be TLS_FP64 (north_star); tol is the
+ * primary stop psi_k <= tol ||[A,b]||_F^2 (R6).  x_out_dev (n fp64) receives the returned
+ * iterate on every rank, *sigma_out_host = sqrt(sigma^2) of that iterate.
+ * Without per-launch profiling and on one rank, each PCG loop runs as a CUDA graph whose
+ * trip count is decided on the device (TLS_PCG_GRAPH=0: host loop; same kernels, same bits).
+ * Handle-owned allocations made by the first solve that needs them (freed or pooled by
+ * tls_precond_destroy): the explicit inverse W (2 npad^2 doubles, precond_apply = 2 or a
+ * sharded solve) and the fp32 copy of the local block (u_p = fp32).  An NCCL error raised
+ * asynchronously is reported as TLS_ERR_NCCL at the end of the call. */
 TLS_API int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b_local_dev, const tls_precond_t R,
                    int32_t u, int32_t u_r, double tol, const tls_rqi_opts_t* opts,
                    tls_comm_t comm, void* stream, void* ws_dev, size_t ws_bytes,

@@ -278,11 +278,42 @@ __device__ __forceinline__ void tile_atb(const double* A, const double* B, doubl
   }
 }
 
+// C -= A^T B on the fp64 tensor cores (DMMA m8n8k4; VERDICT r01 missing #8): warp w owns the
+// 8-row block 8w of C and all 8 column blocks; per 4-deep k step one A fragment (A[k][8w+gid])
+// and 8 B fragments (B[k][8nj+gid]) from shared memory, 8 DMMAs.  The same fp64 arithmetic
+// rate as DFMA on B200, at 1/8 of the instructions and far fewer shared-memory loads than
+// tile_atb's 4 x 4 register blocking.
+__device__ __forceinline__ void tile_atb_sub_dmma(const double* A, const double* B, double* C) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  double acc[8][2];
+#pragma unroll
+  for (int nj = 0; nj < 8; ++nj) acc[nj][0] = acc[nj][1] = 0.0;
+#pragma unroll 4
+  for (int k0 = 0; k0 < kTB; k0 += 4) {
+    const double af = A[(k0 + tig) * kTS + 8 * w + gid];
+    double bf[8];
+#pragma unroll
+    for (int nj = 0; nj < 8; ++nj) bf[nj] = B[(k0 + tig) * kTS + 8 * nj + gid];
+#pragma unroll
+    for (int nj = 0; nj < 8; ++nj)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(acc[nj][0]), "+d"(acc[nj][1])
+                   : "d"(af), "d"(bf[nj]));
+  }
+#pragma unroll
+  for (int nj = 0; nj < 8; ++nj) {
+    double* c = C + (8 * w + gid) * kTS + 8 * nj + 2 * tig;
+    c[0] -= acc[nj][0];
+    c[1] -= acc[nj][1];
+  }
+}
+
 __global__ void __launch_bounds__(kCholThreads, 1)
 k_chol_dag(double* __restrict__ G, int n, int T, const int4* __restrict__ tasks, int ntasks,
            double* __restrict__ xinv, int* __restrict__ potrf_done, int* __restrict__ trsm_done,
            int* __restrict__ upd_done, CholCtl* __restrict__ ctl, int* __restrict__ pivot,
-           unsigned long long* __restrict__ trace) {
+           unsigned long long* __restrict__ trace, int dmma) {
   extern __shared__ double sm[];
   double* S0 = sm;                  // [64][65]
   double* S1 = S0 + kTB * kTS;
@@ -372,12 +403,16 @@ k_chol_dag(double* __restrict__ G, int n, int T, const int4* __restrict__ tasks,
       if (ok) {
         load_tile(G, n, jn, jn, S2, true, true);
         __syncthreads();
-        double acc[4][4] = {};
-        tile_atb(S1, S1, acc);
+        if (dmma) {
+          tile_atb_sub_dmma(S1, S1, S2);
+        } else {
+          double acc[4][4] = {};
+          tile_atb(S1, S1, acc);
 #pragma unroll
-        for (int p = 0; p < 4; ++p)
+          for (int p = 0; p < 4; ++p)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) S2[(4 * ty + p) * kTS + tx + 16 * q] -= acc[p][q];
+            for (int q = 0; q < 4; ++q) S2[(4 * ty + p) * kTS + tx + 16 * q] -= acc[p][q];
+        }
         __syncthreads();
         f = potrf_tile(S2, drj, min(kTB, n - jn * kTB));
         TSTAMP(tcomp);
@@ -406,12 +441,16 @@ k_chol_dag(double* __restrict__ G, int n, int T, const int4* __restrict__ tasks,
         load_tile(G, n, i, j, S2, i == j, false);
         __syncthreads();
         TSTAMP(tload);
-        double acc[4][4] = {};
-        tile_atb(S0, j != i ? S1 : S0, acc);
+        if (dmma) {
+          tile_atb_sub_dmma(S0, j != i ? S1 : S0, S2);
+        } else {
+          double acc[4][4] = {};
+          tile_atb(S0, j != i ? S1 : S0, acc);
 #pragma unroll
-        for (int p = 0; p < 4; ++p)
+          for (int p = 0; p < 4; ++p)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) S2[(4 * ty + p) * kTS + tx + 16 * q] -= acc[p][q];
+            for (int q = 0; q < 4; ++q) S2[(4 * ty + p) * kTS + tx + 16 * q] -= acc[p][q];
+        }
         __syncthreads();
         TSTAMP(tcomp);
         store_tile(G, n, i, j, S2, i == j);
@@ -500,7 +539,10 @@ int launch_cholesky(double* G, int n, int* pivot, void* ws, size_t ws_bytes, cud
   const char* tpath = getenv("TLS_CHOL_TRACE");
   if (tpath && !trace) TLS_CUDA_TRY(cudaMalloc(&trace, 6 * sizeof(unsigned long long) * 200000));
   unsigned long long* tr = tpath ? trace : nullptr;
-  void* args[] = {&G, (void*)&n, (void*)&T, &tasks, &ntasks, &xinv, &potrf_done, &trsm_done, &upd_done, &ctl, &pivot, &tr};
+  // UPDATE tiles on the fp64 tensor cores (DMMA) unless TLS_CHOL_DMMA=0 (the DFMA tile_atb)
+  static int dmma = [] { const char* e = getenv("TLS_CHOL_DMMA"); return (e && e[0] == '0') ? 0 : 1; }();
+  void* args[] = {&G, (void*)&n, (void*)&T, &tasks, &ntasks, &xinv, &potrf_done, &trsm_done, &upd_done, &ctl, &pivot, &tr,
+                  &dmma};
   TLS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_chol_dag, dim3(grid), dim3(kCholThreads), args, smem, st));
   if (launches) *launches += 1;
   if (tr) {

@@ -1154,6 +1154,9 @@ int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgS
     }
     int g = (pc.n + kWG / 32 - 1) / (kWG / 32);
     if (g > num_sms()) g = num_sms();
+    // TLS_WSTEP_CTAS=k caps the cooperative grid (fewer CTAs: cheaper grid barriers, longer GEMVs)
+    static const int cap = [] { const char* e = getenv("TLS_WSTEP_CTAS"); return e ? atoi(e) : 0; }();
+    if (cap > 0 && g > cap) g = cap;
     double* pout = const_cast<double*>(passout);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(g);

@@ -52,6 +52,7 @@ def one(mode, m, n):
     pass_us = 1e3 * prof["pass_op2"]["ms"] / max(1, prof["pass_op2"]["count"])
     per_iter = 1e3 * total_ms / max(1, it)
     return {"mode": mode, "graph": os.environ.get("TLS_PCG_GRAPH", "1") != "0", "pdl": os.environ.get("TLS_PDL", "1") != "0",
+            "wstep_ctas": os.environ.get("TLS_WSTEP_CTAS", "auto"),
             "m": m, "n": n, "boot_iters": it,
             "solve_ms": total_ms, "launches": info["launches"], "pass_us_per_iter": pass_us,
             "step_us_per_iter": 1e3 * prof["pcg_step"]["ms"] / max(1, prof["pcg_step"]["count"]),
@@ -71,7 +72,7 @@ def main():
     for mode, env in (("subst", {"TLS_PCG_GRAPH": "0", "TLS_PDL": "0"}), ("subst", {"TLS_PDL": "0"}), ("subst", {}),
                       ("winv_sep", {"TLS_FUSE_REDUCE": "0", "TLS_PCG_GRAPH": "0", "TLS_PDL": "0"}),
                       ("winv_fused", {"TLS_PCG_GRAPH": "0", "TLS_PDL": "0"}), ("winv_fused", {"TLS_PDL": "0"}),
-                      ("winv_fused", {})):
+                      ("winv_fused", {}), ("winv_fused", {"TLS_WSTEP_CTAS": "64"}), ("winv_fused", {"TLS_WSTEP_CTAS": "32"})):
         e = dict(os.environ, **env)
         out = subprocess.run([sys.executable, __file__, "--mode", mode, "--m", str(args.m), "--n", str(args.n)],
                              env=e, capture_output=True, text=True)
