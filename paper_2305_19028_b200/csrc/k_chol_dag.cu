@@ -539,8 +539,12 @@ int launch_cholesky(double* G, int n, int* pivot, void* ws, size_t ws_bytes, cud
   const char* tpath = getenv("TLS_CHOL_TRACE");
   if (tpath && !trace) TLS_CUDA_TRY(cudaMalloc(&trace, 6 * sizeof(unsigned long long) * 200000));
   unsigned long long* tr = tpath ? trace : nullptr;
-  // UPDATE tiles on the fp64 tensor cores (DMMA) unless TLS_CHOL_DMMA=0 (the DFMA tile_atb)
-  static int dmma = [] { const char* e = getenv("TLS_CHOL_DMMA"); return (e && e[0] == '0') ? 0 : 1; }();
+  // TLS_CHOL_DMMA=1: UPDATE tiles on the fp64 tensor cores (tile_atb_sub_dmma).  Measured
+  // (tools/time_chol.py, profiles/r02_chol_dmma.log): 0.892 vs 0.882 ms at n = 1024, 1.356 vs
+  // 1.310 ms at n = 2000 -- the factorization's critical path is the POTRF of the diagonal
+  // tiles, not the updates, and the DMMA fragments' shared-memory pattern costs more than the
+  // DFMA register blocking saves, so the DFMA tile_atb stays the default
+  static int dmma = [] { const char* e = getenv("TLS_CHOL_DMMA"); return (e && e[0] == '1') ? 1 : 0; }();
   void* args[] = {&G, (void*)&n, (void*)&T, &tasks, &ntasks, &xinv, &potrf_done, &trsm_done, &upd_done, &ctl, &pivot, &tr,
                   &dmma};
   TLS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_chol_dag, dim3(grid), dim3(kCholThreads), args, smem, st));
