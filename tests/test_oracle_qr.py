@@ -294,3 +294,116 @@ def test_norm_scaling_is_the_papers_D_rounded():
         B[:, 1] = [2.0 ** t, 2.0 ** t]                # c = 2^(2t+1) exactly
         d2, _ = norm_scaling(B)
         assert d2[1] == 2.0 ** (t + 1)
+
+
+# ---------------------------------------------------------------- blocked QR (R29, NEXT-2)
+def test_blocked_fp64_equals_lapack_and_b_ge_n_is_unblocked():
+    """R29's compact-WY trailing update is the unblocked factorization in exact arithmetic: in
+    fp64 it gives LAPACK's R (up to row signs) for panel widths that divide n and that do not,
+    and with b >= n it is householder_qr_r bit for bit (no trailing update happens)."""
+    from oracle.qr import householder_qr_r_blocked
+    rng = np.random.default_rng(31)
+    A = rng.standard_normal((120, 21))
+    R0 = np.linalg.qr(A, mode="r")
+    R0 = R0 * np.where(np.diag(R0) < 0, -1.0, 1.0)[:, None]
+    for b in (2, 5, 7, 16):
+        assert np.max(np.abs(householder_qr_r_blocked(A, "fp64", b) - R0)) <= 1e-13 * np.max(np.abs(R0))
+    for fmt in ("fp16", "bf16"):
+        assert np.array_equal(householder_qr_r_blocked(A, fmt, 21), householder_qr_r(A, fmt))
+        assert np.array_equal(householder_qr_r_blocked(A, fmt, 64), householder_qr_r(A, fmt))
+
+
+def _blocked_exact(A, fmt, b):
+    """R29 in exact rational arithmetic: the panel steps as _householder_qr_r_exact, the fp32
+    chunk sums and the fp32 V Y sums rounded to fp32 (exact RNE of rationals) term by term."""
+    rd = lambda x: _rd_frac(Fraction(x), fmt)
+    r32 = lambda x: _rd_frac(Fraction(x), "fp32")
+    m, n = len(A), len(A[0])
+    W = [[rd(Fraction(float(A[i][j]))) for j in range(n)] for i in range(m)]
+    for c0 in range(0, n, b):
+        c1 = min(n, c0 + b)
+        nb = c1 - c0
+        V = [[Fraction(0)] * nb for _ in range(m - c0)]
+        beta = [Fraction(0)] * nb
+        for j in range(c0, c1):
+            x = [W[i][j] for i in range(j, m)]
+            sigma = _rd_sqrt_frac(rd(sum(t * t for t in x)), fmt)
+            alpha = -sigma if x[0] >= 0 else sigma
+            v = list(x)
+            v[0] = rd(x[0] - alpha)
+            bt = rd(Fraction(2) / rd(sum(t * t for t in v)))
+            for k in range(j + 1, c1):
+                wk = rd(bt * rd(sum(v[i - j] * W[i][k] for i in range(j, m))))
+                for i in range(j, m):
+                    W[i][k] = rd(W[i][k] - rd(v[i - j] * wk))
+            W[j][j] = alpha
+            for i in range(j + 1, m):
+                W[i][j] = Fraction(0)
+            for i in range(j, m):
+                V[i - c0][j - c0] = v[i - j]
+            beta[j - c0] = bt
+        if c1 == n:
+            break
+        def chunk_dot(a_col, b_col):              # fp32 row-order sums per 64-row chunk, fp64 across
+            tot = Fraction(0)
+            for s0 in range(0, m - c0, 64):
+                acc = Fraction(0)
+                for i in range(s0, min(m - c0, s0 + 64)):
+                    acc = r32(acc + a_col(i) * b_col(i))
+                tot = tot + acc                   # fp64 sums of a few fp32 values: exact here
+            return tot
+        VtC = [[chunk_dot(lambda i: V[i][p], lambda i: W[c0 + i][k]) for k in range(c1, n)] for p in range(nb)]
+        VtV = [[chunk_dot(lambda i: V[i][p], lambda i: V[i][q]) for q in range(nb)] for p in range(nb)]
+        T = [[Fraction(0)] * nb for _ in range(nb)]
+        for j in range(nb):
+            T[j][j] = beta[j]
+            for i in range(j):
+                T[i][j] = -beta[j] * sum(T[i][l] * VtV[l][j] for l in range(j))
+        Y = [[rd(sum(T[l][p] * VtC[l][k] for l in range(nb))) for k in range(n - c1)] for p in range(nb)]
+        for i in range(m - c0):
+            for k in range(n - c1):
+                acc = Fraction(0)
+                for p in range(nb):
+                    acc = r32(acc + V[i][p] * Y[p][k])
+                W[c0 + i][c1 + k] = rd(W[c0 + i][c1 + k] - acc)
+    R = [[W[i][k] if k >= i else Fraction(0) for k in range(n)] for i in range(n)]
+    return [[(-e if R[i][i] < 0 else e) for e in R[i]] for i in range(n)]
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+@pytest.mark.parametrize("shape,b,seed", [((8, 5), 2, 0), ((9, 6), 3, 1), ((7, 4), 1, 2)])
+def test_blocked_rounding_points_exact(fmt, shape, b, seed):
+    """householder_qr_r_blocked equals R29's rounding sequence evaluated in exact rational
+    arithmetic.  The fp64 pieces (T, T^T V^T C before its single rounding) are exact in
+    rationals and within fp64 rounding in the oracle; on these inputs that never moves a u_f
+    result, and every u_f / fp32 rounding point must match."""
+    from oracle.qr import householder_qr_r_blocked
+    rng = np.random.default_rng(200 + seed)
+    A = rng.standard_normal(shape) * np.array([1.0, 3.0, 0.5, 2.0, 0.7, 1.3][: shape[1]])
+    R = householder_qr_r_blocked(A, fmt, b)
+    Rx = _blocked_exact(A.tolist(), fmt, b)
+    assert np.array_equal(R, np.array([[float(e) for e in row] for row in Rx]))
+    assert not np.array_equal(R, householder_qr_r_blocked(A, "fp64", b))
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+def test_blocked_backward_error_and_preconditioner(fmt):
+    """The blocked fp16 / bf16 R~ satisfies the same probabilistic Gram residual bound as the
+    unblocked one (R = 0 fails it in fp16), stays within a few u_f of it, and preconditions A
+    as well: kappa(A R~^{-1}) < 10 at kappa(A) = 300."""
+    from oracle.qr import householder_qr_r_blocked
+    rng = np.random.default_rng(41)
+    m, n = 400, 24
+    U, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    A = (U * np.logspace(0, -np.log10(300.0), n)) @ V.T
+    Ah = round_to(A, fmt)
+    Rb = householder_qr_r_blocked(A, fmt, 8)
+    Ru = householder_qr_r(A, fmt)
+    u = unit_roundoff(fmt)
+    bound = 2 * np.sqrt(m) * n ** 0.75 * u * np.linalg.norm(Ah) ** 2
+    assert np.linalg.norm(Rb.T @ Rb - Ah.T @ Ah) <= bound
+    if fmt == "fp16":
+        assert np.linalg.norm(Ah.T @ Ah) > bound
+    assert np.linalg.norm(Rb - Ru) <= 50 * u * np.linalg.cond(Ah) * np.linalg.norm(Ru)
+    assert np.linalg.cond(A @ np.linalg.inv(Rb)) < 10.0
