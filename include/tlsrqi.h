@@ -213,6 +213,19 @@ TLS_API size_t tls_qr_workspace_size(const tls_matrix_t* A, int32_t u_f, int32_t
 TLS_API int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, void* stream, void* ws_dev,
                                   size_t ws_bytes, tls_precond_t* R_out, tls_info_t* info);
 
+/* The same preconditioner with the trailing updates blocked (reading R29; SURVEY §8(f) NEXT-2
+ * "on tensor cores"): panels of 128 columns factored as tls_factor_precond_qr does (R25, D of
+ * R27), the panel's 128 reflectors applied to the trailing columns at once in compact WY form
+ * C <- C - V (T^T (V^T C)) with V^T C and V^T V on tcgen05 (fp32 sums per 64-row chunk, fp64
+ * across, as R11), T in fp64, Y = T^T V^T C rounded to u_f and V Y on tcgen05 (fp32), the
+ * difference rounded once to u_f.  In exact arithmetic the same R as the unblocked QR; in u_f
+ * another backward-stable rounding sequence (oracle.qr.householder_qr_r_blocked).  u_f = fp16
+ * or bf16, dense A, one rank (m_global == m_local), n <= 2048.  Workspace:
+ * tls_qr_blocked_workspace_size (the unblocked QR's plus a 16-bit copy of A and the WY panels). */
+TLS_API size_t tls_qr_blocked_workspace_size(const tls_matrix_t* A, int32_t u_f);
+TLS_API int tls_factor_precond_qr_blocked(const tls_matrix_t* A, int32_t u_f, void* stream, void* ws_dev,
+                                          size_t ws_bytes, tls_precond_t* R_out, tls_info_t* info);
+
 /* Handle from host data (tests: import the oracle's R~ to isolate PCG/RQI
  * parity).  Rt_host: n x n row-major upper-triangular values already
  * representable in u_f; d_host: n powers of two; normA2 = ||A||_F^2 (global). */

@@ -133,7 +133,10 @@ __global__ void __launch_bounds__(256) k_round_scaled(const double* __restrict__
 template <int FMT, bool KAHAN>
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchunks, int nsplit, int kpc,
-          int super, int epi, double* __restrict__ part, int kb0) {
+          int super, int epi, double* __restrict__ part, int kb0, const __grid_constant__ CUtensorMap tmapB,
+          int atb) {
+  // atb = 1 (the blocked QR's V^T C, k_qr_wy.cu): A = the single 128-column panel of `tmap`,
+  // B = the 128-column tile blockIdx.x of `tmapB`; otherwise the upper tiles (I, J) of tmap^T tmap
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment for the 128B-swizzled operand panels
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -147,9 +150,10 @@ k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchun
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int t = blockIdx.x, I = 0;
-  while (t >= TT - I) { t -= TT - I; ++I; }
-  const int J = I + t;
-  const bool diag = (I == J);
+  if (!atb) while (t >= TT - I) { t -= TT - I; ++I; }
+  const int J = atb ? (int)blockIdx.x : I + t;
+  const bool diag = !atb && (I == J);
+  const CUtensorMap* mapB = atb ? &tmapB : &tmap;
   const int s = blockIdx.y;
   const int c0 = (int)((int64_t)nchunks * s / nsplit), c1 = (int)((int64_t)nchunks * (s + 1) / nsplit);
   const int kb_total = (int)((m + kTcBK - 1) / kTcBK);
@@ -180,6 +184,7 @@ k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchun
     // ---------------- TMA producer
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      if (atb) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(mapB)) : "memory");
       const uint32_t bytes = diag ? kTcPanel : 2 * kTcPanel;
       int it = 0;
       for (int c = c0; c < c1; ++c) {
@@ -195,8 +200,8 @@ k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchun
           tma_load_2d(a + kTcPanel / 2, &tmap, I * kTcTile + 64, row, &full[st]);
           if (!diag) {
             unsigned char* b = panB + st * kTcPanel;
-            tma_load_2d(b, &tmap, J * kTcTile, row, &full[st]);
-            tma_load_2d(b + kTcPanel / 2, &tmap, J * kTcTile + 64, row, &full[st]);
+            tma_load_2d(b, mapB, J * kTcTile, row, &full[st]);
+            tma_load_2d(b + kTcPanel / 2, mapB, J * kTcTile + 64, row, &full[st]);
           }
         }
       }
@@ -883,7 +888,7 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
     tc_shape(rows, A.n, K_t, TTs, nts, ncs, nss);
     const int ns_use = nsplit < ncs ? nsplit : ncs;               // the part buffer holds nsplit splits
     kfn<<<dim3(ntiles, ns_use), kTcThreads, smem, st>>>(tmap, rows, TT, ncs, ns_use, K_t / kTcBK, gram_super(),
-                                                        ee ? atoi(ee) : 2, part, (int)(r0 / kTcBK));
+                                                        ee ? atoi(ee) : 2, part, (int)(r0 / kTcBK), tmap, 0);
     TLS_LAUNCH_CHECK();
     if (launches) *launches += 2;
   }
@@ -893,4 +898,187 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
   return 0;
 }
 
+// ------------------------------------------------------------------------------ 2''. A^T B for the blocked QR
+// out (128 x ldo, fp64) = A^T B where A is the 16-bit row-major m x 128 matrix at `a` (row
+// stride lda elements) and B the 16-bit row-major m x nb matrix at `b` (row stride ldb), with
+// k_gram_tc's accumulation (fp32 per K_t = 64-row chunk, fp32 sums of 64 chunk sums, fp64
+// flushes and split sums: reading R11 / R29).  b == a, nb == 128: the Gram of the panel.
+__global__ void k_atb_reduce(const double* __restrict__ part, int ntiles, int nsplit, int nb, double* __restrict__ out,
+                             int ldo) {
+  // grid (ntiles, 64): CTA (J, y) sums rows 2y, 2y + 1 of tile J over the splits, in split order
+  const int J = blockIdx.x;
+  const int te = kTcTile * kTcTile;
+  const int e = blockIdx.y * 256 + threadIdx.x;
+  const int i = e / kTcTile, j = e % kTcTile;
+  double acc = 0.0;
+  for (int s = 0; s < nsplit; ++s) acc += part[((size_t)s * ntiles + J) * te + e];
+  if (J * kTcTile + j < nb) out[(size_t)i * ldo + J * kTcTile + j] = acc;
+}
+
+static int make_map16(CUtensorMap* map, int u_f, const void* base, int64_t rows, int64_t cols, int64_t ld) {
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)kTcBK};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(map, u_f == TLS_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (16-bit operand) failed (%d)", (int)r);
+    return TLS_ERR_CUDA;
+  }
+  return 0;
+}
+
+size_t tc_atb_ws_bytes(int nb) {
+  // nsplit * ntiles <= #SMs for every B width up to nb (nsplit = #SMs / ntiles, or 1)
+  const int nt = (nb + kTcTile - 1) / kTcTile;
+  const int tiles = nt > num_sms() ? nt : num_sms();
+  return (size_t)tiles * kTcTile * kTcTile * 8;
+}
+
+int launch_tc_atb(int u_f, const uint16_t* a, int64_t lda, const uint16_t* b, int64_t ldb, int64_t m, int nb,
+                  double* out, int ldo, double* part, size_t part_bytes, cudaStream_t st) {
+  if (m <= 0) {
+    TLS_CUDA_TRY(cudaMemset2DAsync(out, (size_t)ldo * 8, 0, (size_t)nb * 8, kTcTile, st));
+    return 0;
+  }
+  const int ntiles = (nb + kTcTile - 1) / kTcTile;
+  const int nchunks = (int)((m + kTcBK - 1) / kTcBK);
+  int nsplit = num_sms() / ntiles;
+  if (nsplit > nchunks) nsplit = nchunks;
+  if (nsplit < 1) nsplit = 1;
+  if ((size_t)nsplit * ntiles * kTcTile * kTcTile * 8 > part_bytes) {
+    set_error("tc_atb: partials buffer too small");
+    return TLS_ERR_WORKSPACE;
+  }
+  CUtensorMap ma, mb;
+  int rc = make_map16(&ma, u_f, a, m, kTcTile, lda);
+  if (!rc) rc = make_map16(&mb, u_f, b, m, nb, ldb);   // columns past nb: TMA zero fill
+  if (rc) return rc;
+  const size_t smem = 2 * kTcStages * kTcPanel + 1024 + 512;
+  auto kfn = u_f == TLS_FP16 ? k_gram_tc<0, false> : k_gram_tc<1, false>;
+  TLS_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  TLS_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)nsplit * ntiles * kTcTile * kTcTile * 8, st));
+  kfn<<<dim3(ntiles, nsplit), kTcThreads, smem, st>>>(ma, m, 1, nchunks, nsplit, 1, gram_super(), 2, part, 0, mb, 1);
+  TLS_LAUNCH_CHECK();
+  k_atb_reduce<<<dim3(ntiles, kTcTile * kTcTile / 256), 256, 0, st>>>(part, ntiles, nsplit, nb, out, ldo);
+  TLS_LAUNCH_CHECK();
+  return 0;
+}
+
+
+// ------------------------------------------------------------------------------ blocked QR update
+// k_qr_wy_update (reading R29, the compact-WY trailing update of the blocked Householder QR,
+// SURVEY §8(f) NEXT-2 on tensor cores): C <- fl_uf(C - fl32(V Y)) for one 128 x 128 tile of the
+// trailing matrix C.  V Y is one tcgen05 kind::f16 product with K = 128 (the panel's
+// reflectors): A = V from Vt (128 x m', row-major: the rows of C contiguous, MN-major like the
+// Gram's operands), B = Y (128 x n', row-major: MN-major), fp32 accumulator in TMEM.  The
+// epilogue (4 warps, TMEM lane = row of the tile) forms the difference in fp64 (both operands
+// fp32), rounds it once to u_f, and writes the fp32 working copy W and its 16-bit twin W16.
+template <int FMT>
+__global__ void __launch_bounds__(128, 1)
+k_qr_wy_update(const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapY, float* __restrict__ W,
+               uint16_t* __restrict__ W16, int64_t ldw, int64_t ld16, int64_t r0, int c0, int64_t m, int n) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* panA = smem;                         // [2 K-stages][16 KB]
+  unsigned char* panB = smem + 2 * kTcPanel;          // [2][16 KB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 4 * kTcPanel);
+  uint64_t* done = full + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int M0 = blockIdx.x * kTcTile, N0 = blockIdx.y * kTcTile;   // tile origin in (rows - r0, cols - c0)
+  if (threadIdx.x == 0) {
+    mbar_init(full, 1);
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(kTcTile)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  if (threadIdx.x == 0) {                              // TMA: both K halves of A and B at once
+    mbar_arrive_expect_tx(full, 4 * kTcPanel);
+    for (int k = 0; k < 2; ++k) {
+      unsigned char* a = panA + k * kTcPanel;
+      tma_load_2d(a, &mapV, M0, 64 * k, full);
+      tma_load_2d(a + kTcPanel / 2, &mapV, M0 + 64, 64 * k, full);
+      unsigned char* b = panB + k * kTcPanel;
+      tma_load_2d(b, &mapY, N0, 64 * k, full);
+      tma_load_2d(b + kTcPanel / 2, &mapY, N0 + 64, 64 * k, full);
+    }
+  }
+  if (threadIdx.x == 32) {                             // MMA: 2 x 4 steps of K = 16
+    mbar_wait(full, 0);
+    tc_fence_after();
+    const uint32_t idesc = idesc_f16(FMT);
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t a0 = smem_u32(panA + k * kTcPanel), b0 = smem_u32(panB + k * kTcPanel);
+#pragma unroll
+      for (int kk = 0; kk < kTcBK / 16; ++kk) {
+        const uint64_t ad = sw128_desc(a0 + kk * 2048, kTcPanel / 2, 1024);
+        const uint64_t bd = sw128_desc(b0 + kk * 2048, kTcPanel / 2, 1024);
+        tc_mma_f16(tmem, ad, bd, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+      }
+    }
+    tc_commit(done);
+  }
+  mbar_wait(done, 0);
+  tc_fence_after();
+  // epilogue: warp w reads TMEM lanes 32w..32w+31 (rows M0 + 32w + lane of the tile), 32 columns
+  // at a time, and transposes them through shared memory so that W and W16 are read and written
+  // along rows (lane = column)
+  float* stage = reinterpret_cast<float*>(panA) + warp * 32 * 33;    // the operand panels are consumed
+  constexpr int prec = FMT == 0 ? TLS_FP16 : TLS_BF16;
+  for (int cc = 0; cc < kTcTile / 32; ++cc) {
+    uint32_t acc[32];
+    TLS_TMEM_LD32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(cc * 32), acc);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int e = 0; e < 32; ++e) stage[lane * 33 + e] = __uint_as_float(acc[e]);
+    __syncwarp();
+    const int col = c0 + N0 + cc * 32 + lane;
+    for (int r = 0; r < 32; ++r) {
+      const int64_t row = r0 + M0 + warp * 32 + r;
+      if (row < m && col < n) {
+        const double x = round_uf((double)W[row * ldw + col] - (double)stage[r * 33 + lane], prec);
+        W[row * ldw + col] = (float)x;
+        W16[row * ld16 + col] = FMT == 0 ? f64_to_f16_bits(x) : f64_to_bf16_bits(x);
+      }
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTcTile) : "memory");
+  }
+}
+
+int launch_qr_wy_update(int u_f, const uint16_t* Vt, int64_t ldv, const uint16_t* Y, int64_t ldy, float* W,
+                        uint16_t* W16, int64_t ldw, int64_t ld16, int64_t r0, int c0, int64_t m, int n, cudaStream_t st) {
+  const int64_t mr = m - r0;
+  const int nc = n - c0;
+  if (mr <= 0 || nc <= 0) return 0;
+  CUtensorMap mv, my;
+  int rc = make_map16(&mv, u_f, Vt, kTcTile, mr, ldv);      // 128 rows (K) x m' columns (M)
+  if (!rc) rc = make_map16(&my, u_f, Y, kTcTile, nc, ldy);   // 128 rows (K) x n' columns (N)
+  if (rc) return rc;
+  const size_t smem = 4 * kTcPanel + 1024 + 256;
+  auto kfn = u_f == TLS_FP16 ? k_qr_wy_update<0> : k_qr_wy_update<1>;
+  TLS_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)((mr + kTcTile - 1) / kTcTile), (unsigned)((nc + kTcTile - 1) / kTcTile));
+  kfn<<<grid, 128, smem, st>>>(mv, my, W, W16, ldw, ld16, r0, c0, m, n);
+  TLS_LAUNCH_CHECK();
+  return 0;
+}
 }  // namespace tls

@@ -209,7 +209,10 @@ __device__ __forceinline__ void qr_update_v4(float* __restrict__ W, int64_t m, i
                                              double* __restrict__ G, double* qsm, bool pdl_release) {
   constexpr int GPT = CPT / 4;
   const int c = j + 1, c0 = c & ~3;
-  const int ngroups = (ldw - c0) >> 2;
+  // columns up to n (rounded to 4): the whole row for the unblocked factorization (n = the
+  // matrix's n, ldw = round4(n)), the panel for the blocked one (n = the panel's end, R29)
+  const int lde = min(ldw, (n + 3) & ~3);
+  const int ngroups = (lde - c0) >> 2;
   int64_t r0 = (int64_t)b * RB;
   const int64_t r1 = min(m, r0 + RB);
   if (r1 <= j) return;
@@ -337,7 +340,9 @@ template <typename T, int PREC>
 __global__ void __launch_bounds__(kQrThreads) k_qr_fin(const T* __restrict__ W, int n, int ldw, int j, int b0, int nb,
                                                         const double* __restrict__ partP, double* __restrict__ wT,
                                                         double* __restrict__ scal, double* __restrict__ G,
-                                                        int* __restrict__ qflags, int leaf) {
+                                                        int* __restrict__ qflags, int leaf, int ldp) {
+  // ldp: the row stride of the partials (the n of the pass that wrote them: the matrix's n, or the
+  // panel's end in the blocked QR, whose first panel reads the full-width load pass)
   __shared__ double red[32];
   // programmatic dependent launch: the next kernel of the chain may be scheduled now; this
   // one waits for its predecessor's writes before reading anything
@@ -348,7 +353,7 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_fin(const T* __restrict__ W, 
   if (qflags[0]) return;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   double tl = 0.0;
-  for (int b = b0 + t; b < nb; b += kQrThreads) tl += partP[(int64_t)b * n + j];
+  for (int b = b0 + t; b < nb; b += kQrThreads) tl += partP[(int64_t)b * ldp + j];
   const double tail = block_sum(tl, red);                      // fixed order: same bits in every CTA
   const double x0 = (double)W[(int64_t)j * ldw + j];
   const double sigma = round_uf(sqrt(round_uf(fma(x0, x0, tail), prec)), prec);
@@ -368,10 +373,10 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_fin(const T* __restrict__ W, 
   if (k < n) {
     int b = b0 + warp;
     for (; b + 8 < nb; b += 16) {
-      s0 += partP[(int64_t)b * n + k];
-      s1 += partP[(int64_t)(b + 8) * n + k];
+      s0 += partP[(int64_t)b * ldp + k];
+      s1 += partP[(int64_t)(b + 8) * ldp + k];
     }
-    if (b < nb) s0 += partP[(int64_t)b * n + k];
+    if (b < nb) s0 += partP[(int64_t)b * ldp + k];
   }
   cs[warp][lane] = s0 + s1;
   __syncthreads();
@@ -421,7 +426,8 @@ int qr_step_launch(T* W, const DenseView& A, int ldw, const double* dinv, int j,
   const int n = A.n;
   if constexpr (!LOAD && sizeof(T) == 4) {
     const int c0 = (j + 1) & ~3;
-    const int ngroups = (ldw - c0) / 4;
+    const int lde = ldw < ((n + 3) & ~3) ? ldw : ((n + 3) & ~3);
+    const int ngroups = (lde - c0) / 4;
     const int TG = qr_team(ngroups, CPT / 4);
     const int teams = qr_step_threads<CPT>() / TG;
     const size_t smem = teams > 1 ? (size_t)teams * ngroups * 4 * sizeof(double) : 0;
@@ -485,7 +491,7 @@ int qr_t(const DenseView& A, const double* dinv, void* Wbuf, double* partP, doub
     const int nbj = j == 0 ? nb : (int)((m_act(j - 1) + RB - 1) / RB);   // CTAs that wrote them
     const int nf = (n - j - 1 + 31) / 32;
     rc = launch_pdl(k_qr_fin<T, PREC>, nf > 0 ? nf : 1, kQrThreads, 0, st, (const T*)W, n, ldw, j, b0, nbj,
-                    (const double*)partP, wT, scal, G, qflags, leaf);
+                    (const double*)partP, wT, scal, G, qflags, leaf, n);
     if (rc) return rc;
     ++nl;
     if (j + 1 < n) {
@@ -541,4 +547,232 @@ int launch_qr(const DenseView& A, int u_f, const double* dinv, void* Wbuf, doubl
   }
 }
 
+
+// ====================================================================== blocked QR (R29, NEXT-2)
+// Panels of kWyB = 128 columns: the panel is factored by the unblocked chain above restricted
+// to the panel's columns (k_qr_fin + k_qr_step_v4 with n = the panel's end), then its 128
+// reflectors are applied to the trailing columns at once on the tensor cores (compact WY):
+//   V (m' x 128, the Householder vectors, u_f values)     k_wy_extract, k_wy_transpose
+//   V^T V, V^T C (R11-style fp32 chunk sums, fp64)       launch_tc_atb (k_gram_tc, atb mode)
+//   T (fp64, the WY factor), Y = fl_uf(T^T V^T C)        k_wy_T, k_wy_Y
+//   C <- fl_uf(C - fl32(V Y))                             launch_qr_wy_update (tcgen05)
+// A 16-bit twin W16 of the working copy feeds the tensor cores (the values are u_f values, so
+// it is exact); the update writes both.  The next panel's first inner products come from a
+// "virtual" update pass of column c0 - 1 with w = 0 (nothing changes, the partials of column
+// c0 are accumulated), so the panel chain starts exactly as the unblocked one.
+constexpr int kWyB = 128;
+
+template <int PREC>
+__global__ void k_f32_to_16(const float* __restrict__ W, int64_t ldw, uint16_t* __restrict__ W16, int64_t ld16,
+                            int64_t m, int n) {
+  for (int64_t i = blockIdx.x; i < m; i += gridDim.x)
+    for (int k = threadIdx.x; k < ld16; k += blockDim.x) {
+      const double x = k < n ? (double)W[i * ldw + k] : 0.0;
+      W16[i * ld16 + k] = PREC == TLS_FP16 ? f64_to_f16_bits(x) : f64_to_bf16_bits(x);
+    }
+}
+
+// V16[i][jj] (m' x 128, i = row - c0): v_{c0+jj} (the diagonal entry v_0 from scal, below it the
+// panel column as the chain left it, zero above)
+template <int PREC>
+__global__ void k_wy_extract(const float* __restrict__ W, int64_t ldw, const double* __restrict__ scal, int c0, int nb,
+                             int64_t m, uint16_t* __restrict__ V16) {
+  const int jj = threadIdx.x;
+  for (int64_t i = blockIdx.x; i < m - c0; i += gridDim.x) {
+    double v = 0.0;
+    if (jj < nb) {
+      if (i == jj) v = scal[4 * (c0 + jj) + 1];
+      else if (i > jj) v = (double)W[(c0 + i) * ldw + c0 + jj];
+    }
+    V16[i * kWyB + jj] = PREC == TLS_FP16 ? f64_to_f16_bits(v) : f64_to_bf16_bits(v);
+  }
+}
+
+// Vt16 (128 x ldv) = V16^T, 32 x 32 tiles through shared memory
+__global__ void k_wy_transpose(const uint16_t* __restrict__ V16, int64_t mr, uint16_t* __restrict__ Vt16, int64_t ldv) {
+  __shared__ uint16_t tile[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32;
+  const int j0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = i0 + r;
+    tile[r][threadIdx.x] = i < mr ? V16[i * kWyB + j0 + threadIdx.x] : (uint16_t)0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = i0 + threadIdx.x;
+    if (i < ldv) Vt16[(int64_t)(j0 + r) * ldv + i] = tile[threadIdx.x][r];
+  }
+}
+
+// T (128 x 128, fp64, upper): T_jj = beta_j, T[0:j, j] = -beta_j T[0:j, 0:j] VtV[0:j, j]
+// (VtV symmetric: its column j is read as row j, coalesced, into shared memory per step)
+__global__ void __launch_bounds__(kWyB) k_wy_T(const double* __restrict__ VtV, const double* __restrict__ scal, int c0,
+                                               int nb, double* __restrict__ T) {
+  extern __shared__ double Ts[];                       // [128][129], then the column vector [128]
+  double* vc = Ts + kWyB * (kWyB + 1);
+  const int i = threadIdx.x;
+  for (int e = i; e < kWyB * (kWyB + 1); e += blockDim.x) Ts[e] = 0.0;
+  for (int j = 0; j < nb; ++j) {
+    vc[i] = VtV[(int64_t)j * kWyB + i];
+    __syncthreads();
+    const double bj = scal[4 * (c0 + j) + 3];
+    if (i < j) {
+      double s0 = 0.0, s1 = 0.0;                        // two chains: even and odd l, added at the end
+      int l = i;
+      for (; l + 1 < j; l += 2) {
+        s0 = fma(Ts[i * (kWyB + 1) + l], vc[l], s0);
+        s1 = fma(Ts[i * (kWyB + 1) + l + 1], vc[l + 1], s1);
+      }
+      if (l < j) s0 = fma(Ts[i * (kWyB + 1) + l], vc[l], s0);
+      Ts[i * (kWyB + 1) + j] = -bj * (s0 + s1);
+    } else if (i == j) {
+      Ts[i * (kWyB + 1) + j] = bj;
+    }
+    __syncthreads();
+  }
+  for (int e = i; e < kWyB * kWyB; e += blockDim.x) T[e] = Ts[(e / kWyB) * (kWyB + 1) + e % kWyB];
+}
+
+// Y16 (128 x ldy) = fl_uf(T^T Y1) (fp64 products and sums, one rounding), Y1: 128 x ldy1.
+// CTA = 32 columns k (Y1's block staged in shared memory), warp = rows p = warp, warp + 8, ...
+template <int PREC>
+__global__ void __launch_bounds__(256) k_wy_Y(const double* __restrict__ T, const double* __restrict__ Y1, int64_t ldy1,
+                                              int nc, uint16_t* __restrict__ Y16, int64_t ldy) {
+  __shared__ double ys[kWyB][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int k = blockIdx.x * 32 + lane;
+  for (int l = warp; l < kWyB; l += 8) ys[l][lane] = k < nc ? Y1[(int64_t)l * ldy1 + k] : 0.0;
+  __syncthreads();
+  for (int p = warp; p < kWyB; p += 8) {
+    double acc = 0.0;
+    for (int l = 0; l <= p; ++l) acc = fma(__ldg(T + l * kWyB + p), ys[l][lane], acc);   // T upper: l <= p
+    if (k < ldy) Y16[(int64_t)p * ldy + k] = k < nc ? (PREC == TLS_FP16 ? f64_to_f16_bits(round_uf(acc, TLS_FP16))
+                                                                      : f64_to_bf16_bits(round_uf(acc, TLS_BF16)))
+                                                  : (uint16_t)0;
+  }
+}
+
+// R rows [c0, c1): the panel block from the chain's Gp (stride ldgp), the trailing part from W
+// (final after the panel's WY update), signs as R25 (diag(R) >= 0)
+__global__ void k_wy_copy_R(const double* __restrict__ Gp, int ldgp, const float* __restrict__ W, int64_t ldw,
+                            const double* __restrict__ scal, int c0, int c1, int n, int trailing, double* __restrict__ G) {
+  const int j = c0 + blockIdx.x;
+  if (j >= c1) return;
+  const double sg = scal[4 * j] < 0.0 ? -1.0 : 1.0;
+  for (int k = j + threadIdx.x; k < n; k += blockDim.x) {
+    if (k < c1) G[(int64_t)j * n + k] = Gp[(int64_t)j * ldgp + k];
+    else if (trailing) G[(int64_t)j * n + k] = sg * (double)W[(int64_t)j * ldw + k];
+  }
+}
+
+size_t qr_wy_bytes(int64_t m, int n) {
+  const int64_t ld16 = (n + 63) / 64 * 64, ldv = (m + 63) / 64 * 64;
+  return (size_t)m * ld16 * 2 + (size_t)m * kWyB * 2 + (size_t)kWyB * ldv * 2 + (size_t)n * n * 8 +
+         (size_t)kWyB * kWyB * 8 * 2 + (size_t)kWyB * ld16 * 8 + (size_t)kWyB * ld16 * 2 + tc_atb_ws_bytes(n) +
+         (size_t)n * 8 * 5 + 16 * 256;
+}
+
+template <int CPT, int PREC>
+int qr_blocked_t(const DenseView& A, const double* dinv, float* W, double* partP, double* wT, double* scal,
+                 int* qflags, double* G, char* wy, cudaStream_t st, int* launches) {
+  const int n = A.n;
+  const int64_t m = A.m;
+  const int RB = qr_rows_per_cta(m, n);
+  const int nb = (int)((m + RB - 1) / RB);
+  const int ldw = qr_ldw(n, PREC);
+  const int64_t ld16 = (n + 63) / 64 * 64, ldv = (m + 63) / 64 * 64;
+  // carve the WY buffers
+  char* p = wy;
+  auto take = [&](size_t bytes) { char* r = p; p += (bytes + 255) & ~(size_t)255; return r; };
+  uint16_t* W16 = reinterpret_cast<uint16_t*>(take((size_t)m * ld16 * 2));
+  uint16_t* V16 = reinterpret_cast<uint16_t*>(take((size_t)m * kWyB * 2));
+  uint16_t* Vt16 = reinterpret_cast<uint16_t*>(take((size_t)kWyB * ldv * 2));
+  double* Gp = reinterpret_cast<double*>(take((size_t)n * n * 8));
+  double* VtV = reinterpret_cast<double*>(take((size_t)kWyB * kWyB * 8));
+  double* T = reinterpret_cast<double*>(take((size_t)kWyB * kWyB * 8));
+  double* Y1 = reinterpret_cast<double*>(take((size_t)kWyB * ld16 * 8));
+  uint16_t* Y16 = reinterpret_cast<uint16_t*>(take((size_t)kWyB * ld16 * 2));
+  const size_t atb_bytes = tc_atb_ws_bytes(n);
+  double* atb = reinterpret_cast<double*>(take(atb_bytes));
+  double* zw = reinterpret_cast<double*>(take((size_t)n * 8));
+  double* zs = reinterpret_cast<double*>(take((size_t)n * 8 * 4));
+  TLS_CUDA_TRY(cudaMemsetAsync(zw, 0, (size_t)n * 8, st));
+  TLS_CUDA_TRY(cudaMemsetAsync(zs, 0, (size_t)n * 32, st));
+  int nl = 0;
+  // LOAD: W = fl_uf(A D^-1) and the partials of column 0; its 16-bit twin
+  int rc = qr_step_launch<float, true, CPT, PREC>(W, A, ldw, dinv, -1, RB, 0, nb, nullptr, nullptr, partP, Gp, qflags, st);
+  if (rc) return rc;
+  k_f32_to_16<PREC><<<(int)std::min<int64_t>(m, 4096), 256, 0, st>>>(W, ldw, W16, ld16, m, n);
+  nl += 2;
+  for (int c0 = 0; c0 < n; c0 += kWyB) {
+    const int c1 = std::min(n, c0 + kWyB);
+    DenseView Ap = A;
+    Ap.n = c1;                                        // the chain works on the panel's columns only
+    if (c0 > 0) {
+      // the previous panel's R rows: its block from Gp (stride c0, its end), its trailing part from W
+      k_wy_copy_R<<<kWyB, 256, 0, st>>>(Gp, c0, W, ldw, scal, c0 - kWyB, c0, n, 1, G);
+      // partials of column c0 over the panel (the pass of column c0 - 1 with w = 0: no change)
+      const int j = c0 - 1;
+      const int bs = j / RB;
+      rc = qr_step_launch<float, false, CPT, PREC>(W, Ap, ldw, dinv, j, RB, bs, nb - bs, zw, zs, partP, Gp, qflags, st);
+      if (rc) return rc;
+      nl += 2;
+    }
+    for (int j = c0; j < c1; ++j) {
+      const int b0 = (j > 0 ? j - 1 : 0) / RB;
+      const int nf = (c1 - j - 1 + 31) / 32;
+      rc = launch_pdl(k_qr_fin<float, PREC>, nf > 0 ? nf : 1, kQrThreads, 0, st, (const float*)W, c1, ldw, j, b0, nb,
+                      (const double*)partP, wT, scal, Gp, qflags, 0, j == 0 ? n : c1);
+      if (rc) return rc;
+      ++nl;
+      if (j + 1 < c1) {
+        const int bs = j / RB;
+        rc = qr_step_launch<float, false, CPT, PREC>(W, Ap, ldw, dinv, j, RB, bs, nb - bs, wT, scal, partP, Gp, qflags, st);
+        if (rc) return rc;
+        ++nl;
+      }
+    }
+    if (c1 == n) {
+      k_wy_copy_R<<<kWyB, 256, 0, st>>>(Gp, c1, W, ldw, scal, c0, c1, n, 0, G);
+      ++nl;
+      break;
+    }
+    const int64_t mr = m - c0;
+    k_wy_extract<PREC><<<(int)std::min<int64_t>(mr, 8192), kWyB, 0, st>>>(W, ldw, scal, c0, kWyB, m, V16);
+    k_wy_transpose<<<dim3((unsigned)((ldv - c0 + 31) / 32), kWyB / 32), dim3(32, 8), 0, st>>>(V16, mr, Vt16, ldv);
+    TLS_LAUNCH_CHECK();
+    rc = launch_tc_atb(PREC, V16, kWyB, V16, kWyB, mr, kWyB, VtV, kWyB, atb, atb_bytes, st);
+    if (!rc) rc = launch_tc_atb(PREC, V16, kWyB, W16 + (int64_t)c0 * ld16 + c1, ld16, mr, n - c1, Y1, (int)ld16, atb,
+                                atb_bytes, st);
+    if (rc) return rc;
+    const size_t tsm = (size_t)kWyB * (kWyB + 2) * 8;
+    static bool attr = false;
+    if (!attr) {
+      TLS_CUDA_TRY(cudaFuncSetAttribute(k_wy_T, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+      attr = true;
+    }
+    k_wy_T<<<1, kWyB, tsm, st>>>(VtV, scal, c0, kWyB, T);
+    k_wy_Y<PREC><<<(unsigned)((n - c1 + 31) / 32), 256, 0, st>>>(T, Y1, ld16, n - c1, Y16, ld16);
+    TLS_LAUNCH_CHECK();
+    rc = launch_qr_wy_update(PREC, Vt16, ldv, Y16, ld16, W, W16, ldw, ld16, c0, c1, m, n, st);
+    if (rc) return rc;
+    nl += 10;   // extract, transpose, 2 x (atb + reduce + memset), T, Y, update
+  }
+  TLS_LAUNCH_CHECK();
+  if (launches) *launches += nl;
+  return 0;
+}
+
+int launch_qr_blocked(const DenseView& A, int u_f, const double* dinv, void* Wbuf, double* partP, double* wT,
+                      double* scal, int* qflags, double* G, void* wy, cudaStream_t st, int* launches) {
+  if (u_f != TLS_FP16 && u_f != TLS_BF16) {
+    set_error("blocked QR: u_f must be fp16 or bf16 (the tensor-core formats)");
+    return TLS_ERR_UNSUPPORTED;
+  }
+  if (A.n > 8 * kQrThreads) { set_error("blocked QR: n > %d", 8 * kQrThreads); return TLS_ERR_UNSUPPORTED; }
+  float* W = static_cast<float*>(Wbuf);
+  char* wyb = static_cast<char*>(wy);
+  if (u_f == TLS_FP16) return qr_blocked_t<8, TLS_FP16>(A, dinv, W, partP, wT, scal, qflags, G, wyb, st, launches);
+  return qr_blocked_t<8, TLS_BF16>(A, dinv, W, partP, wT, scal, qflags, G, wyb, st, launches);
+}
 }  // namespace tls

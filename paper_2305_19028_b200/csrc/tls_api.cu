@@ -1165,6 +1165,80 @@ int tls_factor_precond_qr(const tls_matrix_t* A, int32_t u_f, tls_comm_t comm, v
   return 0;
 }
 
+size_t tls_qr_blocked_workspace_size(const tls_matrix_t* A, int32_t u_f) {
+  if (check_matrix(A) != 0 || is_csr(A) || (u_f != TLS_FP16 && u_f != TLS_BF16)) return 0;
+  QrBufs q;
+  return carve_qr(A, u_f, 1, nullptr, 0, q, nullptr) + qr_wy_bytes(A->m_local, (int)A->n) + 256;
+}
+
+int tls_factor_precond_qr_blocked(const tls_matrix_t* A, int32_t u_f, void* stream, void* ws, size_t ws_bytes,
+                                  tls_precond_t* R_out, tls_info_t* info) {
+  fill_info_defaults(info);
+  if (R_out) *R_out = nullptr;
+  TLS_TRY(check_matrix(A));
+  if (!R_out || (u_f != TLS_FP16 && u_f != TLS_BF16)) { set_error("blocked QR: u_f must be TLS_FP16 or TLS_BF16"); return TLS_ERR_ARG; }
+  if (is_csr(A)) { set_error("the QR preconditioner takes a dense A"); return TLS_ERR_ARG; }
+  if (A->m_global != A->m_local) { set_error("blocked QR: one rank (the sharded QR is tls_factor_precond_qr's TSQR)"); return TLS_ERR_UNSUPPORTED; }
+  const int n = (int)A->n;
+  Work w;
+  QrBufs q;
+  bool ok = false;
+  const size_t need = carve_qr(A, u_f, 1, ws, ws_bytes, q, &ok);
+  const size_t need_all = tls_qr_blocked_workspace_size(A, u_f);
+  if (!ok || ws_bytes < need_all || !carve_ok(A, ws, ws_bytes, w, false)) {
+    set_error("workspace too small (need %zu)", need_all);
+    return TLS_ERR_WORKSPACE;
+  }
+  void* wy = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(ws) + need + 255) & ~(uintptr_t)255);
+  Ctx cx{static_cast<cudaStream_t>(stream), nullptr};
+  TLS_CUDA_TRY(cudaMemsetAsync(w.flags, 0, 8 * sizeof(int), cx.st));
+  TLS_CUDA_TRY(cudaMemsetAsync(q.qflags, 0, 4 * sizeof(int), cx.st));
+  TLS_TRY(run_pass(cx, A, PASS_COLSTATS, 2, nullptr, nullptr, w, nullptr));
+  double* d = w.d_tmp;
+  double* dinv = w.d_tmp + n;
+  double* normA2 = w.d_tmp + 2 * n;
+  TLS_TRY(launch_scaling(w.colstats, w.colstats + n, n, d, dinv, normA2, &w.flags[0], cx.st, 1));   // R27
+  cx.launches += 1;
+  {
+    ProfScope ps(TLS_PROF_CHOL, cx.st);
+    TLS_CUDA_TRY(cudaMemsetAsync(q.G, 0, (size_t)n * n * 8, cx.st));
+    TLS_TRY(launch_qr_blocked(dense_view(A), u_f, dinv, q.W1, q.part1, q.wT, q.scal, q.qflags, q.G, wy, cx.st,
+                              &cx.launches));
+    cx.passes += 1;
+  }
+  tls_precond_t h = nullptr;
+  TLS_TRY(alloc_precond(n, u_f, &h));
+  k_fill_scaling<<<(h->dev.npad + 255) / 256, 256, 0, cx.st>>>(h->dev.d, h->dev.dinv, d, dinv, n, h->dev.npad);
+  TLS_CUDA_TRY(cudaMemcpyAsync(h->dev.normA2, normA2, sizeof(double), cudaMemcpyDeviceToDevice, cx.st));
+  int rc = launch_pack_R(q.G, n, 0, h->dev, &w.flags[3], cx.st, &cx.launches);
+  cx.launches += 1;
+  if (rc) { tls_precond_destroy(h); return rc; }
+  rc = run_fingerprint(cx, A, normA2 + 1, w.partials);
+  if (rc) { tls_precond_destroy(h); return rc; }
+  int hflags[8], hq[4];
+  double hnorm[2] = {0.0, 0.0};
+  TLS_CUDA_TRY(cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, cx.st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(hq, q.qflags, sizeof(hq), cudaMemcpyDeviceToHost, cx.st));
+  TLS_CUDA_TRY(cudaMemcpyAsync(hnorm, normA2, 2 * sizeof(double), cudaMemcpyDeviceToHost, cx.st));
+  TLS_CUDA_TRY(cudaStreamSynchronize(cx.st));
+  TLS_LAUNCH_CHECK();
+  if (info) { info->passes = cx.passes; info->launches = cx.launches; }
+  int st = 0;
+  if (hflags[0]) { set_error("A has a zero or non-finite column (rank deficient)"); st = TLS_ERR_ARG; }
+  else if (hq[0]) { st = TLS_CHOL_BREAKDOWN; if (info) info->chol_pivot = hq[1]; }
+  else if (hflags[3]) st = TLS_RANGE;
+  if (st) {
+    tls_precond_destroy(h);
+    if (info && st > 0) info->status = st;
+    return st;
+  }
+  h->normA2_host = hnorm[0];
+  h->m_global = A->m_global;
+  h->content = hnorm[1];
+  *R_out = h;
+  return 0;
+}
+
 int tls_precond_import(int64_t n, int32_t u_f, const double* Rt_host, const double* d_host, double normA2,
                        void* stream, tls_precond_t* out) {
   if (!out || n < 1 || n > kMaxDenseN || !Rt_host || !d_host || u_f < TLS_FP16 || u_f > TLS_FP64) {

@@ -170,5 +170,14 @@ size_t qr_work_bytes(int64_t m, int n, int u_f);   // W copy + partials + w^T + 
 // (R_jj = 0) instead of raising the breakdown flag
 int launch_qr(const DenseView& A, int u_f, const double* dinv, void* Wbuf, double* partP, double* wT, double* scal,
               int* qflags, double* G, cudaStream_t st, int* launches, int row_stride = 0, int leaf = 0);
+// ---- blocked QR with tensor-core trailing updates (k_qr.cu + k_gram_tc.cu; reading R29) ----
+size_t qr_wy_bytes(int64_t m, int n);             // buffers beyond the unblocked ones (W16, V, T, Y, ...)
+int launch_qr_blocked(const DenseView& A, int u_f, const double* dinv, void* Wbuf, double* partP, double* wT,
+                      double* scal, int* qflags, double* G, void* wy, cudaStream_t st, int* launches);
+size_t tc_atb_ws_bytes(int nb);
+int launch_tc_atb(int u_f, const uint16_t* a, int64_t lda, const uint16_t* b, int64_t ldb, int64_t m, int nb,
+                  double* out, int ldo, double* part, size_t part_bytes, cudaStream_t st);
+int launch_qr_wy_update(int u_f, const uint16_t* Vt, int64_t ldv, const uint16_t* Y, int64_t ldy, float* W,
+                        uint16_t* W16, int64_t ldw, int64_t ld16, int64_t r0, int c0, int64_t m, int n, cudaStream_t st);
 
 }  // namespace tls

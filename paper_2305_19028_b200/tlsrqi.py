@@ -80,6 +80,8 @@ def lib() -> C.CDLL:
         "tls_factor_precond": (C.c_int, [M, I32, P(tls_rqi_opts_t), VP, VP, VP, SZ, P(VP), P(tls_info_t)]),
         "tls_qr_workspace_size": (SZ, [M, I32, I32]),
         "tls_factor_precond_qr": (C.c_int, [M, I32, VP, VP, VP, SZ, P(VP), P(tls_info_t)]),
+        "tls_qr_blocked_workspace_size": (SZ, [M, I32]),
+        "tls_factor_precond_qr_blocked": (C.c_int, [M, I32, VP, VP, SZ, P(VP), P(tls_info_t)]),
         "tls_precond_import": (C.c_int, [I64, I32, VP, VP, D, VP, P(VP)]),
         "tls_precond_export": (C.c_int, [VP, VP, VP, P(D)]),
         "tls_precond_destroy": (None, [VP]),
@@ -108,7 +110,8 @@ def lib() -> C.CDLL:
 EXPORTED = ["tls_abi_version", "tls_rqi_opts_default", "tls_status_string", "tls_last_error",
             "tls_comm_get_unique_id", "tls_comm_init", "tls_comm_init_shm", "tls_comm_nranks", "tls_comm_rank",
             "tls_comm_destroy", "tls_workspace_size",
-            "tls_factor_precond", "tls_qr_workspace_size", "tls_factor_precond_qr", "tls_precond_import", "tls_precond_export", "tls_precond_destroy",
+            "tls_factor_precond", "tls_qr_workspace_size", "tls_factor_precond_qr", "tls_qr_blocked_workspace_size",
+            "tls_factor_precond_qr_blocked", "tls_precond_import", "tls_precond_export", "tls_precond_destroy",
             "tls_rqi_pcgtls", "tls_solve_host_bytes", "tls_solve_host", "tls_colstats", "tls_gram",
             "tls_pass", "tls_pass_fp32", "tls_precond_apply", "tls_round", "tls_profile_enable", "tls_profile_read"]
 
@@ -290,6 +293,23 @@ def tls_factor_precond_qr(M: tls_matrix_t, u_f, comm=None, stream=None, ws: Opti
     rc = lib().tls_factor_precond_qr(C.byref(M), uf, C.c_void_p(comm) if comm else None, _stream(stream),
                                      _ptr(ws), ws.numel(), C.byref(R), C.byref(info))
     _check(rc, "tls_factor_precond_qr")
+    return rc, (Precond(R.value, int(M.n), uf) if R.value else None), _info_dict(info, bufs)
+
+
+def tls_factor_precond_qr_blocked(M: tls_matrix_t, u_f, stream=None, ws: Optional[torch.Tensor] = None):
+    """Blocked Householder QR in u_f with tensor-core WY trailing updates (R29, NEXT-2).
+    Returns (status, Precond or None, info dict)."""
+    uf = PREC[u_f] if isinstance(u_f, str) else int(u_f)
+    if ws is None:
+        nbytes = int(lib().tls_qr_blocked_workspace_size(C.byref(M), uf))
+        if nbytes == 0:
+            raise TlsError(-1, "tls_qr_blocked_workspace_size")
+        ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    R = C.c_void_p()
+    info, bufs = _info(50)
+    rc = lib().tls_factor_precond_qr_blocked(C.byref(M), uf, _stream(stream), _ptr(ws), ws.numel(), C.byref(R),
+                                             C.byref(info))
+    _check(rc, "tls_factor_precond_qr_blocked")
     return rc, (Precond(R.value, int(M.n), uf) if R.value else None), _info_dict(info, bufs)
 
 
