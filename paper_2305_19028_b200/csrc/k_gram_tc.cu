@@ -37,6 +37,7 @@ constexpr int kTcStages = 4;
 constexpr int kTcAcc = 4;         // TMEM accumulators (4 x 128 columns = all 512): 3 chunks of drain slack
 constexpr int kTcPanel = kTcTile * kTcBK * 2;   // 16 KB: one operand panel (2 TMA boxes of 8 KB)
 constexpr int kTcThreads = 320;
+constexpr size_t kTcSmem = 2 * kTcStages * kTcPanel + 1024 + 512 + 8 * 32 * 33 * 8;   // + the flush staging
 
 // ------------------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
@@ -68,6 +69,25 @@ __device__ __forceinline__ void tc_mma_f16(uint32_t tmem_d, uint64_t adesc, uint
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),   \
         "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), \
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])  \
+      : "r"(taddr)                                                                                               \
+      : "memory")
+
+// fp64 reduction into a partial tile kept in L2 (evict_last): the tiles (36 MB at n = 1024) are
+// re-touched every 64 chunks while ~2 GB of A^ streams through L2 (ncu without the hint: ~1.1 GB
+// of partial-tile traffic each way to DRAM)
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void red_add_keep(double* p, double v, uint64_t pol) {
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+#define TLS_TMEM_LD16(taddr, r)                                                                                  \
+  asm volatile(                                                                                                  \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"      \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),         \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])    \
       : "r"(taddr)                                                                                               \
       : "memory")
 
@@ -238,25 +258,36 @@ k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchun
       }
     }
   } else {
-    // ---------------- epilogue: fp32 chunk sums -> compensated fp32 -> fp64 partial tile
+    // ---------------- epilogue: fp32 chunk sums -> (compensated) fp32 -> fp64 partial tile
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
     const int half = (warp - 2) >> 2;       // column half: 0 -> cols 0..63, 1 -> 64..127
-    const int row = q * 32 + lane;
-    double* out = part + ((size_t)s * gridDim.x + blockIdx.x) * (kTcTile * kTcTile) + (size_t)row * kTcTile + half * 64;
-    float sm[64], cm[64];
+    double* ob = part + ((size_t)s * gridDim.x + blockIdx.x) * (kTcTile * kTcTile) + (size_t)(q * 32) * kTcTile + half * 64;
+    double* stg = reinterpret_cast<double*>(smem + 2 * kTcStages * kTcPanel + 512) + (warp - 2) * 32 * 33;
+    const uint64_t pol = l2_evict_last_policy();
+    float2 sm[32], cm[32];                  // 64 fp32 sums (and Kahan compensations), added pairwise
 #pragma unroll
-    for (int i = 0; i < 64; ++i) { sm[i] = 0.f; cm[i] = 0.f; }
+    for (int i = 0; i < 32; ++i) { sm[i] = make_float2(0.f, 0.f); cm[i] = make_float2(0.f, 0.f); }
     int pending = 0;
-    // flush: fire-and-forget fp64 reductions (RED.ADD.F64) into this CTA's partial
-    // tile (zeroed before the launch); each element has exactly one writer thread, so
-    // its adds are applied in program order (deterministic) and the epilogue never
-    // waits for an L2 round trip.
+    // flush: fire-and-forget fp64 reductions (RED.ADD.F64) into this CTA's partial tile (zeroed
+    // before the launch), coalesced: 32 x 32 blocks transposed through shared memory so that a
+    // warp's reduction covers 32 consecutive columns of one row.  Each element has exactly one
+    // writer thread, so its adds are applied in program order (deterministic) and the epilogue
+    // never waits for an L2 round trip.
     auto flush = [&]() {
 #pragma unroll
-      for (int k = 0; k < 64; ++k) {
-        atomicAdd(out + k, KAHAN ? (double)sm[k] - (double)cm[k] : (double)sm[k]);
-        sm[k] = 0.f;
-        cm[k] = 0.f;
+      for (int cb = 0; cb < 2; ++cb) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float2 v = sm[cb * 16 + e], w = cm[cb * 16 + e];
+          stg[lane * 33 + 2 * e] = KAHAN ? (double)v.x - (double)w.x : (double)v.x;
+          stg[lane * 33 + 2 * e + 1] = KAHAN ? (double)v.y - (double)w.y : (double)v.y;
+          sm[cb * 16 + e] = make_float2(0.f, 0.f);
+          cm[cb * 16 + e] = make_float2(0.f, 0.f);
+        }
+        __syncwarp();
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r) red_add_keep(ob + (size_t)r * kTcTile + cb * 32 + lane, stg[r * 33 + lane], pol);
+        __syncwarp();
       }
       pending = 0;
     };
@@ -280,17 +311,19 @@ k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchun
         if (KAHAN) {
 #pragma unroll
           for (int k = 0; k < 64; ++k) {        // Kahan: |error| <= 2u sum|x| + O(super u^2)
+            float& sk = (k & 1) ? sm[k >> 1].y : sm[k >> 1].x;
+            float& ck = (k & 1) ? cm[k >> 1].y : cm[k >> 1].x;
             const float x = __uint_as_float(k < 32 ? r0[k] : r1[k - 32]);
-            const float y = __fsub_rn(x, cm[k]);
-            const float t = __fadd_rn(sm[k], y);
-            cm[k] = __fsub_rn(__fsub_rn(t, sm[k]), y);
-            sm[k] = t;
+            const float y = __fsub_rn(x, ck);
+            const float t = __fadd_rn(sk, y);
+            ck = __fsub_rn(__fsub_rn(t, sk), y);
+            sk = t;
           }
         } else {
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            sm[k] = __fadd_rn(sm[k], __uint_as_float(r0[k]));
-            sm[k + 32] = __fadd_rn(sm[k + 32], __uint_as_float(r1[k]));
+          for (int k = 0; k < 16; ++k) {
+            sm[k] = __fadd2_rn(sm[k], make_float2(__uint_as_float(r0[2 * k]), __uint_as_float(r0[2 * k + 1])));
+            sm[k + 16] = __fadd2_rn(sm[k + 16], make_float2(__uint_as_float(r1[2 * k]), __uint_as_float(r1[2 * k + 1])));
           }
         }
       }
@@ -303,6 +336,203 @@ k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchun
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTcAcc * kTcTile) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------------------ 2b. SYRK on 128 x 256 blocks
+// k_gram_tc2: k_gram_tc with UMMA N = 256 -- each CTA owns the block (I, P) = tiles (I, 2P) and
+// (I, 2P + 1) of the upper triangle (the lower tile of a diagonal block is computed and dropped).
+// Why (tools/micro/mma_handoff.cu, profiles/r02_mma_handoff.log): with N = 128 a K_t = 64 chunk
+// is 4 MMAs of 64 cycles, and the per-chunk accumulator hand-off (commit, the TMEM ring's
+// barrier round trip, accumulate = 0 restart) adds ~45% to it even with an instant epilogue;
+// with N = 256 a chunk is 512 cycles of MMA and the same hand-off is hidden entirely.  It also
+// loads 24 KB of operand panels per tile and stage instead of 32 KB (the main loop is L2->SM
+// bound).  Two TMEM accumulators of 256 columns; 8 epilogue warps, each draining 128 columns of
+// its lane quarter into 128 fp32 register sums (reading R11 unchanged: fp32 chunk sums of K_t
+// rows, fp32 sums of `super` chunk sums, fp64 flushes, split partials summed in fixed order).
+constexpr int kT2N = 256;
+constexpr int kT2PanelB = kT2N * kTcBK * 2;                 // 32 KB: 4 TMA boxes of 8 KB
+constexpr int kT2Stage = kTcPanel + kT2PanelB;              // 48 KB per stage
+constexpr size_t t2_smem(int stages) { return (size_t)stages * kT2Stage + 1024 + 256 + 8 * 32 * 33 * 4; }   // + flush staging
+
+__host__ __device__ constexpr uint32_t idesc_f16_n(int fmt, int N) {
+  return (1u << 4) | ((uint32_t)fmt << 7) | ((uint32_t)fmt << 10) | (1u << 15) | (1u << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTcTile >> 4) << 24);
+}
+
+static int t2_blocks(int TT) {
+  const int TP = (TT + 1) / 2;
+  int b = 0;
+  for (int I = 0; I < TT; ++I) b += TP - I / 2;
+  return b;
+}
+
+template <int FMT, int kT2Stages>
+__global__ void __launch_bounds__(kTcThreads, 1)
+k_gram_tc2(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchunks, int nsplit, int kpc, int super,
+           double* __restrict__ part, int kb0) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kT2Stages * kT2Stage);
+  uint64_t* empty = full + kT2Stages;
+  uint64_t* tfull = empty + kT2Stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int TP = (TT + 1) / 2;
+  int t = blockIdx.x, I = 0;
+  while (t >= TP - I / 2) { t -= TP - I / 2; ++I; }
+  const int P = I / 2 + t;
+  const bool dblk = (P == I / 2);             // the block holds tile (I, I): A is a half of B
+  const int ahalf = I - 2 * P;
+  const int ntiles = TT * (TT + 1) / 2;
+  const int s = blockIdx.y;
+  const int c0 = (int)((int64_t)nchunks * s / nsplit), c1 = (int)((int64_t)nchunks * (s + 1) / nsplit);
+  const int kb_total = (int)((m + kTcBK - 1) / kTcBK);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kT2Stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(2 * kT2N)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      const uint32_t bytes = dblk ? kT2PanelB : kT2Stage;
+      int it = 0;
+      for (int c = c0; c < c1; ++c) {
+        const int kb1 = min((c + 1) * kpc, kb_total);
+        for (int kb = c * kpc; kb < kb1; ++kb, ++it) {
+          const int st = it % kT2Stages;
+          const uint32_t ph = (uint32_t)(it / kT2Stages) & 1u;
+          if (it >= kT2Stages) mbar_wait(&empty[st], ph ^ 1u);
+          mbar_arrive_expect_tx(&full[st], bytes);
+          const int row = (kb0 + kb) * kTcBK;
+          unsigned char* sa = smem + st * kT2Stage;
+          unsigned char* sb = sa + kTcPanel;
+          if (!dblk) {
+            tma_load_2d(sa, &tmap, I * kTcTile, row, &full[st]);
+            tma_load_2d(sa + kTcPanel / 2, &tmap, I * kTcTile + 64, row, &full[st]);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) tma_load_2d(sb + q * (kTcPanel / 2), &tmap, P * kT2N + 64 * q, row, &full[st]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread): M = 128 (tile row I), N = 256 (tiles 2P, 2P + 1)
+    if (lane == 0) {
+      const uint32_t idesc = idesc_f16_n(FMT, kT2N);
+      // descriptors of stage 0; stage st and K step kk add (st * kT2Stage + kk * 2048) >> 4 to the
+      // start-address field (smem offsets < 256 KB: no carry out of its 14 bits)
+      const uint32_t b00 = smem_u32(smem + kTcPanel);
+      const uint64_t bd0 = sw128_desc(b00, kTcPanel / 2, 1024);
+      const uint64_t ad0 = sw128_desc(dblk ? b00 + (uint32_t)(ahalf * kTcPanel) : smem_u32(smem), kTcPanel / 2, 1024);
+      int it = 0;
+      int st = 0;
+      uint32_t ph = 0;
+      for (int c = c0; c < c1; ++c) {
+        const int j = c - c0;
+        const int buf = j & 1;
+        if (j >= 2) mbar_wait(&tempty[buf], (uint32_t)((j >> 1) - 1) & 1u);
+        tc_fence_after();
+        const uint32_t dtm = tmem_base + (uint32_t)(buf * kT2N);
+        const int kb1 = min((c + 1) * kpc, kb_total);
+        for (int kb = c * kpc; kb < kb1; ++kb, ++it) {
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          const uint64_t so = (uint64_t)((st * kT2Stage) >> 4);
+#pragma unroll
+          for (int kk = 0; kk < kTcBK / 16; ++kk)
+            tc_mma_f16(dtm, ad0 + so + (uint64_t)(kk * 128), bd0 + so + (uint64_t)(kk * 128), idesc,
+                       (kb > c * kpc || kk > 0) ? 1u : 0u);
+          tc_commit(&empty[st]);
+          if (++st == kT2Stages) { st = 0; ph ^= 1u; }
+        }
+        tc_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    // ---------------- epilogue: warp (q, h) drains TMEM lanes 32q.. and columns 128h.. (tile J = 2P + h)
+    const int q = warp & 3;
+    const int h = (warp - 2) >> 2;
+    const int J = 2 * P + h;
+    const bool valid = (J >= I) && (J < TT);
+    const int tix = I * TT - I * (I - 1) / 2 + (J - I);          // upper-triangle index of (I, J)
+    float2 sm[64];                                                 // 128 fp32 sums, added pairwise (FADD2)
+#pragma unroll
+    for (int i = 0; i < 64; ++i) sm[i] = make_float2(0.f, 0.f);
+    float* stg = reinterpret_cast<float*>(smem + kT2Stages * kT2Stage + 256) + (warp - 2) * 32 * 33;
+    const uint64_t pol = l2_evict_last_policy();
+    double* ob = part + ((size_t)s * ntiles + (valid ? tix : 0)) * (kTcTile * kTcTile) + (size_t)(q * 32) * kTcTile;
+    int pending = 0;
+    for (int c = c0; c < c1; ++c) {
+      const int j = c - c0;
+      const int buf = j & 1;
+      mbar_wait(&tfull[buf], (uint32_t)(j >> 1) & 1u);
+      tc_fence_after();
+      if (valid) {
+        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kT2N + h * kTcTile);
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          uint32_t r[16];
+          TLS_TMEM_LD16(ta + g * 16, r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            sm[g * 8 + e] = __fadd2_rn(sm[g * 8 + e], make_float2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (++pending == super || c + 1 == c1) {
+        if (valid) {
+          // coalesced flush: 32 x 32 blocks transposed through shared memory, so that a warp's
+          // fp64 reduction covers 32 consecutive columns of one row (two 128-B lines) instead of
+          // one column of 32 rows (32 lines); each element still has exactly one writer thread
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              stg[lane * 33 + 2 * e] = sm[cb * 16 + e].x;
+              stg[lane * 33 + 2 * e + 1] = sm[cb * 16 + e].y;
+              sm[cb * 16 + e] = make_float2(0.f, 0.f);
+            }
+            __syncwarp();
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) red_add_keep(ob + (size_t)r * kTcTile + cb * 32 + lane, (double)stg[r * 33 + lane], pol);
+            __syncwarp();
+          }
+        }
+        pending = 0;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * kT2N) : "memory");
   }
 }
 
@@ -687,15 +917,28 @@ static int gram_kahan() {
   return e ? atoi(e) != 0 : 0;
 }
 
-static void tc_shape(int64_t m, int n, int K_t, int& TT, int& ntiles, int& nchunks, int& nsplit) {
+// k_gram_tc2 (128 x 256 blocks) for n > 896 (TT >= 8 tiles: measured faster at 2^20 x 1024,
+// 200000 x 2000, 65536 x 2048; slower at n = 256, where a diagonal block wastes half its work);
+// TLS_GRAM_TC=128 / =256 force either kernel; TLS_GRAM_KAHAN uses the 128 x 128 kernel
+static bool gram_tc2_enabled(int n) {
+  const char* e = getenv("TLS_GRAM_TC");
+  if (gram_kahan() || (e && atoi(e) == 128)) return false;
+  if (e && atoi(e) == 256) return true;
+  return (n + kTcTile - 1) / kTcTile >= 8;
+}
+
+static void tc_shape(int64_t m, int n, int K_t, int& TT, int& ntiles, int& nchunks, int& nsplit, bool tc2) {
   TT = (n + kTcTile - 1) / kTcTile;
   ntiles = TT * (TT + 1) / 2;
   nchunks = (int)((m + K_t - 1) / K_t);
   if (nchunks < 1) nchunks = 1;
-  // one wave of persistent-tile CTAs (1 CTA/SM): ntiles * nsplit <= #SMs when possible
-  nsplit = num_sms() / ntiles;
+  // one wave of persistent-tile CTAs (1 CTA/SM): CTAs per split * nsplit <= #SMs when possible
+  nsplit = num_sms() / (tc2 ? t2_blocks(TT) : ntiles);
   if (nsplit > nchunks) nsplit = nchunks;
   if (nsplit < 1) nsplit = 1;
+}
+static void tc_shape(int64_t m, int n, int K_t, int& TT, int& ntiles, int& nchunks, int& nsplit) {
+  tc_shape(m, n, K_t, TT, ntiles, nchunks, nsplit, false);
 }
 
 bool gram_tc_supported(int u_f, int K_t) {
@@ -716,11 +959,14 @@ static size_t fz_ring_bytes(int n, int nsplit) {
 size_t gram_tc_ws_bytes(int64_t m, int n, int K_t) {
   int TT, ntiles, nchunks, nsplit;
   tc_shape(m, n, K_t < kTcBK ? kTcBK : K_t, TT, ntiles, nchunks, nsplit);
+  int ns2 = 0;
+  tc_shape(m, n, K_t < kTcBK ? kTcBK : K_t, TT, ntiles, nchunks, ns2, true);
+  const int nsp = ns2 > nsplit ? ns2 : nsplit;                   // partials for either kernel
   const int npad = (n + 7) / 8 * 8;
   size_t ah = ((size_t)m * npad * 2 + 1023) & ~(size_t)1023;
   const size_t fz = (fz_ring_bytes(n, nsplit) + 1023) & ~(size_t)1023;
   if (fz > ah) ah = fz;
-  return ah + (size_t)nsplit * ntiles * kTcTile * kTcTile * 8;
+  return ah + (size_t)nsp * ntiles * kTcTile * kTcTile * 8;
 }
 
 // TLS_GRAM_FUSED=1 selects the fused kernel.  Measured (tools/time_gram_fused.py, profiles/
@@ -852,13 +1098,23 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
     sd.dev = dev;
   }
   if (nseg > 16) nseg = 16;
-  const size_t smem = 2 * kTcStages * kTcPanel + 1024 + 512;
+  const bool tc2 = gram_tc2_enabled(A.n);
+  if (tc2) tc_shape(A.m, A.n, K_t, TT, ntiles, nchunks, nsplit, true);   // splits of the 128 x 256 blocks
+  // 3 stages (144 KB) measured faster than 4 at 2^20 x 1024, alone (3.46 vs 3.52 ms incl. the
+  // rounding pass) and overlapped with it (3.36 vs 4.80: with 4 stages the SYRK CTA's 226 KB of
+  // shared memory leaves the concurrent rounding pass no L1); TLS_GRAM_STAGES=4 for experiments
+  const char* sge = getenv("TLS_GRAM_STAGES");
+  const int st2 = sge && atoi(sge) == 4 ? 4 : 3;
+  const size_t smem = tc2 ? t2_smem(st2) : kTcSmem;
   const bool kahan = gram_kahan();
   const char* ee = getenv("TLS_GRAM_EPI");   // experiment knob: 0 sync only, 1 + TMEM loads, 2 full
   auto kfn = u_f == TLS_FP16 ? (kahan ? k_gram_tc<0, true> : k_gram_tc<0, false>)
                              : (kahan ? k_gram_tc<1, true> : k_gram_tc<1, false>);
-  TLS_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto kfn2 = u_f == TLS_FP16 ? (st2 == 3 ? k_gram_tc2<0, 3> : k_gram_tc2<0, 4>) : (st2 == 3 ? k_gram_tc2<1, 3> : k_gram_tc2<1, 4>);
+  TLS_CUDA_TRY(cudaFuncSetAttribute(tc2 ? (const void*)kfn2 : (const void*)kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
   TLS_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)nsplit * ntiles * kTcTile * kTcTile * 8, st));
+  const int nblk2 = t2_blocks(TT);
   cudaStream_t rs = nseg > 1 ? sd.s : st;
   if (nseg > 1) {
     TLS_CUDA_TRY(cudaEventRecord(sd.fork, st));                    // D^{-1} and the memset are ready
@@ -887,8 +1143,12 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
     int TTs, nts, ncs, nss;
     tc_shape(rows, A.n, K_t, TTs, nts, ncs, nss);
     const int ns_use = nsplit < ncs ? nsplit : ncs;               // the part buffer holds nsplit splits
-    kfn<<<dim3(ntiles, ns_use), kTcThreads, smem, st>>>(tmap, rows, TT, ncs, ns_use, K_t / kTcBK, gram_super(),
-                                                        ee ? atoi(ee) : 2, part, (int)(r0 / kTcBK), tmap, 0);
+    if (tc2)
+      kfn2<<<dim3(nblk2, ns_use), kTcThreads, smem, st>>>(tmap, rows, TT, ncs, ns_use, K_t / kTcBK, gram_super(), part,
+                                                         (int)(r0 / kTcBK));
+    else
+      kfn<<<dim3(ntiles, ns_use), kTcThreads, smem, st>>>(tmap, rows, TT, ncs, ns_use, K_t / kTcBK, gram_super(),
+                                                          ee ? atoi(ee) : 2, part, (int)(r0 / kTcBK), tmap, 0);
     TLS_LAUNCH_CHECK();
     if (launches) *launches += 2;
   }
@@ -957,7 +1217,7 @@ int launch_tc_atb(int u_f, const uint16_t* a, int64_t lda, const uint16_t* b, in
   int rc = make_map16(&ma, u_f, a, m, kTcTile, lda);
   if (!rc) rc = make_map16(&mb, u_f, b, m, nb, ldb);   // columns past nb: TMA zero fill
   if (rc) return rc;
-  const size_t smem = 2 * kTcStages * kTcPanel + 1024 + 512;
+  const size_t smem = kTcSmem;
   auto kfn = u_f == TLS_FP16 ? k_gram_tc<0, false> : k_gram_tc<1, false>;
   TLS_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   TLS_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)nsplit * ntiles * kTcTile * kTcTile * 8, st));

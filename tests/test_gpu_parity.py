@@ -134,7 +134,23 @@ def test_gram_product_config_bound(T, fmt, m, n):
     """The Gram as tls_factor_precond runs it (K_t = 64 = opts.gram_chunk's default, 64 chunk
     sums per fp64 flush, truncating tensor-core accumulation; reading R11) within the pinned
     two-level bound oracle.rqi.gram_accumulation_bound of the exact Gram, and within that bound
-    plus the oracle's own one-level bound of the oracle's gram_uf (the same K_t)."""
+    plus the oracle's own one-level bound of the oracle's gram_uf (the same K_t).  The default
+    kernel: k_gram_tc2 (128 x 256 blocks) for n > 896, else k_gram_tc; the other one below."""
+    _gram_product_config_bound(T, fmt, m, n)
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+@pytest.mark.parametrize("m,n,tile", [(262144, 1024, "128"), (2100, 513, "256"), (70001, 256, "256")])
+def test_gram_product_config_bound_other_kernel(T, fmt, m, n, tile, monkeypatch):
+    """The same bound for the kernel the default does not pick at that n: k_gram_tc (128 x 128
+    tiles, default for n <= 896; it also serves the blocked QR's A^T B products) at n = 1024, and
+    k_gram_tc2 (128 x 256 blocks, default for n > 896) at n = 513 (odd tile count: a block half
+    outside the matrix) and n = 256 (every block holds a diagonal tile)."""
+    monkeypatch.setenv("TLS_GRAM_TC", tile)
+    _gram_product_config_bound(T, fmt, m, n)
+
+
+def _gram_product_config_bound(T, fmt, m, n):
     P = _problem(m, n, kappa=1e3 if n < 1024 else 1e4)
     d, _ = rqi.column_scaling(P.A)
     rc, G = T.tls_gram(T.matrix(T.dense_operand(dev(P.A))), fmt, dev(d), 64)

@@ -9,6 +9,7 @@ stream), and against the oracle where the result is exactly defined.
   - trsv_ws          per-block mbarriers + st.async DSMEM broadcast inside 8-CTA clusters
   - k_qr_step_v4     per-row team barrier of the in-place update (round 2's race fix)
   - k_gram_fused     ring hand-off counters across CTAs (opt-in path)
+  - k_gram_tc2       the 2-deep TMEM ring, coalesced fp64 flushes through shared memory
   - k_wpcg_step_coop grid barriers + the fused partial reduction
 """
 import os
@@ -123,5 +124,28 @@ def test_fused_gram_bitwise_reproducible(T, monkeypatch):
         assert np.array_equal(_bits(G), ref)
     monkeypatch.setenv("TLS_GRAM_FUSED", "0")
     monkeypatch.setenv("TLS_GRAM_SEGS", "1")          # the unsegmented two-kernel path: same chunking
+    monkeypatch.setenv("TLS_GRAM_TC", "128")          # and the same 128 x 128 tiles and splits
     rc, G0 = T.tls_gram(M, "fp16", d, 64, ws=ws)
     assert np.array_equal(_bits(G0), ref)            # and equal to the two-kernel path
+
+
+@pytest.mark.parametrize("segs", ["8", "1"])
+def test_gram_tc2_bitwise_reproducible(T, monkeypatch, segs):
+    """The default dense Gram (k_gram_tc2, 128 x 256 blocks, rounding overlapped by segments):
+    G bit-identical over repetitions."""
+    monkeypatch.setenv("TLS_GRAM_SEGS", segs)
+    m, n = 300000, 1000                                 # n > 896: the 128 x 256 kernel
+    A = torch.randn((m, n), dtype=torch.float64, device="cuda")
+    M = T.matrix(A)
+    ws = T.workspace(M)
+    d = torch.full((n,), 8.0, dtype=torch.float64, device="cuda")
+    ref = None
+    for i in range(max(3, REPS // 2)):
+        side, _ = _perturb(i)
+        rc, G = T.tls_gram(M, "bf16", d, 64, ws=ws)
+        torch.cuda.synchronize()
+        side.synchronize()
+        assert rc == 0
+        if ref is None:
+            ref = _bits(G)
+        assert np.array_equal(_bits(G), ref)
