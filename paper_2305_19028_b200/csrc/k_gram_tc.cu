@@ -339,6 +339,28 @@ k_gram_tc(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchun
   }
 }
 
+// ------------------------------------------------------------------------------ ring hand-off helpers
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_geq(const int* p, int target, int* err) {
+  for (long it = 0; ld_acquire(p) < target; ++it) {
+    if (it > (1L << 24)) { atomicExch(err, 1); return; }
+    __nanosleep(64);
+  }
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // ------------------------------------------------------------------------------ 2b. SYRK on 128 x 256 blocks
 // k_gram_tc2: k_gram_tc with UMMA N = 256 -- each CTA owns the block (I, P) = tiles (I, 2P) and
 // (I, 2P + 1) of the upper triangle (the lower tile of a diagonal block is computed and dropped).
@@ -367,12 +389,22 @@ static int t2_blocks(int TT) {
   return b;
 }
 
-template <int FMT, int kT2Stages>
-__global__ void __launch_bounds__(kTcThreads, 1)
-k_gram_tc2(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchunks, int nsplit, int kpc, int super,
-           double* __restrict__ part, int kb0) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+// RING (k_gram_fused2's SYRK role): chunk j of split s is read from slot j % R of the split's
+// L2 ring (rows (s R + slot) 64 ..) once ready[s R + slot] >= j / R + 1, and the slot is released
+// (done += 1) as soon as the chunk's panels have landed in shared memory.
+struct T2Ring {
+  int* ready;
+  int* done;
+  int R;
+  int* err;
+  unsigned long long* prof;   // debugging: per CTA [8] ns (k_gram_fused2, TLS_FZ_PROF=1)
+};
+
+template <int FMT, int kT2Stages, bool RING>
+__device__ __forceinline__ void tc2_body(const CUtensorMap* tmap_p, unsigned char* smem, int bidx, int s, int64_t m,
+                                         int TT, int nchunks, int nsplit, int kpc, int super, double* __restrict__ part,
+                                         int kb0, T2Ring rg) {
+  const CUtensorMap& tmap = *tmap_p;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kT2Stages * kT2Stage);
   uint64_t* empty = full + kT2Stages;
   uint64_t* tfull = empty + kT2Stages;
@@ -381,13 +413,12 @@ k_gram_tc2(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchu
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int TP = (TT + 1) / 2;
-  int t = blockIdx.x, I = 0;
+  int t = bidx, I = 0;
   while (t >= TP - I / 2) { t -= TP - I / 2; ++I; }
   const int P = I / 2 + t;
   const bool dblk = (P == I / 2);             // the block holds tile (I, I): A is a half of B
   const int ahalf = I - 2 * P;
   const int ntiles = TT * (TT + 1) / 2;
-  const int s = blockIdx.y;
   const int c0 = (int)((int64_t)nchunks * s / nsplit), c1 = (int)((int64_t)nchunks * (s + 1) / nsplit);
   const int kb_total = (int)((m + kTcBK - 1) / kTcBK);
 
@@ -424,9 +455,25 @@ k_gram_tc2(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchu
         for (int kb = c * kpc; kb < kb1; ++kb, ++it) {
           const int st = it % kT2Stages;
           const uint32_t ph = (uint32_t)(it / kT2Stages) & 1u;
-          if (it >= kT2Stages) mbar_wait(&empty[st], ph ^ 1u);
+          if (it >= kT2Stages) {
+            mbar_wait(&empty[st], ph ^ 1u);
+            if (RING) {       // chunk it - S was consumed (its MMAs are done): free its ring slot
+              // (relaxed: its TMA reads completed before the MMAs could start; a release here cost a
+              // gpu-scope fence per chunk -- measured 3x slower when the MMA thread did it)
+              const int slot = (c - c0 - kT2Stages) % rg.R;
+              asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(rg.done + s * rg.R + slot) : "memory");
+            }
+          }
+          int row = (kb0 + kb) * kTcBK;
+          if (RING) {                                   // kpc == 1: chunk c is block kb
+            const int j = c - c0, slot = j % rg.R;
+            const unsigned long long t0 = rg.prof ? gtime() : 0;
+            wait_geq(&rg.ready[s * rg.R + slot], j / rg.R + 1, rg.err);
+            if (rg.prof) rg.prof[blockIdx.x * 8 + 3] += gtime() - t0;
+            fence_proxy_async_global();                 // generic-proxy writes -> TMA reads
+            row = (s * rg.R + slot) * kTcBK;
+          }
           mbar_arrive_expect_tx(&full[st], bytes);
-          const int row = (kb0 + kb) * kTcBK;
           unsigned char* sa = smem + st * kT2Stage;
           unsigned char* sb = sa + kTcPanel;
           if (!dblk) {
@@ -536,6 +583,16 @@ k_gram_tc2(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchu
   }
 }
 
+template <int FMT, int kT2Stages>
+__global__ void __launch_bounds__(kTcThreads, 1)
+k_gram_tc2(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchunks, int nsplit, int kpc, int super,
+           double* __restrict__ part, int kb0) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  tc2_body<FMT, kT2Stages, false>(&tmap, smem, blockIdx.x, blockIdx.y, m, TT, nchunks, nsplit, kpc, super, part, kb0,
+                                  T2Ring{nullptr, nullptr, 1, nullptr, nullptr});
+}
+
 // ------------------------------------------------------------------------------ 2'. fused rounding + SYRK
 // k_gram_fused: steps 1 and 2 in ONE cooperative launch, with A^ never written to HBM.
 // Every CTA of split s (one per upper 128-tile) also runs 4 converter warps: the 64-row blocks
@@ -578,26 +635,6 @@ struct FzArgs {
   unsigned long long* prof;   // debugging (TLS_FZ_PROF=1): per CTA [8] nanoseconds, else nullptr
 };
 
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void wait_geq(const int* p, int target, int* err) {
-  for (long it = 0; ld_acquire(p) < target; ++it) {
-    if (it > (1L << 24)) { atomicExch(err, 1); return; }
-    __nanosleep(64);
-  }
-}
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
 
 template <int FMT>
 __global__ void __launch_bounds__(kFzThreads, 1)
@@ -867,6 +904,179 @@ k_gram_fused(const __grid_constant__ CUtensorMap tmap, FzArgs fz, int64_t m, int
   }
 }
 
+// ------------------------------------------------------------------------------ 2''. split-role fused Gram
+// k_gram_fused2 (opt-in TLS_GRAM_FUSED=2, n > 896, K_t = 64; A^ "formed on chip,
+// never stored"): ONE cooperative launch of one CTA per SM in two roles.  CTAs [0, nblk2 * nsplit) are
+// k_gram_tc2's SYRK CTAs reading their panels from a per-split L2 ring of kF2R 64-row blocks
+// (tc2_body<RING>); the other CTAs are converters: they stream fp64 A through shared memory with
+// bulk copies (3 pieces of up to 64 KB in flight), form fl_uf(A D^-1) with the same single RNE
+// rounding as k_round_scaled (so G is bit-identical to the two-kernel path with the same splits),
+// and write each block into its ring slot once all nblk2 CTAs of the split have taken the previous
+// generation (done counters), then publish it (ready).  Why split roles: converter warps inside
+// the SYRK CTAs (k_gram_fused) were limited to 4 per SM by the epilogue's registers and ran
+// latency-bound; a whole SM streams ~86 GB/s (tools/micro/conv_bw.cu, profiles/r02_conv_bw.log).
+// Deadlock-free: each converter takes its units in increasing (chunk, split) order, a unit only
+// waits for consumers of an earlier generation, and all CTAs are co-resident (cooperative launch).
+constexpr int kF2R = 32;                 // ring blocks per split
+constexpr int kF2Buf = 3;                // converter pieces in flight
+
+template <int PREC, int prow>
+__device__ __forceinline__ void conv_body(int cv, int ncv, const FzArgs& fz, int64_t m, int nchunks, int nsplit,
+                                          int nblk2, unsigned char* smem) {
+  const int n = fz.n, npad64 = fz.npad64, tid = threadIdx.x;
+  const int64_t ld = fz.ld;
+  double* buf = reinterpret_cast<double*>(smem);                              // [kF2Buf][prow * ld]
+  double* sdinv = buf + (size_t)kF2Buf * prow * ld;                           // [n]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sdinv + ((n + 1) & ~1));        // [kF2Buf]
+  if (tid == 0) {
+    for (int i = 0; i < kF2Buf; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  for (int c = tid; c < n; c += blockDim.x) sdinv[c] = fz.dinv[c];
+  __syncthreads();
+  const int maxch = (nchunks + nsplit - 1) / nsplit;
+  const int64_t total = (int64_t)maxch * nsplit;
+  const int ppu = kTcBK / prow;                                               // pieces per 64-row unit
+  const uint64_t pol = policy_evict_first();
+  struct U { bool any, valid; int s, j, c0s; };
+  auto unit = [&](int64_t p) -> U {
+    U u{};
+    const int64_t idx = cv + (p / ppu) * ncv;
+    if (idx >= total) return u;
+    u.any = true;
+    u.s = (int)(idx % nsplit);
+    u.j = (int)(idx / nsplit);
+    u.c0s = (int)((int64_t)nchunks * u.s / nsplit);
+    u.valid = u.j < (int)((int64_t)nchunks * (u.s + 1) / nsplit) - u.c0s;
+    return u;
+  };
+  auto issue = [&](int64_t p) {                                               // thread 0
+    const U u = unit(p);
+    if (!u.any) return;
+    uint64_t* b = &bar[p % kF2Buf];
+    const int64_t row0 = (int64_t)(u.c0s + u.j) * kTcBK + (p % ppu) * prow;
+    const int64_t rows = u.valid ? (m - row0 < prow ? (m - row0 > 0 ? m - row0 : 0) : prow) : 0;
+    if (rows > 0) {
+      mbar_arrive_expect_tx(b, (uint32_t)(rows * ld * 8));
+      bulk_g2s(buf + (size_t)(p % kF2Buf) * prow * ld, fz.A + row0 * ld, (uint32_t)(rows * ld * 8), b, pol);
+    } else {
+      mbar_arrive(b);
+    }
+  };
+  if (tid == 0)
+    for (int p = 0; p < kF2Buf; ++p) issue(p);
+  uint32_t* ring32 = reinterpret_cast<uint32_t*>(fz.ring);
+  const int pairs = npad64 / 2;
+  int bad = 0;
+  unsigned long long t_ld = 0, t_dn = 0, t_cv = 0, ta = 0, tb = 0;
+  const bool prof = fz.prof != nullptr && tid == 0;
+  for (int64_t p = 0;; ++p) {
+    const U u = unit(p);
+    if (!u.any) break;
+    if (prof) ta = gtime();
+    mbar_wait(&bar[p % kF2Buf], (uint32_t)(p / kF2Buf) & 1u);
+    if (prof) { tb = gtime(); t_ld += tb - ta; }
+    const int sub = (int)(p % ppu);
+    const int slot = u.j % kF2R, gen = u.j / kF2R;
+    if (u.valid) {
+      if (sub == 0) {                                   // the slot's previous block has been taken
+        if (tid == 0 && gen > 0) wait_geq(&fz.done[u.s * kF2R + slot], gen * nblk2, fz.err);
+        __syncthreads();
+        if (prof) { ta = gtime(); t_dn += ta - tb; tb = ta; }
+      }
+      const double* src = buf + (size_t)(p % kF2Buf) * prow * ld;
+      const int64_t row0 = (int64_t)(u.c0s + u.j) * kTcBK + sub * prow;
+      const int64_t rows = m - row0 < prow ? (m - row0 > 0 ? m - row0 : 0) : prow;
+      uint32_t* dst = ring32 + ((int64_t)(u.s * kF2R + slot) * kTcBK + sub * prow) * pairs;
+      for (int cp = tid; cp < pairs; cp += blockDim.x) {
+        const int c = 2 * cp;
+        const double d0 = c < n ? sdinv[c] : 0.0, d1 = c + 1 < n ? sdinv[c + 1] : 0.0;
+#pragma unroll
+        for (int rr = 0; rr < prow; ++rr) {                     // prow independent loads in flight
+          double x0 = 0.0, x1 = 0.0;
+          if (rr < rows) {
+            if (c + 1 < n) {
+              const double2 v = *reinterpret_cast<const double2*>(src + rr * ld + c);
+              x0 = v.x * d0;
+              x1 = v.y * d1;
+            } else if (c < n) {
+              x0 = src[rr * ld + c] * d0;
+            }
+          }
+          const uint16_t h0 = PREC == TLS_FP16 ? f64_to_f16_bits(x0) : f64_to_bf16_bits(x0);   // one RNE rounding
+          const uint16_t h1 = PREC == TLS_FP16 ? f64_to_f16_bits(x1) : f64_to_bf16_bits(x1);
+          const uint32_t lim = PREC == TLS_FP16 ? 0x7c00u : 0x7f80u;
+          bad |= ((h0 & 0x7fffu) >= lim) | ((h1 & 0x7fffu) >= lim);
+          dst[(int64_t)rr * pairs + cp] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+        }
+      }
+    }
+    __syncthreads();                                    // the piece is read and its rows written
+    if (prof) t_cv += gtime() - tb;
+    if (tid == 0) {
+      issue(p + kF2Buf);
+      if (u.valid && sub == ppu - 1) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(fz.ready + u.s * kF2R + slot), "r"(gen + 1) : "memory");
+      }
+    }
+  }
+  if (bad) atomicExch(fz.range, 1);
+  if (prof) {
+    fz.prof[blockIdx.x * 8 + 0] = t_ld;
+    fz.prof[blockIdx.x * 8 + 1] = t_dn;
+    fz.prof[blockIdx.x * 8 + 2] = t_cv;
+  }
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(kTcThreads, 1)
+k_gram_fused2(const __grid_constant__ CUtensorMap rmap, FzArgs fz, int64_t m, int TT, int nchunks, int nsplit,
+              int nblk2, int super, double* __restrict__ part, int prow) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  const int nsy = nblk2 * nsplit;
+  if ((int)blockIdx.x < nsy)
+    tc2_body<FMT, 3, true>(&rmap, smem, blockIdx.x % nblk2, blockIdx.x / nblk2, m, TT, nchunks, nsplit, 1, super, part, 0,
+                           T2Ring{fz.ready, fz.done, kF2R, fz.err, fz.prof});
+  else {
+    constexpr int PREC = FMT == 0 ? TLS_FP16 : TLS_BF16;
+    const int cv = blockIdx.x - nsy, ncv = gridDim.x - nsy;
+    switch (prow) {
+      case 8: conv_body<PREC, 8>(cv, ncv, fz, m, nchunks, nsplit, nblk2, smem); break;
+      case 4: conv_body<PREC, 4>(cv, ncv, fz, m, nchunks, nsplit, nblk2, smem); break;
+      case 2: conv_body<PREC, 2>(cv, ncv, fz, m, nchunks, nsplit, nblk2, smem); break;
+      default: conv_body<PREC, 1>(cv, ncv, fz, m, nchunks, nsplit, nblk2, smem); break;
+    }
+  }
+}
+
+// The split-role plan: nsplit maximising throughput under the measured rates (SYRK ~0.68 us per
+// 128 x 256 block and 64-row chunk at n = 1024; a converter CTA ~86 GB/s of fp64), at least 16
+// converters.  Returns nsplit, or 0 when the fused path does not apply.
+static int fused2_plan(int64_t m, int n, int64_t ld, int sms, int& prow) {
+  const int TT = (n + kTcTile - 1) / kTcTile;
+  const int nblk2 = t2_blocks(TT);
+  prow = 0;
+  for (int r = 8; r >= 1; r >>= 1)
+    if ((int64_t)r * ld * 8 <= 65536) { prow = r; break; }
+  if (prow == 0 || n > kFzMaxN) return 0;
+  const int64_t nchunks = (m + kTcBK - 1) / kTcBK;
+  int best = 0;
+  double bt = 1e30;
+  for (int s = 1; nblk2 * s + 16 <= sms && s <= nchunks; ++s) {
+    const double ts = (double)((nchunks + s - 1) / s) * 0.68e-6;
+    const double tc = (double)m * ld * 8 / ((double)(sms - nblk2 * s) * 86e9);
+    const double t = ts > tc ? ts : tc;
+    if (t < bt) { bt = t; best = s; }
+  }
+  return best;
+}
+
+static size_t conv_smem(int prow, int64_t ld, int n) {
+  return (size_t)kF2Buf * prow * ld * 8 + (size_t)((n + 1) & ~1) * 8 + kF2Buf * 8 + 64;
+}
+
 // ------------------------------------------------------------------------------ 3. split reduction
 __global__ void k_gram_reduce_t(const double* __restrict__ part, int ntiles, int nsplit, int TT, int tile, int n,
                                 double* __restrict__ G) {
@@ -1061,6 +1271,91 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
       return 0;
     }
   }
+  // ---- the split-role fused Gram (k_gram_fused2, opt-in TLS_GRAM_FUSED=2; =1 is k_gram_fused above).
+  // Measured (tools/time_gram_fused2.py, profiles/r02_gram_fused2.txt): G bit-identical to the
+  // two-kernel path with the same splits, but 8.9 ms against 3.27 ms at 2^20 x 1024: sharing L2
+  // with the SYRK's ~10 TB/s of panel reads, a converter SM streams ~44 GB/s instead of the 86 it
+  // reaches alone (tools/micro/conv_bw.cu), and the SYRK CTAs slow down too, so not the default.
+  {
+    const char* fe = getenv("TLS_GRAM_FUSED");
+    const bool want = fe && fe[0] == '2';
+    int prow = 0;
+    int ns2 = (want && gram_tc2_enabled(A.n) && K_t == kTcBK) ? fused2_plan(A.m, A.n, A.ld, sms, prow) : 0;
+    const char* nse = getenv("TLS_GRAM_NSPLIT");                    // test knob: force the split count
+    if (ns2 > 0 && nse && atoi(nse) > 0) {
+      ns2 = atoi(nse);
+      if (ns2 > (sms - 16) / t2_blocks(TT)) ns2 = (sms - 16) / t2_blocks(TT);
+    }
+    const int npad64 = (A.n + 63) / 64 * 64;
+    const size_t ring_bytes = (size_t)ns2 * kF2R * kTcBK * npad64 * 2;
+    int split2 = 0, TT2, nt2, nc2;
+    tc_shape(A.m, A.n, K_t, TT2, nt2, nc2, split2, true);
+    if (ns2 > 0 && ns2 <= split2 && ring_bytes + 2 * (size_t)ns2 * kF2R * 4 + 256 <= a_region) {
+      const int nblk2 = t2_blocks(TT);
+      FzArgs fz;
+      fz.A = A.A;
+      fz.ld = A.ld;
+      fz.n = A.n;
+      fz.dinv = dinv;
+      fz.ring = Ah;
+      fz.npad64 = npad64;
+      fz.ready = reinterpret_cast<int*>(reinterpret_cast<char*>(Ah) + ring_bytes);
+      fz.done = fz.ready + ns2 * kF2R;
+      fz.err = range_flag + 3;            // the factor's flags[4]: a ring hand-off timed out
+      fz.range = range_flag;
+      fz.prof = nullptr;
+      const char* pe = getenv("TLS_FZ_PROF");
+      if (pe && pe[0] == '1') {                  // debugging only: per-CTA wait/work times
+        TLS_CUDA_TRY(cudaMalloc(&fz.prof, (size_t)sms * 8 * 8));
+        TLS_CUDA_TRY(cudaMemsetAsync(fz.prof, 0, (size_t)sms * 8 * 8, st));
+      }
+      TLS_CUDA_TRY(cudaMemsetAsync(fz.ready, 0, 2 * (size_t)ns2 * kF2R * 4, st));
+      TLS_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)ns2 * ntiles * kTcTile * kTcTile * 8, st));
+      CUtensorMap rmap;
+      const cuuint64_t dims[2] = {(cuuint64_t)npad64, (cuuint64_t)ns2 * kF2R * kTcBK};
+      const cuuint64_t strides[1] = {(cuuint64_t)npad64 * 2};
+      const cuuint32_t box[2] = {64, (cuuint32_t)kTcBK};
+      const cuuint32_t estr[2] = {1, 1};
+      const CUresult r = encode_fn()(&rmap, u_f == TLS_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                     2, Ah, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled (fused2 ring) failed (%d)", (int)r);
+        return TLS_ERR_CUDA;
+      }
+      size_t smem2 = t2_smem(3);
+      const size_t cs = conv_smem(prow, A.ld, A.n) + 1024;
+      if (cs > smem2) smem2 = cs;
+      auto kern = u_f == TLS_FP16 ? k_gram_fused2<0> : k_gram_fused2<1>;
+      TLS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      int per_sm = 0;
+      TLS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTcThreads, smem2));
+      if (per_sm >= 1) {
+        int64_t mm = A.m;
+        int tt = TT, nc = nchunks, ns = ns2, nb = nblk2, sup = gram_super(), pr = prow;
+        void* args[] = {(void*)&rmap, &fz, &mm, &tt, &nc, &ns, &nb, &sup, &part, &pr};
+        TLS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(sms), dim3(kTcThreads), args, smem2, st));
+        k_gram_reduce_t<<<ntiles, 256, 0, st>>>(part, ntiles, ns2, TT, kTcTile, A.n, G);
+        TLS_LAUNCH_CHECK();
+        if (fz.prof) {
+          std::vector<unsigned long long> h((size_t)sms * 8);
+          cudaMemcpy(h.data(), fz.prof, h.size() * 8, cudaMemcpyDeviceToHost);
+          const int nsy = nblk2 * ns2;
+          double cv[3] = {}, sy = 0;
+          for (int b = 0; b < sms; ++b) {
+            if (b < nsy) sy += h[b * 8 + 3] / 1e6 / nsy;
+            else for (int k = 0; k < 3; ++k) cv[k] += h[b * 8 + k] / 1e6 / (sms - nsy);
+          }
+          fprintf(stderr, "[fused2] %d SYRK CTAs (%d splits), %d converters; ms per CTA: converter wait-load %.3f "
+                  "wait-done %.3f convert %.3f | SYRK producer wait-ready %.3f\n", nsy, ns2, sms - nsy, cv[0], cv[1], cv[2], sy);
+          cudaFree(fz.prof);
+        }
+        if (launches) *launches += 2;
+        return 0;
+      }
+    }
+  }
   // 1.+2. row segments: k_round_scaled of segment k+1 (side stream) overlaps k_gram_tc of segment
   // k (caller's stream): the rounding pass is HBM-bound, the SYRK L2/latency-bound, and both
   // fit on an SM together (registers 320 x 168 + 256 x 32, one SYRK CTA per SM).  Segment
@@ -1100,6 +1395,8 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
   if (nseg > 16) nseg = 16;
   const bool tc2 = gram_tc2_enabled(A.n);
   if (tc2) tc_shape(A.m, A.n, K_t, TT, ntiles, nchunks, nsplit, true);   // splits of the 128 x 256 blocks
+  if (const char* nse = getenv("TLS_GRAM_NSPLIT"))                         // test knob: fewer splits
+    if (atoi(nse) > 0 && atoi(nse) < nsplit) nsplit = atoi(nse);
   // 3 stages (144 KB) measured faster than 4 at 2^20 x 1024, alone (3.46 vs 3.52 ms incl. the
   // rounding pass) and overlapped with it (3.36 vs 4.80: with 4 stages the SYRK CTA's 226 KB of
   // shared memory leaves the concurrent rounding pass no L1); TLS_GRAM_STAGES=4 for experiments

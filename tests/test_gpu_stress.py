@@ -149,3 +149,29 @@ def test_gram_tc2_bitwise_reproducible(T, monkeypatch, segs):
         if ref is None:
             ref = _bits(G)
         assert np.array_equal(_bits(G), ref)
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+def test_gram_fused2_equals_two_kernel(T, monkeypatch, fmt):
+    """The opt-in split-role fused Gram (k_gram_fused2: converter CTAs write fl_uf(A D^-1) into an
+    L2 ring that the SYRK CTAs read) gives G bit-identical to the two-kernel path (k_round_scaled
+    + k_gram_tc2) run with the same 3 splits and one segment, over repetitions."""
+    m, n = 300001, 1000
+    A = T.dense_operand(torch.randn((m, n), dtype=torch.float64, device="cuda"))
+    M = T.matrix(A)
+    ws = T.workspace(M)
+    d = torch.exp2(torch.randint(-3, 4, (n,), device="cuda").double())
+    monkeypatch.setenv("TLS_GRAM_NSPLIT", "3")
+    monkeypatch.setenv("TLS_GRAM_FUSED", "0")
+    monkeypatch.setenv("TLS_GRAM_SEGS", "1")
+    rc, G0 = T.tls_gram(M, fmt, d, 64, ws=ws)
+    assert rc == 0
+    ref = _bits(G0)
+    monkeypatch.setenv("TLS_GRAM_FUSED", "2")
+    for i in range(3):
+        side, _ = _perturb(i)
+        rc, G = T.tls_gram(M, fmt, d, 64, ws=ws)
+        torch.cuda.synchronize()
+        side.synchronize()
+        assert rc == 0
+        assert np.array_equal(_bits(G), ref)
