@@ -115,27 +115,31 @@ __device__ __forceinline__ double rcp_fast(double x) {
   return fma(r, e, r);
 }
 
+// BS: the diagonal-block size (one warp, registers).  16; 32 was measured slower (POTRF of a
+// 64-tile 54 vs 37 us, n = 2000 factorization 1.86 vs 1.34 ms, profiles/r02_chol_bs.txt): a
+// pivot's shuffles and updates grow with BS on the one-warp critical path faster than the
+// block transitions shrink.
+template <int BS>
 __device__ int potrf_tile(double* S, double* dr, int nb) {
   __shared__ int fail;
-  __shared__ double rowb[2][16];
-  __shared__ double F[16][kTB + 1];      // multipliers of the current block: F[j][i] = U_ji / d_j
-  __shared__ double bdinv[16];           // 1 / d_j of the current block
+  __shared__ double F[BS][kTB + 1];      // multipliers of the current block: F[j][i] = U_ji / d_j
+  __shared__ double bdinv[BS];           // 1 / d_j of the current block
   const int tid = threadIdx.x;
   if (tid == 0) fail = 0;
   __syncthreads();
   PMARK(0);
-  for (int o = 0; o < kTB; o += 16) {
+  for (int o = 0; o < kTB; o += BS) {
     // (1) diagonal block: warp 0, lane t owns column t of the block in registers;
     // row jj of the block is read from lane ii by shuffles (no block barriers)
     if (tid < 32) {
-      const int t = tid & 15;
-      double v[16];
+      const int t = tid & (BS - 1);
+      double v[BS];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = S[(o + i) * kTS + o + t];
+      for (int i = 0; i < BS; ++i) v[i] = S[(o + i) * kTS + o + t];
       int f = 0;
       // no `break`: a loop exit kept the loop rolled and v[] in local memory (measured)
 #pragma unroll
-      for (int jj = 0; jj < 16; ++jj) {
+      for (int jj = 0; jj < BS; ++jj) {
         const double piv = __shfl_sync(0xffffffffu, v[jj], jj);
         if (o + jj < nb && f == 0) {
           if (!(piv > 0.0 && piv < INFINITY)) {      // non-positive, NaN or +inf pivot
@@ -144,16 +148,16 @@ __device__ int potrf_tile(double* S, double* dr, int nb) {
             const double dinv = rcp_fast(piv);
             const double sjt = v[jj];
 #pragma unroll
-            for (int ii = jj + 1; ii < 16; ++ii) {
+            for (int ii = jj + 1; ii < BS; ++ii) {
               const double m = __shfl_sync(0xffffffffu, v[jj], ii) * dinv;
               if (t >= ii) v[ii] = fma(-m, sjt, v[ii]);
             }
           }
         }
       }
-      if (tid < 16) {
+      if (tid < BS) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
+        for (int i = 0; i < BS; ++i)
           if (i <= t) S[(o + i) * kTS + o + t] = v[i];
         // d_t, read back (indexing v[t] with the lane index would put v[] in local memory)
         bdinv[t] = rcp_fast(S[(o + t) * kTS + o + t]);
@@ -163,48 +167,48 @@ __device__ int potrf_tile(double* S, double* dr, int nb) {
     __syncthreads();
     PMARK(1 + (o / 16) * 4);
     if (fail) break;
-    // (2) multipliers of the block and the block row to its right (columns c >= o + 16)
-    for (int e = tid; e < 16 * kTB; e += blockDim.x) {
+    // (2) multipliers of the block and the block row to its right (columns c >= o + BS)
+    for (int e = tid; e < BS * kTB; e += blockDim.x) {
       const int jj = e >> 6, c = e & 63;
       F[jj][c] = (c > o + jj && o + jj < nb) ? S[(o + jj) * kTS + c] * bdinv[jj] : 0.0;   // inside the block for now
     }
     __syncthreads();
-    const int w = kTB - o - 16;                 // columns to the right
+    const int w = kTB - o - BS;                 // columns to the right
     if (tid < w) {
-      const int c = o + 16 + tid;
-      double u[16];
+      const int c = o + BS + tid;
+      double u[BS];
 #pragma unroll
-      for (int jj = 0; jj < 16; ++jj) u[jj] = S[(o + jj) * kTS + c];
+      for (int jj = 0; jj < BS; ++jj) u[jj] = S[(o + jj) * kTS + c];
 #pragma unroll
-      for (int jj = 0; jj < 16; ++jj)
+      for (int jj = 0; jj < BS; ++jj)
 #pragma unroll
-        for (int ii = jj + 1; ii < 16; ++ii) u[ii] = fma(-F[jj][o + ii], u[jj], u[ii]);
+        for (int ii = jj + 1; ii < BS; ++ii) u[ii] = fma(-F[jj][o + ii], u[jj], u[ii]);
 #pragma unroll
-      for (int jj = 0; jj < 16; ++jj) S[(o + jj) * kTS + c] = u[jj];
+      for (int jj = 0; jj < BS; ++jj) S[(o + jj) * kTS + c] = u[jj];
     }
     __syncthreads();
     PMARK(2 + (o / 16) * 4);
     if (w == 0) break;
     // multipliers for the columns right of the block (final U rows of the block)
-    for (int e = tid; e < 16 * w; e += blockDim.x) {
-      const int jj = e / w, c = o + 16 + e % w;
+    for (int e = tid; e < BS * w; e += blockDim.x) {
+      const int jj = e / w, c = o + BS + e % w;
       F[jj][c] = (o + jj < nb) ? S[(o + jj) * kTS + c] * bdinv[jj] : 0.0;
     }
     __syncthreads();
     PMARK(3 + (o / 16) * 4);
-    // (3) trailing update: S_ic -= sum_jj F[jj][i] U[jj][c], o+16 <= i <= c (4 rows at a time)
+    // (3) trailing update: S_ic -= sum_jj F[jj][i] U[jj][c], o+BS <= i <= c (4 rows at a time)
     {
-      const int c = o + 16 + (tid & 63);
+      const int c = o + BS + (tid & 63);
       if (c < kTB) {
-        double uc[16];
+        double uc[BS];
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) uc[jj] = S[(o + jj) * kTS + c];
-        for (int i = o + 16 + (tid >> 6); i <= c; i += 16) {
+        for (int jj = 0; jj < BS; ++jj) uc[jj] = S[(o + jj) * kTS + c];
+        for (int i = o + BS + (tid >> 6); i <= c; i += 16) {
           double acc[4];
 #pragma unroll
           for (int r = 0; r < 4; ++r) acc[r] = (i + 4 * r <= c) ? S[(i + 4 * r) * kTS + c] : 0.0;
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj)
+          for (int jj = 0; jj < BS; ++jj)
 #pragma unroll
             for (int r = 0; r < 4; ++r) acc[r] = fma(-F[jj][min(i + 4 * r, kTB - 1)], uc[jj], acc[r]);
 #pragma unroll
@@ -341,7 +345,7 @@ k_chol_dag(double* __restrict__ G, int n, int T, const int4* __restrict__ tasks,
         __syncthreads();
         TSTAMP(tload);
         const int nb = min(kTB, n - k * kTB);
-        f = potrf_tile(S0, S1, nb);
+        f = potrf_tile<16>(S0, S1, nb);
         TSTAMP(tcomp);
         if (!f) {
           store_tile(G, n, k, k, S0, true);
@@ -414,7 +418,7 @@ k_chol_dag(double* __restrict__ G, int n, int T, const int4* __restrict__ tasks,
             for (int q = 0; q < 4; ++q) S2[(4 * ty + p) * kTS + tx + 16 * q] -= acc[p][q];
         }
         __syncthreads();
-        f = potrf_tile(S2, drj, min(kTB, n - jn * kTB));
+        f = potrf_tile<16>(S2, drj, min(kTB, n - jn * kTB));
         TSTAMP(tcomp);
         if (!f) {
           store_tile(G, n, jn, jn, S2, true);
