@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define TLSRQI_ABI_VERSION 5
+#define TLSRQI_ABI_VERSION 6
 
 #if defined(__GNUC__)
 #define TLS_API __attribute__((visibility("default")))
@@ -169,6 +169,32 @@ TLS_API int tls_comm_init(int nranks, int rank, const void* id_host, int device,
  * tls_comm_destroy (which is collective for this backend). */
 TLS_API int tls_comm_init_shm(int nranks, int rank, const char* name, size_t slot_bytes, int device,
                               tls_comm_t* out);
+/* Peer-memory exchange of the operator pass's sums (the one-shot,
+ * rank-ordered reduction over NVLink instead of ncclAllReduce for the 2n+2 (n+2) pass sums of
+ * PAPER.md Alg. 3 / Alg. 4; k_peer.cu).  Attached to an existing communicator (NCCL or shm, which
+ * still serves the other collectives):
+ *   tls_comm_peer_prepare: allocates this rank's receive buffer (2 x nranks x wcap doubles, wcap >=
+ *     2n + 2 of every solve that uses the communicator) and flags on the communicator's device and
+ *     writes their two CUDA-IPC handles (128 bytes) to handles_out (host);
+ *   every rank then gathers all ranks' 128-byte records in rank order (e.g. torch.distributed
+ *     all_gather) and calls tls_comm_peer_connect(comm, all_handles) (nranks x 128 bytes, host),
+ *     which maps the peers' buffers.
+ * From then on each dense operator/residual pass ends with ONE kernel that reduces this rank's
+ * per-CTA partial sums, stores them into every rank's buffer over peer memory, waits for all
+ * ranks' (flags, system scope) and sums the ranks' contributions in rank order 0..P-1 (identical
+ * bits on every rank; the same order as the shm backend).  The ranks' kernels wait for each
+ * other, so every rank must run on its own GPU, concurrently.  A wait that times out makes the
+ * call return TLS_ERR_NCCL.  Up to 8 ranks.  Errors: TLS_ERR_ARG (order of calls, sizes),
+ * TLS_ERR_CUDA (allocation, IPC). */
+TLS_API int tls_comm_peer_prepare(tls_comm_t comm, int64_t wcap, void* handles_out /* 128 bytes */);
+TLS_API int tls_comm_peer_connect(tls_comm_t comm, const void* all_handles /* nranks x 128 bytes */);
+/* Test hook for the exchange kernel on ONE GPU: nranks emulated ranks in one cooperative launch
+ * (the pool forbids separate launches that wait for each other on one device).  partials: device,
+ * [nranks][G][W] (rank r's G per-CTA rows); out: device, [nranks][W] (rank r's result); `reps`
+ * exchanges in a row (epochs 1..reps: the double-buffered slots are reused).  Allocates and frees
+ * its own buffers; synchronises `stream`. */
+TLS_API int tls_peer_exchange_emulate(int nranks, const double* partials, int G, int W, int reps, double* out,
+                                      void* stream);
 TLS_API int tls_comm_nranks(tls_comm_t comm);   /* 1 for NULL */
 TLS_API int tls_comm_rank(tls_comm_t comm);     /* 0 for NULL */
 TLS_API int tls_comm_destroy(tls_comm_t comm);

@@ -104,6 +104,14 @@ struct tls_comm_s {
   size_t shm_bytes = 0;
   char shm_name[96] = {0};
   double* stage = nullptr;         // pinned staging buffer of slot_bytes
+  // peer-memory exchange of the pass sums (k_peer.cu, tls_comm_peer_prepare / _connect)
+  bool peer = false;
+  PeerTab tab{};
+  double* prbuf = nullptr;         // this rank's receive buffer [2][nranks][pwcap]
+  int* prflag = nullptr;           // this rank's flags [nranks][kXchCtas]
+  int* perr = nullptr;             // device: a wait timed out
+  int pwcap = 0;
+  int pepoch = 0;
 };
 
 struct tls_precond_s {
@@ -212,6 +220,13 @@ static int allreduce_i64(tls_comm_t comm, void* buf, size_t count, cudaStream_t 
 // An NCCL error raised asynchronously (a peer died, a link fault) surfaces at the end of each
 // top-level call as TLS_ERR_NCCL instead of as a later hang.
 static int comm_async_check(tls_comm_t comm) {
+  if (comm != nullptr && comm->peer && comm->perr) {
+    int e = 0;
+    if (cudaMemcpy(&e, comm->perr, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess && e != 0) {
+      set_error("peer exchange: a rank waited too long for the other ranks' pass sums");
+      return TLS_ERR_NCCL;
+    }
+  }
   if (comm == nullptr || comm->comm == nullptr) return 0;
   NcclApi* api = nccl_api();
   if (!api || !api->CommGetAsyncError) return 0;
@@ -542,6 +557,15 @@ int run_pass(Ctx& cx, const tls_matrix_t* A, int mode, int nrhs, const double* q
       ProfScope ps(cat, cx.st);
       TLS_TRY(launch_pass(dv, mode, nrhs, q, b, w.partials, active, cx.st, &G));
     }
+    if (cx.comm && cx.comm->peer && mode != PASS_COLSTATS) {
+      // NEXT-3: this rank's reduction and the all-reduce over ranks in one kernel over peer memory
+      ProfScope ps(TLS_PROF_REDUCE, cx.st);
+      TLS_TRY(launch_reduce_exchange(cx.comm->tab, cx.comm->nranks, cx.comm->rank, 1, w.partials, 0, dv.m > 0 ? G : 0, W,
+                                     cx.comm->pwcap, out, 0, ++cx.comm->pepoch, active, cx.comm->perr, false, cx.st));
+      cx.launches += 2;
+      cx.passes += 1;
+      return 0;
+    }
     if (dv.m > 0) {
       ProfScope ps(TLS_PROF_REDUCE, cx.st);
       TLS_TRY(launch_reduce(w.partials, G, W, mode == PASS_COLSTATS ? dv.n : 0, out, active, cx.st));
@@ -646,6 +670,14 @@ int run_pass32(Ctx& cx, const tls_matrix_t* A, tls_precond_t R, const double* q,
   {
     ProfScope ps(TLS_PROF_PASS_OP2_FP32, cx.st);
     TLS_TRY(launch_pass32(dv, R->a32, q, w.partials, active, cx.st, &G));
+  }
+  if (cx.comm && cx.comm->peer) {
+    ProfScope ps(TLS_PROF_REDUCE, cx.st);
+    TLS_TRY(launch_reduce_exchange(cx.comm->tab, cx.comm->nranks, cx.comm->rank, 1, w.partials, 0, dv.m > 0 ? G : 0, W,
+                                   cx.comm->pwcap, w.passout, 0, ++cx.comm->pepoch, active, cx.comm->perr, false, cx.st));
+    cx.launches += 2;
+    cx.passes += 1;
+    return 0;
   }
   if (dv.m > 0) {
     ProfScope ps(TLS_PROF_REDUCE, cx.st);
@@ -911,7 +943,101 @@ int tls_comm_destroy(tls_comm_t c) {
     if (c->rank == 0) shm_unlink(c->shm_name);
   }
   if (c->stage) cudaFreeHost(c->stage);
+  if (c->peer || c->prbuf) {
+    cudaDeviceSynchronize();
+    for (int p = 0; p < c->nranks && p < kMaxPeers; ++p) {
+      if (p == c->rank) continue;
+      if (c->tab.rbuf[p]) cudaIpcCloseMemHandle(c->tab.rbuf[p]);
+      if (c->tab.rflag[p]) cudaIpcCloseMemHandle(c->tab.rflag[p]);
+    }
+    if (c->prbuf) cudaFree(c->prbuf);
+    if (c->prflag) cudaFree(c->prflag);
+    if (c->perr) cudaFree(c->perr);
+  }
   delete c;
+  return 0;
+}
+
+// ---- peer-memory exchange of the pass sums (NEXT-3; k_peer.cu)
+int tls_comm_peer_prepare(tls_comm_t c, int64_t wcap, void* handles_out) {
+  if (!c || !handles_out || wcap < 4 || wcap > (1 << 24) || c->nranks > kMaxPeers || c->peer || c->prbuf) {
+    set_error("tls_comm_peer_prepare: needs a communicator of <= %d ranks, not yet prepared, 4 <= wcap <= 2^24",
+              kMaxPeers);
+    return TLS_ERR_ARG;
+  }
+  TLS_CUDA_TRY(cudaSetDevice(c->device));
+  const size_t rb = 2 * (size_t)c->nranks * wcap * 8, fb = (size_t)c->nranks * kXchCtas * sizeof(int);
+  TLS_CUDA_TRY(cudaMalloc(&c->prbuf, rb));
+  TLS_CUDA_TRY(cudaMalloc(&c->prflag, fb));
+  TLS_CUDA_TRY(cudaMalloc(&c->perr, sizeof(int)));
+  TLS_CUDA_TRY(cudaMemset(c->prflag, 0, fb));
+  TLS_CUDA_TRY(cudaMemset(c->perr, 0, sizeof(int)));
+  cudaIpcMemHandle_t h[2];
+  TLS_CUDA_TRY(cudaIpcGetMemHandle(&h[0], c->prbuf));
+  TLS_CUDA_TRY(cudaIpcGetMemHandle(&h[1], c->prflag));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  std::memcpy(handles_out, h, 128);
+  c->pwcap = (int)wcap;
+  return 0;
+}
+
+int tls_comm_peer_connect(tls_comm_t c, const void* all_handles) {
+  if (!c || !all_handles || !c->prbuf || c->peer) {
+    set_error("tls_comm_peer_connect: call tls_comm_peer_prepare first (once)");
+    return TLS_ERR_ARG;
+  }
+  TLS_CUDA_TRY(cudaSetDevice(c->device));
+  const char* hb = static_cast<const char*>(all_handles);
+  for (int p = 0; p < c->nranks; ++p) {
+    if (p == c->rank) {
+      c->tab.rbuf[p] = c->prbuf;
+      c->tab.rflag[p] = c->prflag;
+      continue;
+    }
+    cudaIpcMemHandle_t h[2];
+    std::memcpy(h, hb + (size_t)p * 128, 128);
+    void* a = nullptr;
+    void* b = nullptr;
+    TLS_CUDA_TRY(cudaIpcOpenMemHandle(&a, h[0], cudaIpcMemLazyEnablePeerAccess));
+    TLS_CUDA_TRY(cudaIpcOpenMemHandle(&b, h[1], cudaIpcMemLazyEnablePeerAccess));
+    c->tab.rbuf[p] = static_cast<double*>(a);
+    c->tab.rflag[p] = static_cast<int*>(b);
+  }
+  c->peer = true;
+  return 0;
+}
+
+int tls_peer_exchange_emulate(int nranks, const double* partials, int G, int W, int reps, double* out, void* stream) {
+  if (nranks < 1 || nranks > kMaxPeers || G < 0 || W < 1 || reps < 1 || !out || (G > 0 && !partials)) {
+    set_error("tls_peer_exchange_emulate: 1 <= nranks <= %d, W >= 1, reps >= 1", kMaxPeers);
+    return TLS_ERR_ARG;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t rb = 2 * (size_t)nranks * W, fb = (size_t)nranks * kXchCtas;
+  double* bufs = nullptr;
+  int* flags = nullptr;
+  TLS_CUDA_TRY(cudaMalloc(&bufs, rb * nranks * 8));
+  TLS_CUDA_TRY(cudaMalloc(&flags, (fb * nranks + 1) * sizeof(int)));
+  TLS_CUDA_TRY(cudaMemsetAsync(flags, 0, (fb * nranks + 1) * sizeof(int), st));
+  PeerTab t{};
+  for (int p = 0; p < nranks; ++p) {
+    t.rbuf[p] = bufs + (size_t)p * rb;
+    t.rflag[p] = flags + (size_t)p * fb;
+  }
+  int* err = flags + fb * nranks;
+  int rc = 0;
+  for (int e = 1; e <= reps && !rc; ++e)
+    rc = launch_reduce_exchange(t, nranks, 0, nranks, partials, (size_t)G * W, G, W, W, out, (size_t)W, e, nullptr, err, true,
+                                st);
+  int herr = 0;
+  if (!rc) {
+    cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+  }
+  cudaFree(bufs);
+  cudaFree(flags);
+  if (rc) return rc;
+  if (herr) { set_error("tls_peer_exchange_emulate: a wait timed out"); return TLS_ERR_NCCL; }
   return 0;
 }
 

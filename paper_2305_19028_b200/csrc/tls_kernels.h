@@ -36,6 +36,20 @@ int launch_pass32(const DenseView& A, const float* A32, const double* q, double*
 int launch_pass_team(const DenseView& A, int mode, const double* q, const double* b, double* partials,
                      const int* active, cudaStream_t st, int* grid_out);
 // out[w] = sum_g partials[g][w] (max for w < nmax), fixed order.
+// Peer-memory exchange (k_peer.cu, NEXT-3): receive buffers and flags of every rank, as this
+// rank sees them (its own: local pointers; the others': CUDA-IPC peer mappings).
+constexpr int kMaxPeers = 8;
+constexpr int kXchCtas = 128;         // CTAs per rank of k_reduce_exchange (column slices of 32)
+struct PeerTab {
+  double* rbuf[kMaxPeers];            // rank p's receive buffer: [2 parities][P slots][wcap] doubles
+  int* rflag[kMaxPeers];              // rank p's flags: [P ranks][kXchCtas]
+};
+// passout of `ranks_here` ranks (rank0 ..) = rank-ordered sum over all P ranks of each rank's
+// fixed-order reduction of its G partial rows (k_reduce_partials' order); `cooperative` for the
+// one-GPU emulation where all P ranks run in this launch.
+int launch_reduce_exchange(const PeerTab& pt, int P, int rank0, int ranks_here, const double* partials, size_t pstride,
+                           int G, int W, int wcap, double* out, size_t ostride, int epoch, const int* active, int* err,
+                           bool cooperative, cudaStream_t st);
 int launch_reduce(const double* partials, int G, int W, int nmax, double* out, const int* active,
                   cudaStream_t st);
 // d_j = 2^floor(log2 colmax_j), dinv_j = 1/d_j, normA2 = sum_j sumsq_j; *flag = 1 on a zero or

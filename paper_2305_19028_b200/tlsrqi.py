@@ -76,6 +76,9 @@ def lib() -> C.CDLL:
         "tls_comm_init_shm": (C.c_int, [C.c_int, C.c_int, C.c_char_p, SZ, C.c_int, P(VP)]),
         "tls_comm_nranks": (C.c_int, [VP]),
         "tls_comm_rank": (C.c_int, [VP]),
+        "tls_comm_peer_prepare": (C.c_int, [VP, I64, VP]),
+        "tls_comm_peer_connect": (C.c_int, [VP, VP]),
+        "tls_peer_exchange_emulate": (C.c_int, [C.c_int, VP, C.c_int, C.c_int, C.c_int, VP, VP]),
         "tls_workspace_size": (SZ, [M, I32]),
         "tls_factor_precond": (C.c_int, [M, I32, P(tls_rqi_opts_t), VP, VP, VP, SZ, P(VP), P(tls_info_t)]),
         "tls_qr_workspace_size": (SZ, [M, I32, I32]),
@@ -109,6 +112,7 @@ def lib() -> C.CDLL:
 
 EXPORTED = ["tls_abi_version", "tls_rqi_opts_default", "tls_status_string", "tls_last_error",
             "tls_comm_get_unique_id", "tls_comm_init", "tls_comm_init_shm", "tls_comm_nranks", "tls_comm_rank",
+            "tls_comm_peer_prepare", "tls_comm_peer_connect", "tls_peer_exchange_emulate",
             "tls_comm_destroy", "tls_workspace_size",
             "tls_factor_precond", "tls_qr_workspace_size", "tls_factor_precond_qr", "tls_qr_blocked_workspace_size",
             "tls_factor_precond_qr_blocked", "tls_precond_import", "tls_precond_export", "tls_precond_destroy",
@@ -462,6 +466,43 @@ def tls_comm_init_shm(nranks: int, rank: int, name: str, device: int, slot_bytes
     h = C.c_void_p()
     _check(lib().tls_comm_init_shm(nranks, rank, name.encode(), slot_bytes, device, C.byref(h)), "tls_comm_init_shm")
     return h.value
+
+
+def tls_comm_peer_prepare(comm: int, wcap: int) -> bytes:
+    """This rank's 128-byte CUDA-IPC record of its peer-exchange buffers (tlsrqi.h)."""
+    buf = (C.c_char * 128)()
+    _check(lib().tls_comm_peer_prepare(C.c_void_p(comm), int(wcap), buf), "tls_comm_peer_prepare")
+    return bytes(buf)
+
+
+def tls_comm_peer_connect(comm: int, records) -> None:
+    """Map every rank's buffers; `records` = the ranks' 128-byte records in rank order."""
+    blob = b"".join(records)
+    if len(blob) != 128 * len(records):
+        raise ValueError("peer records must be 128 bytes each")
+    _check(lib().tls_comm_peer_connect(C.c_void_p(comm), C.create_string_buffer(blob, len(blob))),
+           "tls_comm_peer_connect")
+
+
+def comm_attach_peer(comm: int, wcap: int, group=None) -> None:
+    """NEXT-3 peer exchange on a communicator whose ranks are processes on DIFFERENT GPUs:
+    prepare, all-gather the ranks' records with torch.distributed (rank order), connect."""
+    import torch.distributed as dist
+    rec = tls_comm_peer_prepare(comm, wcap)
+    recs = [None] * dist.get_world_size(group)
+    dist.all_gather_object(recs, rec, group=group)
+    tls_comm_peer_connect(comm, recs)
+
+
+def tls_peer_exchange_emulate(partials: torch.Tensor, reps: int = 1, stream=None) -> torch.Tensor:
+    """Test hook: the exchange kernel for P emulated ranks in one cooperative launch on this GPU.
+    partials: [P, G, W] fp64 CUDA tensor; returns [P, W] (every rank's pass sums)."""
+    assert partials.is_cuda and partials.dtype == torch.float64 and partials.dim() == 3 and partials.is_contiguous()
+    P, G, W = partials.shape
+    out = torch.empty((P, W), dtype=torch.float64, device=partials.device)
+    _check(lib().tls_peer_exchange_emulate(P, _ptr(partials), G, W, reps, _ptr(out), _stream(stream)),
+           "tls_peer_exchange_emulate")
+    return out
 
 
 def tls_comm_nranks(comm) -> int:

@@ -33,7 +33,7 @@ def test_exports_every_header_symbol(L):
 
 def test_host_entry_points(L):
     from paper_2305_19028_b200 import tlsrqi
-    assert L.tls_abi_version() == 5
+    assert L.tls_abi_version() == 6
     for code, name in tlsrqi.STATUS.items():
         assert tlsrqi.tls_status_string(code) == name
     o = tlsrqi.tls_rqi_opts_default()

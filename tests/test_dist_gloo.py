@@ -203,3 +203,31 @@ def test_row_sharded_qr_preconditioner_world2():
     for rank in range(world):
         r = out[rank]
         assert r["equal_oracle"] and r["d_equal"] and r["replicas"]
+
+
+def _peer_attach_worker(rank, world, port, out):
+    """Host logic of tlsrqi.comm_attach_peer (NEXT-3 peer exchange): every rank prepares its
+    record, the records are all-gathered in rank order and each rank connects with the full,
+    rank-ordered list (the C calls are stubbed: no GPU here)."""
+    import os
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2305_19028_b200 import tlsrqi
+        calls = []
+        tlsrqi.tls_comm_peer_prepare = lambda comm, wcap: bytes([rank]) * 128
+        tlsrqi.tls_comm_peer_connect = lambda comm, recs: calls.append(list(recs))
+        tlsrqi.comm_attach_peer(1234, 2050)
+        out[rank] = calls
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_peer_attach_gathers_records_in_rank_order_world2():
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_peer_attach_worker, args=(world, port, out), nprocs=world, join=True)
+    for rank in range(world):
+        assert out[rank] == [[bytes([0]) * 128, bytes([1]) * 128]]
