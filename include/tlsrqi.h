@@ -272,8 +272,18 @@ TLS_API void tls_precond_destroy(tls_precond_t R);
  * trip count is decided on the device (TLS_PCG_GRAPH=0: host loop; same kernels, same bits).
  * Handle-owned allocations made by the first solve that needs them (freed or pooled by
  * tls_precond_destroy): the explicit inverse W (2 npad^2 doubles, precond_apply = 2 or a
- * sharded solve) and the fp32 copy of the local block (u_p = fp32).  An NCCL error raised
+ * sharded solve) and the fp32 copy of the local block (u_p = fp32); tls_precond_prepare makes
+ * them beforehand, after which the solve allocates nothing.  An NCCL error raised
  * asynchronously is reported as TLS_ERR_NCCL at the end of the call. */
+/* Makes the handle-owned buffers of R that a solve would otherwise allocate on first use, so that
+ * tls_rqi_pcgtls then allocates nothing: what = 1 the explicit inverse W = R~^{-1} and W^T
+ * (2 npad^2 doubles, reading R24), 2 the fp32 copy of this rank's block of A (u_p = fp32, R23;
+ * checked against the handle's content checksum like a solve), 3 both.  ws_dev / ws_bytes as for
+ * tls_rqi_pcgtls (used for what & 2).  Synchronises `stream`.  Errors: TLS_ERR_ARG (what, R of
+ * another A), TLS_ERR_WORKSPACE, TLS_ERR_UNSUPPORTED (fp32 copy of a CSR A or n > 2048),
+ * TLS_ERR_CUDA (allocation). */
+TLS_API int tls_precond_prepare(const tls_matrix_t* A, tls_precond_t R, int32_t what, void* stream, void* ws_dev,
+                                size_t ws_bytes);
 TLS_API int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b_local_dev, const tls_precond_t R,
                    int32_t u, int32_t u_r, double tol, const tls_rqi_opts_t* opts,
                    tls_comm_t comm, void* stream, void* ws_dev, size_t ws_bytes,

@@ -88,6 +88,7 @@ def lib() -> C.CDLL:
         "tls_precond_import": (C.c_int, [I64, I32, VP, VP, D, VP, P(VP)]),
         "tls_precond_export": (C.c_int, [VP, VP, VP, P(D)]),
         "tls_precond_destroy": (None, [VP]),
+        "tls_precond_prepare": (C.c_int, [M, VP, I32, VP, VP, SZ]),
         "tls_rqi_pcgtls": (C.c_int, [M, VP, VP, I32, I32, D, P(tls_rqi_opts_t), VP, VP, VP, SZ, VP,
                                      P(D), P(tls_info_t)]),
         "tls_solve_host_bytes": (SZ, [I64, I64, I64, I32]),
@@ -116,6 +117,7 @@ EXPORTED = ["tls_abi_version", "tls_rqi_opts_default", "tls_status_string", "tls
             "tls_comm_destroy", "tls_workspace_size",
             "tls_factor_precond", "tls_qr_workspace_size", "tls_factor_precond_qr", "tls_qr_blocked_workspace_size",
             "tls_factor_precond_qr_blocked", "tls_precond_import", "tls_precond_export", "tls_precond_destroy",
+            "tls_precond_prepare",
             "tls_rqi_pcgtls", "tls_solve_host_bytes", "tls_solve_host", "tls_colstats", "tls_gram",
             "tls_pass", "tls_pass_fp32", "tls_precond_apply", "tls_round", "tls_profile_enable", "tls_profile_read"]
 
@@ -328,6 +330,15 @@ def tls_precond_import(Rt, d, normA2: float, u_f, stream=None) -> Precond:
     if rc != 0:
         raise TlsError(rc, "tls_precond_import")
     return Precond(R.value, Rt.shape[0], uf)
+
+
+def tls_precond_prepare(M: tls_matrix_t, R: Precond, what: int = 3, stream=None, ws: Optional[torch.Tensor] = None):
+    """Make R's solve-time buffers now (1: explicit inverse W, 2: fp32 copy of A, 3: both), so that
+    tls_rqi_pcgtls allocates nothing (tlsrqi.h)."""
+    if ws is None and what & 2:
+        ws = workspace(M)
+    _check(lib().tls_precond_prepare(C.byref(M), C.c_void_p(R.handle), int(what), _stream(stream), _ptr(ws),
+                                     0 if ws is None else ws.numel()), "tls_precond_prepare")
 
 
 def tls_precond_export(R: Precond):

@@ -102,3 +102,27 @@ def test_peer_capacity_too_small_is_refused(T):
             T.tls_rqi_pcgtls(M, b, R, comm=comm)
     finally:
         T.tls_comm_destroy(comm)
+
+
+def test_precond_prepare_then_solve_allocates_nothing(T):
+    """tls_precond_prepare makes the handle-owned buffers a solve would otherwise allocate on
+    first use (the explicit inverse W, the fp32 copy of A): the solve then
+    leaves the device's free memory unchanged, and gives the same bits as without prepare."""
+    P = tlsgen.dense_problem(65536, 1024, 1e2, 1e-3, 5, twin=True, device="cuda", keep_factors=False)
+    M = T.matrix(P.A)
+    ws = T.workspace(M)
+    o = T.tls_rqi_opts_default(precond_apply=2, u_p="fp32")
+    rc, R0, _ = T.tls_factor_precond(M, "fp16", ws=ws)
+    rc, x0, s0, i0 = T.tls_rqi_pcgtls(M, P.b, R0, opts=o, ws=ws)          # allocates W and the copy itself
+    del R0
+    rc, R, _ = T.tls_factor_precond(M, "fp16", ws=ws)
+    T.tls_precond_prepare(M, R, 3, ws=ws)
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    rc, x, s, info = T.tls_rqi_pcgtls(M, P.b, R, opts=o, ws=ws)
+    torch.cuda.synchronize()
+    assert torch.cuda.mem_get_info()[0] == free0
+    assert info["status"] == i0["status"] == 0 and info["pcg_iters"] == i0["pcg_iters"]
+    assert torch.equal(x, x0) and s == s0
+    with pytest.raises(T.TlsError):
+        T.tls_precond_prepare(M, R, 4, ws=ws)
