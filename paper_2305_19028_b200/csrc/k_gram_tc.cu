@@ -91,6 +91,23 @@ __device__ __forceinline__ void red_add_keep(double* p, double v, uint64_t pol) 
       : "r"(taddr)                                                                                               \
       : "memory")
 
+// TMA multicast: the box lands at the same offset in every CTA of `mask` (cluster) and each
+// destination CTA's mbarrier at `bar`'s offset counts the bytes
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+
 // UMMA shared-memory descriptor, 128-byte swizzle, MN-major canonical layout
 // ((8 elem,8,m),(8 rows,k)) : ((1,8,LBO),(64 elem,SBO)) — what a TMA box of
 // 64 columns (128 B) x 64 rows with CU_TENSOR_MAP_SWIZZLE_128B produces.
@@ -400,7 +417,13 @@ struct T2Ring {
   unsigned long long* prof;   // debugging: per CTA [8] ns (k_gram_fused2, TLS_FZ_PROF=1)
 };
 
-template <int FMT, int kT2Stages, bool RING>
+// MC (2-CTA clusters, TLS_GRAM_MC=1): the two CTAs of a cluster own blocks (2a, P) and
+// (2a + 1, P) -- every block column P has 2P + 2 blocks when TT is even -- and share the
+// 256-column B panel: each loads half of it with TMA multicast into both, so a stage costs the
+// pair 32 + 2 x 16 KB of L2 reads instead of 2 x 48 (the diagonal pair a = P loads B only).  A
+// stage is free again when BOTH CTAs' MMAs are done with it (empty barriers of count 2, commits
+// multicast to the pair).
+template <int FMT, int kT2Stages, bool RING, bool MC = false>
 __device__ __forceinline__ void tc2_body(const CUtensorMap* tmap_p, unsigned char* smem, int bidx, int s, int64_t m,
                                          int TT, int nchunks, int nsplit, int kpc, int super, double* __restrict__ part,
                                          int kb0, T2Ring rg) {
@@ -413,9 +436,16 @@ __device__ __forceinline__ void tc2_body(const CUtensorMap* tmap_p, unsigned cha
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int TP = (TT + 1) / 2;
-  int t = bidx, I = 0;
-  while (t >= TP - I / 2) { t -= TP - I / 2; ++I; }
-  const int P = I / 2 + t;
+  int I = 0, P = 0;
+  if (MC) {                                   // bidx = 2 x pair + rank; pairs (P, a), a = 0..P
+    int pr = bidx >> 1;
+    while (pr >= P + 1) { pr -= P + 1; ++P; }
+    I = 2 * pr + (bidx & 1);
+  } else {
+    int t = bidx;
+    while (t >= TP - I / 2) { t -= TP - I / 2; ++I; }
+    P = I / 2 + t;
+  }
   const bool dblk = (P == I / 2);             // the block holds tile (I, I): A is a half of B
   const int ahalf = I - 2 * P;
   const int ntiles = TT * (TT + 1) / 2;
@@ -425,7 +455,7 @@ __device__ __forceinline__ void tc2_body(const CUtensorMap* tmap_p, unsigned cha
   if (threadIdx.x == 0) {
     for (int i = 0; i < kT2Stages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], MC ? 2 : 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -433,6 +463,7 @@ __device__ __forceinline__ void tc2_body(const CUtensorMap* tmap_p, unsigned cha
     }
     fence_mbar_init();
   }
+  if (MC) cluster_sync_all();                 // the partner's barriers exist before any multicast
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
                  "r"(2 * kT2N)
@@ -480,8 +511,15 @@ __device__ __forceinline__ void tc2_body(const CUtensorMap* tmap_p, unsigned cha
             tma_load_2d(sa, &tmap, I * kTcTile, row, &full[st]);
             tma_load_2d(sa + kTcPanel / 2, &tmap, I * kTcTile + 64, row, &full[st]);
           }
+          if (MC) {
+            const int rk = I & 1;                   // this CTA's half of B, multicast to the pair
 #pragma unroll
-          for (int q = 0; q < 4; ++q) tma_load_2d(sb + q * (kTcPanel / 2), &tmap, P * kT2N + 64 * q, row, &full[st]);
+            for (int q = 2 * rk; q < 2 * rk + 2; ++q)
+              tma_load_2d_mc(sb + q * (kTcPanel / 2), &tmap, P * kT2N + 64 * q, row, &full[st], (uint16_t)3);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) tma_load_2d(sb + q * (kTcPanel / 2), &tmap, P * kT2N + 64 * q, row, &full[st]);
+          }
         }
       }
     }
@@ -512,7 +550,8 @@ __device__ __forceinline__ void tc2_body(const CUtensorMap* tmap_p, unsigned cha
           for (int kk = 0; kk < kTcBK / 16; ++kk)
             tc_mma_f16(dtm, ad0 + so + (uint64_t)(kk * 128), bd0 + so + (uint64_t)(kk * 128), idesc,
                        (kb > c * kpc || kk > 0) ? 1u : 0u);
-          tc_commit(&empty[st]);
+          if (MC) tc_commit_mc(&empty[st], (uint16_t)3);
+          else tc_commit(&empty[st]);
           if (++st == kT2Stages) { st = 0; ph ^= 1u; }
         }
         tc_commit(&tfull[buf]);
@@ -577,20 +616,21 @@ __device__ __forceinline__ void tc2_body(const CUtensorMap* tmap_p, unsigned cha
   }
   tc_fence_before();
   __syncthreads();
+  if (MC) cluster_sync_all();                 // no multicast or remote commit still targets us
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * kT2N) : "memory");
   }
 }
 
-template <int FMT, int kT2Stages>
+template <int FMT, int kT2Stages, bool MC = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_gram_tc2(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchunks, int nsplit, int kpc, int super,
            double* __restrict__ part, int kb0) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  tc2_body<FMT, kT2Stages, false>(&tmap, smem, blockIdx.x, blockIdx.y, m, TT, nchunks, nsplit, kpc, super, part, kb0,
-                                  T2Ring{nullptr, nullptr, 1, nullptr, nullptr});
+  tc2_body<FMT, kT2Stages, false, MC>(&tmap, smem, blockIdx.x, blockIdx.y, m, TT, nchunks, nsplit, kpc, super, part, kb0,
+                                      T2Ring{nullptr, nullptr, 1, nullptr, nullptr});
 }
 
 // ------------------------------------------------------------------------------ 2'. fused rounding + SYRK
@@ -1408,6 +1448,11 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
   auto kfn = u_f == TLS_FP16 ? (kahan ? k_gram_tc<0, true> : k_gram_tc<0, false>)
                              : (kahan ? k_gram_tc<1, true> : k_gram_tc<1, false>);
   auto kfn2 = u_f == TLS_FP16 ? (st2 == 3 ? k_gram_tc2<0, 3> : k_gram_tc2<0, 4>) : (st2 == 3 ? k_gram_tc2<1, 3> : k_gram_tc2<1, 4>);
+  // TLS_GRAM_MC=1: 2-CTA clusters sharing the B panel by TMA multicast (needs an even tile count)
+  const char* mce = getenv("TLS_GRAM_MC");
+  const bool mc = tc2 && mce && mce[0] == '1' && (TT % 2 == 0) && st2 == 3;
+  auto kfn2mc = u_f == TLS_FP16 ? k_gram_tc2<0, 3, true> : k_gram_tc2<1, 3, true>;
+  if (mc) TLS_CUDA_TRY(cudaFuncSetAttribute(kfn2mc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t2_smem(3)));
   TLS_CUDA_TRY(cudaFuncSetAttribute(tc2 ? (const void*)kfn2 : (const void*)kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
   TLS_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)nsplit * ntiles * kTcTile * kTcTile * 8, st));
@@ -1440,7 +1485,22 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
     int TTs, nts, ncs, nss;
     tc_shape(rows, A.n, K_t, TTs, nts, ncs, nss);
     const int ns_use = nsplit < ncs ? nsplit : ncs;               // the part buffer holds nsplit splits
-    if (tc2)
+    if (tc2 && mc) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(nblk2, ns_use);
+      cfg.blockDim = dim3(kTcThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int kbs = (int)(r0 / kTcBK), kpcv = K_t / kTcBK, sup = gram_super();
+      TLS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kfn2mc, tmap, rows, TT, ncs, ns_use, kpcv, sup, part, kbs));
+    } else if (tc2)
       kfn2<<<dim3(nblk2, ns_use), kTcThreads, smem, st>>>(tmap, rows, TT, ncs, ns_use, K_t / kTcBK, gram_super(), part,
                                                          (int)(r0 / kTcBK));
     else

@@ -175,3 +175,26 @@ def test_gram_fused2_equals_two_kernel(T, monkeypatch, fmt):
         side.synchronize()
         assert rc == 0
         assert np.array_equal(_bits(G), ref)
+
+
+@pytest.mark.parametrize("segs", ["1", "8"])
+def test_gram_multicast_clusters_bit_identical(T, monkeypatch, segs):
+    """k_gram_tc2 with 2-CTA clusters sharing the B panel by TMA multicast (opt-in TLS_GRAM_MC=1,
+    empty barriers of count 2 fed by multicast commits) gives G bit-identical to the
+    unclustered kernel, over repetitions."""
+    monkeypatch.setenv("TLS_GRAM_SEGS", segs)
+    m, n = 300001, 1000
+    A = T.dense_operand(torch.randn((m, n), dtype=torch.float64, device="cuda"))
+    M = T.matrix(A)
+    ws = T.workspace(M)
+    d = torch.exp2(torch.randint(-3, 4, (n,), device="cuda").double())
+    monkeypatch.setenv("TLS_GRAM_MC", "0")
+    rc, G0 = T.tls_gram(M, "fp16", d, 64, ws=ws)
+    ref = _bits(G0)
+    monkeypatch.setenv("TLS_GRAM_MC", "1")
+    for i in range(3):
+        side, _ = _perturb(i)
+        rc, G = T.tls_gram(M, "fp16", d, 64, ws=ws)
+        torch.cuda.synchronize()
+        side.synchronize()
+        assert rc == 0 and np.array_equal(_bits(G), ref)
