@@ -392,7 +392,7 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 constexpr int kT2N = 256;
 constexpr int kT2PanelB = kT2N * kTcBK * 2;                 // 32 KB: 4 TMA boxes of 8 KB
 constexpr int kT2Stage = kTcPanel + kT2PanelB;              // 48 KB per stage
-constexpr size_t t2_smem(int stages) { return (size_t)stages * kT2Stage + 1024 + 256 + 8 * 32 * 33 * 4; }   // + flush staging
+constexpr size_t t2_smem(int stages, int ew = 8) { return (size_t)stages * kT2Stage + 1024 + 256 + (size_t)ew * 32 * 33 * 4; }   // + flush staging
 
 __host__ __device__ constexpr uint32_t idesc_f16_n(int fmt, int N) {
   return (1u << 4) | ((uint32_t)fmt << 7) | ((uint32_t)fmt << 10) | (1u << 15) | (1u << 16) |
@@ -423,7 +423,9 @@ struct T2Ring {
 // pair 32 + 2 x 16 KB of L2 reads instead of 2 x 48 (the diagonal pair a = P loads B only).  A
 // stage is free again when BOTH CTAs' MMAs are done with it (empty barriers of count 2, commits
 // multicast to the pair).
-template <int FMT, int kT2Stages, bool RING, bool MC = false>
+// EW: epilogue warps (8: 128 columns each, 10 warps per CTA; 16: 64 columns each, 18 warps, the
+// drain of a chunk split over twice the warps at half the registers per thread).
+template <int FMT, int kT2Stages, bool RING, bool MC = false, int EW = 8>
 __device__ __forceinline__ void tc2_body(const CUtensorMap* tmap_p, unsigned char* smem, int bidx, int s, int64_t m,
                                          int TT, int nchunks, int nsplit, int kpc, int super, double* __restrict__ part,
                                          int kb0, T2Ring rg) {
@@ -459,7 +461,7 @@ __device__ __forceinline__ void tc2_body(const CUtensorMap* tmap_p, unsigned cha
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 8);
+      mbar_init(&tempty[i], EW);
     }
     fence_mbar_init();
   }
@@ -558,18 +560,21 @@ __device__ __forceinline__ void tc2_body(const CUtensorMap* tmap_p, unsigned cha
       }
     }
   } else {
-    // ---------------- epilogue: warp (q, h) drains TMEM lanes 32q.. and columns 128h.. (tile J = 2P + h)
+    // ---------------- epilogue: warp (q, hq) drains TMEM lanes 32q.. and CW columns from hq CW
+    constexpr int CW = kT2N / (EW / 4);                            // 128 (EW = 8) or 64 (EW = 16)
     const int q = warp & 3;
-    const int h = (warp - 2) >> 2;
-    const int J = 2 * P + h;
+    const int hq = (warp - 2) >> 2;
+    const int col0 = hq * CW;                                       // within the 256-column block
+    const int J = 2 * P + col0 / kTcTile;
+    const int tc0 = col0 % kTcTile;                                 // within tile J
     const bool valid = (J >= I) && (J < TT);
     const int tix = I * TT - I * (I - 1) / 2 + (J - I);          // upper-triangle index of (I, J)
-    float2 sm[64];                                                 // 128 fp32 sums, added pairwise (FADD2)
+    float2 sm[CW / 2];                                             // CW fp32 sums, added pairwise (FADD2)
 #pragma unroll
-    for (int i = 0; i < 64; ++i) sm[i] = make_float2(0.f, 0.f);
+    for (int i = 0; i < CW / 2; ++i) sm[i] = make_float2(0.f, 0.f);
     float* stg = reinterpret_cast<float*>(smem + kT2Stages * kT2Stage + 256) + (warp - 2) * 32 * 33;
     const uint64_t pol = l2_evict_last_policy();
-    double* ob = part + ((size_t)s * ntiles + (valid ? tix : 0)) * (kTcTile * kTcTile) + (size_t)(q * 32) * kTcTile;
+    double* ob = part + ((size_t)s * ntiles + (valid ? tix : 0)) * (kTcTile * kTcTile) + (size_t)(q * 32) * kTcTile + tc0;
     int pending = 0;
     for (int c = c0; c < c1; ++c) {
       const int j = c - c0;
@@ -577,9 +582,9 @@ __device__ __forceinline__ void tc2_body(const CUtensorMap* tmap_p, unsigned cha
       mbar_wait(&tfull[buf], (uint32_t)(j >> 1) & 1u);
       tc_fence_after();
       if (valid) {
-        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kT2N + h * kTcTile);
+        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kT2N + col0);
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
+        for (int g = 0; g < CW / 16; ++g) {
           uint32_t r[16];
           TLS_TMEM_LD16(ta + g * 16, r);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -597,7 +602,7 @@ __device__ __forceinline__ void tc2_body(const CUtensorMap* tmap_p, unsigned cha
           // fp64 reduction covers 32 consecutive columns of one row (two 128-B lines) instead of
           // one column of 32 rows (32 lines); each element still has exactly one writer thread
 #pragma unroll
-          for (int cb = 0; cb < 4; ++cb) {
+          for (int cb = 0; cb < CW / 32; ++cb) {
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
               stg[lane * 33 + 2 * e] = sm[cb * 16 + e].x;
@@ -623,14 +628,14 @@ __device__ __forceinline__ void tc2_body(const CUtensorMap* tmap_p, unsigned cha
   }
 }
 
-template <int FMT, int kT2Stages, bool MC = false>
-__global__ void __launch_bounds__(kTcThreads, 1)
+template <int FMT, int kT2Stages, bool MC = false, int EW = 8>
+__global__ void __launch_bounds__(64 + 32 * EW, 1)
 k_gram_tc2(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchunks, int nsplit, int kpc, int super,
            double* __restrict__ part, int kb0) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  tc2_body<FMT, kT2Stages, false, MC>(&tmap, smem, blockIdx.x, blockIdx.y, m, TT, nchunks, nsplit, kpc, super, part, kb0,
-                                      T2Ring{nullptr, nullptr, 1, nullptr, nullptr});
+  tc2_body<FMT, kT2Stages, false, MC, EW>(&tmap, smem, blockIdx.x, blockIdx.y, m, TT, nchunks, nsplit, kpc, super, part,
+                                          kb0, T2Ring{nullptr, nullptr, 1, nullptr, nullptr});
 }
 
 // ------------------------------------------------------------------------------ 2'. fused rounding + SYRK
@@ -1442,7 +1447,10 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
   // shared memory leaves the concurrent rounding pass no L1); TLS_GRAM_STAGES=4 for experiments
   const char* sge = getenv("TLS_GRAM_STAGES");
   const int st2 = sge && atoi(sge) == 4 ? 4 : 3;
-  const size_t smem = tc2 ? t2_smem(st2) : kTcSmem;
+  // TLS_GRAM_EW=16: 16 epilogue warps of 64 columns (experiment)
+  const char* ewe = getenv("TLS_GRAM_EW");
+  const int ew = (ewe && atoi(ewe) == 16 && st2 == 3) ? 16 : 8;
+  const size_t smem = tc2 ? t2_smem(st2, ew) : kTcSmem;
   const bool kahan = gram_kahan();
   const char* ee = getenv("TLS_GRAM_EPI");   // experiment knob: 0 sync only, 1 + TMEM loads, 2 full
   auto kfn = u_f == TLS_FP16 ? (kahan ? k_gram_tc<0, true> : k_gram_tc<0, false>)
@@ -1453,6 +1461,8 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
   const bool mc = tc2 && mce && mce[0] == '1' && (TT % 2 == 0) && st2 == 3;
   auto kfn2mc = u_f == TLS_FP16 ? k_gram_tc2<0, 3, true> : k_gram_tc2<1, 3, true>;
   if (mc) TLS_CUDA_TRY(cudaFuncSetAttribute(kfn2mc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t2_smem(3)));
+  auto kfn2ew = u_f == TLS_FP16 ? k_gram_tc2<0, 3, false, 16> : k_gram_tc2<1, 3, false, 16>;
+  if (ew == 16) TLS_CUDA_TRY(cudaFuncSetAttribute(kfn2ew, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   TLS_CUDA_TRY(cudaFuncSetAttribute(tc2 ? (const void*)kfn2 : (const void*)kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
   TLS_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)nsplit * ntiles * kTcTile * kTcTile * 8, st));
@@ -1500,7 +1510,10 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
       cfg.numAttrs = 1;
       int kbs = (int)(r0 / kTcBK), kpcv = K_t / kTcBK, sup = gram_super();
       TLS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kfn2mc, tmap, rows, TT, ncs, ns_use, kpcv, sup, part, kbs));
-    } else if (tc2)
+    } else if (tc2 && ew == 16)
+      kfn2ew<<<dim3(nblk2, ns_use), 64 + 32 * 16, smem, st>>>(tmap, rows, TT, ncs, ns_use, K_t / kTcBK, gram_super(), part,
+                                                              (int)(r0 / kTcBK));
+    else if (tc2)
       kfn2<<<dim3(nblk2, ns_use), kTcThreads, smem, st>>>(tmap, rows, TT, ncs, ns_use, K_t / kTcBK, gram_super(), part,
                                                          (int)(r0 / kTcBK));
     else
