@@ -24,7 +24,7 @@ def num(d, k):
     except ValueError:
         return float("nan")
     return x * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "ms": 1e-3, "us": 1e-6, "ns": 1e-9}.get(u, 1)
-print("# ncu --set full, one launch each (tools/gpu_round_measure.sh, tools/gpu_kernel_evidence.sh); the SM clock column")
+print("# ncu --set full, one launch each (tools/runs/gpu_round_measure.sh, tools/runs/gpu_kernel_evidence.sh); the SM clock column")
 print("# shows where ncu locked the base clock (1.1 GHz).  DRAM = dram__bytes_read+write; pipes = % of peak sustained active.")
 print(f"{'kernel':46s} {'time':>9s} {'DRAM GB':>8s} {'DRAM%':>6s} {'L2%':>5s} {'tensor%':>8s} {'dmma%':>6s} {'fp64%':>6s} {'issue%':>7s} {'SM clk':>8s}")
 for name, rel in REPS:
