@@ -383,7 +383,17 @@ __global__ void k_reduce_partials(const double* __restrict__ partials, int G, in
   const bool ismax = w < nmax;
   double acc = 0.0;
   if (w < W) {
-    for (int g = g0; g < g1; ++g) {
+    // 8 loads in flight per thread, combined in row order (the same bits as one at a time; the
+    // dependent one-load-per-add loop was L2-latency bound: 9.4 us for 296 x 2050 partials)
+    int g = g0;
+    for (; g + 8 <= g1; g += 8) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = partials[(size_t)(g + k) * W + w];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc = ismax ? fmax(acc, v[k]) : acc + v[k];
+    }
+    for (; g < g1; ++g) {
       const double v = partials[(size_t)g * W + w];
       acc = ismax ? fmax(acc, v) : acc + v;
     }

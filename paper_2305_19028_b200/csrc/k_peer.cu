@@ -38,28 +38,29 @@ __device__ __forceinline__ void st_release_sys(int* p, int v) {
 __global__ void __launch_bounds__(256) k_reduce_exchange(PeerTab pt, int P, int rank0, const double* __restrict__ partials,
                                                         size_t pstride, int G, int W, int wcap,
                                                         double* __restrict__ out, size_t ostride, int epoch,
-                                                        const int* __restrict__ active, int* __restrict__ err) {
+                                                        const int* __restrict__ active, int* __restrict__ err, int cpr) {
   if (active != nullptr && (active[0] | active[1]) == 0) return;   // replicated state: uniform over ranks
-  const int lr = blockIdx.x / kXchCtas, cb = blockIdx.x % kXchCtas;
+  // cpr CTAs per rank (<= kXchCtas; fewer in the one-GPU emulation, where all ranks' CTAs must be
+  // co-resident); CTA cb takes the column blocks cb, cb + cpr, ...
+  const int lr = blockIdx.x / cpr, cb = blockIdx.x % cpr;
   const int r = rank0 + lr;
   const double* part = partials + (size_t)lr * pstride;
   const size_t par = (size_t)(epoch & 1) * P * wcap;                // double buffer by epoch parity
   const int tx = threadIdx.x & 31, grp = threadIdx.x >> 5;
   __shared__ double sm[8][33];
   // ---- 1 + 2: this CTA's column blocks (32 wide, round-robin over the rank's kXchCtas CTAs)
-  for (int w0 = cb * 32; w0 < W; w0 += kXchCtas * 32) {
+  for (int w0 = cb * 32; w0 < W; w0 += cpr * 32) {
     const int w = w0 + tx;
     const int g0 = G * grp / 8, g1 = G * (grp + 1) / 8;
     double acc = 0.0;
     if (w < W) {
       int g = g0;
-      for (; g + 4 <= g1; g += 4) {                  // 4 loads in flight, added in row order
-        const double v0 = part[(size_t)g * W + w], v1 = part[(size_t)(g + 1) * W + w];
-        const double v2 = part[(size_t)(g + 2) * W + w], v3 = part[(size_t)(g + 3) * W + w];
-        acc += v0;
-        acc += v1;
-        acc += v2;
-        acc += v3;
+      for (; g + 8 <= g1; g += 8) {                  // 8 loads in flight, added in row order
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = part[(size_t)(g + k) * W + w];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc += v[k];
       }
       for (; g < g1; ++g) acc += part[(size_t)g * W + w];
     }
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(256) k_reduce_exchange(PeerTab pt, int P, int 
   if (!ok) return;
   const double* rb = pt.rbuf[r] + par;
   if (grp == 0)
-    for (int w = cb * 32 + tx; w < W; w += kXchCtas * 32) {
+    for (int w = cb * 32 + tx; w < W; w += cpr * 32) {
       double acc = rb[w];
       for (int p = 1; p < P; ++p) acc += rb[(size_t)p * wcap + w];
       out[(size_t)lr * ostride + w] = acc;
@@ -108,14 +109,23 @@ int launch_reduce_exchange(const PeerTab& pt, int P, int rank0, int ranks_here, 
     set_error("peer exchange: P = %d (max %d), W = %d > capacity %d", P, kMaxPeers, W, wcap);
     return TLS_ERR_ARG;
   }
-  const dim3 grid(ranks_here * kXchCtas), block(256);
+  int cpr = kXchCtas;
+  if (cooperative) {                  // every rank's CTAs co-resident on this one GPU
+    int per_sm = 0;
+    TLS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_reduce_exchange, 256, 0));
+    const int fit = per_sm * num_sms() / ranks_here;
+    if (fit < cpr) cpr = fit;
+    if (cpr < 1) { set_error("peer exchange emulation: %d ranks do not fit on this GPU", ranks_here); return TLS_ERR_ARG; }
+  }
+  const dim3 grid(ranks_here * cpr), block(256);
   if (cooperative) {
     PeerTab t = pt;
-    void* args[] = {&t, &P, &rank0, (void*)&partials, &pstride, &G, &W, &wcap, &out, &ostride, &epoch, (void*)&active, &err};
+    void* args[] = {&t, &P, &rank0, (void*)&partials, &pstride, &G, &W, &wcap, &out, &ostride, &epoch, (void*)&active, &err,
+                    &cpr};
     TLS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_reduce_exchange, grid, block, args, 0, st));
   } else {
     k_reduce_exchange<<<grid, block, 0, st>>>(pt, P, rank0, partials, pstride, G, W, wcap, out, ostride, epoch, active,
-                                              err);
+                                              err, cpr);
     TLS_LAUNCH_CHECK();
   }
   return 0;

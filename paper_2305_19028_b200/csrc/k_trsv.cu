@@ -545,8 +545,17 @@ __global__ void __launch_bounds__(kWG) k_wpcg_step_coop(PrecondDev pc, PcgVecs v
       const int w = cb * 32 + tx;
       const int g0 = G * grp / 8, g1 = G * (grp + 1) / 8;
       double acc = 0.0;
-      if (w < W)
-        for (int g = g0; g < g1; ++g) acc += partials[(size_t)g * W + w];
+      if (w < W) {
+        int g = g0;                                     // 8 loads in flight, added in row order
+        for (; g + 8 <= g1; g += 8) {
+          double v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = partials[(size_t)(g + k) * W + w];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc += v[k];
+        }
+        for (; g < g1; ++g) acc += partials[(size_t)g * W + w];
+      }
       gs[grp * 33 + tx] = acc;
       __syncthreads();
       if (grp == 0 && w < W) {
