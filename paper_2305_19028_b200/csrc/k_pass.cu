@@ -373,6 +373,7 @@ int launch_pass(const DenseView& A, int mode, int nrhs, const double* q, const d
 }
 
 // --------------------------------------------------------------------------- partial reduction
+constexpr int kRedBatch = 20;   // partial rows in flight per thread: a row group of G = 148 CTAs in one batch
 __global__ void k_reduce_partials(const double* __restrict__ partials, int G, int W, int nmax,
                                   double* __restrict__ out, const int* __restrict__ active) {
   if (active != nullptr && (active[0] | active[1]) == 0) return;
@@ -383,19 +384,16 @@ __global__ void k_reduce_partials(const double* __restrict__ partials, int G, in
   const bool ismax = w < nmax;
   double acc = 0.0;
   if (w < W) {
-    // 8 loads in flight per thread, combined in row order (the same bits as one at a time; the
-    // dependent one-load-per-add loop was L2-latency bound: 9.4 us for 296 x 2050 partials)
-    int g = g0;
-    for (; g + 8 <= g1; g += 8) {
-      double v[8];
+    // a group's rows (<= kRedBatch of them for G <= 8 * kRedBatch) all in flight, combined in
+    // row order (the same bits as one at a time; the dependent one-load-per-add loop was
+    // L2-latency bound: 9.4 us for 296 x 2050 partials; 8 in flight plus a serial tail, round 2)
+    for (int g = g0; g < g1; g += kRedBatch) {
+      double v[kRedBatch];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = partials[(size_t)(g + k) * W + w];
+      for (int k = 0; k < kRedBatch; ++k) v[k] = g + k < g1 ? partials[(size_t)(g + k) * W + w] : 0.0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) acc = ismax ? fmax(acc, v[k]) : acc + v[k];
-    }
-    for (; g < g1; ++g) {
-      const double v = partials[(size_t)g * W + w];
-      acc = ismax ? fmax(acc, v) : acc + v;
+      for (int k = 0; k < kRedBatch; ++k)
+        if (g + k < g1) acc = ismax ? fmax(acc, v[k]) : acc + v[k];
     }
   }
   sm[grp][tx] = acc;

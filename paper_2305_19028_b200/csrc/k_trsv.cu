@@ -19,6 +19,8 @@
 // iteration's back solve; the RQI updates of Alg. 4 (l.238-255) live in
 // k_rqi_eval / k_rqi_update / k_boot_x1.  All reductions are fixed-order.
 #include <cooperative_groups.h>
+#include <cstdio>
+#include <vector>
 
 #include "tls_common.cuh"
 #include "tls_kernels.h"
@@ -86,6 +88,27 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // concurrently with it.
 constexpr int kTW = 8;   // warps of a TRSV CTA
 
+// Built with -DTLS_TRSV_TRACE (TLS_EXTRA_NVCC; diagnostics only) and run with
+// TLS_TRSV_TRACE=<path> (tls_precond_apply): per solution block u, the globaltimer when its
+// owner warp starts solve() (its tile updates are done), when x_{u-1} has arrived and when x_u
+// is published; written by launch_precond_apply as text lines
+// "cta warp u t_solve t_arrived t_published" for RHS 0.  Compiled out by default: a global
+// load per solve() on the chain measurably slowed the solves (tools/trsv_trace.py).
+#ifdef TLS_TRSV_TRACE
+__device__ unsigned long long* g_trsv_trace = nullptr;
+#define TRSV_TRACE_PTR g_trsv_trace
+#else
+#define TRSV_TRACE_PTR ((unsigned long long*)nullptr)
+#endif
+#ifndef TLS_TRSV_RUN
+#define TLS_TRSV_RUN 1
+#endif
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <typename T> struct TileDP { static constexpr int v = SegTraits<T>::NV <= 4 ? 4 : (SegTraits<T>::NV <= 8 ? 2 : 1); };
 
 struct TrsvSm {
@@ -97,7 +120,7 @@ struct TrsvSm {
   double* red;    // [32] block_sum scratch
 };
 // dynamic smem of a TRSV CTA
-static size_t trsv_smem(int npad) {
+__host__ __device__ inline size_t trsv_smem(int npad) {
   return (size_t)npad * 8 + (size_t)kTW * 2048 * 8 + (size_t)kTW * 32 * 8 + (size_t)(npad / 32) * 8 + 32 * 8;
 }
 __device__ __forceinline__ TrsvSm trsv_carve(int npad) {
@@ -179,8 +202,15 @@ __device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv
   for (int i = threadIdx.x; i < NB; i += blockDim.x) mbar_arrive_expect_tx(&sm.bar[i], 256);
   cluster_sync_all();
   // block u (solve order) is owned by CTA u % C, warp (u / C) % kTW; its tiles are
-  // (u, 0 .. u-2) -- the coupling to u-1 is the E block
+  // (u, 0 .. u-2) -- the coupling to u-1 is the E block.  Build-time experiments (round 2,
+  // TLS_EXTRA_NVCC): -DTLS_TRSV_RUN=L, -DTLS_TRSV_EPRE (tools/runs/gpu_r02_t2.sh).
+#if TLS_TRSV_RUN > 1
+  // experiment: runs of L consecutive blocks per CTA (CTA (u / L) % C), most hand-offs CTA-local
+  constexpr int L = TLS_TRSV_RUN;
+  const int first = L * (cr + C * (warp / L)) + warp % L;
+#else
   const int first = cr + C * warp;
+#endif
   const int ustep = C * kTW;
   if (first < NB) {
     double* Dw = sm.D + warp * 2048;
@@ -215,6 +245,9 @@ __device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv
 #pragma unroll
     for (int k = 0; k < NV; ++k) acc[k] = 0.0;
     auto solve = [&]() {
+      unsigned long long* trc = TRSV_TRACE_PTR;
+      unsigned long long t_solve = 0, t_arr = 0;
+      if (trc && lane == 0) t_solve = gtimer();
       // row sums: combine the CPR chunk partials of each row, then move row i's sum to lane i
       double mine = 0.0;
 #pragma unroll
@@ -238,7 +271,27 @@ __device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv
       }
       double xv = z0 + z1;
       if (uc >= 1) {                                     // x_u = z_u - E_u x_{u-1}
+#ifdef TLS_TRSV_EPRE
+        // experiment: E_u's row in registers before the wait, four FMA chains after it
+        double er[32];
+#pragma unroll
+        for (int l = 0; l < 32; ++l) er[l] = Ew[l * 32 + lane];
         mbar_wait_cluster(&sm.bar[uc - 1], ph);
+        if (trc && lane == 0) t_arr = gtimer();
+        const double2* xp = reinterpret_cast<const double2*>(sm.y + 32 * real(uc - 1));
+        double e[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int l = 0; l < 32; l += 4) {
+          const double2 xa = xp[l >> 1], xb = xp[(l >> 1) + 1];
+          e[0] = fma(er[l], xa.x, e[0]);
+          e[1] = fma(er[l + 1], xa.y, e[1]);
+          e[2] = fma(er[l + 2], xb.x, e[2]);
+          e[3] = fma(er[l + 3], xb.y, e[3]);
+        }
+        xv -= (e[0] + e[1]) + (e[2] + e[3]);
+#else
+        mbar_wait_cluster(&sm.bar[uc - 1], ph);
+        if (trc && lane == 0) t_arr = gtimer();
         const double* xp = sm.y + 32 * real(uc - 1);
         double e0 = 0.0, e1 = 0.0;
 #pragma unroll
@@ -247,11 +300,25 @@ __device__ void trsv_ws(const T* __restrict__ M, const double* __restrict__ Dinv
           e1 = fma(Ew[(l + 1) * 32 + lane], xp[l + 1], e1);
         }
         xv -= e0 + e1;
+#endif
       }
       __syncwarp();
       // publish x_u to every CTA of the cluster (including this one)
       const uint32_t ya = y_base + (uint32_t)(o + lane) * 8u, ba = bar_base + (uint32_t)uc * 8u;
+#if TLS_TRSV_RUN > 1
+      const int nxt = ((uc + 1) / TLS_TRSV_RUN) % C;     // experiment: the next block's owner first
+      for (int k = 0; k < C; ++k) {
+        const uint32_t r = (uint32_t)((nxt + k) % C);
+        st_async_f64(mapa_shared(ya, r), xv, mapa_shared(ba, r));
+      }
+#else
       for (int r = 0; r < C; ++r) st_async_f64(mapa_shared(ya, (uint32_t)r), xv, mapa_shared(ba, (uint32_t)r));
+#endif
+      if (trc && lane == 0 && blockIdx.x < (unsigned)C) {
+        const unsigned long long t_pub = gtimer();
+        unsigned long long* e = trc + 6 * (size_t)uc;
+        e[0] = cr; e[1] = warp; e[2] = uc; e[3] = t_solve; e[4] = t_arr; e[5] = t_pub;
+      }
       uc += ustep;
       cc = 0;
       if (uc < NB) stage_dinv_warp(Dw, Dinv + (size_t)real(uc) * 1024, Eblk + (size_t)real(uc) * 1024);
@@ -452,6 +519,32 @@ __global__ void __launch_bounds__(kTriT) k_trtri(PrecondDev pc, double* __restri
 //                 right-hand sides, one warp per row, both RHS in the same read of the row;
 //   k_wpcg_*_mid  the n-vector recurrences of Alg. 3 (l.194-201), one CTA per RHS, with the
 //                 same decisions, state updates and fixed-order reductions as k_pcg_step.
+// One row of a GEMV against up to two vectors in shared memory, lane-strided over [j0, j1)
+// (j0 a multiple of 32): lane l takes j = j0 + l + 32k and adds its products in increasing j,
+// as the plain strided loop does (the same bits), but every load of a 1024-element chunk is
+// issued before the chunk's FMAs -- one L2 round trip per chunk instead of one per few
+// elements (measured: the explicit-inverse step's GEMVs were load-latency bound, VERDICT r01
+// NEXT-3 target).
+__device__ __forceinline__ void row_dot2(const double* __restrict__ Mi, int j0, int j1, const double* v0,
+                                         const double* v1, bool u0, bool u1, double& a0, double& a1, int lane) {
+  for (int c = j0; c < j1; c += 1024) {
+    double m[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const int j = c + lane + 32 * k;
+      m[k] = j < j1 ? __ldg(Mi + j) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const int j = c + lane + 32 * k;
+      if (j < j1) {
+        if (u0) a0 = fma(m[k], v0[j], a0);
+        if (u1) a1 = fma(m[k], v1[j], a1);
+      }
+    }
+  }
+}
+
 // mode 0: s = p = W^T (D^{-1} rhs), omega = 0 (pcg_init); mode 1: w = W^T y with
 // y = D^{-1}(A^T t - sigma^2 q) (variant 0) or D^{-1} q (variant 1); mode 2: q = D^{-1} W p.
 constexpr int kWG = 256;
@@ -485,11 +578,7 @@ __global__ void __launch_bounds__(kWG) k_wgemv_grid(PrecondDev pc, PcgVecs v, co
     // upper rows (W) from the 32-aligned chunk of the diagonal on; lower rows (WT) up to it
     const int j0 = mode == 2 ? (i & ~31) : 0, j1 = mode == 2 ? npad : ((i | 31) + 1);
     double a0 = 0.0, a1 = 0.0;
-    for (int j = j0 + lane; j < j1; j += 32) {
-      const double m = __ldg(Mi + j);
-      if (act[0]) a0 = fma(m, vin[j], a0);
-      if (act[1]) a1 = fma(m, vin[npad + j], a1);
-    }
+    row_dot2(Mi, j0, j1, vin, vin + npad, act[0], act[1], a0, a1, lane);
     a0 = warp_sum(a0);
     a1 = warp_sum(a1);
     if (lane < 2 && act[lane]) {
@@ -529,7 +618,7 @@ __global__ void __launch_bounds__(kWG) k_wpcg_step_coop(PrecondDev pc, PcgVecs v
   const int n = pc.n, npad = pc.npad, tid = threadIdx.x, lane = tid & 31;
   double* vin = wsh;                    // [2][npad]: y, later p'
   double* snb = wsh + 2 * (size_t)npad; // [2][npad]: s'
-  __shared__ double red[32];
+  __shared__ double red[64];
   __shared__ double s_al[2], s_be[2], s_dl[2], s_qq[2], s_eta[2], s_pp[2];
   __shared__ int s_upd[2], s_cont[2], s_brk[2];
   bool act[2];
@@ -546,15 +635,14 @@ __global__ void __launch_bounds__(kWG) k_wpcg_step_coop(PrecondDev pc, PcgVecs v
       const int g0 = G * grp / 8, g1 = G * (grp + 1) / 8;
       double acc = 0.0;
       if (w < W) {
-        int g = g0;                                     // 8 loads in flight, added in row order
-        for (; g + 8 <= g1; g += 8) {
-          double v[8];
+        for (int g = g0; g < g1; g += 20) {             // the group's rows in flight, added in row order
+          double v[20];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) v[k] = partials[(size_t)(g + k) * W + w];
+          for (int k = 0; k < 20; ++k) v[k] = g + k < g1 ? partials[(size_t)(g + k) * W + w] : 0.0;
 #pragma unroll
-          for (int k = 0; k < 8; ++k) acc += v[k];
+          for (int k = 0; k < 20; ++k)
+            if (g + k < g1) acc += v[k];
         }
-        for (; g < g1; ++g) acc += partials[(size_t)g * W + w];
       }
       gs[grp * 33 + tx] = acc;
       __syncthreads();
@@ -580,70 +668,87 @@ __global__ void __launch_bounds__(kWG) k_wpcg_step_coop(PrecondDev pc, PcgVecs v
   for (int i = blockIdx.x * (kWG / 32) + (tid >> 5); i < n; i += nw) {
     const double* Mi = pc.WT + (size_t)i * npad;
     double a0 = 0.0, a1 = 0.0;
-    for (int j = lane; j <= (i | 31); j += 32) {
-      const double m = __ldg(Mi + j);
-      if (act[0]) a0 = fma(m, vin[j], a0);
-      if (act[1]) a1 = fma(m, vin[npad + j], a1);
-    }
+    row_dot2(Mi, 0, (i | 31) + 1, vin, vin + npad, act[0], act[1], a0, a1, lane);
     a0 = warp_sum(a0);
     a1 = warp_sum(a1);
     if (lane < 2 && act[lane]) v.w[(size_t)lane * n + i] = lane == 0 ? a0 : a1;
   }
   grid.sync();
-  // ---- B (redundant in every CTA)
-  for (int r = 0; r < 2; ++r) {
-    if (!act[r]) continue;
-    const size_t off = (size_t)r * n;
-    double e = 0.0;
-    for (int i = tid; i < n; i += kWG) e = fma(v.q[off + i], v.q[off + i], e);
-    const double qq = block_sum(e, red);
-    if (tid == 0) {
-      s_qq[r] = qq;
-      s_upd[r] = 0;
-      s_brk[r] = 0;
-      s_al[r] = 0.0;
-      const double tau = variant == 0 ? passout[(size_t)pass_nrhs * n + r] : S->pp[r];
-      const double delta = tau - sig2 * qq;                     // l.194 (R1)
-      s_dl[r] = delta;
-      if (!isfinite(delta) || delta == 0.0) {                   // loop guard l.192 (R3)
-      } else if (delta < 0.0 && rule == 0) {                    // breakdown (R3)
-        s_brk[r] = 1;
-      } else {
-        s_al[r] = S->eta[r] / delta;                            // l.195
-        s_upd[r] = 1;
-      }
-    }
-    __syncthreads();
-    s_cont[r] = 0;
-    if (!s_upd[r]) continue;
-    const double al = s_al[r];
-    e = 0.0;
+  // ---- B (redundant in every CTA; both right-hand sides share each fixed-order block sum --
+  // block_sum2: the same bits as one block_sum per RHS, half the barriers)
+  {
+    double e0 = 0.0, e1 = 0.0;
     for (int i = tid; i < n; i += kWG) {
-      const double q = v.q[off + i];
-      if (blockIdx.x == 0) v.omega[off + i] = fma(al, q, v.omega[off + i]);   // l.196 (only CTA 0 reads omega)
-      const double w = variant == 0 ? v.w[off + i] : fma(-sig2, v.w[off + i], v.p[off + i]);   // l.197
-      const double sn = fma(-al, w, v.s[off + i]);             // l.198
-      snb[(size_t)r * npad + i] = sn;
-      e = fma(sn, sn, e);
+      if (act[0]) e0 = fma(v.q[i], v.q[i], e0);
+      if (act[1]) e1 = fma(v.q[n + i], v.q[n + i], e1);
     }
-    const double etan = block_sum(e, red);                      // l.199
-    __syncthreads();
+    double qq[2];
+    block_sum2(e0, e1, red, qq[0], qq[1]);
     if (tid == 0) {
-      s_eta[r] = etan;
-      if (!(etan <= S->tol2 * S->eta0[r])) { s_be[r] = etan / S->eta[r]; s_cont[r] = 1; }   // R3; l.200
-    }
-    __syncthreads();
-    e = 0.0;
-    if (s_cont[r]) {
-      const double be = s_be[r];
-      for (int i = tid; i < npad; i += kWG) {
-        const double pn = i < n ? fma(be, v.p[off + i], snb[(size_t)r * npad + i]) : 0.0;   // l.201
-        vin[(size_t)r * npad + i] = pn;
-        e = fma(pn, pn, e);
+      for (int r = 0; r < 2; ++r) {
+        s_upd[r] = 0;
+        s_brk[r] = 0;
+        s_cont[r] = 0;
+        s_al[r] = 0.0;
+        if (!act[r]) continue;
+        s_qq[r] = qq[r];
+        const double tau = variant == 0 ? passout[(size_t)pass_nrhs * n + r] : S->pp[r];
+        const double delta = tau - sig2 * qq[r];                // l.194 (R1)
+        s_dl[r] = delta;
+        if (!isfinite(delta) || delta == 0.0) {                 // loop guard l.192 (R3)
+        } else if (delta < 0.0 && rule == 0) {                  // breakdown (R3)
+          s_brk[r] = 1;
+        } else {
+          s_al[r] = S->eta[r] / delta;                          // l.195
+          s_upd[r] = 1;
+        }
       }
     }
-    const double ppn = block_sum(e, red);
-    if (tid == 0) s_pp[r] = ppn;
+    __syncthreads();
+    bool upd[2];
+    double al[2];
+    for (int r = 0; r < 2; ++r) { upd[r] = act[r] && s_upd[r]; al[r] = s_al[r]; }
+    double es[2] = {0.0, 0.0};
+    for (int i = tid; i < n; i += kWG) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        if (!upd[r]) continue;
+        const size_t off = (size_t)r * n;
+        const double q = v.q[off + i];
+        if (blockIdx.x == 0) v.omega[off + i] = fma(al[r], q, v.omega[off + i]);   // l.196 (only CTA 0 reads omega)
+        const double w = variant == 0 ? v.w[off + i] : fma(-sig2, v.w[off + i], v.p[off + i]);   // l.197
+        const double sn = fma(-al[r], w, v.s[off + i]);        // l.198
+        snb[(size_t)r * npad + i] = sn;
+        es[r] = fma(sn, sn, es[r]);
+      }
+    }
+    double etan[2];
+    block_sum2(es[0], es[1], red, etan[0], etan[1]);           // l.199
+    if (tid == 0) {
+      for (int r = 0; r < 2; ++r) {
+        if (!upd[r]) continue;
+        s_eta[r] = etan[r];
+        if (!(etan[r] <= S->tol2 * S->eta0[r])) { s_be[r] = etan[r] / S->eta[r]; s_cont[r] = 1; }   // R3; l.200
+      }
+    }
+    __syncthreads();
+    bool cont[2];
+    double be[2];
+    for (int r = 0; r < 2; ++r) { cont[r] = upd[r] && s_cont[r]; be[r] = s_be[r]; }
+    double ep[2] = {0.0, 0.0};
+    for (int i = tid; i < npad; i += kWG) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        if (!cont[r]) continue;
+        const size_t off = (size_t)r * n;
+        const double pn = i < n ? fma(be[r], v.p[off + i], snb[(size_t)r * npad + i]) : 0.0;   // l.201
+        vin[(size_t)r * npad + i] = pn;
+        ep[r] = fma(pn, pn, ep[r]);
+      }
+    }
+    double ppn[2];
+    block_sum2(ep[0], ep[1], red, ppn[0], ppn[1]);
+    if (tid == 0) { s_pp[0] = ppn[0]; s_pp[1] = ppn[1]; }
     __syncthreads();
   }
   grid.sync();                          // every CTA has read the old q, s, p
@@ -679,11 +784,7 @@ __global__ void __launch_bounds__(kWG) k_wpcg_step_coop(PrecondDev pc, PcgVecs v
   for (int i = blockIdx.x * (kWG / 32) + (tid >> 5); i < n; i += nw) {
     const double* Mi = pc.W + (size_t)i * npad;
     double a0 = 0.0, a1 = 0.0;
-    for (int j = (i & ~31) + lane; j < npad; j += 32) {
-      const double m = __ldg(Mi + j);
-      if (nq[0]) a0 = fma(m, vin[j], a0);
-      if (nq[1]) a1 = fma(m, vin[npad + j], a1);
-    }
+    row_dot2(Mi, i & ~31, npad, vin, vin + npad, nq[0], nq[1], a0, a1, lane);
     a0 = warp_sum(a0);
     a1 = warp_sum(a1);
     if (lane < 2 && nq[lane]) v.q[(size_t)lane * n + i] = (lane == 0 ? a0 : a1) * pc.dinv[i];
@@ -880,10 +981,76 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_init(PrecondDev pc, int nrh
 // reads its inputs before rank 0 writes anything (cluster barriers), so the replicas
 // take identical decisions.
 constexpr int kVecPerThread = 16;  // npad <= kTW * 32 * 16 = 4096
+// NEXT-3 (partials != nullptr): the operator pass's per-CTA partial rows are reduced here
+// instead of by a k_reduce_partials launch: CTA c of RHS r's cluster sums the columns
+// [c*cw, (c+1)*cw) of v_r (cw = ceil(n / C)) and CTA 0 also t_r^T t_r, in
+// k_reduce_partials' fixed order (8 row groups of the G partial rows, each summed in row
+// order, then the group sums in order: the same bits), and stores them into every CTA's
+// staging vector through DSMEM; a cluster barrier publishes them.  passout is then unused.
+__device__ __forceinline__ void step_reduce_partials(const double* __restrict__ partials, int G, int n, int pass_nrhs,
+                                                     int r, double* stage, double* gs) {
+  const int C = (int)cluster_nctarank(), c = (int)cluster_ctarank();
+  const int tid = threadIdx.x, grp = tid >> 5, tx = tid & 31;
+  const int cw = (n + C - 1) / C, c0 = c * cw, c1 = min(n, c0 + cw);
+  const size_t Wp = (size_t)pass_nrhs * n + 2;
+  const int g0 = G * grp / 8, g1 = G * (grp + 1) / 8;
+  const double* base = partials + (size_t)r * n;
+  const int cwp = cw + 1;                         // gs: [8][cw + 1], tau in the last column
+  for (int cb = c0; cb < c1; cb += 64) {          // 2 column blocks of 32 per pass, 2 x 20 rows in flight
+    double acc[2];
+    bool ok[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) { acc[k] = 0.0; ok[k] = cb + 32 * k + tx < c1; }
+    for (int g = g0; g < g1; g += 20) {
+      double vv[20][2];
+#pragma unroll
+      for (int u = 0; u < 20; ++u)
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          vv[u][k] = (ok[k] && g + u < g1) ? base[(size_t)(g + u) * Wp + cb + 32 * k + tx] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 20; ++u)
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          if (g + u < g1) acc[k] += vv[u][k];
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (ok[k]) gs[grp * cwp + (cb - c0) + 32 * k + tx] = acc[k];
+  }
+  if (c == 0 && tx == 0) {                        // tau_r = t_r^T t_r (CTA 0: c1 > c0 always)
+    double a = 0.0;
+    const double* tp = partials + (size_t)pass_nrhs * n + r;
+    for (int g = g0; g < g1; g += 20) {           // the group's rows in flight, added in row order
+      double vv[20];
+#pragma unroll
+      for (int u = 0; u < 20; ++u) vv[u] = g + u < g1 ? tp[(size_t)(g + u) * Wp] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 20; ++u)
+        if (g + u < g1) a += vv[u];
+    }
+    gs[grp * cwp + cw] = a;
+  }
+  __syncthreads();
+  const uint32_t sb = smem_u32(stage);
+  for (int j = tid; j <= c1 - c0; j += blockDim.x) {
+    const bool tau = j == c1 - c0;
+    if (tau && c != 0) continue;
+    const int jj = tau ? cw : j;
+    double t = gs[jj];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) t += gs[k * cwp + jj];
+    const uint32_t a = sb + (uint32_t)(tau ? n : c0 + j) * 8u;
+    for (int q = 0; q < C; ++q) st_cluster_f64(mapa_shared(a, (uint32_t)q), t);
+  }
+  cluster_sync_all();                             // every CTA's stage is complete
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_step(PrecondDev pc, PcgVecs v, const double* __restrict__ passout,
                                                        PcgState* __restrict__ S, int nrhs, int rule, int next_q,
-                                                       int variant, int pass_nrhs, const int* __restrict__ nq_dev) {
+                                                       int variant, int pass_nrhs, const int* __restrict__ nq_dev,
+                                                       const double* __restrict__ partials, int G) {
   if (nq_dev) next_q = *nq_dev;         // graph-captured loop (NEXT-3): decided on the device
   __shared__ double s_alpha, s_beta, s_delta;
   __shared__ int s_upd, s_cont, s_brk, s_exit;
@@ -895,6 +1062,17 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_step(PrecondDev pc, PcgVecs
   const int n = pc.n, npad = pc.npad, tid = threadIdx.x;
   const size_t off = (size_t)r * n;
   const double sig2 = S->sigma2;
+  // the reduced pass output of this RHS: [v_r (n), tau_r] in shared memory (fused) or passout
+  double* stage = sm.y + trsv_smem(npad) / 8;     // after the TRSV layout (launch_pcg_step sizes it)
+  const double* pv = passout + off;
+  double tau_r = 0.0;
+  if (partials != nullptr) {
+    step_reduce_partials(partials, G, n, pass_nrhs, r, stage, sm.D);
+    pv = stage;
+    tau_r = stage[n];
+  } else if (variant == 0) {
+    tau_r = passout[(size_t)pass_nrhs * n + r];
+  }
   if (tid == 0) {
     s_upd = 0;
     s_brk = 0;
@@ -902,7 +1080,7 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_step(PrecondDev pc, PcgVecs
     s_alpha = 0.0;
     // l.194: delta = p^T C p = t^T t - sigma^2 q^T q with the operator of l.324 (variant 0),
     // or p^T p - sigma^2 q^T q as printed (variant 1, the exact-R identity of l.206)
-    const double tau = variant == 0 ? passout[(size_t)pass_nrhs * n + r] : S->pp[r];
+    const double tau = variant == 0 ? tau_r : S->pp[r];
     const double delta = tau - sig2 * S->qq[r];
     s_delta = delta;
     if (!isfinite(delta) || delta == 0.0) {                 // loop guard l.192 (R3)
@@ -935,7 +1113,7 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_step(PrecondDev pc, PcgVecs
       const double q = v.q[off + i];
       if (rank0) v.omega[off + i] = fma(al, q, v.omega[off + i]);
       // variant 0: w = P^{-T}(A^T t - sigma^2 q); variant 1: solve P^{-T} q (l.197)
-      yv = (variant == 0 ? passout[off + i] - sig2 * q : q) * pc.dinv[i];
+      yv = (variant == 0 ? pv[i] - sig2 * q : q) * pc.dinv[i];
     }
     sm.y[i] = yv;
   }
@@ -1117,7 +1295,37 @@ static int launch_cluster(void (*kern)(KArgs...), int clusters, size_t smem, cud
 int launch_precond_apply(const PrecondDev& pc, int trans, int nrhs, double* Y, int ldY, cudaStream_t st) {
   const size_t sm = trsv_smem(pc.npad);
   int rc = 0;
+#ifdef TLS_TRSV_TRACE
+  const char* tpath = getenv("TLS_TRSV_TRACE");
+#else
+  const char* tpath = nullptr;
+#endif
+  static unsigned long long* tbuf = nullptr;
+  const int NB = pc.npad / 32;
+  if (tpath) {
+    if (!tbuf) TLS_CUDA_TRY(cudaMalloc(&tbuf, 6 * 8 * 256));
+    TLS_CUDA_TRY(cudaMemsetAsync(tbuf, 0, 6 * 8 * 256, st));
+#ifdef TLS_TRSV_TRACE
+    TLS_CUDA_TRY(cudaMemcpyToSymbolAsync(g_trsv_trace, &tbuf, sizeof(tbuf), 0, cudaMemcpyHostToDevice, st));
+#endif
+  }
   TLS_DISPATCH_UF(pc.u_f, { rc = launch_cluster(k_precond_apply<T>, nrhs, sm, st, pc, trans, Y, ldY); });
+  if (tpath && rc == 0 && NB <= 256) {
+#ifdef TLS_TRSV_TRACE
+    unsigned long long* none = nullptr;
+    TLS_CUDA_TRY(cudaMemcpyToSymbolAsync(g_trsv_trace, &none, sizeof(none), 0, cudaMemcpyHostToDevice, st));
+#endif
+    std::vector<unsigned long long> h(6 * (size_t)NB);
+    TLS_CUDA_TRY(cudaMemcpyAsync(h.data(), tbuf, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    TLS_CUDA_TRY(cudaStreamSynchronize(st));
+    FILE* f = fopen(tpath, "w");
+    if (f) {
+      for (int u = 0; u < NB; ++u)
+        fprintf(f, "%llu %llu %llu %llu %llu %llu\n", h[6 * u], h[6 * u + 1], h[6 * u + 2], h[6 * u + 3], h[6 * u + 4],
+                h[6 * u + 5]);
+      fclose(f);
+    }
+  }
   return rc;
 }
 
@@ -1183,14 +1391,11 @@ int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgS
                                     partials, G, pout, nq_dev));
     return 0;
   }
-  if (partials != nullptr) {
-    set_error("launch_pcg_step: the fused reduction needs the explicit-inverse step");
-    return TLS_ERR_ARG;
-  }
-  const size_t sm = trsv_smem(pc.npad);
+  // partials: the fused reduction (step_reduce_partials) needs a staging vector after the TRSV layout
+  const size_t sm = trsv_smem(pc.npad) + (partials ? ((size_t)pc.npad + 32) * 8 : 0);
   int rc = 0;
   TLS_DISPATCH_UF(pc.u_f, { rc = launch_cluster(k_pcg_step<T>, nrhs, sm, st, pc, v, passout, S, nrhs, rule, next_q,
-                                                variant, pass_nrhs, nq_dev); });
+                                                variant, pass_nrhs, nq_dev, partials, G); });
   return rc;
 }
 

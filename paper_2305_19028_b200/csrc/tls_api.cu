@@ -1532,10 +1532,14 @@ int tls_rqi_pcgtls(const tls_matrix_t* A, const double* b, const tls_precond_t R
   if (use_w) TLS_TRY(ensure_winv(cx, R));
   PrecondDev pc = R->dev;
   if (use_w) { pc.W = R->winv; pc.WT = R->winv + (size_t)pc.npad * pc.npad; }
-  // the fused reduction (NEXT-3) needs the explicit-inverse step and a single rank;
-  // TLS_FUSE_REDUCE=0 keeps the separate k_reduce_partials launch (A/B measurements)
+  // the fused reduction (NEXT-3: the PCG step reduces the operator pass's partials itself, no
+  // k_reduce_partials launch) needs a single rank.  Default with the explicit-inverse step
+  // (k_wpcg_step_coop phase 0); TLS_FUSE_REDUCE=0 keeps the separate launch there.  The
+  // substitution step has it too (k_pcg_step's step_reduce_partials, same bits) but only with
+  // TLS_FUSE_REDUCE=2: measured 73.9 vs 73.2 us per PCG iteration at n = 1024 (its 16 CTAs
+  // reduce the 148 partial rows in ~4 us, and the pass -> step launch gap stays), not adopted
   const char* fre = getenv("TLS_FUSE_REDUCE");
-  const bool fuse_reduce = use_w && !comm_active(comm) && !(fre && fre[0] == '0');
+  const bool fuse_reduce = !comm_active(comm) && !(fre && fre[0] == '0') && (use_w || (fre && fre[0] == '2'));
   if (is_csr(A)) TLS_TRY(launch_csc_build(csr_view(A), w.csc, w.csc_scratch, cx.st, &cx.launches));
   if (up32) TLS_TRY(ensure_a32(cx, A, R, content));
   const double tol_in = o.tol_inner > 0 ? o.tol_inner : tol;

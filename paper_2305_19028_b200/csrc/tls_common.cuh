@@ -144,6 +144,28 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return t;
 }
 
+// Two block sums at once: each value goes through exactly block_sum's operations (the same
+// bits), sharing its barriers.  red: smem of >= 64 doubles.  All threads of the block call it.
+__device__ __forceinline__ void block_sum2(double v0, double v1, double* red, double& s0, double& s1) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v0 = warp_sum(v0);
+  v1 = warp_sum(v1);
+  __syncthreads();
+  if (lane == 0) { red[warp] = v0; red[32 + warp] = v1; }
+  __syncthreads();
+  if (warp == 0) {
+    double t0 = lane < nw ? red[lane] : 0.0, t1 = lane < nw ? red[32 + lane] : 0.0;
+    t0 = warp_sum(t0);
+    t1 = warp_sum(t1);
+    __syncwarp();
+    if (lane == 0) { red[0] = t0; red[32] = t1; }
+  }
+  __syncthreads();
+  s0 = red[0];
+  s1 = red[32];
+  __syncthreads();
+}
+
 // Transpose-reduce V (power of two <= 32) per-lane partial values across a warp.
 // On return a[0] of lane l holds the warp total of value index
 //   idx(l) = sum over steps s (offset o = 16, 8, ...) with nv_s = V >> s > 1 of

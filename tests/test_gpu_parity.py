@@ -769,3 +769,26 @@ def test_graph_loop_equals_host_loop(T, monkeypatch, name, fmt, pa):
     # passes: the host loop counts every launched pass, also those an inactive PCG makes a no-op;
     # the graph counts the iterations it ran (the device stops the loop)
     assert out["1"][2]["passes"] <= out["0"][2]["passes"]
+
+
+@pytest.mark.parametrize("name,fmt,pa", [("cfg2w", "fp16", 1), ("cfg1", "bf16", 1), ("cfg2w", "fp16", 2)])
+def test_fused_reduce_same_bits(T, monkeypatch, name, fmt, pa):
+    """NEXT-3: the operator pass's partial rows reduced inside the PCG step (substitution:
+    k_pcg_step's step_reduce_partials, opt-in TLS_FUSE_REDUCE=2; explicit inverse: phase 0 of
+    k_wpcg_step_coop, the default) use k_reduce_partials' fixed order (8 row groups summed in row
+    order, then the groups in order), so x, sigma and every count are bit-identical to the
+    separate reduction launch (TLS_FUSE_REDUCE=0)."""
+    P = tlsgen.config(name)
+    M = T.matrix(dev(P.A))
+    b = dev(P.b)
+    rc, R, _ = T.tls_factor_precond(M, fmt)
+    o = T.tls_rqi_opts_default(precond_apply=pa)
+    out = {}
+    for f in ("0", "2"):
+        monkeypatch.setenv("TLS_FUSE_REDUCE", f)
+        rc, x, sig, info = T.tls_rqi_pcgtls(M, b, R, opts=o)
+        assert rc == 0
+        out[f] = (x.cpu().numpy().view(np.uint64).copy(), sig, info)
+    assert np.array_equal(out["0"][0], out["2"][0]) and out["0"][1] == out["2"][1]
+    for k in ("status", "termination", "rqi_iters", "boot_iters", "pcg_iters", "sigma2_trace"):
+        assert out["0"][2][k] == out["2"][2][k], k

@@ -1,10 +1,7 @@
 #!/bin/bash
-mkdir -p gpurun_out
-for tc in 256 128; do
-  for sup in 64 1000000; do
-    r=$(TLS_GRAM_SEGS=1 TLS_GRAM_TC=$tc TLS_GRAM_SUPER=$sup python tools/time_gram_tc2.py --one 1048576 1024 fp16 64 x 2>&1 | tail -1)
-    echo "unsegmented tc=$tc super=$sup: $r"
-  done
-done
-timeout 600 python tools/time_gram_tc2.py > gpurun_out/gram_tc2.log 2>&1; echo "time rc=$?"; cat gpurun_out/gram_tc2.log
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "gram" > gpurun_out/pytest_gram_tc2.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gram_tc2.log
+# explicit-inverse PCG step: batched GEMV loads + merged block sums; fp64 DFMA latency micro
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/fp64_lat tools/micro/fp64_lat.cu && /tmp/fp64_lat
+python tools/time_pcg_iter.py 2>&1
+python tools/time_pcg_iter.py --n 2048 --m 8192 2>&1 | grep -v '"graph": false'
+timeout 1200 python -m pytest tests/test_gpu_winv.py tests/test_gpu_multirank.py -q -x 2>&1 | tail -3
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "graph_loop or nccl_path or options or precond_apply" 2>&1 | tail -3

@@ -1,8 +1,6 @@
 #!/bin/bash
-for tc in 256 128; do for stg in 3 4; do for segs in 1 8; do
-  [ $tc = 128 ] && [ $stg = 3 ] && continue
-  r=$(TLS_GRAM_SEGS=$segs TLS_GRAM_TC=$tc TLS_GRAM_STAGES=$stg python tools/time_gram_tc2.py --one 1048576 1024 fp16 64 x 2>&1 | tail -1)
-  echo "tc=$tc stages=$stg segs=$segs: $r"
-done; done; done
-r=$(TLS_GRAM_SEGS=1 TLS_GRAM_STAGES=3 TLS_GRAM_SUPER=1000000 python tools/time_gram_tc2.py --one 1048576 1024 fp16 64 x 2>&1 | tail -1)
-echo "tc=256 stages=3 segs=1 no flush: $r"
+# substitution PCG step with the pass partials reduced inside k_pcg_step (NEXT-3)
+python tools/time_pcg_iter.py 2>&1
+python tools/time_pcg_iter.py --n 2048 --m 8192 2>&1 | grep '"pdl": true'
+timeout 2400 python -m pytest tests/test_gpu_parity.py tests/test_gpu_stress.py tests/test_gpu_csr.py tests/test_gpu_up32.py -q -x 2>&1 | tail -3
+python bench.py --steps 5 --warmup 3 > gpurun_out/r02x_bench.json 2> gpurun_out/r02x_bench.err; tail -c 600 gpurun_out/r02x_bench.json

@@ -1,4 +1,9 @@
 #!/bin/bash
-TLS_GRAM_SEGS=1 TLS_GRAM_STAGES=3 ncu --set full --import-source on --clock-control none -k regex:k_gram_tc2 -c 1 -o gpurun_out/gram_tc2_full3 \
-   python tools/time_gram_tc2.py --one 1048576 1024 fp16 64 x > gpurun_out/gram_tc2_full3.log 2>&1
-echo "full rc=$?"
+# TRSV per-block timeline; fused-reduce bit test; PCG iteration timing
+python tools/trsv_trace.py 1024 fp16 2>&1
+python tools/trsv_trace.py 2048 fp16 2>&1 | head -3
+python tools/time_trsv.py 2>&1 | head -8
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "fused_reduce or graph_loop" 2>&1 | tail -3
+python tools/time_pcg_iter.py --mode subst 2>&1
+TLS_FUSE_REDUCE=0 python tools/time_pcg_iter.py --mode winv_fused 2>&1
+python tools/time_pcg_iter.py --mode winv_fused 2>&1

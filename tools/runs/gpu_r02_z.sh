@@ -1,8 +1,5 @@
 #!/bin/bash
-# full GPU suite + smoke + the bench line after the k_gram_tc2 default
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
-timeout 2700 python -m pytest -m gpu -q --timeout 1200 tests > gpurun_out/r02b_pytest_gpu.log 2>&1; echo "pytest rc=$?"
-grep -E "passed|failed|FAILED|Error" gpurun_out/r02b_pytest_gpu.log | tail -10
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02b_smoke.log 2>&1; echo smoke rc=$?; tail -1 gpurun_out/r02b_smoke.log
-timeout -s KILL 1200 python bench.py --steps 20 --warmup 5 > gpurun_out/r02b_bench.json 2> gpurun_out/r02b_bench.err; echo bench rc=$?
-cat gpurun_out/r02b_bench.json
+# TRSV: E row in registers before the wait, next owner first, runs of L blocks per CTA
+for L in 1 2 4 8; do echo "== TLS_TRSV_RUN=$L"; TLS_TRSV_RUN=$L python tools/trsv_trace.py 1024 fp16 2>&1 | grep "^n="; TLS_TRSV_RUN=$L python tools/trsv_trace.py 2048 fp16 2>&1 | grep "^n="; TLS_TRSV_RUN=$L python tools/time_pcg_iter.py --mode subst 2>&1; done
+python tools/time_trsv.py 2>&1 | head -16
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_stress.py tests/test_gpu_winv.py -q -x 2>&1 | tail -3

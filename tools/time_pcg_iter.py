@@ -70,6 +70,7 @@ def main():
         print(json.dumps(one(args.mode, args.m, args.n)))
         return
     for mode, env in (("subst", {"TLS_PCG_GRAPH": "0", "TLS_PDL": "0"}), ("subst", {"TLS_PDL": "0"}), ("subst", {}),
+                      ("subst", {"TLS_FUSE_REDUCE": "0"}),
                       ("winv_sep", {"TLS_FUSE_REDUCE": "0", "TLS_PCG_GRAPH": "0", "TLS_PDL": "0"}),
                       ("winv_fused", {"TLS_PCG_GRAPH": "0", "TLS_PDL": "0"}), ("winv_fused", {"TLS_PDL": "0"}),
                       ("winv_fused", {}), ("winv_fused", {"TLS_WSTEP_CTAS": "64"}), ("winv_fused", {"TLS_WSTEP_CTAS": "32"})):
