@@ -232,61 +232,78 @@ __device__ __forceinline__ void qr_update_v4(float* __restrict__ W, int64_t m, i
       acc[4 * q + e] = 0.0;
     }
   }
-  float4 cur[GPT], nxt[GPT];
-  float nj = 0.f, nc = 0.f;
-  int64_t i = r0 + tm;
-  bool have = tm < teams && i < r1;
-  auto load = [&](int64_t ii) {   // the next row of this team, in flight while row i is updated
+  // rows of this team in flight: a ring of QD rows (static slots, the loop unrolled by QD), so
+  // each row's load is issued QD rows before its update (round 2 continued: with one row ahead
+  // the pass was one L2/HBM round trip per row of a team -- the per-column chain of the QR was
+  // load-latency bound; the arithmetic and its order are unchanged)
+#ifdef TLS_QR_QD
+  constexpr int QD = TLS_QR_QD;                  // build-time A/B (1 = round 2's one row ahead)
+#else
+  // measured (profiles/r02_qr_depth.log): 4 rows ahead 234 vs 287 ms for the unblocked QR at
+  // 65536 x 2048, the same blocked (57.8 vs 56.8 ms) and 5% slower at 16384 x 1024 unblocked
+  constexpr int QD = 4;
+#endif
+  float4 buf[QD][GPT];
+  float bj[QD], bc[QD];
+  auto load = [&](int64_t ii, float4 (&dst)[GPT], float& dj, float& dc) {
     const float* src = W + ii * (int64_t)ldw;
-    nj = src[j];
-    nc = src[c];
+    dj = src[j];
+    dc = src[c];
 #pragma unroll
     for (int q = 0; q < GPT; ++q) {
       const int g = tl + q * TG;
-      if (g < ngroups) nxt[q] = *reinterpret_cast<const float4*>(src + c0 + 4 * g);
+      if (g < ngroups) dst[q] = *reinterpret_cast<const float4*>(src + c0 + 4 * g);
     }
   };
-  if (have) load(i);
-  while (have) {
+  int64_t i = r0 + tm;
+  const bool active_team = tm < teams;
 #pragma unroll
-    for (int q = 0; q < GPT; ++q) cur[q] = nxt[q];
-    const float cj = nj, cc = nc;
-    const int64_t inext = i + teams;
-    const bool hn = inext < r1;
-    if (hn) load(inext);
-    // A team of several warps updates a row in place, and every thread reads the row's column c
-    // (old value) while the thread owning column c's group writes its new value: all of the
-    // team's loads of row `inext` must be performed before any store to it (one iteration
-    // later).  bar.sync orders them (its participants' prior accesses are performed first).
-    // A one-warp team needs none.  (Without it, teams of 3 warps -- n >= ~520 -- read
-    // already-updated column-c values: round 1's QR differed from the oracle there.)
-    if (TG > 32) asm volatile("bar.sync %0, %1;" ::"r"(1 + tm), "r"(TG) : "memory");
-    float* row = W + i * (int64_t)ldw;
-    const float vf = (i == j) ? v0f : cj;
-    const double xd = (double)qr_rdf<PREC>(__fsub_rn(cc, qr_rdf<PREC>(__fmul_rn(vf, wcf))));
-    const bool accum = i > c;
+  for (int d = 0; d < QD; ++d)
+    if (active_team && i + (int64_t)d * teams < r1) load(i + (int64_t)d * teams, buf[d], bj[d], bc[d]);
+  while (active_team && i < r1) {
 #pragma unroll
-    for (int q = 0; q < GPT; ++q) {
-      const int g = tl + q * TG;
-      if (g < ngroups) {
-        float x[4] = {cur[q].x, cur[q].y, cur[q].z, cur[q].w};
+    for (int d = 0; d < QD; ++d) {
+      if (i < r1) {
+        float4 cur[GPT];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          x[e] = qr_rdf<PREC>(__fsub_rn(x[e], qr_rdf<PREC>(__fmul_rn(vf, wk[4 * q + e]))));
-          if (accum) acc[4 * q + e] = fma(xd, (double)x[e], acc[4 * q + e]);
-        }
-        *reinterpret_cast<float4*>(row + c0 + 4 * g) = make_float4(x[0], x[1], x[2], x[3]);
-        if (i == j) {
+        for (int q = 0; q < GPT; ++q) cur[q] = buf[d][q];
+        const float cj = bj[d], cc = bc[d];
+        const int64_t ifar = i + (int64_t)QD * teams;
+        if (ifar < r1) load(ifar, buf[d], bj[d], bc[d]);
+        // A team of several warps updates a row in place, and every thread reads the row's column
+        // c (old value) while the thread owning column c's group writes its new value: all of the
+        // team's loads of a row must be performed before any store to it (QD iterations later).
+        // bar.sync orders them (its participants' prior accesses are performed first).  A one-warp
+        // team needs none.  (Without it, teams of 3 warps -- n >= ~520 -- read already-updated
+        // column-c values: round 1's QR differed from the oracle there.)
+        if (TG > 32) asm volatile("bar.sync %0, %1;" ::"r"(1 + tm), "r"(TG) : "memory");
+        float* row = W + i * (int64_t)ldw;
+        const float vf = (i == j) ? v0f : cj;
+        const double xd = (double)qr_rdf<PREC>(__fsub_rn(cc, qr_rdf<PREC>(__fmul_rn(vf, wcf))));
+        const bool accum = i > c;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int k = c0 + 4 * g + e;
-            if (k >= c && k < n) G[(int64_t)j * n + k] = alpha < 0.0 ? -(double)x[e] : (double)x[e];
+        for (int q = 0; q < GPT; ++q) {
+          const int g = tl + q * TG;
+          if (g < ngroups) {
+            float x[4] = {cur[q].x, cur[q].y, cur[q].z, cur[q].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              x[e] = qr_rdf<PREC>(__fsub_rn(x[e], qr_rdf<PREC>(__fmul_rn(vf, wk[4 * q + e]))));
+              if (accum) acc[4 * q + e] = fma(xd, (double)x[e], acc[4 * q + e]);
+            }
+            *reinterpret_cast<float4*>(row + c0 + 4 * g) = make_float4(x[0], x[1], x[2], x[3]);
+            if (i == j) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int k = c0 + 4 * g + e;
+                if (k >= c && k < n) G[(int64_t)j * n + k] = alpha < 0.0 ? -(double)x[e] : (double)x[e];
+              }
+            }
           }
         }
+        i += teams;
       }
     }
-    i = inext;
-    have = hn;
   }
   if (pdl_release) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int ncv = ngroups * 4;
@@ -369,14 +386,26 @@ __global__ void __launch_bounds__(kQrThreads) k_qr_fin(const T* __restrict__ W, 
   const double vv = ident ? 1.0 : round_uf(fma(v0, v0, tail), prec);
   const double beta = ident ? 0.0 : round_uf(2.0 / vv, prec);
   const int k = j + 1 + blockIdx.x * 32 + lane;
+  // warp w sums the partial rows b0 + w + 16i into s0 and b0 + w + 8 + 16i into s1, in i order;
+  // all of a batch's loads are issued before its adds (round 2 continued: the dependent
+  // two-loads-per-step loop was ~9 L2 round trips per column; same order, same bits)
   double s0 = 0.0, s1 = 0.0;
   if (k < n) {
-    int b = b0 + warp;
-    for (; b + 8 < nb; b += 16) {
-      s0 += partP[(int64_t)b * ldp + k];
-      s1 += partP[(int64_t)(b + 8) * ldp + k];
+    constexpr int kB = 10;                    // rows per accumulator per batch: nb <= 160 in one batch
+    for (int b = b0 + warp; b < nb; b += 16 * kB) {
+      double pa[kB], pb[kB];
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        const int r0 = b + 16 * i, r1 = r0 + 8;
+        pa[i] = r0 < nb ? partP[(int64_t)r0 * ldp + k] : 0.0;
+        pb[i] = r1 < nb ? partP[(int64_t)r1 * ldp + k] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        if (b + 16 * i < nb) s0 += pa[i];
+        if (b + 16 * i + 8 < nb) s1 += pb[i];
+      }
     }
-    if (b < nb) s0 += partP[(int64_t)b * ldp + k];
   }
   cs[warp][lane] = s0 + s1;
   __syncthreads();
@@ -612,8 +641,12 @@ __global__ void __launch_bounds__(kWyB) k_wy_T(const double* __restrict__ VtV, c
   double* vc = Ts + kWyB * (kWyB + 1);
   const int i = threadIdx.x;
   for (int e = i; e < kWyB * (kWyB + 1); e += blockDim.x) Ts[e] = 0.0;
+  // column j + 1 of VtV is loaded while step j computes (round 2 continued: the load at the top
+  // of each of the 128 dependent steps was an L2 round trip on the chain)
+  double vnext = nb > 0 ? VtV[i] : 0.0;
   for (int j = 0; j < nb; ++j) {
-    vc[i] = VtV[(int64_t)j * kWyB + i];
+    vc[i] = vnext;
+    if (j + 1 < nb) vnext = VtV[(int64_t)(j + 1) * kWyB + i];
     __syncthreads();
     const double bj = scal[4 * (c0 + j) + 3];
     if (i < j) {
