@@ -240,8 +240,9 @@ __device__ __forceinline__ void qr_update_v4(float* __restrict__ W, int64_t m, i
   constexpr int QD = TLS_QR_QD;                  // build-time A/B (1 = round 2's one row ahead)
 #else
   // measured (profiles/r02_qr_depth.log): 4 rows ahead 234 vs 287 ms for the unblocked QR at
-  // 65536 x 2048, the same blocked (57.8 vs 56.8 ms) and 5% slower at 16384 x 1024 unblocked
-  constexpr int QD = 4;
+  // 65536 x 2048, the same blocked (57.8 vs 56.8 ms) and 5% slower at 16384 x 1024 unblocked;
+  // the blocked QR's panel passes (one 4-column group per thread) keep 8
+  constexpr int QD = GPT == 1 ? 8 : 4;
 #endif
   float4 buf[QD][GPT];
   float bj[QD], bc[QD];
@@ -705,6 +706,10 @@ size_t qr_wy_bytes(int64_t m, int n) {
          (size_t)n * 8 * 5 + 16 * 256;
 }
 
+// the panel passes cover <= kWyB = 128 columns: one 4-column group per thread, 16 one-warp teams
+// per CTA (512 threads), 8 rows per team in flight (qr_update_v4)
+constexpr int kPanelCPT = 4;
+
 template <int CPT, int PREC>
 int qr_blocked_t(const DenseView& A, const double* dinv, float* W, double* partP, double* wT, double* scal,
                  int* qflags, double* G, char* wy, cudaStream_t st, int* launches) {
@@ -747,7 +752,8 @@ int qr_blocked_t(const DenseView& A, const double* dinv, float* W, double* partP
       // partials of column c0 over the panel (the pass of column c0 - 1 with w = 0: no change)
       const int j = c0 - 1;
       const int bs = j / RB;
-      rc = qr_step_launch<float, false, CPT, PREC>(W, Ap, ldw, dinv, j, RB, bs, nb - bs, zw, zs, partP, Gp, qflags, st);
+      rc = qr_step_launch<float, false, kPanelCPT, PREC>(W, Ap, ldw, dinv, j, RB, bs, nb - bs, zw, zs, partP, Gp, qflags,
+                                                          st);
       if (rc) return rc;
       nl += 2;
     }
@@ -760,7 +766,8 @@ int qr_blocked_t(const DenseView& A, const double* dinv, float* W, double* partP
       ++nl;
       if (j + 1 < c1) {
         const int bs = j / RB;
-        rc = qr_step_launch<float, false, CPT, PREC>(W, Ap, ldw, dinv, j, RB, bs, nb - bs, wT, scal, partP, Gp, qflags, st);
+        rc = qr_step_launch<float, false, kPanelCPT, PREC>(W, Ap, ldw, dinv, j, RB, bs, nb - bs, wT, scal, partP, Gp,
+                                                            qflags, st);
         if (rc) return rc;
         ++nl;
       }
