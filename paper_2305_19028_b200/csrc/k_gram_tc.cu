@@ -1123,21 +1123,44 @@ static size_t conv_smem(int prow, int64_t ld, int n) {
 }
 
 // ------------------------------------------------------------------------------ 3. split reduction
-__global__ void k_gram_reduce_t(const double* __restrict__ part, int ntiles, int nsplit, int TT, int tile, int n,
-                                double* __restrict__ G) {
+// Split partials -> G (both triangles).  CTA (tile, 8-row chunk): every thread adds its elements'
+// nsplit partials in split order (the same bits as one split at a time), with all of them in
+// flight; the row-major write is coalesced and the transposed one goes through shared memory
+// in 64-byte column segments.  (Round 2 continued: one CTA per tile with a strided transposed
+// store took ~125 us per factorization at n = 1024.)
+constexpr int kRedRows = 8;
+constexpr int kRedMaxSplit = 16;
+__global__ void __launch_bounds__(256) k_gram_reduce_t(const double* __restrict__ part, int ntiles, int nsplit, int TT,
+                                                      int tile, int n, double* __restrict__ G) {
+  __shared__ double tr[kRedRows][kTcTile + 1];
   int t = blockIdx.x, I = 0;
   while (t >= TT - I) { t -= TT - I; ++I; }
   const int J = I + t;
   const int te = tile * tile;
-  for (int e = threadIdx.x; e < te; e += blockDim.x) {
-    const int i = e / tile, j = e % tile;
-    const int gi = I * tile + i, gj = J * tile + j;
+  const int i0 = blockIdx.y * kRedRows;
+  const int cpt = tile / 32;                             // columns per lane (tile = 128: 4)
+  const int ri = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = i0 + ri, gi = I * tile + i;
+  for (int c = 0; c < cpt; ++c) {
+    const int j = lane + 32 * c, gj = J * tile + j;
+    const int e = i * tile + j;
+    double v[kRedMaxSplit];
+#pragma unroll
+    for (int s = 0; s < kRedMaxSplit; ++s) v[s] = s < nsplit ? part[((size_t)s * ntiles + blockIdx.x) * te + e] : 0.0;
     double acc = 0.0;
-    for (int s = 0; s < nsplit; ++s) acc += part[((size_t)s * ntiles + blockIdx.x) * te + e];
-    if (gi < n && gj < n) {
-      G[(size_t)gi * n + gj] = acc;
-      G[(size_t)gj * n + gi] = acc;
-    }
+#pragma unroll
+    for (int s = 0; s < kRedMaxSplit; ++s)
+      if (s < nsplit) acc += v[s];
+    for (int s = kRedMaxSplit; s < nsplit; ++s) acc += part[((size_t)s * ntiles + blockIdx.x) * te + e];
+    if (gi < n && gj < n) G[(size_t)gi * n + gj] = acc;
+    tr[ri][j] = acc;
+  }
+  __syncthreads();
+  // transposed: G[gj][gi] for the chunk's 8 rows i: thread = (column j, row lane pair)
+  for (int k = threadIdx.x; k < tile * kRedRows; k += blockDim.x) {
+    const int j = k / kRedRows, r = k % kRedRows;
+    const int gj = J * tile + j, gir = I * tile + i0 + r;
+    if (gj < n && gir < n) G[(size_t)gj * n + gir] = tr[r][j];
   }
 }
 
@@ -1299,7 +1322,7 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
       int tt = TT, nc = nchunks, ns = nsplit, kpc = K_t / kTcBK, sup = gram_super();
       void* args[] = {(void*)&rmap, &fz, &mm, &tt, &nc, &ns, &kpc, &sup, &part};
       TLS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(ntiles, nsplit), dim3(kFzThreads), args, kFzSmem, st));
-      k_gram_reduce_t<<<ntiles, 256, 0, st>>>(part, ntiles, nsplit, TT, kTcTile, A.n, G);
+      k_gram_reduce_t<<<dim3(ntiles, kTcTile / kRedRows), 256, 0, st>>>(part, ntiles, nsplit, TT, kTcTile, A.n, G);
       TLS_LAUNCH_CHECK();
       if (fz.prof) {
         std::vector<unsigned long long> h((size_t)ntiles * nsplit * 8);
@@ -1381,7 +1404,7 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
         int tt = TT, nc = nchunks, ns = ns2, nb = nblk2, sup = gram_super(), pr = prow;
         void* args[] = {(void*)&rmap, &fz, &mm, &tt, &nc, &ns, &nb, &sup, &part, &pr};
         TLS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(sms), dim3(kTcThreads), args, smem2, st));
-        k_gram_reduce_t<<<ntiles, 256, 0, st>>>(part, ntiles, ns2, TT, kTcTile, A.n, G);
+        k_gram_reduce_t<<<dim3(ntiles, kTcTile / kRedRows), 256, 0, st>>>(part, ntiles, ns2, TT, kTcTile, A.n, G);
         TLS_LAUNCH_CHECK();
         if (fz.prof) {
           std::vector<unsigned long long> h((size_t)sms * 8);
@@ -1522,7 +1545,7 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
     TLS_LAUNCH_CHECK();
     if (launches) *launches += 2;
   }
-  k_gram_reduce_t<<<ntiles, 256, 0, st>>>(part, ntiles, nsplit, TT, kTcTile, A.n, G);
+  k_gram_reduce_t<<<dim3(ntiles, kTcTile / kRedRows), 256, 0, st>>>(part, ntiles, nsplit, TT, kTcTile, A.n, G);
   TLS_LAUNCH_CHECK();
   if (launches) *launches += 1;
   return 0;

@@ -455,7 +455,7 @@ __device__ __forceinline__ double fp_weight(int64_t j) {
   return 1.0 + (double)(h >> 40) * 0x1p-24;
 }
 // One CTA per sampled row (coalesced), the row's weighted sum by a fixed-order block
-// reduction into part[r]; k_fingerprint_fin adds the 256 row sums in order.
+// reduction into part[r]; k_fingerprint_fin adds the 256 row sums in a fixed order.
 __global__ void __launch_bounds__(256) k_fingerprint(const double* __restrict__ A, int64_t m, int n, int64_t ld,
                                                      const int64_t* __restrict__ rowptr,
                                                      const int32_t* __restrict__ colidx, double* __restrict__ part) {
@@ -474,12 +474,18 @@ __global__ void __launch_bounds__(256) k_fingerprint(const double* __restrict__ 
   acc = block_sum(acc, red);
   if (t == 0) part[r] = acc;
 }
+// one warp: lane l sums the row sums 8l .. 8l+7 in order (all eight loads in flight), then a
+// fixed butterfly (deterministic; round 2 continued: one thread's 256 dependent adds took ~11 us)
 __global__ void k_fingerprint_fin(const double* __restrict__ part, double* __restrict__ out) {
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int u = 0; u < 256; ++u) s += part[u];
-    out[0] = s;
-  }
+  const int l = threadIdx.x;
+  double v[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) v[u] = part[8 * l + u];
+  double s = 0.0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s += v[u];
+  s = warp_sum(s);
+  if (l == 0) out[0] = s;
 }
 
 int launch_fingerprint(const DenseView* dv, const CsrView* cv, double* out, double* scratch, cudaStream_t st) {
