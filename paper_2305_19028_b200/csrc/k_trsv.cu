@@ -655,13 +655,26 @@ __global__ void __launch_bounds__(kWG) k_wpcg_step_coop(PrecondDev pc, PcgVecs v
     }
     grid.sync();
   }
-  // ---- A
+  // ---- A (the staging loads of four elements first: the shared-memory stores could alias them)
   for (int r = 0; r < 2; ++r) {
     if (!act[r]) continue;
     const size_t off = (size_t)r * n;
-    for (int j = tid; j < npad; j += kWG)
-      vin[(size_t)r * npad + j] =
-          j < n ? (variant == 0 ? passout[off + j] - sig2 * v.q[off + j] : v.q[off + j]) * pc.dinv[j] : 0.0;
+    for (int j0 = tid; j0 < npad; j0 += 4 * kWG) {
+      double po[4], qv[4], dv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + u * kWG;
+        const bool ok = j < n;
+        po[u] = (ok && variant == 0) ? passout[off + j] : 0.0;
+        qv[u] = ok ? v.q[off + j] : 0.0;
+        dv[u] = ok ? pc.dinv[j] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + u * kWG;
+        if (j < npad) vin[(size_t)r * npad + j] = j < n ? (variant == 0 ? po[u] - sig2 * qv[u] : qv[u]) * dv[u] : 0.0;
+      }
+    }
   }
   __syncthreads();
   const int nw = gridDim.x * (kWG / 32);
@@ -709,17 +722,32 @@ __global__ void __launch_bounds__(kWG) k_wpcg_step_coop(PrecondDev pc, PcgVecs v
     double al[2];
     for (int r = 0; r < 2; ++r) { upd[r] = act[r] && s_upd[r]; al[r] = s_al[r]; }
     double es[2] = {0.0, 0.0};
-    for (int i = tid; i < n; i += kWG) {
+    for (int i0 = tid; i0 < n; i0 += 4 * kWG) {     // four elements' loads first (stores could alias)
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         if (!upd[r]) continue;
         const size_t off = (size_t)r * n;
-        const double q = v.q[off + i];
-        if (blockIdx.x == 0) v.omega[off + i] = fma(al[r], q, v.omega[off + i]);   // l.196 (only CTA 0 reads omega)
-        const double w = variant == 0 ? v.w[off + i] : fma(-sig2, v.w[off + i], v.p[off + i]);   // l.197
-        const double sn = fma(-al[r], w, v.s[off + i]);        // l.198
-        snb[(size_t)r * npad + i] = sn;
-        es[r] = fma(sn, sn, es[r]);
+        double qv[4], wv[4], pv[4], sv[4], ov[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * kWG;
+          const bool ok = i < n;
+          qv[u] = ok ? v.q[off + i] : 0.0;
+          wv[u] = ok ? v.w[off + i] : 0.0;
+          pv[u] = (ok && variant != 0) ? v.p[off + i] : 0.0;
+          sv[u] = ok ? v.s[off + i] : 0.0;
+          ov[u] = (ok && blockIdx.x == 0) ? v.omega[off + i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * kWG;
+          if (i >= n) continue;
+          if (blockIdx.x == 0) v.omega[off + i] = fma(al[r], qv[u], ov[u]);   // l.196 (only CTA 0 reads omega)
+          const double w = variant == 0 ? wv[u] : fma(-sig2, wv[u], pv[u]);    // l.197
+          const double sn = fma(-al[r], w, sv[u]);           // l.198
+          snb[(size_t)r * npad + i] = sn;
+          es[r] = fma(sn, sn, es[r]);
+        }
       }
     }
     double etan[2];
@@ -736,14 +764,25 @@ __global__ void __launch_bounds__(kWG) k_wpcg_step_coop(PrecondDev pc, PcgVecs v
     double be[2];
     for (int r = 0; r < 2; ++r) { cont[r] = upd[r] && s_cont[r]; be[r] = s_be[r]; }
     double ep[2] = {0.0, 0.0};
-    for (int i = tid; i < npad; i += kWG) {
+    for (int i0 = tid; i0 < npad; i0 += 4 * kWG) {  // four elements' loads first
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         if (!cont[r]) continue;
         const size_t off = (size_t)r * n;
-        const double pn = i < n ? fma(be[r], v.p[off + i], snb[(size_t)r * npad + i]) : 0.0;   // l.201
-        vin[(size_t)r * npad + i] = pn;
-        ep[r] = fma(pn, pn, ep[r]);
+        double pv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * kWG;
+          pv[u] = i < n ? v.p[off + i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * kWG;
+          if (i >= npad) continue;
+          const double pn = i < n ? fma(be[r], pv[u], snb[(size_t)r * npad + i]) : 0.0;   // l.201
+          vin[(size_t)r * npad + i] = pn;
+          ep[r] = fma(pn, pn, ep[r]);
+        }
       }
     }
     double ppn[2];
@@ -1106,29 +1145,50 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_step(PrecondDev pc, PcgVecs
   }
   if (!s_upd) return;
   const double al = s_alpha;
-  // omega += alpha q (l.196); y = D^{-1}(A^T t - sigma^2 q) for w = P^{-T}(...) (R1)
-  for (int i = tid; i < npad; i += blockDim.x) {
-    double yv = 0.0;
-    if (i < n) {
-      const double q = v.q[off + i];
-      if (rank0) v.omega[off + i] = fma(al, q, v.omega[off + i]);
-      // variant 0: w = P^{-T}(A^T t - sigma^2 q); variant 1: solve P^{-T} q (l.197)
-      yv = (variant == 0 ? pv[i] - sig2 * q : q) * pc.dinv[i];
+  // omega += alpha q (l.196); y = D^{-1}(A^T t - sigma^2 q) for w = P^{-T}(...) (R1).  Four
+  // elements per thread with all their loads issued first (the stores to omega and y could alias
+  // the next element's loads for the compiler, which serialised the round trips)
+  for (int i0 = tid; i0 < npad; i0 += 4 * (int)blockDim.x) {
+    double qv[4], ov[4], pvv[4], dv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * (int)blockDim.x;
+      const bool ok = i < n;
+      qv[u] = ok ? v.q[off + i] : 0.0;
+      ov[u] = (ok && rank0) ? v.omega[off + i] : 0.0;
+      pvv[u] = (ok && variant == 0) ? pv[i] : 0.0;
+      dv[u] = ok ? pc.dinv[i] : 0.0;
     }
-    sm.y[i] = yv;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * (int)blockDim.x;
+      if (i >= npad) continue;
+      double yv = 0.0;
+      if (i < n) {
+        if (rank0) v.omega[off + i] = fma(al, qv[u], ov[u]);
+        // variant 0: w = P^{-T}(A^T t - sigma^2 q); variant 1: solve P^{-T} q (l.197)
+        yv = (variant == 0 ? pvv[u] - sig2 * qv[u] : qv[u]) * dv[u];
+      }
+      sm.y[i] = yv;
+    }
   }
   pre_apply<T, false>(pc, sm);
   // s -= alpha w (l.198), eta' = ||s||^2 (l.199); kept in registers until every CTA has read s, p
   double sn[kVecPerThread], pn[kVecPerThread];
   double e = 0.0;
 #pragma unroll
+  for (int k = 0; k < kVecPerThread; ++k) {      // pn[] holds the old p until the update below
+    const int i = tid + k * (int)blockDim.x;
+    pn[k] = i < n ? v.p[off + i] : 0.0;
+    sn[k] = i < n ? v.s[off + i] : 0.0;
+  }
+#pragma unroll
   for (int k = 0; k < kVecPerThread; ++k) {
     const int i = tid + k * (int)blockDim.x;
-    sn[k] = 0.0;
     if (i < n) {
       // w = solve result (variant 0) or p - sigma^2 P^{-T} q (variant 1, l.197-198)
-      const double w = variant == 0 ? sm.y[i] : fma(-sig2, sm.y[i], v.p[off + i]);
-      sn[k] = fma(-al, w, v.s[off + i]);
+      const double w = variant == 0 ? sm.y[i] : fma(-sig2, sm.y[i], pn[k]);
+      sn[k] = fma(-al, w, sn[k]);
       e = fma(sn[k], sn[k], e);
     }
   }
@@ -1148,8 +1208,7 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_step(PrecondDev pc, PcgVecs
 #pragma unroll
   for (int k = 0; k < kVecPerThread; ++k) {
     const int i = tid + k * (int)blockDim.x;
-    pn[k] = 0.0;
-    if (cont && i < n) pn[k] = fma(be, v.p[off + i], sn[k]);
+    pn[k] = (cont && i < n) ? fma(be, pn[k], sn[k]) : 0.0;
     if (i < npad) sm.y[i] = pn[k];
     ppl = fma(pn[k], pn[k], ppl);
   }
@@ -1175,10 +1234,23 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_step(PrecondDev pc, PcgVecs
   // next q = P^{-1} p (l.193 of the next iteration)
   pre_apply<T, true>(pc, sm);
   e = 0.0;
-  for (int i = tid; i < n; i += blockDim.x) {
-    const double q = sm.y[i] * pc.dinv[i];
-    if (rank0) v.q[off + i] = q;
-    e = fma(q, q, e);
+  for (int i0 = tid; i0 < n; i0 += 4 * (int)blockDim.x) {   // the loads of four elements first
+    double yv[4], dv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * (int)blockDim.x;
+      yv[u] = i < n ? sm.y[i] : 0.0;
+      dv[u] = i < n ? pc.dinv[i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * (int)blockDim.x;
+      if (i < n) {
+        const double q = yv[u] * dv[u];
+        if (rank0) v.q[off + i] = q;
+        e = fma(q, q, e);
+      }
+    }
   }
   const double qq = block_sum(e, sm.red);
   if (rank0 && tid == 0) S->qq[r] = qq;
