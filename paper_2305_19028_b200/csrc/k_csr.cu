@@ -340,37 +340,82 @@ __global__ void __launch_bounds__(kCsrT) k_csr_rows(CsrView A, const double* __r
   const int64_t w0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 4;
   const int64_t wstride = (((int64_t)gridDim.x * blockDim.x) >> 5) * 4;
   double s0 = 0.0, s1 = 0.0;
-  for (int64_t base = w0; base < A.m; base += wstride) {
-    const int64_t i = base + ((threadIdx.x & 31) >> 3);
-    const bool valid = i < A.m;
-    const int64_t r0 = valid ? A.rowptr[i] : 0, r1 = valid ? A.rowptr[i + 1] : 0;
-    double t[NRHS];
+  // two row groups per trip (base, base + wstride), their loads interleaved: the chain rowptr ->
+  // colidx / vals -> q of the second group overlaps the first's (round 2 continued); every row's
+  // products and the s0 / s1 accumulation keep their order (group k before group k + 1)
+  for (int64_t base = w0; base < A.m; base += 2 * wstride) {
+    int64_t ii[2], r0[2], r1[2];
+    bool valid[2];
 #pragma unroll
-    for (int r = 0; r < NRHS; ++r) t[r] = 0.0;
-    for (int64_t e = r0 + sub; e < r1; e += 8) {
-      const double a = A.vals[e];
-      const int j = A.colidx[e];
+    for (int h = 0; h < 2; ++h) {
+      ii[h] = base + h * wstride + ((threadIdx.x & 31) >> 3);
+      valid[h] = ii[h] < A.m;
+      r0[h] = valid[h] ? A.rowptr[ii[h]] : 0;
+      r1[h] = valid[h] ? A.rowptr[ii[h] + 1] : 0;
+    }
+    double t[2][NRHS];
 #pragma unroll
-      for (int r = 0; r < NRHS; ++r) t[r] = fma(a, q[(size_t)r * A.n + j], t[r]);
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) t[h][r] = 0.0;
+    // the first two nonzeros of each of the octet's rows, both groups, loads first
+    {
+      double a[2][2];
+      int jj[2][2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int64_t e = r0[h] + sub + 8 * k;
+          const bool ok = e < r1[h];
+          a[h][k] = ok ? A.vals[e] : 0.0;
+          jj[h][k] = ok ? A.colidx[e] : -1;
+        }
+      double qq[2][2][NRHS];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) qq[h][k][r] = jj[h][k] >= 0 ? q[(size_t)r * A.n + jj[h][k]] : 0.0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          if (jj[h][k] >= 0)
+#pragma unroll
+            for (int r = 0; r < NRHS; ++r) t[h][r] = fma(a[h][k], qq[h][k][r], t[h][r]);
     }
 #pragma unroll
-    for (int r = 0; r < NRHS; ++r) {
-      t[r] += __shfl_xor_sync(0xffffffffu, t[r], 4);
-      t[r] += __shfl_xor_sync(0xffffffffu, t[r], 2);
-      t[r] += __shfl_xor_sync(0xffffffffu, t[r], 1);
-    }
-    if (sub == 0 && valid) {
-      if (MODE == PASS_RESIDUAL) {
-        const double bi = b[i];
-        const double ti = bi - t[0];
-        tbuf[i] = ti;
-        s0 = fma(ti, ti, s0);
-        s1 = fma(bi, ti, s1);
-      } else {
+    for (int h = 0; h < 2; ++h)
+      for (int64_t e = r0[h] + sub + 16; e < r1[h]; e += 8) {     // longer rows: the rest in order
+        const double a = A.vals[e];
+        const int j = A.colidx[e];
 #pragma unroll
-        for (int r = 0; r < NRHS; ++r) tbuf[(size_t)r * A.m + i] = t[r];
-        s0 = fma(t[0], t[0], s0);
-        if (NRHS == 2) s1 = fma(t[NRHS - 1], t[NRHS - 1], s1);
+        for (int r = 0; r < NRHS; ++r) t[h][r] = fma(a, q[(size_t)r * A.n + j], t[h][r]);
+      }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+        t[h][r] += __shfl_xor_sync(0xffffffffu, t[h][r], 4);
+        t[h][r] += __shfl_xor_sync(0xffffffffu, t[h][r], 2);
+        t[h][r] += __shfl_xor_sync(0xffffffffu, t[h][r], 1);
+      }
+      const int64_t i = ii[h];
+      if (sub == 0 && valid[h]) {
+        if (MODE == PASS_RESIDUAL) {
+          const double bi = b[i];
+          const double ti = bi - t[h][0];
+          tbuf[i] = ti;
+          s0 = fma(ti, ti, s0);
+          s1 = fma(bi, ti, s1);
+        } else {
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) tbuf[(size_t)r * A.m + i] = t[h][r];
+          s0 = fma(t[h][0], t[h][0], s0);
+          if (NRHS == 2) s1 = fma(t[h][NRHS - 1], t[h][NRHS - 1], s1);
+        }
       }
     }
   }
@@ -412,6 +457,21 @@ __global__ void __launch_bounds__(kCsrT) k_csr_cols(int64_t m, int n, CscView C,
 #pragma unroll
   for (int r = 0; r < NRHS; ++r) v[r] = 0.0;
   int64_t e = e0 + lane;
+  for (; e + 224 < e1; e += 256) {     // 8 independent gathers in flight per lane (round 2
+    int rw[8];                         // continued: 4 before; the same order, the same bits)
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) { rw[u] = C.rowidx[e + 32 * u]; a[u] = C.vals[e + 32 * u]; }
+    double tv[8][NRHS];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) tv[u][r] = tbuf[(size_t)r * m + rw[u]];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) v[r] = fma(a[u], tv[u][r], v[r]);
+  }
   for (; e + 96 < e1; e += 128) {      // 4 independent gathers in flight per lane
     int rw[4];
     double a[4];
