@@ -376,6 +376,10 @@ int launch_pass(const DenseView& A, int mode, int nrhs, const double* q, const d
 constexpr int kRedBatch = 20;   // partial rows in flight per thread: a row group of G = 148 CTAs in one batch
 __global__ void k_reduce_partials(const double* __restrict__ partials, int G, int W, int nmax,
                                   double* __restrict__ out, const int* __restrict__ active) {
+  // launched with programmatic dependent launch after a pass (round 2 continued): wait for it
+  // before reading anything (a no-op otherwise), let the PCG step that follows launch at once
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (active != nullptr && (active[0] | active[1]) == 0) return;
   __shared__ double sm[8][33];
   const int tx = threadIdx.x, grp = threadIdx.y;
@@ -408,6 +412,19 @@ __global__ void k_reduce_partials(const double* __restrict__ partials, int G, in
 int launch_reduce(const double* partials, int G, int W, int nmax, double* out, const int* active,
                   cudaStream_t st) {
   dim3 blk(32, 8);
+  if (pass_pdl()) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((W + 31) / 32);
+    cfg.blockDim = blk;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    TLS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_reduce_partials, partials, G, W, nmax, out, active));
+    return 0;
+  }
   k_reduce_partials<<<(W + 31) / 32, blk, 0, st>>>(partials, G, W, nmax, out, active);
   TLS_LAUNCH_CHECK();
   return 0;

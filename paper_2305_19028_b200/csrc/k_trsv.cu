@@ -978,8 +978,21 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_init(PrecondDev pc, int nrh
     return;
   }
   const size_t off = (size_t)r * n;
-  // l.191: s_0 = p_0 = P^{-T} f, eta_0 = ||s_0||^2, omega_0 = 0
-  for (int i = tid; i < npad; i += blockDim.x) sm.y[i] = i < n ? v.rhs[off + i] * pc.dinv[i] : 0.0;
+  // l.191: s_0 = p_0 = P^{-T} f, eta_0 = ||s_0||^2, omega_0 = 0 (four elements' loads first)
+  for (int i0 = tid; i0 < npad; i0 += 4 * (int)blockDim.x) {
+    double rv[4], dv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * (int)blockDim.x;
+      rv[u] = i < n ? v.rhs[off + i] : 0.0;
+      dv[u] = i < n ? pc.dinv[i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * (int)blockDim.x;
+      if (i < npad) sm.y[i] = i < n ? rv[u] * dv[u] : 0.0;
+    }
+  }
   pre_apply<T, false>(pc, sm);
   double e = 0.0;
   for (int i = tid; i < n; i += blockDim.x) {
@@ -995,10 +1008,23 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_init(PrecondDev pc, int nrh
   // first q = P^{-1} p (l.193)
   pre_apply<T, true>(pc, sm);
   e = 0.0;
-  for (int i = tid; i < n; i += blockDim.x) {
-    const double q = sm.y[i] * pc.dinv[i];
-    if (rank0) v.q[off + i] = q;
-    e = fma(q, q, e);
+  for (int i0 = tid; i0 < n; i0 += 4 * (int)blockDim.x) {   // the loads of four elements first
+    double yv[4], dv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * (int)blockDim.x;
+      yv[u] = i < n ? sm.y[i] : 0.0;
+      dv[u] = i < n ? pc.dinv[i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * (int)blockDim.x;
+      if (i < n) {
+        const double q = yv[u] * dv[u];
+        if (rank0) v.q[off + i] = q;
+        e = fma(q, q, e);
+      }
+    }
   }
   const double qq = block_sum(e, sm.red);
   if (rank0 && tid == 0) {
@@ -1090,11 +1116,16 @@ __global__ void __launch_bounds__(kTW * 32, 1) k_pcg_step(PrecondDev pc, PcgVecs
                                                        PcgState* __restrict__ S, int nrhs, int rule, int next_q,
                                                        int variant, int pass_nrhs, const int* __restrict__ nq_dev,
                                                        const double* __restrict__ partials, int G) {
-  if (nq_dev) next_q = *nq_dev;         // graph-captured loop (NEXT-3): decided on the device
   __shared__ double s_alpha, s_beta, s_delta;
   __shared__ int s_upd, s_cont, s_brk, s_exit;
   TrsvSm sm = trsv_carve(pc.npad);
   trsv_init(sm, pc.npad);
+  // programmatic dependent launch (round 2 continued): the barrier setup above overlaps the
+  // predecessor's tail; wait for its results before reading anything, and let the next operator
+  // pass launch now (it waits for this grid's completion before reading anything)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (nq_dev) next_q = *nq_dev;         // graph-captured loop (NEXT-3): decided on the device
   const int r = blockIdx.x / (int)cluster_nctarank();
   const bool rank0 = cluster_ctarank() == 0;
   if (r >= nrhs || S->active[r] == 0) return;
@@ -1344,8 +1375,11 @@ static int set_smem(F kern, size_t bytes) {
   }
 
 // kTC-CTA clusters (one per right-hand side) of the single-CTA TRSV kernels
+// pdl: programmatic stream serialisation (the kernel must execute griddepcontrol.wait before it
+// reads its predecessor's results)
 template <typename... KArgs, typename... Args>
-static int launch_cluster(void (*kern)(KArgs...), int clusters, size_t smem, cudaStream_t st, Args... args) {
+static int launch_cluster_pdl(void (*kern)(KArgs...), int clusters, size_t smem, cudaStream_t st, bool pdl,
+                              Args... args) {
   TLS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
   const int C = trsv_cluster();
@@ -1353,15 +1387,22 @@ static int launch_cluster(void (*kern)(KArgs...), int clusters, size_t smem, cud
   cfg.blockDim = dim3(kTW * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = C;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   TLS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
   return 0;
+}
+
+template <typename... KArgs, typename... Args>
+static int launch_cluster(void (*kern)(KArgs...), int clusters, size_t smem, cudaStream_t st, Args... args) {
+  return launch_cluster_pdl(kern, clusters, smem, st, false, args...);
 }
 
 int launch_precond_apply(const PrecondDev& pc, int trans, int nrhs, double* Y, int ldY, cudaStream_t st) {
@@ -1466,8 +1507,8 @@ int launch_pcg_step(const PrecondDev& pc, PcgVecs v, const double* passout, PcgS
   // partials: the fused reduction (step_reduce_partials) needs a staging vector after the TRSV layout
   const size_t sm = trsv_smem(pc.npad) + (partials ? ((size_t)pc.npad + 32) * 8 : 0);
   int rc = 0;
-  TLS_DISPATCH_UF(pc.u_f, { rc = launch_cluster(k_pcg_step<T>, nrhs, sm, st, pc, v, passout, S, nrhs, rule, next_q,
-                                                variant, pass_nrhs, nq_dev, partials, G); });
+  TLS_DISPATCH_UF(pc.u_f, { rc = launch_cluster_pdl(k_pcg_step<T>, nrhs, sm, st, pass_pdl(), pc, v, passout, S, nrhs,
+                                                    rule, next_q, variant, pass_nrhs, nq_dev, partials, G); });
   return rc;
 }
 
