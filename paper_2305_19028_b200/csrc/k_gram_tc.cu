@@ -128,38 +128,55 @@ __host__ __device__ constexpr uint32_t idesc_f16(int fmt) {
 }
 
 // ------------------------------------------------------------------------------ 1. A^ = fl_uf(A D^-1)
-template <int PREC>
-__global__ void __launch_bounds__(256) k_round_scaled(const double* __restrict__ A, int64_t m, int n, int64_t ld,
-                                                      const double* __restrict__ dinv, uint16_t* __restrict__ Ah, int npad,
-                                                      int* __restrict__ range) {
+template <int PREC, int kRows>
+__global__ void __launch_bounds__(256, 6) k_round_scaled(const double* __restrict__ A, int64_t m, int n, int64_t ld,
+                                                         const double* __restrict__ dinv, uint16_t* __restrict__ Ah, int npad,
+                                                         int* __restrict__ range) {
   // Fully coalesced: a warp reads 32 consecutive column pairs of a row (512 B, one
   // 16-byte load per lane; ld even and A 16-B aligned) and writes 32 consecutive u_f
-  // pairs (128 B).  Rows are spread over the grid; each thread keeps two pairs in flight.
+  // pairs (128 B).  Rows are spread over the grid.  Each thread issues the loads of two
+  // pairs in kRows rows (kRows x 2 x 16 B) before its first conversion: beside the segmented
+  // SYRK (168 registers x 320 threads) only ONE 256-thread CTA of this kernel fits an SM
+  // (hence <= 40 registers: __launch_bounds__(256, 6)), and with one row (2 x 16 B) in
+  // flight per thread it was latency-bound there.  Same products, same rounding.  Measured
+  // (tools/time_round.py, profiles/r02f_round.log): tls_gram 2^20 x 1024 3.30 -> 3.24 ms
+  // (fp16), 3.26 -> 3.18 ms (bf16); G bit-identical.
   const int pairs = npad / 2;
+  const int64_t G = gridDim.x;
   int bad = 0;
-  for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
-    const double* src = A + row * ld;
-    uint32_t* dst = reinterpret_cast<uint32_t*>(Ah + row * npad);
+  for (int64_t row0 = blockIdx.x; row0 < m; row0 += kRows * G) {
     for (int p0 = threadIdx.x; p0 < pairs; p0 += 2 * blockDim.x) {
-      double2 v[2];
+      double2 v[kRows][2];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int c = 2 * (p0 + u * (int)blockDim.x);
-        if (c + 1 < n) v[u] = __ldcs(reinterpret_cast<const double2*>(src + c));   // streamed once
-        else v[u] = make_double2(c < n ? src[c] : 0.0, 0.0);
+      for (int r = 0; r < kRows; ++r) {
+        const int64_t row = row0 + r * G;
+        const double* src = A + row * ld;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int c = 2 * (p0 + u * (int)blockDim.x);
+          if (row < m && c + 1 < n) v[r][u] = __ldcs(reinterpret_cast<const double2*>(src + c));   // streamed once
+          else v[r][u] = make_double2(row < m && c < n ? src[c] : 0.0, 0.0);
+        }
       }
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int pp = p0 + u * (int)blockDim.x;
         if (pp >= pairs) break;
         const int c = 2 * pp;
-        const double x0 = c < n ? v[u].x * dinv[c] : 0.0;
-        const double x1 = c + 1 < n ? v[u].y * dinv[c + 1] : 0.0;
-        const uint16_t h0 = PREC == TLS_FP16 ? f64_to_f16_bits(x0) : f64_to_bf16_bits(x0);   // one RNE rounding
-        const uint16_t h1 = PREC == TLS_FP16 ? f64_to_f16_bits(x1) : f64_to_bf16_bits(x1);
-        const uint32_t lim = PREC == TLS_FP16 ? 0x7c00u : 0x7f80u;                               // inf / nan
-        bad |= ((h0 & 0x7fffu) >= lim) | ((h1 & 0x7fffu) >= lim);
-        dst[pp] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+        const double s0 = c < n ? dinv[c] : 0.0;
+        const double s1 = c + 1 < n ? dinv[c + 1] : 0.0;
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) {
+          const int64_t row = row0 + r * G;
+          if (row >= m) break;
+          const double x0 = c < n ? v[r][u].x * s0 : 0.0;
+          const double x1 = c + 1 < n ? v[r][u].y * s1 : 0.0;
+          const uint16_t h0 = PREC == TLS_FP16 ? f64_to_f16_bits(x0) : f64_to_bf16_bits(x0);   // one RNE rounding
+          const uint16_t h1 = PREC == TLS_FP16 ? f64_to_f16_bits(x1) : f64_to_bf16_bits(x1);
+          const uint32_t lim = PREC == TLS_FP16 ? 0x7c00u : 0x7f80u;                               // inf / nan
+          bad |= ((h0 & 0x7fffu) >= lim) | ((h1 & 0x7fffu) >= lim);
+          reinterpret_cast<uint32_t*>(Ah + row * npad)[pp] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+        }
       }
     }
   }
@@ -1490,6 +1507,11 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
                                     (int)smem));
   TLS_CUDA_TRY(cudaMemsetAsync(part, 0, (size_t)nsplit * ntiles * kTcTile * kTcTile * 8, st));
   const int nblk2 = t2_blocks(TT);
+  // TLS_ROUND=1: round 2's one row in flight per thread (read per call: the equality test
+  // switches it); default two rows.  A third form with the loads staged in shared memory by
+  // cp.async was bit-identical and slower (2^20 x 1024: 4.44 vs 3.24 ms, profiles/r02f_round.log)
+  const char* rve = getenv("TLS_ROUND");
+  const int rv = (rve && atoi(rve) == 1) ? 1 : 2;
   cudaStream_t rs = nseg > 1 ? sd.s : st;
   if (nseg > 1) {
     TLS_CUDA_TRY(cudaEventRecord(sd.fork, st));                    // D^{-1} and the memset are ready
@@ -1506,10 +1528,17 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
     if (g > gmax) g = gmax;
     const double* src = A.A + r0 * A.ld;
     uint16_t* dst = Ah + r0 * npad;
-    if (u_f == TLS_FP16)
-      k_round_scaled<TLS_FP16><<<(int)g, 256, 0, rs>>>(src, rows, A.n, A.ld, dinv, dst, npad, range_flag);
-    else
-      k_round_scaled<TLS_BF16><<<(int)g, 256, 0, rs>>>(src, rows, A.n, A.ld, dinv, dst, npad, range_flag);
+    if (rv == 1) {
+      if (u_f == TLS_FP16)
+        k_round_scaled<TLS_FP16, 1><<<(int)g, 256, 0, rs>>>(src, rows, A.n, A.ld, dinv, dst, npad, range_flag);
+      else
+        k_round_scaled<TLS_BF16, 1><<<(int)g, 256, 0, rs>>>(src, rows, A.n, A.ld, dinv, dst, npad, range_flag);
+    } else {
+      if (u_f == TLS_FP16)
+        k_round_scaled<TLS_FP16, 2><<<(int)g, 256, 0, rs>>>(src, rows, A.n, A.ld, dinv, dst, npad, range_flag);
+      else
+        k_round_scaled<TLS_BF16, 2><<<(int)g, 256, 0, rs>>>(src, rows, A.n, A.ld, dinv, dst, npad, range_flag);
+    }
     TLS_LAUNCH_CHECK();
     if (nseg > 1) {
       TLS_CUDA_TRY(cudaEventRecord(sd.ev[k], rs));

@@ -198,3 +198,36 @@ def test_gram_multicast_clusters_bit_identical(T, monkeypatch, segs):
         torch.cuda.synchronize()
         side.synchronize()
         assert rc == 0 and np.array_equal(_bits(G), ref)
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+@pytest.mark.parametrize("m,n", [(300001, 1000), (20001, 257), (70001, 2000)])
+def test_gram_rounding_forms_bit_identical(T, monkeypatch, fmt, m, n):
+    """The Gram's rounding pass fl_uf(A D^-1) in its two forms (TLS_ROUND=1: one row in flight
+    per thread; default: two rows) gives bit-identical G, alone and overlapped with the segmented
+    SYRK, incl. odd n (a last column without a pair partner) and ragged m; and the same range
+    flag when an entry overflows u_f."""
+    A = T.dense_operand(torch.randn((m, n), dtype=torch.float64, device="cuda"))
+    M = T.matrix(A)
+    ws = T.workspace(M)
+    d = torch.full((n,), 8.0, dtype=torch.float64, device="cuda")
+    for segs in ("8", "1"):
+        monkeypatch.setenv("TLS_GRAM_SEGS", segs)
+        ref = None
+        for rv in ("1", "2"):
+            monkeypatch.setenv("TLS_ROUND", rv)
+            rc, G = T.tls_gram(M, fmt, d, 64, ws=ws)
+            torch.cuda.synchronize()
+            assert rc == 0
+            if ref is None:
+                ref = _bits(G)
+            assert np.array_equal(_bits(G), ref), (segs, rv)
+    if fmt == "fp16":                                   # one entry beyond fp16's range after scaling
+        A[m // 2, n - 1] = 1e6
+        rcs = set()
+        for rv in ("1", "2"):
+            monkeypatch.setenv("TLS_ROUND", rv)
+            rc, _ = T.tls_gram(M, fmt, d, 64, ws=ws)
+            torch.cuda.synchronize()
+            rcs.add(rc)
+        assert len(rcs) == 1 and rcs.pop() != 0
