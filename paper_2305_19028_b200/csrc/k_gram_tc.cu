@@ -183,6 +183,91 @@ __global__ void __launch_bounds__(256, 6) k_round_scaled(const double* __restric
   if (bad) atomicExch(range, 1);
 }
 
+// The same pass with the fp64 rows staged in shared memory by the bulk-copy (TMA) engine
+// (TLS_ROUND=3, n even): beside the SYRK only one CTA of the register form fits an SM, with
+// 16 KB of loads in flight; here the bytes in flight live in a ring of kRbStages x 8 KB of
+// the shared memory the SYRK leaves free, issued by one producer lane, and cost no registers.
+// A unit = (row, chunk of <= 1024 columns); same products, same single rounding, same bytes of A^.
+constexpr int kRbStages = 8;
+constexpr int kRbChunk = 1024;                                   // doubles per stage
+constexpr int kRbThreads = 288;                                  // 8 consumer warps + the producer warp
+constexpr size_t kRbSmem = (size_t)kRbStages * kRbChunk * 8 + 2 * kRbStages * 8 + 128;
+template <int PREC>
+__global__ void __launch_bounds__(kRbThreads, 5) k_round_bulk(const double* __restrict__ A, int64_t m, int n, int64_t ld,
+                                                              const double* __restrict__ dinv, uint16_t* __restrict__ Ah,
+                                                              int npad, int* __restrict__ range) {
+  extern __shared__ __align__(128) unsigned char rb_raw[];
+  double* ring = reinterpret_cast<double*>(rb_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(rb_raw + (size_t)kRbStages * kRbChunk * 8);
+  uint64_t* empty = full + kRbStages;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int nch = (n + kRbChunk - 1) / kRbChunk;
+  const int64_t G = gridDim.x;
+  const int64_t nrows = blockIdx.x < m ? (m - blockIdx.x + G - 1) / G : 0;
+  const int64_t units = nrows * nch;
+  if (tid == 0) {
+    for (int i = 0; i < kRbStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 8); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 8) {
+    if (tid == 256) {
+      const uint64_t pol = policy_evict_first();
+      const double* src = A + (int64_t)blockIdx.x * ld;
+      int st = 0, ch = 0;
+      uint32_t ph = 1;                                              // parity of the previous use of the stage
+      bool first = true;
+      for (int64_t u = 0; u < units; ++u) {
+        if (!first) mbar_wait(&empty[st], ph);
+        const int cnt = n - ch * kRbChunk < kRbChunk ? n - ch * kRbChunk : kRbChunk;
+        mbar_arrive_expect_tx(&full[st], (uint32_t)cnt * 8u);
+        bulk_g2s(ring + (size_t)st * kRbChunk, src + ch * kRbChunk, (uint32_t)cnt * 8u, &full[st], pol);
+        if (++ch == nch) { ch = 0; src += G * ld; }
+        if (++st == kRbStages) { st = 0; ph ^= 1; first = false; }
+      }
+    }
+    return;
+  }
+  int bad = 0;
+  const int lane = tid & 31;
+  uint16_t* dst = Ah + (int64_t)blockIdx.x * npad;
+  int st = 0, ch = 0;
+  uint32_t ph = 0;
+  for (int64_t u = 0; u < units; ++u) {
+    const int c0 = ch * kRbChunk;
+    const int cnt = n - c0 < kRbChunk ? n - c0 : kRbChunk;                  // even (n even)
+    const int outp = (npad - c0 < kRbChunk ? npad - c0 : kRbChunk) / 2;     // pairs written (zero pad included)
+    mbar_wait(&full[st], ph);
+    const double2* sp = reinterpret_cast<const double2*>(ring + (size_t)st * kRbChunk);
+    double2 v[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int pp = tid + k * 256;
+      v[k] = 2 * pp < cnt ? sp[pp] : make_double2(0.0, 0.0);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);                                 // this warp has read its part of the stage
+    uint32_t* orow = reinterpret_cast<uint32_t*>(dst) + c0 / 2;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int pp = tid + k * 256;
+      if (pp >= outp) break;
+      const int c = c0 + 2 * pp;
+      const bool in = 2 * pp < cnt;
+      const double x0 = in ? v[k].x * __ldg(dinv + c) : 0.0;
+      const double x1 = in ? v[k].y * __ldg(dinv + c + 1) : 0.0;
+      const uint16_t h0 = PREC == TLS_FP16 ? f64_to_f16_bits(x0) : f64_to_bf16_bits(x0);   // one RNE rounding
+      const uint16_t h1 = PREC == TLS_FP16 ? f64_to_f16_bits(x1) : f64_to_bf16_bits(x1);
+      const uint32_t lim = PREC == TLS_FP16 ? 0x7c00u : 0x7f80u;                               // inf / nan
+      bad |= ((h0 & 0x7fffu) >= lim) | ((h1 & 0x7fffu) >= lim);
+      orow[pp] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+    }
+    if (++ch == nch) { ch = 0; dst += G * npad; }
+    if (++st == kRbStages) { st = 0; ph ^= 1; }
+  }
+  if (bad) atomicExch(range, 1);
+}
+
 // ------------------------------------------------------------------------------ 2. tcgen05 SYRK
 template <int FMT, bool KAHAN>
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -645,8 +730,15 @@ __device__ __forceinline__ void tc2_body(const CUtensorMap* tmap_p, unsigned cha
   }
 }
 
+// TLS_T2_MAXNREG (compile-time experiment): cap the SYRK's registers so that more CTAs of the
+// concurrent rounding pass fit beside it (168 registers x 320 threads leave room for one)
+#ifdef TLS_T2_MAXNREG
+template <int FMT, int kT2Stages, bool MC = false, int EW = 8>
+__global__ void __maxnreg__(TLS_T2_MAXNREG)
+#else
 template <int FMT, int kT2Stages, bool MC = false, int EW = 8>
 __global__ void __launch_bounds__(64 + 32 * EW, 1)
+#endif
 k_gram_tc2(const __grid_constant__ CUtensorMap tmap, int64_t m, int TT, int nchunks, int nsplit, int kpc, int super,
            double* __restrict__ part, int kb0) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -1511,7 +1603,12 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
   // switches it); default two rows.  A third form with the loads staged in shared memory by
   // cp.async was bit-identical and slower (2^20 x 1024: 4.44 vs 3.24 ms, profiles/r02f_round.log)
   const char* rve = getenv("TLS_ROUND");
-  const int rv = (rve && atoi(rve) == 1) ? 1 : 2;
+  int rv = (rve && atoi(rve) == 1) ? 1 : ((rve && atoi(rve) == 3) ? 3 : 2);
+  if (rv == 3 && (A.n & 1)) rv = 2;                                // bulk copies move multiples of 16 B
+  if (rv == 3) {
+    TLS_CUDA_TRY(cudaFuncSetAttribute(k_round_bulk<TLS_FP16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRbSmem));
+    TLS_CUDA_TRY(cudaFuncSetAttribute(k_round_bulk<TLS_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRbSmem));
+  }
   cudaStream_t rs = nseg > 1 ? sd.s : st;
   if (nseg > 1) {
     TLS_CUDA_TRY(cudaEventRecord(sd.fork, st));                    // D^{-1} and the memset are ready
@@ -1528,7 +1625,15 @@ int launch_gram_tc(const DenseView& A, int u_f, const double* dinv, int K_t, dou
     if (g > gmax) g = gmax;
     const double* src = A.A + r0 * A.ld;
     uint16_t* dst = Ah + r0 * npad;
-    if (rv == 1) {
+    if (rv == 3) {
+      const char* ge = getenv("TLS_ROUND_GRID");
+      int64_t gb = (int64_t)num_sms() * (ge && atoi(ge) > 0 ? atoi(ge) : 3);   // 3 per SM measured best (r02h_round_bulk.log)
+      if (gb > rows) gb = rows;
+      if (u_f == TLS_FP16)
+        k_round_bulk<TLS_FP16><<<(int)gb, kRbThreads, kRbSmem, rs>>>(src, rows, A.n, A.ld, dinv, dst, npad, range_flag);
+      else
+        k_round_bulk<TLS_BF16><<<(int)gb, kRbThreads, kRbSmem, rs>>>(src, rows, A.n, A.ld, dinv, dst, npad, range_flag);
+    } else if (rv == 1) {
       if (u_f == TLS_FP16)
         k_round_scaled<TLS_FP16, 1><<<(int)g, 256, 0, rs>>>(src, rows, A.n, A.ld, dinv, dst, npad, range_flag);
       else

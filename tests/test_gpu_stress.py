@@ -201,10 +201,11 @@ def test_gram_multicast_clusters_bit_identical(T, monkeypatch, segs):
 
 
 @pytest.mark.parametrize("fmt", ["fp16", "bf16"])
-@pytest.mark.parametrize("m,n", [(300001, 1000), (20001, 257), (70001, 2000)])
+@pytest.mark.parametrize("m,n", [(300001, 1000), (20001, 257), (70001, 2000), (40001, 1030)])
 def test_gram_rounding_forms_bit_identical(T, monkeypatch, fmt, m, n):
-    """The Gram's rounding pass fl_uf(A D^-1) in its two forms (TLS_ROUND=1: one row in flight
-    per thread; default: two rows) gives bit-identical G, alone and overlapped with the segmented
+    """The Gram's rounding pass fl_uf(A D^-1) in its three forms (TLS_ROUND=1: one row in flight
+    per thread; default: two rows; 3: rows staged in shared memory by the bulk-copy engine, even n,
+    one or two column chunks with a short second chunk) gives bit-identical G, alone and overlapped with the segmented
     SYRK, incl. odd n (a last column without a pair partner) and ragged m; and the same range
     flag when an entry overflows u_f."""
     A = T.dense_operand(torch.randn((m, n), dtype=torch.float64, device="cuda"))
@@ -214,7 +215,7 @@ def test_gram_rounding_forms_bit_identical(T, monkeypatch, fmt, m, n):
     for segs in ("8", "1"):
         monkeypatch.setenv("TLS_GRAM_SEGS", segs)
         ref = None
-        for rv in ("1", "2"):
+        for rv in ("1", "2", "3"):
             monkeypatch.setenv("TLS_ROUND", rv)
             rc, G = T.tls_gram(M, fmt, d, 64, ws=ws)
             torch.cuda.synchronize()
@@ -225,7 +226,7 @@ def test_gram_rounding_forms_bit_identical(T, monkeypatch, fmt, m, n):
     if fmt == "fp16":                                   # one entry beyond fp16's range after scaling
         A[m // 2, n - 1] = 1e6
         rcs = set()
-        for rv in ("1", "2"):
+        for rv in ("1", "2", "3"):
             monkeypatch.setenv("TLS_ROUND", rv)
             rc, _ = T.tls_gram(M, fmt, d, 64, ws=ws)
             torch.cuda.synchronize()
